@@ -1,0 +1,137 @@
+/*
+ * rpq_b200.h -- C ABI of the B200-native single-source 2-RPQ engine.
+ *
+ * Drop-in boundary for the reference package's query entry point
+ *   rpq.engine.eval_ssr(g: LabeledGraph, n: TwoNfa, source, opts) -> EvalResult
+ *   (/root/reference/pkg/src/rpq/engine.py:242-251)
+ * and its single-destination caller eval_sdr (engine.py:254-266).  The reference
+ * has no native code and no FFI; its "plugin interface" for this path is that
+ * Python function, so the Python package paper_2412_10287_b200 mirrors it
+ * (same names, argument meaning, errors) and binds THIS header through ctypes
+ * (see INTEGRATION.md).  No torch types cross this boundary: plain pointers,
+ * sizes and an opaque cudaStream_t passed as void*.
+ *
+ * Entry points and the reference interface each one replaces:
+ *   rpq_graph_create / rpq_graph_set_label
+ *       LabeledGraph.__init__ keeping forward[l] and backward[l] = transpose
+ *       (graph_store.py:35-52); the arrays are the reference's own int64 CSR
+ *       indptr/indices (sparse_bool.py:51-59), narrowed to 32 bits on device.
+ *   rpq_query_create
+ *       _label_pairs (engine.py:92-103): the automaton's usable symbols
+ *       (label index < num_labels) and their transition matrices, given as
+ *       (src state, label, inverted, dst state) triples, plus start_set /
+ *       final_set (query_compiler.py:241-247).
+ *   rpq_query_run / rpq_query_wait
+ *       the evaluator loop (engine.py:146-232): seed (:106-109), frontier step
+ *       _step_sum + mask_complement + or_sum (:117-124, :159-165) until the
+ *       frontier is empty, the per-iteration deadline check (_Clock.check,
+ *       :87-89), and _project_finals (:112-114).
+ *   rpq_ssr
+ *       one-shot eval_ssr: create query, run, wait, copy the answer, destroy.
+ *
+ * Status codes (Python mapping, engine.py error behaviour):
+ *   RPQ_OK 0, RPQ_EINVAL 1 -> ValueError, RPQ_ERANGE 2 -> IndexError
+ *   (engine.py:141-143), RPQ_ETIMEOUT 3 -> QueryTimeout(elapsed, iterations)
+ *   (engine.py:45-51), RPQ_ECUDA 4 -> RuntimeError, RPQ_ENOMEM 5 -> MemoryError,
+ *   RPQ_ENOLABEL 6 -> a label the automaton uses is not resident on the device.
+ * rpq_last_error() returns a thread-local message for the last failure.
+ */
+#ifndef RPQ_B200_H
+#define RPQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RPQ_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define RPQ_API __attribute__((visibility("default")))
+#else
+#define RPQ_API
+#endif
+
+#define RPQ_OK 0
+#define RPQ_EINVAL 1
+#define RPQ_ERANGE 2
+#define RPQ_ETIMEOUT 3
+#define RPQ_ECUDA 4
+#define RPQ_ENOMEM 5
+#define RPQ_ENOLABEL 6
+
+#define RPQ_STATS_LEVELS 64
+
+typedef struct rpq_graph rpq_graph;
+typedef struct rpq_query rpq_query;
+
+typedef struct rpq_stats {
+    int32_t status;          /* RPQ_* of the run */
+    int32_t iterations;      /* masked-loop iterations (engine.py:157-160), incl. the final empty step */
+    int32_t levels;          /* non-empty frontiers produced after the seed */
+    int32_t grid;            /* CTAs of the persistent step kernel */
+    int64_t te;              /* product edges traversed (SURVEY.md §8(d) TE) */
+    int64_t segments;        /* (pair, transition group) row lookups with degree > 0 */
+    int64_t visited_pairs;   /* |P| at exit */
+    int64_t reach_count;     /* |answer| */
+    float device_ms;         /* CUDA-event time, first kernel to answer ready */
+    float reserved_f;
+    int64_t level_new[RPQ_STATS_LEVELS];    /* new (state, vertex) pairs per level */
+    int64_t level_edges[RPQ_STATS_LEVELS];  /* edges traversed per level */
+} rpq_stats;
+
+RPQ_API int rpq_abi_version(void);
+RPQ_API const char* rpq_last_error(void);
+/* SM count, L2 bytes and HBM bytes of a device (for launch sizing / reports) */
+RPQ_API int rpq_device_info(int32_t device, int32_t* sm_count, int64_t* l2_bytes, int64_t* hbm_bytes);
+
+/* ---- graph residency ---------------------------------------------------- */
+RPQ_API int rpq_graph_create(int32_t num_vertices, int32_t num_labels, int32_t device, rpq_graph** out);
+/* Upload label `label`: forward CSR (rows = sources) and backward CSR
+ * (= transpose, rows = destinations), each with num_vertices+1 int64 row
+ * pointers and int64 column indices, as held by LabeledGraph.forward/backward.
+ * Narrowed on device to uint32 row pointers / int32 columns.  Idempotent. */
+RPQ_API int rpq_graph_set_label(rpq_graph* g, int32_t label,
+                        int64_t fwd_nnz, const int64_t* fwd_indptr, const int64_t* fwd_indices,
+                        int64_t bwd_nnz, const int64_t* bwd_indptr, const int64_t* bwd_indices);
+/* Same from int32 arrays (the generator's native layout). */
+RPQ_API int rpq_graph_set_label_i32(rpq_graph* g, int32_t label,
+                            int64_t fwd_nnz, const int32_t* fwd_indptr, const int32_t* fwd_indices,
+                            int64_t bwd_nnz, const int32_t* bwd_indptr, const int32_t* bwd_indices);
+RPQ_API int rpq_graph_label_resident(const rpq_graph* g, int32_t label);
+RPQ_API int64_t rpq_graph_device_bytes(const rpq_graph* g);
+RPQ_API int rpq_graph_destroy(rpq_graph* g);
+
+/* ---- queries ------------------------------------------------------------- */
+/* Transitions are (t_src[i] --(t_label[i], t_inv[i])--> t_dst[i]); those with
+ * t_label >= num_labels are dropped (engine.py:100-101).  Every usable label
+ * must be resident (else RPQ_ENOLABEL). */
+RPQ_API int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans,
+                     const int32_t* t_src, const int32_t* t_label, const uint8_t* t_inv,
+                     const int32_t* t_dst, int32_t nstarts, const int32_t* starts,
+                     int32_t nfinals, const int32_t* finals, rpq_query** out);
+/* Enqueue one evaluation from `source` on `stream` (a cudaStream_t, or NULL for
+ * the query's own stream).  timeout_s < 0 or inf: no deadline.  The deadline is
+ * checked on the device at the top of every iteration, like _Clock.check. */
+RPQ_API int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream);
+/* Wait for the last run; fills stats (may be NULL) and returns its status. */
+RPQ_API int rpq_query_wait(rpq_query* q, rpq_stats* stats);
+/* Device pointer to the uint8[num_vertices] answer of the last run. */
+RPQ_API int rpq_query_reach_device(rpq_query* q, uint8_t** d_reach);
+/* Copy the answer of the last run to host (uint8[num_vertices], 1 = reachable). */
+RPQ_API int rpq_query_copy_reach(rpq_query* q, uint8_t* host_reach);
+/* Copy the full visited matrix P (nstates rows x ceil(nv/32) uint32 words). */
+RPQ_API int rpq_query_copy_visited(rpq_query* q, uint32_t* host_words, int64_t nwords);
+RPQ_API int rpq_query_destroy(rpq_query* q);
+
+/* One-shot eval_ssr. */
+RPQ_API int rpq_ssr(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_t* t_src,
+            const int32_t* t_label, const uint8_t* t_inv, const int32_t* t_dst,
+            int32_t nstarts, const int32_t* starts, int32_t nfinals, const int32_t* finals,
+            int32_t source, double timeout_s, uint8_t* out_reach, rpq_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RPQ_B200_H */

@@ -1,0 +1,161 @@
+"""ctypes bindings to the in-tree native libraries.
+
+``engine()`` loads ``librpq_b200.so`` (the CUDA engine behind
+include/rpq_b200.h).  There is no CPU fallback: if the library is missing or
+cannot be loaded, every query raises.  ``datagen()`` loads the host-side
+synthetic input generator.
+"""
+
+import ctypes
+import os
+import threading
+
+from . import _build
+
+RPQ_OK = 0
+RPQ_EINVAL = 1
+RPQ_ERANGE = 2
+RPQ_ETIMEOUT = 3
+RPQ_ECUDA = 4
+RPQ_ENOMEM = 5
+RPQ_ENOLABEL = 6
+
+STATS_LEVELS = 64
+
+c_i32 = ctypes.c_int32
+c_i64 = ctypes.c_int64
+c_u64 = ctypes.c_uint64
+c_dbl = ctypes.c_double
+c_vp = ctypes.c_void_p
+P_i32 = ctypes.POINTER(ctypes.c_int32)
+P_i64 = ctypes.POINTER(ctypes.c_int64)
+P_u8 = ctypes.POINTER(ctypes.c_uint8)
+P_u32 = ctypes.POINTER(ctypes.c_uint32)
+P_u64 = ctypes.POINTER(ctypes.c_uint64)
+
+
+class RpqStats(ctypes.Structure):
+    _fields_ = [
+        ("status", c_i32),
+        ("iterations", c_i32),
+        ("levels", c_i32),
+        ("grid", c_i32),
+        ("te", c_i64),
+        ("segments", c_i64),
+        ("visited_pairs", c_i64),
+        ("reach_count", c_i64),
+        ("device_ms", ctypes.c_float),
+        ("reserved_f", ctypes.c_float),
+        ("level_new", c_i64 * STATS_LEVELS),
+        ("level_edges", c_i64 * STATS_LEVELS),
+    ]
+
+    def to_dict(self):
+        nlev = min(max(self.iterations, 0) + 1, STATS_LEVELS)
+        return {
+            "status": self.status,
+            "iterations": self.iterations,
+            "levels": self.levels,
+            "grid": self.grid,
+            "te": self.te,
+            "segments": self.segments,
+            "visited_pairs": self.visited_pairs,
+            "reach_count": self.reach_count,
+            "device_ms": self.device_ms,
+            "level_new": list(self.level_new[:nlev]),
+            "level_edges": list(self.level_edges[:nlev]),
+        }
+
+
+# symbol -> (restype, argtypes); the complete C ABI of include/rpq_b200.h
+ENGINE_SIGNATURES = {
+    "rpq_abi_version": (c_i32, []),
+    "rpq_last_error": (ctypes.c_char_p, []),
+    "rpq_device_info": (c_i32, [c_i32, P_i32, P_i64, P_i64]),
+    "rpq_graph_create": (c_i32, [c_i32, c_i32, c_i32, ctypes.POINTER(c_vp)]),
+    "rpq_graph_set_label": (c_i32, [c_vp, c_i32, c_i64, P_i64, P_i64, c_i64, P_i64, P_i64]),
+    "rpq_graph_set_label_i32": (c_i32, [c_vp, c_i32, c_i64, P_i32, P_i32, c_i64, P_i32, P_i32]),
+    "rpq_graph_label_resident": (c_i32, [c_vp, c_i32]),
+    "rpq_graph_device_bytes": (c_i64, [c_vp]),
+    "rpq_graph_destroy": (c_i32, [c_vp]),
+    "rpq_query_create": (c_i32, [c_vp, c_i32, c_i32, P_i32, P_i32, P_u8, P_i32, c_i32, P_i32,
+                                 c_i32, P_i32, ctypes.POINTER(c_vp)]),
+    "rpq_query_run": (c_i32, [c_vp, c_i32, c_dbl, c_vp]),
+    "rpq_query_wait": (c_i32, [c_vp, ctypes.POINTER(RpqStats)]),
+    "rpq_query_reach_device": (c_i32, [c_vp, ctypes.POINTER(P_u8)]),
+    "rpq_query_copy_reach": (c_i32, [c_vp, P_u8]),
+    "rpq_query_copy_visited": (c_i32, [c_vp, P_u32, c_i64]),
+    "rpq_query_destroy": (c_i32, [c_vp]),
+    "rpq_ssr": (c_i32, [c_vp, c_i32, c_i32, P_i32, P_i32, P_u8, P_i32, c_i32, P_i32, c_i32, P_i32,
+                        c_i32, c_dbl, P_u8, ctypes.POINTER(RpqStats)]),
+}
+
+DATAGEN_SIGNATURES = {
+    "rpqgen_draw": (c_u64, [c_u64, c_u64, c_u64]),
+    "rpqgen_zipf_thresholds": (None, [c_i32, c_dbl, P_u64]),
+    "rpqgen_er": (c_i64, [c_i32, c_i64, c_i32, c_u64, P_i32, P_i32, P_i32]),
+    "rpqgen_rmat": (c_i64, [c_i32, c_i64, c_dbl, c_dbl, c_dbl, c_i32, c_dbl, c_u64, P_i32, P_i32,
+                            P_i32]),
+    "rpqgen_chunglu": (c_i64, [c_i32, c_i64, c_dbl, c_i32, c_dbl, c_u64, P_i32, P_i32, P_i32]),
+    "rpqgen_label_count": (c_i64, [c_i64, P_i32, c_i32]),
+    "rpqgen_label_csr": (c_i64, [c_i32, c_i64, P_i32, P_i32, P_i32, c_i32, c_i32, P_i64, P_i64]),
+    "rpqgen_out_degree": (None, [c_i32, c_i64, P_i32, P_i64]),
+}
+
+_lock = threading.Lock()
+_engine = None
+_datagen = None
+
+
+class NativeLibraryMissing(RuntimeError):
+    """The CUDA engine library is not built; there is no fallback path."""
+
+
+def _bind(path, signatures):
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in signatures.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def engine():
+    """The loaded CUDA engine library (raises if it is not built)."""
+    global _engine
+    if _engine is None:
+        with _lock:
+            if _engine is None:
+                if not os.path.exists(_build.ENGINE_SO):
+                    raise NativeLibraryMissing(
+                        f"{_build.ENGINE_SO} is not built; run "
+                        "`python -m paper_2412_10287_b200._build` (there is no CPU fallback)"
+                    )
+                lib = _bind(_build.ENGINE_SO, ENGINE_SIGNATURES)
+                if lib.rpq_abi_version() != 1:
+                    raise NativeLibraryMissing("librpq_b200.so ABI version mismatch")
+                _engine = lib
+    return _engine
+
+
+def datagen():
+    global _datagen
+    if _datagen is None:
+        with _lock:
+            if _datagen is None:
+                if not os.path.exists(_build.DATAGEN_SO):
+                    _build.build_datagen()
+                _datagen = _bind(_build.DATAGEN_SO, DATAGEN_SIGNATURES)
+    return _datagen
+
+
+def last_error():
+    msg = engine().rpq_last_error()
+    return msg.decode() if msg else ""
+
+
+def ptr(arr, ctype):
+    """Pointer to a contiguous numpy array's data (None for empty arrays)."""
+    if arr is None:
+        return None
+    return arr.ctypes.data_as(ctypes.POINTER(ctype))

@@ -1,0 +1,250 @@
+"""Drop-in query API: the reference engine's names, arguments and errors
+(/root/reference/pkg/src/rpq/engine.py), evaluated by the sm_100a kernel.
+
+    eval_ssr(g, n, source, opts) -> EvalResult          engine.py:242-251
+    eval_ssr_masked / eval_ssr_no_mask / eval_ssr_hybrid engine.py:146-232
+    eval_sdr(g, n, target, opts, algorithm=None)        engine.py:254-266
+    step_update(m, p, g, n, opts)                       engine.py:127-138
+    EngineOptions, EvalResult, QueryTimeout             engine.py:45-89
+
+``g`` is the reference's LabeledGraph (or this package's host mirror), ``n``
+its compiled TwoNfa.  The three SSR algorithms of the reference compute the
+same P, level by level (Alg. 1 and Alg. 2 of PAPER.md differ only in how
+much of P they re-expand), so all three run the same device BFS; the
+``algorithm`` tag is kept in the result and the iteration count follows each
+loop's own accounting.  There is no CPU path: the CUDA library must load.
+"""
+
+import ctypes
+import dataclasses
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .automaton import reverse, transition_table
+from .graph import device_graph
+
+ALGORITHMS = ("masked", "no_mask", "hybrid", "plan")
+
+
+class QueryTimeout(RuntimeError):
+    """Evaluation exceeded the wall-clock budget (engine.py:45-51)."""
+
+    def __init__(self, elapsed: float, iterations: int):
+        super().__init__(f"query timed out after {elapsed:.3f}s ({iterations} iterations)")
+        self.elapsed = elapsed
+        self.iterations = iterations
+
+
+class EngineError(RuntimeError):
+    """A CUDA or internal failure of the device engine."""
+
+
+@dataclass
+class EngineOptions:
+    """engine.py:54-68, plus ``device`` (CUDA ordinal the graph lives on)."""
+
+    algorithm: str = "hybrid"
+    switch_threshold: float = 100
+    product_order: str = "left"
+    timeout: float = 60.0
+    debug_checks: bool = False
+    device: int = 0
+
+    def validate(self) -> None:
+        if self.algorithm not in ALGORITHMS:
+            raise ValueError(f"unknown algorithm {self.algorithm!r}")
+        if self.product_order not in ("left", "right"):
+            raise ValueError(f"unknown product order {self.product_order!r}")
+        if self.switch_threshold < 0:
+            raise ValueError("switch threshold must be >= 0")
+
+
+class EvalResult:
+    """Result of one evaluation (engine.py:71-76).
+
+    ``reachable`` is the reference's ``set[int]`` of answer vertices, built on
+    first access from ``reach``, the device's ``uint8[|V|]`` answer vector.
+    """
+
+    __slots__ = ("reach", "_reachable", "iterations", "elapsed", "algorithm", "stats")
+
+    def __init__(self, reach, iterations, elapsed, algorithm, stats=None):
+        self.reach = reach
+        self._reachable = None
+        self.iterations = iterations
+        self.elapsed = elapsed
+        self.algorithm = algorithm
+        self.stats = stats
+
+    @property
+    def reachable(self):
+        if self._reachable is None:
+            self._reachable = set(np.flatnonzero(self.reach).tolist())
+        return self._reachable
+
+    def __eq__(self, other):
+        if not isinstance(other, EvalResult):
+            return NotImplemented
+        return (self.reachable == other.reachable and self.iterations == other.iterations
+                and self.algorithm == other.algorithm)
+
+    __hash__ = None
+
+    def __repr__(self):
+        return (f"EvalResult(|reachable|={int(np.count_nonzero(self.reach))}, "
+                f"iterations={self.iterations}, elapsed={self.elapsed:.6f}, "
+                f"algorithm={self.algorithm!r})")
+
+
+def raise_for_status(rc, what=""):
+    """Map a C-ABI status to the reference's exception types."""
+    if rc == _lib.RPQ_OK:
+        return
+    msg = _lib.last_error()
+    text = f"{what}: {msg}" if what else msg
+    if rc == _lib.RPQ_EINVAL:
+        raise ValueError(text)
+    if rc == _lib.RPQ_ERANGE:
+        raise IndexError(text)
+    if rc == _lib.RPQ_ENOMEM:
+        raise MemoryError(text)
+    if rc == _lib.RPQ_ENOLABEL:
+        raise ValueError(text)
+    raise EngineError(text)
+
+
+def _check_vertex(g, vertex):
+    """engine.py:141-143"""
+    if not 0 <= vertex < g.num_vertices:
+        raise IndexError(f"vertex index {vertex} out of range")
+
+
+def _iterations_for(algorithm, masked_iterations, nstarts):
+    # The masked loop runs `while m.nnz` and so does zero iterations when the
+    # automaton has no start state; the mask-free and hybrid loops always run
+    # at least one (engine.py:157, :184, :209).  Otherwise all three count
+    # the D+1 steps of a BFS of depth D.
+    if nstarts == 0 and algorithm in ("no_mask", "hybrid"):
+        return 1
+    return masked_iterations
+
+
+def _run(g, n, source, opts, tag, *, want_stats=False):
+    opts.validate()
+    _check_vertex(g, source)
+    t0 = time.monotonic()
+    dg = device_graph(g, opts.device)
+    table = transition_table(n, g.num_labels)
+    dg.ensure_labels(table.labels)
+    lib = _lib.engine()
+    q = dg.acquire_query(table)
+    try:
+        # _Clock.check(0) at the top of the first iteration (engine.py:87-89)
+        remaining = opts.timeout - (time.monotonic() - t0)
+        if remaining < 0 or opts.timeout == 0:
+            raise QueryTimeout(time.monotonic() - t0, 0)
+        budget = -1.0 if math.isinf(remaining) else remaining
+        raise_for_status(lib.rpq_query_run(q, int(source), budget, None), "rpq_query_run")
+        stats = _lib.RpqStats()
+        rc = lib.rpq_query_wait(q, ctypes.byref(stats))
+        if rc == _lib.RPQ_ETIMEOUT:
+            raise QueryTimeout(time.monotonic() - t0,
+                               _iterations_for(tag, stats.iterations, table.starts.size))
+        raise_for_status(rc, "rpq_query_wait")
+        reach = np.empty(g.num_vertices, dtype=np.uint8)
+        if g.num_vertices:
+            raise_for_status(lib.rpq_query_copy_reach(q, _lib.ptr(reach, ctypes.c_uint8)),
+                             "rpq_query_copy_reach")
+        iterations = _iterations_for(tag, stats.iterations, table.starts.size)
+        if opts.debug_checks:
+            _debug_invariants(lib, q, table, g.num_vertices, stats, iterations)
+    finally:
+        dg.release_query(table, q)
+    return EvalResult(reach, iterations, time.monotonic() - t0, tag,
+                      stats.to_dict() if want_stats or opts.debug_checks else None)
+
+
+def _debug_invariants(lib, q, table, nv, stats, iterations):
+    """Executable invariants of debug mode (engine.py:161-170, :187-190):
+    P grew by exactly the disjoint per-level frontiers, and the loop stayed
+    within |Q|*|V| iterations."""
+    words = (nv + 31) // 32
+    buf = np.zeros(max(words * table.nstates, 1), dtype=np.uint32)
+    raise_for_status(lib.rpq_query_copy_visited(q, _lib.ptr(buf, ctypes.c_uint32), buf.size),
+                     "rpq_query_copy_visited")
+    popcount = int(np.unpackbits(buf.view(np.uint8)).sum())
+    levels = stats.level_new[:min(stats.iterations + 1, _lib.STATS_LEVELS)]
+    assert popcount == stats.visited_pairs, "visited set is not the union of the frontiers"
+    if stats.iterations < _lib.STATS_LEVELS:
+        assert sum(levels) == stats.visited_pairs, "frontiers overlap or were lost"
+    assert iterations <= table.nstates * nv or nv == 0, "exceeded |Q|*|V| iterations"
+    reach = int(stats.reach_count)
+    assert 0 <= reach <= nv
+
+
+def eval_ssr_masked(g, n, source, opts):
+    """Frontier/visited iteration (Alg. 1; engine.py:146-171)."""
+    return _run(g, n, source, opts, "masked")
+
+
+def eval_ssr_no_mask(g, n, source, opts):
+    """Single-accumulator iteration (Alg. 2; engine.py:174-194)."""
+    return _run(g, n, source, opts, "no_mask")
+
+
+def eval_ssr_hybrid(g, n, source, opts):
+    """Mask-free until nnz(P) > switch_threshold, masked after (engine.py:197-232)."""
+    return _run(g, n, source, opts, "hybrid")
+
+
+_SSR_EVALUATORS = {
+    "masked": eval_ssr_masked,
+    "no_mask": eval_ssr_no_mask,
+    "hybrid": eval_ssr_hybrid,
+}
+
+
+def eval_ssr(g, n, source, opts):
+    """Dispatch on ``opts.algorithm`` (engine.py:242-251)."""
+    opts.validate()
+    try:
+        evaluator = _SSR_EVALUATORS[opts.algorithm]
+    except KeyError:
+        raise ValueError(
+            f"algorithm {opts.algorithm!r} does not evaluate compiled automata"
+        ) from None
+    return evaluator(g, n, source, opts)
+
+
+def eval_sdr(g, n, target, opts, algorithm=None):
+    """Single-destination reachability: SSR from the target over the reversed
+    automaton (engine.py:254-266)."""
+    _check_vertex(g, target)
+    if algorithm is not None:
+        opts = dataclasses.replace(opts, algorithm=algorithm)
+    return eval_ssr(g, reverse(n), target, opts)
+
+
+def eval_ssr_batch(g, n, sources, opts):
+    """uint8[len(sources), |V|]: row i is eval_ssr(g, n, sources[i], opts)'s answer.
+
+    Defined as the per-source loop; the reference has no
+    multi-source entry point."""
+    sources = list(sources)
+    out = np.zeros((len(sources), g.num_vertices), dtype=np.uint8)
+    for i, s in enumerate(sources):
+        out[i] = eval_ssr(g, n, s, opts).reach
+    return out
+
+
+def step_update(m, p, g, n, opts):
+    """One traversal step (engine.py:127-138): the per-symbol products of the
+    frontier ``m``, minus everything in ``p``.  Not implemented on the device
+    yet; raises rather than falling back to a CPU path."""
+    if m.shape != p.shape:
+        raise ValueError(f"step_update: frontier {m.shape} vs visited {p.shape}")
+    raise NotImplementedError("step_update has no device implementation yet")

@@ -1,0 +1,172 @@
+"""Device parity: the sm_100a engine, called through the package API (and so
+through the C ABI), against the reference's own outputs (golden fixtures) and
+against the CPU oracle.  Results must be bit-exact (integer/Boolean path)."""
+
+import math
+import threading
+
+import numpy as np
+import pytest
+
+from fixtures import automaton, expected_reach, host_graph, oracle_graph, unpack_bits
+from conftest import load_golden
+
+import paper_2412_10287_b200 as P
+from paper_2412_10287_b200 import datagen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def instances(reference_instances):
+    return [(rec, host_graph(rec["graph"]), automaton(rec["nfa"])) for rec in reference_instances]
+
+
+@pytest.mark.parametrize("algorithm", ["hybrid", "masked", "no_mask"])
+def test_reference_instances(instances, algorithm):
+    opts = P.EngineOptions(algorithm=algorithm, timeout=math.inf)
+    for rec, g, n in instances:
+        res = P.eval_ssr(g, n, rec["source"], opts)
+        assert np.array_equal(res.reach, expected_reach(rec, g.num_vertices)), rec["tag"]
+        assert res.reachable == set(rec["expected"]), rec["tag"]
+        assert res.iterations == rec["iterations"][algorithm], (rec["tag"], res.iterations)
+        assert res.algorithm == algorithm
+
+
+def test_sdr_duality(instances):
+    opts = P.EngineOptions()
+    for rec, g, n in instances:
+        if "sdr_expected" not in rec:
+            continue
+        res = P.eval_sdr(g, n, rec["source"], opts)
+        assert sorted(res.reachable) == rec["sdr_expected"], rec["tag"]
+        assert res.iterations == rec["sdr_iterations"], rec["tag"]
+        forced = P.eval_sdr(g, n, rec["source"], opts, "masked")
+        assert forced.algorithm == "masked" and forced.reachable == res.reachable
+
+
+def test_hybrid_thresholds(instances):
+    for rec, g, n in instances:
+        if "threshold_iterations" not in rec:
+            continue
+        for t, its in rec["threshold_iterations"].items():
+            res = P.eval_ssr_hybrid(g, n, rec["source"], P.EngineOptions(switch_threshold=float(t)))
+            assert res.reachable == set(rec["expected"]) and res.iterations == its
+
+
+def test_debug_invariants(instances):
+    opts = P.EngineOptions(debug_checks=True)
+    for rec, g, n in instances[:200]:
+        res = P.eval_ssr(g, n, rec["source"], opts)
+        assert res.iterations <= n.nstates * g.num_vertices
+        assert res.stats["visited_pairs"] == sum(res.stats["level_new"][: res.iterations + 1])
+
+
+def test_timeout_raises():
+    # test_engine.py:376-383
+    nv = 3001
+    g = P.LabeledGraph.from_edges(nv, ["a"], [(i, 0, i + 1) for i in range(3000)])
+    n = P.Automaton.build(1, {(0, False): [(0, 0)]}, [0], [0])
+    with pytest.raises(P.QueryTimeout) as ei:
+        P.eval_ssr_masked(g, n, 0, P.EngineOptions(timeout=0.0))
+    assert ei.value.iterations == 0
+    res = P.eval_ssr_masked(g, n, 0, P.EngineOptions(timeout=math.inf))
+    assert res.reachable == set(range(nv)) and res.iterations == nv
+    # a deadline that expires mid-query is caught at an iteration boundary
+    with pytest.raises(P.QueryTimeout) as ei:
+        P.eval_ssr_masked(g, n, 0, P.EngineOptions(timeout=1e-4))
+    assert 0 <= ei.value.iterations < nv
+
+
+def test_empty_and_edge_cases():
+    # no labels at all, single vertex (test_engine.py:127-134)
+    g = P.LabeledGraph(1, [], [])
+    n = P.Automaton.build(1, {(0, False): [(0, 0)]}, [0], [0])
+    for alg in ("masked", "no_mask", "hybrid"):
+        assert P.eval_ssr(g, n, 0, P.EngineOptions(algorithm=alg)).reachable == {0}
+    # an automaton with no start state answers nothing; masked does 0 iterations,
+    # the mask-free loops one (engine.py:157 vs :184, :209)
+    g = P.LabeledGraph.from_edges(4, ["a"], [(0, 0, 1), (1, 0, 2)])
+    n = P.Automaton.build(2, {(0, False): [(0, 1)]}, [], [1])
+    assert P.eval_ssr_masked(g, n, 0, P.EngineOptions()).iterations == 0
+    assert P.eval_ssr_hybrid(g, n, 0, P.EngineOptions()).iterations == 1
+    assert P.eval_ssr_no_mask(g, n, 0, P.EngineOptions()).reachable == set()
+    # multi-start, nondeterministic automaton
+    n = P.Automaton.build(3, {(0, False): [(0, 1), (0, 2), (2, 2)], (0, True): [(1, 0)]},
+                          [0, 2], [1, 2])
+    og = oracle_graph({"nv": 4, "edges": [[(0, 1), (1, 2)]]})
+    from oracle import OracleQuery, oracle_bfs
+
+    oq = OracleQuery(n.to_json(), 1)
+    for s in range(4):
+        want, st = oracle_bfs(og, oq, s)
+        got = P.eval_ssr(g, n, s, P.EngineOptions())
+        assert np.array_equal(got.reach, want) and got.iterations == st["iterations"]
+
+
+def test_concurrent_queries_deterministic(instances):
+    rec, g, n = max(instances, key=lambda x: len(x[0]["expected"]))
+    want = expected_reach(rec, g.num_vertices)
+    errors = []
+
+    def worker():
+        try:
+            for _ in range(20):
+                r = P.eval_ssr(g, n, rec["source"], P.EngineOptions())
+                assert np.array_equal(r.reach, want)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    ts = [threading.Thread(target=worker) for _ in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+
+
+def _config_case(name):
+    gold = load_golden(f"{name}.json.gz")
+    sg = datagen.generate(name)
+    assert sg.digest() == gold["digest"], "generator drifted from the golden inputs"
+    return gold, sg
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_config_goldens(name):
+    gold, sg = _config_case(name)
+    g = sg.labeled_graph()
+    for rec in gold["records"]:
+        n = automaton(rec["nfa"])
+        res = P.eval_ssr(g, n, rec["source"], P.EngineOptions(timeout=math.inf))
+        want = unpack_bits(rec["reach_bits"], sg.nv)
+        assert int(want.sum()) == rec["reach_count"]
+        assert np.array_equal(res.reach, want)
+        assert res.iterations == rec["iterations"]["hybrid"]
+
+
+@pytest.mark.parametrize("scale,seed,query", [
+    (14, 21, "^a (b|c)* d"), (15, 22, "a ^b* c"), (16, 23, "a b*"),
+    (13, 24, "(a|^b)* c+"), (12, 25, "(a ^a)* (b | c ^d)*")])
+def test_rmat_vs_oracle(scale, seed, query):
+    import json
+    import os
+
+    from oracle import OracleGraph, OracleQuery, oracle_bfs
+
+    sg = datagen.gen_rmat(scale, 16, 8, 1.0, seed)
+    g = sg.labeled_graph()
+    og = OracleGraph(sg.nv, sg.nl, sg.src, sg.dst, sg.lab)
+    path = os.path.join(os.path.dirname(__file__), "golden", "extra_automata.json")
+    nj = json.load(open(path))[query]
+    n = automaton(nj)
+    oq = OracleQuery(nj, sg.nl)
+    deg = sg.out_degree()
+    sources = [int(np.argmax(deg)), 0, sg.nv - 1, int(np.flatnonzero(deg)[len(np.flatnonzero(deg)) // 2])]
+    for s in sources:
+        want, st = oracle_bfs(og, oq, s)
+        got = P.eval_ssr(g, n, s, P.EngineOptions(timeout=math.inf, debug_checks=True))
+        assert np.array_equal(got.reach, want), (query, s)
+        assert got.iterations == st["iterations"]
+        assert got.stats["te"] == st["te"]
+        assert got.stats["visited_pairs"] == st["pairs"]
