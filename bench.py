@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark: 2-RPQ product edges traversed per second (GTEPS) and per-query
+latency on the BASELINE.json headline configuration (configs[1] = cfg2):
+
+  R-MAT scale 20 (1,048,576 vertices), edge factor 16, (0.57, 0.19, 0.19, 0.05),
+  self-loops and duplicates removed, 16 Zipf(1.0) labels; two-way query
+  a ^b* c (the reference compiler's minimal 3-state DFA); source = the vertex
+  with the highest out-degree.  Synthetic, seeded (paper_2412_10287_b200/datagen.py).
+
+A step is one single-source query evaluation (seed -> answer vector ready on
+the device).  `value` is device-timed with CUDA events around each step on
+the launching stream (inputs resident in HBM, L2 flushed between steps);
+`e2e` is the same metric through the public API `eval_ssr` with the automaton
+sent host->device every call and the uint8 answer read back to the host.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference]
+
+With N > 1 (torchrun, one rank per GPU) every rank evaluates its own
+independent query -- rank r starts from the r-th highest out-degree vertex --
+with no data-path collective (weak scaling over independent queries).
+`--impl reference` times the reference algorithm's CPU restatement
+(oracle/rpq_oracle.c oracle_port, the hybrid loop of engine.py:197-232) on all
+host cores, one independent query per thread; rank 0 only.
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "2-RPQ edges traversed/sec (GTEPS)"
+UNIT = "GTEPS"
+CONFIG = "cfg2"
+QUERY = "a ^b* c"
+WORKLOAD = ("cfg2: R-MAT scale 20 (1,048,576 V), edge factor 16, abc=(0.57,0.19,0.19), "
+            "16 Zipf(1.0) labels, query a ^b* c (3-state min DFA), source = max out-degree")
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["engine", "reference"], default="engine")
+    ap.add_argument("--config", default=CONFIG)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--direction", choices=["auto", "push", "pull"], default="auto")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--profile", action="store_true",
+                    help="short run for ncu: no e2e leg, no CPU baseline, no clocks")
+    return ap.parse_args()
+
+
+def load_automaton(config, query):
+    with open(os.path.join(ROOT, "paper_2412_10287_b200", "data", "config_automata.json")) as fh:
+        return json.load(fh)[config][f"{query}|min"]
+
+
+def ranked_sources(sg, k):
+    import numpy as np
+
+    deg = sg.out_degree()
+    order = np.lexsort((np.arange(sg.nv), -deg))  # degree desc, id asc
+    return [int(v) for v in order[:k]]
+
+
+def read_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap", "utilization.gpu"]
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _poll(self):
+        cmd = ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+               "--format=csv,noheader,nounits"]
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(cmd, capture_output=True, text=True, timeout=5).stdout.strip()
+                parts = [p.strip() for p in out.split(",")]
+                if len(parts) == len(self.FIELDS):
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def start(self):
+        self._t = threading.Thread(target=self._poll, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            self._stop.clear()
+            self._stop.set()
+        return self.summary()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        busy = [float(s[0]) for s in self.samples
+                if s[0].replace(".", "").isdigit() and s[6].isdigit() and int(s[6]) > 0]
+        reasons = set()
+        for s in self.samples:
+            for name, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                "sw_power_cap"], s[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {
+            "sm_mhz": statistics.median(busy or sm) if (busy or sm) else None,
+            "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
+            "reasons": sorted(reasons),
+            "samples": len(self.samples),
+            "samples_busy": len(busy),
+        }
+
+
+def algorithmic_bytes(te, x, pairs, levels, nstates, nv):
+    """4*TE + 8*X + 8*|P| + 2*L*ceil(R*|V|/8)."""
+    return 4 * te + 8 * x + 8 * pairs + 2 * levels * math.ceil(nstates * nv / 8)
+
+
+def cpu_baseline(sg, nj, source, seconds, engine_reach):
+    """The reference algorithm's C restatement, one thread, bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import OracleGraph, OracleQuery, oracle_port
+
+    og = OracleGraph(sg.nv, sg.nl, sg.src, sg.dst, sg.lab)
+    oq = OracleQuery(nj, sg.nl)
+    oq.prepare(og)
+    runs, total, te = 0, 0.0, None
+    reach = None
+    while total < seconds or runs == 0:
+        reach, st = oracle_port(og, oq, source, "hybrid", 100.0)
+        total += st["seconds"]
+        runs += 1
+    from oracle import oracle_bfs
+
+    _, bst = oracle_bfs(og, oq, source)
+    te = bst["te"]
+    return {
+        "value": te * runs / total / 1e9,
+        "unit": UNIT,
+        "cores": 1,
+        "kind": "port",
+        "sample": (f"{CONFIG} {QUERY} from source {source}, {runs} sequential evaluations "
+                   f"({total:.1f} s) by oracle/rpq_oracle.c oracle_port (engine.py hybrid loop, "
+                   f"sorted-key sparse Boolean ops), 1 thread"),
+        "ms_per_query": 1e3 * total / runs,
+        "parity_with_engine": bool((reach == engine_reach).all()),
+    }
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import OracleGraph, OracleQuery, oracle_bfs, oracle_port
+    from paper_2412_10287_b200 import datagen
+
+    sg = datagen.generate(args.config)
+    nj = load_automaton(args.config, QUERY)
+    source = ranked_sources(sg, 1)[0]
+    og = OracleGraph(sg.nv, sg.nl, sg.src, sg.dst, sg.lab)
+    oq = OracleQuery(nj, sg.nl)
+    oq.prepare(og)
+    _, bst = oracle_bfs(og, oq, source)
+    te = bst["te"]
+    threads = os.cpu_count() or 1
+    pool = ThreadPoolExecutor(max_workers=threads)
+
+    def step():
+        t = time.perf_counter()
+        list(pool.map(lambda _: oracle_port(og, oq, source, "hybrid", 100.0), range(threads)))
+        return time.perf_counter() - t
+
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    total = sum(times)
+    value = threads * te * args.steps / total / 1e9
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "vertices": sg.nv, "edges": sg.ne, "query": QUERY,
+                   "source": source, "te_per_query": te},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": (f"each step: {threads} concurrent evaluations of {QUERY} from "
+                                    f"source {source} (one per host thread) by "
+                                    "oracle/rpq_oracle.c oracle_port (hybrid loop)")},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def run_engine(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_2412_10287_b200 as P
+    from paper_2412_10287_b200 import datagen
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    sg = datagen.generate(args.config)
+    g = sg.labeled_graph()
+    nj = load_automaton(args.config, QUERY)
+    n = P.Automaton.from_json(nj)
+    source = ranked_sources(sg, world)[rank]
+    pq = P.PreparedQuery(g, n, device=local_rank)
+    # a dedicated (non-default) stream: the engine and the timing events share it
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    handle = stream.cuda_stream
+    assert handle, "need a real stream handle"
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    # one untimed run for the work counts (exact TE, |P|, levels) of this query
+    pq.set_options(direction=args.direction, count_te=True)
+    pq.launch(source, -1.0, handle)
+    st0 = pq.wait()
+    pq.set_options(direction=args.direction, count_te=False)
+    per_state = pq.visited_counts()
+    outdeg_q = np.bincount(pq.table.t_src, minlength=pq.table.nstates)
+    x = int((per_state * outdeg_q).sum())
+    te, pairs, iters = int(st0.te), int(st0.visited_pairs), int(st0.iterations)
+    b_alg = algorithmic_bytes(te, x, pairs, iters, pq.table.nstates, sg.nv)
+    engine_reach = pq.reach()
+
+    sampler = None
+    if not args.profile:
+        phys = os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[local_rank]
+        sampler = ClockSampler(phys)
+        sampler.start()
+
+    for i in range(args.warmup):
+        flush.fill_(i & 0xFF)
+        pq.launch(source, -1.0, handle)
+        pq.wait()
+
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches = 0
+    for k in range(args.steps):
+        flush.fill_(k & 0xFF)  # > L2: evicts the graph between steps (outside the events)
+        ev[k][0].record(stream)
+        pq.launch(source, -1.0, handle)
+        launches += 1
+        ev[k][1].record(stream)
+        st = pq.wait()
+        assert st.visited_pairs == pairs and st.iterations == iters
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+
+    # e2e through the public API: automaton H2D + kernel + answer D2H per call
+    e2e_s = []
+    if not args.profile:
+        opts = P.EngineOptions(timeout=math.inf, direction=args.direction)
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            res = P.eval_ssr(g, n, source, opts)
+            e2e_s.append(time.perf_counter() - t)
+            assert res.iterations == iters
+        assert np.array_equal(res.reach, engine_reach)
+    clocks = sampler.stop() if sampler else None
+
+    h2d, d2h_ctl = pq.io_bytes()
+    d2h = d2h_ctl + sg.nv
+    if world > 1:
+        t = torch.tensor([total_ms, sum(e2e_s) if e2e_s else 0.0], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_max_ms, e2e_max_s = float(t[0]), float(t[1])
+        u = torch.tensor([te * args.steps], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(u)
+        units = float(u[0])
+    else:
+        total_max_ms, e2e_max_s, units = total_ms, sum(e2e_s), float(te * args.steps)
+    pq.close()
+    if rank != 0:
+        return None
+
+    value = units / (total_max_ms / 1e3) / 1e9
+    peak, peak_src = read_peaks()
+    kernel_s = total_ms / args.steps / 1e3
+    achieved = b_alg / kernel_s / 1e9
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_max_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic",
+        "config": {
+            "workload": WORKLOAD, "vertices": sg.nv, "edges": sg.ne, "query": QUERY,
+            "automaton_states": pq.table.nstates, "sources": ranked_sources(sg, world),
+            "l2": "flushed between steps (256 MiB write, outside the step events)",
+            "parallelism": f"{world} independent queries (1 per GPU)" if world > 1 else "1 GPU",
+        },
+        "per_query": {
+            "latency_ms_median": statistics.median(step_ms), "latency_ms_min": min(step_ms),
+            "te": te, "x": x, "visited_pairs": pairs, "iterations": iters,
+            "reach": int(st0.reach_count),
+            "level_new": list(st0.level_new[: iters + 1]),
+            "level_edges": list(st0.level_edges[: iters + 1]),
+            "level_dir": ["pull" if d else "push" for d in st0.level_dir[: iters]],
+            "direction_policy": args.direction,
+        },
+        "roofline": {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None,
+            "kernel": "rpq_ssr_kernel (persistent, one launch per query)",
+            "algorithmic_bytes_per_launch": b_alg, "peak_source": peak_src,
+            "note": "algorithmic bytes of SURVEY.md §8(d) per query / mean step time",
+        },
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if e2e_s:
+        out["e2e"] = {"value": units / e2e_max_s / 1e9, "unit": UNIT,
+                      "h2d_bytes_per_step": h2d + 4, "d2h_bytes_per_step": d2h,
+                      "latency_ms_median": 1e3 * statistics.median(e2e_s)}
+    if world == 1 and not args.no_cpu_baseline and not args.profile:
+        out["cpu_baseline"] = cpu_baseline(sg, nj, source, args.cpu_seconds, engine_reach)
+    return out
+
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+    else:
+        if world > 1:
+            import torch
+
+            torch.cuda.set_device(local_rank)
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        out = run_engine(args, rank, world, local_rank)
+        if world > 1:
+            import torch
+
+            torch.distributed.destroy_process_group()
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

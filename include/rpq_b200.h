@@ -71,15 +71,22 @@ typedef struct rpq_stats {
     int32_t iterations;      /* masked-loop iterations (engine.py:157-160), incl. the final empty step */
     int32_t levels;          /* non-empty frontiers produced after the seed */
     int32_t grid;            /* CTAs of the persistent step kernel */
-    int64_t te;              /* product edges traversed (SURVEY.md §8(d) TE) */
+    int64_t te;              /* product edges traversed, SURVEY.md §8(d) TE: exact when
+                                count_te is set, else the edges push levels expanded */
     int64_t segments;        /* (pair, transition group) row lookups with degree > 0 */
     int64_t visited_pairs;   /* |P| at exit */
     int64_t reach_count;     /* |answer| */
     float device_ms;         /* CUDA-event time, first kernel to answer ready */
-    float reserved_f;
-    int64_t level_new[RPQ_STATS_LEVELS];    /* new (state, vertex) pairs per level */
-    int64_t level_edges[RPQ_STATS_LEVELS];  /* edges traversed per level */
+    int32_t pull_levels;     /* levels run in the pull direction */
+    int64_t level_new[RPQ_STATS_LEVELS];    /* |F_L|: new (state, vertex) pairs per level */
+    int64_t level_edges[RPQ_STATS_LEVELS];  /* push-model edges expanded from F_L (-1: pulled) */
+    int8_t level_dir[RPQ_STATS_LEVELS];     /* 0 push, 1 pull */
 } rpq_stats;
+
+/* level direction policy (rpq_query_set_options) */
+#define RPQ_DIR_AUTO 0   /* per level: pull when m_f * alpha > m_u (Beamer) */
+#define RPQ_DIR_PUSH 1   /* always expand the frontier's rows (SpMSpV over CSR) */
+#define RPQ_DIR_PULL 2   /* always scan unvisited rows of the transpose (CSC) */
 
 RPQ_API int rpq_abi_version(void);
 RPQ_API const char* rpq_last_error(void);
@@ -111,6 +118,9 @@ RPQ_API int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans,
                      const int32_t* t_src, const int32_t* t_label, const uint8_t* t_inv,
                      const int32_t* t_dst, int32_t nstarts, const int32_t* starts,
                      int32_t nfinals, const int32_t* finals, rpq_query** out);
+/* Direction policy (RPQ_DIR_*), exact-TE accounting on/off, Beamer's alpha
+ * (default: auto, off, 15).  Results do not depend on these. */
+RPQ_API int rpq_query_set_options(rpq_query* q, int32_t direction, int32_t count_te, double alpha);
 /* Enqueue one evaluation from `source` on `stream` (a cudaStream_t, or NULL for
  * the query's own stream).  timeout_s < 0 or inf: no deadline.  The deadline is
  * checked on the device at the top of every iteration, like _Clock.check. */
@@ -123,6 +133,10 @@ RPQ_API int rpq_query_reach_device(rpq_query* q, uint8_t** d_reach);
 RPQ_API int rpq_query_copy_reach(rpq_query* q, uint8_t* host_reach);
 /* Copy the full visited matrix P (nstates rows x ceil(nv/32) uint32 words). */
 RPQ_API int rpq_query_copy_visited(rpq_query* q, uint32_t* host_words, int64_t nwords);
+/* Bytes one run moves: host->device (the automaton tables, re-sent with every
+ * run) and device->host (the run's status/statistics block; the answer copy
+ * of rpq_query_copy_reach adds num_vertices bytes). */
+RPQ_API int rpq_query_io_bytes(const rpq_query* q, int64_t* h2d_per_run, int64_t* d2h_per_run);
 RPQ_API int rpq_query_destroy(rpq_query* q);
 
 /* One-shot eval_ssr. */

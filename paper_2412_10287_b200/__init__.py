@@ -14,6 +14,7 @@ from .engine import (
     EngineError,
     EngineOptions,
     EvalResult,
+    PreparedQuery,
     QueryTimeout,
     eval_sdr,
     eval_ssr,
@@ -34,6 +35,7 @@ __all__ = [
     "EngineOptions",
     "EvalResult",
     "LabeledGraph",
+    "PreparedQuery",
     "QueryTimeout",
     "TransitionTable",
     "device_graph",

@@ -20,6 +20,10 @@ RPQ_ECUDA = 4
 RPQ_ENOMEM = 5
 RPQ_ENOLABEL = 6
 
+DIR_AUTO = 0
+DIR_PUSH = 1
+DIR_PULL = 2
+
 STATS_LEVELS = 64
 
 c_i32 = ctypes.c_int32
@@ -45,9 +49,10 @@ class RpqStats(ctypes.Structure):
         ("visited_pairs", c_i64),
         ("reach_count", c_i64),
         ("device_ms", ctypes.c_float),
-        ("reserved_f", ctypes.c_float),
+        ("pull_levels", c_i32),
         ("level_new", c_i64 * STATS_LEVELS),
         ("level_edges", c_i64 * STATS_LEVELS),
+        ("level_dir", ctypes.c_int8 * STATS_LEVELS),
     ]
 
     def to_dict(self):
@@ -62,6 +67,8 @@ class RpqStats(ctypes.Structure):
             "visited_pairs": self.visited_pairs,
             "reach_count": self.reach_count,
             "device_ms": self.device_ms,
+            "pull_levels": self.pull_levels,
+            "level_dir": list(self.level_dir[:nlev]),
             "level_new": list(self.level_new[:nlev]),
             "level_edges": list(self.level_edges[:nlev]),
         }
@@ -80,11 +87,13 @@ ENGINE_SIGNATURES = {
     "rpq_graph_destroy": (c_i32, [c_vp]),
     "rpq_query_create": (c_i32, [c_vp, c_i32, c_i32, P_i32, P_i32, P_u8, P_i32, c_i32, P_i32,
                                  c_i32, P_i32, ctypes.POINTER(c_vp)]),
+    "rpq_query_set_options": (c_i32, [c_vp, c_i32, c_i32, c_dbl]),
     "rpq_query_run": (c_i32, [c_vp, c_i32, c_dbl, c_vp]),
     "rpq_query_wait": (c_i32, [c_vp, ctypes.POINTER(RpqStats)]),
     "rpq_query_reach_device": (c_i32, [c_vp, ctypes.POINTER(P_u8)]),
     "rpq_query_copy_reach": (c_i32, [c_vp, P_u8]),
     "rpq_query_copy_visited": (c_i32, [c_vp, P_u32, c_i64]),
+    "rpq_query_io_bytes": (c_i32, [c_vp, P_i64, P_i64]),
     "rpq_query_destroy": (c_i32, [c_vp]),
     "rpq_ssr": (c_i32, [c_vp, c_i32, c_i32, P_i32, P_i32, P_u8, P_i32, c_i32, P_i32, c_i32, P_i32,
                         c_i32, c_dbl, P_u8, ctypes.POINTER(RpqStats)]),

@@ -1,27 +1,8 @@
-// rpq_b200.cu -- B200-native (sm_100a) single-source 2-RPQ frontier BFS.
-//
-// Replaces the reference's per-level frontier step
-//   M <- (sum_a (N^a)^T x M x G^a) <not P>;  P <- P + M      (Alg. 1;
-//   rpq/engine.py:117-124 _step_sum, :146-171 eval_ssr_masked)
-// with one persistent cooperative kernel per query.  See DESIGN.md for the
-// layout; in short:
-//
-//   graph     per label and direction: uint32 row pointers + int32 columns
-//             (forward[l] and backward[l] = transpose, graph_store.py:51-52)
-//   automaton (state, slot) "groups": slot = (label, inverted) adjacency,
-//             targets = the states reached on that symbol (transition matrix row)
-//   P         |Q| bitmaps of |V| bits (visited), L2-resident for the configs
-//   frontier  a work queue of row SEGMENTS (one per discovered (state, vertex)
-//             pair and out-group with non-empty adjacency row) cut into
-//             BUNDLES of <= 64 edges; producers emit the next level's
-//             segments the moment they discover a pair, so each BFS level is
-//             exactly one pass over the queue and one grid barrier.
-//
-// mask_complement + or_sum of the reference (engine.py:159, :165) are fused
-// into the expansion: the first thread whose atomicOr sets a (state, vertex)
-// bit owns the discovery.  np.unique's dedup (sparse_bool.py:250) is implicit
-// in the bitmap.  The answer projection F x P (engine.py:112-114) is the
-// kernel's epilogue.
+// rpq_b200.cu -- host side of the B200-native (sm_100a) single-source 2-RPQ
+// engine behind the C ABI of include/rpq_b200.h: graph residency (per-label
+// CSR in both directions, graph_store.py:51-52), query compilation into the
+// kernel's tables (_label_pairs, engine.py:92-103), workspaces, launch.
+// The device code is in ssr_kernel.cuh.
 #include "rpq_b200.h"
 
 #include <cuda_runtime.h>
@@ -36,6 +17,10 @@
 #include <string>
 #include <vector>
 
+#include "ssr_kernel.cuh"
+
+using namespace rpqk;
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -46,7 +31,7 @@ int fail(int code, const std::string& msg) {
 }
 
 int cuda_fail(cudaError_t e, const char* what) {
-    cudaGetLastError();  // clear sticky-free errors
+    cudaGetLastError();
     return fail(e == cudaErrorMemoryAllocation ? RPQ_ENOMEM : RPQ_ECUDA,
                 std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -56,525 +41,6 @@ int cuda_fail(cudaError_t e, const char* what) {
         cudaError_t e_ = (expr);                            \
         if (e_ != cudaSuccess) return cuda_fail(e_, #expr); \
     } while (0)
-
-constexpr int kThreads = 256;        // 8 warps per CTA
-constexpr int kMinBlocks = 3;       // CTAs per SM the register budget is sized for
-constexpr int kBundle = 32;          // edges per bundle (one per lane; <= 32 segments)
-constexpr int kShards = 64;          // queue shards (+1 overflow shard), by CTA id
-constexpr int kMaxStates = 1024;
-constexpr int kMaxGroups = 256;      // group id is 8 bits in a segment
-constexpr int kMaxSlots = 256;
-constexpr uint32_t kSegLenMax = (1u << 24) - 1;
-constexpr unsigned FULL = 0xffffffffu;
-
-constexpr int ST_OVERFLOW = 100;     // internal: queue capacity exceeded
-constexpr int ST_DEADLOCK = 101;     // internal: barrier spin limit hit
-
-struct Slot {
-    const uint32_t* rowptr;
-    const int32_t* col;
-};
-
-struct Ctl {
-    unsigned int bar_count;
-    unsigned int bar_gen;
-    int status;
-    int done;
-    int iterations;
-    int levels;
-    int overflow;
-    int pad0;
-    unsigned long long t0;
-    // per queue buffer and shard: (segments << 32) | bundles
-    unsigned long long shard_cnt[2][kShards + 1];
-    unsigned long long new_cnt[2];
-    unsigned long long edge_cnt[2];
-    unsigned long long seg_total[2];
-    unsigned long long te;
-    unsigned long long segments;
-    unsigned long long pairs;
-    unsigned long long reach_count;
-    long long level_new[RPQ_STATS_LEVELS];
-    long long level_edges[RPQ_STATS_LEVELS];
-};
-
-// Kernel parameters.  Tables are small int32 arrays staged into shared memory:
-//   gbeg[nstates+1]  groups of state q are [gbeg[q], gbeg[q+1])
-//   gslot[ngroups]   slot of each group
-//   toff[ngroups+1]  targets of group g are targets[toff[g] .. toff[g+1])
-//   targets[ntargets]
-//   starts[nstarts], finals[nfinals]
-struct Params {
-    const int32_t* tables;
-    const Slot* slots;
-    uint32_t* visited;
-    uint2* seg[2];
-    uint2* bun[2];
-    Ctl* ctl;
-    uint8_t* reach;
-    unsigned long long shard_segcap;   // per regular shard
-    unsigned long long shard_buncap;
-    unsigned long long ovf_segcap;     // overflow shard (index kShards)
-    unsigned long long ovf_buncap;
-    unsigned long long seg_alloc;      // entries allocated per buffer
-    unsigned long long bun_alloc;
-    unsigned long long budget_ns;
-    long long W;  // uint32 words per visited row (multiple of 4)
-    int nv;
-    int nstates, ngroups, nslots, ntargets, nstarts, nfinals;
-    int maxT;  // max targets per group
-    int source;
-    int table_ints;
-};
-
-struct Smem {
-    const int32_t* gbeg;
-    const int32_t* gslot;
-    const int32_t* toff;
-    const int32_t* targets;
-    const int32_t* starts;
-    const int32_t* finals;
-    const Slot* slots;
-};
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long globaltimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-__device__ __forceinline__ unsigned lanemask_lt() {
-    unsigned m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
-}
-template <typename T>
-__device__ __forceinline__ T ld_volatile(const T* p) {
-    return *reinterpret_cast<const volatile T*>(p);
-}
-
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        uint32_t o = __shfl_up_sync(FULL, v, d);
-        if (lane >= d) v += o;
-    }
-    return v;
-}
-
-// largest lane j with key_j <= x (key non-decreasing across lanes, key_0 <= x)
-__device__ __forceinline__ int warp_upper_lane(uint32_t key, uint32_t x) {
-    int j = 0;
-#pragma unroll
-    for (int step = 16; step >= 1; step >>= 1) {
-        int cand = j + step;
-        uint32_t k = __shfl_sync(FULL, key, cand & 31);
-        if (cand < 32 && k <= x) j = cand;
-    }
-    return j;
-}
-
-// Grid barrier for a cooperative launch.  The last CTA to arrive runs
-// `serial` (one thread) before releasing everyone: per-level bookkeeping is
-// thereby ordered after all CTAs' work and before any CTA's next level.
-template <class F>
-__device__ __forceinline__ void grid_sync(Ctl* ctl, F serial) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned nblocks = gridDim.x;
-        unsigned gen = ld_acquire_u32(&ctl->bar_gen);
-        __threadfence();
-        unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
-        if (arrived == nblocks - 1) {
-            __threadfence();
-            serial();
-            ctl->bar_count = 0;
-            __threadfence();
-            st_release_u32(&ctl->bar_gen, gen + 1);
-        } else {
-            unsigned long long ts = 0;
-            unsigned spins = 0;
-            while (ld_acquire_u32(&ctl->bar_gen) == gen) {
-                __nanosleep(32);
-                if ((++spins & 4095u) == 0) {
-                    unsigned long long now = globaltimer();
-                    if (ts == 0) ts = now;
-                    else if (now - ts > 20000000000ull) {  // 20 s: cannot happen co-resident
-                        atomicExch(&ctl->status, ST_DEADLOCK);
-                        atomicExch(&ctl->done, 1);
-                        break;
-                    }
-                }
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-constexpr uint32_t kHoleBundle = 0xFFFFFFFFu;  // bundle slot left empty by a spill
-
-// Shard-local reservation of `nseg` segments and `nb` bundles in queue buffer
-// `b` (called by one lane).  Regular shards are indexed by CTA; a reservation
-// that does not fit spills to the overflow shard, and the part of its bundle
-// range that lies inside the regular shard, [*hole_lo, *hole_hi), must be
-// filled with kHoleBundle by the caller.  Returns false when even the
-// overflow shard is full.
-__device__ __forceinline__ bool reserve(const Params& p, int b, uint32_t nseg, uint32_t nb,
-                                        unsigned long long* seg_idx, unsigned long long* bun_idx,
-                                        unsigned long long* hole_lo, unsigned long long* hole_hi) {
-    Ctl* ctl = p.ctl;
-    const int shard = blockIdx.x % kShards;
-    const unsigned long long inc = ((unsigned long long)nseg << 32) | nb;
-    unsigned long long old = atomicAdd(&ctl->shard_cnt[b][shard], inc);
-    unsigned long long s_loc = old >> 32, b_loc = old & 0xFFFFFFFFull;
-    *hole_lo = *hole_hi = 0;
-    if (s_loc + nseg <= p.shard_segcap && b_loc + nb <= p.shard_buncap) {
-        *seg_idx = (unsigned long long)shard * p.shard_segcap + s_loc;
-        *bun_idx = (unsigned long long)shard * p.shard_buncap + b_loc;
-        return true;
-    }
-    if (b_loc < p.shard_buncap) {
-        *hole_lo = (unsigned long long)shard * p.shard_buncap + b_loc;
-        *hole_hi = (unsigned long long)shard * p.shard_buncap +
-                   (b_loc + nb < p.shard_buncap ? b_loc + nb : p.shard_buncap);
-    }
-    old = atomicAdd(&ctl->shard_cnt[b][kShards], inc);
-    s_loc = old >> 32;
-    b_loc = old & 0xFFFFFFFFull;
-    if (s_loc + nseg <= p.ovf_segcap && b_loc + nb <= p.ovf_buncap) {
-        *seg_idx = (unsigned long long)kShards * p.shard_segcap + s_loc;
-        *bun_idx = (unsigned long long)kShards * p.shard_buncap + b_loc;
-        return true;
-    }
-    return false;
-}
-
-// Warp-cooperative emission of the row segments of newly discovered
-// (state q, vertex w) pairs (one candidate per lane) into queue buffer `b`.
-// Returns the number of edges emitted (valid in every lane).
-__device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, int b, bool valid,
-                                            int q, int w, int lane) {
-    const unsigned vmask = __ballot_sync(FULL, valid);
-    if (vmask == 0) return 0;
-    const int ng = valid ? (S.gbeg[q + 1] - S.gbeg[q]) : 0;
-    int maxng = ng;
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) maxng = max(maxng, __shfl_xor_sync(FULL, maxng, d));
-    uint2* seg = p.seg[b];
-    uint2* bun = p.bun[b];
-    uint32_t emitted = 0;
-    for (int k = 0; k < maxng; ++k) {
-        uint32_t lo = 0, deg = 0;
-        int g = 0;
-        if (k < ng) {
-            g = S.gbeg[q] + k;
-            const Slot sl = S.slots[S.gslot[g]];
-            lo = __ldg(sl.rowptr + w);
-            deg = __ldg(sl.rowptr + w + 1) - lo;
-        }
-        for (;;) {  // rows longer than a segment are split (rare)
-            const uint32_t take = min(deg, kSegLenMax);
-            const bool hs = take > 0;
-            const unsigned m = __ballot_sync(FULL, hs);
-            if (m == 0) break;
-            const int rank = __popc(m & lanemask_lt());
-            const uint32_t nseg = (uint32_t)__popc(m);
-            const uint32_t incl = warp_incl_scan(take, lane);
-            const uint32_t excl = incl - take;
-            const uint32_t T = __shfl_sync(FULL, incl, 31);
-            const uint32_t nb = (T + kBundle - 1) / kBundle;
-            unsigned long long sbase = 0, bbase = 0, hlo = 0, hhi = 0;
-            int ok = 1;
-            if (lane == 0) ok = reserve(p, b, nseg, nb, &sbase, &bbase, &hlo, &hhi) ? 1 : 0;
-            ok = __shfl_sync(FULL, ok, 0);
-            hlo = __shfl_sync(FULL, hlo, 0);
-            hhi = __shfl_sync(FULL, hhi, 0);
-            for (unsigned long long h = hlo + lane; h < hhi; h += 32) bun[h] = make_uint2(kHoleBundle, 0);
-            if (!ok) {
-                if (lane == 0) atomicExch(&p.ctl->overflow, 1);
-                return emitted;
-            }
-            sbase = __shfl_sync(FULL, sbase, 0);
-            bbase = __shfl_sync(FULL, bbase, 0);
-            if (hs) seg[sbase + rank] = make_uint2(lo, (take << 8) | (uint32_t)g);
-            for (uint32_t kb0 = 0; kb0 < nb; kb0 += 32) {
-                const uint32_t kb = kb0 + lane;
-                const uint32_t pos = kb * kBundle;
-                const int j = warp_upper_lane(excl, min(pos, T - 1));
-                const uint32_t exj = __shfl_sync(FULL, excl, j);
-                const int rj = __shfl_sync(FULL, rank, j);
-                if (kb < nb) {
-                    const uint32_t cnt = min((uint32_t)kBundle, T - pos);
-                    bun[bbase + kb] = make_uint2((uint32_t)(sbase + rj), (pos - exj) | ((cnt - 1) << 24));
-                }
-            }
-            emitted += T;
-            lo += take;
-            deg -= take;
-        }
-    }
-    return emitted;
-}
-
-// Per-CTA flush of the level's statistics (one atomic per CTA and counter).
-__device__ __forceinline__ void flush_counts(Ctl* ctl, int b, unsigned long long nnew,
-                                             unsigned long long nedge, unsigned long long* red) {
-    // red: 2 * (kThreads/32) shared slots
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
-        nnew += __shfl_xor_sync(FULL, nnew, d);
-        nedge += __shfl_xor_sync(FULL, nedge, d);
-    }
-    if (lane == 0) {
-        red[2 * wid] = nnew;
-        red[2 * wid + 1] = nedge;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long a = 0, c = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
-            a += red[2 * i];
-            c += red[2 * i + 1];
-        }
-        if (a) atomicAdd(&ctl->new_cnt[b], a);
-        if (c) atomicAdd(&ctl->edge_cnt[b], c);
-    }
-    __syncthreads();
-}
-
-// Bookkeeping after frontier F_L (queue buffer L&1) has been produced.
-// Mirrors the masked loop exactly (engine.py:156-160): the loop runs while the
-// frontier is non-empty, checks the deadline first, then steps.
-__device__ __forceinline__ void level_bookkeeping(const Params& p, int L) {
-    Ctl* ctl = p.ctl;
-    const int b = L & 1;
-    const unsigned long long nnew = ld_volatile(&ctl->new_cnt[b]);
-    const unsigned long long nedge = ld_volatile(&ctl->edge_cnt[b]);
-    unsigned long long nbun = 0, nseg = 0;
-    for (int s = 0; s <= kShards; ++s) {
-        const unsigned long long c = ld_volatile(&ctl->shard_cnt[b][s]);
-        const unsigned long long bc = c & 0xFFFFFFFFull, sc = c >> 32;
-        const unsigned long long bcap = s < kShards ? p.shard_buncap : p.ovf_buncap;
-        const unsigned long long scap = s < kShards ? p.shard_segcap : p.ovf_segcap;
-        nbun += bc < bcap ? bc : bcap;
-        nseg += sc < scap ? sc : scap;
-    }
-    ctl->pairs += nnew;
-    if (L < RPQ_STATS_LEVELS) ctl->level_new[L] = (long long)nnew;
-    if (ld_volatile(&ctl->overflow)) {
-        ctl->status = ST_OVERFLOW;
-        ctl->iterations = L;
-        ctl->done = 1;
-    } else if (ld_volatile(&ctl->status) != 0) {
-        ctl->done = 1;
-    } else if (nnew == 0) {
-        ctl->iterations = L;
-        ctl->done = 1;
-    } else {
-        if (L > 0) ctl->levels = L;
-        if (globaltimer() - ctl->t0 > p.budget_ns) {
-            ctl->status = RPQ_ETIMEOUT;
-            ctl->iterations = L;
-            ctl->done = 1;
-        } else {
-            if (L < RPQ_STATS_LEVELS) ctl->level_edges[L] = (long long)nedge;
-            ctl->te += nedge;
-            ctl->segments += nseg;
-            if (nbun == 0) {  // nothing to expand: the next step is empty
-                ctl->iterations = L + 1;
-                ctl->done = 1;
-            }
-        }
-    }
-    // the other buffer is produced into during the next level
-    for (int s = 0; s <= kShards; ++s) {
-        ctl->shard_cnt[b ^ 1][s] = 0;
-    }
-    ctl->new_cnt[b ^ 1] = 0;
-    ctl->edge_cnt[b ^ 1] = 0;
-}
-
-__global__ void __launch_bounds__(kThreads, kMinBlocks) rpq_ssr_kernel(Params p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ unsigned long long s_red[2 * (kThreads / 32)];
-    __shared__ unsigned long long s_bpre[kShards + 2];  // bundle prefix over shards
-    __shared__ unsigned long long s_bbase[kShards + 1]; // bundle base index of each shard
-    Slot* s_slots = reinterpret_cast<Slot*>(smem_raw);
-    int32_t* s_tab = reinterpret_cast<int32_t*>(smem_raw + sizeof(Slot) * p.nslots);
-    for (int i = threadIdx.x; i < p.nslots; i += blockDim.x) s_slots[i] = p.slots[i];
-    for (int i = threadIdx.x; i < p.table_ints; i += blockDim.x) s_tab[i] = p.tables[i];
-    Smem S;
-    S.slots = s_slots;
-    S.gbeg = s_tab;
-    S.gslot = S.gbeg + p.nstates + 1;
-    S.toff = S.gslot + p.ngroups;
-    S.targets = S.toff + p.ngroups + 1;
-    S.starts = S.targets + p.ntargets;
-    S.finals = S.starts + p.nstarts;
-
-    Ctl* ctl = p.ctl;
-    const int lane = threadIdx.x & 31;
-    const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long gthreads = (long long)gridDim.x * blockDim.x;
-    if (gtid == 0) ctl->t0 = globaltimer();
-
-    // ---- phase 0: P <- 0 --------------------------------------------------
-    {
-        uint4* v4 = reinterpret_cast<uint4*>(p.visited);
-        const long long n4 = (long long)p.nstates * p.W / 4;
-        for (long long i = gtid; i < n4; i += gthreads) v4[i] = make_uint4(0, 0, 0, 0);
-    }
-    grid_sync(ctl, [] {});
-
-    // ---- seed: P = M = {(q_s, source)} (engine.py:106-109, :154-155) ------
-    {
-        unsigned long long nnew = 0, nedge = 0;
-        if (blockIdx.x == 0 && threadIdx.x < 32) {
-            for (int i0 = 0; i0 < p.nstarts; i0 += 32) {
-                const int i = i0 + lane;
-                bool fresh = false;
-                int q = 0;
-                if (i < p.nstarts) {
-                    q = S.starts[i];
-                    uint32_t* word = p.visited + (long long)q * p.W + (p.source >> 5);
-                    const uint32_t bit = 1u << (p.source & 31);
-                    fresh = !(atomicOr(word, bit) & bit);
-                }
-                nnew += fresh ? 1 : 0;
-                const uint32_t T = emit_pairs(p, S, 0, fresh, q, p.source, lane);
-                if (lane == 0) nedge += T;
-            }
-        }
-        flush_counts(ctl, 0, nnew, nedge, s_red);
-    }
-    grid_sync(ctl, [&] { level_bookkeeping(p, 0); });
-
-    // ---- level loop ---------------------------------------------------------
-    const int wid = threadIdx.x >> 5;
-    const int wpb = blockDim.x >> 5;
-    for (int L = 0;; ++L) {
-        if (ld_volatile(&ctl->done)) break;
-        const int cur = L & 1, nxt = cur ^ 1;
-        // bundle prefix over shards (each shard's bundles are contiguous)
-        if (threadIdx.x == 0) {
-            unsigned long long run = 0;
-            for (int s = 0; s <= kShards; ++s) {
-                s_bpre[s] = run;
-                s_bbase[s] = (unsigned long long)s * p.shard_buncap;
-                unsigned long long c = ld_volatile(&ctl->shard_cnt[cur][s]) & 0xFFFFFFFFull;
-                const unsigned long long cap = s < kShards ? p.shard_buncap : p.ovf_buncap;
-                run += c < cap ? c : cap;
-            }
-            s_bpre[kShards + 1] = run;
-        }
-        __syncthreads();
-        const unsigned long long nb = s_bpre[kShards + 1];
-        const uint2* bun = p.bun[cur];
-        const uint2* seg = p.seg[cur];
-        unsigned long long nnew = 0, nedge = 0;
-        // bundles are dealt round-robin over warps, CTA-major so that
-        // consecutive bundles (often of one row) land on different SMs
-        const unsigned long long step = (unsigned long long)gridDim.x * wpb;
-        for (unsigned long long bi = (unsigned long long)wid * gridDim.x + blockIdx.x; bi < nb; bi += step) {
-            int s = 0;
-#pragma unroll
-            for (int h = 64; h >= 1; h >>= 1)
-                if (s + h <= kShards && s_bpre[s + h] <= bi) s += h;
-            const uint2 bd = __ldcg(bun + s_bbase[s] + (bi - s_bpre[s]));
-            if (bd.x == kHoleBundle) continue;
-            const uint32_t s0 = bd.x;
-            const uint32_t off = bd.y & 0xFFFFFFu;
-            const uint32_t cnt = (bd.y >> 24) + 1;
-            uint32_t my_start = 0, my_len = 0, my_grp = 0;
-            if ((unsigned long long)s0 + lane < p.seg_alloc) {
-                const uint2 sg = __ldcg(seg + s0 + lane);
-                my_start = sg.x;
-                my_len = sg.y >> 8;
-                my_grp = sg.y & 0xFFu;
-            }
-            if (lane == 0) {
-                my_start += off;
-                my_len -= off;
-            }
-            const uint32_t incl = warp_incl_scan(my_len, lane);
-            const uint32_t excl = incl - my_len;
-            const uint32_t e = lane;
-            const bool active = e < cnt;
-            const int j = warp_upper_lane(excl, active ? e : 0);
-            const uint32_t sj = __shfl_sync(FULL, my_start, j);
-            const uint32_t exj = __shfl_sync(FULL, excl, j);
-            const int gj = (int)__shfl_sync(FULL, my_grp, j);
-            int w = 0;
-            int t0 = 0, t1 = 0;
-            if (active) {
-                const Slot sl = S.slots[S.gslot[gj]];
-                w = __ldg(sl.col + sj + (e - exj));
-                t0 = S.toff[gj];
-                t1 = S.toff[gj + 1];
-            }
-            for (int k = 0; k < p.maxT; ++k) {
-                bool fresh = false;
-                int q2 = 0;
-                if (active && t0 + k < t1) {
-                    q2 = S.targets[t0 + k];
-                    uint32_t* word = p.visited + (long long)q2 * p.W + (w >> 5);
-                    const uint32_t bit = 1u << (w & 31);
-                    if (!(*word & bit)) fresh = !(atomicOr(word, bit) & bit);
-                }
-                nnew += fresh ? 1 : 0;
-                const uint32_t T = emit_pairs(p, S, nxt, fresh, q2, w, lane);
-                if (lane == 0) nedge += T;
-            }
-        }
-        flush_counts(ctl, nxt, nnew, nedge, s_red);
-        grid_sync(ctl, [&] { level_bookkeeping(p, L + 1); });
-    }
-
-    // ---- epilogue: answer = OR of P's rows at final states (engine.py:112-114)
-    if (ld_volatile(&ctl->status) == 0) {
-        const long long nwords = ((long long)p.nv + 31) >> 5;
-        unsigned long long cnt = 0;
-        for (long long i = gtid; i < nwords; i += gthreads) {
-            uint32_t acc = 0;
-            for (int f = 0; f < p.nfinals; ++f)
-                acc |= __ldcg(p.visited + (long long)S.finals[f] * p.W + i);
-            cnt += __popc(acc);
-            uint8_t* out = p.reach + i * 32;
-            if (i * 32 + 32 <= p.nv) {
-                uint32_t bytes[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint32_t nib = (acc >> (4 * k)) & 0xFu;
-                    bytes[k] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
-                }
-                reinterpret_cast<uint4*>(out)[0] = make_uint4(bytes[0], bytes[1], bytes[2], bytes[3]);
-                reinterpret_cast<uint4*>(out)[1] = make_uint4(bytes[4], bytes[5], bytes[6], bytes[7]);
-            } else {
-                for (int k = 0; i * 32 + k < p.nv; ++k) out[k] = (acc >> k) & 1u;
-            }
-        }
-#pragma unroll
-        for (int d = 16; d >= 1; d >>= 1) cnt += __shfl_xor_sync(FULL, cnt, d);
-        if (lane == 0 && cnt) atomicAdd(&ctl->reach_count, cnt);
-    }
-}
-
-// int64 -> narrow copy used at upload (sparse_bool.py keeps int64 everywhere)
-template <typename In, typename Out>
-__global__ void narrow_kernel(const In* __restrict__ in, Out* __restrict__ out, long long n) {
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x)
-        out[i] = (Out)in[i];
-}
 
 }  // namespace
 
@@ -602,12 +68,17 @@ struct rpq_graph {
 struct rpq_query {
     rpq_graph* g = nullptr;
     int32_t nstates = 0;
-    std::vector<int32_t> tables;  // host copy
-    std::vector<Slot> slots;
-    int ngroups = 0, nslots = 0, ntargets = 0, nstarts = 0, nfinals = 0, maxT = 0;
+    std::vector<int32_t> tables;  // kernel tables, layout of rpqk::Smem
+    std::vector<Slot> slots;      // A_s for every slot, then A_s^T
+    std::vector<unsigned long long> slot_nnz;
+    int ngroups = 0, nslots = 0, ntargets = 0, nstarts = 0, nfinals = 0, nin = 0, maxT = 0;
     int32_t* d_tables = nullptr;
     Slot* d_slots = nullptr;
+    unsigned long long* d_slot_nnz = nullptr;
+    int32_t* h_tables = nullptr;  // pinned copies, re-sent with every run
+    Slot* h_slots = nullptr;
     uint32_t* d_visited = nullptr;
+    uint32_t* d_fb[3] = {nullptr, nullptr, nullptr};
     uint2* d_seg[2] = {nullptr, nullptr};
     uint2* d_bun[2] = {nullptr, nullptr};
     Ctl* d_ctl = nullptr;
@@ -616,13 +87,15 @@ struct rpq_query {
     unsigned long long shard_segcap = 0, shard_buncap = 0, ovf_segcap = 0, ovf_buncap = 0;
     unsigned long long seg_alloc = 0, bun_alloc = 0;
     long long W = 0;
+    int dir_mode = 0;
+    int count_te = 0;
+    float alpha = 15.0f;
     cudaStream_t own_stream = nullptr;
     cudaStream_t last_stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int grid = 0;
     size_t smem = 0;
     bool ran = false;
-    std::mutex mu;
 };
 
 namespace {
@@ -686,11 +159,16 @@ int set_label_impl(rpq_graph* g, int32_t label, int64_t fn, const I* fp, const I
 void free_query_buffers(rpq_query* q) {
     if (q->d_tables) cudaFree(q->d_tables);
     if (q->d_slots) cudaFree(q->d_slots);
+    if (q->d_slot_nnz) cudaFree(q->d_slot_nnz);
     if (q->d_visited) cudaFree(q->d_visited);
+    for (int f = 0; f < 3; ++f)
+        if (q->d_fb[f]) cudaFree(q->d_fb[f]);
     for (int b = 0; b < 2; ++b) {
         if (q->d_seg[b]) cudaFree(q->d_seg[b]);
         if (q->d_bun[b]) cudaFree(q->d_bun[b]);
     }
+    if (q->h_tables) cudaFreeHost(q->h_tables);
+    if (q->h_slots) cudaFreeHost(q->h_slots);
     if (q->d_ctl) cudaFree(q->d_ctl);
     if (q->h_ctl) cudaFreeHost(q->h_ctl);
     if (q->d_reach) cudaFree(q->d_reach);
@@ -780,10 +258,12 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
         (nfinals && !finals))
         return fail(RPQ_EINVAL, "null automaton array");
 
-    // usable transitions -> slots (label, inv) and (state, slot) groups
+    // usable transitions -> slots (label, inv), push groups (state, slot) ->
+    // targets, pull in-transitions target -> (source state, slot)
     std::map<std::pair<int, int>, int> slot_of;
-    std::map<std::pair<int, int>, std::set<int>> group_targets;  // (state, slot) -> targets
     std::vector<std::pair<int, int>> slot_keys;
+    std::map<std::pair<int, int>, std::set<int>> group_targets;
+    std::map<int, std::set<std::pair<int, int>>> in_trans;
     {
         std::set<std::pair<int, int>> keys;
         for (int i = 0; i < ntrans; ++i) {
@@ -799,8 +279,9 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
         }
         for (int i = 0; i < ntrans; ++i) {
             if (t_label[i] >= g->nl) continue;
-            int s = slot_of[{t_label[i], t_inv[i] ? 1 : 0}];
-            group_targets[{t_src[i], s}].insert(t_dst[i]);
+            const int sl = slot_of[{t_label[i], t_inv[i] ? 1 : 0}];
+            group_targets[{t_src[i], sl}].insert(t_dst[i]);
+            in_trans[t_dst[i]].insert({t_src[i], sl});
         }
     }
     if ((int)slot_keys.size() > kMaxSlots) return fail(RPQ_EINVAL, "too many distinct symbols");
@@ -813,23 +294,32 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     rpq_query* q = new rpq_query();
     q->g = g;
     q->nstates = nstates;
-    std::vector<int32_t> gbeg(nstates + 1, 0), gslot, toff, targets;
+    std::vector<int32_t> gbeg(nstates + 1, 0), gslot, toff, targets, ibeg(nstates + 1, 0), isrc,
+        islot;
     std::vector<int> gcount(nstates, 0);
     for (auto& kv : group_targets) gcount[kv.first.first]++;
-    for (int s = 0; s < nstates; ++s) gbeg[s + 1] = gbeg[s] + gcount[s];
-    // std::map iterates (state, slot) in order, so groups of a state are contiguous
+    for (int st = 0; st < nstates; ++st) gbeg[st + 1] = gbeg[st] + gcount[st];
+    // std::map iterates (state, slot) in order, so a state's groups are contiguous
     int maxT = 0;
     toff.push_back(0);
-    uint64_t seg_per_vertex = 0, edge_bound = 0;
+    uint64_t groups_total = 0, edge_bound = 0;
     for (auto& kv : group_targets) {
         gslot.push_back(kv.first.second);
         for (int t : kv.second) targets.push_back(t);
         toff.push_back((int32_t)targets.size());
         maxT = std::max<int>(maxT, (int)kv.second.size());
         const auto& key = slot_keys[kv.first.second];
-        const int64_t nnz = g->labels[key.first].nnz[key.second];
-        seg_per_vertex += 1;
-        edge_bound += (uint64_t)nnz;
+        groups_total += 1;
+        edge_bound += (uint64_t)g->labels[key.first].nnz[key.second];
+    }
+    for (int st = 0; st < nstates; ++st) {
+        auto it = in_trans.find(st);
+        if (it != in_trans.end())
+            for (auto& e : it->second) {
+                isrc.push_back(e.first);
+                islot.push_back(e.second);
+            }
+        ibeg[st + 1] = (int32_t)isrc.size();
     }
     std::set<int> sset, fset;
     for (int i = 0; i < nstarts; ++i)
@@ -841,24 +331,31 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     q->ntargets = (int)targets.size();
     q->nstarts = (int)sset.size();
     q->nfinals = (int)fset.size();
+    q->nin = (int)isrc.size();
     q->maxT = maxT;
-    q->tables.insert(q->tables.end(), gbeg.begin(), gbeg.end());
-    q->tables.insert(q->tables.end(), gslot.begin(), gslot.end());
-    q->tables.insert(q->tables.end(), toff.begin(), toff.end());
-    q->tables.insert(q->tables.end(), targets.begin(), targets.end());
-    q->tables.insert(q->tables.end(), sset.begin(), sset.end());
-    q->tables.insert(q->tables.end(), fset.begin(), fset.end());
-    for (auto& k : slot_keys) {
-        const LabelDev& L = g->labels[k.first];
-        q->slots.push_back(Slot{L.rowptr[k.second], L.col[k.second]});
-    }
+    auto& T = q->tables;
+    T.insert(T.end(), gbeg.begin(), gbeg.end());
+    T.insert(T.end(), gslot.begin(), gslot.end());
+    T.insert(T.end(), toff.begin(), toff.end());
+    T.insert(T.end(), targets.begin(), targets.end());
+    T.insert(T.end(), sset.begin(), sset.end());
+    T.insert(T.end(), fset.begin(), fset.end());
+    T.insert(T.end(), ibeg.begin(), ibeg.end());
+    T.insert(T.end(), isrc.begin(), isrc.end());
+    T.insert(T.end(), islot.begin(), islot.end());
+    for (int pass = 0; pass < 2; ++pass)
+        for (auto& k : slot_keys) {
+            const LabelDev& L = g->labels[k.first];
+            const int d = pass == 0 ? k.second : 1 - k.second;  // pass 1: the transpose
+            q->slots.push_back(Slot{L.rowptr[d], L.col[d]});
+        }
+    for (auto& k : slot_keys) q->slot_nnz.push_back((unsigned long long)g->labels[k.first].nnz[k.second]);
+
     // queue capacities: every (state, vertex) pair is discovered at most once,
-    // so a level holds at most |V| segments per group (+ splits of huge rows);
-    // bundles are at most one partial per emission plus edges / kBundle.
-    const uint64_t nv = (uint64_t)g->nv;
-    // bound = worst case of one level; regular shards get 1/kShards of it
-    // with headroom, the overflow shard the whole bound
-    const unsigned long long segbound = nv * seg_per_vertex + edge_bound / kSegLenMax + 64;
+    // so one level holds at most |V| segments per group (+ splits of huge
+    // rows); bundles are at most one partial per emission plus edges/kBundle.
+    const unsigned long long nv = (unsigned long long)g->nv;
+    const unsigned long long segbound = nv * groups_total + edge_bound / kSegLenMax + 64;
     const unsigned long long bunbound = segbound + edge_bound / kBundle + 64;
     q->shard_segcap = segbound / kShards + segbound / (4 * kShards) + 1024;
     q->shard_buncap = bunbound / kShards + bunbound / (4 * kShards) + 1024;
@@ -866,9 +363,10 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     q->ovf_buncap = bunbound;
     q->seg_alloc = q->shard_segcap * kShards + q->ovf_segcap + 32;
     q->bun_alloc = q->shard_buncap * kShards + q->ovf_buncap;
-    if (q->seg_alloc >= 0xFFFFFFFFull || q->shard_buncap >= 0xFFFFFFFFull || q->ovf_buncap >= 0xFFFFFFFFull) {
+    if (q->seg_alloc >= 0xFFFFFFFFull || q->shard_buncap >= 0xFFFFFFFFull ||
+        q->ovf_buncap >= 0xFFFFFFFFull) {
         delete q;
-        return fail(RPQ_EINVAL, "segment queue would exceed 2^32 entries");
+        return fail(RPQ_EINVAL, "frontier queue would exceed 2^32 entries");
     }
     q->W = (((long long)g->nv + 31) / 32 + 3) / 4 * 4;
 
@@ -878,19 +376,22 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
         return rc;
     };
     if (cudaSetDevice(g->device) != cudaSuccess) return bail(fail(RPQ_ECUDA, "cudaSetDevice"));
-#define QTRY(expr)                                                  \
-    do {                                                            \
-        cudaError_t e_ = (expr);                                    \
-        if (e_ != cudaSuccess) return bail(cuda_fail(e_, #expr));   \
+#define QTRY(expr)                                                \
+    do {                                                          \
+        cudaError_t e_ = (expr);                                  \
+        if (e_ != cudaSuccess) return bail(cuda_fail(e_, #expr)); \
     } while (0)
-    QTRY(cudaMalloc(&q->d_tables, std::max<size_t>(q->tables.size(), 1) * sizeof(int32_t)));
+    const size_t bitmap_bytes = (size_t)q->W * nstates * sizeof(uint32_t);
+    QTRY(cudaMalloc(&q->d_tables, std::max<size_t>(T.size(), 1) * sizeof(int32_t)));
     QTRY(cudaMalloc(&q->d_slots, std::max<size_t>(q->slots.size(), 1) * sizeof(Slot)));
-    QTRY(cudaMalloc(&q->d_visited, (size_t)q->W * nstates * sizeof(uint32_t)));
+    QTRY(cudaMalloc(&q->d_slot_nnz, std::max<size_t>(q->slot_nnz.size(), 1) * sizeof(unsigned long long)));
+    QTRY(cudaMalloc(&q->d_visited, bitmap_bytes));
+    for (int f = 0; f < 3; ++f) QTRY(cudaMalloc(&q->d_fb[f], bitmap_bytes));
     for (int b = 0; b < 2; ++b) {
         QTRY(cudaMalloc(&q->d_seg[b], (size_t)q->seg_alloc * sizeof(uint2)));
         QTRY(cudaMalloc(&q->d_bun[b], (size_t)q->bun_alloc * sizeof(uint2)));
-        // segments beyond a bundle's own are read (and ignored) by the
-        // consumer's 32-wide load; keep them finite so its scan cannot wrap
+        // a consumer reads up to 32 segments past a bundle's own; keep them
+        // finite so its scan cannot wrap
         QTRY(cudaMemset(q->d_seg[b], 0, (size_t)q->seg_alloc * sizeof(uint2)));
     }
     QTRY(cudaMalloc(&q->d_ctl, sizeof(Ctl)));
@@ -899,22 +400,32 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     QTRY(cudaStreamCreateWithFlags(&q->own_stream, cudaStreamNonBlocking));
     QTRY(cudaEventCreate(&q->ev0));
     QTRY(cudaEventCreate(&q->ev1));
-    if (!q->tables.empty())
-        QTRY(cudaMemcpy(q->d_tables, q->tables.data(), q->tables.size() * sizeof(int32_t),
+    QTRY(cudaMallocHost(&q->h_tables, std::max<size_t>(T.size(), 1) * sizeof(int32_t)));
+    QTRY(cudaMallocHost(&q->h_slots, std::max<size_t>(q->slots.size(), 1) * sizeof(Slot)));
+    if (!T.empty()) std::memcpy(q->h_tables, T.data(), T.size() * sizeof(int32_t));
+    if (!q->slots.empty()) std::memcpy(q->h_slots, q->slots.data(), q->slots.size() * sizeof(Slot));
+    if (!q->slot_nnz.empty())
+        QTRY(cudaMemcpy(q->d_slot_nnz, q->slot_nnz.data(), q->slot_nnz.size() * sizeof(unsigned long long),
                         cudaMemcpyHostToDevice));
-    if (!q->slots.empty())
-        QTRY(cudaMemcpy(q->d_slots, q->slots.data(), q->slots.size() * sizeof(Slot),
-                        cudaMemcpyHostToDevice));
-    q->smem = q->slots.size() * sizeof(Slot) + q->tables.size() * sizeof(int32_t) + 16;
+    q->smem = q->slots.size() * sizeof(Slot) + T.size() * sizeof(int32_t) + 16;
     if (q->smem > 48 * 1024)
-        QTRY(cudaFuncSetAttribute(rpq_ssr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)q->smem));
+        QTRY(cudaFuncSetAttribute(ssr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q->smem));
     int per_sm = 0;
-    QTRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rpq_ssr_kernel, kThreads, q->smem));
+    QTRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ssr_kernel, kThreads, q->smem));
     if (per_sm < 1) return bail(fail(RPQ_ECUDA, "step kernel cannot be resident"));
     q->grid = g->sm_count * per_sm;
 #undef QTRY
     *out = q;
+    return RPQ_OK;
+}
+
+int rpq_query_set_options(rpq_query* q, int32_t direction, int32_t count_te, double alpha) {
+    if (!q) return fail(RPQ_EINVAL, "null query");
+    if (direction < RPQ_DIR_AUTO || direction > RPQ_DIR_PULL) return fail(RPQ_EINVAL, "bad direction");
+    if (!(alpha > 0)) return fail(RPQ_EINVAL, "alpha must be > 0");
+    q->dir_mode = direction;
+    q->count_te = count_te ? 1 : 0;
+    q->alpha = (float)alpha;
     return RPQ_OK;
 }
 
@@ -927,7 +438,9 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     Params p{};
     p.tables = q->d_tables;
     p.slots = q->d_slots;
+    p.slot_nnz = q->d_slot_nnz;
     p.visited = q->d_visited;
+    for (int f = 0; f < 3; ++f) p.fb[f] = q->d_fb[f];
     for (int b = 0; b < 2; ++b) {
         p.seg[b] = q->d_seg[b];
         p.bun[b] = q->d_bun[b];
@@ -939,7 +452,6 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     p.ovf_segcap = q->ovf_segcap;
     p.ovf_buncap = q->ovf_buncap;
     p.seg_alloc = q->seg_alloc;
-    p.bun_alloc = q->bun_alloc;
     if (!(timeout_s >= 0) || std::isinf(timeout_s) || timeout_s > 1.0e9)
         p.budget_ns = ~0ull;
     else
@@ -952,14 +464,25 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     p.ntargets = q->ntargets;
     p.nstarts = q->nstarts;
     p.nfinals = q->nfinals;
+    p.nin = q->nin;
     p.maxT = q->maxT;
     p.source = source;
     p.table_ints = (int)q->tables.size();
+    p.dir_mode = q->dir_mode;
+    p.count_te = q->count_te;
+    p.alpha = q->alpha;
     CUDA_TRY(cudaEventRecord(q->ev0, st));
+    // the automaton travels with every run (a query's input), from pinned memory
+    if (!q->tables.empty())
+        CUDA_TRY(cudaMemcpyAsync(q->d_tables, q->h_tables, q->tables.size() * sizeof(int32_t),
+                                 cudaMemcpyHostToDevice, st));
+    if (!q->slots.empty())
+        CUDA_TRY(cudaMemcpyAsync(q->d_slots, q->h_slots, q->slots.size() * sizeof(Slot),
+                                 cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemsetAsync(q->d_ctl, 0, sizeof(Ctl), st));
     void* args[] = {&p};
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)rpq_ssr_kernel, dim3(q->grid), dim3(kThreads),
-                                         args, q->smem, st));
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)ssr_kernel, dim3(q->grid), dim3(kThreads), args,
+                                         q->smem, st));
     CUDA_TRY(cudaEventRecord(q->ev1, st));
     CUDA_TRY(cudaMemcpyAsync(q->h_ctl, q->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     q->last_stream = st;
@@ -980,7 +503,9 @@ int rpq_query_wait(rpq_query* q, rpq_stats* stats) {
         stats->iterations = c.iterations;
         stats->levels = c.levels;
         stats->grid = q->grid;
-        stats->te = (int64_t)c.te;
+        stats->te = q->count_te ? (int64_t)c.te_exact : (int64_t)c.te_push;
+        stats->pull_levels = 0;
+        for (int i = 0; i < 64 && i <= c.iterations; ++i) stats->pull_levels += c.level_dir[i] == DIR_PULL;
         stats->segments = (int64_t)c.segments;
         stats->visited_pairs = (int64_t)c.pairs;
         stats->reach_count = (int64_t)c.reach_count;
@@ -988,6 +513,7 @@ int rpq_query_wait(rpq_query* q, rpq_stats* stats) {
         for (int i = 0; i < RPQ_STATS_LEVELS; ++i) {
             stats->level_new[i] = c.level_new[i];
             stats->level_edges[i] = c.level_edges[i];
+            stats->level_dir[i] = (int8_t)c.level_dir[i];
         }
     }
     if (c.status == ST_OVERFLOW) {
@@ -1022,12 +548,21 @@ int rpq_query_copy_reach(rpq_query* q, uint8_t* host_reach) {
 int rpq_query_copy_visited(rpq_query* q, uint32_t* host_words, int64_t nwords) {
     if (!q || !host_words) return fail(RPQ_EINVAL, "null argument");
     const int64_t words = ((int64_t)q->g->nv + 31) / 32;
+    if (q->g->nv == 0) return RPQ_OK;
     if (nwords < words * q->nstates) return fail(RPQ_EINVAL, "output buffer too small");
     if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
     cudaStream_t st = q->last_stream ? q->last_stream : q->own_stream;
     CUDA_TRY(cudaStreamSynchronize(st));
     CUDA_TRY(cudaMemcpy2D(host_words, (size_t)words * 4, q->d_visited, (size_t)q->W * 4,
                           (size_t)words * 4, (size_t)q->nstates, cudaMemcpyDeviceToHost));
+    return RPQ_OK;
+}
+
+int rpq_query_io_bytes(const rpq_query* q, int64_t* h2d_per_run, int64_t* d2h_per_run) {
+    if (!q) return fail(RPQ_EINVAL, "null query");
+    if (h2d_per_run)
+        *h2d_per_run = (int64_t)(q->tables.size() * sizeof(int32_t) + q->slots.size() * sizeof(Slot));
+    if (d2h_per_run) *d2h_per_run = (int64_t)sizeof(Ctl);
     return RPQ_OK;
 }
 

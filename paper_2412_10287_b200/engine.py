@@ -28,6 +28,7 @@ from .automaton import reverse, transition_table
 from .graph import device_graph
 
 ALGORITHMS = ("masked", "no_mask", "hybrid", "plan")
+DIRECTIONS = {"auto": _lib.DIR_AUTO, "push": _lib.DIR_PUSH, "pull": _lib.DIR_PULL}
 
 
 class QueryTimeout(RuntimeError):
@@ -53,8 +54,15 @@ class EngineOptions:
     timeout: float = 60.0
     debug_checks: bool = False
     device: int = 0
+    direction: str = "auto"  # per-level push/pull policy of the device BFS
+    alpha: float = 15.0  # Beamer's switch constant (pull when m_f * alpha > m_u)
+    count_te: bool = False  # exact product-edge count in EvalResult.stats
 
     def validate(self) -> None:
+        if self.direction not in DIRECTIONS:
+            raise ValueError(f"unknown direction {self.direction!r}")
+        if not self.alpha > 0:
+            raise ValueError("alpha must be > 0")
         if self.algorithm not in ALGORITHMS:
             raise ValueError(f"unknown algorithm {self.algorithm!r}")
         if self.product_order not in ("left", "right"):
@@ -143,6 +151,9 @@ def _run(g, n, source, opts, tag, *, want_stats=False):
     lib = _lib.engine()
     q = dg.acquire_query(table)
     try:
+        raise_for_status(lib.rpq_query_set_options(
+            q, DIRECTIONS[opts.direction], int(opts.count_te or opts.debug_checks), opts.alpha),
+            "rpq_query_set_options")
         # _Clock.check(0) at the top of the first iteration (engine.py:87-89)
         remaining = opts.timeout - (time.monotonic() - t0)
         if remaining < 0 or opts.timeout == 0:
@@ -165,7 +176,7 @@ def _run(g, n, source, opts, tag, *, want_stats=False):
     finally:
         dg.release_query(table, q)
     return EvalResult(reach, iterations, time.monotonic() - t0, tag,
-                      stats.to_dict() if want_stats or opts.debug_checks else None)
+                      stats.to_dict() if want_stats or opts.debug_checks or opts.count_te else None)
 
 
 def _debug_invariants(lib, q, table, nv, stats, iterations):
@@ -248,3 +259,69 @@ def step_update(m, p, g, n, opts):
     if m.shape != p.shape:
         raise ValueError(f"step_update: frontier {m.shape} vs visited {p.shape}")
     raise NotImplementedError("step_update has no device implementation yet")
+
+
+class PreparedQuery:
+    """An automaton bound to a device-resident graph, for callers that
+    evaluate it many times (batches of sources, the bench).  ``launch`` only
+    enqueues work on ``stream`` (a raw cudaStream_t handle, e.g.
+    ``torch.cuda.current_stream().cuda_stream``); ``wait`` returns the run's
+    statistics; ``reach`` copies the answer to the host."""
+
+    def __init__(self, g, n, device=0):
+        self.g = g
+        self.dg = device_graph(g, device)
+        self.table = transition_table(n, g.num_labels)
+        self.dg.ensure_labels(self.table.labels)
+        self.q = self.dg.acquire_query(self.table)
+        self.nv = int(g.num_vertices)
+
+    def set_options(self, direction="auto", count_te=False, alpha=15.0):
+        raise_for_status(_lib.engine().rpq_query_set_options(
+            self.q, DIRECTIONS[direction], int(count_te), float(alpha)), "rpq_query_set_options")
+
+    def launch(self, source, timeout=-1.0, stream=None):
+        _check_vertex(self.g, source)
+        raise_for_status(_lib.engine().rpq_query_run(self.q, int(source), float(timeout), stream),
+                         "rpq_query_run")
+
+    def wait(self):
+        stats = _lib.RpqStats()
+        rc = _lib.engine().rpq_query_wait(self.q, ctypes.byref(stats))
+        if rc == _lib.RPQ_ETIMEOUT:
+            raise QueryTimeout(stats.device_ms / 1e3, stats.iterations)
+        raise_for_status(rc, "rpq_query_wait")
+        return stats
+
+    def reach(self, out=None):
+        out = np.empty(self.nv, dtype=np.uint8) if out is None else out
+        if self.nv:
+            raise_for_status(_lib.engine().rpq_query_copy_reach(self.q, _lib.ptr(out, ctypes.c_uint8)),
+                             "rpq_query_copy_reach")
+        return out
+
+    def visited_counts(self):
+        """Pairs of P per automaton state (popcount of each visited row)."""
+        words = (self.nv + 31) // 32
+        buf = np.zeros(max(words * self.table.nstates, 1), dtype=np.uint32)
+        raise_for_status(_lib.engine().rpq_query_copy_visited(
+            self.q, _lib.ptr(buf, ctypes.c_uint32), buf.size), "rpq_query_copy_visited")
+        rows = buf[: words * self.table.nstates].reshape(self.table.nstates, words)
+        return np.unpackbits(rows.view(np.uint8), axis=1).sum(axis=1).astype(np.int64)
+
+    def io_bytes(self):
+        h2d, d2h = ctypes.c_int64(), ctypes.c_int64()
+        raise_for_status(_lib.engine().rpq_query_io_bytes(self.q, ctypes.byref(h2d), ctypes.byref(d2h)),
+                         "rpq_query_io_bytes")
+        return int(h2d.value), int(d2h.value)
+
+    def close(self):
+        if self.q is not None:
+            self.dg.release_query(self.table, self.q)
+            self.q = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

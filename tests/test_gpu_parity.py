@@ -22,9 +22,11 @@ def instances(reference_instances):
     return [(rec, host_graph(rec["graph"]), automaton(rec["nfa"])) for rec in reference_instances]
 
 
-@pytest.mark.parametrize("algorithm", ["hybrid", "masked", "no_mask"])
-def test_reference_instances(instances, algorithm):
-    opts = P.EngineOptions(algorithm=algorithm, timeout=math.inf)
+@pytest.mark.parametrize("algorithm,direction", [
+    ("hybrid", "auto"), ("masked", "auto"), ("no_mask", "auto"),
+    ("hybrid", "push"), ("hybrid", "pull"), ("masked", "pull")])
+def test_reference_instances(instances, algorithm, direction):
+    opts = P.EngineOptions(algorithm=algorithm, timeout=math.inf, direction=direction)
     for rec, g, n in instances:
         res = P.eval_ssr(g, n, rec["source"], opts)
         assert np.array_equal(res.reach, expected_reach(rec, g.num_vertices)), rec["tag"]
@@ -132,23 +134,27 @@ def _config_case(name):
     return gold, sg
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg5"])
 def test_config_goldens(name):
     gold, sg = _config_case(name)
     g = sg.labeled_graph()
     for rec in gold["records"]:
         n = automaton(rec["nfa"])
-        res = P.eval_ssr(g, n, rec["source"], P.EngineOptions(timeout=math.inf))
         want = unpack_bits(rec["reach_bits"], sg.nv)
         assert int(want.sum()) == rec["reach_count"]
-        assert np.array_equal(res.reach, want)
-        assert res.iterations == rec["iterations"]["hybrid"]
+        for direction in ("auto", "push", "pull"):
+            res = P.eval_ssr(g, n, rec["source"],
+                             P.EngineOptions(timeout=math.inf, direction=direction))
+            assert np.array_equal(res.reach, want), direction
+            assert res.iterations == rec["iterations"]["hybrid"], direction
 
 
+@pytest.mark.parametrize("direction", ["auto", "push", "pull"])
 @pytest.mark.parametrize("scale,seed,query", [
     (14, 21, "^a (b|c)* d"), (15, 22, "a ^b* c"), (16, 23, "a b*"),
-    (13, 24, "(a|^b)* c+"), (12, 25, "(a ^a)* (b | c ^d)*")])
-def test_rmat_vs_oracle(scale, seed, query):
+    (13, 24, "(a|^b)* c+"), (12, 25, "(a ^a)* (b | c ^d)*"), (14, 26, "(a|b|c|d)*"),
+    (13, 27, "a ^b c*")])
+def test_rmat_vs_oracle(scale, seed, query, direction):
     import json
     import os
 
@@ -165,8 +171,22 @@ def test_rmat_vs_oracle(scale, seed, query):
     sources = [int(np.argmax(deg)), 0, sg.nv - 1, int(np.flatnonzero(deg)[len(np.flatnonzero(deg)) // 2])]
     for s in sources:
         want, st = oracle_bfs(og, oq, s)
-        got = P.eval_ssr(g, n, s, P.EngineOptions(timeout=math.inf, debug_checks=True))
+        got = P.eval_ssr(g, n, s, P.EngineOptions(timeout=math.inf, debug_checks=True,
+                                                  direction=direction))
         assert np.array_equal(got.reach, want), (query, s)
         assert got.iterations == st["iterations"]
         assert got.stats["te"] == st["te"]
         assert got.stats["visited_pairs"] == st["pairs"]
+
+
+def test_cfg3_golden():
+    """R-MAT scale 24 (263M edges) against the reference's own answer."""
+    gold, sg = _config_case("cfg3")
+    g = sg.labeled_graph()
+    for rec in gold["records"]:
+        n = automaton(rec["nfa"])
+        want = unpack_bits(rec["reach_bits"], sg.nv)
+        for direction in ("auto", "push", "pull"):
+            res = P.eval_ssr(g, n, rec["source"], P.EngineOptions(timeout=math.inf, direction=direction))
+            assert np.array_equal(res.reach, want), direction
+            assert res.iterations == rec["iterations"]["hybrid"], direction
