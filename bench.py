@@ -40,8 +40,15 @@ METRIC = "2-RPQ edges traversed/sec (GTEPS)"
 UNIT = "GTEPS"
 CONFIG = "cfg2"
 QUERY = "a ^b* c"
-WORKLOAD = ("cfg2: R-MAT scale 20 (1,048,576 V), edge factor 16, abc=(0.57,0.19,0.19), "
-            "16 Zipf(1.0) labels, query a ^b* c (3-state min DFA), source = max out-degree")
+WORKLOADS = {
+    "cfg1": ("a b*", "cfg1: Erdos-Renyi 10,000 V / 100,000 E, 4 uniform labels, query a b* "
+                     "(2-state min DFA), source 0"),
+    "cfg2": ("a ^b* c", "cfg2: R-MAT scale 20 (1,048,576 V), edge factor 16, abc=(0.57,0.19,0.19), "
+                        "16 Zipf(1.0) labels, query a ^b* c (3-state min DFA), source = max out-degree"),
+    "cfg3": ("^a (b|c)* d", "cfg3: R-MAT scale 24 (16,777,216 V), edge factor 16, 64 Zipf(1.0) labels, "
+                            "query ^a (b|c)* d (3-state min DFA), source = max out-degree"),
+}
+WORKLOAD = WORKLOADS[CONFIG][1]
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -55,6 +62,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--direction", choices=["auto", "push", "pull"], default="auto")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between steps (diagnostic)")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no e2e leg, no CPU baseline, no clocks")
     return ap.parse_args()
@@ -188,6 +196,8 @@ def run_reference(args, rank, world):
     from oracle import OracleGraph, OracleQuery, oracle_bfs, oracle_port
     from paper_2412_10287_b200 import datagen
 
+    global QUERY, WORKLOAD
+    QUERY, WORKLOAD = WORKLOADS[args.config]
     sg = datagen.generate(args.config)
     nj = load_automaton(args.config, QUERY)
     source = ranked_sources(sg, 1)[0]
@@ -233,6 +243,8 @@ def run_engine(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    global QUERY, WORKLOAD
+    QUERY, WORKLOAD = WORKLOADS[args.config]
     sg = datagen.generate(args.config)
     g = sg.labeled_graph()
     nj = load_automaton(args.config, QUERY)
@@ -276,7 +288,8 @@ def run_engine(args, rank, world, local_rank):
           for _ in range(args.steps)]
     launches = 0
     for k in range(args.steps):
-        flush.fill_(k & 0xFF)  # > L2: evicts the graph between steps (outside the events)
+        if not args.no_flush:
+            flush.fill_(k & 0xFF)  # > L2: evicts the graph between steps (outside the events)
         ev[k][0].record(stream)
         pq.launch(source, -1.0, handle)
         launches += 1
@@ -340,6 +353,9 @@ def run_engine(args, rank, world, local_rank):
             "level_new": list(st0.level_new[: iters + 1]),
             "level_edges": list(st0.level_edges[: iters + 1]),
             "level_dir": ["pull" if d else "push" for d in st0.level_dir[: iters]],
+            "level_end_us": [t / 1e3 for t in st0.level_ns[: iters + 1]],
+            "level_work_us": [t / 1e3 for t in st0.work_ns[: iters]],
+            "level_bar_us": [t / 1e3 for t in st0.bar_ns[: iters]],
             "direction_policy": args.direction,
         },
         "roofline": {

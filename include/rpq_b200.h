@@ -80,6 +80,9 @@ typedef struct rpq_stats {
     int32_t pull_levels;     /* levels run in the pull direction */
     int64_t level_new[RPQ_STATS_LEVELS];    /* |F_L|: new (state, vertex) pairs per level */
     int64_t level_edges[RPQ_STATS_LEVELS];  /* push-model edges expanded from F_L (-1: pulled) */
+    int64_t level_ns[RPQ_STATS_LEVELS];     /* kernel start -> level L's decision taken (CTA 0) */
+    int64_t work_ns[RPQ_STATS_LEVELS];      /* kernel start -> last CTA done with level L's work */
+    int64_t bar_ns[RPQ_STATS_LEVELS];       /* kernel start -> CTA 0 past the barrier after level L */
     int8_t level_dir[RPQ_STATS_LEVELS];     /* 0 push, 1 pull */
 } rpq_stats;
 
@@ -119,7 +122,7 @@ RPQ_API int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans,
                      const int32_t* t_dst, int32_t nstarts, const int32_t* starts,
                      int32_t nfinals, const int32_t* finals, rpq_query** out);
 /* Direction policy (RPQ_DIR_*), exact-TE accounting on/off, Beamer's alpha
- * (default: auto, off, 15).  Results do not depend on these. */
+ * (default: auto, off, 4).  Results do not depend on these. */
 RPQ_API int rpq_query_set_options(rpq_query* q, int32_t direction, int32_t count_te, double alpha);
 /* Enqueue one evaluation from `source` on `stream` (a cudaStream_t, or NULL for
  * the query's own stream).  timeout_s < 0 or inf: no deadline.  The deadline is

@@ -52,6 +52,9 @@ class RpqStats(ctypes.Structure):
         ("pull_levels", c_i32),
         ("level_new", c_i64 * STATS_LEVELS),
         ("level_edges", c_i64 * STATS_LEVELS),
+        ("level_ns", c_i64 * STATS_LEVELS),
+        ("work_ns", c_i64 * STATS_LEVELS),
+        ("bar_ns", c_i64 * STATS_LEVELS),
         ("level_dir", ctypes.c_int8 * STATS_LEVELS),
     ]
 
@@ -69,6 +72,9 @@ class RpqStats(ctypes.Structure):
             "device_ms": self.device_ms,
             "pull_levels": self.pull_levels,
             "level_dir": list(self.level_dir[:nlev]),
+            "level_us": [t / 1e3 for t in self.level_ns[:nlev]],
+            "work_us": [t / 1e3 for t in self.work_ns[:nlev]],
+            "bar_us": [t / 1e3 for t in self.bar_ns[:nlev]],
             "level_new": list(self.level_new[:nlev]),
             "level_edges": list(self.level_edges[:nlev]),
         }

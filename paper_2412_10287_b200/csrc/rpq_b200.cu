@@ -89,7 +89,7 @@ struct rpq_query {
     long long W = 0;
     int dir_mode = 0;
     int count_te = 0;
-    float alpha = 15.0f;
+    float alpha = 4.0f;
     cudaStream_t own_stream = nullptr;
     cudaStream_t last_stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -413,7 +413,7 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     int per_sm = 0;
     QTRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ssr_kernel, kThreads, q->smem));
     if (per_sm < 1) return bail(fail(RPQ_ECUDA, "step kernel cannot be resident"));
-    q->grid = g->sm_count * per_sm;
+    q->grid = std::min(g->sm_count * per_sm, kShards);  // one queue shard per CTA
 #undef QTRY
     *out = q;
     return RPQ_OK;
@@ -504,16 +504,19 @@ int rpq_query_wait(rpq_query* q, rpq_stats* stats) {
         stats->levels = c.levels;
         stats->grid = q->grid;
         stats->te = q->count_te ? (int64_t)c.te_exact : (int64_t)c.te_push;
-        stats->pull_levels = 0;
-        for (int i = 0; i < 64 && i <= c.iterations; ++i) stats->pull_levels += c.level_dir[i] == DIR_PULL;
         stats->segments = (int64_t)c.segments;
         stats->visited_pairs = (int64_t)c.pairs;
         stats->reach_count = (int64_t)c.reach_count;
         stats->device_ms = ms;
+        stats->pull_levels = c.pull_levels;
         for (int i = 0; i < RPQ_STATS_LEVELS; ++i) {
-            stats->level_new[i] = c.level_new[i];
-            stats->level_edges[i] = c.level_edges[i];
-            stats->level_dir[i] = (int8_t)c.level_dir[i];
+            const bool ran_level = i <= c.iterations;
+            stats->level_new[i] = ran_level ? c.level_new[i] : 0;
+            stats->level_edges[i] = ran_level ? c.level_edges[i] : 0;
+            stats->level_ns[i] = ran_level ? (int64_t)c.level_ns[i] : 0;
+            stats->work_ns[i] = ran_level ? (int64_t)c.work_ns[i] : 0;
+            stats->bar_ns[i] = ran_level ? (int64_t)c.bar_ns[i] : 0;
+            stats->level_dir[i] = ran_level && i < c.iterations ? (int8_t)c.level_dir[i] : 0;
         }
     }
     if (c.status == ST_OVERFLOW) {

@@ -26,17 +26,27 @@
 
 namespace rpqk {
 
-constexpr int kThreads = 256;        // 8 warps per CTA
-constexpr int kMinBlocks = 3;        // CTAs per SM the register budget targets
-constexpr int kBundle = 32;          // edges per bundle (<= 32 segments)
-constexpr int kShards = 64;          // queue shards (+1 overflow shard), by CTA
+constexpr int kThreads = 768;        // 24 warps per CTA, one CTA per SM
+constexpr int kMinBlocks = 1;
+constexpr int kWarps = kThreads / 32;
+constexpr int kEdgesPerLane = 4;     // push: edges each lane expands per bundle
+constexpr int kBundle = 32 * kEdgesPerLane;  // edges per bundle; an emission pass has
+                                             // <= 32 segments, so a bundle spans <= 32
+constexpr int kPullVerts = 4;        // pull: vertices (words of 32) per lane per task
+constexpr int kShards = 160;         // queue shards, one per CTA (+1 overflow shard)
 constexpr int kMaxStates = 256;
 constexpr int kMaxGroups = 256;      // group id is 8 bits in a segment
 constexpr int kMaxSlots = 128;
 constexpr uint32_t kSegLenMax = (1u << 24) - 1;
-constexpr uint32_t kHoleBundle = 0xFFFFFFFFu;
+constexpr int kFastGroups = 4;       // emission: groups per state handled in one pass
+// bundle = uint2 {x, y}; y bit 31 = inline, bits 0..6 = edges - 1,
+//   inline  : x = column offset of the first edge, y bits 7..14 = group
+//   indirect: x = index of the first segment, y bits 7..30 = offset into it
+// a hole (bundle slot left empty by a spill) has y = 0xFFFFFFFF
+constexpr uint32_t kHoleY = 0xFFFFFFFFu;
+constexpr uint32_t kInline = 0x80000000u;
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int kPullInline = 4;       // in-edges each lane tests before warp help
+constexpr int kPullInline = 2;       // in-edges each lane tests before warp help
 
 constexpr int ST_OVERFLOW = 100;
 constexpr int ST_DEADLOCK = 101;
@@ -49,30 +59,44 @@ struct Slot {
     const int32_t* col;
 };
 
+// Counters are never reset while anyone may still read them: queue counters
+// rotate over 3 sets by barrier epoch e (produced in epoch e-1, read after
+// barrier e, reset in epoch e+1), frontier statistics over 3 sets by level.
+// Every CTA reads the same values after a barrier and so takes the same
+// decision: no serial section, no broadcast.
+struct QCnt {
+    unsigned long long shard[kShards + 1];  // (segments << 32) | bundles
+    unsigned long long edges;               // push-model edges emitted
+    unsigned int overflow;
+    unsigned int expire;                    // 1 + level whose deadline check failed
+};
+
+struct FCnt {
+    unsigned long long nnew;                // |F_L|
+    unsigned int state[kMaxStates];         // |F_L| per state
+};
+
 struct Ctl {
-    unsigned int bar_count;
-    unsigned int bar_gen;
+    unsigned int bar;        // monotonic barrier arrivals
+    int abort;
+    unsigned long long t0;
+    QCnt qc[3];
+    FCnt fc[3];
+    // results, written by CTA 0 only
     int status;
-    int done;
     int iterations;
     int levels;
-    int overflow;
-    int dir;   // direction of the level about to run
-    int plan;  // 1: the push level about to run must first emit its queue from F
-    int pad;
-    unsigned long long t0;
-    unsigned long long shard_cnt[2][kShards + 1];  // (segments << 32) | bundles
-    unsigned long long new_cnt[2];
-    unsigned long long edge_cnt[2];
-    unsigned int state_front[2][kMaxStates];       // |F_L| per state, by parity of L
-    unsigned long long state_vis[kMaxStates];      // |P| per state
-    unsigned long long te_push;                    // edges expanded by push levels
-    unsigned long long te_exact;                   // push-model TE over P (flag)
+    int pull_levels;
+    unsigned long long te_push;
+    unsigned long long te_exact;
     unsigned long long segments;
     unsigned long long pairs;
     unsigned long long reach_count;
     long long level_new[64];
     long long level_edges[64];
+    unsigned long long level_ns[64];
+    unsigned long long work_ns[64];  // latest CTA finishing level L's work (from t0)
+    unsigned long long bar_ns[64];   // CTA 0 leaving the barrier after level L
     int level_dir[64];
 };
 
@@ -131,9 +155,29 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
     return m;
 }
+// control-plane loads after a fence: L2 (coherence point), weak, pipelined
 template <typename T>
-__device__ __forceinline__ T ld_volatile(const T* p) {
-    return *reinterpret_cast<const volatile T*>(p);
+__device__ __forceinline__ T ldcg(const T* p) {
+    return __ldcg(p);
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+    return v;
+}
+__device__ __forceinline__ double warp_sum_f64(double v) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+    return v;
+}
+__device__ __forceinline__ unsigned long long warp_incl_scan_u64(unsigned long long v, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        unsigned long long o = __shfl_up_sync(FULL, v, d);
+        if (lane >= d) v += o;
+    }
+    return v;
 }
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
@@ -157,68 +201,59 @@ __device__ __forceinline__ int warp_upper_lane(uint32_t key, uint32_t x) {
     return j;
 }
 
-// Control words every thread needs after a barrier, broadcast through smem.
-struct CtlView {
+// What every thread of a CTA needs to know after a barrier (warp 0 derives it
+// from the global counters; all CTAs derive the same values).
+struct View {
     int done;
-    int dir;
-    int plan;
+    int dir;        // direction of the level about to run
+    int plan;       // push level whose queue must first be emitted from F_L
+    int status;
+    int iterations;
 };
 
-// Grid barrier for a cooperative launch.  The last CTA to arrive runs
-// `serial` (one thread) before releasing everyone, so per-level bookkeeping
-// is ordered after all CTAs' work and before any CTA's next level.  Waiters
-// spin on a relaxed load (no per-iteration L1 invalidation) and fence once.
-template <class F>
-__device__ __forceinline__ void grid_sync(Ctl* ctl, CtlView* view, F serial) {
+// Grid barrier for a cooperative launch over a monotonic arrival counter:
+// barrier number e completes when e * gridDim.x arrivals are counted.
+// Waiters spin on a relaxed load and fence once afterwards (acquire side; the
+// fence also invalidates this SM's L1: CCTL.IVALL).
+__device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned epoch) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned nblocks = gridDim.x;
-        unsigned gen = ld_relaxed_u32(&ctl->bar_gen);
         __threadfence();
-        unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
-        if (arrived == nblocks - 1) {
-            __threadfence();
-            serial();
-            ctl->bar_count = 0;
-            __threadfence();
-            st_release_u32(&ctl->bar_gen, gen + 1);
-        } else {
-            unsigned long long ts = 0;
-            unsigned spins = 0;
-            while (ld_relaxed_u32(&ctl->bar_gen) == gen) {
-                __nanosleep(20);
-                if ((++spins & 4095u) == 0) {
-                    unsigned long long now = globaltimer();
-                    if (ts == 0) {
-                        ts = now;
-                    } else if (now - ts > 20000000000ull) {  // 20 s: cannot happen co-resident
-                        atomicExch(&ctl->status, ST_DEADLOCK);
-                        atomicExch(&ctl->done, 1);
-                        break;
-                    }
+        atomicAdd(&ctl->bar, 1u);
+        const unsigned target = epoch * gridDim.x;
+        unsigned long long ts = 0;
+        unsigned spins = 0;
+        while (ld_relaxed_u32(&ctl->bar) < target) {
+            __nanosleep(16);
+            if ((++spins & 4095u) == 0) {
+                const unsigned long long now = globaltimer();
+                if (ts == 0) {
+                    ts = now;
+                } else if (now - ts > 20000000000ull) {  // 20 s: cannot happen co-resident
+                    atomicExch(&ctl->abort, 1);
+                    break;
                 }
             }
         }
-        __threadfence();  // acquire side; also invalidates this SM's L1 (CCTL.IVALL)
-        view->done = ld_volatile(&ctl->done);
-        view->dir = ld_volatile(&ctl->dir);
-        view->plan = ld_volatile(&ctl->plan);
+        __threadfence();
     }
     __syncthreads();
 }
 
-// Shard-local reservation of `nseg` segments and `nb` bundles in queue buffer
-// `b` (one lane).  A reservation that does not fit its CTA's shard spills to
-// the overflow shard; the part of its bundle range inside the regular shard,
-// [*hole_lo, *hole_hi), must then be filled with kHoleBundle by the caller.
-__device__ __forceinline__ bool reserve(const Params& p, int b, uint32_t nseg, uint32_t nb,
-                                        unsigned long long* seg_idx, unsigned long long* bun_idx,
-                                        unsigned long long* hole_lo, unsigned long long* hole_hi) {
-    Ctl* ctl = p.ctl;
-    const int shard = blockIdx.x % kShards;
+// Reservation of `nseg` segments and `nb` bundles (one lane).  Each CTA owns
+// queue shard blockIdx.x and reserves in it with a shared-memory counter
+// (published to the global shard counter once per epoch by flush_counts);
+// a reservation that does not fit spills to the overflow shard through a
+// global atomic, and the part of its bundle range inside the CTA's shard,
+// [*hole_lo, *hole_hi), must then be filled with holes (y = kHoleY).
+__device__ __forceinline__ bool reserve(const Params& p, unsigned long long* s_resv, QCnt* qc,
+                                        uint32_t nseg, uint32_t nb, unsigned long long* seg_idx,
+                                        unsigned long long* bun_idx, unsigned long long* hole_lo,
+                                        unsigned long long* hole_hi) {
+    const int shard = blockIdx.x;
     const unsigned long long inc = ((unsigned long long)nseg << 32) | nb;
-    unsigned long long old = atomicAdd(&ctl->shard_cnt[b][shard], inc);
-    unsigned long long s_loc = old >> 32, b_loc = old & 0xFFFFFFFFull;
+    const unsigned long long old = atomicAdd(s_resv, inc);
+    const unsigned long long s_loc = old >> 32, b_loc = old & 0xFFFFFFFFull;
     *hole_lo = *hole_hi = 0;
     if (s_loc + nseg <= p.shard_segcap && b_loc + nb <= p.shard_buncap) {
         *seg_idx = (unsigned long long)shard * p.shard_segcap + s_loc;
@@ -230,20 +265,27 @@ __device__ __forceinline__ bool reserve(const Params& p, int b, uint32_t nseg, u
         *hole_hi = (unsigned long long)shard * p.shard_buncap +
                    (b_loc + nb < p.shard_buncap ? b_loc + nb : p.shard_buncap);
     }
-    old = atomicAdd(&ctl->shard_cnt[b][kShards], inc);
-    s_loc = old >> 32;
-    b_loc = old & 0xFFFFFFFFull;
-    if (s_loc + nseg <= p.ovf_segcap && b_loc + nb <= p.ovf_buncap) {
-        *seg_idx = (unsigned long long)kShards * p.shard_segcap + s_loc;
-        *bun_idx = (unsigned long long)kShards * p.shard_buncap + b_loc;
+    const unsigned long long o2 = atomicAdd(&qc->shard[kShards], inc);
+    const unsigned long long s2 = o2 >> 32, b2 = o2 & 0xFFFFFFFFull;
+    if (s2 + nseg <= p.ovf_segcap && b2 + nb <= p.ovf_buncap) {
+        *seg_idx = (unsigned long long)kShards * p.shard_segcap + s2;
+        *bun_idx = (unsigned long long)kShards * p.shard_buncap + b2;
         return true;
     }
     return false;
 }
 
+// Where an epoch's emission goes.
+struct Out {
+    QCnt* qc;
+    uint2* seg;
+    uint2* bun;
+    unsigned long long* s_resv;  // this CTA's shard fill: (segments << 32) | bundles
+};
+
 // Warp-cooperative emission of the row segments of (state q, vertex w) pairs
-// (one candidate per lane) into queue buffer `b`.  Returns the edges emitted.
-__device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, int b, bool valid,
+// (one candidate per lane).  Returns the edges emitted.
+__device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, const Out& o, bool valid,
                                                int q, int w, int lane) {
     const unsigned vmask = __ballot_sync(FULL, valid);
     if (vmask == 0) return 0;
@@ -251,8 +293,99 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, i
     int maxng = ng;
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) maxng = max(maxng, __shfl_xor_sync(FULL, maxng, d));
-    uint2* seg = p.seg[b];
-    uint2* bun = p.bun[b];
+    if (maxng <= kFastGroups) {
+        // all groups' row pointers in flight together, one reservation
+        uint32_t lo[kFastGroups], deg[kFastGroups];
+        int g[kFastGroups];
+#pragma unroll
+        for (int k = 0; k < kFastGroups; ++k) {
+            lo[k] = 0;
+            deg[k] = 0;
+            g[k] = 0;
+            if (k < ng) {
+                g[k] = S.gbeg[q] + k;
+                const Slot sl = S.slots[S.gslot[g[k]]];
+                lo[k] = __ldg(sl.rowptr + w);
+                deg[k] = __ldg(sl.rowptr + w + 1);
+            }
+        }
+        bool huge = false;
+#pragma unroll
+        for (int k = 0; k < kFastGroups; ++k) {
+            deg[k] -= lo[k];
+            huge |= deg[k] > kSegLenMax;
+        }
+        if (!__any_sync(FULL, huge)) {
+            uint32_t excl[kFastGroups], T[kFastGroups], nb[kFastGroups], nseg[kFastGroups];
+            int rank[kFastGroups];
+            uint32_t NS = 0, NB = 0, TT = 0;
+#pragma unroll
+            for (int k = 0; k < kFastGroups; ++k) {
+                if (k < maxng) {
+                    const unsigned m = __ballot_sync(FULL, deg[k] > 0);
+                    rank[k] = __popc(m & lanemask_lt());
+                    nseg[k] = (uint32_t)__popc(m);
+                    const uint32_t incl = warp_incl_scan(deg[k], lane);
+                    excl[k] = incl - deg[k];
+                    T[k] = __shfl_sync(FULL, incl, 31);
+                    nb[k] = (T[k] + kBundle - 1) / kBundle;
+                    NS += nseg[k];
+                    NB += nb[k];
+                    TT += T[k];
+                } else {
+                    rank[k] = 0;
+                    nseg[k] = nb[k] = T[k] = excl[k] = 0;
+                }
+            }
+            if (NB == 0) return 0;
+            unsigned long long sbase = 0, bbase = 0, hlo = 0, hhi = 0;
+            int ok = 1;
+            if (lane == 0) ok = reserve(p, o.s_resv, o.qc, NS, NB, &sbase, &bbase, &hlo, &hhi) ? 1 : 0;
+            ok = __shfl_sync(FULL, ok, 0);
+            hlo = __shfl_sync(FULL, hlo, 0);
+            hhi = __shfl_sync(FULL, hhi, 0);
+            for (unsigned long long h = hlo + lane; h < hhi; h += 32) o.bun[h] = make_uint2(0u, kHoleY);
+            if (!ok) {
+                if (lane == 0) atomicExch(&o.qc->overflow, 1u);
+                return 0;
+            }
+            sbase = __shfl_sync(FULL, sbase, 0);
+            bbase = __shfl_sync(FULL, bbase, 0);
+#pragma unroll
+            for (int k = 0; k < kFastGroups; ++k) {
+                if (k >= maxng) break;
+                if (nb[k] == 0) continue;
+                bool need_seg = false;
+                for (uint32_t kb0 = 0; kb0 < nb[k]; kb0 += 32) {
+                    const uint32_t kb = kb0 + lane;
+                    const uint32_t pos = kb * kBundle;
+                    const uint32_t cnt = kb < nb[k] ? min((uint32_t)kBundle, T[k] - pos) : 1u;
+                    const uint32_t first = min(pos, T[k] - 1);
+                    const int j = warp_upper_lane(excl[k], first);
+                    const int jl = warp_upper_lane(excl[k], min(pos + cnt - 1, T[k] - 1));
+                    const uint32_t exj = __shfl_sync(FULL, excl[k], j);
+                    const int rj = __shfl_sync(FULL, rank[k], j);
+                    const uint32_t loj = __shfl_sync(FULL, lo[k], j);
+                    const int gj = __shfl_sync(FULL, g[k], j);
+                    if (kb < nb[k]) {
+                        uint2 bd;
+                        if (j == jl) {  // within one row: carry the row offset inline
+                            bd = make_uint2(loj + (pos - exj), kInline | ((uint32_t)gj << 7) | (cnt - 1));
+                        } else {
+                            bd = make_uint2((uint32_t)(sbase + rj), ((pos - exj) << 7) | (cnt - 1));
+                            need_seg = true;
+                        }
+                        o.bun[bbase + kb] = bd;
+                    }
+                }
+                if (__any_sync(FULL, need_seg) && deg[k] > 0)
+                    o.seg[sbase + rank[k]] = make_uint2(lo[k], (deg[k] << 8) | (uint32_t)g[k]);
+                sbase += nseg[k];
+                bbase += nb[k];
+            }
+            return TT;
+        }
+    }
     uint32_t emitted = 0;
     for (int k = 0; k < maxng; ++k) {
         uint32_t lo = 0, deg = 0;
@@ -276,18 +409,18 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, i
             const uint32_t nb = (T + kBundle - 1) / kBundle;
             unsigned long long sbase = 0, bbase = 0, hlo = 0, hhi = 0;
             int ok = 1;
-            if (lane == 0) ok = reserve(p, b, nseg, nb, &sbase, &bbase, &hlo, &hhi) ? 1 : 0;
+            if (lane == 0) ok = reserve(p, o.s_resv, o.qc, nseg, nb, &sbase, &bbase, &hlo, &hhi) ? 1 : 0;
             ok = __shfl_sync(FULL, ok, 0);
             hlo = __shfl_sync(FULL, hlo, 0);
             hhi = __shfl_sync(FULL, hhi, 0);
-            for (unsigned long long h = hlo + lane; h < hhi; h += 32) bun[h] = make_uint2(kHoleBundle, 0);
+            for (unsigned long long h = hlo + lane; h < hhi; h += 32) o.bun[h] = make_uint2(0u, kHoleY);
             if (!ok) {
-                if (lane == 0) atomicExch(&p.ctl->overflow, 1);
+                if (lane == 0) atomicExch(&o.qc->overflow, 1u);
                 return emitted;
             }
             sbase = __shfl_sync(FULL, sbase, 0);
             bbase = __shfl_sync(FULL, bbase, 0);
-            if (hs) seg[sbase + rank] = make_uint2(lo, (take << 8) | (uint32_t)g);
+            if (hs) o.seg[sbase + rank] = make_uint2(lo, (take << 8) | (uint32_t)g);
             for (uint32_t kb0 = 0; kb0 < nb; kb0 += 32) {
                 const uint32_t kb = kb0 + lane;
                 const uint32_t pos = kb * kBundle;
@@ -296,7 +429,7 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, i
                 const int rj = __shfl_sync(FULL, rank, j);
                 if (kb < nb) {
                     const uint32_t cnt = min((uint32_t)kBundle, T - pos);
-                    bun[bbase + kb] = make_uint2((uint32_t)(sbase + rj), (pos - exj) | ((cnt - 1) << 24));
+                    o.bun[bbase + kb] = make_uint2((uint32_t)(sbase + rj), ((pos - exj) << 7) | (cnt - 1));
                 }
             }
             emitted += T;
@@ -307,182 +440,305 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, i
     return emitted;
 }
 
-// Per-CTA flush of a level's counters (one atomic per CTA and counter).
-__device__ __forceinline__ void flush_counts(Ctl* ctl, int b, unsigned long long nnew,
+// Per-warp staging of discovered pairs so that emission passes are full
+// (<= 63 staged; a pass emits 32).
+struct Stage {
+    int* q;  // smem [64]
+    int* w;  // smem [64]
+    int n;
+};
+
+__device__ __forceinline__ uint32_t stage_add(const Params& p, const Smem& S, const Out& o, Stage& st,
+                                              bool fresh, int q, int w, int lane) {
+    const unsigned m = __ballot_sync(FULL, fresh);
+    if (!m) return 0;
+    if (fresh) {
+        const int pos = st.n + __popc(m & lanemask_lt());
+        st.q[pos] = q;
+        st.w[pos] = w;
+    }
+    st.n += __popc(m);
+    __syncwarp();
+    uint32_t T = 0;
+    if (st.n >= 32) {
+        const int qq = st.q[lane], ww = st.w[lane];
+        __syncwarp();
+        T = emit_pairs(p, S, o, true, qq, ww, lane);
+        const int rem = st.n - 32;
+        int tq = 0, tw = 0;
+        if (lane < rem) {
+            tq = st.q[32 + lane];
+            tw = st.w[32 + lane];
+        }
+        __syncwarp();
+        if (lane < rem) {
+            st.q[lane] = tq;
+            st.w[lane] = tw;
+        }
+        st.n = rem;
+        __syncwarp();
+    }
+    return T;
+}
+
+__device__ __forceinline__ uint32_t stage_flush(const Params& p, const Smem& S, const Out& o, Stage& st,
+                                                int lane) {
+    if (st.n == 0) return 0;
+    const bool v = lane < st.n;
+    const int qq = v ? st.q[lane] : 0, ww = v ? st.w[lane] : 0;
+    __syncwarp();
+    st.n = 0;
+    return emit_pairs(p, S, o, v, qq, ww, lane);
+}
+
+// End-of-epoch flush of a CTA's counts: one atomic per CTA and counter.
+__device__ __forceinline__ void flush_counts(unsigned long long* nnew_dst, const Out& o,
+                                             unsigned int* state_dst, unsigned long long nnew,
                                              unsigned long long nedge, unsigned long long* red,
                                              unsigned int* s_state, int nstates) {
+    unsigned long long* edges_dst = &o.qc->edges;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
-        nnew += __shfl_xor_sync(FULL, nnew, d);
-        nedge += __shfl_xor_sync(FULL, nedge, d);
-    }
+    nnew = warp_sum_u64(nnew);
+    nedge = warp_sum_u64(nedge);
     if (lane == 0) {
         red[2 * wid] = nnew;
         red[2 * wid + 1] = nedge;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long a = 0, c = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
-            a += red[2 * i];
-            c += red[2 * i + 1];
-        }
-        if (a) atomicAdd(&ctl->new_cnt[b], a);
-        if (c) atomicAdd(&ctl->edge_cnt[b], c);
-    }
-    for (int q = threadIdx.x; q < nstates; q += blockDim.x) {
-        const unsigned int c = s_state[q];
-        if (c) {
-            atomicAdd(&ctl->state_front[b][q], c);
-            s_state[q] = 0;
+    if (wid == 0) {
+        unsigned long long a = lane < kWarps ? red[2 * lane] : 0ull;
+        unsigned long long c = lane < kWarps ? red[2 * lane + 1] : 0ull;
+        a = warp_sum_u64(a);
+        c = warp_sum_u64(c);
+        if (lane == 0 && a && nnew_dst) atomicAdd(nnew_dst, a);
+        if (lane == 0 && c) atomicAdd(edges_dst, c);
+        if (lane == 0) {  // publish this CTA's shard fill (the local counter may exceed capacity)
+            o.qc->shard[blockIdx.x] = *o.s_resv;
+            *o.s_resv = 0;
         }
     }
-    __syncthreads();
+    if (state_dst)
+        for (int q = threadIdx.x; q < nstates; q += blockDim.x) {
+            const unsigned int c = s_state[q];
+            if (c) {
+                atomicAdd(&state_dst[q], c);
+                s_state[q] = 0;
+            }
+        }
 }
 
-__device__ __forceinline__ void count_state(unsigned int* s_state, bool fresh, int q) {
-    if (fresh) atomicAdd(&s_state[q], 1u);
-}
-
-// Queue totals of buffer b (bundles / segments, clamped to shard capacity).
-__device__ __forceinline__ void queue_totals(const Params& p, int b, unsigned long long* nbun,
-                                             unsigned long long* nseg) {
-    unsigned long long tb = 0, ts = 0;
-    for (int s = 0; s <= kShards; ++s) {
-        const unsigned long long c = ld_volatile(&p.ctl->shard_cnt[b][s]);
-        const unsigned long long bc = c & 0xFFFFFFFFull, sc = c >> 32;
-        const unsigned long long bcap = s < kShards ? p.shard_buncap : p.ovf_buncap;
-        const unsigned long long scap = s < kShards ? p.shard_segcap : p.ovf_segcap;
-        tb += bc < bcap ? bc : bcap;
-        ts += sc < scap ? sc : scap;
+// Totals of the queue produced in the previous epoch, and the per-shard
+// bundle prefix the consumers index with.  Warp-cooperative (warp 0).
+__device__ __forceinline__ void queue_scan(const Params& p, const QCnt* qc, int lane,
+                                           unsigned long long* s_bpre, unsigned long long* nbun,
+                                           unsigned long long* nseg) {
+    constexpr int R = (kShards + 1 + 31) / 32;
+    unsigned long long c[R], sc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {  // issue all loads first
+        const int sh = 32 * r + lane;
+        const unsigned long long v = sh <= kShards ? ldcg(&qc->shard[sh]) : 0ull;
+        const unsigned long long bcap = sh < kShards ? p.shard_buncap : p.ovf_buncap;
+        const unsigned long long scap = sh < kShards ? p.shard_segcap : p.ovf_segcap;
+        c[r] = min(v & 0xFFFFFFFFull, bcap);
+        sc[r] = min(v >> 32, scap);
     }
-    *nbun = tb;
-    *nseg = ts;
+    unsigned long long carry = 0, segs = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int sh = 32 * r + lane;
+        const unsigned long long incl = warp_incl_scan_u64(c[r], lane);
+        if (sh <= kShards) s_bpre[sh] = carry + incl - c[r];
+        carry += __shfl_sync(FULL, incl, 31);
+        segs += sc[r];
+    }
+    if (lane == 0) s_bpre[kShards + 1] = carry;
+    *nbun = carry;
+    *nseg = warp_sum_u64(segs);
 }
 
-// Bookkeeping after frontier F_L has been produced (serial, one thread).
-// Mirrors the masked loop (engine.py:156-160): run while the frontier is
-// non-empty, check the deadline first, then step.  Also picks the direction
-// of level L.
-__device__ void level_bookkeeping(const Params& p, const Smem& S, int L) {
+// Decision after frontier F_L has been produced (warp 0 of every CTA; every
+// CTA reads the same counters and reaches the same result).  Mirrors the
+// masked loop (engine.py:156-160): run while the frontier is non-empty,
+// check the deadline, then step; and picks the direction of level L.
+__device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, int prev_dir, int lane,
+                             View* v, unsigned long long* s_bpre, unsigned long long* s_sv,
+                             unsigned int* s_front) {
     Ctl* ctl = p.ctl;
-    const int b = L & 1;
-    const unsigned long long nnew = ld_volatile(&ctl->new_cnt[b]);
-    const unsigned long long nedge = ld_volatile(&ctl->edge_cnt[b]);
-    const int produced_by_push = (L == 0) || (ctl->dir == DIR_PUSH);
+    const QCnt* qc = &ctl->qc[e % 3];
+    const FCnt* fc = &ctl->fc[L % 3];
+    const unsigned long long nnew = ldcg(&fc->nnew);
+    const unsigned long long nedge = ldcg(&qc->edges);
+    const unsigned int overflow = ldcg(&qc->overflow);
+    const unsigned int expire = ldcg(&qc->expire);
+    const int abort = ldcg(&ctl->abort);
     unsigned long long nbun, nseg;
-    queue_totals(p, b, &nbun, &nseg);
-    ctl->pairs += nnew;
-    for (int q = 0; q < p.nstates; ++q) ctl->state_vis[q] += ctl->state_front[b][q];
-    if (L < 64) ctl->level_new[L] = (long long)nnew;
-    if (ld_volatile(&ctl->overflow)) {
-        ctl->status = ST_OVERFLOW;
-        ctl->iterations = L;
-        ctl->done = 1;
-    } else if (ld_volatile(&ctl->status) != 0) {
-        ctl->done = 1;
+    queue_scan(p, qc, lane, s_bpre, &nbun, &nseg);
+    for (int q = lane; q < p.nstates; q += 32) {
+        const unsigned int f = ldcg(&fc->state[q]);
+        s_front[q] = f;
+        s_sv[q] += f;
+    }
+    __syncwarp();
+    const int produced_by_push = (L == 0) || prev_dir == DIR_PUSH;
+    int done = 0, iterations = 0, status = 0, next = DIR_PUSH, plan = 0;
+    long long ledges = -1;
+    if (abort) {
+        status = ST_DEADLOCK;
+        done = 1;
+    } else if (overflow) {
+        status = ST_OVERFLOW;
+        iterations = L;
+        done = 1;
+    } else if (expire) {
+        status = RPQ_ETIMEOUT;
+        iterations = (int)expire - 1;
+        done = 1;
     } else if (nnew == 0) {
-        ctl->iterations = L;
-        ctl->done = 1;
-    } else if (globaltimer() - ctl->t0 > p.budget_ns) {
-        ctl->status = RPQ_ETIMEOUT;
-        ctl->iterations = L;
-        ctl->done = 1;
+        iterations = L;
+        done = 1;
     } else {
-        if (L > 0) ctl->levels = L;
-        int next = DIR_PUSH;
         if (p.dir_mode == 2) {
             next = DIR_PULL;
         } else if (p.dir_mode == 0) {
             // m_f: edges out of F_L (exact after a push level, estimated from
             // average degrees after a pull level); m_u: in-edges of unvisited
-            // targets whose source state has a frontier.  Beamer: pull when
-            // m_f * alpha > m_u.
-            double mf = 0.0, mu = 0.0;
+            // targets whose source state has a frontier.  Pull when
+            // m_f * alpha > m_u (Beamer's rule; alpha tuned for these kernels).
             const double nv = (double)p.nv;
-            if (produced_by_push) {
-                mf = (double)nedge;
-            } else {
-                for (int q = 0; q < p.nstates; ++q) {
-                    const unsigned int f = ctl->state_front[b][q];
-                    if (!f) continue;
+            double mf = 0.0, mu = 0.0;
+            for (int q = lane; q < p.nstates; q += 32) {
+                if (!produced_by_push && s_front[q])
                     for (int g = S.gbeg[q]; g < S.gbeg[q + 1]; ++g)
-                        mf += (double)f * (double)p.slot_nnz[S.gslot[g]] / nv;
-                }
+                        mf += (double)s_front[q] * (double)p.slot_nnz[S.gslot[g]] / nv;
+                const double unvis = nv - (double)s_sv[q];
+                for (int k = S.ibeg[q]; k < S.ibeg[q + 1]; ++k)
+                    if (s_front[S.isrc[k]]) mu += (double)p.slot_nnz[S.islot[k]] * unvis / nv;
             }
-            for (int q2 = 0; q2 < p.nstates; ++q2) {
-                const double unvis = nv - (double)ctl->state_vis[q2];
-                for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k)
-                    if (ctl->state_front[b][S.isrc[k]])
-                        mu += (double)p.slot_nnz[S.islot[k]] * unvis / nv;
-            }
+            mf = produced_by_push ? (double)nedge : warp_sum_f64(mf);
+            mu = warp_sum_f64(mu);
             next = (mf * (double)p.alpha > mu) ? DIR_PULL : DIR_PUSH;
         }
-        ctl->plan = 0;
         if (next == DIR_PUSH) {
             if (produced_by_push) {
-                ctl->te_push += nedge;
-                ctl->segments += nseg;
-                if (L < 64) ctl->level_edges[L] = (long long)nedge;
+                ledges = (long long)nedge;
                 if (nbun == 0) {  // nothing to expand: the next step is empty
-                    ctl->iterations = L + 1;
-                    ctl->done = 1;
+                    iterations = L + 1;
+                    done = 1;
                 }
             } else {
-                ctl->plan = 1;  // emit F_L's queue from its bitmap first
+                plan = 1;  // emit F_L's queue from its bitmap first
             }
-        } else if (L < 64) {
-            ctl->level_edges[L] = -1;  // pull: edges scanned are not push-model edges
         }
-        ctl->dir = next;
-        if (L < 64) ctl->level_dir[L] = next;
     }
-    // the other parity is produced into during level L
-    for (int s = 0; s <= kShards; ++s) ctl->shard_cnt[b ^ 1][s] = 0;
-    ctl->new_cnt[b ^ 1] = 0;
-    ctl->edge_cnt[b ^ 1] = 0;
-    for (int q = 0; q < p.nstates; ++q) ctl->state_front[b ^ 1][q] = 0;
+    if (lane == 0) {
+        v->done = done;
+        v->dir = next;
+        v->plan = plan;
+        v->status = status;
+        v->iterations = iterations;
+        if (blockIdx.x == 0) {  // results and statistics
+            const unsigned long long now = globaltimer();
+            ctl->pairs += nnew;
+            if (L < 64) {
+                ctl->level_new[L] = (long long)nnew;
+                ctl->level_ns[L] = now - ctl->t0;
+                ctl->level_edges[L] = ledges;
+                ctl->level_dir[L] = next;
+            }
+            if (!done) {
+                if (L > 0) ctl->levels = L;
+                if (next == DIR_PULL) ctl->pull_levels += 1;
+                if (next == DIR_PUSH && produced_by_push) {
+                    ctl->te_push += nedge;
+                    ctl->segments += nseg;
+                }
+                // _Clock.check at the top of iteration L (engine.py:87-89):
+                // recorded now, acted upon at the next decision by every CTA
+                if (now - ctl->t0 > p.budget_ns) ctl->qc[(e + 1) % 3].expire = (unsigned)L + 1;
+            } else {
+                ctl->status = status;
+                ctl->iterations = iterations;
+            }
+        }
+    }
 }
 
-// After a plan phase emitted F_L's queue into buffer L&1.
-__device__ void plan_bookkeeping(const Params& p, int L) {
+// Decision after a plan epoch emitted F_L's queue.
+__device__ void decide_plan(const Params& p, unsigned e, int L, int lane, View* v, unsigned long long* s_bpre) {
     Ctl* ctl = p.ctl;
-    const int b = L & 1;
+    const QCnt* qc = &ctl->qc[e % 3];
+    const unsigned long long nedge = ldcg(&qc->edges);
+    const unsigned int overflow = ldcg(&qc->overflow);
+    const unsigned int expire = ldcg(&qc->expire);
+    const int abort = ldcg(&ctl->abort);
     unsigned long long nbun, nseg;
-    queue_totals(p, b, &nbun, &nseg);
-    const unsigned long long nedge = ld_volatile(&ctl->edge_cnt[b]);
-    ctl->plan = 0;
-    if (ld_volatile(&ctl->overflow)) {
-        ctl->status = ST_OVERFLOW;
-        ctl->iterations = L;
-        ctl->done = 1;
-        return;
+    queue_scan(p, qc, lane, s_bpre, &nbun, &nseg);
+    int done = 0, status = 0, iterations = 0;
+    if (abort) {
+        status = ST_DEADLOCK;
+        done = 1;
+    } else if (overflow) {
+        status = ST_OVERFLOW;
+        iterations = L;
+        done = 1;
+    } else if (expire) {
+        status = RPQ_ETIMEOUT;
+        iterations = (int)expire - 1;
+        done = 1;
+    } else if (nbun == 0) {
+        iterations = L + 1;
+        done = 1;
     }
-    ctl->te_push += nedge;
-    ctl->segments += nseg;
-    if (L < 64) ctl->level_edges[L] = (long long)nedge;
-    if (nbun == 0) {
-        ctl->iterations = L + 1;
-        ctl->done = 1;
+    if (lane == 0) {
+        v->done = done;
+        v->plan = 0;
+        v->status = status;
+        v->iterations = iterations;
+        if (blockIdx.x == 0) {
+            if (L < 64) ctl->level_edges[L] = (long long)nedge;
+            ctl->te_push += nedge;
+            ctl->segments += nseg;
+            if (done) {
+                ctl->status = status;
+                ctl->iterations = iterations;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void reset_qc(QCnt* qc, int tid) {
+    for (int i = tid; i <= kShards; i += kThreads) qc->shard[i] = 0;
+    if (tid == 0) {
+        qc->edges = 0;
+        qc->overflow = 0;
+        qc->expire = 0;
     }
 }
 
 __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ unsigned long long s_red[2 * (kThreads / 32)];
+    __shared__ unsigned long long s_red[2 * kWarps];
     __shared__ unsigned long long s_bpre[kShards + 2];
-    __shared__ unsigned int s_state[kMaxStates];     // per-state discoveries (flushed per level)
-    __shared__ unsigned char s_active[kMaxStates];   // state has a non-empty current frontier
+    __shared__ unsigned long long s_sv[kMaxStates];  // |P| per state (same in every CTA)
+    __shared__ unsigned int s_front[kMaxStates];     // |F_L| per state
+    __shared__ unsigned int s_state[kMaxStates];     // this CTA's discoveries per state
     __shared__ int s_ptarget[kMaxStates];            // pull target states of this level
     __shared__ int s_nptarget;
-    __shared__ CtlView s_view;
+    __shared__ View s_view;
+    __shared__ int s_stage[kWarps][2][64];
+    __shared__ unsigned long long s_resv;
 
     Slot* s_slots = reinterpret_cast<Slot*>(smem_raw);
     int32_t* s_tab = reinterpret_cast<int32_t*>(smem_raw + sizeof(Slot) * 2 * p.nslots);
     for (int i = threadIdx.x; i < 2 * p.nslots; i += blockDim.x) s_slots[i] = p.slots[i];
     for (int i = threadIdx.x; i < p.table_ints; i += blockDim.x) s_tab[i] = p.tables[i];
-    for (int i = threadIdx.x; i < kMaxStates; i += blockDim.x) s_state[i] = 0;
+    if (threadIdx.x == 0) s_resv = 0;
+    for (int i = threadIdx.x; i < kMaxStates; i += blockDim.x) {
+        s_state[i] = 0;
+        s_sv[i] = 0;
+        s_front[i] = 0;
+    }
     Smem S;
     S.slots = s_slots;
     S.gbeg = s_tab;
@@ -498,31 +754,38 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     Ctl* ctl = p.ctl;
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    const int wpb = blockDim.x >> 5;
     const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long gthreads = (long long)gridDim.x * blockDim.x;
-    const long long gwarp = (long long)blockIdx.x * wpb + wid;
-    const long long nwarps = (long long)gridDim.x * wpb;
+    const long long gwarp = (long long)blockIdx.x * kWarps + wid;
+    const long long nwarps = (long long)gridDim.x * kWarps;
     const long long Wn = ((long long)p.nv + 31) >> 5;  // used words per bitmap row
+    const long long nbits4 = (long long)p.nstates * p.W / 4;
+    const bool cta0 = blockIdx.x == 0;
+    Stage stage;
+    stage.q = s_stage[wid][0];
+    stage.w = s_stage[wid][1];
+    stage.n = 0;
     if (gtid == 0) ctl->t0 = globaltimer();
 
-    // ---- phase 0: P <- 0, F <- 0 --------------------------------------------
+    unsigned e = 0;  // barriers passed
+
+    // ---- epoch 0: P <- 0, F <- 0 --------------------------------------------
     {
-        const long long n4 = (long long)p.nstates * p.W / 4;
         uint4* v4 = reinterpret_cast<uint4*>(p.visited);
-        for (long long i = gtid; i < n4; i += gthreads) v4[i] = make_uint4(0, 0, 0, 0);
+        for (long long i = gtid; i < nbits4; i += gthreads) v4[i] = make_uint4(0, 0, 0, 0);
         for (int f = 0; f < 3; ++f) {
             uint4* f4 = reinterpret_cast<uint4*>(p.fb[f]);
-            for (long long i = gtid; i < n4; i += gthreads) f4[i] = make_uint4(0, 0, 0, 0);
+            for (long long i = gtid; i < nbits4; i += gthreads) f4[i] = make_uint4(0, 0, 0, 0);
         }
     }
-    __syncthreads();
-    grid_sync(ctl, &s_view, [] {});
+    grid_barrier(ctl, ++e);
 
-    // ---- seed: P = M = {(q_s, source)} (engine.py:106-109, :154-155) --------
+    // ---- epoch 1: seed P = M = {(q_s, source)} (engine.py:106-109, :154-155)
     {
+        const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv};
+        if (cta0) reset_qc(&ctl->qc[(e + 2) % 3], threadIdx.x);
         unsigned long long nnew = 0, nedge = 0;
-        if (blockIdx.x == 0 && wid == 0) {
+        if (cta0 && wid == 0) {
             for (int i0 = 0; i0 < p.nstarts; i0 += 32) {
                 const int i = i0 + lane;
                 bool fresh = false;
@@ -535,35 +798,38 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                     if (fresh) atomicOr(p.fb[0] + off, bit);
                 }
                 nnew += fresh ? 1 : 0;
-                count_state(s_state, fresh, q);
-                const uint32_t T = emit_pairs(p, S, 0, fresh, q, p.source, lane);
+                if (fresh) atomicAdd(&s_state[q], 1u);
+                const uint32_t T = emit_pairs(p, S, o, fresh, q, p.source, lane);
                 if (lane == 0) nedge += T;
             }
         }
         __syncthreads();
-        flush_counts(ctl, 0, nnew, nedge, s_red, s_state, p.nstates);
+        flush_counts(&ctl->fc[0].nnew, o, ctl->fc[0].state, nnew, nedge, s_red, s_state, p.nstates);
     }
-    grid_sync(ctl, &s_view, [&] { level_bookkeeping(p, S, 0); });
+    grid_barrier(ctl, ++e);
+    if (wid == 0) decide_level(p, S, e, 0, DIR_PUSH, lane, &s_view, s_bpre, s_sv, s_front);
+    __syncthreads();
 
     // ---- level loop -----------------------------------------------------------
-    for (int L = 0;; ++L) {
+    int L = 0;
+    int dir = DIR_PUSH;
+    for (;;) {
         if (s_view.done) break;
-        const int cur = L & 1, nxt = cur ^ 1;
+        dir = s_view.dir;
         const uint32_t* fcur = p.fb[L % 3];
         uint32_t* fnext = p.fb[(L + 1) % 3];
 
-        if (s_view.dir == DIR_PUSH && s_view.plan) {
-            // plan: emit F_L's row segments from its bitmap (after a pull level)
-            for (int q = threadIdx.x; q < p.nstates; q += blockDim.x)
-                s_active[q] = ld_volatile(&ctl->state_front[cur][q]) != 0;
-            __syncthreads();
+        if (dir == DIR_PUSH && s_view.plan) {
+            // ---- plan epoch: emit F_L's row segments from its bitmap (after pull)
+            const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv};
+            if (cta0) reset_qc(&ctl->qc[(e + 2) % 3], threadIdx.x);
             unsigned long long nedge = 0;
             for (int q = 0; q < p.nstates; ++q) {
-                if (!s_active[q] || S.gbeg[q + 1] == S.gbeg[q]) continue;
+                if (!s_front[q] || S.gbeg[q + 1] == S.gbeg[q]) continue;
                 const uint32_t* row = fcur + (long long)q * p.W;
                 for (long long w0 = gwarp * 32; w0 < Wn; w0 += nwarps * 32) {
                     const long long wi = w0 + lane;
-                    uint32_t bits = wi < Wn ? row[wi] : 0u;
+                    const uint32_t bits = wi < Wn ? row[wi] : 0u;
                     unsigned any = __ballot_sync(FULL, bits != 0);
                     while (any) {
                         const int src_lane = __ffs(any) - 1;
@@ -571,166 +837,235 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                         const uint32_t wb = __shfl_sync(FULL, bits, src_lane);
                         const bool valid = (wb >> lane) & 1u;
                         const int v = (int)((w0 + src_lane) * 32 + lane);
-                        const uint32_t T = emit_pairs(p, S, cur, valid, q, v, lane);
+                        const uint32_t T = stage_add(p, S, o, stage, valid, q, v, lane);
                         if (lane == 0) nedge += T;
                     }
                 }
             }
-            flush_counts(ctl, cur, 0, nedge, s_red, s_state, 0);
-            grid_sync(ctl, &s_view, [&] { plan_bookkeeping(p, L); });
+            {
+                const uint32_t T = stage_flush(p, S, o, stage, lane);
+                if (lane == 0) nedge += T;
+            }
+            __syncthreads();
+            flush_counts(nullptr, o, nullptr, 0, nedge, s_red, s_state, 0);
+            grid_barrier(ctl, ++e);
+            if (wid == 0) decide_plan(p, e, L, lane, &s_view, s_bpre);
+            __syncthreads();
             if (s_view.done) break;
         }
 
-        // zero the bitmap level L+1 will write into F_{L+2}
-        {
-            uint4* z4 = reinterpret_cast<uint4*>(p.fb[(L + 2) % 3]);
-            const long long n4 = (long long)p.nstates * p.W / 4;
-            for (long long i = gtid; i < n4; i += gthreads) z4[i] = make_uint4(0, 0, 0, 0);
+        // ---- expand epoch of level L -------------------------------------------
+        const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv};
+        if (cta0) {
+            reset_qc(&ctl->qc[(e + 2) % 3], threadIdx.x);
+            FCnt* fz = &ctl->fc[(L + 2) % 3];
+            for (int q = threadIdx.x; q < kMaxStates; q += blockDim.x) fz->state[q] = 0;
+            if (threadIdx.x == 0) fz->nnew = 0;
         }
-
+        {  // zero the bitmap level L+1 will write F_{L+2} into
+            uint4* z4 = reinterpret_cast<uint4*>(p.fb[(L + 2) % 3]);
+            for (long long i = gtid; i < nbits4; i += gthreads) z4[i] = make_uint4(0, 0, 0, 0);
+        }
         unsigned long long nnew = 0, nedge = 0;
-        if (s_view.dir == DIR_PUSH) {
-            // ---- push: expand the bundles of F_L's queue ------------------------
-            if (threadIdx.x == 0) {
-                unsigned long long run = 0;
-                for (int s = 0; s <= kShards; ++s) {
-                    s_bpre[s] = run;
-                    const unsigned long long c = ld_volatile(&ctl->shard_cnt[cur][s]) & 0xFFFFFFFFull;
-                    const unsigned long long cap = s < kShards ? p.shard_buncap : p.ovf_buncap;
-                    run += c < cap ? c : cap;
-                }
-                s_bpre[kShards + 1] = run;
-            }
-            __syncthreads();
+        if (dir == DIR_PUSH) {
+            // ---- push: expand the bundles of F_L's queue (produced last epoch)
             const unsigned long long nb = s_bpre[kShards + 1];
-            const uint2* bun = p.bun[cur];
-            const uint2* seg = p.seg[cur];
+            const uint2* bun = p.bun[e & 1];
+            const uint2* seg = p.seg[e & 1];
             // CTA-major dealing: consecutive bundles (often one row) land on different SMs
-            const unsigned long long step = (unsigned long long)gridDim.x * wpb;
+            const unsigned long long step = (unsigned long long)gridDim.x * kWarps;
             for (unsigned long long bi = (unsigned long long)wid * gridDim.x + blockIdx.x; bi < nb;
                  bi += step) {
-                int s = 0;
+                int sh = 0;
 #pragma unroll
-                for (int h = 64; h >= 1; h >>= 1)
-                    if (s + h <= kShards && s_bpre[s + h] <= bi) s += h;
-                const uint2 bd = __ldcg(bun + (unsigned long long)s * p.shard_buncap + (bi - s_bpre[s]));
-                if (bd.x == kHoleBundle) continue;
-                const uint32_t s0 = bd.x;
-                const uint32_t off = bd.y & 0xFFFFFFu;
-                const uint32_t cnt = (bd.y >> 24) + 1;
-                uint32_t my_start = 0, my_len = 0, my_grp = 0;
-                if ((unsigned long long)s0 + lane < p.seg_alloc) {
-                    const uint2 sg = __ldcg(seg + s0 + lane);
-                    my_start = sg.x;
-                    my_len = sg.y >> 8;
-                    my_grp = sg.y & 0xFFu;
+                for (int h = 128; h >= 1; h >>= 1)
+                    if (sh + h <= kShards && s_bpre[sh + h] <= bi) sh += h;
+                const uint2 bd = __ldcg(bun + (unsigned long long)sh * p.shard_buncap + (bi - s_bpre[sh]));
+                if (bd.y == kHoleY) continue;
+                const uint32_t cnt = (bd.y & 127u) + 1;
+                int w[kEdgesPerLane], gj[kEdgesPerLane];
+                if (bd.y & kInline) {
+                    // one row: columns bd.x .. bd.x + cnt - 1
+                    const int g = (int)((bd.y >> 7) & 0xFFu);
+                    const int32_t* col = S.slots[S.gslot[g]].col + bd.x;
+#pragma unroll
+                    for (int u = 0; u < kEdgesPerLane; ++u) {
+                        const uint32_t ed = (uint32_t)(lane + 32 * u);
+                        gj[u] = ed < cnt ? g : -1;
+                        w[u] = ed < cnt ? __ldg(col + ed) : 0;
+                    }
+                } else {
+                    const uint32_t s0 = bd.x;
+                    const uint32_t off = (bd.y >> 7) & 0xFFFFFFu;
+                    uint32_t my_start = 0, my_len = 0, my_grp = 0;
+                    if ((unsigned long long)s0 + lane < p.seg_alloc) {
+                        const uint2 sg = __ldcg(seg + s0 + lane);
+                        my_start = sg.x;
+                        my_len = sg.y >> 8;
+                        my_grp = sg.y & 0xFFu;
+                    }
+                    if (lane == 0) {
+                        my_start += off;
+                        my_len -= off;
+                    }
+                    const uint32_t incl = warp_incl_scan(my_len, lane);
+                    const uint32_t excl = incl - my_len;
+                    // edges lane, lane+32, ...: locate, then issue all column loads
+#pragma unroll
+                    for (int u = 0; u < kEdgesPerLane; ++u) {
+                        const uint32_t ed = (uint32_t)(lane + 32 * u);
+                        const bool active = ed < cnt;
+                        const int j = warp_upper_lane(excl, active ? ed : 0u);
+                        const uint32_t sj = __shfl_sync(FULL, my_start, j);
+                        const uint32_t exj = __shfl_sync(FULL, excl, j);
+                        const int g = (int)__shfl_sync(FULL, my_grp, j);
+                        gj[u] = active ? g : -1;
+                        w[u] = active ? __ldg(S.slots[S.gslot[g]].col + sj + (ed - exj)) : 0;
+                    }
                 }
-                if (lane == 0) {
-                    my_start += off;
-                    my_len -= off;
-                }
-                const uint32_t incl = warp_incl_scan(my_len, lane);
-                const uint32_t excl = incl - my_len;
-                const bool active = (uint32_t)lane < cnt;
-                const int j = warp_upper_lane(excl, active ? (uint32_t)lane : 0u);
-                const uint32_t sj = __shfl_sync(FULL, my_start, j);
-                const uint32_t exj = __shfl_sync(FULL, excl, j);
-                const int gj = (int)__shfl_sync(FULL, my_grp, j);
-                int w = 0, t0 = 0, t1 = 0;
-                if (active) {
-                    const Slot sl = S.slots[S.gslot[gj]];
-                    w = __ldg(sl.col + sj + ((uint32_t)lane - exj));
-                    t0 = S.toff[gj];
-                    t1 = S.toff[gj + 1];
-                }
+                // probe P for every target, then claim with atomicOr
                 for (int k = 0; k < p.maxT; ++k) {
-                    bool fresh = false;
-                    int q2 = 0;
-                    if (active && t0 + k < t1) {
-                        q2 = S.targets[t0 + k];
-                        const long long off2 = (long long)q2 * p.W + (w >> 5);
-                        const uint32_t bit = 1u << (w & 31);
-                        if (!(p.visited[off2] & bit)) {
-                            fresh = !(atomicOr(p.visited + off2, bit) & bit);
-                            if (fresh) atomicOr(fnext + off2, bit);
+                    uint32_t old[kEdgesPerLane];
+                    int q2[kEdgesPerLane];
+#pragma unroll
+                    for (int u = 0; u < kEdgesPerLane; ++u) {
+                        q2[u] = -1;
+                        old[u] = 0xFFFFFFFFu;
+                        if (gj[u] >= 0) {
+                            const int t0 = S.toff[gj[u]];
+                            if (t0 + k < S.toff[gj[u] + 1]) {
+                                q2[u] = S.targets[t0 + k];
+                                old[u] = p.visited[(long long)q2[u] * p.W + (w[u] >> 5)];
+                            }
                         }
                     }
-                    nnew += fresh ? 1 : 0;
-                    count_state(s_state, fresh, q2);
-                    const uint32_t T = emit_pairs(p, S, nxt, fresh, q2, w, lane);
-                    if (lane == 0) nedge += T;
+#pragma unroll
+                    for (int u = 0; u < kEdgesPerLane; ++u) {
+                        const uint32_t bit = 1u << (w[u] & 31);
+                        if (q2[u] >= 0 && !(old[u] & bit)) {
+                            const long long off2 = (long long)q2[u] * p.W + (w[u] >> 5);
+                            old[u] = atomicOr(p.visited + off2, bit);
+                            if (!(old[u] & bit)) atomicOr(fnext + off2, bit);
+                        } else {
+                            old[u] = 0xFFFFFFFFu;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kEdgesPerLane; ++u) {
+                        const bool fresh = q2[u] >= 0 && !(old[u] & (1u << (w[u] & 31)));
+                        nnew += fresh ? 1 : 0;
+                        if (fresh) atomicAdd(&s_state[q2[u]], 1u);
+                        const uint32_t T = stage_add(p, S, o, stage, fresh, q2[u], w[u], lane);
+                        if (lane == 0) nedge += T;
+                    }
                 }
+            }
+            {
+                const uint32_t T = stage_flush(p, S, o, stage, lane);
+                if (lane == 0) nedge += T;
             }
         } else {
             // ---- pull: unvisited (q', w) scan A_s^T row w for a member of F_L[q]
             if (threadIdx.x == 0) {
                 int n = 0;
-                for (int q = 0; q < p.nstates; ++q)
-                    s_active[q] = ld_volatile(&ctl->state_front[cur][q]) != 0;
                 for (int q2 = 0; q2 < p.nstates; ++q2) {
                     bool any = false;
-                    for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k) any |= s_active[S.isrc[k]] != 0;
+                    for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k) any |= s_front[S.isrc[k]] != 0;
                     if (any) s_ptarget[n++] = q2;
                 }
                 s_nptarget = n;
             }
             __syncthreads();
-            const long long ntask = (long long)s_nptarget * Wn;
+            const long long nblk = (Wn + kPullVerts - 1) / kPullVerts;
+            const long long ntask = (long long)s_nptarget * nblk;
             for (long long task = gwarp; task < ntask; task += nwarps) {
-                const int q2 = s_ptarget[task / Wn];
-                const long long word = task % Wn;
-                const long long voff = (long long)q2 * p.W + word;
-                const uint32_t vis = p.visited[voff];
-                const int w = (int)(word * 32 + lane);
-                const bool need = w < p.nv && !((vis >> lane) & 1u);
-                if (__ballot_sync(FULL, need) == 0) continue;
-                bool found = false;
+                const int q2 = s_ptarget[task / nblk];
+                const long long word0 = (task % nblk) * kPullVerts;
+                uint32_t vis[kPullVerts];
+                bool need[kPullVerts], found[kPullVerts];
+                int w[kPullVerts];
+#pragma unroll
+                for (int u = 0; u < kPullVerts; ++u)
+                    vis[u] = word0 + u < Wn ? p.visited[(long long)q2 * p.W + word0 + u] : 0xFFFFFFFFu;
+                bool any_need = false;
+#pragma unroll
+                for (int u = 0; u < kPullVerts; ++u) {
+                    w[u] = (int)((word0 + u) * 32 + lane);
+                    need[u] = w[u] < p.nv && !((vis[u] >> lane) & 1u);
+                    found[u] = false;
+                    any_need |= need[u];
+                }
+                if (__ballot_sync(FULL, any_need) == 0) continue;
                 for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k) {
                     const int q = S.isrc[k];
-                    if (!s_active[q]) continue;
-                    const bool look = need && !found;
-                    if (__ballot_sync(FULL, look) == 0) break;
+                    if (!s_front[q]) continue;
+                    bool look[kPullVerts], any_look = false;
+#pragma unroll
+                    for (int u = 0; u < kPullVerts; ++u) {
+                        look[u] = need[u] && !found[u];
+                        any_look |= look[u];
+                    }
+                    if (__ballot_sync(FULL, any_look) == 0) break;
                     const Slot ps = S.slots[p.nslots + S.islot[k]];
                     const uint32_t* frow = fcur + (long long)q * p.W;
-                    uint32_t lo = 0, hi = 0;
-                    if (look) {
-                        lo = __ldg(ps.rowptr + w);
-                        hi = __ldg(ps.rowptr + w + 1);
+                    uint32_t lo[kPullVerts], hi[kPullVerts];
+#pragma unroll
+                    for (int u = 0; u < kPullVerts; ++u) {
+                        lo[u] = look[u] ? __ldg(ps.rowptr + w[u]) : 0u;
+                        hi[u] = look[u] ? __ldg(ps.rowptr + w[u] + 1) : 0u;
                     }
-                    // first kPullInline in-edges per lane, loads issued together
-                    int u[kPullInline];
+                    // the first kPullInline in-edges of every vertex: all loads in flight together
+                    int cand[kPullVerts][kPullInline];
 #pragma unroll
-                    for (int i = 0; i < kPullInline; ++i)
-                        u[i] = (look && lo + i < hi) ? __ldg(ps.col + lo + i) : -1;
+                    for (int u = 0; u < kPullVerts; ++u)
 #pragma unroll
-                    for (int i = 0; i < kPullInline; ++i)
-                        if (u[i] >= 0 && ((frow[u[i] >> 5] >> (u[i] & 31)) & 1u)) found = true;
-                    // longer rows: the whole warp scans one row at a time
-                    unsigned longrows = __ballot_sync(FULL, look && !found && hi - lo > kPullInline);
-                    while (longrows) {
-                        const int ln = __ffs(longrows) - 1;
-                        longrows &= longrows - 1;
-                        const uint32_t rlo = __shfl_sync(FULL, lo, ln) + kPullInline;
-                        const uint32_t rhi = __shfl_sync(FULL, hi, ln);
-                        bool hit = false;
-                        for (uint32_t e = rlo; e < rhi; e += 32) {
-                            bool h = false;
-                            if (e + lane < rhi) {
-                                const int uu = __ldg(ps.col + e + lane);
-                                h = (frow[uu >> 5] >> (uu & 31)) & 1u;
+                        for (int i = 0; i < kPullInline; ++i)
+                            cand[u][i] = (lo[u] + i < hi[u]) ? __ldg(ps.col + lo[u] + i) : -1;
+                    uint32_t fw[kPullVerts][kPullInline];
+#pragma unroll
+                    for (int u = 0; u < kPullVerts; ++u)
+#pragma unroll
+                        for (int i = 0; i < kPullInline; ++i)
+                            fw[u][i] = cand[u][i] >= 0 ? frow[cand[u][i] >> 5] : 0u;
+#pragma unroll
+                    for (int u = 0; u < kPullVerts; ++u)
+#pragma unroll
+                        for (int i = 0; i < kPullInline; ++i)
+                            if (cand[u][i] >= 0 && ((fw[u][i] >> (cand[u][i] & 31)) & 1u)) found[u] = true;
+                    // longer rows: the whole warp scans one row at a time, early exit
+#pragma unroll
+                    for (int u = 0; u < kPullVerts; ++u) {
+                        unsigned longrows = __ballot_sync(FULL, look[u] && !found[u] && hi[u] - lo[u] > kPullInline);
+                        while (longrows) {
+                            const int ln = __ffs(longrows) - 1;
+                            longrows &= longrows - 1;
+                            const uint32_t rlo = __shfl_sync(FULL, lo[u], ln) + kPullInline;
+                            const uint32_t rhi = __shfl_sync(FULL, hi[u], ln);
+                            bool hit = false;
+                            for (uint32_t ed = rlo; ed < rhi; ed += 128) {
+                                int uu[4];
+#pragma unroll
+                                for (int c = 0; c < 4; ++c)
+                                    uu[c] = ed + 32 * c + lane < rhi ? __ldg(ps.col + ed + 32 * c + lane) : -1;
+                                bool h = false;
+#pragma unroll
+                                for (int c = 0; c < 4; ++c)
+                                    if (uu[c] >= 0) h |= (frow[uu[c] >> 5] >> (uu[c] & 31)) & 1u;
+                                if (__ballot_sync(FULL, h)) {
+                                    hit = true;
+                                    break;
+                                }
                             }
-                            if (__ballot_sync(FULL, h)) {
-                                hit = true;
-                                break;
-                            }
+                            if (hit && lane == ln) found[u] = true;
                         }
-                        if (hit && lane == ln) found = true;
                     }
                 }
-                const unsigned fmask = __ballot_sync(FULL, found);
-                if (fmask) {
-                    if (lane == 0) {
-                        p.visited[voff] = vis | fmask;
+#pragma unroll
+                for (int u = 0; u < kPullVerts; ++u) {
+                    const unsigned fmask = __ballot_sync(FULL, found[u]);
+                    if (fmask && lane == u) {
+                        const long long voff = (long long)q2 * p.W + word0 + u;
+                        p.visited[voff] = vis[u] | fmask;
                         fnext[voff] = fmask;
                         nnew += __popc(fmask);
                         atomicAdd(&s_state[q2], (unsigned)__popc(fmask));
@@ -738,12 +1073,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                 }
             }
         }
-        flush_counts(ctl, nxt, nnew, nedge, s_red, s_state, p.nstates);
-        grid_sync(ctl, &s_view, [&] { level_bookkeeping(p, S, L + 1); });
+        __syncthreads();
+        if (threadIdx.x == 0 && L < 64) atomicMax(&ctl->work_ns[L], globaltimer() - ctl->t0);
+        flush_counts(&ctl->fc[(L + 1) % 3].nnew, o, ctl->fc[(L + 1) % 3].state, nnew, nedge, s_red,
+                     s_state, p.nstates);
+        grid_barrier(ctl, ++e);
+        if (cta0 && threadIdx.x == 0 && L < 64) ctl->bar_ns[L] = globaltimer() - ctl->t0;
+        ++L;
+        if (wid == 0) decide_level(p, S, e, L, dir, lane, &s_view, s_bpre, s_sv, s_front);
+        __syncthreads();
     }
 
     // ---- epilogue: answer = OR of P's rows at final states (engine.py:112-114)
-    if (ld_volatile(&ctl->status) == 0) {
+    if (s_view.status == 0) {
         unsigned long long cnt = 0;
         for (long long i = gtid; i < Wn; i += gthreads) {
             uint32_t acc = 0;
@@ -763,7 +1105,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                 for (int k = 0; i * 32 + k < p.nv; ++k) out[k] = (acc >> k) & 1u;
             }
         }
-        // exact push-model TE = sum over (q, v) in P of the out-degrees of q's groups
+        // exact push-model TE = sum over (q, v) in P of q's group out-degrees x targets
         unsigned long long te = 0;
         if (p.count_te) {
             for (int q = 0; q < p.nstates; ++q) {
@@ -782,11 +1124,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                 }
             }
         }
-#pragma unroll
-        for (int d = 16; d >= 1; d >>= 1) {
-            cnt += __shfl_xor_sync(FULL, cnt, d);
-            te += __shfl_xor_sync(FULL, te, d);
-        }
+        cnt = warp_sum_u64(cnt);
+        te = warp_sum_u64(te);
         if (lane == 0 && cnt) atomicAdd(&ctl->reach_count, cnt);
         if (lane == 0 && te) atomicAdd(&ctl->te_exact, te);
     }

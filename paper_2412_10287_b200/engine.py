@@ -55,7 +55,7 @@ class EngineOptions:
     debug_checks: bool = False
     device: int = 0
     direction: str = "auto"  # per-level push/pull policy of the device BFS
-    alpha: float = 15.0  # Beamer's switch constant (pull when m_f * alpha > m_u)
+    alpha: float = 4.0  # Beamer's switch constant (pull when m_f * alpha > m_u)
     count_te: bool = False  # exact product-edge count in EvalResult.stats
 
     def validate(self) -> None:
@@ -276,7 +276,7 @@ class PreparedQuery:
         self.q = self.dg.acquire_query(self.table)
         self.nv = int(g.num_vertices)
 
-    def set_options(self, direction="auto", count_te=False, alpha=15.0):
+    def set_options(self, direction="auto", count_te=False, alpha=4.0):
         raise_for_status(_lib.engine().rpq_query_set_options(
             self.q, DIRECTIONS[direction], int(count_te), float(alpha)), "rpq_query_set_options")
 
