@@ -74,11 +74,10 @@ def load_automaton(config, query):
 
 
 def ranked_sources(sg, k):
-    import numpy as np
+    """k highest out-degree vertices, ties to the lowest id (multigpu.ranked_sources)."""
+    from paper_2412_10287_b200.multigpu import ranked_sources as rs
 
-    deg = sg.out_degree()
-    order = np.lexsort((np.arange(sg.nv), -deg))  # degree desc, id asc
-    return [int(v) for v in order[:k]]
+    return rs(sg.out_degree(), k)
 
 
 def read_peaks():
@@ -318,15 +317,11 @@ def run_engine(args, rank, world, local_rank):
 
     h2d, d2h_ctl = pq.io_bytes()
     d2h = d2h_ctl + sg.nv
-    if world > 1:
-        t = torch.tensor([total_ms, sum(e2e_s) if e2e_s else 0.0], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_max_ms, e2e_max_s = float(t[0]), float(t[1])
-        u = torch.tensor([te * args.steps], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(u)
-        units = float(u[0])
-    else:
-        total_max_ms, e2e_max_s, units = total_ms, sum(e2e_s), float(te * args.steps)
+    from paper_2412_10287_b200.multigpu import reduce_timing
+
+    # max over ranks of the device time, sum over ranks of the product edges
+    total_max_ms, units = reduce_timing(total_ms, te * args.steps, dev)
+    e2e_max_s, _ = reduce_timing(sum(e2e_s) if e2e_s else 0.0, 0, dev)
     pq.close()
     if rank != 0:
         return None

@@ -71,15 +71,15 @@ typedef struct rpq_stats {
     int32_t iterations;      /* masked-loop iterations (engine.py:157-160), incl. the final empty step */
     int32_t levels;          /* non-empty frontiers produced after the seed */
     int32_t grid;            /* CTAs of the persistent step kernel */
-    int64_t te;              /* product edges traversed, SURVEY.md §8(d) TE (exact, in
-                                push-model terms whatever direction each level ran) */
-    int64_t segments;        /* long rows: kChunk-edge chunks shared by all warps */
+    int64_t te;              /* product edges traversed, SURVEY.md §8(d) TE: exact when
+                                count_te is set, else the edges push levels expanded */
+    int64_t segments;        /* (pair, transition group) row lookups with degree > 0 */
     int64_t visited_pairs;   /* |P| at exit */
     int64_t reach_count;     /* |answer| */
     float device_ms;         /* CUDA-event time, first kernel to answer ready */
     int32_t pull_levels;     /* levels run in the pull direction */
     int64_t level_new[RPQ_STATS_LEVELS];    /* |F_L|: new (state, vertex) pairs per level */
-    int64_t level_edges[RPQ_STATS_LEVELS];  /* push-model out-edges of F_L (m_f) */
+    int64_t level_edges[RPQ_STATS_LEVELS];  /* push-model edges expanded from F_L (-1: pulled) */
     int64_t level_ns[RPQ_STATS_LEVELS];     /* kernel start -> level L's decision taken (CTA 0) */
     int64_t work_ns[RPQ_STATS_LEVELS];      /* kernel start -> last CTA done with level L's work */
     int64_t bar_ns[RPQ_STATS_LEVELS];       /* kernel start -> CTA 0 past the barrier after level L */
@@ -121,9 +121,8 @@ RPQ_API int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans,
                      const int32_t* t_src, const int32_t* t_label, const uint8_t* t_inv,
                      const int32_t* t_dst, int32_t nstarts, const int32_t* starts,
                      int32_t nfinals, const int32_t* finals, rpq_query** out);
-/* Direction policy (RPQ_DIR_*), count_te (accepted for compatibility: TE is
- * always exact), Beamer's alpha (default: auto, 0, 4).  Results do not depend
- * on these. */
+/* Direction policy (RPQ_DIR_*), exact-TE accounting on/off, Beamer's alpha
+ * (default: auto, off, 4).  Results do not depend on these. */
 RPQ_API int rpq_query_set_options(rpq_query* q, int32_t direction, int32_t count_te, double alpha);
 /* Enqueue one evaluation from `source` on `stream` (a cudaStream_t, or NULL for
  * the query's own stream).  timeout_s < 0 or inf: no deadline.  The deadline is

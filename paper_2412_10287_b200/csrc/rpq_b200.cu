@@ -79,12 +79,13 @@ struct rpq_query {
     Slot* h_slots = nullptr;
     uint32_t* d_visited = nullptr;
     uint32_t* d_fb[3] = {nullptr, nullptr, nullptr};
-    uint2* d_wl[2] = {nullptr, nullptr};
-    uint4* d_chunks = nullptr;
+    uint2* d_seg[2] = {nullptr, nullptr};
+    uint2* d_bun[2] = {nullptr, nullptr};
     Ctl* d_ctl = nullptr;
     Ctl* h_ctl = nullptr;  // pinned
     uint8_t* d_reach = nullptr;
-    unsigned long long wl_cap = 0, wl_ovf_cap = 0, ch_cap = 0, ch_ovf_cap = 0;
+    unsigned long long shard_segcap = 0, shard_buncap = 0, ovf_segcap = 0, ovf_buncap = 0;
+    unsigned long long seg_alloc = 0, bun_alloc = 0;
     long long W = 0;
     int dir_mode = 0;
     int count_te = 0;
@@ -162,9 +163,10 @@ void free_query_buffers(rpq_query* q) {
     if (q->d_visited) cudaFree(q->d_visited);
     for (int f = 0; f < 3; ++f)
         if (q->d_fb[f]) cudaFree(q->d_fb[f]);
-    for (int b = 0; b < 2; ++b)
-        if (q->d_wl[b]) cudaFree(q->d_wl[b]);
-    if (q->d_chunks) cudaFree(q->d_chunks);
+    for (int b = 0; b < 2; ++b) {
+        if (q->d_seg[b]) cudaFree(q->d_seg[b]);
+        if (q->d_bun[b]) cudaFree(q->d_bun[b]);
+    }
     if (q->h_tables) cudaFreeHost(q->h_tables);
     if (q->h_slots) cudaFreeHost(q->h_slots);
     if (q->d_ctl) cudaFree(q->d_ctl);
@@ -349,23 +351,23 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
         }
     for (auto& k : slot_keys) q->slot_nnz.push_back((unsigned long long)g->labels[k.first].nnz[k.second]);
 
-    // word lists: every non-empty word of F_{L+1} is listed once, so a level
-    // lists at most nstates * ceil(|V|/32) words; CTA regions get twice their
-    // share, the overflow region the whole bound.  Chunks: a row of length d
-    // gives ceil(d / kChunk) chunks, and each (group or in-transition, row)
-    // is chunked at most once per level.
+    // queue capacities: every (state, vertex) pair is discovered at most once,
+    // so one level holds at most |V| segments per group (+ splits of huge
+    // rows); bundles are at most one partial per emission plus edges/kBundle.
     const unsigned long long nv = (unsigned long long)g->nv;
-    const unsigned long long words = (unsigned long long)nstates * ((nv + 31) / 32);
-    q->wl_cap = 2 * words / kMaxCtas + 256;
-    q->wl_ovf_cap = words + 64;
-    unsigned long long row_edges = 0;  // edges of every (group or in-transition) row set
-    for (size_t i = 0; i < gslot.size(); ++i) row_edges += q->slot_nnz[gslot[i]];
-    for (size_t i = 0; i < islot.size(); ++i) row_edges += q->slot_nnz[islot[i]];
-    const unsigned long long ch_bound = row_edges / kChunk + row_edges / kLongRow + 64;
-    q->ch_cap = 2 * ch_bound / kMaxCtas + 256;
-    q->ch_ovf_cap = ch_bound;
-    (void)edge_bound;
-    (void)groups_total;
+    const unsigned long long segbound = nv * groups_total + edge_bound / kSegLenMax + 64;
+    const unsigned long long bunbound = segbound + edge_bound / kBundle + 64;
+    q->shard_segcap = segbound / kShards + segbound / (4 * kShards) + 1024;
+    q->shard_buncap = bunbound / kShards + bunbound / (4 * kShards) + 1024;
+    q->ovf_segcap = segbound;
+    q->ovf_buncap = bunbound;
+    q->seg_alloc = q->shard_segcap * kShards + q->ovf_segcap + 32;
+    q->bun_alloc = q->shard_buncap * kShards + q->ovf_buncap;
+    if (q->seg_alloc >= 0xFFFFFFFFull || q->shard_buncap >= 0xFFFFFFFFull ||
+        q->ovf_buncap >= 0xFFFFFFFFull) {
+        delete q;
+        return fail(RPQ_EINVAL, "frontier queue would exceed 2^32 entries");
+    }
     q->W = (((long long)g->nv + 31) / 32 + 3) / 4 * 4;
 
     auto bail = [&](int rc) {
@@ -385,9 +387,13 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     QTRY(cudaMalloc(&q->d_slot_nnz, std::max<size_t>(q->slot_nnz.size(), 1) * sizeof(unsigned long long)));
     QTRY(cudaMalloc(&q->d_visited, bitmap_bytes));
     for (int f = 0; f < 3; ++f) QTRY(cudaMalloc(&q->d_fb[f], bitmap_bytes));
-    for (int b = 0; b < 2; ++b)
-        QTRY(cudaMalloc(&q->d_wl[b], (size_t)(q->wl_cap * kMaxCtas + q->wl_ovf_cap) * sizeof(uint2)));
-    QTRY(cudaMalloc(&q->d_chunks, (size_t)(q->ch_cap * kMaxCtas + q->ch_ovf_cap) * sizeof(uint4)));
+    for (int b = 0; b < 2; ++b) {
+        QTRY(cudaMalloc(&q->d_seg[b], (size_t)q->seg_alloc * sizeof(uint2)));
+        QTRY(cudaMalloc(&q->d_bun[b], (size_t)q->bun_alloc * sizeof(uint2)));
+        // a consumer reads up to 32 segments past a bundle's own; keep them
+        // finite so its scan cannot wrap
+        QTRY(cudaMemset(q->d_seg[b], 0, (size_t)q->seg_alloc * sizeof(uint2)));
+    }
     QTRY(cudaMalloc(&q->d_ctl, sizeof(Ctl)));
     QTRY(cudaMallocHost(&q->h_ctl, sizeof(Ctl)));
     QTRY(cudaMalloc(&q->d_reach, (size_t)(q->W * 32 + 32)));
@@ -407,7 +413,7 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     int per_sm = 0;
     QTRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ssr_kernel, kThreads, q->smem));
     if (per_sm < 1) return bail(fail(RPQ_ECUDA, "step kernel cannot be resident"));
-    q->grid = std::min(g->sm_count * per_sm, kMaxCtas);  // one word-list region per CTA
+    q->grid = std::min(g->sm_count * per_sm, kShards);  // one queue shard per CTA
 #undef QTRY
     *out = q;
     return RPQ_OK;
@@ -435,14 +441,17 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     p.slot_nnz = q->d_slot_nnz;
     p.visited = q->d_visited;
     for (int f = 0; f < 3; ++f) p.fb[f] = q->d_fb[f];
-    for (int b = 0; b < 2; ++b) p.wl[b] = q->d_wl[b];
-    p.chunks = q->d_chunks;
+    for (int b = 0; b < 2; ++b) {
+        p.seg[b] = q->d_seg[b];
+        p.bun[b] = q->d_bun[b];
+    }
     p.ctl = q->d_ctl;
     p.reach = q->d_reach;
-    p.wl_cap = q->wl_cap;
-    p.wl_ovf_cap = q->wl_ovf_cap;
-    p.ch_cap = q->ch_cap;
-    p.ch_ovf_cap = q->ch_ovf_cap;
+    p.shard_segcap = q->shard_segcap;
+    p.shard_buncap = q->shard_buncap;
+    p.ovf_segcap = q->ovf_segcap;
+    p.ovf_buncap = q->ovf_buncap;
+    p.seg_alloc = q->seg_alloc;
     if (!(timeout_s >= 0) || std::isinf(timeout_s) || timeout_s > 1.0e9)
         p.budget_ns = ~0ull;
     else
@@ -494,8 +503,8 @@ int rpq_query_wait(rpq_query* q, rpq_stats* stats) {
         stats->iterations = c.iterations;
         stats->levels = c.levels;
         stats->grid = q->grid;
-        stats->te = (int64_t)c.te;
-        stats->segments = (int64_t)c.chunks;
+        stats->te = q->count_te ? (int64_t)c.te_exact : (int64_t)c.te_push;
+        stats->segments = (int64_t)c.segments;
         stats->visited_pairs = (int64_t)c.pairs;
         stats->reach_count = (int64_t)c.reach_count;
         stats->device_ms = ms;
@@ -512,7 +521,7 @@ int rpq_query_wait(rpq_query* q, rpq_stats* stats) {
     }
     if (c.status == ST_OVERFLOW) {
         if (stats) stats->status = RPQ_ECUDA;
-        return fail(RPQ_ECUDA, "internal: frontier word list or chunk buffer capacity exceeded");
+        return fail(RPQ_ECUDA, "internal: frontier queue capacity exceeded");
     }
     if (c.status == ST_DEADLOCK) {
         if (stats) stats->status = RPQ_ECUDA;

@@ -1,55 +1,52 @@
 // ssr_kernel.cuh -- the persistent sm_100a kernel that evaluates one
 // single-source 2-RPQ: the reference's whole evaluator loop
 //   P <- seed; while M: M <- (sum_a (N^a)^T x M x G^a) <not P>; P <- P + M
-// (rpq/engine.py:146-171, Alg. 1) in ONE cooperative launch.
+// (rpq/engine.py:146-171, Alg. 1) in ONE cooperative launch, one
+// grid barrier per BFS level.
 //
 // Layout:
-//   slot s    = (label, inverted) symbol; A_s = forward[l] or backward[l]
-//               (graph_store.py:87-91) as uint32 row pointers + int32 columns;
-//               A_s^T (the other direction) is what pull levels scan.
-//   group g   = (state q, slot s) with targets {q' : q -s-> q'}: one row of
-//               the transposed transition matrix (engine.py:102).
-//   P         = |Q| bitmaps of |V| bits.
-//   F_L       = 3 rotating bitmaps of the same shape (read L%3, write (L+1)%3,
-//               zero (L+2)%3), plus the list of F_L's NON-EMPTY 32-bit WORDS:
-//               whoever first sets a bit in a word of F_{L+1} appends the
-//               word.  Push levels iterate that list, so sparse levels cost
-//               O(|F|), and bitmaps give O(1) membership for pull levels.
+//   slot s          = (label, inverted) symbol; A_s = forward[l] or backward[l]
+//                     (graph_store.py:87-91) as uint32 rowptr + int32 columns;
+//                     A_s^T (the other direction) is what pull levels scan.
+//   group g         = (state q, slot s) with targets {q' : q -s-> q'}: one row
+//                     of the transposed transition matrix (engine.py:102).
+//   visited P       = |Q| bitmaps of |V| bits; frontier F_L = 3 rotating
+//                     bitmaps of the same shape (read L%3, write (L+1)%3,
+//                     zero (L+2)%3).
+//   push work queue = row SEGMENTS (start, len, group) cut into BUNDLES of
+//                     <= 32 edges, double-buffered by level parity, written
+//                     by the warp that discovers a pair (sharded counters).
 //
-// A level is one epoch (plus a chunk epoch when some rows are too long for
-// one warp) and one grid barrier per epoch:
-//   push: a warp takes 32 listed words, expands their set bits 32 frontier
-//         items at a time -- row pointers of all groups in flight, then the
-//         items' edges kEPL per lane -- and claims (q', w) with atomicOr on P.
-//         Rows longer than kBigRow are cut into kChunk-edge chunks that every
-//         warp shares in the chunk epoch.
-//   pull: every unvisited (q', w) with a possible predecessor scans row w of
-//         A_s^T for a member of F_L[q], early exit; rows longer than
-//         kLongRow are chunked the same way.
-// mask_complement + or_sum of the reference (engine.py:159, :165) are the
-// atomicOr claim; np.unique's dedup (sparse_bool.py:250) is the bitmap.
-// The direction of each level follows Beamer's rule on the exact out-edge
-// count of the frontier (accumulated when pairs are discovered).
+// Per level the direction is push (expand the queue) or pull (every
+// unvisited (q', w) scans A_s^T row w for a frontier member of the source
+// state, early exit), chosen from the frontier's edge count against the
+// unvisited edge estimate (Beamer's rule).  Either way the result is the
+// same set: P only grows by (q', w) pairs with a frontier predecessor.
 #pragma once
 
 namespace rpqk {
 
-constexpr int kThreads = 1024;       // 32 warps per CTA, one CTA per SM
+constexpr int kThreads = 768;        // 24 warps per CTA, one CTA per SM
 constexpr int kMinBlocks = 1;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxCtas = 160;
+constexpr int kEdgesPerLane = 4;     // push: edges each lane expands per bundle
+constexpr int kBundle = 32 * kEdgesPerLane;  // edges per bundle; an emission pass has
+                                             // <= 32 segments, so a bundle spans <= 32
+constexpr int kPullVerts = 4;        // pull: vertices (words of 32) per lane per task
+constexpr int kShards = 160;         // queue shards, one per CTA (+1 overflow shard)
 constexpr int kMaxStates = 256;
-constexpr int kMaxGroups = 256;
+constexpr int kMaxGroups = 256;      // group id is 8 bits in a segment
 constexpr int kMaxSlots = 128;
-constexpr int kFastGroups = 4;       // groups per state expanded with all loads in flight
-constexpr int kEPL = 4;              // push: edges per lane per sub-round
-constexpr uint32_t kBigRow = 32;     // push rows longer than this become chunks
-constexpr uint32_t kChunk = 512;     // edges per chunk
-constexpr int kPullVerts = 4;        // pull: words (x32 vertices) per warp task
-constexpr int kPullInline = 2;       // in-edges each lane tests first
-constexpr int kPullStep = 4;         // in-edges per lane per medium-row step
-constexpr uint32_t kLongRow = 32;    // pull rows longer than this (after inline) become chunks
+constexpr uint32_t kSegLenMax = (1u << 24) - 1;
+constexpr int kFastGroups = 4;       // emission: groups per state handled in one pass
+// bundle = uint2 {x, y}; y bit 31 = inline, bits 0..6 = edges - 1,
+//   inline  : x = column offset of the first edge, y bits 7..14 = group
+//   indirect: x = index of the first segment, y bits 7..30 = offset into it
+// a hole (bundle slot left empty by a spill) has y = 0xFFFFFFFF
+constexpr uint32_t kHoleY = 0xFFFFFFFFu;
+constexpr uint32_t kInline = 0x80000000u;
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int kPullInline = 2;       // in-edges each lane tests before warp help
 
 constexpr int ST_OVERFLOW = 100;
 constexpr int ST_DEADLOCK = 101;
@@ -62,68 +59,69 @@ struct Slot {
     const int32_t* col;
 };
 
-// Per-frontier counters, rotating over 3 sets by level: the set of F_L is
-// produced during level L-1, read by every CTA after the barrier that ends
-// level L-1, and reset by CTA 0 during level L+1.  Every CTA reads the same
-// values and so takes the same decisions: no serial section, no broadcast.
-struct LCnt {
-    unsigned long long nnew;      // |F_L|
-    unsigned long long mf;        // sum over F_L of out-degree x targets (TE share)
-    unsigned long long wl_ovf;    // entries in the word list's overflow region
-    unsigned long long ch_ovf;    // chunks in the chunk buffer's overflow region
+// Counters are never reset while anyone may still read them: queue counters
+// rotate over 3 sets by barrier epoch e (produced in epoch e-1, read after
+// barrier e, reset in epoch e+1), frontier statistics over 3 sets by level.
+// Every CTA reads the same values after a barrier and so takes the same
+// decision: no serial section, no broadcast.
+struct QCnt {
+    unsigned long long shard[kShards + 1];  // (segments << 32) | bundles
+    unsigned long long edges;               // push-model edges emitted
     unsigned int overflow;
-    unsigned int expire;          // 1 + level whose deadline check failed
-    unsigned int wl_cta[kMaxCtas];  // word-list fill of each CTA's region
-    unsigned int ch_cta[kMaxCtas];  // chunk fill of each CTA's region
-    unsigned int state[kMaxStates]; // |F_L| per state
+    unsigned int expire;                    // 1 + level whose deadline check failed
+};
+
+struct FCnt {
+    unsigned long long nnew;                // |F_L|
+    unsigned int state[kMaxStates];         // |F_L| per state
 };
 
 struct Ctl {
-    unsigned int bar;  // monotonic barrier arrivals
+    unsigned int bar;        // monotonic barrier arrivals
     int abort;
     unsigned long long t0;
-    LCnt lc[3];
+    QCnt qc[3];
+    FCnt fc[3];
     // results, written by CTA 0 only
     int status;
     int iterations;
     int levels;
     int pull_levels;
-    unsigned long long te;
-    unsigned long long chunks;
+    unsigned long long te_push;
+    unsigned long long te_exact;
+    unsigned long long segments;
     unsigned long long pairs;
     unsigned long long reach_count;
     long long level_new[64];
     long long level_edges[64];
     unsigned long long level_ns[64];
-    unsigned long long work_ns[64];  // latest CTA finishing level L's main epoch (from t0)
-    unsigned long long bar_ns[64];   // CTA 0 past the last barrier of level L
+    unsigned long long work_ns[64];  // latest CTA finishing level L's work (from t0)
+    unsigned long long bar_ns[64];   // CTA 0 leaving the barrier after level L
     int level_dir[64];
 };
 
 struct Params {
     const int32_t* tables;
-    const Slot* slots;  // A_s, then A_s^T at [nslots, 2*nslots)
+    const Slot* slots;       // A_s, then A_s^T at [nslots, 2*nslots)
     const unsigned long long* slot_nnz;
     uint32_t* visited;
     uint32_t* fb[3];
-    uint2* wl[2];       // word lists {q, word} by level parity
-    uint4* chunks;      // long-row chunks of the current level (CTA regions + overflow)
+    uint2* seg[2];
+    uint2* bun[2];
     Ctl* ctl;
     uint8_t* reach;
-    unsigned long long wl_cap;      // entries per CTA region
-    unsigned long long wl_ovf_cap;  // entries in the overflow region
-    unsigned long long ch_cap;      // chunks per CTA region
-    unsigned long long ch_ovf_cap;  // chunks in the overflow region
+    unsigned long long shard_segcap, shard_buncap, ovf_segcap, ovf_buncap;
+    unsigned long long seg_alloc;
     unsigned long long budget_ns;
-    long long W;  // words per bitmap row (multiple of 4)
+    long long W;             // words per bitmap row (multiple of 4)
     int nv;
     int nstates, ngroups, nslots, ntargets, nstarts, nfinals, nin;
     int maxT;
     int source;
     int table_ints;
-    int dir_mode;  // 0 auto, 1 push only, 2 pull only
-    int count_te;  // kept for the ABI; TE is always exact now
-    float alpha;   // pull when m_f * alpha > m_u
+    int dir_mode;            // 0 auto, 1 push only, 2 pull after the seed
+    int count_te;
+    float alpha;             // pull when m_f * alpha > m_u
 };
 
 struct Smem {
@@ -144,6 +142,9 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -159,6 +160,7 @@ template <typename T>
 __device__ __forceinline__ T ldcg(const T* p) {
     return __ldcg(p);
 }
+
 __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
@@ -169,6 +171,15 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
     for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
     return v;
 }
+__device__ __forceinline__ unsigned long long warp_incl_scan_u64(unsigned long long v, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        unsigned long long o = __shfl_up_sync(FULL, v, d);
+        if (lane >= d) v += o;
+    }
+    return v;
+}
+
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -177,6 +188,7 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
     }
     return v;
 }
+
 // largest lane j with key_j <= x (key non-decreasing across lanes, key_0 <= x)
 __device__ __forceinline__ int warp_upper_lane(uint32_t key, uint32_t x) {
     int j = 0;
@@ -189,14 +201,14 @@ __device__ __forceinline__ int warp_upper_lane(uint32_t key, uint32_t x) {
     return j;
 }
 
-// What every thread of a CTA needs after a barrier (warp 0 derives it from
-// the global counters; every CTA derives the same values).
+// What every thread of a CTA needs to know after a barrier (warp 0 derives it
+// from the global counters; all CTAs derive the same values).
 struct View {
     int done;
-    int dir;
+    int dir;        // direction of the level about to run
+    int plan;       // push level whose queue must first be emitted from F_L
     int status;
     int iterations;
-    unsigned long long nwl;  // F_L's listed words (regions + overflow)
 };
 
 // Grid barrier for a cooperative launch over a monotonic arrival counter:
@@ -228,278 +240,349 @@ __device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned epoch) {
     __syncthreads();
 }
 
-// Per-CTA context of the frontier being built.
-struct Ctx {
-    LCnt* lc;           // counters of F_{L+1}
-    uint2* wl;          // its word list
-    uint32_t* fnext;    // its bitmap
-    unsigned* s_wl;     // this CTA's word-list fill (smem)
-    unsigned* s_ch;     // this CTA's chunk fill (smem)
-    unsigned* s_state;  // this CTA's discoveries per state (smem)
+// Reservation of `nseg` segments and `nb` bundles (one lane).  Each CTA owns
+// queue shard blockIdx.x and reserves in it with a shared-memory counter
+// (published to the global shard counter once per epoch by flush_counts);
+// a reservation that does not fit spills to the overflow shard through a
+// global atomic, and the part of its bundle range inside the CTA's shard,
+// [*hole_lo, *hole_hi), must then be filled with holes (y = kHoleY).
+__device__ __forceinline__ bool reserve(const Params& p, unsigned long long* s_resv, QCnt* qc,
+                                        uint32_t nseg, uint32_t nb, unsigned long long* seg_idx,
+                                        unsigned long long* bun_idx, unsigned long long* hole_lo,
+                                        unsigned long long* hole_hi) {
+    const int shard = blockIdx.x;
+    const unsigned long long inc = ((unsigned long long)nseg << 32) | nb;
+    const unsigned long long old = atomicAdd(s_resv, inc);
+    const unsigned long long s_loc = old >> 32, b_loc = old & 0xFFFFFFFFull;
+    *hole_lo = *hole_hi = 0;
+    if (s_loc + nseg <= p.shard_segcap && b_loc + nb <= p.shard_buncap) {
+        *seg_idx = (unsigned long long)shard * p.shard_segcap + s_loc;
+        *bun_idx = (unsigned long long)shard * p.shard_buncap + b_loc;
+        return true;
+    }
+    if (b_loc < p.shard_buncap) {
+        *hole_lo = (unsigned long long)shard * p.shard_buncap + b_loc;
+        *hole_hi = (unsigned long long)shard * p.shard_buncap +
+                   (b_loc + nb < p.shard_buncap ? b_loc + nb : p.shard_buncap);
+    }
+    const unsigned long long o2 = atomicAdd(&qc->shard[kShards], inc);
+    const unsigned long long s2 = o2 >> 32, b2 = o2 & 0xFFFFFFFFull;
+    if (s2 + nseg <= p.ovf_segcap && b2 + nb <= p.ovf_buncap) {
+        *seg_idx = (unsigned long long)kShards * p.shard_segcap + s2;
+        *bun_idx = (unsigned long long)kShards * p.shard_buncap + b2;
+        return true;
+    }
+    return false;
+}
+
+// Where an epoch's emission goes.
+struct Out {
+    QCnt* qc;
+    uint2* seg;
+    uint2* bun;
+    unsigned long long* s_resv;  // this CTA's shard fill: (segments << 32) | bundles
 };
 
-// Warp-cooperative append of up to N (q, word) entries per lane (app[i]) to
-// the word list: the CTA's region first, the overflow region for what does
-// not fit.  One shared-memory atomic per call.
-template <int N>
-__device__ __forceinline__ void wl_append(const Params& p, const Ctx& c, const bool* app, const int* q,
-                                          const int* w, int lane) {
-    unsigned mine = 0;
+// Warp-cooperative emission of the row segments of (state q, vertex w) pairs
+// (one candidate per lane).  Returns the edges emitted.
+__device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, const Out& o, bool valid,
+                                               int q, int w, int lane) {
+    const unsigned vmask = __ballot_sync(FULL, valid);
+    if (vmask == 0) return 0;
+    const int ng = valid ? (S.gbeg[q + 1] - S.gbeg[q]) : 0;
+    int maxng = ng;
 #pragma unroll
-    for (int i = 0; i < N; ++i) mine += app[i] ? 1u : 0u;
-    const unsigned incl = warp_incl_scan(mine, lane);
-    const unsigned n = __shfl_sync(FULL, incl, 31);
-    if (n == 0) return;
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(c.s_wl, n);
-    base = __shfl_sync(FULL, base, 0);
-    const unsigned long long cap = p.wl_cap;
-    const unsigned fit = base >= cap ? 0u : (unsigned)min((unsigned long long)n, cap - base);
-    unsigned long long ob = 0;
-    if (fit < n) {
-        if (lane == 0) ob = atomicAdd(&c.lc->wl_ovf, (unsigned long long)(n - fit));
-        ob = __shfl_sync(FULL, ob, 0);
-        if (ob + (n - fit) > p.wl_ovf_cap) {
-            if (lane == 0) atomicExch(&c.lc->overflow, 1u);
-            return;
-        }
-    }
-    unsigned r = incl - mine;
+    for (int d = 16; d >= 1; d >>= 1) maxng = max(maxng, __shfl_xor_sync(FULL, maxng, d));
+    if (maxng <= kFastGroups) {
+        // all groups' row pointers in flight together, one reservation
+        uint32_t lo[kFastGroups], deg[kFastGroups];
+        int g[kFastGroups];
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-        if (!app[i]) continue;
-        const uint2 ent = make_uint2((uint32_t)q[i], (uint32_t)(w[i] >> 5));
-        if (r < fit)
-            c.wl[(unsigned long long)blockIdx.x * cap + base + r] = ent;
-        else
-            c.wl[(unsigned long long)kMaxCtas * cap + ob + (r - fit)] = ent;
-        ++r;
-    }
-}
-
-// Out-degree x targets of (q[i], w[i]) over their groups, for N pairs per
-// lane (q < 0: none), with every row-pointer load in flight together: each
-// pair's share of TE / m_f.
-template <int N>
-__device__ __forceinline__ unsigned long long out_edges(const Smem& S, const int* q, const int* w) {
-    unsigned long long s = 0;
-    int ng[N];
-    int maxg = 0;
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-        ng[i] = q[i] >= 0 ? S.gbeg[q[i] + 1] - S.gbeg[q[i]] : 0;
-        maxg = max(maxg, ng[i]);
-    }
-    constexpr int G = 2;  // groups per batch (register budget)
-    for (int k0 = 0; k0 < maxg; k0 += G) {
-        uint32_t lo[N][G], hi[N][G];
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-            for (int k = 0; k < G; ++k) {
-                lo[i][k] = hi[i][k] = 0;
-                if (k0 + k < ng[i]) {
-                    const Slot sl = S.slots[S.gslot[S.gbeg[q[i]] + k0 + k]];
-                    lo[i][k] = __ldg(sl.rowptr + w[i]);
-                    hi[i][k] = __ldg(sl.rowptr + w[i] + 1);
-                }
-            }
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-            for (int k = 0; k < G; ++k)
-                if (k0 + k < ng[i]) {
-                    const int g = S.gbeg[q[i]] + k0 + k;
-                    s += (unsigned long long)(hi[i][k] - lo[i][k]) * (unsigned long long)(S.toff[g + 1] - S.toff[g]);
-                }
-    }
-    return s;
-}
-
-// Bookkeeping of freshly claimed pairs (N per lane, fresh[i]): F bit (and a
-// word-list entry when the word was empty), counts, out-edge total.  With
-// set_f false the caller already wrote F and tells which words to list.
-template <int N>
-__device__ __forceinline__ void record_fresh(const Params& p, const Smem& S, const Ctx& c, const bool* fresh,
-                                             const int* q, const int* w, int lane, unsigned long long& nnew,
-                                             unsigned long long& mf) {
-    bool app[N];
-    int qq[N];
-    uint32_t old[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-        old[i] = 1;
-        if (fresh[i]) old[i] = atomicOr(c.fnext + (long long)q[i] * p.W + (w[i] >> 5), 1u << (w[i] & 31));
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-        app[i] = fresh[i] && old[i] == 0;
-        qq[i] = fresh[i] ? q[i] : -1;
-        if (fresh[i]) {
-            nnew += 1;
-            atomicAdd(&c.s_state[q[i]], 1u);
-        }
-    }
-    mf += out_edges<N>(S, qq, w);
-    wl_append<N>(p, c, app, q, w, lane);
-}
-
-// Claim every (target of group g[u], w[u]) not yet in P; kEPL edges per lane
-// (g < 0: no edge).  Probes, claims and bookkeeping each keep all kEPL
-// operations in flight.
-__device__ __forceinline__ void claim_edges(const Params& p, const Smem& S, const Ctx& c, const int* w,
-                                            const int* g, int lane, unsigned long long& nnew,
-                                            unsigned long long& mf) {
-    for (int k = 0; k < p.maxT; ++k) {
-        uint32_t old[kEPL];
-        int q2[kEPL];
-#pragma unroll
-        for (int u = 0; u < kEPL; ++u) {
-            q2[u] = -1;
-            old[u] = 0xFFFFFFFFu;
-            if (g[u] >= 0) {
-                const int t0 = S.toff[g[u]];
-                if (t0 + k < S.toff[g[u] + 1]) {
-                    q2[u] = S.targets[t0 + k];
-                    old[u] = p.visited[(long long)q2[u] * p.W + (w[u] >> 5)];
-                }
+        for (int k = 0; k < kFastGroups; ++k) {
+            lo[k] = 0;
+            deg[k] = 0;
+            g[k] = 0;
+            if (k < ng) {
+                g[k] = S.gbeg[q] + k;
+                const Slot sl = S.slots[S.gslot[g[k]]];
+                lo[k] = __ldg(sl.rowptr + w);
+                deg[k] = __ldg(sl.rowptr + w + 1);
             }
         }
+        bool huge = false;
 #pragma unroll
-        for (int u = 0; u < kEPL; ++u) {
-            const uint32_t bit = 1u << (w[u] & 31);
-            if (q2[u] >= 0 && !(old[u] & bit))
-                old[u] = atomicOr(p.visited + (long long)q2[u] * p.W + (w[u] >> 5), bit);
-            else
-                old[u] = 0xFFFFFFFFu;
+        for (int k = 0; k < kFastGroups; ++k) {
+            deg[k] -= lo[k];
+            huge |= deg[k] > kSegLenMax;
         }
-        bool fresh[kEPL];
+        if (!__any_sync(FULL, huge)) {
+            uint32_t excl[kFastGroups], T[kFastGroups], nb[kFastGroups], nseg[kFastGroups];
+            int rank[kFastGroups];
+            uint32_t NS = 0, NB = 0, TT = 0;
 #pragma unroll
-        for (int u = 0; u < kEPL; ++u) fresh[u] = q2[u] >= 0 && !(old[u] & (1u << (w[u] & 31)));
-        if (__any_sync(FULL, fresh[0] || fresh[1] || fresh[2] || fresh[3]))
-            record_fresh<kEPL>(p, S, c, fresh, q2, w, lane, nnew, mf);
+            for (int k = 0; k < kFastGroups; ++k) {
+                if (k < maxng) {
+                    const unsigned m = __ballot_sync(FULL, deg[k] > 0);
+                    rank[k] = __popc(m & lanemask_lt());
+                    nseg[k] = (uint32_t)__popc(m);
+                    const uint32_t incl = warp_incl_scan(deg[k], lane);
+                    excl[k] = incl - deg[k];
+                    T[k] = __shfl_sync(FULL, incl, 31);
+                    nb[k] = (T[k] + kBundle - 1) / kBundle;
+                    NS += nseg[k];
+                    NB += nb[k];
+                    TT += T[k];
+                } else {
+                    rank[k] = 0;
+                    nseg[k] = nb[k] = T[k] = excl[k] = 0;
+                }
+            }
+            if (NB == 0) return 0;
+            unsigned long long sbase = 0, bbase = 0, hlo = 0, hhi = 0;
+            int ok = 1;
+            if (lane == 0) ok = reserve(p, o.s_resv, o.qc, NS, NB, &sbase, &bbase, &hlo, &hhi) ? 1 : 0;
+            ok = __shfl_sync(FULL, ok, 0);
+            hlo = __shfl_sync(FULL, hlo, 0);
+            hhi = __shfl_sync(FULL, hhi, 0);
+            for (unsigned long long h = hlo + lane; h < hhi; h += 32) o.bun[h] = make_uint2(0u, kHoleY);
+            if (!ok) {
+                if (lane == 0) atomicExch(&o.qc->overflow, 1u);
+                return 0;
+            }
+            sbase = __shfl_sync(FULL, sbase, 0);
+            bbase = __shfl_sync(FULL, bbase, 0);
+#pragma unroll
+            for (int k = 0; k < kFastGroups; ++k) {
+                if (k >= maxng) break;
+                if (nb[k] == 0) continue;
+                bool need_seg = false;
+                for (uint32_t kb0 = 0; kb0 < nb[k]; kb0 += 32) {
+                    const uint32_t kb = kb0 + lane;
+                    const uint32_t pos = kb * kBundle;
+                    const uint32_t cnt = kb < nb[k] ? min((uint32_t)kBundle, T[k] - pos) : 1u;
+                    const uint32_t first = min(pos, T[k] - 1);
+                    const int j = warp_upper_lane(excl[k], first);
+                    const int jl = warp_upper_lane(excl[k], min(pos + cnt - 1, T[k] - 1));
+                    const uint32_t exj = __shfl_sync(FULL, excl[k], j);
+                    const int rj = __shfl_sync(FULL, rank[k], j);
+                    const uint32_t loj = __shfl_sync(FULL, lo[k], j);
+                    const int gj = __shfl_sync(FULL, g[k], j);
+                    if (kb < nb[k]) {
+                        uint2 bd;
+                        if (j == jl) {  // within one row: carry the row offset inline
+                            bd = make_uint2(loj + (pos - exj), kInline | ((uint32_t)gj << 7) | (cnt - 1));
+                        } else {
+                            bd = make_uint2((uint32_t)(sbase + rj), ((pos - exj) << 7) | (cnt - 1));
+                            need_seg = true;
+                        }
+                        o.bun[bbase + kb] = bd;
+                    }
+                }
+                if (__any_sync(FULL, need_seg) && deg[k] > 0)
+                    o.seg[sbase + rank[k]] = make_uint2(lo[k], (deg[k] << 8) | (uint32_t)g[k]);
+                sbase += nseg[k];
+                bbase += nb[k];
+            }
+            return TT;
+        }
     }
+    uint32_t emitted = 0;
+    for (int k = 0; k < maxng; ++k) {
+        uint32_t lo = 0, deg = 0;
+        int g = 0;
+        if (k < ng) {
+            g = S.gbeg[q] + k;
+            const Slot sl = S.slots[S.gslot[g]];
+            lo = __ldg(sl.rowptr + w);
+            deg = __ldg(sl.rowptr + w + 1) - lo;
+        }
+        for (;;) {  // rows longer than a segment are split (rare)
+            const uint32_t take = min(deg, kSegLenMax);
+            const bool hs = take > 0;
+            const unsigned m = __ballot_sync(FULL, hs);
+            if (m == 0) break;
+            const int rank = __popc(m & lanemask_lt());
+            const uint32_t nseg = (uint32_t)__popc(m);
+            const uint32_t incl = warp_incl_scan(take, lane);
+            const uint32_t excl = incl - take;
+            const uint32_t T = __shfl_sync(FULL, incl, 31);
+            const uint32_t nb = (T + kBundle - 1) / kBundle;
+            unsigned long long sbase = 0, bbase = 0, hlo = 0, hhi = 0;
+            int ok = 1;
+            if (lane == 0) ok = reserve(p, o.s_resv, o.qc, nseg, nb, &sbase, &bbase, &hlo, &hhi) ? 1 : 0;
+            ok = __shfl_sync(FULL, ok, 0);
+            hlo = __shfl_sync(FULL, hlo, 0);
+            hhi = __shfl_sync(FULL, hhi, 0);
+            for (unsigned long long h = hlo + lane; h < hhi; h += 32) o.bun[h] = make_uint2(0u, kHoleY);
+            if (!ok) {
+                if (lane == 0) atomicExch(&o.qc->overflow, 1u);
+                return emitted;
+            }
+            sbase = __shfl_sync(FULL, sbase, 0);
+            bbase = __shfl_sync(FULL, bbase, 0);
+            if (hs) o.seg[sbase + rank] = make_uint2(lo, (take << 8) | (uint32_t)g);
+            for (uint32_t kb0 = 0; kb0 < nb; kb0 += 32) {
+                const uint32_t kb = kb0 + lane;
+                const uint32_t pos = kb * kBundle;
+                const int j = warp_upper_lane(excl, min(pos, T - 1));
+                const uint32_t exj = __shfl_sync(FULL, excl, j);
+                const int rj = __shfl_sync(FULL, rank, j);
+                if (kb < nb) {
+                    const uint32_t cnt = min((uint32_t)kBundle, T - pos);
+                    o.bun[bbase + kb] = make_uint2((uint32_t)(sbase + rj), ((pos - exj) << 7) | (cnt - 1));
+                }
+            }
+            emitted += T;
+            lo += take;
+            deg -= take;
+        }
+    }
+    return emitted;
 }
 
-// Warp-cooperative append of the kChunk-edge chunks of long rows (lanes with
-// `big`): the CTA's region first, the overflow region for what does not fit.
-__device__ __forceinline__ void add_chunks(const Params& p, const Ctx& c, bool big, uint32_t start, uint32_t len,
-                                           uint32_t a, uint32_t b, int lane) {
-    if (!__any_sync(FULL, big)) return;
-    const unsigned mine = big ? (len + kChunk - 1) / kChunk : 0u;
-    const unsigned incl = warp_incl_scan(mine, lane);
-    const unsigned n = __shfl_sync(FULL, incl, 31);
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(c.s_ch, n);
-    base = __shfl_sync(FULL, base, 0);
-    const unsigned long long cap = p.ch_cap;
-    const unsigned fit = base >= cap ? 0u : (unsigned)min((unsigned long long)n, cap - base);
-    unsigned long long ob = 0;
-    if (fit < n) {
-        if (lane == 0) ob = atomicAdd(&c.lc->ch_ovf, (unsigned long long)(n - fit));
-        ob = __shfl_sync(FULL, ob, 0);
-        if (ob + (n - fit) > p.ch_ovf_cap) {
-            if (lane == 0) atomicExch(&c.lc->overflow, 1u);
-            return;
+// Per-warp staging of discovered pairs so that emission passes are full
+// (<= 63 staged; a pass emits 32).
+struct Stage {
+    int* q;  // smem [64]
+    int* w;  // smem [64]
+    int n;
+};
+
+__device__ __forceinline__ uint32_t stage_add(const Params& p, const Smem& S, const Out& o, Stage& st,
+                                              bool fresh, int q, int w, int lane) {
+    const unsigned m = __ballot_sync(FULL, fresh);
+    if (!m) return 0;
+    if (fresh) {
+        const int pos = st.n + __popc(m & lanemask_lt());
+        st.q[pos] = q;
+        st.w[pos] = w;
+    }
+    st.n += __popc(m);
+    __syncwarp();
+    uint32_t T = 0;
+    if (st.n >= 32) {
+        const int qq = st.q[lane], ww = st.w[lane];
+        __syncwarp();
+        T = emit_pairs(p, S, o, true, qq, ww, lane);
+        const int rem = st.n - 32;
+        int tq = 0, tw = 0;
+        if (lane < rem) {
+            tq = st.q[32 + lane];
+            tw = st.w[32 + lane];
         }
+        __syncwarp();
+        if (lane < rem) {
+            st.q[lane] = tq;
+            st.w[lane] = tw;
+        }
+        st.n = rem;
+        __syncwarp();
     }
-    unsigned r = incl - mine;
-    for (unsigned i = 0; i < mine; ++i, ++r) {
-        const uint32_t off = i * kChunk;
-        const uint4 ent = make_uint4(start + off, min(kChunk, len - off), a, b);
-        if (r < fit)
-            p.chunks[(unsigned long long)blockIdx.x * cap + base + r] = ent;
-        else
-            p.chunks[(unsigned long long)kMaxCtas * cap + ob + (r - fit)] = ent;
-    }
+    return T;
 }
 
-// End-of-epoch flush of a CTA's counts: one atomic per CTA and counter, and
-// the CTA's word-list fill.  Call after __syncthreads().
-__device__ __forceinline__ void flush_counts(const Ctx& c, unsigned long long nnew, unsigned long long mf,
-                                             unsigned long long* red, int nstates) {
+__device__ __forceinline__ uint32_t stage_flush(const Params& p, const Smem& S, const Out& o, Stage& st,
+                                                int lane) {
+    if (st.n == 0) return 0;
+    const bool v = lane < st.n;
+    const int qq = v ? st.q[lane] : 0, ww = v ? st.w[lane] : 0;
+    __syncwarp();
+    st.n = 0;
+    return emit_pairs(p, S, o, v, qq, ww, lane);
+}
+
+// End-of-epoch flush of a CTA's counts: one atomic per CTA and counter.
+__device__ __forceinline__ void flush_counts(unsigned long long* nnew_dst, const Out& o,
+                                             unsigned int* state_dst, unsigned long long nnew,
+                                             unsigned long long nedge, unsigned long long* red,
+                                             unsigned int* s_state, int nstates) {
+    unsigned long long* edges_dst = &o.qc->edges;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     nnew = warp_sum_u64(nnew);
-    mf = warp_sum_u64(mf);
+    nedge = warp_sum_u64(nedge);
     if (lane == 0) {
         red[2 * wid] = nnew;
-        red[2 * wid + 1] = mf;
+        red[2 * wid + 1] = nedge;
     }
     __syncthreads();
     if (wid == 0) {
         unsigned long long a = lane < kWarps ? red[2 * lane] : 0ull;
-        unsigned long long b = lane < kWarps ? red[2 * lane + 1] : 0ull;
+        unsigned long long c = lane < kWarps ? red[2 * lane + 1] : 0ull;
         a = warp_sum_u64(a);
-        b = warp_sum_u64(b);
-        if (lane == 0) {
-            if (a) atomicAdd(&c.lc->nnew, a);
-            if (b) atomicAdd(&c.lc->mf, b);
-            c.lc->wl_cta[blockIdx.x] = *c.s_wl;
-            c.lc->ch_cta[blockIdx.x] = *c.s_ch;
+        c = warp_sum_u64(c);
+        if (lane == 0 && a && nnew_dst) atomicAdd(nnew_dst, a);
+        if (lane == 0 && c) atomicAdd(edges_dst, c);
+        if (lane == 0) {  // publish this CTA's shard fill (the local counter may exceed capacity)
+            o.qc->shard[blockIdx.x] = *o.s_resv;
+            *o.s_resv = 0;
         }
     }
-    for (int q = threadIdx.x; q < nstates; q += blockDim.x) {
-        const unsigned int v = c.s_state[q];
-        if (v) {
-            atomicAdd(&c.lc->state[q], v);
-            c.s_state[q] = 0;
+    if (state_dst)
+        for (int q = threadIdx.x; q < nstates; q += blockDim.x) {
+            const unsigned int c = s_state[q];
+            if (c) {
+                atomicAdd(&state_dst[q], c);
+                s_state[q] = 0;
+            }
         }
-    }
 }
 
-// Exclusive prefix of per-CTA region fills (clamped to the region capacity)
-// into s_pre[0..gridDim.x]; returns the total.  Warp-cooperative.
-__device__ __forceinline__ unsigned region_prefix(const unsigned* fill, unsigned long long cap, unsigned* s_pre,
-                                                  int lane) {
-    constexpr int R = (kMaxCtas + 31) / 32;
-    unsigned cnt[R];
+// Totals of the queue produced in the previous epoch, and the per-shard
+// bundle prefix the consumers index with.  Warp-cooperative (warp 0).
+__device__ __forceinline__ void queue_scan(const Params& p, const QCnt* qc, int lane,
+                                           unsigned long long* s_bpre, unsigned long long* nbun,
+                                           unsigned long long* nseg) {
+    constexpr int R = (kShards + 1 + 31) / 32;
+    unsigned long long c[R], sc[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int cc = 32 * r + lane;
-        cnt[r] = cc < (int)gridDim.x ? (unsigned)min((unsigned long long)ldcg(&fill[cc]), cap) : 0u;
+    for (int r = 0; r < R; ++r) {  // issue all loads first
+        const int sh = 32 * r + lane;
+        const unsigned long long v = sh <= kShards ? ldcg(&qc->shard[sh]) : 0ull;
+        const unsigned long long bcap = sh < kShards ? p.shard_buncap : p.ovf_buncap;
+        const unsigned long long scap = sh < kShards ? p.shard_segcap : p.ovf_segcap;
+        c[r] = min(v & 0xFFFFFFFFull, bcap);
+        sc[r] = min(v >> 32, scap);
     }
-    unsigned carry = 0;
+    unsigned long long carry = 0, segs = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int cc = 32 * r + lane;
-        const unsigned incl = warp_incl_scan(cnt[r], lane);
-        if (cc <= (int)gridDim.x) s_pre[cc] = carry + incl - cnt[r];
+        const int sh = 32 * r + lane;
+        const unsigned long long incl = warp_incl_scan_u64(c[r], lane);
+        if (sh <= kShards) s_bpre[sh] = carry + incl - c[r];
         carry += __shfl_sync(FULL, incl, 31);
+        segs += sc[r];
     }
-    return carry;
+    if (lane == 0) s_bpre[kShards + 1] = carry;
+    *nbun = carry;
+    *nseg = warp_sum_u64(segs);
 }
 
-// Region holding global index idx < s_pre[gridDim.x] (binary search in smem).
-__device__ __forceinline__ int region_of(const unsigned* s_pre, unsigned long long idx) {
-    int r = 0;
-#pragma unroll
-    for (int h = 128; h >= 1; h >>= 1)
-        if (r + h < (int)gridDim.x && s_pre[r + h] <= idx) r += h;
-    return r;
-}
-
-// Decision after F_L has been built (warp 0 of every CTA; every CTA reads the
-// same counters and reaches the same result).  Mirrors the masked loop
-// (engine.py:156-160): run while the frontier is non-empty, check the
-// deadline, then step; and picks the direction of level L.
-__device__ void decide_level(const Params& p, const Smem& S, int L, int lane, View* v, unsigned* s_wpre,
-                             unsigned long long* s_sv, unsigned int* s_front) {
+// Decision after frontier F_L has been produced (warp 0 of every CTA; every
+// CTA reads the same counters and reaches the same result).  Mirrors the
+// masked loop (engine.py:156-160): run while the frontier is non-empty,
+// check the deadline, then step; and picks the direction of level L.
+__device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, int prev_dir, int lane,
+                             View* v, unsigned long long* s_bpre, unsigned long long* s_sv,
+                             unsigned int* s_front) {
     Ctl* ctl = p.ctl;
-    const LCnt* lc = &ctl->lc[L % 3];
-    const unsigned long long nnew = ldcg(&lc->nnew);
-    const unsigned long long mf = ldcg(&lc->mf);
-    const unsigned long long wovf = ldcg(&lc->wl_ovf);
-    const unsigned int overflow = ldcg(&lc->overflow);
-    const unsigned int expire = ldcg(&lc->expire);
+    const QCnt* qc = &ctl->qc[e % 3];
+    const FCnt* fc = &ctl->fc[L % 3];
+    const unsigned long long nnew = ldcg(&fc->nnew);
+    const unsigned long long nedge = ldcg(&qc->edges);
+    const unsigned int overflow = ldcg(&qc->overflow);
+    const unsigned int expire = ldcg(&qc->expire);
     const int abort = ldcg(&ctl->abort);
-    const unsigned carry = region_prefix(lc->wl_cta, p.wl_cap, s_wpre, lane);
+    unsigned long long nbun, nseg;
+    queue_scan(p, qc, lane, s_bpre, &nbun, &nseg);
     for (int q = lane; q < p.nstates; q += 32) {
-        const unsigned int f = ldcg(&lc->state[q]);
+        const unsigned int f = ldcg(&fc->state[q]);
         s_front[q] = f;
         s_sv[q] += f;
     }
     __syncwarp();
-    int done = 0, iterations = 0, status = 0, next = DIR_PUSH;
+    const int produced_by_push = (L == 0) || prev_dir == DIR_PUSH;
+    int done = 0, iterations = 0, status = 0, next = DIR_PUSH, plan = 0;
+    long long ledges = -1;
     if (abort) {
         status = ST_DEADLOCK;
         done = 1;
@@ -514,48 +597,65 @@ __device__ void decide_level(const Params& p, const Smem& S, int L, int lane, Vi
     } else if (nnew == 0) {
         iterations = L;
         done = 1;
-    } else if (mf == 0) {
-        iterations = L + 1;  // nothing to expand: the next step is empty
-        done = 1;
     } else {
         if (p.dir_mode == 2) {
             next = DIR_PULL;
         } else if (p.dir_mode == 0) {
-            // m_u: in-edges of unvisited targets whose source state has a
-            // frontier.  Pull when m_f * alpha > m_u (Beamer's rule).
+            // m_f: edges out of F_L (exact after a push level, estimated from
+            // average degrees after a pull level); m_u: in-edges of unvisited
+            // targets whose source state has a frontier.  Pull when
+            // m_f * alpha > m_u (Beamer's rule; alpha tuned for these kernels).
             const double nv = (double)p.nv;
-            double mu = 0.0;
+            double mf = 0.0, mu = 0.0;
             for (int q = lane; q < p.nstates; q += 32) {
+                if (!produced_by_push && s_front[q])
+                    for (int g = S.gbeg[q]; g < S.gbeg[q + 1]; ++g)
+                        mf += (double)s_front[q] * (double)p.slot_nnz[S.gslot[g]] / nv;
                 const double unvis = nv - (double)s_sv[q];
                 for (int k = S.ibeg[q]; k < S.ibeg[q + 1]; ++k)
                     if (s_front[S.isrc[k]]) mu += (double)p.slot_nnz[S.islot[k]] * unvis / nv;
             }
+            mf = produced_by_push ? (double)nedge : warp_sum_f64(mf);
             mu = warp_sum_f64(mu);
-            next = ((double)mf * (double)p.alpha > mu) ? DIR_PULL : DIR_PUSH;
+            next = (mf * (double)p.alpha > mu) ? DIR_PULL : DIR_PUSH;
+        }
+        if (next == DIR_PUSH) {
+            if (produced_by_push) {
+                ledges = (long long)nedge;
+                if (nbun == 0) {  // nothing to expand: the next step is empty
+                    iterations = L + 1;
+                    done = 1;
+                }
+            } else {
+                plan = 1;  // emit F_L's queue from its bitmap first
+            }
         }
     }
     if (lane == 0) {
         v->done = done;
         v->dir = next;
+        v->plan = plan;
         v->status = status;
         v->iterations = iterations;
-        v->nwl = (unsigned long long)carry + wovf;
         if (blockIdx.x == 0) {  // results and statistics
             const unsigned long long now = globaltimer();
             ctl->pairs += nnew;
-            if (nnew && !status) ctl->te += mf;
             if (L < 64) {
                 ctl->level_new[L] = (long long)nnew;
                 ctl->level_ns[L] = now - ctl->t0;
-                ctl->level_edges[L] = (long long)mf;
+                ctl->level_edges[L] = ledges;
                 ctl->level_dir[L] = next;
             }
             if (!done) {
                 if (L > 0) ctl->levels = L;
                 if (next == DIR_PULL) ctl->pull_levels += 1;
+                if (next == DIR_PUSH && produced_by_push) {
+                    ctl->te_push += nedge;
+                    ctl->segments += nseg;
+                }
                 // _Clock.check at the top of iteration L (engine.py:87-89):
                 // recorded now, acted upon at the next decision by every CTA
-                if (now - ctl->t0 > p.budget_ns) ctl->lc[(L + 1) % 3].expire = (unsigned)L + 1;
+                if (now - ctl->t0 > p.budget_ns) ctl->qc[(e + 1) % 3].expire = (unsigned)L + 1;
             } else {
                 ctl->status = status;
                 ctl->iterations = iterations;
@@ -564,65 +664,81 @@ __device__ void decide_level(const Params& p, const Smem& S, int L, int lane, Vi
     }
 }
 
-__device__ __forceinline__ void reset_lc(LCnt* lc, int tid) {
-    for (int i = tid; i < kMaxCtas; i += kThreads) {
-        lc->wl_cta[i] = 0;
-        lc->ch_cta[i] = 0;
+// Decision after a plan epoch emitted F_L's queue.
+__device__ void decide_plan(const Params& p, unsigned e, int L, int lane, View* v, unsigned long long* s_bpre) {
+    Ctl* ctl = p.ctl;
+    const QCnt* qc = &ctl->qc[e % 3];
+    const unsigned long long nedge = ldcg(&qc->edges);
+    const unsigned int overflow = ldcg(&qc->overflow);
+    const unsigned int expire = ldcg(&qc->expire);
+    const int abort = ldcg(&ctl->abort);
+    unsigned long long nbun, nseg;
+    queue_scan(p, qc, lane, s_bpre, &nbun, &nseg);
+    int done = 0, status = 0, iterations = 0;
+    if (abort) {
+        status = ST_DEADLOCK;
+        done = 1;
+    } else if (overflow) {
+        status = ST_OVERFLOW;
+        iterations = L;
+        done = 1;
+    } else if (expire) {
+        status = RPQ_ETIMEOUT;
+        iterations = (int)expire - 1;
+        done = 1;
+    } else if (nbun == 0) {
+        iterations = L + 1;
+        done = 1;
     }
-    for (int i = tid; i < kMaxStates; i += kThreads) lc->state[i] = 0;
-    if (tid == 0) {
-        lc->nnew = 0;
-        lc->mf = 0;
-        lc->wl_ovf = 0;
-        lc->ch_ovf = 0;
-        lc->overflow = 0;
-        lc->expire = 0;
+    if (lane == 0) {
+        v->done = done;
+        v->plan = 0;
+        v->status = status;
+        v->iterations = iterations;
+        if (blockIdx.x == 0) {
+            if (L < 64) ctl->level_edges[L] = (long long)nedge;
+            ctl->te_push += nedge;
+            ctl->segments += nseg;
+            if (done) {
+                ctl->status = status;
+                ctl->iterations = iterations;
+            }
+        }
     }
 }
 
-// One pull scan of a medium row / chunk: any member of F (bitmap row frow)
-// among col[lo, hi)?  Warp-cooperative, 128 columns per step.
-__device__ __forceinline__ bool warp_row_hit(const int32_t* col, uint32_t lo, uint32_t hi, const uint32_t* frow,
-                                             int lane) {
-    for (uint32_t ed = lo; ed < hi; ed += 128) {
-        int uu[4];
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) uu[cc] = ed + 32 * cc + lane < hi ? __ldg(col + ed + 32 * cc + lane) : -1;
-        bool h = false;
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
-            if (uu[cc] >= 0) h |= (frow[uu[cc] >> 5] >> (uu[cc] & 31)) & 1u;
-        if (__ballot_sync(FULL, h)) return true;
+__device__ __forceinline__ void reset_qc(QCnt* qc, int tid) {
+    for (int i = tid; i <= kShards; i += kThreads) qc->shard[i] = 0;
+    if (tid == 0) {
+        qc->edges = 0;
+        qc->overflow = 0;
+        qc->expire = 0;
     }
-    return false;
 }
 
 __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ unsigned long long s_red[2 * kWarps];
-    __shared__ unsigned s_wpre[kMaxCtas + 1];       // F_L's word-list prefix over CTA regions
+    __shared__ unsigned long long s_bpre[kShards + 2];
     __shared__ unsigned long long s_sv[kMaxStates];  // |P| per state (same in every CTA)
     __shared__ unsigned int s_front[kMaxStates];     // |F_L| per state
     __shared__ unsigned int s_state[kMaxStates];     // this CTA's discoveries per state
     __shared__ int s_ptarget[kMaxStates];            // pull target states of this level
     __shared__ int s_nptarget;
-    __shared__ unsigned s_wl;                        // this CTA's word-list fill
-    __shared__ unsigned s_ch;                        // this CTA's chunk fill
-    __shared__ unsigned s_cpre[kMaxCtas + 1];        // chunk prefix over CTA regions
-    __shared__ unsigned long long s_nch;
-    __shared__ unsigned s_task;                      // push: next task in this CTA's range
     __shared__ View s_view;
+    __shared__ int s_stage[kWarps][2][64];
+    __shared__ unsigned long long s_resv;
 
     Slot* s_slots = reinterpret_cast<Slot*>(smem_raw);
     int32_t* s_tab = reinterpret_cast<int32_t*>(smem_raw + sizeof(Slot) * 2 * p.nslots);
     for (int i = threadIdx.x; i < 2 * p.nslots; i += blockDim.x) s_slots[i] = p.slots[i];
     for (int i = threadIdx.x; i < p.table_ints; i += blockDim.x) s_tab[i] = p.tables[i];
+    if (threadIdx.x == 0) s_resv = 0;
     for (int i = threadIdx.x; i < kMaxStates; i += blockDim.x) {
         s_state[i] = 0;
         s_sv[i] = 0;
         s_front[i] = 0;
     }
-    if (threadIdx.x == 0) s_wl = s_ch = 0;
     Smem S;
     S.slots = s_slots;
     S.gbeg = s_tab;
@@ -645,6 +761,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     const long long Wn = ((long long)p.nv + 31) >> 5;  // used words per bitmap row
     const long long nbits4 = (long long)p.nstates * p.W / 4;
     const bool cta0 = blockIdx.x == 0;
+    Stage stage;
+    stage.q = s_stage[wid][0];
+    stage.w = s_stage[wid][1];
+    stage.n = 0;
     if (gtid == 0) ctl->t0 = globaltimer();
 
     unsigned e = 0;  // barriers passed
@@ -660,10 +780,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     }
     grid_barrier(ctl, ++e);
 
-    // ---- epoch 1: seed F_0 = P = {(q_s, source)} (engine.py:106-109, :154-155)
+    // ---- epoch 1: seed P = M = {(q_s, source)} (engine.py:106-109, :154-155)
     {
-        const Ctx c{&ctl->lc[0], p.wl[0], p.fb[0], &s_wl, &s_ch, s_state};
-        unsigned long long nnew = 0, mf = 0;
+        const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv};
+        if (cta0) reset_qc(&ctl->qc[(e + 2) % 3], threadIdx.x);
+        unsigned long long nnew = 0, nedge = 0;
         if (cta0 && wid == 0) {
             for (int i0 = 0; i0 < p.nstarts; i0 += 32) {
                 const int i = i0 + lane;
@@ -671,135 +792,177 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                 int q = 0;
                 if (i < p.nstarts) {
                     q = S.starts[i];
+                    const long long off = (long long)q * p.W + (p.source >> 5);
                     const uint32_t bit = 1u << (p.source & 31);
-                    fresh = !(atomicOr(p.visited + (long long)q * p.W + (p.source >> 5), bit) & bit);
+                    fresh = !(atomicOr(p.visited + off, bit) & bit);
+                    if (fresh) atomicOr(p.fb[0] + off, bit);
                 }
-                const bool fa[1] = {fresh};
-                const int qa[1] = {q}, wa[1] = {p.source};
-                record_fresh<1>(p, S, c, fa, qa, wa, lane, nnew, mf);
+                nnew += fresh ? 1 : 0;
+                if (fresh) atomicAdd(&s_state[q], 1u);
+                const uint32_t T = emit_pairs(p, S, o, fresh, q, p.source, lane);
+                if (lane == 0) nedge += T;
             }
         }
         __syncthreads();
-        flush_counts(c, nnew, mf, s_red, p.nstates);
+        flush_counts(&ctl->fc[0].nnew, o, ctl->fc[0].state, nnew, nedge, s_red, s_state, p.nstates);
     }
     grid_barrier(ctl, ++e);
-    if (wid == 0) decide_level(p, S, 0, lane, &s_view, s_wpre, s_sv, s_front);
+    if (wid == 0) decide_level(p, S, e, 0, DIR_PUSH, lane, &s_view, s_bpre, s_sv, s_front);
     __syncthreads();
 
     // ---- level loop -----------------------------------------------------------
     int L = 0;
+    int dir = DIR_PUSH;
     for (;;) {
         if (s_view.done) break;
-        const int dir = s_view.dir;
+        dir = s_view.dir;
         const uint32_t* fcur = p.fb[L % 3];
-        const Ctx c{&ctl->lc[(L + 1) % 3], p.wl[(L + 1) & 1], p.fb[(L + 1) % 3], &s_wl, &s_ch, s_state};
-        if (threadIdx.x == 0) s_wl = s_ch = s_task = 0;
-        if (cta0) reset_lc(&ctl->lc[(L + 2) % 3], threadIdx.x);
+        uint32_t* fnext = p.fb[(L + 1) % 3];
+
+        if (dir == DIR_PUSH && s_view.plan) {
+            // ---- plan epoch: emit F_L's row segments from its bitmap (after pull)
+            const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv};
+            if (cta0) reset_qc(&ctl->qc[(e + 2) % 3], threadIdx.x);
+            unsigned long long nedge = 0;
+            for (int q = 0; q < p.nstates; ++q) {
+                if (!s_front[q] || S.gbeg[q + 1] == S.gbeg[q]) continue;
+                const uint32_t* row = fcur + (long long)q * p.W;
+                for (long long w0 = gwarp * 32; w0 < Wn; w0 += nwarps * 32) {
+                    const long long wi = w0 + lane;
+                    const uint32_t bits = wi < Wn ? row[wi] : 0u;
+                    unsigned any = __ballot_sync(FULL, bits != 0);
+                    while (any) {
+                        const int src_lane = __ffs(any) - 1;
+                        any &= any - 1;
+                        const uint32_t wb = __shfl_sync(FULL, bits, src_lane);
+                        const bool valid = (wb >> lane) & 1u;
+                        const int v = (int)((w0 + src_lane) * 32 + lane);
+                        const uint32_t T = stage_add(p, S, o, stage, valid, q, v, lane);
+                        if (lane == 0) nedge += T;
+                    }
+                }
+            }
+            {
+                const uint32_t T = stage_flush(p, S, o, stage, lane);
+                if (lane == 0) nedge += T;
+            }
+            __syncthreads();
+            flush_counts(nullptr, o, nullptr, 0, nedge, s_red, s_state, 0);
+            grid_barrier(ctl, ++e);
+            if (wid == 0) decide_plan(p, e, L, lane, &s_view, s_bpre);
+            __syncthreads();
+            if (s_view.done) break;
+        }
+
+        // ---- expand epoch of level L -------------------------------------------
+        const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv};
+        if (cta0) {
+            reset_qc(&ctl->qc[(e + 2) % 3], threadIdx.x);
+            FCnt* fz = &ctl->fc[(L + 2) % 3];
+            for (int q = threadIdx.x; q < kMaxStates; q += blockDim.x) fz->state[q] = 0;
+            if (threadIdx.x == 0) fz->nnew = 0;
+        }
         {  // zero the bitmap level L+1 will write F_{L+2} into
             uint4* z4 = reinterpret_cast<uint4*>(p.fb[(L + 2) % 3]);
             for (long long i = gtid; i < nbits4; i += gthreads) z4[i] = make_uint4(0, 0, 0, 0);
         }
-        __syncthreads();
-        unsigned long long nnew = 0, mf = 0;
-
+        unsigned long long nnew = 0, nedge = 0;
         if (dir == DIR_PUSH) {
-            // ---- push: expand the set bits of F_L's listed words -------------
-            const unsigned long long nwl = s_view.nwl;
-            const unsigned nreg = s_wpre[gridDim.x];
-            const uint2* wl = p.wl[L & 1];
-            // words per warp task: enough tasks for every warp while the list is short
-            // the list is split into one contiguous range per CTA; the CTA's
-            // warps take `span`-word tasks from it through a shared counter
-            unsigned span = 8;
-            while (span > 1 && (unsigned long long)span * nwarps > nwl) span >>= 1;
-            const unsigned long long per_cta = (nwl + gridDim.x - 1) / gridDim.x;
-            const unsigned long long r_lo = min(nwl, per_cta * blockIdx.x);
-            const unsigned long long r_hi = min(nwl, r_lo + per_cta);
-            for (;;) {
-                unsigned long long c0 = 0;
-                if (lane == 0) c0 = r_lo + (unsigned long long)atomicAdd(&s_task, span);
-                c0 = __shfl_sync(FULL, c0, 0);
-                if (c0 >= r_hi) break;
-                const unsigned long long idx = c0 + lane;
-                int q = 0;
-                uint32_t word = 0, bits = 0;
-                if ((unsigned)lane < span && idx < r_hi) {
-                    uint2 ent;
-                    if (idx < nreg) {
-                        const int r = region_of(s_wpre, idx);
-                        ent = __ldcg(wl + (unsigned long long)r * p.wl_cap + (idx - s_wpre[r]));
-                    } else {
-                        ent = __ldcg(wl + (unsigned long long)kMaxCtas * p.wl_cap + (idx - nreg));
+            // ---- push: expand the bundles of F_L's queue (produced last epoch)
+            const unsigned long long nb = s_bpre[kShards + 1];
+            const uint2* bun = p.bun[e & 1];
+            const uint2* seg = p.seg[e & 1];
+            // CTA-major dealing: consecutive bundles (often one row) land on different SMs
+            const unsigned long long step = (unsigned long long)gridDim.x * kWarps;
+            for (unsigned long long bi = (unsigned long long)wid * gridDim.x + blockIdx.x; bi < nb;
+                 bi += step) {
+                int sh = 0;
+#pragma unroll
+                for (int h = 128; h >= 1; h >>= 1)
+                    if (sh + h <= kShards && s_bpre[sh + h] <= bi) sh += h;
+                const uint2 bd = __ldcg(bun + (unsigned long long)sh * p.shard_buncap + (bi - s_bpre[sh]));
+                if (bd.y == kHoleY) continue;
+                const uint32_t cnt = (bd.y & 127u) + 1;
+                int w[kEdgesPerLane], gj[kEdgesPerLane];
+                if (bd.y & kInline) {
+                    // one row: columns bd.x .. bd.x + cnt - 1
+                    const int g = (int)((bd.y >> 7) & 0xFFu);
+                    const int32_t* col = S.slots[S.gslot[g]].col + bd.x;
+#pragma unroll
+                    for (int u = 0; u < kEdgesPerLane; ++u) {
+                        const uint32_t ed = (uint32_t)(lane + 32 * u);
+                        gj[u] = ed < cnt ? g : -1;
+                        w[u] = ed < cnt ? __ldg(col + ed) : 0;
                     }
-                    q = (int)ent.x;
-                    word = ent.y;
-                    bits = fcur[(long long)q * p.W + word];
+                } else {
+                    const uint32_t s0 = bd.x;
+                    const uint32_t off = (bd.y >> 7) & 0xFFFFFFu;
+                    uint32_t my_start = 0, my_len = 0, my_grp = 0;
+                    if ((unsigned long long)s0 + lane < p.seg_alloc) {
+                        const uint2 sg = __ldcg(seg + s0 + lane);
+                        my_start = sg.x;
+                        my_len = sg.y >> 8;
+                        my_grp = sg.y & 0xFFu;
+                    }
+                    if (lane == 0) {
+                        my_start += off;
+                        my_len -= off;
+                    }
+                    const uint32_t incl = warp_incl_scan(my_len, lane);
+                    const uint32_t excl = incl - my_len;
+                    // edges lane, lane+32, ...: locate, then issue all column loads
+#pragma unroll
+                    for (int u = 0; u < kEdgesPerLane; ++u) {
+                        const uint32_t ed = (uint32_t)(lane + 32 * u);
+                        const bool active = ed < cnt;
+                        const int j = warp_upper_lane(excl, active ? ed : 0u);
+                        const uint32_t sj = __shfl_sync(FULL, my_start, j);
+                        const uint32_t exj = __shfl_sync(FULL, excl, j);
+                        const int g = (int)__shfl_sync(FULL, my_grp, j);
+                        gj[u] = active ? g : -1;
+                        w[u] = active ? __ldg(S.slots[S.gslot[g]].col + sj + (ed - exj)) : 0;
+                    }
                 }
-                const uint32_t pc = __popc(bits);
-                const uint32_t iincl = warp_incl_scan(pc, lane);
-                const uint32_t iexcl = iincl - pc;
-                const uint32_t NI = __shfl_sync(FULL, iincl, 31);
-                for (uint32_t r0 = 0; r0 < NI; r0 += 32) {
-                    // one frontier item (q, v) per lane
-                    const uint32_t t = r0 + lane;
-                    const bool act = t < NI;
-                    const int j = warp_upper_lane(iexcl, act ? t : 0u);
-                    const uint32_t bj = __shfl_sync(FULL, bits, j);
-                    const int qv = __shfl_sync(FULL, q, j);
-                    const uint32_t wj = __shfl_sync(FULL, word, j);
-                    const uint32_t ej = __shfl_sync(FULL, iexcl, j);
-                    const int v = act ? (int)(wj * 32 + __fns(bj, 0, (int)(t - ej) + 1)) : 0;
-                    const int ng = act ? S.gbeg[qv + 1] - S.gbeg[qv] : 0;
-                    int maxng = ng;
+                // probe P for every target, then claim with atomicOr
+                for (int k = 0; k < p.maxT; ++k) {
+                    uint32_t old[kEdgesPerLane];
+                    int q2[kEdgesPerLane];
 #pragma unroll
-                    for (int d = 16; d >= 1; d >>= 1) maxng = max(maxng, __shfl_xor_sync(FULL, maxng, d));
-                    for (int k0 = 0; k0 < maxng; k0 += kFastGroups) {
-                        // row pointers of up to kFastGroups groups in flight together
-                        uint32_t lo[kFastGroups], deg[kFastGroups];
-                        int g[kFastGroups];
-#pragma unroll
-                        for (int k = 0; k < kFastGroups; ++k) {
-                            lo[k] = deg[k] = 0;
-                            g[k] = -1;
-                            if (k0 + k < ng) {
-                                g[k] = S.gbeg[qv] + k0 + k;
-                                const Slot sl = S.slots[S.gslot[g[k]]];
-                                lo[k] = __ldg(sl.rowptr + v);
-                                deg[k] = __ldg(sl.rowptr + v + 1);
-                            }
-                        }
-#pragma unroll
-                        for (int k = 0; k < kFastGroups; ++k) {
-                            deg[k] -= lo[k];
-                            if (k0 + k >= maxng) continue;
-                            const bool big = deg[k] > kBigRow;  // long row: chunks for the chunk epoch
-                            add_chunks(p, c, big, lo[k], deg[k], (uint32_t)g[k], 0u, lane);
-                            if (big) deg[k] = 0;
-                        }
-#pragma unroll
-                        for (int k = 0; k < kFastGroups; ++k) {
-                            if (k0 + k >= maxng) break;
-                            const uint32_t dincl = warp_incl_scan(deg[k], lane);
-                            const uint32_t dexcl = dincl - deg[k];
-                            const uint32_t T = __shfl_sync(FULL, dincl, 31);
-                            for (uint32_t e0 = 0; e0 < T; e0 += 32 * kEPL) {
-                                int w[kEPL], gg[kEPL];
-#pragma unroll
-                                for (int u = 0; u < kEPL; ++u) {
-                                    const uint32_t ed = e0 + 32 * u + lane;
-                                    const bool a = ed < T;
-                                    const int jj = warp_upper_lane(dexcl, a ? ed : 0u);
-                                    const uint32_t loj = __shfl_sync(FULL, lo[k], jj);
-                                    const uint32_t exj = __shfl_sync(FULL, dexcl, jj);
-                                    const int gj = __shfl_sync(FULL, g[k], jj);
-                                    gg[u] = a ? gj : -1;
-                                    w[u] = a ? __ldg(S.slots[S.gslot[gj]].col + loj + (ed - exj)) : 0;
-                                }
-                                claim_edges(p, S, c, w, gg, lane, nnew, mf);
+                    for (int u = 0; u < kEdgesPerLane; ++u) {
+                        q2[u] = -1;
+                        old[u] = 0xFFFFFFFFu;
+                        if (gj[u] >= 0) {
+                            const int t0 = S.toff[gj[u]];
+                            if (t0 + k < S.toff[gj[u] + 1]) {
+                                q2[u] = S.targets[t0 + k];
+                                old[u] = p.visited[(long long)q2[u] * p.W + (w[u] >> 5)];
                             }
                         }
                     }
+#pragma unroll
+                    for (int u = 0; u < kEdgesPerLane; ++u) {
+                        const uint32_t bit = 1u << (w[u] & 31);
+                        if (q2[u] >= 0 && !(old[u] & bit)) {
+                            const long long off2 = (long long)q2[u] * p.W + (w[u] >> 5);
+                            old[u] = atomicOr(p.visited + off2, bit);
+                            if (!(old[u] & bit)) atomicOr(fnext + off2, bit);
+                        } else {
+                            old[u] = 0xFFFFFFFFu;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kEdgesPerLane; ++u) {
+                        const bool fresh = q2[u] >= 0 && !(old[u] & (1u << (w[u] & 31)));
+                        nnew += fresh ? 1 : 0;
+                        if (fresh) atomicAdd(&s_state[q2[u]], 1u);
+                        const uint32_t T = stage_add(p, S, o, stage, fresh, q2[u], w[u], lane);
+                        if (lane == 0) nedge += T;
+                    }
                 }
+            }
+            {
+                const uint32_t T = stage_flush(p, S, o, stage, lane);
+                if (lane == 0) nedge += T;
             }
         } else {
             // ---- pull: unvisited (q', w) scan A_s^T row w for a member of F_L[q]
@@ -851,7 +1014,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                         lo[u] = look[u] ? __ldg(ps.rowptr + w[u]) : 0u;
                         hi[u] = look[u] ? __ldg(ps.rowptr + w[u] + 1) : 0u;
                     }
-                    // the first kPullInline in-edges of every vertex, all loads in flight
+                    // the first kPullInline in-edges of every vertex: all loads in flight together
                     int cand[kPullVerts][kPullInline];
 #pragma unroll
                     for (int u = 0; u < kPullVerts; ++u)
@@ -869,125 +1032,55 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
 #pragma unroll
                         for (int i = 0; i < kPullInline; ++i)
                             if (cand[u][i] >= 0 && ((fw[u][i] >> (cand[u][i] & 31)) & 1u)) found[u] = true;
-                    // the rest of the row: long rows become chunks; medium rows
-                    // are scanned by their own lane, kPullStep columns of every
-                    // vertex in flight per step, early exit
-                    bool medium[kPullVerts];
-                    uint32_t pos[kPullVerts];
+                    // longer rows: the whole warp scans one row at a time, early exit
 #pragma unroll
                     for (int u = 0; u < kPullVerts; ++u) {
-                        const bool more = look[u] && !found[u] && hi[u] - lo[u] > kPullInline;
-                        const bool longrow = more && hi[u] - lo[u] - kPullInline > kLongRow;
-                        add_chunks(p, c, longrow, lo[u] + kPullInline, hi[u] - lo[u] - kPullInline, (uint32_t)w[u],
-                                   ((uint32_t)q2 << 16) | (uint32_t)k, lane);
-                        medium[u] = more && !longrow;
-                        pos[u] = lo[u] + kPullInline;
-                    }
-                    for (;;) {
-                        bool any = false;
+                        unsigned longrows = __ballot_sync(FULL, look[u] && !found[u] && hi[u] - lo[u] > kPullInline);
+                        while (longrows) {
+                            const int ln = __ffs(longrows) - 1;
+                            longrows &= longrows - 1;
+                            const uint32_t rlo = __shfl_sync(FULL, lo[u], ln) + kPullInline;
+                            const uint32_t rhi = __shfl_sync(FULL, hi[u], ln);
+                            bool hit = false;
+                            for (uint32_t ed = rlo; ed < rhi; ed += 128) {
+                                int uu[4];
 #pragma unroll
-                        for (int u = 0; u < kPullVerts; ++u) any |= medium[u];
-                        if (!any) break;
-                        int cc[kPullVerts][kPullStep];
+                                for (int c = 0; c < 4; ++c)
+                                    uu[c] = ed + 32 * c + lane < rhi ? __ldg(ps.col + ed + 32 * c + lane) : -1;
+                                bool h = false;
 #pragma unroll
-                        for (int u = 0; u < kPullVerts; ++u)
-#pragma unroll
-                            for (int i = 0; i < kPullStep; ++i)
-                                cc[u][i] = medium[u] && pos[u] + i < hi[u] ? __ldg(ps.col + pos[u] + i) : -1;
-#pragma unroll
-                        for (int u = 0; u < kPullVerts; ++u) {
-                            if (!medium[u]) continue;
-#pragma unroll
-                            for (int i = 0; i < kPullStep; ++i)
-                                if (cc[u][i] >= 0 && ((frow[cc[u][i] >> 5] >> (cc[u][i] & 31)) & 1u)) found[u] = true;
-                            pos[u] += kPullStep;
-                            if (found[u] || pos[u] >= hi[u]) medium[u] = false;
+                                for (int c = 0; c < 4; ++c)
+                                    if (uu[c] >= 0) h |= (frow[uu[c] >> 5] >> (uu[c] & 31)) & 1u;
+                                if (__ballot_sync(FULL, h)) {
+                                    hit = true;
+                                    break;
+                                }
+                            }
+                            if (hit && lane == ln) found[u] = true;
                         }
                     }
                 }
-                bool app[kPullVerts];
-                int qa[kPullVerts], qf[kPullVerts];
 #pragma unroll
                 for (int u = 0; u < kPullVerts; ++u) {
                     const unsigned fmask = __ballot_sync(FULL, found[u]);
-                    app[u] = fmask != 0 && lane == 0;
-                    qa[u] = q2;
-                    qf[u] = found[u] ? q2 : -1;
-                    if (app[u]) {  // this warp owns the word: plain stores
+                    if (fmask && lane == u) {
                         const long long voff = (long long)q2 * p.W + word0 + u;
                         p.visited[voff] = vis[u] | fmask;
-                        c.fnext[voff] = fmask;
+                        fnext[voff] = fmask;
                         nnew += __popc(fmask);
-                        atomicAdd(&c.s_state[q2], (unsigned)__popc(fmask));
+                        atomicAdd(&s_state[q2], (unsigned)__popc(fmask));
                     }
-                }
-                if (__any_sync(FULL, found[0] || found[1] || found[2] || found[3])) {
-                    mf += out_edges<kPullVerts>(S, qf, w);
-                    wl_append<kPullVerts>(p, c, app, qa, w, lane);
                 }
             }
         }
         __syncthreads();
         if (threadIdx.x == 0 && L < 64) atomicMax(&ctl->work_ns[L], globaltimer() - ctl->t0);
-        flush_counts(c, nnew, mf, s_red, p.nstates);
+        flush_counts(&ctl->fc[(L + 1) % 3].nnew, o, ctl->fc[(L + 1) % 3].state, nnew, nedge, s_red,
+                     s_state, p.nstates);
         grid_barrier(ctl, ++e);
-
-        // ---- chunk epoch: long rows cut into kChunk-edge pieces, all warps ----
-        if (wid == 0) {
-            const unsigned reg = region_prefix(c.lc->ch_cta, p.ch_cap, s_cpre, lane);
-            const unsigned long long ovf = min(ldcg(&c.lc->ch_ovf), p.ch_ovf_cap);
-            if (lane == 0) s_nch = reg + ovf;
-        }
-        __syncthreads();
-        const unsigned long long nch = s_nch;
-        if (nch) {
-            unsigned long long cn = 0, cm = 0;
-            if (cta0 && threadIdx.x == 0) ctl->chunks += nch;
-            const unsigned creg = s_cpre[gridDim.x];
-            // CTA-major dealing spreads one row's chunks over different SMs
-            for (unsigned long long ci = (unsigned long long)wid * gridDim.x + blockIdx.x; ci < nch; ci += nwarps) {
-                uint4 ch;
-                if (ci < creg) {
-                    const int r = region_of(s_cpre, ci);
-                    ch = __ldcg(p.chunks + (unsigned long long)r * p.ch_cap + (ci - s_cpre[r]));
-                } else {
-                    ch = __ldcg(p.chunks + (unsigned long long)kMaxCtas * p.ch_cap + (ci - creg));
-                }
-                if (dir == DIR_PUSH) {
-                    const int g = (int)ch.z;
-                    const int32_t* col = S.slots[S.gslot[g]].col + ch.x;
-                    for (uint32_t e0 = 0; e0 < ch.y; e0 += 32 * kEPL) {
-                        int w[kEPL], gg[kEPL];
-#pragma unroll
-                        for (int u = 0; u < kEPL; ++u) {
-                            const uint32_t ed = e0 + 32 * u + lane;
-                            gg[u] = ed < ch.y ? g : -1;
-                            w[u] = ed < ch.y ? __ldg(col + ed) : 0;
-                        }
-                        claim_edges(p, S, c, w, gg, lane, cn, cm);
-                    }
-                } else {
-                    const int w = (int)ch.z;
-                    const int q2 = (int)(ch.w >> 16), k = (int)(ch.w & 0xFFFFu);
-                    const long long voff = (long long)q2 * p.W + (w >> 5);
-                    const uint32_t bit = 1u << (w & 31);
-                    if (p.visited[voff] & bit) continue;  // found by another row or chunk
-                    const Slot ps = S.slots[p.nslots + S.islot[k]];
-                    const bool hit =
-                        warp_row_hit(ps.col, ch.x, ch.x + ch.y, fcur + (long long)S.isrc[k] * p.W, lane);
-                    bool fresh[1] = {false};
-                    if (hit && lane == 0) fresh[0] = !(atomicOr(p.visited + voff, bit) & bit);
-                    const int qa[1] = {q2}, wa[1] = {w};
-                    record_fresh<1>(p, S, c, fresh, qa, wa, lane, cn, cm);
-                }
-            }
-            __syncthreads();
-            flush_counts(c, cn, cm, s_red, p.nstates);
-            grid_barrier(ctl, ++e);
-        }
         if (cta0 && threadIdx.x == 0 && L < 64) ctl->bar_ns[L] = globaltimer() - ctl->t0;
         ++L;
-        if (wid == 0) decide_level(p, S, L, lane, &s_view, s_wpre, s_sv, s_front);
+        if (wid == 0) decide_level(p, S, e, L, dir, lane, &s_view, s_bpre, s_sv, s_front);
         __syncthreads();
     }
 
@@ -1012,8 +1105,29 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                 for (int k = 0; i * 32 + k < p.nv; ++k) out[k] = (acc >> k) & 1u;
             }
         }
+        // exact push-model TE = sum over (q, v) in P of q's group out-degrees x targets
+        unsigned long long te = 0;
+        if (p.count_te) {
+            for (int q = 0; q < p.nstates; ++q) {
+                if (S.gbeg[q + 1] == S.gbeg[q]) continue;
+                for (long long i = gtid; i < Wn; i += gthreads) {
+                    uint32_t bits = __ldcg(p.visited + (long long)q * p.W + i);
+                    while (bits) {
+                        const int v = (int)(i * 32 + __ffs(bits) - 1);
+                        bits &= bits - 1;
+                        for (int g = S.gbeg[q]; g < S.gbeg[q + 1]; ++g) {
+                            const Slot sl = S.slots[S.gslot[g]];
+                            te += (unsigned long long)(__ldg(sl.rowptr + v + 1) - __ldg(sl.rowptr + v)) *
+                                  (unsigned long long)(S.toff[g + 1] - S.toff[g]);
+                        }
+                    }
+                }
+            }
+        }
         cnt = warp_sum_u64(cnt);
+        te = warp_sum_u64(te);
         if (lane == 0 && cnt) atomicAdd(&ctl->reach_count, cnt);
+        if (lane == 0 && te) atomicAdd(&ctl->te_exact, te);
     }
 }
 

@@ -1,0 +1,16 @@
+#!/bin/bash
+# One GPU-box pass: parity tests, bench (engine + reference arms), ncu evidence.
+# Usage (under gpurun): bash tools/gpu_round.sh <tag>
+tag=${1:-r01}
+out=gpurun_out
+mkdir -p $out
+timeout 900 python -m pytest tests -q -m gpu > $out/gpu_tests_$tag.log 2>&1; echo "tests_rc=$?"; tail -3 $out/gpu_tests_$tag.log
+timeout 300 python __graft_entry__.py --smoke > $out/smoke_$tag.log 2>&1; echo "smoke_rc=$?"
+timeout 600 python bench.py > $out/bench_$tag.json 2> $out/bench_$tag.err; echo "bench_rc=$?"
+timeout 600 python bench.py --impl reference > $out/bench_ref_$tag.json 2> $out/bench_ref_$tag.err; echo "ref_rc=$?"
+timeout 900 python bench.py --config cfg3 --steps 5 --warmup 2 --no-cpu-baseline > $out/bench_cfg3_$tag.json 2> $out/bench_cfg3_$tag.err; echo "cfg3_rc=$?"
+timeout 300 python bench.py --profile --steps 3 --warmup 1 > $out/prof_plain_$tag.log 2>&1 && \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_$tag.csv \
+    python bench.py --profile --steps 3 --warmup 1 > $out/ncu_launches_$tag.log 2>&1; echo "ncu_launch_rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:ssr_kernel -s 2 -c 1 \
+    -o $out/prof_cfg2_$tag python bench.py --profile --steps 3 --warmup 1 > $out/ncu_full_$tag.log 2>&1; echo "ncu_full_rc=$?"
