@@ -316,7 +316,7 @@ def run_engine(args, rank, world, local_rank):
     clocks = sampler.stop() if sampler else None
 
     h2d, d2h_ctl = pq.io_bytes()
-    d2h = d2h_ctl + sg.nv
+    d2h = d2h_ctl + (sg.nv + 31) // 32 * 4  # eval_ssr reads back the answer bitmap
     from paper_2412_10287_b200.multigpu import reduce_timing
 
     # max over ranks of the device time, sum over ranks of the product edges

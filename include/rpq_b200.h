@@ -134,11 +134,17 @@ RPQ_API int rpq_query_wait(rpq_query* q, rpq_stats* stats);
 RPQ_API int rpq_query_reach_device(rpq_query* q, uint8_t** d_reach);
 /* Copy the answer of the last run to host (uint8[num_vertices], 1 = reachable). */
 RPQ_API int rpq_query_copy_reach(rpq_query* q, uint8_t* host_reach);
+/* Output mode: 0 (default) keeps the answer on the device; 1 also copies the
+ * answer bitmap (ceil(nv/32) uint32 words, bit v%32 of word v/32) into pinned
+ * host memory as part of every run, ready after rpq_query_wait. */
+RPQ_API int rpq_query_set_output(rpq_query* q, int32_t mode);
+/* The answer of the last run as a bitmap (host copy). */
+RPQ_API int rpq_query_copy_reach_bits(rpq_query* q, uint32_t* host_words, int64_t nwords);
 /* Copy the full visited matrix P (nstates rows x ceil(nv/32) uint32 words). */
 RPQ_API int rpq_query_copy_visited(rpq_query* q, uint32_t* host_words, int64_t nwords);
 /* Bytes one run moves: host->device (the automaton tables, re-sent with every
- * run) and device->host (the run's status/statistics block; the answer copy
- * of rpq_query_copy_reach adds num_vertices bytes). */
+ * run) and device->host (the run's status/statistics block, plus the answer
+ * bitmap in output mode 1). */
 RPQ_API int rpq_query_io_bytes(const rpq_query* q, int64_t* h2d_per_run, int64_t* d2h_per_run);
 RPQ_API int rpq_query_destroy(rpq_query* q);
 

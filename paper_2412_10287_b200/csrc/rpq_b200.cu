@@ -84,6 +84,15 @@ struct rpq_query {
     Ctl* d_ctl = nullptr;
     Ctl* h_ctl = nullptr;  // pinned
     uint8_t* d_reach = nullptr;
+    uint32_t* d_reach_bits = nullptr;
+    uint32_t* h_reach_bits = nullptr;  // pinned; filled by run() when output_mode == 1
+    int output_mode = 0;
+    RunArgs* h_run = nullptr;  // pinned per-run inputs
+    RunArgs* d_run = nullptr;
+    cudaGraphExec_t graph = nullptr;  // captured run sequence (per output mode)
+    int graph_mode = -1;
+    bool graph_failed = false;
+    bool inflight = false;
     unsigned long long shard_segcap = 0, shard_buncap = 0, ovf_segcap = 0, ovf_buncap = 0;
     unsigned long long seg_alloc = 0, bun_alloc = 0;
     long long W = 0;
@@ -172,6 +181,11 @@ void free_query_buffers(rpq_query* q) {
     if (q->d_ctl) cudaFree(q->d_ctl);
     if (q->h_ctl) cudaFreeHost(q->h_ctl);
     if (q->d_reach) cudaFree(q->d_reach);
+    if (q->d_reach_bits) cudaFree(q->d_reach_bits);
+    if (q->h_reach_bits) cudaFreeHost(q->h_reach_bits);
+    if (q->h_run) cudaFreeHost(q->h_run);
+    if (q->d_run) cudaFree(q->d_run);
+    if (q->graph) cudaGraphExecDestroy(q->graph);
     if (q->ev0) cudaEventDestroy(q->ev0);
     if (q->ev1) cudaEventDestroy(q->ev1);
     if (q->own_stream) cudaStreamDestroy(q->own_stream);
@@ -397,6 +411,10 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     QTRY(cudaMalloc(&q->d_ctl, sizeof(Ctl)));
     QTRY(cudaMallocHost(&q->h_ctl, sizeof(Ctl)));
     QTRY(cudaMalloc(&q->d_reach, (size_t)(q->W * 32 + 32)));
+    QTRY(cudaMalloc(&q->d_reach_bits, (size_t)q->W * sizeof(uint32_t)));
+    QTRY(cudaMallocHost(&q->h_reach_bits, (size_t)q->W * sizeof(uint32_t)));
+    QTRY(cudaMallocHost(&q->h_run, sizeof(RunArgs)));
+    QTRY(cudaMalloc(&q->d_run, sizeof(RunArgs)));
     QTRY(cudaStreamCreateWithFlags(&q->own_stream, cudaStreamNonBlocking));
     QTRY(cudaEventCreate(&q->ev0));
     QTRY(cudaEventCreate(&q->ev1));
@@ -429,13 +447,11 @@ int rpq_query_set_options(rpq_query* q, int32_t direction, int32_t count_te, dou
     return RPQ_OK;
 }
 
-int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) {
-    if (!q) return fail(RPQ_EINVAL, "null query");
-    if (source < 0 || source >= q->g->nv)
-        return fail(RPQ_ERANGE, "vertex index " + std::to_string(source) + " out of range");
-    if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
-    cudaStream_t st = stream ? (cudaStream_t)stream : q->own_stream;
+namespace {
+
+Params make_params(const rpq_query* q) {
     Params p{};
+    p.run = q->d_run;
     p.tables = q->d_tables;
     p.slots = q->d_slots;
     p.slot_nnz = q->d_slot_nnz;
@@ -447,15 +463,12 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     }
     p.ctl = q->d_ctl;
     p.reach = q->d_reach;
+    p.reach_bits = q->d_reach_bits;
     p.shard_segcap = q->shard_segcap;
     p.shard_buncap = q->shard_buncap;
     p.ovf_segcap = q->ovf_segcap;
     p.ovf_buncap = q->ovf_buncap;
     p.seg_alloc = q->seg_alloc;
-    if (!(timeout_s >= 0) || std::isinf(timeout_s) || timeout_s > 1.0e9)
-        p.budget_ns = ~0ull;
-    else
-        p.budget_ns = (unsigned long long)(timeout_s * 1e9);
     p.W = q->W;
     p.nv = q->g->nv;
     p.nstates = q->nstates;
@@ -466,27 +479,97 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     p.nfinals = q->nfinals;
     p.nin = q->nin;
     p.maxT = q->maxT;
-    p.source = source;
     p.table_ints = (int)q->tables.size();
-    p.dir_mode = q->dir_mode;
-    p.count_te = q->count_te;
-    p.alpha = q->alpha;
-    CUDA_TRY(cudaEventRecord(q->ev0, st));
-    // the automaton travels with every run (a query's input), from pinned memory
-    if (!q->tables.empty())
-        CUDA_TRY(cudaMemcpyAsync(q->d_tables, q->h_tables, q->tables.size() * sizeof(int32_t),
-                                 cudaMemcpyHostToDevice, st));
-    if (!q->slots.empty())
-        CUDA_TRY(cudaMemcpyAsync(q->d_slots, q->h_slots, q->slots.size() * sizeof(Slot),
-                                 cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemsetAsync(q->d_ctl, 0, sizeof(Ctl), st));
+    return p;
+}
+
+// The run sequence: inputs H2D (run block + automaton tables, pinned), control
+// block reset, the cooperative kernel, statistics (and answer bitmap) D2H.
+cudaError_t enqueue_run(rpq_query* q, cudaStream_t st) {
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(q->d_run, q->h_run, sizeof(RunArgs), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return e;
+    if (!q->tables.empty() &&
+        (e = cudaMemcpyAsync(q->d_tables, q->h_tables, q->tables.size() * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return e;
+    if (!q->slots.empty() &&
+        (e = cudaMemcpyAsync(q->d_slots, q->h_slots, q->slots.size() * sizeof(Slot), cudaMemcpyHostToDevice,
+                             st)) != cudaSuccess)
+        return e;
+    if ((e = cudaMemsetAsync(q->d_ctl, 0, sizeof(Ctl), st)) != cudaSuccess) return e;
+    Params p = make_params(q);
     void* args[] = {&p};
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)ssr_kernel, dim3(q->grid), dim3(kThreads), args,
-                                         q->smem, st));
+    if ((e = cudaLaunchCooperativeKernel((const void*)ssr_kernel, dim3(q->grid), dim3(kThreads), args, q->smem,
+                                         st)) != cudaSuccess)
+        return e;
+    if ((e = cudaMemcpyAsync(q->h_ctl, q->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+        return e;
+    if (q->output_mode == 1 && q->g->nv > 0 &&
+        (e = cudaMemcpyAsync(q->h_reach_bits, q->d_reach_bits, (size_t)((q->g->nv + 31) / 32) * 4,
+                             cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+        return e;
+    return cudaSuccess;
+}
+
+// Capture enqueue_run into a graph once per output mode: one cudaGraphLaunch
+// per run.  Falls back to direct launches if capture is not possible.
+void build_graph(rpq_query* q) {
+    if (q->graph && q->graph_mode == q->output_mode) return;
+    if (q->graph) {
+        cudaGraphExecDestroy(q->graph);
+        q->graph = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(q->own_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        q->graph_failed = true;
+        return;
+    }
+    cudaError_t e = enqueue_run(q, q->own_stream);
+    cudaError_t e2 = cudaStreamEndCapture(q->own_stream, &g);
+    if (e != cudaSuccess || e2 != cudaSuccess || !g ||
+        cudaGraphInstantiate(&q->graph, g, 0) != cudaSuccess) {
+        cudaGetLastError();
+        q->graph = nullptr;
+        q->graph_failed = true;
+    } else {
+        q->graph_mode = q->output_mode;
+    }
+    if (g) cudaGraphDestroy(g);
+}
+
+}  // namespace
+
+int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) {
+    if (!q) return fail(RPQ_EINVAL, "null query");
+    if (source < 0 || source >= q->g->nv)
+        return fail(RPQ_ERANGE, "vertex index " + std::to_string(source) + " out of range");
+    if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+    cudaStream_t st = stream ? (cudaStream_t)stream : q->own_stream;
+    // the pinned input block is read by the previous run's H2D copy: let it finish
+    if (q->inflight) CUDA_TRY(cudaStreamSynchronize(q->last_stream));
+    RunArgs ra{};
+    ra.source = source;
+    ra.dir_mode = q->dir_mode;
+    ra.count_te = q->count_te;
+    ra.alpha = q->alpha;
+    if (!(timeout_s >= 0) || std::isinf(timeout_s) || timeout_s > 1.0e9)
+        ra.budget_ns = ~0ull;
+    else
+        ra.budget_ns = (unsigned long long)(timeout_s * 1e9);
+    *q->h_run = ra;
+    if (!q->graph_failed) build_graph(q);
+    // timing events bracket the whole run (graph event nodes cannot be timed)
+    CUDA_TRY(cudaEventRecord(q->ev0, st));
+    if (q->graph)
+        CUDA_TRY(cudaGraphLaunch(q->graph, st));
+    else
+        CUDA_TRY(enqueue_run(q, st));
     CUDA_TRY(cudaEventRecord(q->ev1, st));
-    CUDA_TRY(cudaMemcpyAsync(q->h_ctl, q->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     q->last_stream = st;
     q->ran = true;
+    q->inflight = true;
     return RPQ_OK;
 }
 
@@ -494,6 +577,7 @@ int rpq_query_wait(rpq_query* q, rpq_stats* stats) {
     if (!q) return fail(RPQ_EINVAL, "null query");
     if (!q->ran) return fail(RPQ_EINVAL, "query has not been run");
     CUDA_TRY(cudaStreamSynchronize(q->last_stream));
+    q->inflight = false;
     const Ctl& c = *q->h_ctl;
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, q->ev0, q->ev1));
@@ -561,11 +645,35 @@ int rpq_query_copy_visited(rpq_query* q, uint32_t* host_words, int64_t nwords) {
     return RPQ_OK;
 }
 
+int rpq_query_set_output(rpq_query* q, int32_t mode) {
+    if (!q) return fail(RPQ_EINVAL, "null query");
+    if (mode < 0 || mode > 1) return fail(RPQ_EINVAL, "output mode must be 0 or 1");
+    q->output_mode = mode;
+    return RPQ_OK;
+}
+
+int rpq_query_copy_reach_bits(rpq_query* q, uint32_t* host_words, int64_t nwords) {
+    if (!q || (!host_words && nwords)) return fail(RPQ_EINVAL, "null argument");
+    const int64_t words = ((int64_t)q->g->nv + 31) / 32;
+    if (nwords < words) return fail(RPQ_EINVAL, "output buffer too small");
+    if (!q->ran) return fail(RPQ_EINVAL, "query has not been run");
+    if (q->output_mode == 1) {  // already on the host (pinned), after rpq_query_wait
+        std::memcpy(host_words, q->h_reach_bits, (size_t)words * 4);
+        return RPQ_OK;
+    }
+    if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+    cudaStream_t st = q->last_stream ? q->last_stream : q->own_stream;
+    CUDA_TRY(cudaMemcpyAsync(host_words, q->d_reach_bits, (size_t)words * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return RPQ_OK;
+}
+
 int rpq_query_io_bytes(const rpq_query* q, int64_t* h2d_per_run, int64_t* d2h_per_run) {
     if (!q) return fail(RPQ_EINVAL, "null query");
     if (h2d_per_run)
         *h2d_per_run = (int64_t)(q->tables.size() * sizeof(int32_t) + q->slots.size() * sizeof(Slot));
-    if (d2h_per_run) *d2h_per_run = (int64_t)sizeof(Ctl);
+    if (d2h_per_run)
+        *d2h_per_run = (int64_t)sizeof(Ctl) + (q->output_mode == 1 ? ((int64_t)q->g->nv + 31) / 32 * 4 : 0);
     return RPQ_OK;
 }
 

@@ -100,7 +100,19 @@ struct Ctl {
     int level_dir[64];
 };
 
+// Per-run inputs, copied host->device with the automaton tables at the start
+// of every run (so a captured CUDA graph replays without parameter updates).
+struct RunArgs {
+    int source;
+    int dir_mode;  // 0 auto, 1 push only, 2 pull after the seed
+    int count_te;
+    float alpha;   // pull when m_f * alpha > m_u
+    unsigned long long budget_ns;
+    unsigned long long pad[2];
+};
+
 struct Params {
+    const RunArgs* run;
     const int32_t* tables;
     const Slot* slots;       // A_s, then A_s^T at [nslots, 2*nslots)
     const unsigned long long* slot_nnz;
@@ -110,6 +122,7 @@ struct Params {
     uint2* bun[2];
     Ctl* ctl;
     uint8_t* reach;
+    uint32_t* reach_bits;  // the answer as a bitmap (same bits as reach)
     unsigned long long shard_segcap, shard_buncap, ovf_segcap, ovf_buncap;
     unsigned long long seg_alloc;
     unsigned long long budget_ns;
@@ -117,11 +130,7 @@ struct Params {
     int nv;
     int nstates, ngroups, nslots, ntargets, nstarts, nfinals, nin;
     int maxT;
-    int source;
     int table_ints;
-    int dir_mode;            // 0 auto, 1 push only, 2 pull after the seed
-    int count_te;
-    float alpha;             // pull when m_f * alpha > m_u
 };
 
 struct Smem {
@@ -135,6 +144,7 @@ struct Smem {
     const int32_t* isrc;     // [nin]
     const int32_t* islot;    // [nin]
     const Slot* slots;       // [2*nslots]
+    const RunArgs* run;      // this run's inputs (shared-memory copy)
 };
 
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
@@ -598,9 +608,9 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
         iterations = L;
         done = 1;
     } else {
-        if (p.dir_mode == 2) {
+        if (S.run->dir_mode == 2) {
             next = DIR_PULL;
-        } else if (p.dir_mode == 0) {
+        } else if (S.run->dir_mode == 0) {
             // m_f: edges out of F_L (exact after a push level, estimated from
             // average degrees after a pull level); m_u: in-edges of unvisited
             // targets whose source state has a frontier.  Pull when
@@ -617,7 +627,7 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
             }
             mf = produced_by_push ? (double)nedge : warp_sum_f64(mf);
             mu = warp_sum_f64(mu);
-            next = (mf * (double)p.alpha > mu) ? DIR_PULL : DIR_PUSH;
+            next = (mf * (double)S.run->alpha > mu) ? DIR_PULL : DIR_PUSH;
         }
         if (next == DIR_PUSH) {
             if (produced_by_push) {
@@ -655,7 +665,7 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
                 }
                 // _Clock.check at the top of iteration L (engine.py:87-89):
                 // recorded now, acted upon at the next decision by every CTA
-                if (now - ctl->t0 > p.budget_ns) ctl->qc[(e + 1) % 3].expire = (unsigned)L + 1;
+                if (now - ctl->t0 > S.run->budget_ns) ctl->qc[(e + 1) % 3].expire = (unsigned)L + 1;
             } else {
                 ctl->status = status;
                 ctl->iterations = iterations;
@@ -728,6 +738,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     __shared__ View s_view;
     __shared__ int s_stage[kWarps][2][64];
     __shared__ unsigned long long s_resv;
+    __shared__ unsigned s_task;  // next task index of this CTA in the current epoch
+    __shared__ RunArgs s_run;
 
     Slot* s_slots = reinterpret_cast<Slot*>(smem_raw);
     int32_t* s_tab = reinterpret_cast<int32_t*>(smem_raw + sizeof(Slot) * 2 * p.nslots);
@@ -739,7 +751,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
         s_sv[i] = 0;
         s_front[i] = 0;
     }
+    if (threadIdx.x == 0) s_run = *p.run;
     Smem S;
+    S.run = &s_run;
     S.slots = s_slots;
     S.gbeg = s_tab;
     S.gslot = S.gbeg + p.nstates + 1;
@@ -792,14 +806,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                 int q = 0;
                 if (i < p.nstarts) {
                     q = S.starts[i];
-                    const long long off = (long long)q * p.W + (p.source >> 5);
-                    const uint32_t bit = 1u << (p.source & 31);
+                    const long long off = (long long)q * p.W + (S.run->source >> 5);
+                    const uint32_t bit = 1u << (S.run->source & 31);
                     fresh = !(atomicOr(p.visited + off, bit) & bit);
                     if (fresh) atomicOr(p.fb[0] + off, bit);
                 }
                 nnew += fresh ? 1 : 0;
                 if (fresh) atomicAdd(&s_state[q], 1u);
-                const uint32_t T = emit_pairs(p, S, o, fresh, q, p.source, lane);
+                const uint32_t T = emit_pairs(p, S, o, fresh, q, S.run->source, lane);
                 if (lane == 0) nedge += T;
             }
         }
@@ -856,6 +870,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
 
         // ---- expand epoch of level L -------------------------------------------
         const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv};
+        if (threadIdx.x == 0) s_task = 0;
         if (cta0) {
             reset_qc(&ctl->qc[(e + 2) % 3], threadIdx.x);
             FCnt* fz = &ctl->fc[(L + 2) % 3];
@@ -866,6 +881,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
             uint4* z4 = reinterpret_cast<uint4*>(p.fb[(L + 2) % 3]);
             for (long long i = gtid; i < nbits4; i += gthreads) z4[i] = make_uint4(0, 0, 0, 0);
         }
+        __syncthreads();  // s_task
         unsigned long long nnew = 0, nedge = 0;
         if (dir == DIR_PUSH) {
             // ---- push: expand the bundles of F_L's queue (produced last epoch)
@@ -874,8 +890,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
             const uint2* seg = p.seg[e & 1];
             // CTA-major dealing: consecutive bundles (often one row) land on different SMs
             const unsigned long long step = (unsigned long long)gridDim.x * kWarps;
-            for (unsigned long long bi = (unsigned long long)wid * gridDim.x + blockIdx.x; bi < nb;
-                 bi += step) {
+            // CTA c owns bundles c, c + G, c + 2G, ... (a strided sample of the
+            // queue, so heavy rows spread over SMs); its warps take them one at a
+            // time from a shared counter, so fast warps do more of them
+            (void)step;
+            for (;;) {
+                unsigned long long bi = 0;
+                if (lane == 0) bi = (unsigned long long)atomicAdd(&s_task, 1u) * gridDim.x + blockIdx.x;
+                bi = __shfl_sync(FULL, bi, 0);
+                if (bi >= nb) break;
                 int sh = 0;
 #pragma unroll
                 for (int h = 128; h >= 1; h >>= 1)
@@ -978,7 +1001,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
             __syncthreads();
             const long long nblk = (Wn + kPullVerts - 1) / kPullVerts;
             const long long ntask = (long long)s_nptarget * nblk;
-            for (long long task = gwarp; task < ntask; task += nwarps) {
+            for (;;) {
+                long long task = 0;
+                if (lane == 0) task = (long long)atomicAdd(&s_task, 1u) * gridDim.x + blockIdx.x;
+                task = __shfl_sync(FULL, task, 0);
+                if (task >= ntask) break;
                 const int q2 = s_ptarget[task / nblk];
                 const long long word0 = (task % nblk) * kPullVerts;
                 uint32_t vis[kPullVerts];
@@ -1091,6 +1118,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
             uint32_t acc = 0;
             for (int f = 0; f < p.nfinals; ++f) acc |= __ldcg(p.visited + (long long)S.finals[f] * p.W + i);
             cnt += __popc(acc);
+            p.reach_bits[i] = acc;
             uint8_t* out = p.reach + i * 32;
             if (i * 32 + 32 <= p.nv) {
                 uint32_t bytes[8];
@@ -1107,7 +1135,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
         }
         // exact push-model TE = sum over (q, v) in P of q's group out-degrees x targets
         unsigned long long te = 0;
-        if (p.count_te) {
+        if (S.run->count_te) {
             for (int q = 0; q < p.nstates; ++q) {
                 if (S.gbeg[q + 1] == S.gbeg[q]) continue;
                 for (long long i = gtid; i < Wn; i += gthreads) {

@@ -19,6 +19,7 @@ import ctypes
 import dataclasses
 import math
 import time
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -78,15 +79,33 @@ class EvalResult:
     first access from ``reach``, the device's ``uint8[|V|]`` answer vector.
     """
 
-    __slots__ = ("reach", "_reachable", "iterations", "elapsed", "algorithm", "stats")
+    __slots__ = ("_reach", "_bits", "_nv", "_reachable", "iterations", "elapsed", "algorithm", "stats")
 
-    def __init__(self, reach, iterations, elapsed, algorithm, stats=None):
-        self.reach = reach
+    def __init__(self, reach, iterations, elapsed, algorithm, stats=None, bits=None, nv=None):
+        self._reach = reach
+        self._bits = bits  # answer bitmap as read back from the device (uint32 words)
+        self._nv = nv
         self._reachable = None
         self.iterations = iterations
         self.elapsed = elapsed
         self.algorithm = algorithm
         self.stats = stats
+
+    @property
+    def reach(self):
+        """uint8[|V|]: 1 where the vertex is an answer (decoded on first use)."""
+        if self._reach is None:
+            self._reach = bits_to_reach(self._bits, self._nv)
+        return self._reach
+
+    @property
+    def bits(self):
+        """The answer as uint32 words, bit v % 32 of word v // 32."""
+        if self._bits is None:
+            packed = np.packbits(self._reach, bitorder="little")
+            packed = np.concatenate([packed, np.zeros(-packed.size % 4, dtype=np.uint8)])
+            self._bits = packed.view(np.uint32)
+        return self._bits
 
     @property
     def reachable(self):
@@ -103,7 +122,7 @@ class EvalResult:
     __hash__ = None
 
     def __repr__(self):
-        return (f"EvalResult(|reachable|={int(np.count_nonzero(self.reach))}, "
+        return (f"EvalResult(|reachable|={len(self.reachable)}, "
                 f"iterations={self.iterations}, elapsed={self.elapsed:.6f}, "
                 f"algorithm={self.algorithm!r})")
 
@@ -141,12 +160,36 @@ def _iterations_for(algorithm, masked_iterations, nstarts):
     return masked_iterations
 
 
+_TABLES = {}  # id(automaton) -> (weakref, num_labels, TransitionTable)
+
+
+def _table_for(n, num_labels):
+    """transition_table(n, num_labels), cached per automaton object (compiled
+    automata are not mutated after compile; query_compiler.py treats them as
+    values)."""
+    hit = _TABLES.get(id(n))
+    if hit is not None and hit[0]() is n and hit[1] == num_labels:
+        return hit[2]
+    table = transition_table(n, num_labels)
+    try:
+        ref = weakref.ref(n, lambda _r, k=id(n): _TABLES.pop(k, None))
+    except TypeError:
+        return table
+    _TABLES[id(n)] = (ref, num_labels, table)
+    return table
+
+
+def bits_to_reach(words, nv):
+    """uint8[nv] answer vector from the answer bitmap (bit v%32 of word v/32)."""
+    return np.unpackbits(words.view(np.uint8), bitorder="little")[:nv]
+
+
 def _run(g, n, source, opts, tag, *, want_stats=False):
     opts.validate()
     _check_vertex(g, source)
     t0 = time.monotonic()
     dg = device_graph(g, opts.device)
-    table = transition_table(n, g.num_labels)
+    table = _table_for(n, g.num_labels)
     dg.ensure_labels(table.labels)
     lib = _lib.engine()
     q = dg.acquire_query(table)
@@ -154,6 +197,7 @@ def _run(g, n, source, opts, tag, *, want_stats=False):
         raise_for_status(lib.rpq_query_set_options(
             q, DIRECTIONS[opts.direction], int(opts.count_te or opts.debug_checks), opts.alpha),
             "rpq_query_set_options")
+        raise_for_status(lib.rpq_query_set_output(q, 1), "rpq_query_set_output")
         # _Clock.check(0) at the top of the first iteration (engine.py:87-89)
         remaining = opts.timeout - (time.monotonic() - t0)
         if remaining < 0 or opts.timeout == 0:
@@ -166,17 +210,19 @@ def _run(g, n, source, opts, tag, *, want_stats=False):
             raise QueryTimeout(time.monotonic() - t0,
                                _iterations_for(tag, stats.iterations, table.starts.size))
         raise_for_status(rc, "rpq_query_wait")
-        reach = np.empty(g.num_vertices, dtype=np.uint8)
+        # the answer bitmap is already in pinned host memory (output mode 1)
+        words = np.empty((g.num_vertices + 31) // 32, dtype=np.uint32)
         if g.num_vertices:
-            raise_for_status(lib.rpq_query_copy_reach(q, _lib.ptr(reach, ctypes.c_uint8)),
-                             "rpq_query_copy_reach")
+            raise_for_status(lib.rpq_query_copy_reach_bits(q, _lib.ptr(words, ctypes.c_uint32),
+                                                           words.size), "rpq_query_copy_reach_bits")
         iterations = _iterations_for(tag, stats.iterations, table.starts.size)
         if opts.debug_checks:
             _debug_invariants(lib, q, table, g.num_vertices, stats, iterations)
     finally:
         dg.release_query(table, q)
-    return EvalResult(reach, iterations, time.monotonic() - t0, tag,
-                      stats.to_dict() if want_stats or opts.debug_checks or opts.count_te else None)
+    return EvalResult(None, iterations, time.monotonic() - t0, tag,
+                      stats.to_dict() if want_stats or opts.debug_checks or opts.count_te else None,
+                      bits=words, nv=g.num_vertices)
 
 
 def _debug_invariants(lib, q, table, nv, stats, iterations):
