@@ -134,6 +134,13 @@ RPQ_API int rpq_query_wait(rpq_query* q, rpq_stats* stats);
 RPQ_API int rpq_query_reach_device(rpq_query* q, uint8_t** d_reach);
 /* Copy the answer of the last run to host (uint8[num_vertices], 1 = reachable). */
 RPQ_API int rpq_query_copy_reach(rpq_query* q, uint8_t* host_reach);
+/* One traversal step (step_update, engine.py:127-138): given the frontier M
+ * and the visited set P as bitmaps (nstates rows of row_words uint32 words,
+ * bit v%32 of word v/32), write mask_complement(step_sum(M), P) -- the pairs
+ * one symbol away from M that are not in P -- as a bitmap of the same shape.
+ * Synchronous. */
+RPQ_API int rpq_query_step(rpq_query* q, const uint32_t* m_words, const uint32_t* p_words, int64_t row_words,
+                           uint32_t* out_words);
 /* Output mode: 0 (default) keeps the answer on the device; 1 also copies the
  * answer bitmap (ceil(nv/32) uint32 words, bit v%32 of word v/32) into pinned
  * host memory as part of every run, ready after rpq_query_wait. */

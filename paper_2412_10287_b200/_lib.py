@@ -99,6 +99,7 @@ ENGINE_SIGNATURES = {
     "rpq_query_reach_device": (c_i32, [c_vp, ctypes.POINTER(P_u8)]),
     "rpq_query_copy_reach": (c_i32, [c_vp, P_u8]),
     "rpq_query_copy_visited": (c_i32, [c_vp, P_u32, c_i64]),
+    "rpq_query_step": (c_i32, [c_vp, P_u32, P_u32, c_i64, P_u32]),
     "rpq_query_set_output": (c_i32, [c_vp, c_i32]),
     "rpq_query_copy_reach_bits": (c_i32, [c_vp, P_u32, c_i64]),
     "rpq_query_io_bytes": (c_i32, [c_vp, P_i64, P_i64]),

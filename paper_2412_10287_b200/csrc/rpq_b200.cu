@@ -550,6 +550,7 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     // the pinned input block is read by the previous run's H2D copy: let it finish
     if (q->inflight) CUDA_TRY(cudaStreamSynchronize(q->last_stream));
     RunArgs ra{};
+    ra.mode = 0;
     ra.source = source;
     ra.dir_mode = q->dir_mode;
     ra.count_te = q->count_te;
@@ -642,6 +643,44 @@ int rpq_query_copy_visited(rpq_query* q, uint32_t* host_words, int64_t nwords) {
     CUDA_TRY(cudaStreamSynchronize(st));
     CUDA_TRY(cudaMemcpy2D(host_words, (size_t)words * 4, q->d_visited, (size_t)q->W * 4,
                           (size_t)words * 4, (size_t)q->nstates, cudaMemcpyDeviceToHost));
+    return RPQ_OK;
+}
+
+int rpq_query_step(rpq_query* q, const uint32_t* m_words, const uint32_t* p_words, int64_t row_words,
+                   uint32_t* out_words) {
+    if (!q || !m_words || !p_words || !out_words) return fail(RPQ_EINVAL, "null argument");
+    const int64_t words = ((int64_t)q->g->nv + 31) / 32;
+    if (row_words < words) return fail(RPQ_EINVAL, "row_words < ceil(num_vertices / 32)");
+    if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+    cudaStream_t st = q->own_stream;
+    if (q->inflight) CUDA_TRY(cudaStreamSynchronize(q->last_stream));
+    const size_t dpitch = (size_t)q->W * 4, spitch = (size_t)row_words * 4, width = (size_t)words * 4;
+    if (words > 0) {
+        CUDA_TRY(cudaMemset2DAsync(q->d_visited, dpitch, 0, dpitch, (size_t)q->nstates, st));
+        CUDA_TRY(cudaMemset2DAsync(q->d_fb[0], dpitch, 0, dpitch, (size_t)q->nstates, st));
+        CUDA_TRY(cudaMemcpy2DAsync(q->d_visited, dpitch, p_words, spitch, width, (size_t)q->nstates,
+                                   cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpy2DAsync(q->d_fb[0], dpitch, m_words, spitch, width, (size_t)q->nstates,
+                                   cudaMemcpyHostToDevice, st));
+    }
+    RunArgs ra{};
+    ra.mode = 1;
+    ra.dir_mode = 1;
+    ra.alpha = q->alpha;
+    ra.budget_ns = ~0ull;
+    *q->h_run = ra;
+    CUDA_TRY(cudaEventRecord(q->ev0, st));
+    CUDA_TRY(enqueue_run(q, st));
+    CUDA_TRY(cudaEventRecord(q->ev1, st));
+    q->last_stream = st;
+    q->ran = true;
+    q->inflight = true;
+    rpq_stats stats;
+    const int rc = rpq_query_wait(q, &stats);
+    if (rc != RPQ_OK) return rc;
+    if (words > 0)
+        CUDA_TRY(cudaMemcpy2D(out_words, spitch, q->d_fb[1], dpitch, width, (size_t)q->nstates,
+                              cudaMemcpyDeviceToHost));
     return RPQ_OK;
 }
 

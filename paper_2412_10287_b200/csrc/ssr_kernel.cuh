@@ -103,12 +103,13 @@ struct Ctl {
 // Per-run inputs, copied host->device with the automaton tables at the start
 // of every run (so a captured CUDA graph replays without parameter updates).
 struct RunArgs {
+    int mode;  // 0: full evaluation from `source`; 1: one step from (M = F_0, P = visited) given
     int source;
     int dir_mode;  // 0 auto, 1 push only, 2 pull after the seed
     int count_te;
     float alpha;   // pull when m_f * alpha > m_u
     unsigned long long budget_ns;
-    unsigned long long pad[2];
+    unsigned long long pad;
 };
 
 struct Params {
@@ -783,11 +784,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
 
     unsigned e = 0;  // barriers passed
 
-    // ---- epoch 0: P <- 0, F <- 0 --------------------------------------------
+    const bool step_mode = s_run.mode == 1;  // step_update (engine.py:127-138)
+    // ---- epoch 0: P <- 0, F <- 0 (step mode: P and F_0 = M come from the host)
     {
         uint4* v4 = reinterpret_cast<uint4*>(p.visited);
-        for (long long i = gtid; i < nbits4; i += gthreads) v4[i] = make_uint4(0, 0, 0, 0);
-        for (int f = 0; f < 3; ++f) {
+        if (!step_mode)
+            for (long long i = gtid; i < nbits4; i += gthreads) v4[i] = make_uint4(0, 0, 0, 0);
+        for (int f = step_mode ? 1 : 0; f < 3; ++f) {
             uint4* f4 = reinterpret_cast<uint4*>(p.fb[f]);
             for (long long i = gtid; i < nbits4; i += gthreads) f4[i] = make_uint4(0, 0, 0, 0);
         }
@@ -795,7 +798,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     grid_barrier(ctl, ++e);
 
     // ---- epoch 1: seed P = M = {(q_s, source)} (engine.py:106-109, :154-155)
-    {
+    if (!step_mode) {
         const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv};
         if (cta0) reset_qc(&ctl->qc[(e + 2) % 3], threadIdx.x);
         unsigned long long nnew = 0, nedge = 0;
@@ -820,8 +823,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
         __syncthreads();
         flush_counts(&ctl->fc[0].nnew, o, ctl->fc[0].state, nnew, nedge, s_red, s_state, p.nstates);
     }
-    grid_barrier(ctl, ++e);
-    if (wid == 0) decide_level(p, S, e, 0, DIR_PUSH, lane, &s_view, s_bpre, s_sv, s_front);
+    if (!step_mode) {
+        grid_barrier(ctl, ++e);
+        if (wid == 0) decide_level(p, S, e, 0, DIR_PUSH, lane, &s_view, s_bpre, s_sv, s_front);
+    } else if (threadIdx.x == 0) {
+        // one push step from F_0 = M: emit M's rows (plan epoch), expand, stop
+        s_view.done = 0;
+        s_view.dir = DIR_PUSH;
+        s_view.plan = 1;
+        s_view.status = 0;
+        s_view.iterations = 0;
+    }
+    if (step_mode)
+        for (int q = threadIdx.x; q < p.nstates; q += blockDim.x) s_front[q] = 1;
     __syncthreads();
 
     // ---- level loop -----------------------------------------------------------
@@ -1107,6 +1121,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
         grid_barrier(ctl, ++e);
         if (cta0 && threadIdx.x == 0 && L < 64) ctl->bar_ns[L] = globaltimer() - ctl->t0;
         ++L;
+        if (step_mode) {
+            if (threadIdx.x == 0) {
+                s_view.done = 1;
+                s_view.status = 1;  // (no answer projection in step mode)
+                if (cta0) ctl->iterations = 1;
+            }
+            __syncthreads();
+            break;
+        }
         if (wid == 0) decide_level(p, S, e, L, dir, lane, &s_view, s_bpre, s_sv, s_front);
         __syncthreads();
     }

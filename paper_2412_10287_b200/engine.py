@@ -298,13 +298,54 @@ def eval_ssr_batch(g, n, sources, opts):
     return out
 
 
+def _csr_to_bits(m, nstates, nv):
+    words = (nv + 31) // 32
+    out = np.zeros((nstates, max(words, 1)), dtype=np.uint32)
+    indptr = np.asarray(m.indptr, dtype=np.int64)
+    cols = np.asarray(m.indices, dtype=np.int64)
+    rows = np.repeat(np.arange(indptr.size - 1, dtype=np.int64), np.diff(indptr))
+    if cols.size:
+        np.bitwise_or.at(out, (rows, cols >> 5), (np.uint32(1) << (cols & 31).astype(np.uint32)))
+    return out
+
+
+def _bits_to_csr(bits, nv):
+    nstates = bits.shape[0]
+    dense = np.unpackbits(bits.view(np.uint8), axis=1, bitorder="little")[:, :nv]
+    rows, cols = np.nonzero(dense)
+    indptr = np.zeros(nstates + 1, dtype=np.int64)
+    np.add.at(indptr, rows + 1, 1)
+    np.cumsum(indptr, out=indptr)
+    return indptr, cols.astype(np.int64)
+
+
 def step_update(m, p, g, n, opts):
     """One traversal step (engine.py:127-138): the per-symbol products of the
-    frontier ``m``, minus everything in ``p``.  Not implemented on the device
-    yet; raises rather than falling back to a CPU path."""
+    frontier ``m``, minus everything in ``p`` -- on the device.  ``m`` and
+    ``p`` are |Q| x |V| Boolean matrices (the reference's SparseBoolMatrix or
+    any object with nrows/ncols/indptr/indices); the result has m's type."""
     if m.shape != p.shape:
         raise ValueError(f"step_update: frontier {m.shape} vs visited {p.shape}")
-    raise NotImplementedError("step_update has no device implementation yet")
+    opts.validate()
+    nstates, nv = m.shape
+    if nstates != n.nstates or nv != g.num_vertices:
+        raise ValueError(f"step_update: matrices must be {n.nstates}x{g.num_vertices}, got {m.shape}")
+    dg = device_graph(g, opts.device)
+    table = _table_for(n, g.num_labels)
+    dg.ensure_labels(table.labels)
+    lib = _lib.engine()
+    q = dg.acquire_query(table)
+    try:
+        mb = _csr_to_bits(m, nstates, nv)
+        pb = _csr_to_bits(p, nstates, nv)
+        out = np.zeros_like(mb)
+        if nv:
+            raise_for_status(lib.rpq_query_step(q, _lib.ptr(mb, ctypes.c_uint32), _lib.ptr(pb, ctypes.c_uint32),
+                                                mb.shape[1], _lib.ptr(out, ctypes.c_uint32)), "rpq_query_step")
+    finally:
+        dg.release_query(table, q)
+    indptr, indices = _bits_to_csr(out, nv)
+    return type(m)(nstates, nv, indptr, indices)
 
 
 class PreparedQuery:

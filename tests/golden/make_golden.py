@@ -39,6 +39,7 @@ sys.path.insert(0, ROOT)
 import helpers  # noqa: E402  (reference test helpers)
 from rpq.engine import (  # noqa: E402
     EngineOptions,
+    step_update,
     eval_sdr,
     eval_ssr,
     eval_ssr_hybrid,
@@ -150,6 +151,35 @@ def gen_random():
         }
         out.append(d)
     out.extend(known_answers())
+    return out
+
+
+def gen_steps():
+    """step_update (engine.py:127-138) on the RNG stream of
+    test_engine.py:318-329 (seed 12: single-pair frontier, empty P) and on
+    random frontiers / visited sets (seed 0x57)."""
+    out = []
+    rng = random.Random(12)
+    for i in range(20):
+        g = helpers.random_graph(rng, max_vertices=15, max_edges=60)
+        n = ref_compile(helpers.random_ast(rng, max_depth=3), g.label_ids)
+        m = SparseBoolMatrix.from_pairs(n.nstates, g.num_vertices, [(0, rng.randrange(g.num_vertices))])
+        pm = SparseBoolMatrix.zero(n.nstates, g.num_vertices)
+        r = step_update(m, pm, g, n, EngineOptions())
+        out.append({"tag": f"orders_12/{i}", "graph": graph_json(g), "nfa": nfa_json(n),
+                    "m": m.pairs(), "p": pm.pairs(), "expected": r.pairs()})
+    rng = random.Random(0x57)
+    for i in range(80):
+        g = helpers.random_graph(rng, max_vertices=30, max_edges=150)
+        n = ref_compile(helpers.random_ast(rng, unknown_label="zz"), g.label_ids)
+        allp = [(q, v) for q in range(n.nstates) for v in range(g.num_vertices)]
+        mp = [x for x in allp if rng.random() < 0.15]
+        pp = [x for x in allp if rng.random() < 0.3]
+        m = SparseBoolMatrix.from_pairs(n.nstates, g.num_vertices, mp)
+        pm = SparseBoolMatrix.from_pairs(n.nstates, g.num_vertices, pp)
+        r = step_update(m, pm, g, n, EngineOptions())
+        out.append({"tag": f"random_57/{i}", "graph": graph_json(g), "nfa": nfa_json(n),
+                    "m": m.pairs(), "p": pm.pairs(), "expected": r.pairs()})
     return out
 
 
@@ -266,6 +296,12 @@ def main():
         with gzip.open(path, "wt") as fh:
             json.dump(inst, fh)
         print(f"wrote {len(inst)} instances to {path}")
+    elif what == "steps":
+        out = gen_steps()
+        path = os.path.join(HERE, "step_update.json.gz")
+        with gzip.open(path, "wt") as fh:
+            json.dump(out, fh)
+        print(f"wrote {len(out)} step cases to {path}")
     elif what == "extra":
         labels = {c: i for i, c in enumerate("abcdefgh")}
         queries = ["^a (b|c)* d", "a ^b* c", "a b*", "(a|^b)* c+", "(a ^a)* (b | c ^d)*",

@@ -168,3 +168,14 @@ def test_config_automata_are_the_reference_compilations():
             n = automaton(nj)
             assert n.nstates == nj["nstates"]
             assert math.isfinite(n.nstates)
+
+
+def test_step_update_validates_shapes():
+    from paper_2412_10287_b200.graph import CsrMatrix
+
+    g = P.LabeledGraph.from_edges(3, ["a"], [(0, 0, 1)])
+    n = P.Automaton.build(1, {(0, False): [(0, 0)]}, [0], [0])
+    with pytest.raises(ValueError):  # test_engine.py:331-335
+        P.step_update(CsrMatrix.from_pairs(1, 2, []), CsrMatrix.from_pairs(2, 1, []), g, n, P.EngineOptions())
+    with pytest.raises(ValueError):
+        P.step_update(CsrMatrix.from_pairs(2, 3, []), CsrMatrix.from_pairs(2, 3, []), g, n, P.EngineOptions())

@@ -190,3 +190,18 @@ def test_cfg3_golden():
             res = P.eval_ssr(g, n, rec["source"], P.EngineOptions(timeout=math.inf, direction=direction))
             assert np.array_equal(res.reach, want), direction
             assert res.iterations == rec["iterations"]["hybrid"], direction
+
+
+def test_step_update_goldens():
+    """step_update (engine.py:127-138) against the reference's own results."""
+    from paper_2412_10287_b200.graph import CsrMatrix
+
+    for rec in load_golden("step_update.json.gz"):
+        g = host_graph(rec["graph"])
+        n = automaton(rec["nfa"])
+        shape = (n.nstates, g.num_vertices)
+        m = CsrMatrix.from_pairs(*shape, [tuple(x) for x in rec["m"]])
+        p = CsrMatrix.from_pairs(*shape, [tuple(x) for x in rec["p"]])
+        out = P.step_update(m, p, g, n, P.EngineOptions())
+        assert isinstance(out, CsrMatrix)
+        assert out.pairs() == [tuple(x) for x in rec["expected"]], rec["tag"]
