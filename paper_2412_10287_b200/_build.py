@@ -34,8 +34,11 @@ def _run(cmd):
 
 
 def build_engine(force=False):
+    import glob
+
     src = os.path.join(CSRC, "rpq_b200.cu")
-    deps = [src, os.path.join(INCLUDE, "rpq_b200.h"), __file__]
+    deps = (glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+            + glob.glob(os.path.join(INCLUDE, "*.h")) + [__file__])
     if force or _stale(ENGINE_SO, deps):
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-v", "-I", INCLUDE,

@@ -220,6 +220,7 @@ struct View {
     int plan;       // push level whose queue must first be emitted from F_L
     int status;
     int iterations;
+    unsigned long long nfront;  // |F_L|
 };
 
 // Grid barrier for a cooperative launch over a monotonic arrival counter:
@@ -292,6 +293,7 @@ struct Out {
     uint2* seg;
     uint2* bun;
     unsigned long long* s_resv;  // this CTA's shard fill: (segments << 32) | bundles
+    uint32_t bsz;                // edges per emitted bundle (32..kBundle)
 };
 
 // Warp-cooperative emission of the row segments of (state q, vertex w) pairs
@@ -339,7 +341,7 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
                     const uint32_t incl = warp_incl_scan(deg[k], lane);
                     excl[k] = incl - deg[k];
                     T[k] = __shfl_sync(FULL, incl, 31);
-                    nb[k] = (T[k] + kBundle - 1) / kBundle;
+                    nb[k] = (T[k] + o.bsz - 1) / o.bsz;
                     NS += nseg[k];
                     NB += nb[k];
                     TT += T[k];
@@ -369,8 +371,8 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
                 bool need_seg = false;
                 for (uint32_t kb0 = 0; kb0 < nb[k]; kb0 += 32) {
                     const uint32_t kb = kb0 + lane;
-                    const uint32_t pos = kb * kBundle;
-                    const uint32_t cnt = kb < nb[k] ? min((uint32_t)kBundle, T[k] - pos) : 1u;
+                    const uint32_t pos = kb * o.bsz;
+                    const uint32_t cnt = kb < nb[k] ? min(o.bsz, T[k] - pos) : 1u;
                     const uint32_t first = min(pos, T[k] - 1);
                     const int j = warp_upper_lane(excl[k], first);
                     const int jl = warp_upper_lane(excl[k], min(pos + cnt - 1, T[k] - 1));
@@ -417,7 +419,7 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
             const uint32_t incl = warp_incl_scan(take, lane);
             const uint32_t excl = incl - take;
             const uint32_t T = __shfl_sync(FULL, incl, 31);
-            const uint32_t nb = (T + kBundle - 1) / kBundle;
+            const uint32_t nb = (T + o.bsz - 1) / o.bsz;
             unsigned long long sbase = 0, bbase = 0, hlo = 0, hhi = 0;
             int ok = 1;
             if (lane == 0) ok = reserve(p, o.s_resv, o.qc, nseg, nb, &sbase, &bbase, &hlo, &hhi) ? 1 : 0;
@@ -434,12 +436,12 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
             if (hs) o.seg[sbase + rank] = make_uint2(lo, (take << 8) | (uint32_t)g);
             for (uint32_t kb0 = 0; kb0 < nb; kb0 += 32) {
                 const uint32_t kb = kb0 + lane;
-                const uint32_t pos = kb * kBundle;
+                const uint32_t pos = kb * o.bsz;
                 const int j = warp_upper_lane(excl, min(pos, T - 1));
                 const uint32_t exj = __shfl_sync(FULL, excl, j);
                 const int rj = __shfl_sync(FULL, rank, j);
                 if (kb < nb) {
-                    const uint32_t cnt = min((uint32_t)kBundle, T - pos);
+                    const uint32_t cnt = min(o.bsz, T - pos);
                     o.bun[bbase + kb] = make_uint2((uint32_t)(sbase + rj), ((pos - exj) << 7) | (cnt - 1));
                 }
             }
@@ -618,6 +620,13 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
             // m_f * alpha > m_u (Beamer's rule; alpha tuned for these kernels).
             const double nv = (double)p.nv;
             double mf = 0.0, mu = 0.0;
+            int ntarget = 0;  // states a pull level would scan
+            for (int q = lane; q < p.nstates; q += 32) {
+                bool t = false;
+                for (int k = S.ibeg[q]; k < S.ibeg[q + 1]; ++k) t |= s_front[S.isrc[k]] != 0;
+                ntarget += t ? 1 : 0;
+            }
+            for (int d = 16; d >= 1; d >>= 1) ntarget += __shfl_xor_sync(FULL, ntarget, d);
             for (int q = lane; q < p.nstates; q += 32) {
                 if (!produced_by_push && s_front[q])
                     for (int g = S.gbeg[q]; g < S.gbeg[q + 1]; ++g)
@@ -628,7 +637,15 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
             }
             mf = produced_by_push ? (double)nedge : warp_sum_f64(mf);
             mu = warp_sum_f64(mu);
-            next = (mf * (double)S.run->alpha > mu) ? DIR_PULL : DIR_PUSH;
+            if (produced_by_push) {
+                next = (mf * (double)S.run->alpha > mu) ? DIR_PULL : DIR_PUSH;
+            } else {
+                // after a pull level stay in pull while the frontier is large
+                // (Beamer: |F| > |V| / beta, beta = 24, with |V| counted once
+                // per state the pull would scan); switching back costs a plan
+                // epoch that re-emits F from its bitmap
+                next = ((double)nnew * 24.0 > nv * (double)ntarget) ? DIR_PULL : DIR_PUSH;
+            }
         }
         if (next == DIR_PUSH) {
             if (produced_by_push) {
@@ -648,6 +665,7 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
         v->plan = plan;
         v->status = status;
         v->iterations = iterations;
+        v->nfront = nnew;
         if (blockIdx.x == 0) {  // results and statistics
             const unsigned long long now = globaltimer();
             ctl->pairs += nnew;
@@ -799,7 +817,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
 
     // ---- epoch 1: seed P = M = {(q_s, source)} (engine.py:106-109, :154-155)
     if (!step_mode) {
-        const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv};
+        const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, 32u};
         if (cta0) reset_qc(&ctl->qc[(e + 2) % 3], threadIdx.x);
         unsigned long long nnew = 0, nedge = 0;
         if (cta0 && wid == 0) {
@@ -849,7 +867,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
 
         if (dir == DIR_PUSH && s_view.plan) {
             // ---- plan epoch: emit F_L's row segments from its bitmap (after pull)
-            const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv};
+            const uint32_t bsz = s_view.nfront < (unsigned long long)nwarps * 8 ? 32u : (uint32_t)kBundle;
+            const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, bsz};
             if (cta0) reset_qc(&ctl->qc[(e + 2) % 3], threadIdx.x);
             unsigned long long nedge = 0;
             for (int q = 0; q < p.nstates; ++q) {
@@ -883,7 +902,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
         }
 
         // ---- expand epoch of level L -------------------------------------------
-        const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv};
+        // small queues: emit small bundles so the next level spreads over more warps
+        const uint32_t bsz = (dir == DIR_PUSH ? s_bpre[kShards + 1] : s_view.nfront / 8) < (unsigned long long)nwarps
+                                 ? 32u : (uint32_t)kBundle;
+        const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, bsz};
         if (threadIdx.x == 0) s_task = 0;
         if (cta0) {
             reset_qc(&ctl->qc[(e + 2) % 3], threadIdx.x);
