@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -72,11 +73,12 @@ struct rpq_query {
     std::vector<Slot> slots;      // A_s for every slot, then A_s^T
     std::vector<unsigned long long> slot_nnz;
     int ngroups = 0, nslots = 0, ntargets = 0, nstarts = 0, nfinals = 0, nin = 0, maxT = 0;
-    int32_t* d_tables = nullptr;
-    Slot* d_slots = nullptr;
+    unsigned char* d_in = nullptr;  // per-run input block: RunArgs | slots | tables
+    unsigned char* h_in = nullptr;  // its pinned host copy
+    size_t in_bytes = 0, off_slots = 0, off_tables = 0;
+    unsigned int bar_next = 0;      // barrier counter value the next run starts from
     unsigned long long* d_slot_nnz = nullptr;
-    int32_t* h_tables = nullptr;  // pinned copies, re-sent with every run
-    Slot* h_slots = nullptr;
+
     uint32_t* d_visited = nullptr;
     uint32_t* d_fb[3] = {nullptr, nullptr, nullptr};
     uint2* d_seg[2] = {nullptr, nullptr};
@@ -87,8 +89,7 @@ struct rpq_query {
     uint32_t* d_reach_bits = nullptr;
     uint32_t* h_reach_bits = nullptr;  // pinned; filled by run() when output_mode == 1
     int output_mode = 0;
-    RunArgs* h_run = nullptr;  // pinned per-run inputs
-    RunArgs* d_run = nullptr;
+
     cudaGraphExec_t graph = nullptr;  // captured run sequence (per output mode)
     int graph_mode = -1;
     bool graph_failed = false;
@@ -166,8 +167,8 @@ int set_label_impl(rpq_graph* g, int32_t label, int64_t fn, const I* fp, const I
 }
 
 void free_query_buffers(rpq_query* q) {
-    if (q->d_tables) cudaFree(q->d_tables);
-    if (q->d_slots) cudaFree(q->d_slots);
+    if (q->d_in) cudaFree(q->d_in);
+    if (q->h_in) cudaFreeHost(q->h_in);
     if (q->d_slot_nnz) cudaFree(q->d_slot_nnz);
     if (q->d_visited) cudaFree(q->d_visited);
     for (int f = 0; f < 3; ++f)
@@ -176,15 +177,13 @@ void free_query_buffers(rpq_query* q) {
         if (q->d_seg[b]) cudaFree(q->d_seg[b]);
         if (q->d_bun[b]) cudaFree(q->d_bun[b]);
     }
-    if (q->h_tables) cudaFreeHost(q->h_tables);
-    if (q->h_slots) cudaFreeHost(q->h_slots);
+
     if (q->d_ctl) cudaFree(q->d_ctl);
     if (q->h_ctl) cudaFreeHost(q->h_ctl);
     if (q->d_reach) cudaFree(q->d_reach);
     if (q->d_reach_bits) cudaFree(q->d_reach_bits);
     if (q->h_reach_bits) cudaFreeHost(q->h_reach_bits);
-    if (q->h_run) cudaFreeHost(q->h_run);
-    if (q->d_run) cudaFree(q->d_run);
+
     if (q->graph) cudaGraphExecDestroy(q->graph);
     if (q->ev0) cudaEventDestroy(q->ev0);
     if (q->ev1) cudaEventDestroy(q->ev1);
@@ -396,8 +395,11 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
         if (e_ != cudaSuccess) return bail(cuda_fail(e_, #expr)); \
     } while (0)
     const size_t bitmap_bytes = (size_t)q->W * nstates * sizeof(uint32_t);
-    QTRY(cudaMalloc(&q->d_tables, std::max<size_t>(T.size(), 1) * sizeof(int32_t)));
-    QTRY(cudaMalloc(&q->d_slots, std::max<size_t>(q->slots.size(), 1) * sizeof(Slot)));
+    q->off_slots = (sizeof(RunArgs) + 15) / 16 * 16;
+    q->off_tables = q->off_slots + q->slots.size() * sizeof(Slot);
+    q->in_bytes = q->off_tables + std::max<size_t>(T.size(), 1) * sizeof(int32_t);
+    QTRY(cudaMalloc(&q->d_in, q->in_bytes));
+    QTRY(cudaMallocHost(&q->h_in, q->in_bytes));
     QTRY(cudaMalloc(&q->d_slot_nnz, std::max<size_t>(q->slot_nnz.size(), 1) * sizeof(unsigned long long)));
     QTRY(cudaMalloc(&q->d_visited, bitmap_bytes));
     for (int f = 0; f < 3; ++f) QTRY(cudaMalloc(&q->d_fb[f], bitmap_bytes));
@@ -413,15 +415,14 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     QTRY(cudaMalloc(&q->d_reach, (size_t)(q->W * 32 + 32)));
     QTRY(cudaMalloc(&q->d_reach_bits, (size_t)q->W * sizeof(uint32_t)));
     QTRY(cudaMallocHost(&q->h_reach_bits, (size_t)q->W * sizeof(uint32_t)));
-    QTRY(cudaMallocHost(&q->h_run, sizeof(RunArgs)));
-    QTRY(cudaMalloc(&q->d_run, sizeof(RunArgs)));
+
     QTRY(cudaStreamCreateWithFlags(&q->own_stream, cudaStreamNonBlocking));
     QTRY(cudaEventCreate(&q->ev0));
     QTRY(cudaEventCreate(&q->ev1));
-    QTRY(cudaMallocHost(&q->h_tables, std::max<size_t>(T.size(), 1) * sizeof(int32_t)));
-    QTRY(cudaMallocHost(&q->h_slots, std::max<size_t>(q->slots.size(), 1) * sizeof(Slot)));
-    if (!T.empty()) std::memcpy(q->h_tables, T.data(), T.size() * sizeof(int32_t));
-    if (!q->slots.empty()) std::memcpy(q->h_slots, q->slots.data(), q->slots.size() * sizeof(Slot));
+    std::memset(q->h_in, 0, q->in_bytes);
+    if (!q->slots.empty()) std::memcpy(q->h_in + q->off_slots, q->slots.data(), q->slots.size() * sizeof(Slot));
+    if (!T.empty()) std::memcpy(q->h_in + q->off_tables, T.data(), T.size() * sizeof(int32_t));
+    QTRY(cudaMemset(q->d_ctl, 0, sizeof(Ctl)));
     if (!q->slot_nnz.empty())
         QTRY(cudaMemcpy(q->d_slot_nnz, q->slot_nnz.data(), q->slot_nnz.size() * sizeof(unsigned long long),
                         cudaMemcpyHostToDevice));
@@ -451,9 +452,9 @@ namespace {
 
 Params make_params(const rpq_query* q) {
     Params p{};
-    p.run = q->d_run;
-    p.tables = q->d_tables;
-    p.slots = q->d_slots;
+    p.run = reinterpret_cast<const RunArgs*>(q->d_in);
+    p.tables = reinterpret_cast<const int32_t*>(q->d_in + q->off_tables);
+    p.slots = reinterpret_cast<const Slot*>(q->d_in + q->off_slots);
     p.slot_nnz = q->d_slot_nnz;
     p.visited = q->d_visited;
     for (int f = 0; f < 3; ++f) p.fb[f] = q->d_fb[f];
@@ -487,23 +488,16 @@ Params make_params(const rpq_query* q) {
 // block reset, the cooperative kernel, statistics (and answer bitmap) D2H.
 cudaError_t enqueue_run(rpq_query* q, cudaStream_t st) {
     cudaError_t e;
-    if ((e = cudaMemcpyAsync(q->d_run, q->h_run, sizeof(RunArgs), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    // inputs: run arguments + automaton tables in one pinned block
+    if ((e = cudaMemcpyAsync(q->d_in, q->h_in, q->in_bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
         return e;
-    if (!q->tables.empty() &&
-        (e = cudaMemcpyAsync(q->d_tables, q->h_tables, q->tables.size() * sizeof(int32_t),
-                             cudaMemcpyHostToDevice, st)) != cudaSuccess)
-        return e;
-    if (!q->slots.empty() &&
-        (e = cudaMemcpyAsync(q->d_slots, q->h_slots, q->slots.size() * sizeof(Slot), cudaMemcpyHostToDevice,
-                             st)) != cudaSuccess)
-        return e;
-    if ((e = cudaMemsetAsync(q->d_ctl, 0, sizeof(Ctl), st)) != cudaSuccess) return e;
     Params p = make_params(q);
     void* args[] = {&p};
     if ((e = cudaLaunchCooperativeKernel((const void*)ssr_kernel, dim3(q->grid), dim3(kThreads), args, q->smem,
                                          st)) != cudaSuccess)
         return e;
-    if ((e = cudaMemcpyAsync(q->h_ctl, q->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    // outputs: the control block's results prefix (and the answer bitmap)
+    if ((e = cudaMemcpyAsync(q->h_ctl, q->d_ctl, offsetof(Ctl, qc), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
         return e;
     if (q->output_mode == 1 && q->g->nv > 0 &&
         (e = cudaMemcpyAsync(q->h_reach_bits, q->d_reach_bits, (size_t)((q->g->nv + 31) / 32) * 4,
@@ -548,9 +542,14 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
     cudaStream_t st = stream ? (cudaStream_t)stream : q->own_stream;
     // the pinned input block is read by the previous run's H2D copy: let it finish
-    if (q->inflight) CUDA_TRY(cudaStreamSynchronize(q->last_stream));
+    if (q->inflight) {
+        CUDA_TRY(cudaStreamSynchronize(q->last_stream));
+        q->bar_next = q->h_ctl->bar;
+        q->inflight = false;
+    }
     RunArgs ra{};
     ra.mode = 0;
+    ra.bar_base = q->bar_next;
     ra.source = source;
     ra.dir_mode = q->dir_mode;
     ra.count_te = q->count_te;
@@ -559,7 +558,7 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
         ra.budget_ns = ~0ull;
     else
         ra.budget_ns = (unsigned long long)(timeout_s * 1e9);
-    *q->h_run = ra;
+    *reinterpret_cast<RunArgs*>(q->h_in) = ra;
     if (!q->graph_failed) build_graph(q);
     // timing events bracket the whole run (graph event nodes cannot be timed)
     CUDA_TRY(cudaEventRecord(q->ev0, st));
@@ -579,6 +578,7 @@ int rpq_query_wait(rpq_query* q, rpq_stats* stats) {
     if (!q->ran) return fail(RPQ_EINVAL, "query has not been run");
     CUDA_TRY(cudaStreamSynchronize(q->last_stream));
     q->inflight = false;
+    q->bar_next = q->h_ctl->bar;
     const Ctl& c = *q->h_ctl;
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, q->ev0, q->ev1));
@@ -653,7 +653,11 @@ int rpq_query_step(rpq_query* q, const uint32_t* m_words, const uint32_t* p_word
     if (row_words < words) return fail(RPQ_EINVAL, "row_words < ceil(num_vertices / 32)");
     if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
     cudaStream_t st = q->own_stream;
-    if (q->inflight) CUDA_TRY(cudaStreamSynchronize(q->last_stream));
+    if (q->inflight) {
+        CUDA_TRY(cudaStreamSynchronize(q->last_stream));
+        q->bar_next = q->h_ctl->bar;
+        q->inflight = false;
+    }
     const size_t dpitch = (size_t)q->W * 4, spitch = (size_t)row_words * 4, width = (size_t)words * 4;
     if (words > 0) {
         CUDA_TRY(cudaMemset2DAsync(q->d_visited, dpitch, 0, dpitch, (size_t)q->nstates, st));
@@ -668,7 +672,8 @@ int rpq_query_step(rpq_query* q, const uint32_t* m_words, const uint32_t* p_word
     ra.dir_mode = 1;
     ra.alpha = q->alpha;
     ra.budget_ns = ~0ull;
-    *q->h_run = ra;
+    ra.bar_base = q->bar_next;
+    *reinterpret_cast<RunArgs*>(q->h_in) = ra;
     CUDA_TRY(cudaEventRecord(q->ev0, st));
     CUDA_TRY(enqueue_run(q, st));
     CUDA_TRY(cudaEventRecord(q->ev1, st));
@@ -710,9 +715,9 @@ int rpq_query_copy_reach_bits(rpq_query* q, uint32_t* host_words, int64_t nwords
 int rpq_query_io_bytes(const rpq_query* q, int64_t* h2d_per_run, int64_t* d2h_per_run) {
     if (!q) return fail(RPQ_EINVAL, "null query");
     if (h2d_per_run)
-        *h2d_per_run = (int64_t)(q->tables.size() * sizeof(int32_t) + q->slots.size() * sizeof(Slot));
+        *h2d_per_run = (int64_t)q->in_bytes;
     if (d2h_per_run)
-        *d2h_per_run = (int64_t)sizeof(Ctl) + (q->output_mode == 1 ? ((int64_t)q->g->nv + 31) / 32 * 4 : 0);
+        *d2h_per_run = (int64_t)offsetof(Ctl, qc) + (q->output_mode == 1 ? ((int64_t)q->g->nv + 31) / 32 * 4 : 0);
     return RPQ_OK;
 }
 

@@ -77,13 +77,11 @@ struct FCnt {
 };
 
 struct Ctl {
-    unsigned int bar;        // monotonic barrier arrivals
+    // ---- results prefix: the only part copied back to the host ------------
+    unsigned int bar;        // monotonic barrier arrivals (never reset: runs continue from bar_base)
     int abort;
     unsigned long long t0;
-    QCnt qc[3];
-    FCnt fc[3];
-    // results, written by CTA 0 only
-    int status;
+    int status;              // written by CTA 0 only, as are the fields below
     int iterations;
     int levels;
     int pull_levels;
@@ -98,6 +96,9 @@ struct Ctl {
     unsigned long long work_ns[64];  // latest CTA finishing level L's work (from t0)
     unsigned long long bar_ns[64];   // CTA 0 leaving the barrier after level L
     int level_dir[64];
+    // ---- working counters (zeroed by CTA 0 at the start of every run) -----
+    QCnt qc[3];
+    FCnt fc[3];
 };
 
 // Per-run inputs, copied host->device with the automaton tables at the start
@@ -109,7 +110,8 @@ struct RunArgs {
     int count_te;
     float alpha;   // pull when m_f * alpha > m_u
     unsigned long long budget_ns;
-    unsigned long long pad;
+    unsigned int bar_base;  // barrier counter value this run starts from
+    unsigned int pad;
 };
 
 struct Params {
@@ -227,15 +229,15 @@ struct View {
 // barrier number e completes when e * gridDim.x arrivals are counted.
 // Waiters spin on a relaxed load and fence once afterwards (acquire side; the
 // fence also invalidates this SM's L1: CCTL.IVALL).
-__device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned epoch) {
+__device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned epoch, unsigned base) {
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(&ctl->bar, 1u);
-        const unsigned target = epoch * gridDim.x;
+        const unsigned target = base + epoch * gridDim.x;
         unsigned long long ts = 0;
         unsigned spins = 0;
-        while (ld_relaxed_u32(&ctl->bar) < target) {
+        while ((int)(ld_relaxed_u32(&ctl->bar) - target) < 0) {  // wrap-safe
             __nanosleep(16);
             if ((++spins & 4095u) == 0) {
                 const unsigned long long now = globaltimer();
@@ -798,7 +800,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     stage.q = s_stage[wid][0];
     stage.w = s_stage[wid][1];
     stage.n = 0;
-    if (gtid == 0) ctl->t0 = globaltimer();
+    // CTA 0 resets the control block (except the barrier counter, which only
+    // grows); nobody else reads it before the first barrier
+    if (cta0) {
+        unsigned char* z = reinterpret_cast<unsigned char*>(ctl) + 8;  // keep bar, abort set below
+        for (size_t i = threadIdx.x * 8; i + 8 <= sizeof(Ctl) - 8; i += (size_t)blockDim.x * 8)
+            *reinterpret_cast<unsigned long long*>(z + i) = 0ull;
+        if (threadIdx.x == 0) ctl->abort = 0;
+        __syncthreads();
+        if (threadIdx.x == 0) ctl->t0 = globaltimer();
+    }
 
     unsigned e = 0;  // barriers passed
 
@@ -813,7 +824,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
             for (long long i = gtid; i < nbits4; i += gthreads) f4[i] = make_uint4(0, 0, 0, 0);
         }
     }
-    grid_barrier(ctl, ++e);
+    grid_barrier(ctl, ++e, s_run.bar_base);
 
     // ---- epoch 1: seed P = M = {(q_s, source)} (engine.py:106-109, :154-155)
     if (!step_mode) {
@@ -842,7 +853,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
         flush_counts(&ctl->fc[0].nnew, o, ctl->fc[0].state, nnew, nedge, s_red, s_state, p.nstates);
     }
     if (!step_mode) {
-        grid_barrier(ctl, ++e);
+        grid_barrier(ctl, ++e, s_run.bar_base);
         if (wid == 0) decide_level(p, S, e, 0, DIR_PUSH, lane, &s_view, s_bpre, s_sv, s_front);
     } else if (threadIdx.x == 0) {
         // one push step from F_0 = M: emit M's rows (plan epoch), expand, stop
@@ -895,7 +906,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
             }
             __syncthreads();
             flush_counts(nullptr, o, nullptr, 0, nedge, s_red, s_state, 0);
-            grid_barrier(ctl, ++e);
+            grid_barrier(ctl, ++e, s_run.bar_base);
             if (wid == 0) decide_plan(p, e, L, lane, &s_view, s_bpre);
             __syncthreads();
             if (s_view.done) break;
@@ -1140,7 +1151,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
         if (threadIdx.x == 0 && L < 64) atomicMax(&ctl->work_ns[L], globaltimer() - ctl->t0);
         flush_counts(&ctl->fc[(L + 1) % 3].nnew, o, ctl->fc[(L + 1) % 3].state, nnew, nedge, s_red,
                      s_state, p.nstates);
-        grid_barrier(ctl, ++e);
+        grid_barrier(ctl, ++e, s_run.bar_base);
         if (cta0 && threadIdx.x == 0 && L < 64) ctl->bar_ns[L] = globaltimer() - ctl->t0;
         ++L;
         if (step_mode) {
