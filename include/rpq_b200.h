@@ -109,6 +109,19 @@ RPQ_API int rpq_graph_set_label(rpq_graph* g, int32_t label,
 RPQ_API int rpq_graph_set_label_i32(rpq_graph* g, int32_t label,
                             int64_t fwd_nnz, const int32_t* fwd_indptr, const int32_t* fwd_indices,
                             int64_t bwd_nnz, const int32_t* bwd_indptr, const int32_t* bwd_indices);
+/* Graph from an edge list (src[i] --label[i]--> dst[i], int32 vertex and
+ * label indices), ingested on the device: duplicates (src, label, dst)
+ * collapse, self-loops stay (graph_store.py:161-176).  A label's forward and
+ * backward CSR are built on the device the first time a query uses it (or by
+ * rpq_graph_materialize_label), so graphs with thousands of labels only pay
+ * for the labels queried. */
+RPQ_API int rpq_graph_create_coo(int32_t num_vertices, int32_t num_labels, int64_t nnz, const int32_t* src,
+                                 const int32_t* dst, const int32_t* label, int32_t device, rpq_graph** out);
+RPQ_API int rpq_graph_materialize_label(rpq_graph* g, int32_t label);
+/* Copy a resident label's CSR (transpose: the backward direction) to host:
+ * rowptr uint32[num_vertices+1], col int32[nnz]; either may be NULL. */
+RPQ_API int rpq_graph_copy_label(const rpq_graph* g, int32_t label, int32_t transpose, uint32_t* rowptr,
+                                 int32_t* col, int64_t col_capacity, int64_t* nnz);
 RPQ_API int rpq_graph_label_resident(const rpq_graph* g, int32_t label);
 RPQ_API int64_t rpq_graph_device_bytes(const rpq_graph* g);
 RPQ_API int rpq_graph_destroy(rpq_graph* g);

@@ -88,6 +88,10 @@ ENGINE_SIGNATURES = {
     "rpq_graph_create": (c_i32, [c_i32, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     "rpq_graph_set_label": (c_i32, [c_vp, c_i32, c_i64, P_i64, P_i64, c_i64, P_i64, P_i64]),
     "rpq_graph_set_label_i32": (c_i32, [c_vp, c_i32, c_i64, P_i32, P_i32, c_i64, P_i32, P_i32]),
+    "rpq_graph_create_coo": (c_i32, [c_i32, c_i32, c_i64, P_i32, P_i32, P_i32, c_i32,
+                                     ctypes.POINTER(c_vp)]),
+    "rpq_graph_materialize_label": (c_i32, [c_vp, c_i32]),
+    "rpq_graph_copy_label": (c_i32, [c_vp, c_i32, c_i32, P_u32, P_i32, c_i64, P_i64]),
     "rpq_graph_label_resident": (c_i32, [c_vp, c_i32]),
     "rpq_graph_device_bytes": (c_i64, [c_vp]),
     "rpq_graph_destroy": (c_i32, [c_vp]),

@@ -1,0 +1,65 @@
+// ingest.cuh -- device-side graph ingest: an edge list (src, label, dst) is
+// grouped by label on the device once; the canonical CSR of a label in either
+// direction (rows sorted, duplicates collapsed, self-loops kept -- the layout
+// of the reference's LabeledGraph: graph_store.py:161-176, sparse_bool.py:51-87)
+// is built on first use by a radix sort of packed (row, col) keys.
+#pragma once
+
+#include <cub/cub.cuh>
+
+namespace rpqk {
+
+// label histogram (one atomic per edge into shared memory, then global)
+__global__ void label_histogram_kernel(const int32_t* __restrict__ lab, long long n, int nl,
+                                       unsigned long long* __restrict__ hist) {
+    extern __shared__ unsigned int s_hist[];
+    const bool local = nl <= 8192;
+    if (local)
+        for (int i = threadIdx.x; i < nl; i += blockDim.x) s_hist[i] = 0;
+    __syncthreads();
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int l = lab[i];
+        if (l < 0 || l >= nl) continue;
+        if (local)
+            atomicAdd(&s_hist[l], 1u);
+        else
+            atomicAdd(&hist[l], 1ull);
+    }
+    __syncthreads();
+    if (local)
+        for (int i = threadIdx.x; i < nl; i += blockDim.x)
+            if (s_hist[i]) atomicAdd(&hist[i], (unsigned long long)s_hist[i]);
+}
+
+// scatter edges into their label's segment as packed (src << 32 | dst) keys
+__global__ void label_scatter_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                                     const int32_t* __restrict__ lab, long long n, int nl,
+                                     unsigned long long* __restrict__ cursor, unsigned long long* __restrict__ out) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int l = lab[i];
+        if (l < 0 || l >= nl) continue;
+        const unsigned long long pos = atomicAdd(&cursor[l], 1ull);
+        out[pos] = ((unsigned long long)(uint32_t)src[i] << 32) | (uint32_t)dst[i];
+    }
+}
+
+// keys (row << 32 | col) -> transposed keys (col << 32 | row)
+__global__ void swap_halves_kernel(const unsigned long long* __restrict__ in, unsigned long long* __restrict__ out,
+                                   long long n) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long k = in[i];
+        out[i] = (k << 32) | (k >> 32);
+    }
+}
+
+// sorted unique keys -> row counts (atomic) and columns
+__global__ void keys_to_csr_kernel(const unsigned long long* __restrict__ keys, long long n,
+                                   uint32_t* __restrict__ rowcnt, int32_t* __restrict__ col) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long k = keys[i];
+        col[i] = (int32_t)(uint32_t)k;
+        atomicAdd(&rowcnt[(uint32_t)(k >> 32) + 1], 1u);
+    }
+}
+
+}  // namespace rpqk

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "ssr_kernel.cuh"
+#include "ingest.cuh"
 
 using namespace rpqk;
 
@@ -64,6 +65,10 @@ struct rpq_graph {
     std::vector<LabelDev> labels;
     std::mutex mu;
     int64_t bytes = 0;
+    // device-ingested edge list (rpq_graph_create_coo): packed (src << 32 | dst)
+    // keys grouped by label; labels are built from it on first use
+    unsigned long long* d_coo = nullptr;
+    std::vector<unsigned long long> coo_off;  // nl + 1 segment offsets
 };
 
 struct rpq_query {
@@ -166,6 +171,89 @@ int set_label_impl(rpq_graph* g, int32_t label, int64_t fn, const I* fp, const I
     return RPQ_OK;
 }
 
+// Build label l's forward and backward CSR from the device edge list.
+int materialize_label(rpq_graph* g, int32_t l) {
+    LabelDev& L = g->labels[l];
+    if (L.resident) return RPQ_OK;
+    if (!g->d_coo) return fail(RPQ_ENOLABEL, "label " + std::to_string(l) + " is not resident");
+    const unsigned long long lo = g->coo_off[l], n = g->coo_off[l + 1] - lo;
+    const int64_t nv = g->nv;
+    int bits = 1;
+    while (bits < 32 && (1ll << bits) < nv) ++bits;
+    unsigned long long *keys = nullptr, *tmp = nullptr;
+    long long* d_nsel = nullptr;
+    void* temp = nullptr;
+    size_t temp_bytes = 0, need = 0;
+    auto cleanup = [&]() {
+        if (keys) cudaFree(keys);
+        if (tmp) cudaFree(tmp);
+        if (d_nsel) cudaFree(d_nsel);
+        if (temp) cudaFree(temp);
+    };
+#define MTRY(expr)                                                       \
+    do {                                                                 \
+        cudaError_t e_ = (expr);                                         \
+        if (e_ != cudaSuccess) {                                         \
+            cleanup();                                                   \
+            free_label(L);                                               \
+            return cuda_fail(e_, #expr);                                 \
+        }                                                                \
+    } while (0)
+    const size_t nn = (size_t)std::max<unsigned long long>(n, 1);
+    MTRY(cudaMalloc(&keys, nn * 8));
+    MTRY(cudaMalloc(&tmp, nn * 8));
+    MTRY(cudaMalloc(&d_nsel, sizeof(long long)));
+    MTRY(cub::DeviceRadixSort::SortKeys(nullptr, need, keys, tmp, (int)0, 0, 64));
+    temp_bytes = need;
+    if (n > 0) {
+        MTRY(cub::DeviceRadixSort::SortKeys(nullptr, need, keys, tmp, (long long)n, 0, 32 + bits));
+        temp_bytes = std::max(temp_bytes, need);
+        MTRY(cub::DeviceSelect::Unique(nullptr, need, tmp, keys, d_nsel, (long long)n));
+        temp_bytes = std::max(temp_bytes, need);
+    }
+    MTRY(cudaMalloc(&temp, std::max<size_t>(temp_bytes, 16)));
+    for (int dir = 0; dir < 2; ++dir) {
+        long long m = 0;
+        if (n > 0) {
+            // keys of this direction into `keys`, sort into `tmp`, unique back into `keys`
+            if (dir == 0)
+                MTRY(cudaMemcpy(keys, g->d_coo + lo, n * 8, cudaMemcpyDeviceToDevice));
+            else {
+                swap_halves_kernel<<<1184, 256>>>(g->d_coo + lo, keys, (long long)n);
+                MTRY(cudaGetLastError());
+            }
+            size_t tb = temp_bytes;
+            MTRY(cub::DeviceRadixSort::SortKeys(temp, tb, keys, tmp, (long long)n, 0, 32 + bits));
+            tb = temp_bytes;
+            MTRY(cub::DeviceSelect::Unique(temp, tb, tmp, keys, d_nsel, (long long)n));
+            long long nsel = 0;
+            MTRY(cudaMemcpy(&nsel, d_nsel, sizeof(long long), cudaMemcpyDeviceToHost));
+            m = nsel;
+        }
+        MTRY(cudaMalloc(&L.rowptr[dir], (size_t)(nv + 1) * sizeof(uint32_t)));
+        MTRY(cudaMalloc(&L.col[dir], (size_t)std::max<long long>(m, 1) * sizeof(int32_t)));
+        MTRY(cudaMemset(L.rowptr[dir], 0, (size_t)(nv + 1) * sizeof(uint32_t)));
+        if (m > 0) {
+            keys_to_csr_kernel<<<1184, 256>>>(keys, m, L.rowptr[dir], L.col[dir]);
+            MTRY(cudaGetLastError());
+            size_t tb = 0;
+            MTRY(cub::DeviceScan::InclusiveSum(nullptr, tb, L.rowptr[dir], L.rowptr[dir], (int)(nv + 1)));
+            void* t2 = nullptr;
+            MTRY(cudaMalloc(&t2, std::max<size_t>(tb, 16)));
+            cudaError_t e2 = cub::DeviceScan::InclusiveSum(t2, tb, L.rowptr[dir], L.rowptr[dir], (int)(nv + 1));
+            cudaFree(t2);
+            MTRY(e2);
+        }
+        L.nnz[dir] = m;
+        g->bytes += (nv + 1) * 4 + std::max<long long>(m, 1) * 4;
+    }
+    MTRY(cudaDeviceSynchronize());
+#undef MTRY
+    cleanup();
+    L.resident = true;
+    return RPQ_OK;
+}
+
 void free_query_buffers(rpq_query* q) {
     if (q->d_in) cudaFree(q->d_in);
     if (q->h_in) cudaFreeHost(q->h_in);
@@ -242,6 +330,102 @@ int rpq_graph_set_label_i32(rpq_graph* g, int32_t label, int64_t fwd_nnz, const 
                                    bwd_indices);
 }
 
+int rpq_graph_create_coo(int32_t num_vertices, int32_t num_labels, int64_t nnz, const int32_t* src,
+                         const int32_t* dst, const int32_t* label, int32_t device, rpq_graph** out) {
+    if (!out) return fail(RPQ_EINVAL, "null output handle");
+    *out = nullptr;
+    if (nnz < 0 || (nnz > 0 && (!src || !dst || !label))) return fail(RPQ_EINVAL, "null edge array");
+    rpq_graph* g = nullptr;
+    int rc = rpq_graph_create(num_vertices, num_labels, device, &g);
+    if (rc != RPQ_OK) return rc;
+    for (int64_t i = 0; i < nnz; i += 1 << 20) {  // validate on the host (cheap next to the upload)
+        const int64_t hi = std::min<int64_t>(nnz, i + (1 << 20));
+        for (int64_t j = i; j < hi; ++j)
+            if (src[j] < 0 || src[j] >= num_vertices || dst[j] < 0 || dst[j] >= num_vertices || label[j] < 0 ||
+                label[j] >= num_labels) {
+                rpq_graph_destroy(g);
+                return fail(RPQ_EINVAL, "edge " + std::to_string(j) + " out of range");
+            }
+    }
+    int32_t *d_src = nullptr, *d_dst = nullptr, *d_lab = nullptr;
+    unsigned long long *hist = nullptr, *cursor = nullptr;
+    auto cleanup = [&]() {
+        if (d_src) cudaFree(d_src);
+        if (d_dst) cudaFree(d_dst);
+        if (d_lab) cudaFree(d_lab);
+        if (hist) cudaFree(hist);
+        if (cursor) cudaFree(cursor);
+    };
+#define GTRY(expr)                                \
+    do {                                          \
+        cudaError_t e_ = (expr);                  \
+        if (e_ != cudaSuccess) {                  \
+            cleanup();                            \
+            rpq_graph_destroy(g);                 \
+            return cuda_fail(e_, #expr);          \
+        }                                         \
+    } while (0)
+    const size_t nn = (size_t)std::max<int64_t>(nnz, 1);
+    GTRY(cudaMalloc(&d_src, nn * 4));
+    GTRY(cudaMalloc(&d_dst, nn * 4));
+    GTRY(cudaMalloc(&d_lab, nn * 4));
+    GTRY(cudaMalloc(&g->d_coo, nn * 8));
+    GTRY(cudaMalloc(&hist, (size_t)(num_labels + 1) * 8));
+    GTRY(cudaMalloc(&cursor, (size_t)(num_labels + 1) * 8));
+    if (nnz > 0) {
+        GTRY(cudaMemcpy(d_src, src, nnz * 4, cudaMemcpyHostToDevice));
+        GTRY(cudaMemcpy(d_dst, dst, nnz * 4, cudaMemcpyHostToDevice));
+        GTRY(cudaMemcpy(d_lab, label, nnz * 4, cudaMemcpyHostToDevice));
+    }
+    GTRY(cudaMemset(hist, 0, (size_t)(num_labels + 1) * 8));
+    const int nl = num_labels;
+    if (nnz > 0 && nl > 0) {
+        const size_t sh = nl <= 8192 ? (size_t)nl * 4 : 0;
+        label_histogram_kernel<<<1184, 256, sh>>>(d_lab, nnz, nl, hist);
+        GTRY(cudaGetLastError());
+    }
+    std::vector<unsigned long long> h(nl + 1, 0);
+    if (nl > 0) GTRY(cudaMemcpy(h.data(), hist, (size_t)nl * 8, cudaMemcpyDeviceToHost));
+    g->coo_off.assign(nl + 1, 0);
+    for (int l = 0; l < nl; ++l) g->coo_off[l + 1] = g->coo_off[l] + h[l];
+    if (nl > 0) GTRY(cudaMemcpy(cursor, g->coo_off.data(), (size_t)nl * 8, cudaMemcpyHostToDevice));
+    if (nnz > 0 && nl > 0) {
+        label_scatter_kernel<<<1184, 256>>>(d_src, d_dst, d_lab, nnz, nl, cursor, g->d_coo);
+        GTRY(cudaGetLastError());
+    }
+    GTRY(cudaDeviceSynchronize());
+#undef GTRY
+    cleanup();
+    g->bytes += (int64_t)nn * 8;
+    *out = g;
+    return RPQ_OK;
+}
+
+int rpq_graph_materialize_label(rpq_graph* g, int32_t label) {
+    if (!g) return fail(RPQ_EINVAL, "null graph");
+    if (label < 0 || label >= g->nl) return fail(RPQ_EINVAL, "label index out of range");
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (cudaSetDevice(g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+    return materialize_label(g, label);
+}
+
+int rpq_graph_copy_label(const rpq_graph* g, int32_t label, int32_t transpose, uint32_t* rowptr, int32_t* col,
+                         int64_t col_capacity, int64_t* nnz) {
+    if (!g || label < 0 || label >= g->nl) return fail(RPQ_EINVAL, "bad graph or label");
+    const LabelDev& L = g->labels[label];
+    if (!L.resident) return fail(RPQ_ENOLABEL, "label " + std::to_string(label) + " is not resident");
+    const int d = transpose ? 1 : 0;
+    if (nnz) *nnz = L.nnz[d];
+    if (cudaSetDevice(g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+    if (rowptr)
+        CUDA_TRY(cudaMemcpy(rowptr, L.rowptr[d], ((size_t)g->nv + 1) * 4, cudaMemcpyDeviceToHost));
+    if (col) {
+        if (col_capacity < L.nnz[d]) return fail(RPQ_EINVAL, "column buffer too small");
+        if (L.nnz[d] > 0) CUDA_TRY(cudaMemcpy(col, L.col[d], (size_t)L.nnz[d] * 4, cudaMemcpyDeviceToHost));
+    }
+    return RPQ_OK;
+}
+
 int rpq_graph_label_resident(const rpq_graph* g, int32_t label) {
     if (!g || label < 0 || label >= g->nl) return 0;
     return g->labels[label].resident ? 1 : 0;
@@ -253,6 +437,7 @@ int rpq_graph_destroy(rpq_graph* g) {
     if (!g) return RPQ_OK;
     cudaSetDevice(g->device);
     for (auto& L : g->labels) free_label(L);
+    if (g->d_coo) cudaFree(g->d_coo);
     delete g;
     return RPQ_OK;
 }
@@ -300,9 +485,14 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     if ((int)slot_keys.size() > kMaxSlots) return fail(RPQ_EINVAL, "too many distinct symbols");
     if ((int)group_targets.size() > kMaxGroups)
         return fail(RPQ_EINVAL, "automaton has more than 256 (state, symbol) groups");
-    for (auto& k : slot_keys)
-        if (!g->labels[k.first].resident)
-            return fail(RPQ_ENOLABEL, "label " + std::to_string(k.first) + " is not resident");
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        if (cudaSetDevice(g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+        for (auto& k : slot_keys) {
+            const int rc = materialize_label(g, k.first);  // device edge list, if any
+            if (rc != RPQ_OK) return rc;
+        }
+    }
 
     rpq_query* q = new rpq_query();
     q->g = g;

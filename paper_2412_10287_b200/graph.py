@@ -197,7 +197,11 @@ def _raise_status(rc, what):
 class DeviceGraph:
     """Device-resident image of a host graph (``rpq_graph`` handle)."""
 
-    def __init__(self, host_graph, device=0):
+    def __init__(self, host_graph, device=0, ingest="auto"):
+        """ingest: "csr" uploads the host's per-label CSR (forward/backward);
+        "coo" uploads the edge list once and builds each label's CSR on the
+        device when a query first needs it; "auto" uses "coo" when the host
+        graph was built from an edge list (LabeledGraph.from_coo)."""
         try:  # weak, so the cache below does not keep host graphs alive
             self._host = weakref.ref(host_graph)
         except TypeError:
@@ -205,10 +209,21 @@ class DeviceGraph:
         self.device = int(device)
         self.num_vertices = int(host_graph.num_vertices)
         self.num_labels = int(host_graph.num_labels)
+        coo = getattr(host_graph, "_coo", None)
+        self.ingest = "coo" if ingest == "coo" or (ingest == "auto" and coo is not None) else "csr"
         lib = _lib.engine()
         handle = ctypes.c_void_p()
-        rc = lib.rpq_graph_create(self.num_vertices, self.num_labels, self.device,
-                                  ctypes.byref(handle))
+        if self.ingest == "coo":
+            if coo is None:
+                raise ValueError("ingest='coo' needs a graph built from an edge list")
+            src, dst, lab = coo
+            rc = lib.rpq_graph_create_coo(self.num_vertices, self.num_labels, int(src.size),
+                                          _lib.ptr(src, ctypes.c_int32), _lib.ptr(dst, ctypes.c_int32),
+                                          _lib.ptr(lab, ctypes.c_int32), self.device,
+                                          ctypes.byref(handle))
+        else:
+            rc = lib.rpq_graph_create(self.num_vertices, self.num_labels, self.device,
+                                      ctypes.byref(handle))
         if rc:
             _raise_status(rc, "rpq_graph_create")
         self.handle = handle
@@ -241,6 +256,11 @@ class DeviceGraph:
         for label in labels:
             if lib.rpq_graph_label_resident(self.handle, label):
                 continue
+            if self.ingest == "coo":
+                rc = lib.rpq_graph_materialize_label(self.handle, label)
+                if rc:
+                    _raise_status(rc, f"device build of label {label}")
+                continue
             host = self.host
             if host is None:
                 raise RuntimeError("host graph of this device image was released")
@@ -262,6 +282,21 @@ class DeviceGraph:
                     _lib.ptr(bi, ctypes.c_int64))
             if rc:
                 _raise_status(rc, f"upload of label {label}")
+
+    def label_csr(self, label, transpose=False):
+        """(rowptr uint32[|V|+1], col int32[nnz]) of a resident label, copied back."""
+        lib = _lib.engine()
+        nnz = ctypes.c_int64()
+        rc = lib.rpq_graph_copy_label(self.handle, label, int(transpose), None, None, 0, ctypes.byref(nnz))
+        if rc:
+            _raise_status(rc, "rpq_graph_copy_label")
+        rowptr = np.empty(self.num_vertices + 1, dtype=np.uint32)
+        col = np.empty(max(nnz.value, 1), dtype=np.int32)
+        rc = lib.rpq_graph_copy_label(self.handle, label, int(transpose), _lib.ptr(rowptr, ctypes.c_uint32),
+                                      _lib.ptr(col, ctypes.c_int32), col.size, ctypes.byref(nnz))
+        if rc:
+            _raise_status(rc, "rpq_graph_copy_label")
+        return rowptr, col[: nnz.value]
 
     @property
     def device_bytes(self):
