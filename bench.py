@@ -47,6 +47,11 @@ WORKLOADS = {
                         "16 Zipf(1.0) labels, query a ^b* c (3-state min DFA), source = max out-degree"),
     "cfg3": ("^a (b|c)* d", "cfg3: R-MAT scale 24 (16,777,216 V), edge factor 16, 64 Zipf(1.0) labels, "
                             "query ^a (b|c)* d (3-state min DFA), source = max out-degree"),
+    "cfg4": ("(a|b|c|d)*", "cfg4: Chung-Lu 90M V / 1.2B raw edges (exponent 2.1), 2,000 Zipf(1.1) labels, "
+                           "query (a|b|c|d)* (1-state min DFA), source = max out-degree"),
+    "cfg5": ("(a1 a2*) (a3 a4*) (a5 a6*) (a7 a8*) (a9 a10*) (a11 a12*) (a13 a14*) (a15 a16*)",
+             "cfg5: R-MAT scale 22, 32 Zipf(1.0) labels, 8-group chain query (9-state min DFA), "
+             "source = max out-degree"),
 }
 WORKLOAD = WORKLOADS[CONFIG][1]
 L2_FLUSH_BYTES = 256 << 20
@@ -61,6 +66,8 @@ def parse_args():
     ap.add_argument("--config", default=CONFIG)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--direction", choices=["auto", "push", "pull"], default="auto")
+    ap.add_argument("--emit-mode", type=int, default=None, help="tuning: 0 inline, 1 plan, 2 adaptive")
+    ap.add_argument("--emit-inline-max", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between steps (diagnostic)")
     ap.add_argument("--profile", action="store_true",
@@ -257,6 +264,7 @@ def run_engine(args, rank, world, local_rank):
     assert handle, "need a real stream handle"
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
+    pq.set_tuning(args.emit_mode, args.emit_inline_max)
     # one untimed run for the work counts (exact TE, |P|, levels) of this query
     pq.set_options(direction=args.direction, count_te=True)
     pq.launch(source, -1.0, handle)

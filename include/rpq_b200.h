@@ -137,6 +137,14 @@ RPQ_API int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans,
 /* Direction policy (RPQ_DIR_*), exact-TE accounting on/off, Beamer's alpha
  * (default: auto, off, 4).  Results do not depend on these. */
 RPQ_API int rpq_query_set_options(rpq_query* q, int32_t direction, int32_t count_te, double alpha);
+/* Tuning knobs (results do not depend on them):
+ *   RPQ_TUNE_EMIT_MODE: how a push level's successors get their work queue --
+ *     0 (default) at discovery, 1 from the frontier bitmap in vertex order
+ *     (an extra epoch per level), 2 by frontier size;
+ *   RPQ_TUNE_EMIT_INLINE_MAX: mode 2 emits at discovery while |F_L| < value. */
+#define RPQ_TUNE_EMIT_MODE 0
+#define RPQ_TUNE_EMIT_INLINE_MAX 1
+RPQ_API int rpq_query_set_tuning(rpq_query* q, int32_t key, double value);
 /* Enqueue one evaluation from `source` on `stream` (a cudaStream_t, or NULL for
  * the query's own stream).  timeout_s < 0 or inf: no deadline.  The deadline is
  * checked on the device at the top of every iteration, like _Clock.check. */

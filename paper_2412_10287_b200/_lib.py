@@ -98,6 +98,7 @@ ENGINE_SIGNATURES = {
     "rpq_query_create": (c_i32, [c_vp, c_i32, c_i32, P_i32, P_i32, P_u8, P_i32, c_i32, P_i32,
                                  c_i32, P_i32, ctypes.POINTER(c_vp)]),
     "rpq_query_set_options": (c_i32, [c_vp, c_i32, c_i32, c_dbl]),
+    "rpq_query_set_tuning": (c_i32, [c_vp, c_i32, c_dbl]),
     "rpq_query_run": (c_i32, [c_vp, c_i32, c_dbl, c_vp]),
     "rpq_query_wait": (c_i32, [c_vp, ctypes.POINTER(RpqStats)]),
     "rpq_query_reach_device": (c_i32, [c_vp, ctypes.POINTER(P_u8)]),

@@ -104,6 +104,8 @@ struct rpq_query {
     long long W = 0;
     int dir_mode = 0;
     int count_te = 0;
+    int emit_mode = 0;
+    unsigned int emit_inline_max = 1u << 16;
     float alpha = 4.0f;
     cudaStream_t own_stream = nullptr;
     cudaStream_t last_stream = nullptr;
@@ -725,6 +727,22 @@ void build_graph(rpq_query* q) {
 
 }  // namespace
 
+int rpq_query_set_tuning(rpq_query* q, int32_t key, double value) {
+    if (!q) return fail(RPQ_EINVAL, "null query");
+    switch (key) {
+        case RPQ_TUNE_EMIT_MODE:
+            if (value < 0 || value > 2) return fail(RPQ_EINVAL, "emit mode must be 0, 1 or 2");
+            q->emit_mode = (int)value;
+            return RPQ_OK;
+        case RPQ_TUNE_EMIT_INLINE_MAX:
+            if (value < 0 || value > 4.0e9) return fail(RPQ_EINVAL, "bad inline threshold");
+            q->emit_inline_max = (unsigned int)value;
+            return RPQ_OK;
+        default:
+            return fail(RPQ_EINVAL, "unknown tuning key");
+    }
+}
+
 int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) {
     if (!q) return fail(RPQ_EINVAL, "null query");
     if (source < 0 || source >= q->g->nv)
@@ -740,6 +758,8 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     RunArgs ra{};
     ra.mode = 0;
     ra.bar_base = q->bar_next;
+    ra.emit_mode = q->emit_mode;
+    ra.emit_inline_max = q->emit_inline_max;
     ra.source = source;
     ra.dir_mode = q->dir_mode;
     ra.count_te = q->count_te;

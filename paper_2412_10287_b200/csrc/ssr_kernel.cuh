@@ -111,7 +111,10 @@ struct RunArgs {
     float alpha;   // pull when m_f * alpha > m_u
     unsigned long long budget_ns;
     unsigned int bar_base;  // barrier counter value this run starts from
-    unsigned int pad;
+    int emit_mode;          // 0: emit F_{L+1}'s queue at discovery; 1: from F's bitmap
+                            // in vertex order (plan epoch); 2: by frontier size
+    unsigned int emit_inline_max;  // mode 2: inline while |F_L| < this
+    unsigned int pad2;
 };
 
 struct Params {
@@ -148,6 +151,8 @@ struct Smem {
     const int32_t* islot;    // [nin]
     const Slot* slots;       // [2*nslots]
     const RunArgs* run;      // this run's inputs (shared-memory copy)
+    uint64_t pf;             // L2 policy: evict first (graph, queues)
+    uint64_t pl;             // L2 policy: evict last (P and F bitmaps)
 };
 
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
@@ -168,6 +173,52 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
     return m;
 }
+
+// ---- L2 residency: the graph streams through L2 (evict-first); the P and F
+// bitmaps, probed at random, should stay resident (evict-last) ------------
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* a, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int32_t ld_stream_i32(const int32_t* a, uint64_t pol) {
+    int32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_queue(const uint2* a, uint64_t pol) {  // written earlier in this kernel
+    uint2 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_queue(uint2* a, uint2 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(a), "r"(v.x), "r"(v.y), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t ld_bits(const uint32_t* a, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint32_t or_bits(uint32_t* a, uint32_t b, uint64_t pol) {
+    uint32_t v;
+    asm volatile("atom.global.L2::cache_hint.or.b32 %0, [%1], %2, %3;" : "=r"(v) : "l"(a), "r"(b), "l"(pol) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_or_bits(uint32_t* a, uint32_t b, uint64_t pol) {
+    asm volatile("red.global.L2::cache_hint.or.b32 [%0], %1, %2;" ::"l"(a), "r"(b), "l"(pol) : "memory");
+}
+
 // control-plane loads after a fence: L2 (coherence point), weak, pipelined
 template <typename T>
 __device__ __forceinline__ T ldcg(const T* p) {
@@ -320,8 +371,8 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
             if (k < ng) {
                 g[k] = S.gbeg[q] + k;
                 const Slot sl = S.slots[S.gslot[g[k]]];
-                lo[k] = __ldg(sl.rowptr + w);
-                deg[k] = __ldg(sl.rowptr + w + 1);
+                lo[k] = ld_stream_u32(sl.rowptr + w, S.pf);
+                deg[k] = ld_stream_u32(sl.rowptr + w + 1, S.pf);
             }
         }
         bool huge = false;
@@ -390,11 +441,11 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
                             bd = make_uint2((uint32_t)(sbase + rj), ((pos - exj) << 7) | (cnt - 1));
                             need_seg = true;
                         }
-                        o.bun[bbase + kb] = bd;
+                        st_queue(o.bun + bbase + kb, bd, S.pf);
                     }
                 }
                 if (__any_sync(FULL, need_seg) && deg[k] > 0)
-                    o.seg[sbase + rank[k]] = make_uint2(lo[k], (deg[k] << 8) | (uint32_t)g[k]);
+                    st_queue(o.seg + sbase + rank[k], make_uint2(lo[k], (deg[k] << 8) | (uint32_t)g[k]), S.pf);
                 sbase += nseg[k];
                 bbase += nb[k];
             }
@@ -408,8 +459,8 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
         if (k < ng) {
             g = S.gbeg[q] + k;
             const Slot sl = S.slots[S.gslot[g]];
-            lo = __ldg(sl.rowptr + w);
-            deg = __ldg(sl.rowptr + w + 1) - lo;
+            lo = ld_stream_u32(sl.rowptr + w, S.pf);
+            deg = ld_stream_u32(sl.rowptr + w + 1, S.pf) - lo;
         }
         for (;;) {  // rows longer than a segment are split (rare)
             const uint32_t take = min(deg, kSegLenMax);
@@ -576,7 +627,7 @@ __device__ __forceinline__ void queue_scan(const Params& p, const QCnt* qc, int 
 // CTA reads the same counters and reaches the same result).  Mirrors the
 // masked loop (engine.py:156-160): run while the frontier is non-empty,
 // check the deadline, then step; and picks the direction of level L.
-__device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, int prev_dir, int lane,
+__device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, int prev_queued, int lane,
                              View* v, unsigned long long* s_bpre, unsigned long long* s_sv,
                              unsigned int* s_front) {
     Ctl* ctl = p.ctl;
@@ -595,7 +646,8 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
         s_sv[q] += f;
     }
     __syncwarp();
-    const int produced_by_push = (L == 0) || prev_dir == DIR_PUSH;
+    // F_L's queue was emitted at discovery (exact m_f and bundles available)
+    const int produced_by_push = prev_queued;
     int done = 0, iterations = 0, status = 0, next = DIR_PUSH, plan = 0;
     long long ledges = -1;
     if (abort) {
@@ -774,6 +826,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     }
     if (threadIdx.x == 0) s_run = *p.run;
     Smem S;
+    S.pf = policy_evict_first();
+    S.pl = policy_evict_last();
     S.run = &s_run;
     S.slots = s_slots;
     S.gbeg = s_tab;
@@ -854,7 +908,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     }
     if (!step_mode) {
         grid_barrier(ctl, ++e, s_run.bar_base);
-        if (wid == 0) decide_level(p, S, e, 0, DIR_PUSH, lane, &s_view, s_bpre, s_sv, s_front);
+        if (wid == 0) decide_level(p, S, e, 0, 1, lane, &s_view, s_bpre, s_sv, s_front);
     } else if (threadIdx.x == 0) {
         // one push step from F_0 = M: emit M's rows (plan epoch), expand, stop
         s_view.done = 0;
@@ -930,6 +984,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
         }
         __syncthreads();  // s_task
         unsigned long long nnew = 0, nedge = 0;
+        // emit F_{L+1}'s queue now (at discovery) or later from F's bitmap
+        const bool emit_inline = dir == DIR_PUSH &&
+                                 (s_run.emit_mode == 0 ||
+                                  (s_run.emit_mode == 2 && s_view.nfront < s_run.emit_inline_max));
+        const int queued = emit_inline ? 1 : 0;
         if (dir == DIR_PUSH) {
             // ---- push: expand the bundles of F_L's queue (produced last epoch)
             const unsigned long long nb = s_bpre[kShards + 1];
@@ -950,7 +1009,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
 #pragma unroll
                 for (int h = 128; h >= 1; h >>= 1)
                     if (sh + h <= kShards && s_bpre[sh + h] <= bi) sh += h;
-                const uint2 bd = __ldcg(bun + (unsigned long long)sh * p.shard_buncap + (bi - s_bpre[sh]));
+                const uint2 bd = ld_queue(bun + (unsigned long long)sh * p.shard_buncap + (bi - s_bpre[sh]), S.pf);
                 if (bd.y == kHoleY) continue;
                 const uint32_t cnt = (bd.y & 127u) + 1;
                 int w[kEdgesPerLane], gj[kEdgesPerLane];
@@ -962,14 +1021,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                     for (int u = 0; u < kEdgesPerLane; ++u) {
                         const uint32_t ed = (uint32_t)(lane + 32 * u);
                         gj[u] = ed < cnt ? g : -1;
-                        w[u] = ed < cnt ? __ldg(col + ed) : 0;
+                        w[u] = ed < cnt ? ld_stream_i32(col + ed, S.pf) : 0;
                     }
                 } else {
                     const uint32_t s0 = bd.x;
                     const uint32_t off = (bd.y >> 7) & 0xFFFFFFu;
                     uint32_t my_start = 0, my_len = 0, my_grp = 0;
                     if ((unsigned long long)s0 + lane < p.seg_alloc) {
-                        const uint2 sg = __ldcg(seg + s0 + lane);
+                        const uint2 sg = ld_queue(seg + s0 + lane, S.pf);
                         my_start = sg.x;
                         my_len = sg.y >> 8;
                         my_grp = sg.y & 0xFFu;
@@ -990,7 +1049,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                         const uint32_t exj = __shfl_sync(FULL, excl, j);
                         const int g = (int)__shfl_sync(FULL, my_grp, j);
                         gj[u] = active ? g : -1;
-                        w[u] = active ? __ldg(S.slots[S.gslot[g]].col + sj + (ed - exj)) : 0;
+                        w[u] = active ? ld_stream_i32(S.slots[S.gslot[g]].col + sj + (ed - exj), S.pf) : 0;
                     }
                 }
                 // probe P for every target, then claim with atomicOr
@@ -1005,7 +1064,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                             const int t0 = S.toff[gj[u]];
                             if (t0 + k < S.toff[gj[u] + 1]) {
                                 q2[u] = S.targets[t0 + k];
-                                old[u] = p.visited[(long long)q2[u] * p.W + (w[u] >> 5)];
+                                old[u] = ld_bits(p.visited + (long long)q2[u] * p.W + (w[u] >> 5), S.pl);
                             }
                         }
                     }
@@ -1014,8 +1073,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                         const uint32_t bit = 1u << (w[u] & 31);
                         if (q2[u] >= 0 && !(old[u] & bit)) {
                             const long long off2 = (long long)q2[u] * p.W + (w[u] >> 5);
-                            old[u] = atomicOr(p.visited + off2, bit);
-                            if (!(old[u] & bit)) atomicOr(fnext + off2, bit);
+                            old[u] = or_bits(p.visited + off2, bit, S.pl);
+                            if (!(old[u] & bit)) red_or_bits(fnext + off2, bit, S.pl);
                         } else {
                             old[u] = 0xFFFFFFFFu;
                         }
@@ -1025,12 +1084,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                         const bool fresh = q2[u] >= 0 && !(old[u] & (1u << (w[u] & 31)));
                         nnew += fresh ? 1 : 0;
                         if (fresh) atomicAdd(&s_state[q2[u]], 1u);
-                        const uint32_t T = stage_add(p, S, o, stage, fresh, q2[u], w[u], lane);
-                        if (lane == 0) nedge += T;
+                        if (emit_inline) {
+                            const uint32_t T = stage_add(p, S, o, stage, fresh, q2[u], w[u], lane);
+                            if (lane == 0) nedge += T;
+                        }
                     }
                 }
             }
-            {
+            if (emit_inline) {
                 const uint32_t T = stage_flush(p, S, o, stage, lane);
                 if (lane == 0) nedge += T;
             }
@@ -1060,7 +1121,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                 int w[kPullVerts];
 #pragma unroll
                 for (int u = 0; u < kPullVerts; ++u)
-                    vis[u] = word0 + u < Wn ? p.visited[(long long)q2 * p.W + word0 + u] : 0xFFFFFFFFu;
+                    vis[u] = word0 + u < Wn ? ld_bits(p.visited + (long long)q2 * p.W + word0 + u, S.pl) : 0xFFFFFFFFu;
                 bool any_need = false;
 #pragma unroll
                 for (int u = 0; u < kPullVerts; ++u) {
@@ -1085,8 +1146,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                     uint32_t lo[kPullVerts], hi[kPullVerts];
 #pragma unroll
                     for (int u = 0; u < kPullVerts; ++u) {
-                        lo[u] = look[u] ? __ldg(ps.rowptr + w[u]) : 0u;
-                        hi[u] = look[u] ? __ldg(ps.rowptr + w[u] + 1) : 0u;
+                        lo[u] = look[u] ? ld_stream_u32(ps.rowptr + w[u], S.pf) : 0u;
+                        hi[u] = look[u] ? ld_stream_u32(ps.rowptr + w[u] + 1, S.pf) : 0u;
                     }
                     // the first kPullInline in-edges of every vertex: all loads in flight together
                     int cand[kPullVerts][kPullInline];
@@ -1094,13 +1155,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                     for (int u = 0; u < kPullVerts; ++u)
 #pragma unroll
                         for (int i = 0; i < kPullInline; ++i)
-                            cand[u][i] = (lo[u] + i < hi[u]) ? __ldg(ps.col + lo[u] + i) : -1;
+                            cand[u][i] = (lo[u] + i < hi[u]) ? ld_stream_i32(ps.col + lo[u] + i, S.pf) : -1;
                     uint32_t fw[kPullVerts][kPullInline];
 #pragma unroll
                     for (int u = 0; u < kPullVerts; ++u)
 #pragma unroll
                         for (int i = 0; i < kPullInline; ++i)
-                            fw[u][i] = cand[u][i] >= 0 ? frow[cand[u][i] >> 5] : 0u;
+                            fw[u][i] = cand[u][i] >= 0 ? ld_bits(frow + (cand[u][i] >> 5), S.pl) : 0u;
 #pragma unroll
                     for (int u = 0; u < kPullVerts; ++u)
 #pragma unroll
@@ -1120,11 +1181,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                                 int uu[4];
 #pragma unroll
                                 for (int c = 0; c < 4; ++c)
-                                    uu[c] = ed + 32 * c + lane < rhi ? __ldg(ps.col + ed + 32 * c + lane) : -1;
+                                    uu[c] = ed + 32 * c + lane < rhi ? ld_stream_i32(ps.col + ed + 32 * c + lane, S.pf) : -1;
                                 bool h = false;
 #pragma unroll
                                 for (int c = 0; c < 4; ++c)
-                                    if (uu[c] >= 0) h |= (frow[uu[c] >> 5] >> (uu[c] & 31)) & 1u;
+                                    if (uu[c] >= 0) h |= (ld_bits(frow + (uu[c] >> 5), S.pl) >> (uu[c] & 31)) & 1u;
                                 if (__ballot_sync(FULL, h)) {
                                     hit = true;
                                     break;
@@ -1163,7 +1224,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
             __syncthreads();
             break;
         }
-        if (wid == 0) decide_level(p, S, e, L, dir, lane, &s_view, s_bpre, s_sv, s_front);
+        if (wid == 0) decide_level(p, S, e, L, queued, lane, &s_view, s_bpre, s_sv, s_front);
         __syncthreads();
     }
 

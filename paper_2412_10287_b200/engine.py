@@ -367,6 +367,14 @@ class PreparedQuery:
         raise_for_status(_lib.engine().rpq_query_set_options(
             self.q, DIRECTIONS[direction], int(count_te), float(alpha)), "rpq_query_set_options")
 
+    def set_tuning(self, emit_mode=None, emit_inline_max=None):
+        lib = _lib.engine()
+        if emit_mode is not None:
+            raise_for_status(lib.rpq_query_set_tuning(self.q, 0, float(emit_mode)), "rpq_query_set_tuning")
+        if emit_inline_max is not None:
+            raise_for_status(lib.rpq_query_set_tuning(self.q, 1, float(emit_inline_max)),
+                             "rpq_query_set_tuning")
+
     def launch(self, source, timeout=-1.0, stream=None):
         _check_vertex(self.g, source)
         raise_for_status(_lib.engine().rpq_query_run(self.q, int(source), float(timeout), stream),
