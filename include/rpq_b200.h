@@ -86,6 +86,27 @@ typedef struct rpq_stats {
     int8_t level_dir[RPQ_STATS_LEVELS];     /* 0 push, 1 pull */
 } rpq_stats;
 
+/* Multi-source batches: up to RPQ_BATCH sources per run (one bit each). */
+#define RPQ_BATCH 32
+
+typedef struct rpq_batch_stats {
+    int32_t status;          /* RPQ_* of the run */
+    int32_t nsrc;            /* sources in the run */
+    int32_t levels;          /* levels expanded (max over the batch) */
+    int32_t grid;            /* CTAs of the persistent kernel */
+    int64_t te;              /* sum over sources of product edges traversed (exact) */
+    int64_t rows;            /* edges read: each frontier row once for all sources holding it */
+    int64_t visited_pairs;   /* sum over sources of |P_s| */
+    float device_ms;         /* CUDA-event time of the run */
+    int32_t iterations[RPQ_BATCH];   /* per source: masked-loop iterations (engine.py:157-160),
+                                        i.e. non-empty frontiers incl. the seed */
+    int64_t reach_count[RPQ_BATCH];  /* per source: |answer_s| */
+    int64_t level_items[RPQ_STATS_LEVELS];  /* (state, vertex) items with a non-empty source word */
+    int64_t level_new[RPQ_STATS_LEVELS];    /* (pair, source) discoveries forming level L */
+    int64_t level_ns[RPQ_STATS_LEVELS];     /* kernel start -> level L starts (CTA 0) */
+    int64_t level_rows[RPQ_STATS_LEVELS];   /* edges read before level L starts */
+} rpq_batch_stats;
+
 /* level direction policy (rpq_query_set_options) */
 #define RPQ_DIR_AUTO 0   /* per level: pull when m_f * alpha > m_u (Beamer) */
 #define RPQ_DIR_PUSH 1   /* always expand the frontier's rows (SpMSpV over CSR) */
@@ -175,6 +196,20 @@ RPQ_API int rpq_query_copy_visited(rpq_query* q, uint32_t* host_words, int64_t n
  * bitmap in output mode 1). */
 RPQ_API int rpq_query_io_bytes(const rpq_query* q, int64_t* h2d_per_run, int64_t* d2h_per_run);
 RPQ_API int rpq_query_destroy(rpq_query* q);
+
+/* ---- multi-source batches (eval_ssr_batch) ---------------
+ * One run evaluates the query from nsrc <= RPQ_BATCH sources at once; answer
+ * row s equals rpq_query_run(sources[s]).  Frontier rows are shared by the
+ * sources that hold them at the same level (bit-sliced source words).
+ * Workspaces are allocated on the first batch run of a query. */
+RPQ_API int rpq_query_run_batch(rpq_query* q, int32_t nsrc, const int32_t* sources, double timeout_s,
+                                void* stream);
+RPQ_API int rpq_query_wait_batch(rpq_query* q, rpq_batch_stats* stats);
+/* Answer bitmaps of the last batch run: nsrc rows of row_words uint32 words
+ * (>= ceil(nv/32)), bit v%32 of word v/32 of row s = v reachable from sources[s]. */
+RPQ_API int rpq_query_copy_batch_bits(rpq_query* q, uint32_t* host_words, int64_t row_words);
+/* Device pointer to the same bitmaps (RPQ_BATCH rows of *row_words words). */
+RPQ_API int rpq_query_batch_bits_device(rpq_query* q, uint32_t** d_bits, int64_t* row_words);
 
 /* One-shot eval_ssr. */
 RPQ_API int rpq_ssr(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_t* t_src,

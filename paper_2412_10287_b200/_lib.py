@@ -80,6 +80,47 @@ class RpqStats(ctypes.Structure):
         }
 
 
+BATCH = 32
+
+
+class RpqBatchStats(ctypes.Structure):
+    _fields_ = [
+        ("status", c_i32),
+        ("nsrc", c_i32),
+        ("levels", c_i32),
+        ("grid", c_i32),
+        ("te", c_i64),
+        ("rows", c_i64),
+        ("visited_pairs", c_i64),
+        ("device_ms", ctypes.c_float),
+        ("iterations", c_i32 * BATCH),
+        ("reach_count", c_i64 * BATCH),
+        ("level_items", c_i64 * STATS_LEVELS),
+        ("level_new", c_i64 * STATS_LEVELS),
+        ("level_ns", c_i64 * STATS_LEVELS),
+        ("level_rows", c_i64 * STATS_LEVELS),
+    ]
+
+    def to_dict(self):
+        nlev = min(max(self.levels, 0), STATS_LEVELS)
+        return {
+            "status": self.status,
+            "nsrc": self.nsrc,
+            "levels": self.levels,
+            "grid": self.grid,
+            "te": self.te,
+            "rows": self.rows,
+            "visited_pairs": self.visited_pairs,
+            "device_ms": self.device_ms,
+            "iterations": list(self.iterations[: self.nsrc]),
+            "reach_count": list(self.reach_count[: self.nsrc]),
+            "level_items": list(self.level_items[:nlev]),
+            "level_new": list(self.level_new[:nlev]),
+            "level_us": [t / 1e3 for t in self.level_ns[:nlev]],
+            "level_rows": list(self.level_rows[:nlev]),
+        }
+
+
 # symbol -> (restype, argtypes); the complete C ABI of include/rpq_b200.h
 ENGINE_SIGNATURES = {
     "rpq_abi_version": (c_i32, []),
@@ -109,6 +150,10 @@ ENGINE_SIGNATURES = {
     "rpq_query_copy_reach_bits": (c_i32, [c_vp, P_u32, c_i64]),
     "rpq_query_io_bytes": (c_i32, [c_vp, P_i64, P_i64]),
     "rpq_query_destroy": (c_i32, [c_vp]),
+    "rpq_query_run_batch": (c_i32, [c_vp, c_i32, P_i32, c_dbl, c_vp]),
+    "rpq_query_wait_batch": (c_i32, [c_vp, ctypes.POINTER(RpqBatchStats)]),
+    "rpq_query_copy_batch_bits": (c_i32, [c_vp, P_u32, c_i64]),
+    "rpq_query_batch_bits_device": (c_i32, [c_vp, ctypes.POINTER(P_u32), P_i64]),
     "rpq_ssr": (c_i32, [c_vp, c_i32, c_i32, P_i32, P_i32, P_u8, P_i32, c_i32, P_i32, c_i32, P_i32,
                         c_i32, c_dbl, P_u8, ctypes.POINTER(RpqStats)]),
 }

@@ -1,0 +1,527 @@
+// batch_kernel.cuh -- up to 32 single-source 2-RPQs from different sources in
+// ONE persistent launch, bit-sliced: every (state q, vertex v) pair carries a
+// 32-bit word whose bit s says "(q, v) belongs to source s's set".  Per source
+// this is exactly the masked evaluator (rpq/engine.py:146-171):
+//   M_s <- step(M_s) <not P_s>;  P_s <- P_s + M_s
+// but a frontier row v is read ONCE for all sources whose frontier holds
+// (q, v) at that level, so adjacency traffic is shared across the batch
+// (SURVEY.md §8(d) "batched sources", §8(e) regime 1).
+//
+// Layout:
+//   vis[q][v]   uint32 source word: P, one row of nvp words per state
+//   fw[L&1]     uint32 source word: M at level L (same shape); a word is
+//               cleared when its item is expanded, so fw[(L+1)&1] is all zero
+//               again when level L+1 starts writing it
+//   list[L&1]   items (v, q) with fw[L&1][q][v] != 0, each once: appended by
+//               the discovery that turns the word from 0 to non-zero
+//   heavy       row chunks (lo, hi, group, word) of rows longer than
+//               kLightDeg, expanded in a second phase of the level
+// Per level: phase 1 expands light rows warp-cooperatively (prefix sum over
+// the 32 items' degrees, 32 edges per step) and cuts heavy rows into chunks;
+// phase 2 (only when chunks exist) spreads the chunks over every warp.
+#pragma once
+
+namespace rpqk {
+
+constexpr int kBatch = 32;             // sources per launch (bits of a source word)
+constexpr uint32_t kLightDeg = 64;     // rows up to this many edges stay in phase 1
+constexpr uint32_t kChunk = 256;       // edges per heavy chunk
+constexpr int kBStage = 64;            // staged list appends per warp
+
+struct BCnt {
+    unsigned int nlist;       // |list_L|
+    unsigned int nheavy;      // heavy chunks produced while expanding level L
+    unsigned int overflow;
+    unsigned int expire;      // the deadline check at the top of level L failed
+    unsigned long long nnew;  // (pair, source) discoveries forming M_L
+    unsigned int active;      // sources with a non-empty M_L
+    unsigned int pad;
+};
+
+struct BCtl {
+    // ---- results prefix (copied back to the host) ------------------------
+    unsigned int bar;  // monotonic barrier arrivals (runs continue from bar_base)
+    int abort;
+    unsigned long long t0;
+    int status;
+    int levels;
+    unsigned long long te;     // sum over sources of product-graph edges expanded
+    unsigned long long rows;   // edges read: sum over items of the row length (shared by a word's sources)
+    unsigned long long pairs;  // sum over sources of |P_s|
+    int last_level[kBatch];    // last level with a non-empty M_s
+    unsigned long long reach_count[kBatch];
+    unsigned long long level_items[64];
+    unsigned long long level_new[64];
+    unsigned long long level_ns[64];
+    unsigned long long level_rows[64];  // edges read at level L (cumulative counter snapshot)
+    unsigned int level_active[64];
+    // ---- working counters ------------------------------------------------
+    BCnt bc[3];
+};
+
+struct BatchArgs {
+    int nsrc;
+    unsigned int bar_base;
+    unsigned long long budget_ns;
+    int sources[kBatch];
+};
+
+struct BParams {
+    const BatchArgs* run;
+    const int32_t* tables;
+    const Slot* slots;
+    uint32_t* vis;
+    uint32_t* fw[2];
+    uint2* list[2];
+    uint4* heavy;
+    BCtl* ctl;
+    uint32_t* out;  // [kBatch][W] answer bitmaps
+    long long nvp;  // words per state row of vis / fw (>= nv, multiple of 128)
+    long long W;    // words per answer row (multiple of 4)
+    unsigned long long list_cap, heavy_cap;
+    int nv, nstates, ngroups, nslots, ntargets, nstarts, nfinals, nin, table_ints;
+};
+
+struct BWarp {  // per-warp state of an expansion phase
+    uint2* buf;  // staged appends (shared memory, kBStage entries)
+    int n;
+};
+
+constexpr int kBEdges = 4;  // edges per lane in flight per step
+
+__device__ __forceinline__ void bflush(const BParams& p, BCnt* nxt, uint2* lst, BWarp& st, int lane, bool all) {
+    const int m = all ? st.n : 32;
+    if (m <= 0) return;
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(&nxt->nlist, (unsigned)m);
+    base = __shfl_sync(FULL, base, 0);
+    if (lane < m) {
+        if ((unsigned long long)base + lane < p.list_cap)
+            lst[base + lane] = st.buf[lane];
+        else
+            atomicExch(&nxt->overflow, 1u);
+    }
+    __syncwarp();
+    const bool mv = lane + m < st.n;
+    uint2 t = make_uint2(0, 0);
+    if (mv) t = st.buf[m + lane];
+    __syncwarp();
+    if (mv) st.buf[lane] = t;
+    __syncwarp();
+    st.n -= m;
+}
+
+// Source words w[c] reach (t[c], u[c]) (K edges per lane, loads overlapped):
+// the sources not yet at (t, u) join P and M_{L+1}.  P is read first (from
+// L2) and only ORed into where that read shows missing bits; the read may
+// miss bits set earlier in this level, never bits of earlier levels, so the
+// bits ORed into M_{L+1} are exactly the discoveries of this level (a bit may
+// be discovered by several edges; the item is listed once: by the OR that
+// turns M_{L+1}'s word from zero).
+template <int K>
+__device__ __forceinline__ void bvisit(const BParams& p, uint32_t* fnext, BCnt* nxt, uint2* lst,
+                                       const bool (&act)[K], const int (&t)[K], const int (&u)[K],
+                                       const uint32_t (&w)[K], BWarp& st, int lane) {
+    long long off[K];
+    uint32_t seen[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+        off[c] = (long long)t[c] * p.nvp + u[c];
+        seen[c] = act[c] ? __ldcg(p.vis + off[c]) : 0xFFFFFFFFu;
+    }
+    bool app[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+        const uint32_t nw = w[c] & ~seen[c];
+        app[c] = false;
+        if (nw) {
+            atomicOr(p.vis + off[c], nw);  // result unused: RED
+            app[c] = atomicOr(fnext + off[c], nw) == 0u;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+        const unsigned m = __ballot_sync(FULL, app[c]);
+        if (m) {
+            if (app[c]) st.buf[st.n + __popc(m & lanemask_lt())] = make_uint2((uint32_t)u[c], (uint32_t)t[c]);
+            st.n += __popc(m);
+            __syncwarp();
+            if (st.n >= 32) bflush(p, nxt, lst, st, lane, false);
+        }
+    }
+}
+
+// End of a phase: staged appends out; per-CTA sums of the items' statistics
+// (|M_L| and its sources, into `cnt`) and of the edges read.
+__device__ __forceinline__ void bphase_end(const BParams& p, BCnt* nxt, uint2* lst, BWarp& st, int lane,
+                                           unsigned long long te, unsigned long long rows,
+                                           unsigned long long nnew, uint32_t act, BCnt* cnt,
+                                           unsigned long long* s_red, unsigned* s_or) {
+    bflush(p, nxt, lst, st, lane, true);
+    const int wid = threadIdx.x >> 5;
+    unsigned long long a = warp_sum_u64(nnew), b = warp_sum_u64(te), r = warp_sum_u64(rows);
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) act |= __shfl_xor_sync(FULL, act, d);
+    if (lane == 0) {
+        s_red[3 * wid] = a;
+        s_red[3 * wid + 1] = b;
+        s_red[3 * wid + 2] = r;
+        if (act) atomicOr(s_or, act);
+    }
+    __syncthreads();
+    if (wid == 0) {
+        a = lane < kWarps ? s_red[3 * lane] : 0ull;
+        b = lane < kWarps ? s_red[3 * lane + 1] : 0ull;
+        r = lane < kWarps ? s_red[3 * lane + 2] : 0ull;
+        a = warp_sum_u64(a);
+        b = warp_sum_u64(b);
+        r = warp_sum_u64(r);
+        if (lane == 0) {
+            if (a) atomicAdd(&cnt->nnew, a);
+            if (b) atomicAdd(&p.ctl->te, b);
+            if (r) atomicAdd(&p.ctl->rows, r);
+            if (*s_or) atomicOr(&cnt->active, *s_or);
+            *s_or = 0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ unsigned long long s_red[3 * kWarps];
+    __shared__ uint2 s_buf[kWarps][kBStage];
+    __shared__ unsigned s_or;
+    __shared__ unsigned s_task;
+    __shared__ int s_single;  // every (state, symbol) group has exactly one target (a DFA)
+    __shared__ BatchArgs s_run;
+
+    Slot* s_slots = reinterpret_cast<Slot*>(smem_raw);
+    int32_t* s_tab = reinterpret_cast<int32_t*>(smem_raw + sizeof(Slot) * 2 * p.nslots);
+    for (int i = threadIdx.x; i < 2 * p.nslots; i += blockDim.x) s_slots[i] = p.slots[i];
+    for (int i = threadIdx.x; i < p.table_ints; i += blockDim.x) s_tab[i] = p.tables[i];
+    if (threadIdx.x == 0) {
+        s_run = *p.run;
+        s_or = 0;
+    }
+    const int32_t* gbeg = s_tab;
+    const int32_t* gslot = gbeg + p.nstates + 1;
+    const int32_t* toff = gslot + p.ngroups;
+    const int32_t* targets = toff + p.ngroups + 1;
+    const int32_t* starts = targets + p.ntargets;
+    const int32_t* finals = starts + p.nstarts;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int one = 1;
+        for (int g = 0; g < p.ngroups; ++g) one &= (toff[g + 1] - toff[g]) == 1;
+        s_single = one;
+    }
+
+    BCtl* ctl = p.ctl;
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long gthreads = (long long)gridDim.x * blockDim.x;
+    const bool cta0 = blockIdx.x == 0;
+    BWarp st;
+    st.buf = s_buf[wid];
+    st.n = 0;
+    if (cta0) {  // reset the control block (except the barrier counter)
+        unsigned char* z = reinterpret_cast<unsigned char*>(ctl) + 8;
+        for (size_t i = threadIdx.x * 8; i + 8 <= sizeof(BCtl) - 8; i += (size_t)blockDim.x * 8)
+            *reinterpret_cast<unsigned long long*>(z + i) = 0ull;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            ctl->abort = 0;
+            ctl->t0 = globaltimer();
+        }
+        for (int s = threadIdx.x; s < kBatch; s += blockDim.x) ctl->last_level[s] = -1;
+    }
+    __syncthreads();
+    const unsigned bar_base = s_run.bar_base;
+    unsigned e = 0;
+
+    // ---- epoch 0: P <- 0, M <- 0 for every source
+    {
+        const long long n4 = (long long)p.nstates * p.nvp / 4;
+        uint4* a = reinterpret_cast<uint4*>(p.vis);
+        uint4* b = reinterpret_cast<uint4*>(p.fw[0]);
+        uint4* c = reinterpret_cast<uint4*>(p.fw[1]);
+        const uint4 z = make_uint4(0, 0, 0, 0);
+        for (long long i = gtid; i < n4; i += gthreads) {
+            a[i] = z;
+            b[i] = z;
+            c[i] = z;
+        }
+    }
+    grid_barrier_on(&ctl->bar, &ctl->abort, ++e, bar_base);
+
+    // ---- epoch 1: seed P_s = M_s = {(q_s, source_s)} (engine.py:106-109)
+    if (cta0 && wid == 0) {
+        const bool act = lane < s_run.nsrc;
+        const int src = act ? s_run.sources[lane] : 0;
+        for (int i = 0; i < p.nstarts; ++i) {
+            const int q = starts[i];
+            const long long off = (long long)q * p.nvp + src;
+            bool app = false;
+            if (act) {
+                const uint32_t bit = 1u << lane;
+                atomicOr(p.vis + off, bit);
+                app = atomicOr(p.fw[0] + off, bit) == 0u;
+            }
+            const unsigned m = __ballot_sync(FULL, app);
+            if (app) st.buf[st.n + __popc(m & lanemask_lt())] = make_uint2((uint32_t)src, (uint32_t)q);
+            st.n += __popc(m);
+            __syncwarp();
+            if (st.n >= 32) bflush(p, &ctl->bc[0], p.list[0], st, lane, false);
+        }
+    }
+    bphase_end(p, &ctl->bc[0], p.list[0], st, lane, 0ull, 0ull, 0ull, 0u, &ctl->bc[0], s_red, &s_or);
+    grid_barrier_on(&ctl->bar, &ctl->abort, ++e, bar_base);
+
+    // ---- level loop
+    int status = 0;
+    int L = 0;
+    for (;;) {
+        BCnt* cur = &ctl->bc[L % 3];
+        BCnt* nxt = &ctl->bc[(L + 1) % 3];
+        const unsigned ncur = ldcg(&cur->nlist);
+        const unsigned ovf = ldcg(&cur->overflow);
+        const unsigned expire = ldcg(&cur->expire);
+        const int abort = ldcg(&ctl->abort);
+        if (abort) {
+            status = ST_DEADLOCK;
+            break;
+        }
+        if (ovf) {
+            status = ST_OVERFLOW;
+            break;
+        }
+        if (cta0 && threadIdx.x == 0) {
+            const unsigned long long now = globaltimer();
+            BCnt* old = &ctl->bc[(L + 2) % 3];  // level L-1's counters: statistics, then reset
+            if (L > 0) {
+                const unsigned act = ldcg(&old->active);
+                const unsigned long long nn = ldcg(&old->nnew);
+                for (int s = 0; s < kBatch; ++s)
+                    if (act >> s & 1u) ctl->last_level[s] = L - 1;
+                ctl->pairs += nn;
+                if (L - 1 < 64) {
+                    ctl->level_new[L - 1] = nn;
+                    ctl->level_active[L - 1] = act;
+                }
+            }
+            old->nlist = 0;
+            old->nheavy = 0;
+            old->overflow = 0;
+            old->expire = 0;
+            old->nnew = 0;
+            old->active = 0;
+            if (L < 64) {
+                ctl->level_items[L] = ncur;
+                ctl->level_ns[L] = now - ctl->t0;
+                ctl->level_rows[L] = ldcg(&ctl->rows);
+            }
+            if (ncur) ctl->levels = L + 1;
+            if (now - ctl->t0 > s_run.budget_ns) nxt->expire = 1;
+        }
+        if (ncur == 0) break;
+        if (expire) {  // _Clock.check at the top of the iteration (engine.py:87-89)
+            status = RPQ_ETIMEOUT;
+            break;
+        }
+        const uint2* lcur = p.list[L & 1];
+        uint2* lnext = p.list[(L + 1) & 1];
+        uint32_t* fcur = p.fw[L & 1];
+        uint32_t* fnext = p.fw[(L + 1) & 1];
+        if (threadIdx.x == 0) s_task = 0;
+        __syncthreads();
+
+        // ---- phase 1: light rows; heavy rows become chunks
+        unsigned long long te = 0, rows = 0, nnew = 0;
+        uint32_t active = 0;
+        for (;;) {
+            unsigned k = 0;
+            if (lane == 0) k = atomicAdd(&s_task, 1u);
+            k = __shfl_sync(FULL, k, 0);
+            const unsigned long long task = blockIdx.x + (unsigned long long)k * gridDim.x;
+            if (task * 32 >= ncur) break;
+            const unsigned long long i = task * 32 + lane;
+            const bool valid = i < ncur;
+            uint2 it = make_uint2(0, 0);
+            uint32_t w = 0;
+            if (valid) {
+                it = lcur[i];
+                const long long off = (long long)it.y * p.nvp + it.x;
+                w = fcur[off];
+                fcur[off] = 0u;  // fw[L&1] must be zero when level L+1 writes it
+            }
+            nnew += __popc(w);  // M_L's (pair, source) members, each in exactly one item
+            active |= w;
+            const int v = (int)it.x, q = (int)it.y;
+            const int ng = valid ? gbeg[q + 1] - gbeg[q] : 0;
+            int maxng = ng;
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) maxng = max(maxng, __shfl_xor_sync(FULL, maxng, d));
+            for (int kg = 0; kg < maxng; ++kg) {
+                int g = 0;
+                uint32_t lo = 0, deg = 0;
+                if (kg < ng) {
+                    g = gbeg[q] + kg;
+                    const Slot sl = s_slots[gslot[g]];
+                    lo = sl.rowptr[v];
+                    deg = sl.rowptr[v + 1] - lo;
+                }
+                te += (unsigned long long)deg * __popc(w);
+                rows += deg;
+                // heavy rows -> chunks of kChunk edges (one atomic per warp)
+                const bool heavy = deg > kLightDeg;
+                const uint32_t nch = heavy ? (deg + kChunk - 1) / kChunk : 0u;
+                const uint32_t cincl = warp_incl_scan(nch, lane);
+                const uint32_t ctot = __shfl_sync(FULL, cincl, 31);
+                if (ctot) {
+                    unsigned cbase = 0;
+                    if (lane == 0) cbase = atomicAdd(&cur->nheavy, ctot);
+                    cbase = __shfl_sync(FULL, cbase, 0);
+                    if (heavy) {
+                        unsigned long long c0 = (unsigned long long)cbase + cincl - nch;
+                        for (uint32_t c = 0; c < nch; ++c) {
+                            if (c0 + c < p.heavy_cap) {
+                                const uint32_t a = lo + c * kChunk;
+                                const uint32_t b = min(lo + deg, a + kChunk);
+                                p.heavy[c0 + c] = make_uint4(a, b, (uint32_t)g, w);
+                            } else {
+                                atomicExch(&nxt->overflow, 1u);
+                            }
+                        }
+                    }
+                }
+                if (heavy) deg = 0;
+                // light rows: kBEdges x 32 edges per step over the warp's concatenated rows
+                const uint32_t incl = warp_incl_scan(deg, lane);
+                const uint32_t excl = incl - deg;
+                const uint32_t T = __shfl_sync(FULL, incl, 31);
+                if (s_single) {
+                    for (uint32_t e0 = 0; e0 < T; e0 += 32 * kBEdges) {
+                        bool act[kBEdges];
+                        int tt[kBEdges], uu[kBEdges];
+                        uint32_t ww[kBEdges];
+#pragma unroll
+                        for (int c = 0; c < kBEdges; ++c) {
+                            const uint32_t x = e0 + 32 * c + lane;
+                            const int j = warp_upper_lane(excl, x);
+                            const uint32_t lo_j = __shfl_sync(FULL, lo, j);
+                            const uint32_t ex_j = __shfl_sync(FULL, excl, j);
+                            const int g_j = __shfl_sync(FULL, g, j);
+                            ww[c] = __shfl_sync(FULL, w, j);
+                            act[c] = x < T;
+                            uu[c] = act[c] ? s_slots[gslot[g_j]].col[lo_j + (x - ex_j)] : 0;
+                            tt[c] = act[c] ? targets[toff[g_j]] : 0;
+                        }
+                        bvisit<kBEdges>(p, fnext, nxt, lnext, act, tt, uu, ww, st, lane);
+                    }
+                } else {
+                    for (uint32_t e0 = 0; e0 < T; e0 += 32) {
+                        const uint32_t x = e0 + lane;
+                        const int j = warp_upper_lane(excl, x);
+                        const uint32_t lo_j = __shfl_sync(FULL, lo, j);
+                        const uint32_t ex_j = __shfl_sync(FULL, excl, j);
+                        const int g_j = __shfl_sync(FULL, g, j);
+                        const uint32_t w_j = __shfl_sync(FULL, w, j);
+                        const bool a0 = x < T;
+                        const int u = a0 ? s_slots[gslot[g_j]].col[lo_j + (x - ex_j)] : 0;
+                        // targets of g_j: warp-uniform trip count
+                        const int t0 = a0 ? toff[g_j] : 0, t1 = a0 ? toff[g_j + 1] : 0;
+                        int nt = t1 - t0;
+                        for (int d = 16; d >= 1; d >>= 1) nt = max(nt, __shfl_xor_sync(FULL, nt, d));
+                        for (int k2 = 0; k2 < nt; ++k2) {
+                            const bool act[1] = {a0 && t0 + k2 < t1};
+                            const int tt[1] = {act[0] ? targets[t0 + k2] : 0};
+                            const int uu[1] = {u};
+                            const uint32_t ww[1] = {w_j};
+                            bvisit<1>(p, fnext, nxt, lnext, act, tt, uu, ww, st, lane);
+                        }
+                    }
+                }
+            }
+        }
+        bphase_end(p, nxt, lnext, st, lane, te, rows, nnew, active, cur, s_red, &s_or);
+        grid_barrier_on(&ctl->bar, &ctl->abort, ++e, bar_base);
+
+        // ---- phase 2: heavy chunks, spread over every warp of the grid
+        const unsigned nh = min((unsigned long long)ldcg(&cur->nheavy), p.heavy_cap);
+        if (nh) {
+            for (unsigned long long c = blockIdx.x + (unsigned long long)wid * gridDim.x; c < nh;
+                 c += (unsigned long long)gridDim.x * kWarps) {
+                const uint4 h = p.heavy[c];
+                const int g = (int)h.z;
+                const int32_t* col = s_slots[gslot[g]].col;
+                const int t0 = toff[g], t1 = toff[g + 1];
+                if (s_single) {
+                    for (uint32_t a = h.x; a < h.y; a += 32 * kBEdges) {
+                        bool act[kBEdges];
+                        int tt[kBEdges], uu[kBEdges];
+                        uint32_t ww[kBEdges];
+#pragma unroll
+                        for (int c2 = 0; c2 < kBEdges; ++c2) {
+                            const uint32_t x = a + 32 * c2 + lane;
+                            act[c2] = x < h.y;
+                            uu[c2] = act[c2] ? col[x] : 0;
+                            tt[c2] = targets[t0];
+                            ww[c2] = h.w;
+                        }
+                        bvisit<kBEdges>(p, fnext, nxt, lnext, act, tt, uu, ww, st, lane);
+                    }
+                } else {
+                    for (uint32_t a = h.x; a < h.y; a += 32) {
+                        const bool a0 = a + lane < h.y;
+                        const int u = a0 ? col[a + lane] : 0;
+                        for (int t = t0; t < t1; ++t) {
+                            const bool act[1] = {a0};
+                            const int tt[1] = {targets[t]};
+                            const int uu[1] = {u};
+                            const uint32_t ww[1] = {h.w};
+                            bvisit<1>(p, fnext, nxt, lnext, act, tt, uu, ww, st, lane);
+                        }
+                    }
+                }
+            }
+            bphase_end(p, nxt, lnext, st, lane, 0ull, 0ull, 0ull, 0u, cur, s_red, &s_or);
+            grid_barrier_on(&ctl->bar, &ctl->abort, ++e, bar_base);
+        }
+        ++L;
+    }
+
+    // ---- epilogue: answer_s = OR of P_s's rows at final states (engine.py:112-114),
+    // transposed from source words to one bitmap per source
+    if (status == 0) {
+        const long long nblk = (p.nv + 127) / 128;
+        const long long gwarp = (long long)blockIdx.x * kWarps + wid;
+        const long long nwarps = (long long)gridDim.x * kWarps;
+        unsigned long long cnt = 0;
+        for (long long b = gwarp; b < nblk; b += nwarps) {
+            uint32_t mine[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const long long v = b * 128 + 32 * k + lane;
+                uint32_t acc = 0;
+                if (v < p.nv)
+                    for (int f = 0; f < p.nfinals; ++f) acc |= p.vis[(long long)finals[f] * p.nvp + v];
+                mine[k] = 0;
+#pragma unroll 4
+                for (int s = 0; s < kBatch; ++s) {
+                    const uint32_t bits = __ballot_sync(FULL, (acc >> s) & 1u);
+                    if (lane == s) mine[k] = bits;
+                }
+            }
+            if (lane < s_run.nsrc) {
+                *reinterpret_cast<uint4*>(p.out + (long long)lane * p.W + b * 4) =
+                    make_uint4(mine[0], mine[1], mine[2], mine[3]);
+                cnt += __popc(mine[0]) + __popc(mine[1]) + __popc(mine[2]) + __popc(mine[3]);
+            }
+        }
+        if (lane < s_run.nsrc && cnt) atomicAdd(&ctl->reach_count[lane], cnt);
+    }
+    if (cta0 && threadIdx.x == 0) ctl->status = status;
+}
+
+}  // namespace rpqk

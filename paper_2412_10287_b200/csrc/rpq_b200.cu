@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "ssr_kernel.cuh"
+#include "batch_kernel.cuh"
 #include "ingest.cuh"
 
 using namespace rpqk;
@@ -113,6 +114,25 @@ struct rpq_query {
     int grid = 0;
     size_t smem = 0;
     bool ran = false;
+    uint64_t edge_bound = 0;  // sum over groups of the slot's nnz
+
+    // multi-source batch workspace (batch_kernel.cuh), allocated on first use
+    uint32_t* d_bvis = nullptr;
+    uint32_t* d_bfw[2] = {nullptr, nullptr};
+    uint2* d_blist[2] = {nullptr, nullptr};
+    uint4* d_bheavy = nullptr;
+    BCtl* d_bctl = nullptr;
+    BCtl* h_bctl = nullptr;  // pinned
+    BatchArgs* d_bargs = nullptr;
+    BatchArgs* h_bargs = nullptr;  // pinned
+    uint32_t* d_bout = nullptr;
+    long long bnvp = 0;
+    unsigned long long blist_cap = 0, bheavy_cap = 0;
+    int bgrid = 0;
+    int bnsrc = 0;
+    unsigned int bbar_next = 0;
+    bool binflight = false, bran = false;
+    cudaStream_t blast_stream = nullptr;
 };
 
 namespace {
@@ -273,6 +293,18 @@ void free_query_buffers(rpq_query* q) {
     if (q->d_reach) cudaFree(q->d_reach);
     if (q->d_reach_bits) cudaFree(q->d_reach_bits);
     if (q->h_reach_bits) cudaFreeHost(q->h_reach_bits);
+
+    if (q->d_bvis) cudaFree(q->d_bvis);
+    for (int b = 0; b < 2; ++b) {
+        if (q->d_bfw[b]) cudaFree(q->d_bfw[b]);
+        if (q->d_blist[b]) cudaFree(q->d_blist[b]);
+    }
+    if (q->d_bheavy) cudaFree(q->d_bheavy);
+    if (q->d_bctl) cudaFree(q->d_bctl);
+    if (q->h_bctl) cudaFreeHost(q->h_bctl);
+    if (q->d_bargs) cudaFree(q->d_bargs);
+    if (q->h_bargs) cudaFreeHost(q->h_bargs);
+    if (q->d_bout) cudaFree(q->d_bout);
 
     if (q->graph) cudaGraphExecDestroy(q->graph);
     if (q->ev0) cudaEventDestroy(q->ev0);
@@ -531,6 +563,7 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
         if (starts[i] >= 0 && starts[i] < nstates) sset.insert(starts[i]);
     for (int i = 0; i < nfinals; ++i)
         if (finals[i] >= 0 && finals[i] < nstates) fset.insert(finals[i]);
+    q->edge_bound = edge_bound;
     q->ngroups = (int)gslot.size();
     q->nslots = (int)slot_keys.size();
     q->ntargets = (int)targets.size();
@@ -928,6 +961,202 @@ int rpq_query_io_bytes(const rpq_query* q, int64_t* h2d_per_run, int64_t* d2h_pe
         *h2d_per_run = (int64_t)q->in_bytes;
     if (d2h_per_run)
         *d2h_per_run = (int64_t)offsetof(Ctl, qc) + (q->output_mode == 1 ? ((int64_t)q->g->nv + 31) / 32 * 4 : 0);
+    return RPQ_OK;
+}
+
+namespace {
+
+int batch_alloc(rpq_query* q) {
+    if (q->d_bvis) return RPQ_OK;
+#define BTRY(expr)                                                    \
+    do {                                                              \
+        cudaError_t e_ = (expr);                                      \
+        if (e_ != cudaSuccess) {                                      \
+            const int rc_ = cuda_fail(e_, #expr);                     \
+            for (int b = 0; b < 2; ++b) {                             \
+                if (q->d_bfw[b]) cudaFree(q->d_bfw[b]);               \
+                if (q->d_blist[b]) cudaFree(q->d_blist[b]);           \
+                q->d_bfw[b] = nullptr;                                \
+                q->d_blist[b] = nullptr;                              \
+            }                                                         \
+            if (q->d_bheavy) cudaFree(q->d_bheavy);                   \
+            if (q->d_bctl) cudaFree(q->d_bctl);                       \
+            if (q->h_bctl) cudaFreeHost(q->h_bctl);                   \
+            if (q->d_bargs) cudaFree(q->d_bargs);                     \
+            if (q->h_bargs) cudaFreeHost(q->h_bargs);                 \
+            if (q->d_bout) cudaFree(q->d_bout);                       \
+            if (q->d_bvis) cudaFree(q->d_bvis);                       \
+            q->d_bheavy = nullptr;                                    \
+            q->d_bctl = nullptr;                                      \
+            q->h_bctl = nullptr;                                      \
+            q->d_bargs = nullptr;                                     \
+            q->h_bargs = nullptr;                                     \
+            q->d_bout = nullptr;                                      \
+            q->d_bvis = nullptr;                                      \
+            return rc_;                                               \
+        }                                                             \
+    } while (0)
+    const long long nv = q->g->nv;
+    q->bnvp = (nv + 127) / 128 * 128;
+    // every (state, vertex) item is listed at most once per level
+    q->blist_cap = (unsigned long long)q->nstates * (unsigned long long)std::max<long long>(nv, 1);
+    // rows longer than kLightDeg: at most nnz / kLightDeg of them per group and
+    // level, each cut into ceil(deg / kChunk) chunks
+    q->bheavy_cap = q->edge_bound / kLightDeg + q->edge_bound / kChunk + 1024;
+    if (q->blist_cap >= 0xFFFFFFFFull || q->bheavy_cap >= 0xFFFFFFFFull)
+        return fail(RPQ_EINVAL, "batch frontier would exceed 2^32 entries");
+    const size_t words = (size_t)q->nstates * (size_t)q->bnvp;
+    BTRY(cudaMalloc(&q->d_bvis, words * 4));
+    for (int b = 0; b < 2; ++b) {
+        BTRY(cudaMalloc(&q->d_bfw[b], words * 4));
+        BTRY(cudaMalloc(&q->d_blist[b], (size_t)q->blist_cap * sizeof(uint2)));
+    }
+    BTRY(cudaMalloc(&q->d_bheavy, (size_t)q->bheavy_cap * sizeof(uint4)));
+    BTRY(cudaMalloc(&q->d_bctl, sizeof(BCtl)));
+    BTRY(cudaMemset(q->d_bctl, 0, sizeof(BCtl)));
+    BTRY(cudaMallocHost(&q->h_bctl, sizeof(BCtl)));
+    BTRY(cudaMalloc(&q->d_bargs, sizeof(BatchArgs)));
+    BTRY(cudaMallocHost(&q->h_bargs, sizeof(BatchArgs)));
+    BTRY(cudaMalloc(&q->d_bout, (size_t)kBatch * (size_t)q->W * 4));
+    if (q->smem > 48 * 1024)
+        BTRY(cudaFuncSetAttribute(batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q->smem));
+    int per_sm = 0;
+    BTRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batch_kernel, kThreads, q->smem));
+    if (per_sm < 1) BTRY(cudaErrorInvalidConfiguration);
+    q->bgrid = q->g->sm_count * per_sm;
+    q->bbar_next = 0;
+#undef BTRY
+    return RPQ_OK;
+}
+
+}  // namespace
+
+int rpq_query_run_batch(rpq_query* q, int32_t nsrc, const int32_t* sources, double timeout_s, void* stream) {
+    if (!q) return fail(RPQ_EINVAL, "null query");
+    if (nsrc < 1 || nsrc > kBatch) return fail(RPQ_EINVAL, "nsrc must be in [1, 32]");
+    if (!sources) return fail(RPQ_EINVAL, "null sources");
+    for (int i = 0; i < nsrc; ++i)
+        if (sources[i] < 0 || sources[i] >= q->g->nv)
+            return fail(RPQ_ERANGE, "vertex index " + std::to_string(sources[i]) + " out of range");
+    if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+    const int rc = batch_alloc(q);
+    if (rc != RPQ_OK) return rc;
+    cudaStream_t st = stream ? (cudaStream_t)stream : q->own_stream;
+    if (q->binflight) {  // the pinned argument block is read by the previous run's copy
+        CUDA_TRY(cudaStreamSynchronize(q->blast_stream));
+        q->bbar_next = q->h_bctl->bar;
+        q->binflight = false;
+    }
+    BatchArgs a{};
+    a.nsrc = nsrc;
+    a.bar_base = q->bbar_next;
+    if (!(timeout_s >= 0) || std::isinf(timeout_s) || timeout_s > 1.0e9)
+        a.budget_ns = ~0ull;
+    else
+        a.budget_ns = (unsigned long long)(timeout_s * 1e9);
+    for (int i = 0; i < nsrc; ++i) a.sources[i] = sources[i];
+    *q->h_bargs = a;
+    BParams p{};
+    p.run = q->d_bargs;
+    p.tables = reinterpret_cast<const int32_t*>(q->d_in + q->off_tables);
+    p.slots = reinterpret_cast<const Slot*>(q->d_in + q->off_slots);
+    p.vis = q->d_bvis;
+    for (int b = 0; b < 2; ++b) {
+        p.fw[b] = q->d_bfw[b];
+        p.list[b] = q->d_blist[b];
+    }
+    p.heavy = q->d_bheavy;
+    p.ctl = q->d_bctl;
+    p.out = q->d_bout;
+    p.nvp = q->bnvp;
+    p.W = q->W;
+    p.list_cap = q->blist_cap;
+    p.heavy_cap = q->bheavy_cap;
+    p.nv = q->g->nv;
+    p.nstates = q->nstates;
+    p.ngroups = q->ngroups;
+    p.nslots = q->nslots;
+    p.ntargets = q->ntargets;
+    p.nstarts = q->nstarts;
+    p.nfinals = q->nfinals;
+    p.nin = q->nin;
+    p.table_ints = (int)q->tables.size();
+    void* args[] = {&p};
+    CUDA_TRY(cudaEventRecord(q->ev0, st));
+    // the automaton tables live in the single-source input block: send it too
+    CUDA_TRY(cudaMemcpyAsync(q->d_in, q->h_in, q->in_bytes, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(q->d_bargs, q->h_bargs, sizeof(BatchArgs), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)batch_kernel, dim3(q->bgrid), dim3(kThreads), args, q->smem,
+                                         st));
+    CUDA_TRY(cudaMemcpyAsync(q->h_bctl, q->d_bctl, offsetof(BCtl, bc), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(q->ev1, st));
+    q->blast_stream = st;
+    q->bnsrc = nsrc;
+    q->bran = true;
+    q->binflight = true;
+    return RPQ_OK;
+}
+
+int rpq_query_wait_batch(rpq_query* q, rpq_batch_stats* stats) {
+    if (!q) return fail(RPQ_EINVAL, "null query");
+    if (!q->bran) return fail(RPQ_EINVAL, "no batch has been run");
+    CUDA_TRY(cudaStreamSynchronize(q->blast_stream));
+    q->binflight = false;
+    const BCtl& c = *q->h_bctl;
+    q->bbar_next = c.bar;
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, q->ev0, q->ev1));
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        stats->status = c.status;
+        stats->nsrc = q->bnsrc;
+        stats->levels = c.levels;
+        stats->grid = q->bgrid;
+        stats->te = (int64_t)c.te;
+        stats->rows = (int64_t)c.rows;
+        stats->visited_pairs = (int64_t)c.pairs;
+        stats->device_ms = ms;
+        for (int s = 0; s < q->bnsrc; ++s) {
+            stats->iterations[s] = c.last_level[s] + 1;
+            stats->reach_count[s] = (int64_t)c.reach_count[s];
+        }
+        for (int i = 0; i < RPQ_STATS_LEVELS && i < c.levels; ++i) {
+            stats->level_items[i] = (int64_t)c.level_items[i];
+            stats->level_new[i] = (int64_t)c.level_new[i];
+            stats->level_ns[i] = (int64_t)c.level_ns[i];
+            stats->level_rows[i] = (int64_t)c.level_rows[i];
+        }
+    }
+    if (c.status == ST_OVERFLOW) {
+        if (stats) stats->status = RPQ_ECUDA;
+        return fail(RPQ_ECUDA, "internal: batch frontier capacity exceeded");
+    }
+    if (c.status == ST_DEADLOCK) {
+        if (stats) stats->status = RPQ_ECUDA;
+        return fail(RPQ_ECUDA, "internal: grid barrier spin limit exceeded");
+    }
+    if (c.status == RPQ_ETIMEOUT) return fail(RPQ_ETIMEOUT, "query timed out");
+    if (c.status != 0) return fail(RPQ_ECUDA, "kernel status " + std::to_string(c.status));
+    return RPQ_OK;
+}
+
+int rpq_query_copy_batch_bits(rpq_query* q, uint32_t* host_words, int64_t row_words) {
+    if (!q || !host_words) return fail(RPQ_EINVAL, "null argument");
+    if (!q->bran) return fail(RPQ_EINVAL, "no batch has been run");
+    const int64_t words = ((int64_t)q->g->nv + 31) / 32;
+    if (row_words < words) return fail(RPQ_EINVAL, "row_words < ceil(num_vertices / 32)");
+    if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+    CUDA_TRY(cudaStreamSynchronize(q->blast_stream));
+    if (words == 0) return RPQ_OK;
+    CUDA_TRY(cudaMemcpy2D(host_words, (size_t)row_words * 4, q->d_bout, (size_t)q->W * 4, (size_t)words * 4,
+                          (size_t)q->bnsrc, cudaMemcpyDeviceToHost));
+    return RPQ_OK;
+}
+
+int rpq_query_batch_bits_device(rpq_query* q, uint32_t** d_bits, int64_t* row_words) {
+    if (!q || !d_bits || !row_words) return fail(RPQ_EINVAL, "null argument");
+    *d_bits = q->d_bout;
+    *row_words = q->W;
     return RPQ_OK;
 }
 

@@ -280,22 +280,22 @@ struct View {
 // barrier number e completes when e * gridDim.x arrivals are counted.
 // Waiters spin on a relaxed load and fence once afterwards (acquire side; the
 // fence also invalidates this SM's L1: CCTL.IVALL).
-__device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned epoch, unsigned base) {
+__device__ __forceinline__ void grid_barrier_on(unsigned* bar, int* abort, unsigned epoch, unsigned base) {
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        atomicAdd(&ctl->bar, 1u);
+        atomicAdd(bar, 1u);
         const unsigned target = base + epoch * gridDim.x;
         unsigned long long ts = 0;
         unsigned spins = 0;
-        while ((int)(ld_relaxed_u32(&ctl->bar) - target) < 0) {  // wrap-safe
+        while ((int)(ld_relaxed_u32(bar) - target) < 0) {  // wrap-safe
             __nanosleep(16);
             if ((++spins & 4095u) == 0) {
                 const unsigned long long now = globaltimer();
                 if (ts == 0) {
                     ts = now;
                 } else if (now - ts > 20000000000ull) {  // 20 s: cannot happen co-resident
-                    atomicExch(&ctl->abort, 1);
+                    atomicExch(abort, 1);
                     break;
                 }
             }
@@ -303,6 +303,9 @@ __device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned epoch, unsigned 
         __threadfence();
     }
     __syncthreads();
+}
+__device__ __forceinline__ void grid_barrier(Ctl* ctl, unsigned epoch, unsigned base) {
+    grid_barrier_on(&ctl->bar, &ctl->abort, epoch, base);
 }
 
 // Reservation of `nseg` segments and `nb` bundles (one lane).  Each CTA owns

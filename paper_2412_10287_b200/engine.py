@@ -286,15 +286,52 @@ def eval_sdr(g, n, target, opts, algorithm=None):
     return eval_ssr(g, reverse(n), target, opts)
 
 
-def eval_ssr_batch(g, n, sources, opts):
+def eval_ssr_batch(g, n, sources, opts, *, stats=None):
     """uint8[len(sources), |V|]: row i is eval_ssr(g, n, sources[i], opts)'s answer.
 
     Defined as the per-source loop; the reference has no
-    multi-source entry point."""
-    sources = list(sources)
-    out = np.zeros((len(sources), g.num_vertices), dtype=np.uint8)
-    for i, s in enumerate(sources):
-        out[i] = eval_ssr(g, n, s, opts).reach
+    multi-source entry point.  Evaluated 32 sources per kernel launch with
+    bit-sliced frontiers (batch_kernel.cuh).  ``opts.timeout`` bounds each
+    launch of up to 32 sources.  If ``stats`` is a list, the statistics of
+    every launch are appended to it."""
+    opts.validate()
+    sources = [int(s) for s in sources]
+    for s in sources:
+        _check_vertex(g, s)
+    nv = int(g.num_vertices)
+    out = np.zeros((len(sources), nv), dtype=np.uint8)
+    if not sources:
+        return out
+    t0 = time.monotonic()
+    dg = device_graph(g, opts.device)
+    table = _table_for(n, g.num_labels)
+    dg.ensure_labels(table.labels)
+    lib = _lib.engine()
+    q = dg.acquire_query(table)
+    try:
+        words = (nv + 31) // 32
+        bits = np.zeros((_lib.BATCH, max(words, 1)), dtype=np.uint32)
+        for b0 in range(0, len(sources), _lib.BATCH):
+            chunk = np.ascontiguousarray(sources[b0:b0 + _lib.BATCH], dtype=np.int32)
+            if opts.timeout == 0 and table.starts.size:
+                raise QueryTimeout(time.monotonic() - t0, 0)  # _Clock.check(0), engine.py:87-89
+            budget = -1.0 if math.isinf(opts.timeout) else float(opts.timeout)
+            raise_for_status(lib.rpq_query_run_batch(q, chunk.size, _lib.ptr(chunk, ctypes.c_int32), budget,
+                                                     None), "rpq_query_run_batch")
+            st = _lib.RpqBatchStats()
+            rc = lib.rpq_query_wait_batch(q, ctypes.byref(st))
+            if rc == _lib.RPQ_ETIMEOUT:
+                raise QueryTimeout(time.monotonic() - t0, int(st.levels))
+            raise_for_status(rc, "rpq_query_wait_batch")
+            if stats is not None:
+                stats.append(st.to_dict())
+            if nv:
+                raise_for_status(lib.rpq_query_copy_batch_bits(q, _lib.ptr(bits, ctypes.c_uint32), bits.shape[1]),
+                                 "rpq_query_copy_batch_bits")
+                rows = np.unpackbits(bits[: chunk.size].view(np.uint8), axis=1, bitorder="little")
+                out[b0:b0 + chunk.size] = rows[:, :nv]
+    finally:
+        dg.release_query(table, q)
     return out
 
 
@@ -387,6 +424,32 @@ class PreparedQuery:
             raise QueryTimeout(stats.device_ms / 1e3, stats.iterations)
         raise_for_status(rc, "rpq_query_wait")
         return stats
+
+    def launch_batch(self, sources, timeout=-1.0, stream=None):
+        """Enqueue one multi-source run (<= 32 sources, bit-sliced)."""
+        src = np.ascontiguousarray([int(s) for s in sources], dtype=np.int32)
+        for s in src:
+            _check_vertex(self.g, int(s))
+        self._batch_src = src  # keep alive until the copy is enqueued (synchronous here)
+        raise_for_status(_lib.engine().rpq_query_run_batch(self.q, src.size, _lib.ptr(src, ctypes.c_int32),
+                                                           float(timeout), stream), "rpq_query_run_batch")
+
+    def wait_batch(self):
+        stats = _lib.RpqBatchStats()
+        rc = _lib.engine().rpq_query_wait_batch(self.q, ctypes.byref(stats))
+        if rc == _lib.RPQ_ETIMEOUT:
+            raise QueryTimeout(stats.device_ms / 1e3, stats.levels)
+        raise_for_status(rc, "rpq_query_wait_batch")
+        return stats
+
+    def batch_reach(self, nsrc):
+        """uint8[nsrc, |V|] answers of the last batch run."""
+        words = (self.nv + 31) // 32
+        bits = np.zeros((nsrc, max(words, 1)), dtype=np.uint32)
+        if self.nv:
+            raise_for_status(_lib.engine().rpq_query_copy_batch_bits(self.q, _lib.ptr(bits, ctypes.c_uint32),
+                                                                     bits.shape[1]), "rpq_query_copy_batch_bits")
+        return np.unpackbits(bits.view(np.uint8), axis=1, bitorder="little")[:, : self.nv]
 
     def reach(self, out=None):
         out = np.empty(self.nv, dtype=np.uint8) if out is None else out

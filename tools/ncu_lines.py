@@ -29,9 +29,9 @@ def line_map(so, kernel_substr):
             infn = kernel_substr in ln
         if not infn:
             continue
-        m = re.search(r'line (\d+)', ln)
+        m = re.search(r'File "([^"]+)", line (\d+)', ln)
         if "//## File" in ln and m:
-            cur = int(m.group(1))
+            cur = (m.group(1), int(m.group(2)))
             continue
         m = re.match(r"\s*/\*([0-9a-f]+)\*/", ln)
         if m and cur is not None:
@@ -58,11 +58,22 @@ def main():
         by_line[ln][0] += smp
         by_line[ln][1] += ins
     tot = sum(v[0] for v in by_line.values())
-    src = open(os.path.join(os.path.dirname(so), "csrc", "ssr_kernel.cuh")).read().splitlines()
+    srcs = {}
+
+    def text_of(key):
+        if not key:
+            return "?", "?"
+        path, ln = key
+        if path not in srcs:
+            cand = path if os.path.exists(path) else os.path.join(os.path.dirname(so), "csrc", os.path.basename(path))
+            srcs[path] = open(cand).read().splitlines() if os.path.exists(cand) else []
+        lines = srcs[path]
+        return f"{os.path.basename(path)}:{ln}", (lines[ln - 1].strip()[:80] if ln <= len(lines) else "?")
+
     print(f"total samples {tot}")
-    for ln, (smp, ins) in sorted(by_line.items(), key=lambda kv: -kv[1][0])[:int(os.environ.get("TOP", 30))]:
-        text = src[ln - 1].strip()[:80] if ln and ln <= len(src) else "?"
-        print(f"{smp:7d} {100.0 * smp / max(tot, 1):5.1f}% {ins:10d}  L{ln}: {text}")
+    for key, (smp, ins) in sorted(by_line.items(), key=lambda kv: -kv[1][0])[:int(os.environ.get("TOP", 30))]:
+        loc, text = text_of(key)
+        print(f"{smp:7d} {100.0 * smp / max(tot, 1):5.1f}% {ins:10d}  {loc}: {text}")
 
 
 if __name__ == "__main__":
