@@ -183,6 +183,14 @@ RPQ_API int rpq_query_copy_reach(rpq_query* q, uint8_t* host_reach);
  * Synchronous. */
 RPQ_API int rpq_query_step(rpq_query* q, const uint32_t* m_words, const uint32_t* p_words, int64_t row_words,
                            uint32_t* out_words);
+/* Words per state row of the query's bitmaps (>= ceil(nv/32), multiple of 4). */
+RPQ_API int rpq_query_row_words(const rpq_query* q, int64_t* row_words);
+/* Device-resident step for the vertex-partitioned evaluator:
+ * on `stream`, out = step_sum(M) masked by the complement of P, and P |= out.
+ * d_m, d_p, d_out are device bitmaps of nstates rows x rpq_query_row_words
+ * words, distinct.  Asynchronous; rpq_query_wait returns its status. */
+RPQ_API int rpq_query_step_device(rpq_query* q, const uint32_t* d_m, uint32_t* d_p, uint32_t* d_out,
+                                  void* stream);
 /* Output mode: 0 (default) keeps the answer on the device; 1 also copies the
  * answer bitmap (ceil(nv/32) uint32 words, bit v%32 of word v/32) into pinned
  * host memory as part of every run, ready after rpq_query_wait. */

@@ -711,12 +711,12 @@ Params make_params(const rpq_query* q) {
 
 // The run sequence: inputs H2D (run block + automaton tables, pinned), control
 // block reset, the cooperative kernel, statistics (and answer bitmap) D2H.
-cudaError_t enqueue_run(rpq_query* q, cudaStream_t st) {
+cudaError_t enqueue_run(rpq_query* q, cudaStream_t st, const Params* override = nullptr) {
     cudaError_t e;
     // inputs: run arguments + automaton tables in one pinned block
     if ((e = cudaMemcpyAsync(q->d_in, q->h_in, q->in_bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
         return e;
-    Params p = make_params(q);
+    Params p = override ? *override : make_params(q);
     void* args[] = {&p};
     if ((e = cudaLaunchCooperativeKernel((const void*)ssr_kernel, dim3(q->grid), dim3(kThreads), args, q->smem,
                                          st)) != cudaSuccess)
@@ -929,6 +929,45 @@ int rpq_query_step(rpq_query* q, const uint32_t* m_words, const uint32_t* p_word
     if (words > 0)
         CUDA_TRY(cudaMemcpy2D(out_words, spitch, q->d_fb[1], dpitch, width, (size_t)q->nstates,
                               cudaMemcpyDeviceToHost));
+    return RPQ_OK;
+}
+
+int rpq_query_row_words(const rpq_query* q, int64_t* row_words) {
+    if (!q || !row_words) return fail(RPQ_EINVAL, "null argument");
+    *row_words = q->W;
+    return RPQ_OK;
+}
+
+int rpq_query_step_device(rpq_query* q, const uint32_t* d_m, uint32_t* d_p, uint32_t* d_out, void* stream) {
+    if (!q || !d_m || !d_p || !d_out) return fail(RPQ_EINVAL, "null argument");
+    if (d_out == d_m || d_out == d_p || d_m == d_p) return fail(RPQ_EINVAL, "M, P and the output must be distinct");
+    if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+    cudaStream_t st = stream ? (cudaStream_t)stream : q->own_stream;
+    if (q->inflight) {  // the pinned input block is read by the previous run's copy
+        CUDA_TRY(cudaStreamSynchronize(q->last_stream));
+        q->bar_next = q->h_ctl->bar;
+        q->inflight = false;
+    }
+    RunArgs ra{};
+    ra.mode = 1;
+    ra.dir_mode = 1;
+    ra.alpha = q->alpha;
+    ra.budget_ns = ~0ull;
+    ra.bar_base = q->bar_next;
+    *reinterpret_cast<RunArgs*>(q->h_in) = ra;
+    // the caller's buffers stand in for P and F_0 / F_1; F_2 is the query's
+    // (step mode reads F_0, writes F_1, zeroes F_1 and F_2 first, keeps P)
+    Params p = make_params(q);
+    p.visited = d_p;
+    p.fb[0] = const_cast<uint32_t*>(d_m);
+    p.fb[1] = d_out;
+    p.fb[2] = q->d_fb[2];
+    CUDA_TRY(cudaEventRecord(q->ev0, st));
+    CUDA_TRY(enqueue_run(q, st, &p));
+    CUDA_TRY(cudaEventRecord(q->ev1, st));
+    q->last_stream = st;
+    q->ran = true;
+    q->inflight = true;
     return RPQ_OK;
 }
 
