@@ -853,6 +853,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     const long long Wn = ((long long)p.nv + 31) >> 5;  // used words per bitmap row
     const long long nbits4 = (long long)p.nstates * p.W / 4;
     const bool cta0 = blockIdx.x == 0;
+    __syncthreads();  // s_run, tables and counters above are read by every thread below
     Stage stage;
     stage.q = s_stage[wid][0];
     stage.w = s_stage[wid][1];

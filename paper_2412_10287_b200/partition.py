@@ -204,10 +204,12 @@ class DeviceStep:
                                                              out.data_ptr(), stream), "rpq_query_step_device")
 
     def finish(self):
+        """Status of the last step (raises on failure); its device time in ms."""
         from .engine import raise_for_status
 
         st = _lib.RpqStats()
         raise_for_status(_lib.engine().rpq_query_wait(self.pq.q, ctypes.byref(st)), "rpq_query_step_device")
+        return float(st.device_ms)
 
     def close(self):
         self.pq.close()
@@ -238,7 +240,7 @@ def _bit(v):
     return np.array([1 << (v & 31)], dtype=np.uint32).view(np.int32)[0].item()
 
 
-def run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout=math.inf):
+def run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout=math.inf, profile=False):
     """The partitioned masked loop.  Returns (reach uint8[nv], iterations,
     stats).  `shards` are the shards of THIS process (one per rank under
     torch.distributed, all k for LocalExchange).  Device work runs on one
@@ -252,13 +254,14 @@ def run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout=mat
         s = torch.cuda.Stream(dev)
         s.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(s):
-            out = _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, s.cuda_stream)
+            out = _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, s.cuda_stream,
+                              profile)
         torch.cuda.current_stream(dev).wait_stream(s)
         return out
-    return _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, None)
+    return _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, None, profile)
 
 
-def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, stream):
+def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, stream, profile):
     import torch
 
     t0 = time.monotonic()
@@ -278,6 +281,7 @@ def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, s
                 sh.p[q, sw] |= sb
     iterations = 0
     levels_us = []
+    step_ms = []  # profile: per level, each local shard's step kernel time
     sync = (lambda: torch.cuda.synchronize(dev)) if m.is_cuda else (lambda: None)
     while bool(m.any()):
         if time.monotonic() - t0 > timeout:  # _Clock.check, engine.py:87-89
@@ -298,6 +302,8 @@ def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, s
             m[:, w0:w1] = gathered[r, :, : w1 - w0]
         sync()
         levels_us.append((time.monotonic() - t0) * 1e6)
+        if profile:
+            step_ms.append([sh.step.finish() if hasattr(sh.step, "finish") else 0.0 for sh in shards])
     for sh in shards:
         if hasattr(sh.step, "finish"):
             sh.step.finish()
@@ -316,7 +322,7 @@ def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, s
     for r, (w0, w1) in enumerate(ranges):
         words[w0:w1] = g_host[r, 0, : w1 - w0]
     reach = np.unpackbits(words.view(np.uint8), bitorder="little")[:nv]
-    return reach, iterations, {"levels_wall_us": levels_us, "ranges": ranges}
+    return reach, iterations, {"levels_wall_us": levels_us, "ranges": ranges, "step_ms": step_ms}
 
 
 def _or_rows(t):

@@ -80,3 +80,17 @@ def test_partition_edge_cases():
         assert reach.tolist() == [1, 1, 1, 0, 0] and its == 3
         reach, its, _ = _run_local(g, n, 4, k)
         assert reach.tolist() == [0, 0, 0, 0, 1] and its == 1
+
+
+def test_first_step_after_create_keeps_p():
+    """Regression: the kernel read its per-run arguments from shared memory
+    before every thread could see them, so a query's first step-mode launch
+    could run as a full evaluation (clearing P and M)."""
+    sg = datagen.gen_rmat(16, 16, 8, 1.0, 77)
+    g = sg.labeled_graph()
+    nj = json.load(open(os.path.join(GOLDEN, "extra_automata.json")))["^a (b|c)* d"]
+    n = automaton(nj)
+    for _ in range(3):
+        reach, its, _ = _run_local(g, n, int(np.argmax(sg.out_degree())), 1)
+        want = P.eval_ssr(g, n, int(np.argmax(sg.out_degree())), P.EngineOptions(algorithm="masked"))
+        assert np.array_equal(reach, want.reach) and its == want.iterations
