@@ -165,6 +165,9 @@ RPQ_API int rpq_query_set_options(rpq_query* q, int32_t direction, int32_t count
  *   RPQ_TUNE_EMIT_INLINE_MAX: mode 2 emits at discovery while |F_L| < value. */
 #define RPQ_TUNE_EMIT_MODE 0
 #define RPQ_TUNE_EMIT_INLINE_MAX 1
+#define RPQ_TUNE_FLAGS 3  /* push variants: bit 0 (default on) claim without probing P first,
+                             bit 1 prefetch candidate targets' row pointers into L2 */
+#define RPQ_TUNE_TRACE 2  /* diagnostics: record per-CTA phase stamps of the first `value` levels */
 RPQ_API int rpq_query_set_tuning(rpq_query* q, int32_t key, double value);
 /* Enqueue one evaluation from `source` on `stream` (a cudaStream_t, or NULL for
  * the query's own stream).  timeout_s < 0 or inf: no deadline.  The deadline is
@@ -183,6 +186,12 @@ RPQ_API int rpq_query_copy_reach(rpq_query* q, uint8_t* host_reach);
  * Synchronous. */
 RPQ_API int rpq_query_step(rpq_query* q, const uint32_t* m_words, const uint32_t* p_words, int64_t row_words,
                            uint32_t* out_words);
+/* Diagnostics (RPQ_TUNE_TRACE): per level L, CTA c, stamp k (0 level start,
+ * 1 plan epoch done, 2 last warp done with the expansion, 3 past the barrier,
+ * 4 counters flushed, 7 decision taken (stamped at the decision that
+ * starts level L); slots 5-6 unused) in ns from kernel
+ * start at host[(L * grid + c) * 8 + k]; *grid receives the CTA count. */
+RPQ_API int rpq_query_copy_trace(rpq_query* q, uint64_t* host, int64_t n, int32_t* grid);
 /* Words per state row of the query's bitmaps (>= ceil(nv/32), multiple of 4). */
 RPQ_API int rpq_query_row_words(const rpq_query* q, int64_t* row_words);
 /* Device-resident step for the vertex-partitioned evaluator:

@@ -107,6 +107,7 @@ struct rpq_query {
     int count_te = 0;
     int emit_mode = 0;
     unsigned int emit_inline_max = 1u << 16;
+    unsigned int run_flags = RF_NO_PROBE;
     float alpha = 4.0f;
     cudaStream_t own_stream = nullptr;
     cudaStream_t last_stream = nullptr;
@@ -115,6 +116,8 @@ struct rpq_query {
     size_t smem = 0;
     bool ran = false;
     uint64_t edge_bound = 0;  // sum over groups of the slot's nnz
+    unsigned long long* d_trace = nullptr;  // diagnostics (RPQ_TUNE_TRACE)
+    int trace_levels = 0;
 
     // multi-source batch workspace (batch_kernel.cuh), allocated on first use
     uint32_t* d_bvis = nullptr;
@@ -294,6 +297,7 @@ void free_query_buffers(rpq_query* q) {
     if (q->d_reach_bits) cudaFree(q->d_reach_bits);
     if (q->h_reach_bits) cudaFreeHost(q->h_reach_bits);
 
+    if (q->d_trace) cudaFree(q->d_trace);
     if (q->d_bvis) cudaFree(q->d_bvis);
     for (int b = 0; b < 2; ++b) {
         if (q->d_bfw[b]) cudaFree(q->d_bfw[b]);
@@ -706,6 +710,8 @@ Params make_params(const rpq_query* q) {
     p.nin = q->nin;
     p.maxT = q->maxT;
     p.table_ints = (int)q->tables.size();
+    p.trace = q->d_trace;
+    p.trace_levels = q->d_trace ? q->trace_levels : 0;
     return p;
 }
 
@@ -771,6 +777,27 @@ int rpq_query_set_tuning(rpq_query* q, int32_t key, double value) {
             if (value < 0 || value > 4.0e9) return fail(RPQ_EINVAL, "bad inline threshold");
             q->emit_inline_max = (unsigned int)value;
             return RPQ_OK;
+        case RPQ_TUNE_FLAGS:
+            if (value < 0 || value > 3) return fail(RPQ_EINVAL, "flags must be in [0, 3]");
+            q->run_flags = (unsigned)value;
+            return RPQ_OK;
+        case RPQ_TUNE_TRACE: {
+            if (value < 0 || value > 4096) return fail(RPQ_EINVAL, "trace levels must be in [0, 4096]");
+            if (q->d_trace) cudaFree(q->d_trace);
+            q->d_trace = nullptr;
+            q->trace_levels = (int)value;
+            if (q->trace_levels > 0) {
+                const size_t bytes = (size_t)q->trace_levels * q->grid * 8 * sizeof(unsigned long long);
+                CUDA_TRY(cudaMalloc(&q->d_trace, bytes));
+                CUDA_TRY(cudaMemset(q->d_trace, 0, bytes));
+            }
+            if (q->graph) {  // the captured run holds the old parameters
+                cudaGraphExecDestroy(q->graph);
+                q->graph = nullptr;
+                q->graph_mode = -1;
+            }
+            return RPQ_OK;
+        }
         default:
             return fail(RPQ_EINVAL, "unknown tuning key");
     }
@@ -793,6 +820,7 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     ra.bar_base = q->bar_next;
     ra.emit_mode = q->emit_mode;
     ra.emit_inline_max = q->emit_inline_max;
+    ra.flags = q->run_flags;
     ra.source = source;
     ra.dir_mode = q->dir_mode;
     ra.count_te = q->count_te;
@@ -929,6 +957,18 @@ int rpq_query_step(rpq_query* q, const uint32_t* m_words, const uint32_t* p_word
     if (words > 0)
         CUDA_TRY(cudaMemcpy2D(out_words, spitch, q->d_fb[1], dpitch, width, (size_t)q->nstates,
                               cudaMemcpyDeviceToHost));
+    return RPQ_OK;
+}
+
+int rpq_query_copy_trace(rpq_query* q, uint64_t* host, int64_t n, int32_t* grid) {
+    if (!q || !grid) return fail(RPQ_EINVAL, "null argument");
+    *grid = q->grid;
+    const int64_t need = (int64_t)q->trace_levels * q->grid * 8;
+    if (!q->d_trace) return fail(RPQ_EINVAL, "tracing is off (RPQ_TUNE_TRACE)");
+    if (!host || n < need) return fail(RPQ_EINVAL, "trace buffer too small");
+    if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+    CUDA_TRY(cudaStreamSynchronize(q->last_stream ? q->last_stream : q->own_stream));
+    CUDA_TRY(cudaMemcpy(host, q->d_trace, (size_t)need * 8, cudaMemcpyDeviceToHost));
     return RPQ_OK;
 }
 

@@ -114,8 +114,11 @@ struct RunArgs {
     int emit_mode;          // 0: emit F_{L+1}'s queue at discovery; 1: from F's bitmap
                             // in vertex order (plan epoch); 2: by frontier size
     unsigned int emit_inline_max;  // mode 2: inline while |F_L| < this
-    unsigned int pad2;
+    unsigned int flags;            // RF_* push-path variants (tuning)
 };
+
+constexpr unsigned RF_NO_PROBE = 1u;     // claim with atomicOr without reading P first
+constexpr unsigned RF_PREFETCH = 2u;     // prefetch candidate targets' row pointers into L2
 
 struct Params {
     const RunArgs* run;
@@ -137,6 +140,8 @@ struct Params {
     int nstates, ngroups, nslots, ntargets, nstarts, nfinals, nin;
     int maxT;
     int table_ints;
+    unsigned long long* trace;  // diagnostics: [level][cta][4] globaltimer stamps, or null
+    int trace_levels;
 };
 
 struct Smem {
@@ -150,6 +155,7 @@ struct Smem {
     const int32_t* isrc;     // [nin]
     const int32_t* islot;    // [nin]
     const Slot* slots;       // [2*nslots]
+    const float* nnz;        // [nslots] edges of each slot (decision estimates)
     const RunArgs* run;      // this run's inputs (shared-memory copy)
     uint64_t pf;             // L2 policy: evict first (graph, queues)
     uint64_t pl;             // L2 policy: evict last (P and F bitmaps)
@@ -204,6 +210,9 @@ __device__ __forceinline__ uint2 ld_queue(const uint2* a, uint64_t pol) {  // wr
 __device__ __forceinline__ void st_queue(uint2* a, uint2 v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(a), "r"(v.x), "r"(v.y), "l"(pol)
                  : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* a) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
 }
 __device__ __forceinline__ uint32_t ld_bits(const uint32_t* a, uint64_t pol) {
     uint32_t v;
@@ -601,28 +610,33 @@ __device__ __forceinline__ void flush_counts(unsigned long long* nnew_dst, const
 __device__ __forceinline__ void queue_scan(const Params& p, const QCnt* qc, int lane,
                                            unsigned long long* s_bpre, unsigned long long* nbun,
                                            unsigned long long* nseg) {
+    // lane l owns shards [l*R, l*R + R): all loads in flight, a serial prefix
+    // per lane, one warp scan of the lane totals
     constexpr int R = (kShards + 1 + 31) / 32;
-    unsigned long long c[R], sc[R];
+    unsigned long long c[R];
+    unsigned long long tot = 0, segs = 0;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {  // issue all loads first
-        const int sh = 32 * r + lane;
+    for (int r = 0; r < R; ++r) {
+        const int sh = lane * R + r;
         const unsigned long long v = sh <= kShards ? ldcg(&qc->shard[sh]) : 0ull;
         const unsigned long long bcap = sh < kShards ? p.shard_buncap : p.ovf_buncap;
         const unsigned long long scap = sh < kShards ? p.shard_segcap : p.ovf_segcap;
         c[r] = min(v & 0xFFFFFFFFull, bcap);
-        sc[r] = min(v >> 32, scap);
+        segs += min(v >> 32, scap);
     }
-    unsigned long long carry = 0, segs = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) tot += c[r];
+    const unsigned long long incl = warp_incl_scan_u64(tot, lane);
+    unsigned long long run = incl - tot;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int sh = 32 * r + lane;
-        const unsigned long long incl = warp_incl_scan_u64(c[r], lane);
-        if (sh <= kShards) s_bpre[sh] = carry + incl - c[r];
-        carry += __shfl_sync(FULL, incl, 31);
-        segs += sc[r];
+        const int sh = lane * R + r;
+        if (sh <= kShards) s_bpre[sh] = run;
+        run += c[r];
     }
-    if (lane == 0) s_bpre[kShards + 1] = carry;
-    *nbun = carry;
+    const unsigned long long total = __shfl_sync(FULL, incl, 31);
+    if (lane == 0) s_bpre[kShards + 1] = total;
+    *nbun = total;
     *nseg = warp_sum_u64(segs);
 }
 
@@ -636,6 +650,11 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
     Ctl* ctl = p.ctl;
     const QCnt* qc = &ctl->qc[e % 3];
     const FCnt* fc = &ctl->fc[L % 3];
+    // every load of the decision in flight at once (one L2 round trip)
+    constexpr int RS = kMaxStates / 32;
+    unsigned int fst[RS];
+#pragma unroll
+    for (int r = 0; r < RS; ++r) fst[r] = 32 * r + lane < p.nstates ? ldcg(&fc->state[32 * r + lane]) : 0u;
     const unsigned long long nnew = ldcg(&fc->nnew);
     const unsigned long long nedge = ldcg(&qc->edges);
     const unsigned int overflow = ldcg(&qc->overflow);
@@ -643,10 +662,13 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
     const int abort = ldcg(&ctl->abort);
     unsigned long long nbun, nseg;
     queue_scan(p, qc, lane, s_bpre, &nbun, &nseg);
-    for (int q = lane; q < p.nstates; q += 32) {
-        const unsigned int f = ldcg(&fc->state[q]);
-        s_front[q] = f;
-        s_sv[q] += f;
+#pragma unroll
+    for (int r = 0; r < RS; ++r) {
+        const int q = 32 * r + lane;
+        if (q < p.nstates) {
+            s_front[q] = fst[r];
+            s_sv[q] += fst[r];
+        }
     }
     __syncwarp();
     // F_L's queue was emitted at discovery (exact m_f and bundles available)
@@ -675,33 +697,38 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
             // average degrees after a pull level); m_u: in-edges of unvisited
             // targets whose source state has a frontier.  Pull when
             // m_f * alpha > m_u (Beamer's rule; alpha tuned for these kernels).
-            const double nv = (double)p.nv;
-            double mf = 0.0, mu = 0.0;
+            const float nv = (float)p.nv, inv_nv = 1.0f / (float)p.nv;
+            float mf = 0.0f, mu = 0.0f;
             int ntarget = 0;  // states a pull level would scan
             for (int q = lane; q < p.nstates; q += 32) {
                 bool t = false;
-                for (int k = S.ibeg[q]; k < S.ibeg[q + 1]; ++k) t |= s_front[S.isrc[k]] != 0;
-                ntarget += t ? 1 : 0;
-            }
-            for (int d = 16; d >= 1; d >>= 1) ntarget += __shfl_xor_sync(FULL, ntarget, d);
-            for (int q = lane; q < p.nstates; q += 32) {
-                if (!produced_by_push && s_front[q])
-                    for (int g = S.gbeg[q]; g < S.gbeg[q + 1]; ++g)
-                        mf += (double)s_front[q] * (double)p.slot_nnz[S.gslot[g]] / nv;
-                const double unvis = nv - (double)s_sv[q];
+                float unvis_frac = (nv - (float)s_sv[q]) * inv_nv;
                 for (int k = S.ibeg[q]; k < S.ibeg[q + 1]; ++k)
-                    if (s_front[S.isrc[k]]) mu += (double)p.slot_nnz[S.islot[k]] * unvis / nv;
+                    if (s_front[S.isrc[k]]) {
+                        t = true;
+                        mu += S.nnz[S.islot[k]] * unvis_frac;
+                    }
+                ntarget += t ? 1 : 0;
+                if (!produced_by_push && s_front[q]) {
+                    const float fq = (float)s_front[q] * inv_nv;
+                    for (int g = S.gbeg[q]; g < S.gbeg[q + 1]; ++g) mf += fq * S.nnz[S.gslot[g]];
+                }
             }
-            mf = produced_by_push ? (double)nedge : warp_sum_f64(mf);
-            mu = warp_sum_f64(mu);
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) {
+                ntarget += __shfl_xor_sync(FULL, ntarget, d);
+                mu += __shfl_xor_sync(FULL, mu, d);
+                mf += __shfl_xor_sync(FULL, mf, d);
+            }
+            if (produced_by_push) mf = (float)nedge;
             if (produced_by_push) {
-                next = (mf * (double)S.run->alpha > mu) ? DIR_PULL : DIR_PUSH;
+                next = (mf * S.run->alpha > mu) ? DIR_PULL : DIR_PUSH;
             } else {
                 // after a pull level stay in pull while the frontier is large
                 // (Beamer: |F| > |V| / beta, beta = 24, with |V| counted once
                 // per state the pull would scan); switching back costs a plan
                 // epoch that re-emits F from its bitmap
-                next = ((double)nnew * 24.0 > nv * (double)ntarget) ? DIR_PULL : DIR_PUSH;
+                next = ((float)nnew * 24.0f > nv * (float)ntarget) ? DIR_PULL : DIR_PUSH;
             }
         }
         if (next == DIR_PUSH) {
@@ -716,6 +743,8 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
             }
         }
     }
+    if (p.trace && L < p.trace_levels && lane == 0)
+        p.trace[((long long)L * gridDim.x + blockIdx.x) * 8 + 7] = globaltimer() - ctl->t0;
     if (lane == 0) {
         v->done = done;
         v->dir = next;
@@ -725,7 +754,7 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
         v->nfront = nnew;
         if (blockIdx.x == 0) {  // results and statistics
             const unsigned long long now = globaltimer();
-            ctl->pairs += nnew;
+            atomicAdd(&ctl->pairs, nnew);  // fire-and-forget: no round trip on CTA 0's path
             if (L < 64) {
                 ctl->level_new[L] = (long long)nnew;
                 ctl->level_ns[L] = now - ctl->t0;
@@ -734,10 +763,10 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
             }
             if (!done) {
                 if (L > 0) ctl->levels = L;
-                if (next == DIR_PULL) ctl->pull_levels += 1;
+                if (next == DIR_PULL) atomicAdd(&ctl->pull_levels, 1);
                 if (next == DIR_PUSH && produced_by_push) {
-                    ctl->te_push += nedge;
-                    ctl->segments += nseg;
+                    atomicAdd(&ctl->te_push, nedge);
+                    atomicAdd(&ctl->segments, nseg);
                 }
                 // _Clock.check at the top of iteration L (engine.py:87-89):
                 // recorded now, acted upon at the next decision by every CTA
@@ -802,6 +831,14 @@ __device__ __forceinline__ void reset_qc(QCnt* qc, int tid) {
     }
 }
 
+// Diagnostic stamp k of level L for this CTA (thread 0): 0 level start (after
+// the decision), 1 plan epoch done, 2 last warp done with the expansion,
+// 3 past the barrier, 4 counters flushed.
+__device__ __forceinline__ void stamp(const Params& p, int L, int k) {
+    if (p.trace && L < p.trace_levels && threadIdx.x == 0)
+        p.trace[((long long)L * gridDim.x + blockIdx.x) * 8 + k] = globaltimer() - p.ctl->t0;
+}
+
 __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ unsigned long long s_red[2 * kWarps];
@@ -815,13 +852,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     __shared__ int s_stage[kWarps][2][64];
     __shared__ unsigned long long s_resv;
     __shared__ unsigned s_task;  // next task index of this CTA in the current epoch
+    __shared__ unsigned long long s_wend;  // diagnostics: latest warp done with the epoch
     __shared__ RunArgs s_run;
+    __shared__ float s_nnz[kMaxSlots];
 
     Slot* s_slots = reinterpret_cast<Slot*>(smem_raw);
+    for (int i = threadIdx.x; i < p.nslots; i += blockDim.x) s_nnz[i] = (float)p.slot_nnz[i];
     int32_t* s_tab = reinterpret_cast<int32_t*>(smem_raw + sizeof(Slot) * 2 * p.nslots);
     for (int i = threadIdx.x; i < 2 * p.nslots; i += blockDim.x) s_slots[i] = p.slots[i];
     for (int i = threadIdx.x; i < p.table_ints; i += blockDim.x) s_tab[i] = p.tables[i];
-    if (threadIdx.x == 0) s_resv = 0;
+    if (threadIdx.x == 0) {
+        s_resv = 0;
+        s_wend = 0;
+    }
     for (int i = threadIdx.x; i < kMaxStates; i += blockDim.x) {
         s_state[i] = 0;
         s_sv[i] = 0;
@@ -833,6 +876,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     S.pl = policy_evict_last();
     S.run = &s_run;
     S.slots = s_slots;
+    S.nnz = s_nnz;
     S.gbeg = s_tab;
     S.gslot = S.gbeg + p.nstates + 1;
     S.toff = S.gslot + p.ngroups;
@@ -930,6 +974,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     int dir = DIR_PUSH;
     for (;;) {
         if (s_view.done) break;
+        stamp(p, L, 0);
         dir = s_view.dir;
         const uint32_t* fcur = p.fb[L % 3];
         uint32_t* fnext = p.fb[(L + 1) % 3];
@@ -967,6 +1012,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
             grid_barrier(ctl, ++e, s_run.bar_base);
             if (wid == 0) decide_plan(p, e, L, lane, &s_view, s_bpre);
             __syncthreads();
+            stamp(p, L, 1);
             if (s_view.done) break;
         }
 
@@ -1068,7 +1114,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                             const int t0 = S.toff[gj[u]];
                             if (t0 + k < S.toff[gj[u] + 1]) {
                                 q2[u] = S.targets[t0 + k];
-                                old[u] = ld_bits(p.visited + (long long)q2[u] * p.W + (w[u] >> 5), S.pl);
+                                if (!(s_run.flags & RF_NO_PROBE))
+                                    old[u] = ld_bits(p.visited + (long long)q2[u] * p.W + (w[u] >> 5), S.pl);
+                                else
+                                    old[u] = 0u;
+                                if ((s_run.flags & RF_PREFETCH) && emit_inline)
+                                    for (int g2 = S.gbeg[q2[u]]; g2 < S.gbeg[q2[u] + 1]; ++g2)
+                                        prefetch_l2(S.slots[S.gslot[g2]].rowptr + w[u]);
                             }
                         }
                     }
@@ -1212,11 +1264,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                 }
             }
         }
+        if (p.trace && lane == 0) atomicMax(&s_wend, globaltimer());  // this warp's work done
         __syncthreads();
+        if (p.trace && L < p.trace_levels && threadIdx.x == 0) {
+            p.trace[((long long)L * gridDim.x + blockIdx.x) * 8 + 2] = s_wend - ctl->t0;
+            s_wend = 0;
+        }
         if (threadIdx.x == 0 && L < 64) atomicMax(&ctl->work_ns[L], globaltimer() - ctl->t0);
         flush_counts(&ctl->fc[(L + 1) % 3].nnew, o, ctl->fc[(L + 1) % 3].state, nnew, nedge, s_red,
                      s_state, p.nstates);
+        stamp(p, L, 4);
         grid_barrier(ctl, ++e, s_run.bar_base);
+        stamp(p, L, 3);
         if (cta0 && threadIdx.x == 0 && L < 64) ctl->bar_ns[L] = globaltimer() - ctl->t0;
         ++L;
         if (step_mode) {
