@@ -98,6 +98,16 @@ def read_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def ncu_traffic(config):
+    """DRAM bytes per launch of the step kernel from the committed ncu --set
+    full capture (profiles/ncu_dram_bytes.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_dram_bytes.json")) as fh:
+            return float(json.load(fh)[config]["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -366,7 +376,7 @@ def run_engine(args, rank, world, local_rank):
         },
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None,
+            "frac": achieved / peak, "traffic": ncu_traffic(args.config),
             "kernel": "rpq_ssr_kernel (persistent, one launch per query)",
             "algorithmic_bytes_per_launch": b_alg, "peak_source": peak_src,
             "note": "algorithmic bytes of SURVEY.md §8(d) per query / mean step time",
