@@ -167,6 +167,8 @@ RPQ_API int rpq_query_set_options(rpq_query* q, int32_t direction, int32_t count
 #define RPQ_TUNE_EMIT_INLINE_MAX 1
 #define RPQ_TUNE_FLAGS 3  /* push variants: bit 0 (default on) claim without probing P first,
                              bit 1 prefetch candidate targets' row pointers into L2 */
+#define RPQ_TUNE_SMALL 4  /* 1 (default): state spaces of <= 12,288 x 32 pairs run on one CTA
+                             with shared-memory bitmaps; 0: always the grid kernel */
 #define RPQ_TUNE_TRACE 2  /* diagnostics: record per-CTA phase stamps of the first `value` levels */
 RPQ_API int rpq_query_set_tuning(rpq_query* q, int32_t key, double value);
 /* Enqueue one evaluation from `source` on `stream` (a cudaStream_t, or NULL for

@@ -20,6 +20,7 @@
 
 #include "ssr_kernel.cuh"
 #include "batch_kernel.cuh"
+#include "small_kernel.cuh"
 #include "ingest.cuh"
 
 using namespace rpqk;
@@ -108,6 +109,9 @@ struct rpq_query {
     int emit_mode = 0;
     unsigned int emit_inline_max = 1u << 16;
     unsigned int run_flags = RF_NO_PROBE;
+    bool small_ok = false;    // |Q| x |V| fits the single-CTA kernel
+    int allow_small = 1;      // RPQ_TUNE_SMALL
+    size_t small_smem = 0;
     float alpha = 4.0f;
     cudaStream_t own_stream = nullptr;
     cudaStream_t last_stream = nullptr;
@@ -662,6 +666,15 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     QTRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ssr_kernel, kThreads, q->smem));
     if (per_sm < 1) return bail(fail(RPQ_ECUDA, "step kernel cannot be resident"));
     q->grid = std::min(g->sm_count * per_sm, kShards);  // one queue shard per CTA
+    if ((long long)nstates * q->W <= kSmallMaxWords) {
+        q->small_smem = q->slots.size() * sizeof(Slot) + (T.size() * sizeof(int32_t) + 15) / 16 * 16 +
+                        3 * (size_t)nstates * (size_t)q->W * sizeof(uint32_t);
+        if (q->small_smem <= 200 * 1024) {
+            QTRY(cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)std::max<size_t>(q->small_smem, 48 * 1024)));
+            q->small_ok = true;
+        }
+    }
 #undef QTRY
     *out = q;
     return RPQ_OK;
@@ -717,16 +730,24 @@ Params make_params(const rpq_query* q) {
 
 // The run sequence: inputs H2D (run block + automaton tables, pinned), control
 // block reset, the cooperative kernel, statistics (and answer bitmap) D2H.
-cudaError_t enqueue_run(rpq_query* q, cudaStream_t st, const Params* override = nullptr) {
+// The single-CTA kernel runs a full evaluation when the state space fits its
+// shared memory (and no pull levels were asked for).
+bool use_small(const rpq_query* q) { return q->small_ok && q->allow_small && q->dir_mode != RPQ_DIR_PULL; }
+
+cudaError_t enqueue_run(rpq_query* q, cudaStream_t st, const Params* override = nullptr, bool small = false) {
     cudaError_t e;
     // inputs: run arguments + automaton tables in one pinned block
     if ((e = cudaMemcpyAsync(q->d_in, q->h_in, q->in_bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
         return e;
     Params p = override ? *override : make_params(q);
     void* args[] = {&p};
-    if ((e = cudaLaunchCooperativeKernel((const void*)ssr_kernel, dim3(q->grid), dim3(kThreads), args, q->smem,
-                                         st)) != cudaSuccess)
+    if (small) {
+        small_kernel<<<1, kSmallThreads, q->small_smem, st>>>(p);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    } else if ((e = cudaLaunchCooperativeKernel((const void*)ssr_kernel, dim3(q->grid), dim3(kThreads), args,
+                                                q->smem, st)) != cudaSuccess) {
         return e;
+    }
     // outputs: the control block's results prefix (and the answer bitmap)
     if ((e = cudaMemcpyAsync(q->h_ctl, q->d_ctl, offsetof(Ctl, qc), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
         return e;
@@ -740,7 +761,8 @@ cudaError_t enqueue_run(rpq_query* q, cudaStream_t st, const Params* override = 
 // Capture enqueue_run into a graph once per output mode: one cudaGraphLaunch
 // per run.  Falls back to direct launches if capture is not possible.
 void build_graph(rpq_query* q) {
-    if (q->graph && q->graph_mode == q->output_mode) return;
+    const int variant = q->output_mode | (use_small(q) ? 2 : 0);
+    if (q->graph && q->graph_mode == variant) return;
     if (q->graph) {
         cudaGraphExecDestroy(q->graph);
         q->graph = nullptr;
@@ -751,7 +773,7 @@ void build_graph(rpq_query* q) {
         q->graph_failed = true;
         return;
     }
-    cudaError_t e = enqueue_run(q, q->own_stream);
+    cudaError_t e = enqueue_run(q, q->own_stream, nullptr, use_small(q));
     cudaError_t e2 = cudaStreamEndCapture(q->own_stream, &g);
     if (e != cudaSuccess || e2 != cudaSuccess || !g ||
         cudaGraphInstantiate(&q->graph, g, 0) != cudaSuccess) {
@@ -759,7 +781,7 @@ void build_graph(rpq_query* q) {
         q->graph = nullptr;
         q->graph_failed = true;
     } else {
-        q->graph_mode = q->output_mode;
+        q->graph_mode = variant;
     }
     if (g) cudaGraphDestroy(g);
 }
@@ -776,6 +798,10 @@ int rpq_query_set_tuning(rpq_query* q, int32_t key, double value) {
         case RPQ_TUNE_EMIT_INLINE_MAX:
             if (value < 0 || value > 4.0e9) return fail(RPQ_EINVAL, "bad inline threshold");
             q->emit_inline_max = (unsigned int)value;
+            return RPQ_OK;
+        case RPQ_TUNE_SMALL:
+            if (value != 0 && value != 1) return fail(RPQ_EINVAL, "small-kernel switch must be 0 or 1");
+            q->allow_small = (int)value;
             return RPQ_OK;
         case RPQ_TUNE_FLAGS:
             if (value < 0 || value > 3) return fail(RPQ_EINVAL, "flags must be in [0, 3]");
@@ -836,7 +862,7 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     if (q->graph)
         CUDA_TRY(cudaGraphLaunch(q->graph, st));
     else
-        CUDA_TRY(enqueue_run(q, st));
+        CUDA_TRY(enqueue_run(q, st, nullptr, use_small(q)));
     CUDA_TRY(cudaEventRecord(q->ev1, st));
     q->last_stream = st;
     q->ran = true;

@@ -58,8 +58,11 @@ class EngineOptions:
     direction: str = "auto"  # per-level push/pull policy of the device BFS
     alpha: float = 4.0  # Beamer's switch constant (pull when m_f * alpha > m_u)
     count_te: bool = False  # exact product-edge count in EvalResult.stats
+    kernel: str = "auto"  # "auto": small state spaces run on one CTA; "grid": always the grid kernel
 
     def validate(self) -> None:
+        if self.kernel not in ("auto", "grid"):
+            raise ValueError(f"unknown kernel {self.kernel!r}")
         if self.direction not in DIRECTIONS:
             raise ValueError(f"unknown direction {self.direction!r}")
         if not self.alpha > 0:
@@ -197,6 +200,8 @@ def _run(g, n, source, opts, tag, *, want_stats=False):
         raise_for_status(lib.rpq_query_set_options(
             q, DIRECTIONS[opts.direction], int(opts.count_te or opts.debug_checks), opts.alpha),
             "rpq_query_set_options")
+        raise_for_status(lib.rpq_query_set_tuning(q, 4, 1.0 if opts.kernel == "auto" else 0.0),
+                         "rpq_query_set_tuning")
         raise_for_status(lib.rpq_query_set_output(q, 1), "rpq_query_set_output")
         # _Clock.check(0) at the top of the first iteration (engine.py:87-89)
         remaining = opts.timeout - (time.monotonic() - t0)
@@ -404,8 +409,11 @@ class PreparedQuery:
         raise_for_status(_lib.engine().rpq_query_set_options(
             self.q, DIRECTIONS[direction], int(count_te), float(alpha)), "rpq_query_set_options")
 
-    def set_tuning(self, emit_mode=None, emit_inline_max=None):
+    def set_tuning(self, emit_mode=None, emit_inline_max=None, kernel=None):
         lib = _lib.engine()
+        if kernel is not None:
+            raise_for_status(lib.rpq_query_set_tuning(self.q, 4, 1.0 if kernel == "auto" else 0.0),
+                             "rpq_query_set_tuning")
         if emit_mode is not None:
             raise_for_status(lib.rpq_query_set_tuning(self.q, 0, float(emit_mode)), "rpq_query_set_tuning")
         if emit_inline_max is not None:

@@ -22,11 +22,14 @@ def instances(reference_instances):
     return [(rec, host_graph(rec["graph"]), automaton(rec["nfa"])) for rec in reference_instances]
 
 
-@pytest.mark.parametrize("algorithm,direction", [
-    ("hybrid", "auto"), ("masked", "auto"), ("no_mask", "auto"),
-    ("hybrid", "push"), ("hybrid", "pull"), ("masked", "pull")])
-def test_reference_instances(instances, algorithm, direction):
-    opts = P.EngineOptions(algorithm=algorithm, timeout=math.inf, direction=direction)
+@pytest.mark.parametrize("algorithm,direction,kernel", [
+    ("hybrid", "auto", "auto"), ("masked", "auto", "auto"), ("no_mask", "auto", "auto"),
+    ("hybrid", "push", "auto"), ("hybrid", "pull", "auto"), ("masked", "pull", "auto"),
+    ("hybrid", "auto", "grid"), ("masked", "push", "grid"), ("no_mask", "auto", "grid")])
+def test_reference_instances(instances, algorithm, direction, kernel):
+    """kernel="auto" runs these small instances on the single-CTA kernel
+    (except forced pull); "grid" forces the persistent grid kernel."""
+    opts = P.EngineOptions(algorithm=algorithm, timeout=math.inf, direction=direction, kernel=kernel)
     for rec, g, n in instances:
         res = P.eval_ssr(g, n, rec["source"], opts)
         assert np.array_equal(res.reach, expected_reach(rec, g.num_vertices)), rec["tag"]
@@ -56,27 +59,29 @@ def test_hybrid_thresholds(instances):
             assert res.reachable == set(rec["expected"]) and res.iterations == its
 
 
-def test_debug_invariants(instances):
-    opts = P.EngineOptions(debug_checks=True)
+@pytest.mark.parametrize("kernel", ["auto", "grid"])
+def test_debug_invariants(instances, kernel):
+    opts = P.EngineOptions(debug_checks=True, kernel=kernel)
     for rec, g, n in instances[:200]:
         res = P.eval_ssr(g, n, rec["source"], opts)
         assert res.iterations <= n.nstates * g.num_vertices
         assert res.stats["visited_pairs"] == sum(res.stats["level_new"][: res.iterations + 1])
 
 
-def test_timeout_raises():
+@pytest.mark.parametrize("kernel", ["auto", "grid"])
+def test_timeout_raises(kernel):
     # test_engine.py:376-383
     nv = 3001
     g = P.LabeledGraph.from_edges(nv, ["a"], [(i, 0, i + 1) for i in range(3000)])
     n = P.Automaton.build(1, {(0, False): [(0, 0)]}, [0], [0])
     with pytest.raises(P.QueryTimeout) as ei:
-        P.eval_ssr_masked(g, n, 0, P.EngineOptions(timeout=0.0))
+        P.eval_ssr_masked(g, n, 0, P.EngineOptions(timeout=0.0, kernel=kernel))
     assert ei.value.iterations == 0
-    res = P.eval_ssr_masked(g, n, 0, P.EngineOptions(timeout=math.inf))
+    res = P.eval_ssr_masked(g, n, 0, P.EngineOptions(timeout=math.inf, kernel=kernel))
     assert res.reachable == set(range(nv)) and res.iterations == nv
     # a deadline that expires mid-query is caught at an iteration boundary
     with pytest.raises(P.QueryTimeout) as ei:
-        P.eval_ssr_masked(g, n, 0, P.EngineOptions(timeout=1e-4))
+        P.eval_ssr_masked(g, n, 0, P.EngineOptions(timeout=1e-4, kernel=kernel))
     assert 0 <= ei.value.iterations < nv
 
 
@@ -149,7 +154,7 @@ def test_config_goldens(name):
             assert res.iterations == rec["iterations"]["hybrid"], direction
 
 
-@pytest.mark.parametrize("direction", ["auto", "push", "pull"])
+@pytest.mark.parametrize("direction", ["auto", "push", "pull", "grid-auto"])
 @pytest.mark.parametrize("scale,seed,query", [
     (14, 21, "^a (b|c)* d"), (15, 22, "a ^b* c"), (16, 23, "a b*"),
     (13, 24, "(a|^b)* c+"), (12, 25, "(a ^a)* (b | c ^d)*"), (14, 26, "(a|b|c|d)*"),
@@ -171,8 +176,9 @@ def test_rmat_vs_oracle(scale, seed, query, direction):
     sources = [int(np.argmax(deg)), 0, sg.nv - 1, int(np.flatnonzero(deg)[len(np.flatnonzero(deg)) // 2])]
     for s in sources:
         want, st = oracle_bfs(og, oq, s)
+        d, kernel = ("auto", "grid") if direction == "grid-auto" else (direction, "auto")
         got = P.eval_ssr(g, n, s, P.EngineOptions(timeout=math.inf, debug_checks=True,
-                                                  direction=direction))
+                                                  direction=d, kernel=kernel))
         assert np.array_equal(got.reach, want), (query, s)
         assert got.iterations == st["iterations"]
         assert got.stats["te"] == st["te"]
