@@ -7,18 +7,22 @@
 // (q, v) at that level, so adjacency traffic is shared across the batch
 // (SURVEY.md §8(d) "batched sources", §8(e) regime 1).
 //
-// Layout (DESIGN.md §3b):
-//   vis[q][v]   uint32 source word: P, one row of nvp words per state
-//   fw[L&1]     uint32 source word: M at level L (same shape); a word is
-//               cleared when its item is expanded, so fw[(L+1)&1] is all zero
-//               again when level L+1 starts writing it
-//   list[L&1]   items (v, q) with fw[L&1][q][v] != 0, each once: appended by
-//               the discovery that turns the word from 0 to non-zero
-//   heavy       row chunks (lo, hi, group, word) of rows longer than
-//               kLightDeg, expanded in a second phase of the level
-// Per level: phase 1 expands light rows warp-cooperatively (prefix sum over
-// the 32 items' degrees, 32 edges per step) and cuts heavy rows into chunks;
-// phase 2 (only when chunks exist) spreads the chunks over every warp.
+// Layout (DESIGN.md §3):
+//   vis[q][v]     uint32 source word: P, one row of nvp words per state
+//   fw[L&1][q][v] uint32 source word: M at level L.  A word is cleared when
+//                 it is expanded, so fw[(L+1)&1] is all zero again when level
+//                 L+1 starts writing it
+//   act[L&1][q][b] one flag per 256-vertex block of M_L holding a non-empty
+//                 word ("skip inactive (state, vertex-block)
+//                 tiles"); raised by the discovery that first writes into it
+//   heavy         row chunks (lo, hi, group, word) of rows longer than
+//                 kLightDeg, expanded in a second phase of the level
+// Per level: phase 1 sweeps the active blocks (a warp per block, coalesced
+// word reads, 32 words per step), expands rows of <= kLightDeg edges
+// warp-cooperatively (prefix over the items' degrees, kBEdges edges per lane
+// in flight) and cuts longer rows into chunks; phase 2 (only when chunks
+// exist) spreads the chunks over every warp.  Discoveries are fire-and-forget
+// ORs (RED) into P and M_{L+1}: no atomic round trip, no work list.
 #pragma once
 
 namespace rpqk {
@@ -26,15 +30,18 @@ namespace rpqk {
 constexpr int kBatch = 32;             // sources per launch (bits of a source word)
 constexpr uint32_t kLightDeg = 64;     // rows up to this many edges stay in phase 1
 constexpr uint32_t kChunk = 256;       // edges per heavy chunk
-constexpr int kBStage = 64;            // staged list appends per warp
+constexpr int kBlockShift = 8;         // activity flag per 2^8 vertices
+constexpr int kBlockWords = 1 << kBlockShift;
+constexpr int kBEdges = 4;             // edges per lane in flight per step
 
 struct BCnt {
-    unsigned int nlist;       // |list_L|
-    unsigned int nheavy;      // heavy chunks produced while expanding level L
+    unsigned int nact;         // active blocks of M_L (flags raised while producing it)
+    unsigned int nheavy;       // heavy chunks produced while expanding level L
     unsigned int overflow;
-    unsigned int expire;      // the deadline check at the top of level L failed
-    unsigned long long nnew;  // (pair, source) discoveries forming M_L
-    unsigned int active;      // sources with a non-empty M_L
+    unsigned int expire;       // the deadline check at the top of level L failed
+    unsigned long long nnew;   // |M_L| summed over sources (from the items)
+    unsigned long long items;  // (state, vertex) words of M_L that were non-empty
+    unsigned int active;       // sources with a non-empty M_L
     unsigned int pad;
 };
 
@@ -53,7 +60,7 @@ struct BCtl {
     unsigned long long level_items[64];
     unsigned long long level_new[64];
     unsigned long long level_ns[64];
-    unsigned long long level_rows[64];  // edges read at level L (cumulative counter snapshot)
+    unsigned long long level_rows[64];  // edges read before level L starts (cumulative)
     unsigned int level_active[64];
     // ---- working counters ------------------------------------------------
     BCnt bc[3];
@@ -72,56 +79,28 @@ struct BParams {
     const Slot* slots;
     uint32_t* vis;
     uint32_t* fw[2];
-    uint2* list[2];
+    uint32_t* act[2];  // [nstates][nblk] activity flags by level parity
     uint4* heavy;
     BCtl* ctl;
-    uint32_t* out;  // [kBatch][W] answer bitmaps
-    long long nvp;  // words per state row of vis / fw (>= nv, multiple of 128)
-    long long W;    // words per answer row (multiple of 4)
-    unsigned long long list_cap, heavy_cap;
+    uint32_t* out;   // [kBatch][W] answer bitmaps
+    long long nvp;   // words per state row of vis / fw (>= nv, multiple of kBlockWords)
+    long long nblk;  // nvp / kBlockWords
+    long long W;     // words per answer row (multiple of 4)
+    unsigned long long heavy_cap;
     int nv, nstates, ngroups, nslots, ntargets, nstarts, nfinals, nin, table_ints;
 };
-
-struct BWarp {  // per-warp state of an expansion phase
-    uint2* buf;  // staged appends (shared memory, kBStage entries)
-    int n;
-};
-
-constexpr int kBEdges = 4;  // edges per lane in flight per step
-
-__device__ __forceinline__ void bflush(const BParams& p, BCnt* nxt, uint2* lst, BWarp& st, int lane, bool all) {
-    const int m = all ? st.n : 32;
-    if (m <= 0) return;
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(&nxt->nlist, (unsigned)m);
-    base = __shfl_sync(FULL, base, 0);
-    if (lane < m) {
-        if ((unsigned long long)base + lane < p.list_cap)
-            lst[base + lane] = st.buf[lane];
-        else
-            atomicExch(&nxt->overflow, 1u);
-    }
-    __syncwarp();
-    const bool mv = lane + m < st.n;
-    uint2 t = make_uint2(0, 0);
-    if (mv) t = st.buf[m + lane];
-    __syncwarp();
-    if (mv) st.buf[lane] = t;
-    __syncwarp();
-    st.n -= m;
-}
 
 // Source words w[c] reach (t[c], u[c]) (K edges per lane, loads overlapped):
 // the sources not yet at (t, u) join P and M_{L+1}.  P is read first (from
 // L2) and only ORed into where that read shows missing bits; the read may
 // miss bits set earlier in this level, never bits of earlier levels, so the
 // bits ORed into M_{L+1} are exactly the discoveries of this level (a bit may
-// be discovered by several edges; the item is listed once: by the OR that
-// turns M_{L+1}'s word from zero).
+// be discovered by several edges; ORs are idempotent).  The first discovery
+// into a 256-vertex block raises its activity flag for the next level.
 template <int K>
-__device__ __forceinline__ void bvisit(const BParams& p, uint32_t* fnext, BCnt* nxt, uint2* lst,
-                                       const bool (&act)[K], const int (&t)[K], const int (&u)[K],
-                                       const uint32_t (&w)[K], BWarp& st, int lane) {
+__device__ __forceinline__ void bvisit(const BParams& p, uint32_t* fnext, uint32_t* anext, const bool (&act)[K],
+                                       const int (&t)[K], const int (&u)[K], const uint32_t (&w)[K],
+                                       unsigned& nact) {
     long long off[K];
     uint32_t seen[K];
 #pragma unroll
@@ -129,57 +108,54 @@ __device__ __forceinline__ void bvisit(const BParams& p, uint32_t* fnext, BCnt* 
         off[c] = (long long)t[c] * p.nvp + u[c];
         seen[c] = act[c] ? __ldcg(p.vis + off[c]) : 0xFFFFFFFFu;
     }
-    bool app[K];
+    uint32_t* flag[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) {
         const uint32_t nw = w[c] & ~seen[c];
-        app[c] = false;
+        flag[c] = nullptr;
         if (nw) {
-            atomicOr(p.vis + off[c], nw);  // result unused: RED
-            app[c] = atomicOr(fnext + off[c], nw) == 0u;
+            atomicOr(p.vis + off[c], nw);  // results unused: RED
+            atomicOr(fnext + off[c], nw);
+            flag[c] = anext + (long long)t[c] * p.nblk + (u[c] >> kBlockShift);
         }
     }
+    uint32_t fl[K];
 #pragma unroll
-    for (int c = 0; c < K; ++c) {
-        const unsigned m = __ballot_sync(FULL, app[c]);
-        if (m) {
-            if (app[c]) st.buf[st.n + __popc(m & lanemask_lt())] = make_uint2((uint32_t)u[c], (uint32_t)t[c]);
-            st.n += __popc(m);
-            __syncwarp();
-            if (st.n >= 32) bflush(p, nxt, lst, st, lane, false);
-        }
-    }
+    for (int c = 0; c < K; ++c) fl[c] = flag[c] ? __ldcg(flag[c]) : 1u;
+#pragma unroll
+    for (int c = 0; c < K; ++c)
+        if (!fl[c] && atomicExch(flag[c], 1u) == 0u) ++nact;
 }
 
-// End of a phase: staged appends out; per-CTA sums of the items' statistics
-// (|M_L| and its sources, into `cnt`) and of the edges read.
-__device__ __forceinline__ void bphase_end(const BParams& p, BCnt* nxt, uint2* lst, BWarp& st, int lane,
-                                           unsigned long long te, unsigned long long rows,
-                                           unsigned long long nnew, uint32_t act, BCnt* cnt,
+// End of a phase: per-CTA sums into the counters.
+__device__ __forceinline__ void bphase_end(const BParams& p, BCnt* nxt, unsigned nact, unsigned long long te,
+                                           unsigned long long rows, unsigned long long nnew,
+                                           unsigned long long items, uint32_t act, BCnt* cnt,
                                            unsigned long long* s_red, unsigned* s_or) {
-    bflush(p, nxt, lst, st, lane, true);
-    const int wid = threadIdx.x >> 5;
-    unsigned long long a = warp_sum_u64(nnew), b = warp_sum_u64(te), r = warp_sum_u64(rows);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned long long a = warp_sum_u64(nnew), b = warp_sum_u64(te), r = warp_sum_u64(rows);
+    const unsigned long long it = warp_sum_u64(items), na = warp_sum_u64(nact);
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) act |= __shfl_xor_sync(FULL, act, d);
     if (lane == 0) {
-        s_red[3 * wid] = a;
-        s_red[3 * wid + 1] = b;
-        s_red[3 * wid + 2] = r;
+        s_red[5 * wid] = a;
+        s_red[5 * wid + 1] = b;
+        s_red[5 * wid + 2] = r;
+        s_red[5 * wid + 3] = it;
+        s_red[5 * wid + 4] = na;
         if (act) atomicOr(s_or, act);
     }
     __syncthreads();
     if (wid == 0) {
-        a = lane < kWarps ? s_red[3 * lane] : 0ull;
-        b = lane < kWarps ? s_red[3 * lane + 1] : 0ull;
-        r = lane < kWarps ? s_red[3 * lane + 2] : 0ull;
-        a = warp_sum_u64(a);
-        b = warp_sum_u64(b);
-        r = warp_sum_u64(r);
+        unsigned long long v[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) v[k] = warp_sum_u64(lane < kWarps ? s_red[5 * lane + k] : 0ull);
         if (lane == 0) {
-            if (a) atomicAdd(&cnt->nnew, a);
-            if (b) atomicAdd(&p.ctl->te, b);
-            if (r) atomicAdd(&p.ctl->rows, r);
+            if (v[0]) atomicAdd(&cnt->nnew, v[0]);
+            if (v[1]) atomicAdd(&p.ctl->te, v[1]);
+            if (v[2]) atomicAdd(&p.ctl->rows, v[2]);
+            if (v[3]) atomicAdd(&cnt->items, v[3]);
+            if (v[4]) atomicAdd(&nxt->nact, (unsigned)v[4]);
             if (*s_or) atomicOr(&cnt->active, *s_or);
             *s_or = 0;
         }
@@ -188,8 +164,7 @@ __device__ __forceinline__ void bphase_end(const BParams& p, BCnt* nxt, uint2* l
 
 __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ unsigned long long s_red[3 * kWarps];
-    __shared__ uint2 s_buf[kWarps][kBStage];
+    __shared__ unsigned long long s_red[5 * kWarps];
     __shared__ unsigned s_or;
     __shared__ unsigned s_task;
     __shared__ int s_single;  // every (state, symbol) group has exactly one target (a DFA)
@@ -222,9 +197,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
     const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long gthreads = (long long)gridDim.x * blockDim.x;
     const bool cta0 = blockIdx.x == 0;
-    BWarp st;
-    st.buf = s_buf[wid];
-    st.n = 0;
     if (cta0) {  // reset the control block (except the barrier counter)
         unsigned char* z = reinterpret_cast<unsigned char*>(ctl) + 8;
         for (size_t i = threadIdx.x * 8; i + 8 <= sizeof(BCtl) - 8; i += (size_t)blockDim.x * 8)
@@ -239,8 +211,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
     __syncthreads();
     const unsigned bar_base = s_run.bar_base;
     unsigned e = 0;
+    const long long nbt = (long long)p.nstates * p.nblk;  // blocks over all states
 
-    // ---- epoch 0: P <- 0, M <- 0 for every source
+    // ---- epoch 0: P <- 0, M <- 0, no active block, for every source
     {
         const long long n4 = (long long)p.nstates * p.nvp / 4;
         uint4* a = reinterpret_cast<uint4*>(p.vis);
@@ -252,30 +225,27 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
             b[i] = z;
             c[i] = z;
         }
+        for (long long i = gtid; i < nbt; i += gthreads) {
+            p.act[0][i] = 0u;
+            p.act[1][i] = 0u;
+        }
     }
     grid_barrier_on(&ctl->bar, &ctl->abort, ++e, bar_base);
 
     // ---- epoch 1: seed P_s = M_s = {(q_s, source_s)} (engine.py:106-109)
-    if (cta0 && wid == 0) {
-        const bool act = lane < s_run.nsrc;
-        const int src = act ? s_run.sources[lane] : 0;
+    unsigned nact = 0;
+    if (cta0 && wid == 0 && lane < s_run.nsrc) {
+        const int src = s_run.sources[lane];
         for (int i = 0; i < p.nstarts; ++i) {
             const int q = starts[i];
             const long long off = (long long)q * p.nvp + src;
-            bool app = false;
-            if (act) {
-                const uint32_t bit = 1u << lane;
-                atomicOr(p.vis + off, bit);
-                app = atomicOr(p.fw[0] + off, bit) == 0u;
-            }
-            const unsigned m = __ballot_sync(FULL, app);
-            if (app) st.buf[st.n + __popc(m & lanemask_lt())] = make_uint2((uint32_t)src, (uint32_t)q);
-            st.n += __popc(m);
-            __syncwarp();
-            if (st.n >= 32) bflush(p, &ctl->bc[0], p.list[0], st, lane, false);
+            atomicOr(p.vis + off, 1u << lane);
+            atomicOr(p.fw[0] + off, 1u << lane);
+            if (atomicExch(p.act[0] + (long long)q * p.nblk + (src >> kBlockShift), 1u) == 0u) ++nact;
         }
     }
-    bphase_end(p, &ctl->bc[0], p.list[0], st, lane, 0ull, 0ull, 0ull, 0u, &ctl->bc[0], s_red, &s_or);
+    bphase_end(p, &ctl->bc[0], nact, 0ull, 0ull, 0ull, 0ull, 0u, &ctl->bc[0], s_red, &s_or);
+    nact = 0;
     grid_barrier_on(&ctl->bar, &ctl->abort, ++e, bar_base);
 
     // ---- level loop
@@ -284,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
     for (;;) {
         BCnt* cur = &ctl->bc[L % 3];
         BCnt* nxt = &ctl->bc[(L + 1) % 3];
-        const unsigned ncur = ldcg(&cur->nlist);
+        const unsigned ncur = ldcg(&cur->nact);
         const unsigned ovf = ldcg(&cur->overflow);
         const unsigned expire = ldcg(&cur->expire);
         const int abort = ldcg(&ctl->abort);
@@ -307,17 +277,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
                 ctl->pairs += nn;
                 if (L - 1 < 64) {
                     ctl->level_new[L - 1] = nn;
+                    ctl->level_items[L - 1] = ldcg(&old->items);
                     ctl->level_active[L - 1] = act;
                 }
             }
-            old->nlist = 0;
+            old->nact = 0;
             old->nheavy = 0;
             old->overflow = 0;
             old->expire = 0;
             old->nnew = 0;
+            old->items = 0;
             old->active = 0;
             if (L < 64) {
-                ctl->level_items[L] = ncur;
                 ctl->level_ns[L] = now - ctl->t0;
                 ctl->level_rows[L] = ldcg(&ctl->rows);
             }
@@ -329,122 +300,125 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
             status = RPQ_ETIMEOUT;
             break;
         }
-        const uint2* lcur = p.list[L & 1];
-        uint2* lnext = p.list[(L + 1) & 1];
+        uint32_t* acur = p.act[L & 1];
+        uint32_t* anext = p.act[(L + 1) & 1];
         uint32_t* fcur = p.fw[L & 1];
         uint32_t* fnext = p.fw[(L + 1) & 1];
         if (threadIdx.x == 0) s_task = 0;
         __syncthreads();
 
-        // ---- phase 1: light rows; heavy rows become chunks
-        unsigned long long te = 0, rows = 0, nnew = 0;
+        // ---- phase 1: a warp per active block; light rows now, heavy rows as chunks
+        unsigned long long te = 0, rows = 0, nnew = 0, items = 0;
         uint32_t active = 0;
         for (;;) {
             unsigned k = 0;
             if (lane == 0) k = atomicAdd(&s_task, 1u);
             k = __shfl_sync(FULL, k, 0);
-            const unsigned long long task = blockIdx.x + (unsigned long long)k * gridDim.x;
-            if (task * 32 >= ncur) break;
-            const unsigned long long i = task * 32 + lane;
-            const bool valid = i < ncur;
-            uint2 it = make_uint2(0, 0);
-            uint32_t w = 0;
-            if (valid) {
-                it = lcur[i];
-                const long long off = (long long)it.y * p.nvp + it.x;
-                w = fcur[off];
-                fcur[off] = 0u;  // fw[L&1] must be zero when level L+1 writes it
-            }
-            nnew += __popc(w);  // M_L's (pair, source) members, each in exactly one item
-            active |= w;
-            const int v = (int)it.x, q = (int)it.y;
-            const int ng = valid ? gbeg[q + 1] - gbeg[q] : 0;
-            int maxng = ng;
+            const long long blk = blockIdx.x + (long long)k * gridDim.x;
+            if (blk >= nbt) break;
+            if (__ldcg(acur + blk) == 0u) continue;  // warp-uniform
+            if (lane == 0) acur[blk] = 0u;            // consumed (level L+2 raises it again)
+            const int q = (int)(blk / p.nblk);
+            const long long v0 = (blk - (long long)q * p.nblk) * kBlockWords;
+            uint32_t* row = fcur + (long long)q * p.nvp;
+            uint32_t wv[kBlockWords / 32];
 #pragma unroll
-            for (int d = 16; d >= 1; d >>= 1) maxng = max(maxng, __shfl_xor_sync(FULL, maxng, d));
-            for (int kg = 0; kg < maxng; ++kg) {
-                int g = 0;
-                uint32_t lo = 0, deg = 0;
-                if (kg < ng) {
-                    g = gbeg[q] + kg;
-                    const Slot sl = s_slots[gslot[g]];
-                    lo = sl.rowptr[v];
-                    deg = sl.rowptr[v + 1] - lo;
+            for (int r = 0; r < kBlockWords / 32; ++r) wv[r] = __ldcg(row + v0 + 32 * r + lane);  // all in flight
+            const int ng = gbeg[q + 1] - gbeg[q];
+#pragma unroll 1
+            for (int r = 0; r < kBlockWords / 32; ++r) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int r2 = 0; r2 < kBlockWords / 32; ++r2)
+                    if (r2 == r) w = wv[r2];
+                if (!__any_sync(FULL, w != 0u)) continue;
+                const int v = (int)(v0 + 32 * r + lane);
+                if (w) {
+                    row[v] = 0u;        // fw[L&1] must be zero when level L+1 writes it
+                    nnew += __popc(w);  // M_L's (pair, source) members, each in exactly one word
+                    ++items;
+                    active |= w;
                 }
-                te += (unsigned long long)deg * __popc(w);
-                rows += deg;
-                // heavy rows -> chunks of kChunk edges (one atomic per warp)
-                const bool heavy = deg > kLightDeg;
-                const uint32_t nch = heavy ? (deg + kChunk - 1) / kChunk : 0u;
-                const uint32_t cincl = warp_incl_scan(nch, lane);
-                const uint32_t ctot = __shfl_sync(FULL, cincl, 31);
-                if (ctot) {
-                    unsigned cbase = 0;
-                    if (lane == 0) cbase = atomicAdd(&cur->nheavy, ctot);
-                    cbase = __shfl_sync(FULL, cbase, 0);
-                    if (heavy) {
-                        unsigned long long c0 = (unsigned long long)cbase + cincl - nch;
-                        for (uint32_t c = 0; c < nch; ++c) {
-                            if (c0 + c < p.heavy_cap) {
-                                const uint32_t a = lo + c * kChunk;
-                                const uint32_t b = min(lo + deg, a + kChunk);
-                                p.heavy[c0 + c] = make_uint4(a, b, (uint32_t)g, w);
-                            } else {
-                                atomicExch(&nxt->overflow, 1u);
+                for (int kg = 0; kg < ng; ++kg) {
+                    const int g = gbeg[q] + kg;
+                    uint32_t lo = 0, deg = 0;
+                    if (w) {
+                        const Slot sl = s_slots[gslot[g]];
+                        lo = sl.rowptr[v];
+                        deg = sl.rowptr[v + 1] - lo;
+                    }
+                    te += (unsigned long long)deg * __popc(w);
+                    rows += deg;
+                    // heavy rows -> chunks of kChunk edges (one atomic per warp)
+                    const bool heavy = deg > kLightDeg;
+                    const uint32_t nch = heavy ? (deg + kChunk - 1) / kChunk : 0u;
+                    const uint32_t cincl = warp_incl_scan(nch, lane);
+                    const uint32_t ctot = __shfl_sync(FULL, cincl, 31);
+                    if (ctot) {
+                        unsigned cbase = 0;
+                        if (lane == 0) cbase = atomicAdd(&cur->nheavy, ctot);
+                        cbase = __shfl_sync(FULL, cbase, 0);
+                        if (heavy) {
+                            const unsigned long long c0 = (unsigned long long)cbase + cincl - nch;
+                            for (uint32_t c = 0; c < nch; ++c) {
+                                if (c0 + c < p.heavy_cap) {
+                                    const uint32_t a = lo + c * kChunk;
+                                    const uint32_t b = min(lo + deg, a + kChunk);
+                                    p.heavy[c0 + c] = make_uint4(a, b, (uint32_t)g, w);
+                                } else {
+                                    atomicExch(&nxt->overflow, 1u);
+                                }
                             }
+                            deg = 0u;
                         }
                     }
-                }
-                if (heavy) deg = 0;
-                // light rows: kBEdges x 32 edges per step over the warp's concatenated rows
-                const uint32_t incl = warp_incl_scan(deg, lane);
-                const uint32_t excl = incl - deg;
-                const uint32_t T = __shfl_sync(FULL, incl, 31);
-                if (s_single) {
-                    for (uint32_t e0 = 0; e0 < T; e0 += 32 * kBEdges) {
-                        bool act[kBEdges];
-                        int tt[kBEdges], uu[kBEdges];
-                        uint32_t ww[kBEdges];
+                    // light rows: kBEdges x 32 edges per step over the warp's concatenated rows
+                    const uint32_t incl = warp_incl_scan(deg, lane);
+                    const uint32_t excl = incl - deg;
+                    const uint32_t T = __shfl_sync(FULL, incl, 31);
+                    const int32_t* col = s_slots[gslot[g]].col;
+                    if (s_single) {
+                        const int tq = targets[toff[g]];
+                        for (uint32_t e0 = 0; e0 < T; e0 += 32 * kBEdges) {
+                            bool act[kBEdges];
+                            int tt[kBEdges], uu[kBEdges];
+                            uint32_t ww[kBEdges];
 #pragma unroll
-                        for (int c = 0; c < kBEdges; ++c) {
-                            const uint32_t x = e0 + 32 * c + lane;
+                            for (int c = 0; c < kBEdges; ++c) {
+                                const uint32_t x = e0 + 32 * c + lane;
+                                const int j = warp_upper_lane(excl, x);
+                                const uint32_t lo_j = __shfl_sync(FULL, lo, j);
+                                const uint32_t ex_j = __shfl_sync(FULL, excl, j);
+                                ww[c] = __shfl_sync(FULL, w, j);
+                                act[c] = x < T;
+                                uu[c] = act[c] ? col[lo_j + (x - ex_j)] : 0;
+                                tt[c] = tq;
+                            }
+                            bvisit<kBEdges>(p, fnext, anext, act, tt, uu, ww, nact);
+                        }
+                    } else {
+                        for (uint32_t e0 = 0; e0 < T; e0 += 32) {
+                            const uint32_t x = e0 + lane;
                             const int j = warp_upper_lane(excl, x);
                             const uint32_t lo_j = __shfl_sync(FULL, lo, j);
                             const uint32_t ex_j = __shfl_sync(FULL, excl, j);
-                            const int g_j = __shfl_sync(FULL, g, j);
-                            ww[c] = __shfl_sync(FULL, w, j);
-                            act[c] = x < T;
-                            uu[c] = act[c] ? s_slots[gslot[g_j]].col[lo_j + (x - ex_j)] : 0;
-                            tt[c] = act[c] ? targets[toff[g_j]] : 0;
-                        }
-                        bvisit<kBEdges>(p, fnext, nxt, lnext, act, tt, uu, ww, st, lane);
-                    }
-                } else {
-                    for (uint32_t e0 = 0; e0 < T; e0 += 32) {
-                        const uint32_t x = e0 + lane;
-                        const int j = warp_upper_lane(excl, x);
-                        const uint32_t lo_j = __shfl_sync(FULL, lo, j);
-                        const uint32_t ex_j = __shfl_sync(FULL, excl, j);
-                        const int g_j = __shfl_sync(FULL, g, j);
-                        const uint32_t w_j = __shfl_sync(FULL, w, j);
-                        const bool a0 = x < T;
-                        const int u = a0 ? s_slots[gslot[g_j]].col[lo_j + (x - ex_j)] : 0;
-                        // targets of g_j: warp-uniform trip count
-                        const int t0 = a0 ? toff[g_j] : 0, t1 = a0 ? toff[g_j + 1] : 0;
-                        int nt = t1 - t0;
-                        for (int d = 16; d >= 1; d >>= 1) nt = max(nt, __shfl_xor_sync(FULL, nt, d));
-                        for (int k2 = 0; k2 < nt; ++k2) {
-                            const bool act[1] = {a0 && t0 + k2 < t1};
-                            const int tt[1] = {act[0] ? targets[t0 + k2] : 0};
-                            const int uu[1] = {u};
-                            const uint32_t ww[1] = {w_j};
-                            bvisit<1>(p, fnext, nxt, lnext, act, tt, uu, ww, st, lane);
+                            const uint32_t w_j = __shfl_sync(FULL, w, j);
+                            const bool a0 = x < T;
+                            const int u = a0 ? col[lo_j + (x - ex_j)] : 0;
+                            for (int t = toff[g]; t < toff[g + 1]; ++t) {
+                                const bool act[1] = {a0};
+                                const int tt[1] = {targets[t]};
+                                const int uu[1] = {u};
+                                const uint32_t ww[1] = {w_j};
+                                bvisit<1>(p, fnext, anext, act, tt, uu, ww, nact);
+                            }
                         }
                     }
                 }
             }
         }
-        bphase_end(p, nxt, lnext, st, lane, te, rows, nnew, active, cur, s_red, &s_or);
+        bphase_end(p, nxt, nact, te, rows, nnew, items, active, cur, s_red, &s_or);
+        nact = 0;
         grid_barrier_on(&ctl->bar, &ctl->abort, ++e, bar_base);
 
         // ---- phase 2: heavy chunks, spread over every warp of the grid
@@ -469,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
                             tt[c2] = targets[t0];
                             ww[c2] = h.w;
                         }
-                        bvisit<kBEdges>(p, fnext, nxt, lnext, act, tt, uu, ww, st, lane);
+                        bvisit<kBEdges>(p, fnext, anext, act, tt, uu, ww, nact);
                     }
                 } else {
                     for (uint32_t a = h.x; a < h.y; a += 32) {
@@ -480,12 +454,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
                             const int tt[1] = {targets[t]};
                             const int uu[1] = {u};
                             const uint32_t ww[1] = {h.w};
-                            bvisit<1>(p, fnext, nxt, lnext, act, tt, uu, ww, st, lane);
+                            bvisit<1>(p, fnext, anext, act, tt, uu, ww, nact);
                         }
                     }
                 }
             }
-            bphase_end(p, nxt, lnext, st, lane, 0ull, 0ull, 0ull, 0u, cur, s_red, &s_or);
+            bphase_end(p, nxt, nact, 0ull, 0ull, 0ull, 0ull, 0u, cur, s_red, &s_or);
+            nact = 0;
             grid_barrier_on(&ctl->bar, &ctl->abort, ++e, bar_base);
         }
         ++L;

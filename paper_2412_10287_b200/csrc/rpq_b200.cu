@@ -126,15 +126,15 @@ struct rpq_query {
     // multi-source batch workspace (batch_kernel.cuh), allocated on first use
     uint32_t* d_bvis = nullptr;
     uint32_t* d_bfw[2] = {nullptr, nullptr};
-    uint2* d_blist[2] = {nullptr, nullptr};
+    uint32_t* d_bact[2] = {nullptr, nullptr};
     uint4* d_bheavy = nullptr;
     BCtl* d_bctl = nullptr;
     BCtl* h_bctl = nullptr;  // pinned
     BatchArgs* d_bargs = nullptr;
     BatchArgs* h_bargs = nullptr;  // pinned
     uint32_t* d_bout = nullptr;
-    long long bnvp = 0;
-    unsigned long long blist_cap = 0, bheavy_cap = 0;
+    long long bnvp = 0, bnblk = 0;
+    unsigned long long bheavy_cap = 0;
     int bgrid = 0;
     int bnsrc = 0;
     unsigned int bbar_next = 0;
@@ -305,7 +305,7 @@ void free_query_buffers(rpq_query* q) {
     if (q->d_bvis) cudaFree(q->d_bvis);
     for (int b = 0; b < 2; ++b) {
         if (q->d_bfw[b]) cudaFree(q->d_bfw[b]);
-        if (q->d_blist[b]) cudaFree(q->d_blist[b]);
+        if (q->d_bact[b]) cudaFree(q->d_bact[b]);
     }
     if (q->d_bheavy) cudaFree(q->d_bheavy);
     if (q->d_bctl) cudaFree(q->d_bctl);
@@ -1080,9 +1080,9 @@ int batch_alloc(rpq_query* q) {
             const int rc_ = cuda_fail(e_, #expr);                     \
             for (int b = 0; b < 2; ++b) {                             \
                 if (q->d_bfw[b]) cudaFree(q->d_bfw[b]);               \
-                if (q->d_blist[b]) cudaFree(q->d_blist[b]);           \
+                if (q->d_bact[b]) cudaFree(q->d_bact[b]);             \
                 q->d_bfw[b] = nullptr;                                \
-                q->d_blist[b] = nullptr;                              \
+                q->d_bact[b] = nullptr;                               \
             }                                                         \
             if (q->d_bheavy) cudaFree(q->d_bheavy);                   \
             if (q->d_bctl) cudaFree(q->d_bctl);                       \
@@ -1102,19 +1102,17 @@ int batch_alloc(rpq_query* q) {
         }                                                             \
     } while (0)
     const long long nv = q->g->nv;
-    q->bnvp = (nv + 127) / 128 * 128;
-    // every (state, vertex) item is listed at most once per level
-    q->blist_cap = (unsigned long long)q->nstates * (unsigned long long)std::max<long long>(nv, 1);
+    q->bnvp = std::max<long long>((nv + kBlockWords - 1) / kBlockWords, 1) * kBlockWords;
+    q->bnblk = q->bnvp / kBlockWords;
     // rows longer than kLightDeg: at most nnz / kLightDeg of them per group and
     // level, each cut into ceil(deg / kChunk) chunks
     q->bheavy_cap = q->edge_bound / kLightDeg + q->edge_bound / kChunk + 1024;
-    if (q->blist_cap >= 0xFFFFFFFFull || q->bheavy_cap >= 0xFFFFFFFFull)
-        return fail(RPQ_EINVAL, "batch frontier would exceed 2^32 entries");
+    if (q->bheavy_cap >= 0xFFFFFFFFull) return fail(RPQ_EINVAL, "batch chunk list would exceed 2^32 entries");
     const size_t words = (size_t)q->nstates * (size_t)q->bnvp;
     BTRY(cudaMalloc(&q->d_bvis, words * 4));
     for (int b = 0; b < 2; ++b) {
         BTRY(cudaMalloc(&q->d_bfw[b], words * 4));
-        BTRY(cudaMalloc(&q->d_blist[b], (size_t)q->blist_cap * sizeof(uint2)));
+        BTRY(cudaMalloc(&q->d_bact[b], (size_t)q->nstates * (size_t)q->bnblk * 4));
     }
     BTRY(cudaMalloc(&q->d_bheavy, (size_t)q->bheavy_cap * sizeof(uint4)));
     BTRY(cudaMalloc(&q->d_bctl, sizeof(BCtl)));
@@ -1168,14 +1166,14 @@ int rpq_query_run_batch(rpq_query* q, int32_t nsrc, const int32_t* sources, doub
     p.vis = q->d_bvis;
     for (int b = 0; b < 2; ++b) {
         p.fw[b] = q->d_bfw[b];
-        p.list[b] = q->d_blist[b];
+        p.act[b] = q->d_bact[b];
     }
     p.heavy = q->d_bheavy;
     p.ctl = q->d_bctl;
     p.out = q->d_bout;
     p.nvp = q->bnvp;
+    p.nblk = q->bnblk;
     p.W = q->W;
-    p.list_cap = q->blist_cap;
     p.heavy_cap = q->bheavy_cap;
     p.nv = q->g->nv;
     p.nstates = q->nstates;
