@@ -32,7 +32,9 @@ constexpr uint32_t kLightDeg = 64;     // rows up to this many edges stay in pha
 constexpr uint32_t kChunk = 256;       // edges per heavy chunk
 constexpr int kBlockShift = 8;         // activity flag per 2^8 vertices
 constexpr int kBlockWords = 1 << kBlockShift;
-constexpr int kBEdges = 4;             // edges per lane in flight per step
+constexpr int kBEdges = 4;             // edges per lane in flight per step (chunks)
+constexpr int kGroups = 2;             // phase 1: groups of a state expanded together
+constexpr int kGEdges = 2;             // phase 1: edges per lane and group per step
 
 struct BCnt {
     unsigned int nact;         // active blocks of M_L (flags raised while producing it)
@@ -125,6 +127,35 @@ __device__ __forceinline__ void bvisit(const BParams& p, uint32_t* fnext, uint32
 #pragma unroll
     for (int c = 0; c < K; ++c)
         if (!fl[c] && atomicExch(flag[c], 1u) == 0u) ++nact;
+}
+
+// Rows longer than kLightDeg become chunks of kChunk edges for phase 2 (one
+// atomic per warp); returns the degree phase 1 expands itself (0 if chunked).
+__device__ __forceinline__ uint32_t split_heavy(const BParams& p, BCnt* cur, BCnt* nxt, int g, uint32_t lo,
+                                                uint32_t deg, uint32_t w, int lane) {
+    const bool heavy = deg > kLightDeg;
+    const uint32_t nch = heavy ? (deg + kChunk - 1) / kChunk : 0u;
+    const uint32_t cincl = warp_incl_scan(nch, lane);
+    const uint32_t ctot = __shfl_sync(FULL, cincl, 31);
+    if (ctot) {
+        unsigned cbase = 0;
+        if (lane == 0) cbase = atomicAdd(&cur->nheavy, ctot);
+        cbase = __shfl_sync(FULL, cbase, 0);
+        if (heavy) {
+            const unsigned long long c0 = (unsigned long long)cbase + cincl - nch;
+            for (uint32_t c = 0; c < nch; ++c) {
+                if (c0 + c < p.heavy_cap) {
+                    const uint32_t a = lo + c * kChunk;
+                    const uint32_t b = min(lo + deg, a + kChunk);
+                    p.heavy[c0 + c] = make_uint4(a, b, (uint32_t)g, w);
+                } else {
+                    atomicExch(&nxt->overflow, 1u);
+                }
+            }
+            return 0u;
+        }
+    }
+    return deg;
 }
 
 // End of a phase: per-CTA sums into the counters.
@@ -339,64 +370,86 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
                     ++items;
                     active |= w;
                 }
-                for (int kg = 0; kg < ng; ++kg) {
-                    const int g = gbeg[q] + kg;
-                    uint32_t lo = 0, deg = 0;
-                    if (w) {
-                        const Slot sl = s_slots[gslot[g]];
-                        lo = sl.rowptr[v];
-                        deg = sl.rowptr[v + 1] - lo;
-                    }
-                    te += (unsigned long long)deg * __popc(w);
-                    rows += deg;
-                    // heavy rows -> chunks of kChunk edges (one atomic per warp)
-                    const bool heavy = deg > kLightDeg;
-                    const uint32_t nch = heavy ? (deg + kChunk - 1) / kChunk : 0u;
-                    const uint32_t cincl = warp_incl_scan(nch, lane);
-                    const uint32_t ctot = __shfl_sync(FULL, cincl, 31);
-                    if (ctot) {
-                        unsigned cbase = 0;
-                        if (lane == 0) cbase = atomicAdd(&cur->nheavy, ctot);
-                        cbase = __shfl_sync(FULL, cbase, 0);
-                        if (heavy) {
-                            const unsigned long long c0 = (unsigned long long)cbase + cincl - nch;
-                            for (uint32_t c = 0; c < nch; ++c) {
-                                if (c0 + c < p.heavy_cap) {
-                                    const uint32_t a = lo + c * kChunk;
-                                    const uint32_t b = min(lo + deg, a + kChunk);
-                                    p.heavy[c0 + c] = make_uint4(a, b, (uint32_t)g, w);
-                                } else {
-                                    atomicExch(&nxt->overflow, 1u);
+                if (s_single) {
+                    // a DFA: every group has one target.  Up to kGroups groups
+                    // at once: their row pointers, then their column loads,
+                    // in flight together
+                    for (int kg0 = 0; kg0 < ng; kg0 += kGroups) {
+                        uint32_t lo[kGroups], deg[kGroups], excl[kGroups], T[kGroups];
+                        int tq[kGroups];
+                        const int32_t* colk[kGroups];
+#pragma unroll
+                        for (int k = 0; k < kGroups; ++k) {
+                            lo[k] = deg[k] = 0;
+                            tq[k] = 0;
+                            colk[k] = nullptr;
+                            if (kg0 + k < ng) {
+                                const int g = gbeg[q] + kg0 + k;
+                                const Slot sl = s_slots[gslot[g]];
+                                colk[k] = sl.col;
+                                tq[k] = targets[toff[g]];
+                                if (w) {
+                                    lo[k] = sl.rowptr[v];
+                                    deg[k] = sl.rowptr[v + 1];
                                 }
                             }
-                            deg = 0u;
+                        }
+                        uint32_t Tmax = 0;
+#pragma unroll
+                        for (int k = 0; k < kGroups; ++k) {
+                            if (kg0 + k >= ng) {
+                                T[k] = excl[k] = 0;
+                                continue;
+                            }
+                            const int g = gbeg[q] + kg0 + k;
+                            deg[k] -= lo[k];
+                            te += (unsigned long long)deg[k] * __popc(w);
+                            rows += deg[k];
+                            deg[k] = split_heavy(p, cur, nxt, g, lo[k], deg[k], w, lane);
+                            const uint32_t incl = warp_incl_scan(deg[k], lane);
+                            excl[k] = incl - deg[k];
+                            T[k] = __shfl_sync(FULL, incl, 31);
+                            Tmax = max(Tmax, T[k]);
+                        }
+                        for (uint32_t e0 = 0; e0 < Tmax; e0 += 32 * kGEdges) {
+                            constexpr int K = kGroups * kGEdges;
+                            bool act[K];
+                            int tt[K], uu[K];
+                            uint32_t ww[K];
+#pragma unroll
+                            for (int k = 0; k < kGroups; ++k) {
+#pragma unroll
+                                for (int c = 0; c < kGEdges; ++c) {
+                                    const int i = k * kGEdges + c;
+                                    const uint32_t x = e0 + 32 * c + lane;
+                                    const int j = warp_upper_lane(excl[k], x);
+                                    const uint32_t lo_j = __shfl_sync(FULL, lo[k], j);
+                                    const uint32_t ex_j = __shfl_sync(FULL, excl[k], j);
+                                    ww[i] = __shfl_sync(FULL, w, j);
+                                    act[i] = x < T[k];
+                                    uu[i] = act[i] ? colk[k][lo_j + (x - ex_j)] : 0;
+                                    tt[i] = tq[k];
+                                }
+                            }
+                            bvisit<K>(p, fnext, anext, act, tt, uu, ww, nact);
                         }
                     }
-                    // light rows: kBEdges x 32 edges per step over the warp's concatenated rows
-                    const uint32_t incl = warp_incl_scan(deg, lane);
-                    const uint32_t excl = incl - deg;
-                    const uint32_t T = __shfl_sync(FULL, incl, 31);
-                    const int32_t* col = s_slots[gslot[g]].col;
-                    if (s_single) {
-                        const int tq = targets[toff[g]];
-                        for (uint32_t e0 = 0; e0 < T; e0 += 32 * kBEdges) {
-                            bool act[kBEdges];
-                            int tt[kBEdges], uu[kBEdges];
-                            uint32_t ww[kBEdges];
-#pragma unroll
-                            for (int c = 0; c < kBEdges; ++c) {
-                                const uint32_t x = e0 + 32 * c + lane;
-                                const int j = warp_upper_lane(excl, x);
-                                const uint32_t lo_j = __shfl_sync(FULL, lo, j);
-                                const uint32_t ex_j = __shfl_sync(FULL, excl, j);
-                                ww[c] = __shfl_sync(FULL, w, j);
-                                act[c] = x < T;
-                                uu[c] = act[c] ? col[lo_j + (x - ex_j)] : 0;
-                                tt[c] = tq;
-                            }
-                            bvisit<kBEdges>(p, fnext, anext, act, tt, uu, ww, nact);
+                } else {
+                    for (int kg = 0; kg < ng; ++kg) {
+                        const int g = gbeg[q] + kg;
+                        uint32_t lo = 0, deg = 0;
+                        if (w) {
+                            const Slot sl = s_slots[gslot[g]];
+                            lo = sl.rowptr[v];
+                            deg = sl.rowptr[v + 1] - lo;
                         }
-                    } else {
+                        te += (unsigned long long)deg * __popc(w);
+                        rows += deg;
+                        deg = split_heavy(p, cur, nxt, g, lo, deg, w, lane);
+                        const uint32_t incl = warp_incl_scan(deg, lane);
+                        const uint32_t excl = incl - deg;
+                        const uint32_t T = __shfl_sync(FULL, incl, 31);
+                        const int32_t* col = s_slots[gslot[g]].col;
                         for (uint32_t e0 = 0; e0 < T; e0 += 32) {
                             const uint32_t x = e0 + lane;
                             const int j = warp_upper_lane(excl, x);
