@@ -198,6 +198,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
     __shared__ unsigned long long s_red[5 * kWarps];
     __shared__ unsigned s_or;
     __shared__ unsigned s_task;
+    __shared__ unsigned s_nlist;
+    __shared__ uint32_t s_list[kThreads];  // active blocks of the current group
     __shared__ int s_single;  // every (state, symbol) group has exactly one target (a DFA)
     __shared__ BatchArgs s_run;
 
@@ -335,20 +337,33 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
         uint32_t* anext = p.act[(L + 1) & 1];
         uint32_t* fcur = p.fw[L & 1];
         uint32_t* fnext = p.fw[(L + 1) & 1];
-        if (threadIdx.x == 0) s_task = 0;
-        __syncthreads();
-
         // ---- phase 1: a warp per active block; light rows now, heavy rows as chunks
         unsigned long long te = 0, rows = 0, nnew = 0, items = 0;
         uint32_t active = 0;
+        // CTA c owns blocks c, c + G, c + 2G, ... (hubs spread over SMs); it
+        // reads kThreads of their flags at once, lists the active ones in
+        // shared memory, and its warps take them from a shared counter
+        for (long long i0 = 0; blockIdx.x + i0 * gridDim.x < nbt; i0 += kThreads) {
+            if (threadIdx.x == 0) {
+                s_nlist = 0;
+                s_task = 0;
+            }
+            __syncthreads();
+            {
+                const long long b = blockIdx.x + (i0 + threadIdx.x) * gridDim.x;
+                if (b < nbt && __ldcg(acur + b) != 0u) {
+                    acur[b] = 0u;  // consumed (level L+2 raises it again)
+                    s_list[atomicAdd(&s_nlist, 1u)] = (uint32_t)b;
+                }
+            }
+            __syncthreads();
+            const unsigned nlisted = s_nlist;
         for (;;) {
             unsigned k = 0;
             if (lane == 0) k = atomicAdd(&s_task, 1u);
             k = __shfl_sync(FULL, k, 0);
-            const long long blk = blockIdx.x + (long long)k * gridDim.x;
-            if (blk >= nbt) break;
-            if (__ldcg(acur + blk) == 0u) continue;  // warp-uniform
-            if (lane == 0) acur[blk] = 0u;            // consumed (level L+2 raises it again)
+            if (k >= nlisted) break;
+            const long long blk = s_list[k];
             const int q = (int)(blk / p.nblk);
             const long long v0 = (blk - (long long)q * p.nblk) * kBlockWords;
             uint32_t* row = fcur + (long long)q * p.nvp;
@@ -469,6 +484,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
                     }
                 }
             }
+        }
+            __syncthreads();  // s_list / s_task are refilled for the next group of blocks
         }
         bphase_end(p, nxt, nact, te, rows, nnew, items, active, cur, s_red, &s_or);
         nact = 0;
