@@ -177,6 +177,13 @@ RPQ_API int rpq_query_set_tuning(rpq_query* q, int32_t key, double value);
 RPQ_API int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream);
 /* Wait for the last run; fills stats (may be NULL) and returns its status. */
 RPQ_API int rpq_query_wait(rpq_query* q, rpq_stats* stats);
+/* One evaluation, start to answer, in one call (the eval_ssr fast path):
+ * rpq_query_set_options + small-kernel switch + run on the query's stream +
+ * wait + the answer bitmap (ceil(nv/32) words; NULL/0 to keep it on the
+ * device).  Returns the run's status; stats may be NULL. */
+RPQ_API int rpq_query_eval(rpq_query* q, int32_t source, double timeout_s, int32_t direction, int32_t count_te,
+                           double alpha, int32_t allow_small, rpq_stats* stats, uint32_t* reach_words,
+                           int64_t nwords);
 /* Device pointer to the uint8[num_vertices] answer of the last run. */
 RPQ_API int rpq_query_reach_device(rpq_query* q, uint8_t** d_reach);
 /* Copy the answer of the last run to host (uint8[num_vertices], 1 = reachable). */

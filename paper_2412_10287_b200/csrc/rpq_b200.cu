@@ -914,6 +914,22 @@ int rpq_query_wait(rpq_query* q, rpq_stats* stats) {
     return RPQ_OK;
 }
 
+int rpq_query_eval(rpq_query* q, int32_t source, double timeout_s, int32_t direction, int32_t count_te,
+                   double alpha, int32_t allow_small, rpq_stats* stats, uint32_t* reach_words, int64_t nwords) {
+    if (!q) return fail(RPQ_EINVAL, "null query");
+    const int64_t words = ((int64_t)q->g->nv + 31) / 32;
+    if (reach_words == nullptr ? nwords != 0 : nwords < words) return fail(RPQ_EINVAL, "answer buffer too small");
+    int rc = rpq_query_set_options(q, direction, count_te, alpha);
+    if (rc == RPQ_OK) rc = rpq_query_set_tuning(q, RPQ_TUNE_SMALL, allow_small ? 1.0 : 0.0);
+    if (rc == RPQ_OK) rc = rpq_query_set_output(q, reach_words ? 1 : 0);
+    if (rc == RPQ_OK) rc = rpq_query_run(q, source, timeout_s, nullptr);
+    if (rc != RPQ_OK) return rc;
+    rc = rpq_query_wait(q, stats);
+    if (rc != RPQ_OK) return rc;
+    if (reach_words && words) std::memcpy(reach_words, q->h_reach_bits, (size_t)words * 4);
+    return RPQ_OK;
+}
+
 int rpq_query_reach_device(rpq_query* q, uint8_t** d_reach) {
     if (!q || !d_reach) return fail(RPQ_EINVAL, "null argument");
     *d_reach = q->d_reach;

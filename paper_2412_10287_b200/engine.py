@@ -197,29 +197,22 @@ def _run(g, n, source, opts, tag, *, want_stats=False):
     lib = _lib.engine()
     q = dg.acquire_query(table)
     try:
-        raise_for_status(lib.rpq_query_set_options(
-            q, DIRECTIONS[opts.direction], int(opts.count_te or opts.debug_checks), opts.alpha),
-            "rpq_query_set_options")
-        raise_for_status(lib.rpq_query_set_tuning(q, 4, 1.0 if opts.kernel == "auto" else 0.0),
-                         "rpq_query_set_tuning")
-        raise_for_status(lib.rpq_query_set_output(q, 1), "rpq_query_set_output")
         # _Clock.check(0) at the top of the first iteration (engine.py:87-89)
         remaining = opts.timeout - (time.monotonic() - t0)
         if remaining < 0 or opts.timeout == 0:
             raise QueryTimeout(time.monotonic() - t0, 0)
         budget = -1.0 if math.isinf(remaining) else remaining
-        raise_for_status(lib.rpq_query_run(q, int(source), budget, None), "rpq_query_run")
+        words = np.empty((g.num_vertices + 31) // 32, dtype=np.uint32)
         stats = _lib.RpqStats()
-        rc = lib.rpq_query_wait(q, ctypes.byref(stats))
+        # options, run, wait and the answer bitmap in one C call
+        rc = lib.rpq_query_eval(q, int(source), budget, DIRECTIONS[opts.direction],
+                                int(opts.count_te or opts.debug_checks), opts.alpha,
+                                1 if opts.kernel == "auto" else 0, ctypes.byref(stats),
+                                _lib.ptr(words, ctypes.c_uint32) if words.size else None, words.size)
         if rc == _lib.RPQ_ETIMEOUT:
             raise QueryTimeout(time.monotonic() - t0,
                                _iterations_for(tag, stats.iterations, table.starts.size))
-        raise_for_status(rc, "rpq_query_wait")
-        # the answer bitmap is already in pinned host memory (output mode 1)
-        words = np.empty((g.num_vertices + 31) // 32, dtype=np.uint32)
-        if g.num_vertices:
-            raise_for_status(lib.rpq_query_copy_reach_bits(q, _lib.ptr(words, ctypes.c_uint32),
-                                                           words.size), "rpq_query_copy_reach_bits")
+        raise_for_status(rc, "rpq_query_eval")
         iterations = _iterations_for(tag, stats.iterations, table.starts.size)
         if opts.debug_checks:
             _debug_invariants(lib, q, table, g.num_vertices, stats, iterations)

@@ -227,6 +227,7 @@ class DeviceGraph:
         if rc:
             _raise_status(rc, "rpq_graph_create")
         self.handle = handle
+        self._resident = set()  # labels known to be resident (they stay resident)
         self._lock = threading.Lock()
         self._queries = {}
         self._finalizer = weakref.finalize(self, DeviceGraph._release, handle.value, self._queries)
@@ -252,14 +253,18 @@ class DeviceGraph:
 
     def ensure_labels(self, labels):
         """Upload every listed label (forward + backward CSR) not yet resident."""
+        if self._resident.issuperset(labels):  # the per-query fast path: no C call
+            return
         lib = _lib.engine()
         for label in labels:
             if lib.rpq_graph_label_resident(self.handle, label):
+                self._resident.add(label)
                 continue
             if self.ingest == "coo":
                 rc = lib.rpq_graph_materialize_label(self.handle, label)
                 if rc:
                     _raise_status(rc, f"device build of label {label}")
+                self._resident.add(label)
                 continue
             host = self.host
             if host is None:
@@ -282,6 +287,7 @@ class DeviceGraph:
                     _lib.ptr(bi, ctypes.c_int64))
             if rc:
                 _raise_status(rc, f"upload of label {label}")
+            self._resident.add(label)
 
     def label_csr(self, label, transpose=False):
         """(rowptr uint32[|V|+1], col int32[nnz]) of a resident label, copied back."""
