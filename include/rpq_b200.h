@@ -201,10 +201,14 @@ RPQ_API int rpq_query_step(rpq_query* q, const uint32_t* m_words, const uint32_t
  * starts level L); slots 5-6 unused) in ns from kernel
  * start at host[(L * grid + c) * 8 + k]; *grid receives the CTA count. */
 RPQ_API int rpq_query_copy_trace(rpq_query* q, uint64_t* host, int64_t n, int32_t* grid);
+/* Owned target words [word_lo, word_hi) of a partitioned rank: a pull step
+ * scans only these targets (empty range: all).  Default empty. */
+RPQ_API int rpq_query_set_owned(rpq_query* q, int64_t word_lo, int64_t word_hi);
 /* Words per state row of the query's bitmaps (>= ceil(nv/32), multiple of 4). */
 RPQ_API int rpq_query_row_words(const rpq_query* q, int64_t* row_words);
 /* Device-resident step for the vertex-partitioned evaluator:
- * on `stream`, out = step_sum(M) masked by the complement of P, and P |= out.
+ * on `stream`, out = step_sum(M) masked by the complement of P, and P |= out,
+ * by push or (direction auto/pull, M dense) pull over the owned targets.
  * d_m, d_p, d_out are device bitmaps of nstates rows x rpq_query_row_words
  * words, distinct.  Asynchronous; rpq_query_wait returns its status. */
 RPQ_API int rpq_query_step_device(rpq_query* q, const uint32_t* d_m, uint32_t* d_p, uint32_t* d_out,

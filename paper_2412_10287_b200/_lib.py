@@ -151,6 +151,7 @@ ENGINE_SIGNATURES = {
     "rpq_query_io_bytes": (c_i32, [c_vp, P_i64, P_i64]),
     "rpq_query_destroy": (c_i32, [c_vp]),
     "rpq_query_row_words": (c_i32, [c_vp, P_i64]),
+    "rpq_query_set_owned": (c_i32, [c_vp, c_i64, c_i64]),
     "rpq_query_eval": (c_i32, [c_vp, c_i32, c_dbl, c_i32, c_i32, c_dbl, c_i32, ctypes.POINTER(RpqStats), P_u32,
                                c_i64]),
     "rpq_query_copy_trace": (c_i32, [c_vp, P_u64, c_i64, P_i32]),

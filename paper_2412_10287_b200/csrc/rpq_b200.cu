@@ -109,6 +109,7 @@ struct rpq_query {
     int emit_mode = 0;
     unsigned int emit_inline_max = 1u << 16;
     unsigned int run_flags = RF_NO_PROBE;
+    long long own_w0 = 0, own_w1 = 0;  // owned word range (partitioned step); empty = all
     bool small_ok = false;    // |Q| x |V| fits the single-CTA kernel
     int allow_small = 1;      // RPQ_TUNE_SMALL
     size_t small_smem = 0;
@@ -1014,6 +1015,14 @@ int rpq_query_copy_trace(rpq_query* q, uint64_t* host, int64_t n, int32_t* grid)
     return RPQ_OK;
 }
 
+int rpq_query_set_owned(rpq_query* q, int64_t word_lo, int64_t word_hi) {
+    if (!q) return fail(RPQ_EINVAL, "null query");
+    if (word_lo < 0 || word_hi < word_lo || word_hi > q->W) return fail(RPQ_EINVAL, "bad owned word range");
+    q->own_w0 = word_lo;
+    q->own_w1 = word_hi;
+    return RPQ_OK;
+}
+
 int rpq_query_row_words(const rpq_query* q, int64_t* row_words) {
     if (!q || !row_words) return fail(RPQ_EINVAL, "null argument");
     *row_words = q->W;
@@ -1032,10 +1041,13 @@ int rpq_query_step_device(rpq_query* q, const uint32_t* d_m, uint32_t* d_p, uint
     }
     RunArgs ra{};
     ra.mode = 1;
-    ra.dir_mode = 1;
+    ra.dir_mode = q->dir_mode;  // auto: pull when M is dense against the owned targets
     ra.alpha = q->alpha;
     ra.budget_ns = ~0ull;
     ra.bar_base = q->bar_next;
+    ra.flags = q->run_flags;
+    ra.own_w0 = q->own_w0;
+    ra.own_w1 = q->own_w1;
     *reinterpret_cast<RunArgs*>(q->h_in) = ra;
     // the caller's buffers stand in for P and F_0 / F_1; F_2 is the query's
     // (step mode reads F_0, writes F_1, zeroes F_1 and F_2 first, keeps P)

@@ -115,6 +115,7 @@ struct RunArgs {
                             // in vertex order (plan epoch); 2: by frontier size
     unsigned int emit_inline_max;  // mode 2: inline while |F_L| < this
     unsigned int flags;            // RF_* push-path variants (tuning)
+    long long own_w0, own_w1;      // step mode: owned word range of a partitioned rank (empty: all)
 };
 
 constexpr unsigned RF_NO_PROBE = 1u;     // claim with atomicOr without reading P first
@@ -957,16 +958,41 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     if (!step_mode) {
         grid_barrier(ctl, ++e, s_run.bar_base);
         if (wid == 0) decide_level(p, S, e, 0, 1, lane, &s_view, s_bpre, s_sv, s_front);
-    } else if (threadIdx.x == 0) {
-        // one push step from F_0 = M: emit M's rows (plan epoch), expand, stop
-        s_view.done = 0;
-        s_view.dir = DIR_PUSH;
-        s_view.plan = 1;
-        s_view.status = 0;
-        s_view.iterations = 0;
+    } else {
+        // one step from F_0 = M: count M per state (one epoch), then pull
+        // (when M is dense against the owned targets) or push (emit M's rows
+        // in a plan epoch, expand), and stop
+        for (int q = 0; q < p.nstates; ++q) {
+            unsigned c = 0;
+            const uint32_t* row = p.fb[0] + (long long)q * p.W;
+            for (long long i = gtid; i < Wn; i += gthreads) c += __popc(row[i]);
+            c = (unsigned)warp_sum_u64(c);
+            if (lane == 0 && c) atomicAdd(&ctl->fc[0].state[q], c);
+        }
+        grid_barrier(ctl, ++e, s_run.bar_base);
+        if (threadIdx.x == 0) {
+            unsigned long long nf = 0;
+            for (int q = 0; q < p.nstates; ++q) {
+                s_front[q] = ldcg(&ctl->fc[0].state[q]);
+                nf += s_front[q];
+            }
+            int ntarget = 0;
+            for (int q2 = 0; q2 < p.nstates; ++q2) {
+                bool t = false;
+                for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k) t |= s_front[S.isrc[k]] != 0;
+                ntarget += t ? 1 : 0;
+            }
+            const long long own = (s_run.own_w1 > s_run.own_w0 ? s_run.own_w1 - s_run.own_w0 : Wn) * 32;
+            int dir = s_run.dir_mode == 2 ? DIR_PULL : DIR_PUSH;
+            if (s_run.dir_mode == 0 && (float)nf * 24.0f > (float)own * (float)ntarget) dir = DIR_PULL;
+            s_view.done = nf == 0;
+            s_view.dir = dir;
+            s_view.plan = dir == DIR_PUSH;
+            s_view.status = 0;
+            s_view.iterations = 0;
+            s_view.nfront = nf;
+        }
     }
-    if (step_mode)
-        for (int q = threadIdx.x; q < p.nstates; q += blockDim.x) s_front[q] = 1;
     __syncthreads();
 
     // ---- level loop -----------------------------------------------------------
@@ -1163,7 +1189,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                 s_nptarget = n;
             }
             __syncthreads();
-            const long long nblk = (Wn + kPullVerts - 1) / kPullVerts;
+            // targets: the owned word range (vertex-partitioned step), else all
+            const long long pw0 = s_run.own_w1 > s_run.own_w0 ? s_run.own_w0 : 0;
+            const long long pw1 = s_run.own_w1 > s_run.own_w0 ? min((long long)s_run.own_w1, Wn) : Wn;
+            const long long nblk = (pw1 - pw0 + kPullVerts - 1) / kPullVerts;
             const long long ntask = (long long)s_nptarget * nblk;
             for (;;) {
                 long long task = 0;
@@ -1171,13 +1200,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                 task = __shfl_sync(FULL, task, 0);
                 if (task >= ntask) break;
                 const int q2 = s_ptarget[task / nblk];
-                const long long word0 = (task % nblk) * kPullVerts;
+                const long long word0 = pw0 + (task % nblk) * kPullVerts;
                 uint32_t vis[kPullVerts];
                 bool need[kPullVerts], found[kPullVerts];
                 int w[kPullVerts];
 #pragma unroll
                 for (int u = 0; u < kPullVerts; ++u)
-                    vis[u] = word0 + u < Wn ? ld_bits(p.visited + (long long)q2 * p.W + word0 + u, S.pl) : 0xFFFFFFFFu;
+                    vis[u] = word0 + u < pw1 ? ld_bits(p.visited + (long long)q2 * p.W + word0 + u, S.pl) : 0xFFFFFFFFu;
                 bool any_need = false;
 #pragma unroll
                 for (int u = 0; u < kPullVerts; ++u) {

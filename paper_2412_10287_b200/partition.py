@@ -182,7 +182,7 @@ class DeviceStep:
     """next = step(M) <not P>, P |= next: the persistent kernel's step mode on
     the rank's graph (rpq_query_step_device)."""
 
-    def __init__(self, lg, ln, device):
+    def __init__(self, lg, ln, device, owned=None):
         from .engine import PreparedQuery
 
         from .engine import raise_for_status
@@ -194,6 +194,9 @@ class DeviceStep:
         w = ctypes.c_int64()
         raise_for_status(_lib.engine().rpq_query_row_words(self.pq.q, ctypes.byref(w)), "rpq_query_row_words")
         self.row_words = int(w.value)
+        if owned is not None:  # pull steps scan only the owned targets
+            raise_for_status(_lib.engine().rpq_query_set_owned(self.pq.q, int(owned[0]), int(owned[1])),
+                             "rpq_query_set_owned")
 
     def __call__(self, m, p, out, stream):
         from .engine import raise_for_status
@@ -228,7 +231,7 @@ class Shard:
         self.device = device
         if step is None:
             lg, ln = local_problem(g, n, self.v0, self.v1)
-            step = DeviceStep(lg, ln, device)
+            step = DeviceStep(lg, ln, device, owned=(self.w0, self.w1))
         self.step = step
         self.row_words = getattr(step, "row_words", ((nv + 31) // 32 + 3) // 4 * 4)
         shape = (self.nstates, self.row_words)
@@ -240,11 +243,13 @@ def _bit(v):
     return np.array([1 << (v & 31)], dtype=np.uint32).view(np.int32)[0].item()
 
 
-def run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout=math.inf, profile=False):
+def run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout=math.inf, profile=False,
+               bits=False):
     """The partitioned masked loop.  Returns (reach uint8[nv], iterations,
-    stats).  `shards` are the shards of THIS process (one per rank under
-    torch.distributed, all k for LocalExchange).  Device work runs on one
-    dedicated stream shared by the step kernels and the torch operations."""
+    stats) -- the answer as the uint32 bitmap instead with bits=True.  `shards`
+    are the shards of THIS process (one per rank under torch.distributed, all k
+    for LocalExchange).  Device work runs on one dedicated stream shared by the
+    step kernels and the torch operations."""
     import contextlib
 
     import torch
@@ -255,21 +260,25 @@ def run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout=mat
         s.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(s):
             out = _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, s.cuda_stream,
-                              profile)
+                              profile, bits)
         torch.cuda.current_stream(dev).wait_stream(s)
         return out
-    return _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, None, profile)
+    return _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, None, profile, bits)
 
 
-def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, stream, profile):
+def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, stream, profile, bits):
     import torch
 
     t0 = time.monotonic()
     dev = shards[0].device
     nstates = shards[0].nstates
     row_words = shards[0].row_words
+    k = len(ranges)
     wmax = max(max(w1 - w0 for w0, w1 in ranges), 1)
     m = torch.zeros((nstates, row_words), dtype=torch.int32, device=dev)
+    # one shard owning everything: the step's output IS the next frontier (no exchange)
+    alone = k == 1 and len(shards) == 1
+    send = [torch.zeros((nstates, wmax), dtype=torch.int32, device=dev) for _ in shards] if not alone else []
     for sh in shards:
         sh.p.zero_()
     # seed M = P = {(q_s, source)} (engine.py:106-109, :154-155); P on its owner
@@ -291,18 +300,17 @@ def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, s
         iterations += 1
         for sh in shards:
             sh.step(m, sh.p, sh.next, stream)
-        slices = []
-        for sh in shards:
-            sl = torch.zeros((nstates, wmax), dtype=torch.int32, device=dev)
-            sl[:, : sh.w1 - sh.w0] = sh.next[:, sh.w0: sh.w1]
-            slices.append(sl)
-        gathered = exchange.allgather(slices)
-        m.zero_()
-        for r, (w0, w1) in enumerate(ranges):
-            m[:, w0:w1] = gathered[r, :, : w1 - w0]
-        sync()
-        levels_us.append((time.monotonic() - t0) * 1e6)
+        if alone:
+            m, shards[0].next = shards[0].next, m  # the step zeroes its output first
+        else:
+            for sh, sl in zip(shards, send):
+                sl[:, : sh.w1 - sh.w0].copy_(sh.next[:, sh.w0: sh.w1])
+            gathered = exchange.allgather(send)
+            for r, (w0, w1) in enumerate(ranges):
+                m[:, w0:w1].copy_(gathered[r, :, : w1 - w0])
         if profile:
+            sync()
+            levels_us.append((time.monotonic() - t0) * 1e6)
             step_ms.append([sh.step.finish() if hasattr(sh.step, "finish") else 0.0 for sh in shards])
     for sh in shards:
         if hasattr(sh.step, "finish"):
@@ -321,8 +329,10 @@ def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, s
     g_host = gathered.cpu().numpy().view(np.uint32)
     for r, (w0, w1) in enumerate(ranges):
         words[w0:w1] = g_host[r, 0, : w1 - w0]
-    reach = np.unpackbits(words.view(np.uint8), bitorder="little")[:nv]
-    return reach, iterations, {"levels_wall_us": levels_us, "ranges": ranges, "step_ms": step_ms}
+    stats = {"levels_wall_us": levels_us, "ranges": ranges, "step_ms": step_ms}
+    if bits:
+        return words, iterations, stats
+    return np.unpackbits(words.view(np.uint8), bitorder="little")[:nv], iterations, stats
 
 
 def _or_rows(t):
@@ -350,8 +360,8 @@ def eval_ssr_partitioned(g, n, source, opts=None, group=None):
     sh = Shard(g, n, ranges, ex.rank, dev)
     t0 = time.monotonic()
     try:
-        reach, its, _ = run_levels([sh], ex, ranges, g.num_vertices, table.starts.tolist(),
-                                   table.finals.tolist(), int(source), opts.timeout)
+        words, its, _ = run_levels([sh], ex, ranges, g.num_vertices, table.starts.tolist(),
+                                   table.finals.tolist(), int(source), opts.timeout, bits=True)
     finally:
         sh.step.close()
-    return EvalResult(reach, its, time.monotonic() - t0, "masked")
+    return EvalResult(None, its, time.monotonic() - t0, "masked", bits=words, nv=g.num_vertices)
