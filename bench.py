@@ -98,6 +98,27 @@ def read_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def per_level_roofline(st0, level_ns, x, pairs, nstates, nv, peak):
+    """SURVEY §8(d) bytes per level -- 4 E_L + 8 X_L + 8 |F_L| + 2 ceil(|Q||V|/8),
+    E_L the push-model edges out of F_L (counted by the untimed count_te run,
+    pull levels included), X_L = |F_L| x (X / |P|) -- over the level's median
+    device time (decision to decision, from the kernel's own stamps)."""
+    iters = int(st0.iterations)
+    out = []
+    for L in range(min(iters, 63)):
+        ts = [(ln[L + 1] - ln[L]) / 1e3 for ln in level_ns if len(ln) > L + 1 and ln[L + 1] > ln[L]]
+        if not ts:
+            break
+        t_us = statistics.median(ts)
+        f = int(st0.level_new[L])
+        e = int(st0.level_edges[L])
+        b = 4 * max(e, 0) + 8 * (f * x / max(pairs, 1)) + 8 * f + 2 * math.ceil(nstates * nv / 8)
+        gbs = b / (t_us * 1e-6) / 1e9 if t_us > 0 else 0.0
+        out.append({"level": L, "dir": "pull" if st0.level_dir[L] else "push", "frontier": f, "edges": e,
+                    "bytes": int(b), "us": round(t_us, 2), "gbs": round(gbs, 1), "frac": round(gbs / peak, 4)})
+    return out
+
+
 def ncu_traffic(config):
     """DRAM bytes per launch of the step kernel from the committed ncu --set
     full capture (profiles/ncu_dram_bytes.json), or None."""
@@ -307,6 +328,7 @@ def run_engine(args, rank, world, local_rank):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     launches = 0
+    level_ns = []  # per timed step: the kernel's own level stamps
     for k in range(args.steps):
         if not args.no_flush:
             flush.fill_(k & 0xFF)  # > L2: evicts the graph between steps (outside the events)
@@ -316,6 +338,7 @@ def run_engine(args, rank, world, local_rank):
         ev[k][1].record(stream)
         st = pq.wait()
         assert st.visited_pairs == pairs and st.iterations == iters
+        level_ns.append(list(st.level_ns[: min(iters + 1, 64)]))
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -344,13 +367,14 @@ def run_engine(args, rank, world, local_rank):
 
     # max over ranks of the device time, sum over ranks of the product edges
     total_max_ms, units = reduce_timing(total_ms, te * args.steps, dev)
+    peak, peak_src = read_peaks()
+    per_level = per_level_roofline(st0, level_ns, x, pairs, pq.table.nstates, sg.nv, peak)
     e2e_max_s, _ = reduce_timing(sum(e2e_s) if e2e_s else 0.0, 0, dev)
     pq.close()
     if rank != 0:
         return None
 
     value = units / (total_max_ms / 1e3) / 1e9
-    peak, peak_src = read_peaks()
     kernel_s = total_ms / args.steps / 1e3
     achieved = b_alg / kernel_s / 1e9
     out = {
@@ -382,6 +406,9 @@ def run_engine(args, rank, world, local_rank):
             "kernel": "rpq_ssr_kernel (persistent, one launch per query)",
             "algorithmic_bytes_per_launch": b_alg, "peak_source": peak_src,
             "note": "algorithmic bytes of SURVEY.md §8(d) per query / mean step time",
+            "per_level": per_level,
+            # the frontier step with the most edges (north_star's "frontier step" figure)
+            "densest_level_frac": max(per_level, key=lambda lv: lv["edges"])["frac"] if per_level else None,
         },
         "gpu_launches": launches,
         "clocks": clocks,

@@ -645,7 +645,8 @@ __device__ __forceinline__ void queue_scan(const Params& p, const QCnt* qc, int 
 // CTA reads the same counters and reaches the same result).  Mirrors the
 // masked loop (engine.py:156-160): run while the frontier is non-empty,
 // check the deadline, then step; and picks the direction of level L.
-__device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, int prev_queued, int lane,
+__device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, int prev_queued, int prev_dir,
+                             int lane,
                              View* v, unsigned long long* s_bpre, unsigned long long* s_sv,
                              unsigned int* s_front) {
     Ctl* ctl = p.ctl;
@@ -762,6 +763,9 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
                 ctl->level_edges[L] = ledges;
                 ctl->level_dir[L] = next;
             }
+            // count_te: a pull level L-1 also counted F_{L-1}'s push-model edges
+            if (L >= 1 && L - 1 < 64 && prev_dir == DIR_PULL && S.run->count_te)
+                ctl->level_edges[L - 1] = (long long)nedge;
             if (!done) {
                 if (L > 0) ctl->levels = L;
                 if (next == DIR_PULL) atomicAdd(&ctl->pull_levels, 1);
@@ -830,6 +834,29 @@ __device__ __forceinline__ void reset_qc(QCnt* qc, int tid) {
         qc->overflow = 0;
         qc->expire = 0;
     }
+}
+
+// Push-model edges out of frontier F (sum over its pairs of group degree x
+// targets): this thread's share of a grid-stride sweep.  count_te only.
+__device__ unsigned long long frontier_edges(const Params& p, const Smem& S, const uint32_t* f, long long gtid,
+                                             long long gthreads, long long Wn) {
+    unsigned long long te = 0;
+    for (int q = 0; q < p.nstates; ++q) {
+        if (S.gbeg[q + 1] == S.gbeg[q]) continue;
+        for (long long i = gtid; i < Wn; i += gthreads) {
+            uint32_t bits = __ldcg(f + (long long)q * p.W + i);
+            while (bits) {
+                const int v = (int)(i * 32 + __ffs(bits) - 1);
+                bits &= bits - 1;
+                for (int g = S.gbeg[q]; g < S.gbeg[q + 1]; ++g) {
+                    const Slot sl = S.slots[S.gslot[g]];
+                    te += (unsigned long long)(__ldg(sl.rowptr + v + 1) - __ldg(sl.rowptr + v)) *
+                          (unsigned long long)(S.toff[g + 1] - S.toff[g]);
+                }
+            }
+        }
+    }
+    return te;
 }
 
 // Diagnostic stamp k of level L for this CTA (thread 0): 0 level start (after
@@ -957,7 +984,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     }
     if (!step_mode) {
         grid_barrier(ctl, ++e, s_run.bar_base);
-        if (wid == 0) decide_level(p, S, e, 0, 1, lane, &s_view, s_bpre, s_sv, s_front);
+        if (wid == 0) decide_level(p, S, e, 0, 1, DIR_PUSH, lane, &s_view, s_bpre, s_sv, s_front);
     } else {
         // one step from F_0 = M: count M per state (one epoch), then pull
         // (when M is dense against the owned targets) or push (emit M's rows
@@ -1179,6 +1206,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
             }
         } else {
             // ---- pull: unvisited (q', w) scan A_s^T row w for a member of F_L[q]
+            if (S.run->count_te)  // diagnostics: F_L's push-model edges (per-level roofline)
+                nedge += frontier_edges(p, S, fcur, gtid, gthreads, Wn);
             if (threadIdx.x == 0) {
                 int n = 0;
                 for (int q2 = 0; q2 < p.nstates; ++q2) {
@@ -1316,7 +1345,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
             __syncthreads();
             break;
         }
-        if (wid == 0) decide_level(p, S, e, L, queued, lane, &s_view, s_bpre, s_sv, s_front);
+        if (wid == 0) decide_level(p, S, e, L, queued, dir, lane, &s_view, s_bpre, s_sv, s_front);
         __syncthreads();
     }
 

@@ -183,6 +183,10 @@ def test_rmat_vs_oracle(scale, seed, query, direction):
         assert got.iterations == st["iterations"]
         assert got.stats["te"] == st["te"]
         assert got.stats["visited_pairs"] == st["pairs"]
+        # per-level push-model edges (pull levels too, under count_te) add up to TE (DFAs)
+        dfa = all(np.all(np.diff(np.asarray(m.indptr)) <= 1) for m in n.transitions.values())
+        if got.iterations < 64 and dfa:
+            assert sum(got.stats["level_edges"][: got.iterations]) == st["te"], (query, s, direction)
 
 
 def test_cfg3_golden():
