@@ -810,6 +810,11 @@ int rpq_query_set_tuning(rpq_query* q, int32_t key, double value) {
             return RPQ_OK;
         case RPQ_TUNE_TRACE: {
             if (value < 0 || value > 4096) return fail(RPQ_EINVAL, "trace levels must be in [0, 4096]");
+            if (q->inflight) {  // a run in flight may still write the old buffer
+                CUDA_TRY(cudaStreamSynchronize(q->last_stream));
+                q->bar_next = q->h_ctl->bar;
+                q->inflight = false;
+            }
             if (q->d_trace) cudaFree(q->d_trace);
             q->d_trace = nullptr;
             q->trace_levels = (int)value;
