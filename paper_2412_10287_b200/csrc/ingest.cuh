@@ -62,4 +62,30 @@ __global__ void keys_to_csr_kernel(const unsigned long long* __restrict__ keys, 
     }
 }
 
+// Merged adjacency (rows of several slots concatenated per vertex): degree sums
+__global__ void merge_degree_kernel(const uint32_t* const* __restrict__ rowptrs, int k, long long nv,
+                                    uint32_t* __restrict__ deg) {
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        uint32_t d = 0;
+        for (int s = 0; s < k; ++s) d += rowptrs[s][v + 1] - rowptrs[s][v];
+        deg[v + 1] = d;
+    }
+}
+
+// ... and the columns, one warp per vertex (coalesced segment copies)
+__global__ void merge_copy_kernel(const uint32_t* const* __restrict__ rowptrs, const int32_t* const* __restrict__ cols,
+                                  int k, long long nv, const uint32_t* __restrict__ mrow, int32_t* __restrict__ mcol) {
+    const int lane = threadIdx.x & 31;
+    for (long long v = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < nv;
+         v += ((long long)gridDim.x * blockDim.x) >> 5) {
+        uint32_t at = mrow[v];
+        for (int s = 0; s < k; ++s) {
+            const uint32_t lo = rowptrs[s][v], hi = rowptrs[s][v + 1];
+            for (uint32_t e = lo + lane; e < hi; e += 32) mcol[at + (e - lo)] = cols[s][e];
+            at += hi - lo;
+        }
+    }
+}
+
 }  // namespace rpqk

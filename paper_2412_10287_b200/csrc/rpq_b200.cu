@@ -11,6 +11,7 @@
 #include <cstddef>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -71,6 +72,10 @@ struct rpq_graph {
     // keys grouped by label; labels are built from it on first use
     unsigned long long* d_coo = nullptr;
     std::vector<unsigned long long> coo_off;  // nl + 1 segment offsets
+    // merged slots: the rows of several (label, inverted) symbols concatenated
+    // per vertex, built when an automaton state reads them all into the same
+    // targets (e.g. (a|b|c|d)*); keyed by the sorted symbol list
+    std::map<std::vector<std::pair<int, int>>, LabelDev> merged;
 };
 
 struct rpq_query {
@@ -284,6 +289,83 @@ int materialize_label(rpq_graph* g, int32_t l) {
     return RPQ_OK;
 }
 
+// The merged adjacency of `syms` (each (label, inverted), resident) in both
+// directions: direction d of the merged slot holds, per vertex, the rows of
+// every symbol's direction-d matrix (its transpose for d = 1), concatenated.
+// Duplicates across symbols are kept: a target reached twice is claimed once.
+int build_merged(rpq_graph* g, const std::vector<std::pair<int, int>>& syms, LabelDev** out) {
+    auto it = g->merged.find(syms);
+    if (it != g->merged.end()) {
+        *out = &it->second;
+        return RPQ_OK;
+    }
+    LabelDev M;
+    const long long nv = g->nv;
+    const int k = (int)syms.size();
+    const uint32_t** d_rp = nullptr;
+    const int32_t** d_cl = nullptr;
+    void* temp = nullptr;
+    auto cleanup = [&]() {
+        if (d_rp) cudaFree(d_rp);
+        if (d_cl) cudaFree(d_cl);
+        if (temp) cudaFree(temp);
+    };
+#define GTRY(expr)                         \
+    do {                                   \
+        cudaError_t e_ = (expr);           \
+        if (e_ != cudaSuccess) {           \
+            cleanup();                     \
+            free_label(M);                 \
+            return cuda_fail(e_, #expr);   \
+        }                                  \
+    } while (0)
+    GTRY(cudaMalloc(&d_rp, sizeof(uint32_t*) * k));
+    GTRY(cudaMalloc(&d_cl, sizeof(int32_t*) * k));
+    for (int dir = 0; dir < 2; ++dir) {
+        std::vector<const uint32_t*> rp(k);
+        std::vector<const int32_t*> cl(k);
+        unsigned long long nnz = 0;
+        for (int i = 0; i < k; ++i) {
+            const LabelDev& L = g->labels[syms[i].first];
+            const int d = dir == 0 ? syms[i].second : 1 - syms[i].second;
+            rp[i] = L.rowptr[d];
+            cl[i] = L.col[d];
+            nnz += (unsigned long long)L.nnz[d];
+        }
+        if (nnz > 0xFFFFFFFFull) {
+            cleanup();
+            free_label(M);
+            return fail(RPQ_EINVAL, "merged adjacency would exceed 2^32 edges");
+        }
+        GTRY(cudaMemcpy(d_rp, rp.data(), sizeof(uint32_t*) * k, cudaMemcpyHostToDevice));
+        GTRY(cudaMemcpy(d_cl, cl.data(), sizeof(int32_t*) * k, cudaMemcpyHostToDevice));
+        GTRY(cudaMalloc(&M.rowptr[dir], (size_t)(nv + 1) * 4));
+        GTRY(cudaMalloc(&M.col[dir], (size_t)std::max<unsigned long long>(nnz, 1) * 4));
+        GTRY(cudaMemset(M.rowptr[dir], 0, (size_t)(nv + 1) * 4));
+        if (nv > 0) {
+            merge_degree_kernel<<<1184, 256>>>(d_rp, k, nv, M.rowptr[dir]);
+            GTRY(cudaGetLastError());
+            size_t tb = 0;
+            GTRY(cub::DeviceScan::InclusiveSum(nullptr, tb, M.rowptr[dir], M.rowptr[dir], (int)(nv + 1)));
+            GTRY(cudaMalloc(&temp, std::max<size_t>(tb, 16)));
+            GTRY(cub::DeviceScan::InclusiveSum(temp, tb, M.rowptr[dir], M.rowptr[dir], (int)(nv + 1)));
+            cudaFree(temp);
+            temp = nullptr;
+            merge_copy_kernel<<<1184, 256>>>(d_rp, d_cl, k, nv, M.rowptr[dir], M.col[dir]);
+            GTRY(cudaGetLastError());
+        }
+        M.nnz[dir] = (int64_t)nnz;
+        g->bytes += (nv + 1) * 4 + (int64_t)std::max<unsigned long long>(nnz, 1) * 4;
+    }
+    GTRY(cudaDeviceSynchronize());
+#undef GTRY
+    cleanup();
+    M.resident = true;
+    auto res = g->merged.emplace(syms, M);
+    *out = &res.first->second;
+    return RPQ_OK;
+}
+
 void free_query_buffers(rpq_query* q) {
     if (q->d_in) cudaFree(q->d_in);
     if (q->h_in) cudaFreeHost(q->h_in);
@@ -480,6 +562,7 @@ int rpq_graph_destroy(rpq_graph* g) {
     if (!g) return RPQ_OK;
     cudaSetDevice(g->device);
     for (auto& L : g->labels) free_label(L);
+    for (auto& kv : g->merged) free_label(kv.second);
     if (g->d_coo) cudaFree(g->d_coo);
     delete g;
     return RPQ_OK;
@@ -528,14 +611,65 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     if ((int)slot_keys.size() > kMaxSlots) return fail(RPQ_EINVAL, "too many distinct symbols");
     if ((int)group_targets.size() > kMaxGroups)
         return fail(RPQ_EINVAL, "automaton has more than 256 (state, symbol) groups");
+    // slot entries: direction 0 = the push matrix A_s, 1 = its transpose
+    struct SlotEnt {
+        const uint32_t* rowptr[2];
+        const int32_t* col[2];
+        int64_t nnz[2];
+    };
+    std::vector<SlotEnt> ents;
     {
         std::lock_guard<std::mutex> lk(g->mu);
         if (cudaSetDevice(g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
         for (auto& k : slot_keys) {
             const int rc = materialize_label(g, k.first);  // device edge list, if any
             if (rc != RPQ_OK) return rc;
+            const LabelDev& L = g->labels[k.first];
+            ents.push_back(SlotEnt{{L.rowptr[k.second], L.rowptr[1 - k.second]},
+                                   {L.col[k.second], L.col[1 - k.second]},
+                                   {L.nnz[k.second], L.nnz[1 - k.second]}});
+        }
+        // A state that reads several symbols into the same targets (e.g. the
+        // one state of (a|b|c|d)*) gets one merged slot: its rows are the
+        // symbols' rows concatenated, so a pair costs one row-pointer read and
+        // one column run instead of one per symbol; pull in-rows likewise.
+        // RPQ_MERGE=0 in the environment turns this off (A/B measurements).
+        const char* env = std::getenv("RPQ_MERGE");
+        if (!(env && env[0] == '0')) {
+            std::map<std::pair<int, std::set<int>>, std::vector<int>> buckets;
+            for (auto& kv : group_targets) buckets[{kv.first.first, kv.second}].push_back(kv.first.second);
+            std::map<std::vector<std::pair<int, int>>, int> merged_slot;
+            std::map<std::pair<int, int>, std::set<int>> ng;
+            std::map<int, std::set<std::pair<int, int>>> nin;
+            for (auto& b : buckets) {
+                const int st = b.first.first;
+                int sl = b.second[0];
+                if (b.second.size() >= 2) {
+                    std::vector<std::pair<int, int>> syms;
+                    for (int x : b.second) syms.push_back(slot_keys[x]);
+                    std::sort(syms.begin(), syms.end());
+                    auto f = merged_slot.find(syms);
+                    if (f != merged_slot.end()) {
+                        sl = f->second;
+                    } else {
+                        LabelDev* M = nullptr;
+                        const int rc = build_merged(g, syms, &M);
+                        if (rc != RPQ_OK) return rc;
+                        sl = (int)ents.size();
+                        ents.push_back(SlotEnt{{M->rowptr[0], M->rowptr[1]}, {M->col[0], M->col[1]},
+                                               {M->nnz[0], M->nnz[1]}});
+                        merged_slot[syms] = sl;
+                    }
+                }
+                ng[{st, sl}] = b.first.second;
+                for (int t : b.first.second) nin[t].insert({st, sl});
+            }
+            // in-transitions are the same relation read by target: rebuilt from the groups
+            group_targets.swap(ng);
+            in_trans.swap(nin);
         }
     }
+    if ((int)ents.size() > kMaxSlots) return fail(RPQ_EINVAL, "too many distinct symbols");
 
     rpq_query* q = new rpq_query();
     q->g = g;
@@ -554,9 +688,8 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
         for (int t : kv.second) targets.push_back(t);
         toff.push_back((int32_t)targets.size());
         maxT = std::max<int>(maxT, (int)kv.second.size());
-        const auto& key = slot_keys[kv.first.second];
         groups_total += 1;
-        edge_bound += (uint64_t)g->labels[key.first].nnz[key.second];
+        edge_bound += (uint64_t)ents[kv.first.second].nnz[0];
     }
     for (int st = 0; st < nstates; ++st) {
         auto it = in_trans.find(st);
@@ -574,7 +707,7 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
         if (finals[i] >= 0 && finals[i] < nstates) fset.insert(finals[i]);
     q->edge_bound = edge_bound;
     q->ngroups = (int)gslot.size();
-    q->nslots = (int)slot_keys.size();
+    q->nslots = (int)ents.size();
     q->ntargets = (int)targets.size();
     q->nstarts = (int)sset.size();
     q->nfinals = (int)fset.size();
@@ -590,13 +723,9 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     T.insert(T.end(), ibeg.begin(), ibeg.end());
     T.insert(T.end(), isrc.begin(), isrc.end());
     T.insert(T.end(), islot.begin(), islot.end());
-    for (int pass = 0; pass < 2; ++pass)
-        for (auto& k : slot_keys) {
-            const LabelDev& L = g->labels[k.first];
-            const int d = pass == 0 ? k.second : 1 - k.second;  // pass 1: the transpose
-            q->slots.push_back(Slot{L.rowptr[d], L.col[d]});
-        }
-    for (auto& k : slot_keys) q->slot_nnz.push_back((unsigned long long)g->labels[k.first].nnz[k.second]);
+    for (int pass = 0; pass < 2; ++pass)  // pass 1: the transposes
+        for (auto& en : ents) q->slots.push_back(Slot{en.rowptr[pass], en.col[pass]});
+    for (auto& en : ents) q->slot_nnz.push_back((unsigned long long)en.nnz[0]);
 
     // queue capacities: every (state, vertex) pair is discovered at most once,
     // so one level holds at most |V| segments per group (+ splits of huge
