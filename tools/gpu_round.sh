@@ -5,13 +5,16 @@
 tag=${1:-r01}
 out=gpurun_out
 mkdir -p $out
-timeout 900 python -m pytest tests -q -m gpu > $out/gpu_tests_$tag.log 2>&1; echo "tests_rc=$?"; tail -3 $out/gpu_tests_$tag.log
+timeout -s KILL 900 python -m pytest tests -q -m gpu > $out/gpu_tests_$tag.log 2>&1; echo "tests_rc=$?"; tail -3 $out/gpu_tests_$tag.log
 timeout 300 python __graft_entry__.py --smoke > $out/smoke_$tag.log 2>&1; echo "smoke_rc=$?"
 timeout 600 python bench.py > $out/bench_$tag.json 2> $out/bench_$tag.err; echo "bench_rc=$?"
 timeout 600 python bench.py --impl reference > $out/bench_ref_$tag.json 2> $out/bench_ref_$tag.err; echo "ref_rc=$?"
 timeout 900 python bench.py --config cfg3 --steps 5 --warmup 3 --no-cpu-baseline > $out/bench_cfg3_$tag.json 2> $out/bench_cfg3_$tag.err; echo "cfg3_rc=$?"
 timeout 1500 python tools/config_sweep.py cfg1 cfg2 cfg3 cfg5 cfg4 --sources 8 --reps 3 > $out/sweep_$tag.jsonl 2> $out/sweep_$tag.err; echo "sweep_rc=$?"
 timeout 900 python tools/batch_probe.py cfg5 --single 64 > $out/batch_cfg5_$tag.json 2> $out/batch_cfg5_$tag.err; echo "batch_rc=$?"
+for qi in 0 1 2 3; do
+  timeout 900 python tools/batch_probe.py cfg4 --sources 32 --single 32 --query $qi 2>/dev/null | tail -1 >> $out/batch_cfg4_$tag.jsonl
+done; echo "batch4_rc=$?"
 timeout 900 python -m torch.distributed.run --nnodes 1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29561 \
     tools/partition_bench.py > $out/partition_r1_$tag.json 2> $out/partition_r1_$tag.err; echo "part_rc=$?"
 timeout 900 python tools/partition_bench.py --local-shards 4 > $out/partition_l4_$tag.json 2> $out/partition_l4_$tag.err; echo "part4_rc=$?"

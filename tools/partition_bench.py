@@ -80,6 +80,7 @@ def main():
     args_run = (shards, ex, ranges, g.num_vertices, table.starts.tolist(), table.finals.tolist(), source)
     reach0, its0, prof = partition.run_levels(*args_run, profile=True)  # warm-up + per-level step times
     bits0 = None
+    partition.run_levels(*args_run, bits=True)  # second warm-up (first runs allocate and touch memory)
     walls = []
     for _ in range(args.reps):
         if distributed:
