@@ -31,15 +31,50 @@ __global__ void label_histogram_kernel(const int32_t* __restrict__ lab, long lon
             if (s_hist[i]) atomicAdd(&hist[i], (unsigned long long)s_hist[i]);
 }
 
-// scatter edges into their label's segment as packed (src << 32 | dst) keys
+// scatter edges into their label's segment as packed (src << 32 | dst) keys.
+// Labels with a shared-memory histogram (nl <= 8192): a block takes a chunk of
+// edges, counts it per label in shared memory, reserves one range per label
+// with a single global atomic, then places its edges with shared-memory
+// cursors (no global atomic per edge: a few hot Zipf labels would serialize).
+constexpr int kScatterChunk = 4096;
 __global__ void label_scatter_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                                      const int32_t* __restrict__ lab, long long n, int nl,
                                      unsigned long long* __restrict__ cursor, unsigned long long* __restrict__ out) {
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const int l = lab[i];
-        if (l < 0 || l >= nl) continue;
-        const unsigned long long pos = atomicAdd(&cursor[l], 1ull);
-        out[pos] = ((unsigned long long)(uint32_t)src[i] << 32) | (uint32_t)dst[i];
+    extern __shared__ unsigned int s_cnt[];  // [nl] counts, then reused as cursors
+    const bool local = nl <= 8192;
+    if (!local) {  // many labels: one global atomic per edge
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+             i += (long long)gridDim.x * blockDim.x) {
+            const int l = lab[i];
+            if (l < 0 || l >= nl) continue;
+            const unsigned long long pos = atomicAdd(&cursor[l], 1ull);
+            out[pos] = ((unsigned long long)(uint32_t)src[i] << 32) | (uint32_t)dst[i];
+        }
+        return;
+    }
+    unsigned long long* s_base = reinterpret_cast<unsigned long long*>(s_cnt + ((nl + 1) & ~1));
+    for (long long c0 = (long long)blockIdx.x * kScatterChunk; c0 < n; c0 += (long long)gridDim.x * kScatterChunk) {
+        const long long c1 = min(n, c0 + (long long)kScatterChunk);
+        for (int i = threadIdx.x; i < nl; i += blockDim.x) s_cnt[i] = 0;
+        __syncthreads();
+        for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+            const int l = lab[i];
+            if (l >= 0 && l < nl) atomicAdd(&s_cnt[l], 1u);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+            const unsigned c = s_cnt[i];
+            s_base[i] = c ? atomicAdd(&cursor[i], (unsigned long long)c) : 0ull;
+            s_cnt[i] = 0;
+        }
+        __syncthreads();
+        for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+            const int l = lab[i];
+            if (l < 0 || l >= nl) continue;
+            const unsigned long long pos = s_base[l] + atomicAdd(&s_cnt[l], 1u);
+            out[pos] = ((unsigned long long)(uint32_t)src[i] << 32) | (uint32_t)dst[i];
+        }
+        __syncthreads();
     }
 }
 

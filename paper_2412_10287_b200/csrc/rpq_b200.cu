@@ -515,7 +515,11 @@ int rpq_graph_create_coo(int32_t num_vertices, int32_t num_labels, int64_t nnz, 
     for (int l = 0; l < nl; ++l) g->coo_off[l + 1] = g->coo_off[l] + h[l];
     if (nl > 0) GTRY(cudaMemcpy(cursor, g->coo_off.data(), (size_t)nl * 8, cudaMemcpyHostToDevice));
     if (nnz > 0 && nl > 0) {
-        label_scatter_kernel<<<1184, 256>>>(d_src, d_dst, d_lab, nnz, nl, cursor, g->d_coo);
+        // shared memory: nl counters (padded to even) + nl 64-bit range bases
+        const size_t sm = nl <= 8192 ? (size_t)((nl + 1) & ~1) * 4 + (size_t)nl * 8 : 0;
+        if (sm > 48 * 1024)
+            GTRY(cudaFuncSetAttribute(label_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        label_scatter_kernel<<<1184, 256, sm>>>(d_src, d_dst, d_lab, nnz, nl, cursor, g->d_coo);
         GTRY(cudaGetLastError());
     }
     GTRY(cudaDeviceSynchronize());
