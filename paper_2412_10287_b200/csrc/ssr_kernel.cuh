@@ -956,27 +956,79 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
     }
     grid_barrier(ctl, ++e, s_run.bar_base);
 
-    // ---- epoch 1: seed P = M = {(q_s, source)} (engine.py:106-109, :154-155)
+    // ---- epoch 1: seed P = M = {(q_s, source)} (engine.py:106-109, :154-155).
+    // P was just cleared, so every start state is fresh: every CTA knows the
+    // seed rows (the source's rows of each start state's groups) and writes a
+    // share of their bundles -- a hub source's row (millions of edges) is not
+    // emitted by one warp.  All seed bundles are inline (each lies in one row).
     if (!step_mode) {
         const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, 32u};
         if (cta0) reset_qc(&ctl->qc[(e + 2) % 3], threadIdx.x);
         unsigned long long nnew = 0, nedge = 0;
-        if (cta0 && wid == 0) {
-            for (int i0 = 0; i0 < p.nstarts; i0 += 32) {
-                const int i = i0 + lane;
-                bool fresh = false;
-                int q = 0;
-                if (i < p.nstarts) {
-                    q = S.starts[i];
-                    const long long off = (long long)q * p.W + (S.run->source >> 5);
-                    const uint32_t bit = 1u << (S.run->source & 31);
-                    fresh = !(atomicOr(p.visited + off, bit) & bit);
-                    if (fresh) atomicOr(p.fb[0] + off, bit);
+        const int src = S.run->source;
+        if (cta0 && wid == 0) {  // claim the seed pairs
+            for (int i = lane; i < p.nstarts; i += 32) {
+                const int q = S.starts[i];
+                const long long off = (long long)q * p.W + (src >> 5);
+                const uint32_t bit = 1u << (src & 31);
+                atomicOr(p.visited + off, bit);
+                atomicOr(p.fb[0] + off, bit);
+                atomicAdd(&s_state[q], 1u);
+                nnew += 1;
+            }
+        }
+        // the seed rows: one per (start state, group), in shared memory
+        __shared__ uint32_t s_slo[kMaxGroups], s_sgrp[kMaxGroups];
+        __shared__ unsigned long long s_sdeg[kMaxGroups + 1], s_sbun[kMaxGroups + 1];
+        __shared__ int s_nrows;
+        __shared__ uint32_t s_sbsz;
+        if (threadIdx.x == 0) {
+            int n = 0;
+            unsigned long long edges = 0, bundles = 0;
+            s_sdeg[0] = s_sbun[0] = 0;
+            for (int i = 0; i < p.nstarts; ++i) {
+                const int q = S.starts[i];
+                for (int g = S.gbeg[q]; g < S.gbeg[q + 1] && n < kMaxGroups; ++g) {
+                    const Slot sl = S.slots[S.gslot[g]];
+                    const uint32_t lo = sl.rowptr[src], hi = sl.rowptr[src + 1];
+                    s_slo[n] = lo;
+                    s_sgrp[n] = (uint32_t)g;
+                    edges += hi - lo;
+                    s_sdeg[n + 1] = edges;
+                    ++n;
                 }
-                nnew += fresh ? 1 : 0;
-                if (fresh) atomicAdd(&s_state[q], 1u);
-                const uint32_t T = emit_pairs(p, S, o, fresh, q, S.run->source, lane);
-                if (lane == 0) nedge += T;
+            }
+            // small seed rows: 32-edge bundles spread the first level over more warps
+            const uint32_t bsz = edges < (unsigned long long)nwarps * 32 ? 32u : (uint32_t)kBundle;
+            for (int r = 0; r < n; ++r) {
+                bundles += (s_sdeg[r + 1] - s_sdeg[r] + bsz - 1) / bsz;
+                s_sbun[r + 1] = bundles;
+            }
+            s_nrows = n;
+            s_sbsz = bsz;
+            if (cta0) nedge = edges;
+        }
+        __syncthreads();
+        {
+            const int nrows = s_nrows;
+            const uint32_t bsz = s_sbsz;
+            const unsigned long long nb = s_sbun[nrows];
+            // bundle b goes to shard b % G at index b / G (this CTA writes its shard)
+            const unsigned long long mine = nb > blockIdx.x ? (nb - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+            if (mine > p.shard_buncap) {
+                if (threadIdx.x == 0) atomicExch(&o.qc->overflow, 1u);
+            } else {
+                for (unsigned long long k = threadIdx.x; k < mine; k += blockDim.x) {
+                    const unsigned long long b = blockIdx.x + k * gridDim.x;
+                    int r = 0;
+                    while (r + 1 < nrows && s_sbun[r + 1] <= b) ++r;  // few rows: linear
+                    const unsigned long long pos = (b - s_sbun[r]) * bsz;
+                    const unsigned long long deg = s_sdeg[r + 1] - s_sdeg[r];
+                    const uint32_t cnt = (uint32_t)min((unsigned long long)bsz, deg - pos);
+                    o.bun[(unsigned long long)blockIdx.x * p.shard_buncap + k] =
+                        make_uint2(s_slo[r] + (uint32_t)pos, kInline | (s_sgrp[r] << 7) | (cnt - 1));
+                }
+                if (threadIdx.x == 0) s_resv = ((cta0 ? (unsigned long long)nrows : 0ull) << 32) | mine;
             }
         }
         __syncthreads();
