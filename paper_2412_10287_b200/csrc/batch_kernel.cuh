@@ -564,7 +564,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
                 cnt += __popc(mine[0]) + __popc(mine[1]) + __popc(mine[2]) + __popc(mine[3]);
             }
         }
-        if (lane < s_run.nsrc && cnt) atomicAdd(&ctl->reach_count[lane], cnt);
+        // per source: shared-memory sums, then one global atomic per CTA
+        if (threadIdx.x < kBatch) s_red[threadIdx.x] = 0ull;
+        __syncthreads();
+        if (lane < s_run.nsrc && cnt) atomicAdd(&s_red[lane], cnt);
+        __syncthreads();
+        if (threadIdx.x < s_run.nsrc && s_red[threadIdx.x])
+            atomicAdd(&ctl->reach_count[threadIdx.x], s_red[threadIdx.x]);
     }
     if (cta0 && threadIdx.x == 0) ctl->status = status;
 }

@@ -1442,10 +1442,20 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                 }
             }
         }
+        // one atomic per CTA, not per warp (thousands on one address serialize)
         cnt = warp_sum_u64(cnt);
         te = warp_sum_u64(te);
-        if (lane == 0 && cnt) atomicAdd(&ctl->reach_count, cnt);
-        if (lane == 0 && te) atomicAdd(&ctl->te_exact, te);
+        if (lane == 0) {
+            s_red[2 * wid] = cnt;
+            s_red[2 * wid + 1] = te;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            cnt = warp_sum_u64(lane < kWarps ? s_red[2 * lane] : 0ull);
+            te = warp_sum_u64(lane < kWarps ? s_red[2 * lane + 1] : 0ull);
+            if (lane == 0 && cnt) atomicAdd(&ctl->reach_count, cnt);
+            if (lane == 0 && te) atomicAdd(&ctl->te_exact, te);
+        }
     }
 }
 
