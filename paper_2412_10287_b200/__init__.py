@@ -25,6 +25,7 @@ from .engine import (
     step_update,
 )
 from .graph import CsrMatrix, DeviceGraph, LabeledGraph, device_graph
+from .plan import eval_plan
 
 __all__ = [
     "ALGORITHMS",
@@ -39,6 +40,7 @@ __all__ = [
     "QueryTimeout",
     "TransitionTable",
     "device_graph",
+    "eval_plan",
     "eval_sdr",
     "eval_ssr",
     "eval_ssr_batch",

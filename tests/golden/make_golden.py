@@ -7,6 +7,7 @@ paper_2412_10287_b200/data/, and the tests read only those files.
     python tests/golden/make_golden.py random      # reference test-suite instances
     python tests/golden/make_golden.py automata    # compiled config queries
     python tests/golden/make_golden.py config cfg1 cfg2 [cfg3 cfg5 ...]
+    python tests/golden/make_golden.py plan        # eval_plan (engine.py:292-390) on the same streams
 
 Instance sources (each replays the reference test's own RNG stream):
   engine_random_15   test_engine.py:403-415 (seed 15, 40 instances, unknown label "zz")
@@ -39,6 +40,7 @@ sys.path.insert(0, ROOT)
 import helpers  # noqa: E402  (reference test helpers)
 from rpq.engine import (  # noqa: E402
     EngineOptions,
+    eval_plan,
     step_update,
     eval_sdr,
     eval_ssr,
@@ -151,6 +153,54 @@ def gen_random():
         }
         out.append(d)
     out.extend(known_answers())
+    return out
+
+
+def ast_json(node):
+    kind = type(node).__name__
+    if kind == "Label":
+        return {"k": "label", "name": node.name, "inv": bool(node.inverted)}
+    if kind in ("Concat", "Alt"):
+        return {"k": kind.lower(), "c": [ast_json(c) for c in node.children]}
+    return {"k": kind.lower(), "c": ast_json(node.child)}
+
+
+def plan_record(g, ast, vertex, tag):
+    opts = EngineOptions(timeout=math.inf)
+    src = eval_plan(g, ast, ("source", vertex), opts)
+    dst = eval_plan(g, ast, ("destination", vertex), opts)
+    return {"tag": tag, "graph": graph_json(g), "ast": ast_json(ast), "vertex": vertex,
+            "source": {"reach": sorted(src.reachable), "iterations": src.iterations},
+            "destination": {"reach": sorted(dst.reachable), "iterations": dst.iterations}}
+
+
+def gen_plan():
+    """eval_plan on the RNG streams of test_engine.py:403-415 (seed 15) and
+    test_acceptance.py:60-84 (seed 0xC1, first 200), replayed call for call,
+    plus the plan-specific cases of test_engine.py:122-153."""
+    out = []
+    rng = random.Random(15)
+    for i in range(40):
+        g = helpers.random_graph(rng, max_vertices=30, max_edges=150)
+        ast = helpers.random_ast(rng, unknown_label="zz")
+        ref_compile(ast, g.label_ids)
+        source = rng.randrange(g.num_vertices)
+        out.append(plan_record(g, ast, source, f"engine_random_15/{i}"))
+    rng = random.Random(0xC1)
+    for i in range(200):
+        g = helpers.random_graph(rng, max_vertices=50, max_labels=4, max_edges=300)
+        ast = helpers.random_ast(rng, labels="abcd", max_depth=4, unknown_label="zz")
+        source = rng.randrange(g.num_vertices)
+        out.append(plan_record(g, ast, source, f"acceptance_c1/{i}"))
+    for tag, text, q, v in [
+        ("chain a b c", "0\ta\t1\n1\tb\t2\n2\tc\t3\n", "a b c", "0"),      # test_engine.py:126-131
+        ("chain a b c back", "0\ta\t1\n1\tb\t2\n2\tc\t3\n", "a b c", "3"),
+        ("star identity", "0\tb\t1\n", "a*", "1"),                                 # :134-137
+        ("nested star", "0\ta\t1\n1\tb\t1\n1\ta\t2\n2\tc\t3\n", "(a b*)* c", "0"),  # :140-146
+        ("a* no edges", "0\tb\t1\n", "a*", "0"),                                   # test_engine.py:91
+    ]:
+        g = helpers.load_text(text)
+        out.append(plan_record(g, parse_query(q), g.vertex_index(v), f"known/{tag}"))
     return out
 
 
@@ -296,6 +346,12 @@ def main():
         with gzip.open(path, "wt") as fh:
             json.dump(inst, fh)
         print(f"wrote {len(inst)} instances to {path}")
+    elif what == "plan":
+        out = gen_plan()
+        path = os.path.join(HERE, "plan.json.gz")
+        with gzip.open(path, "wt") as fh:
+            json.dump(out, fh)
+        print(f"wrote {len(out)} plan cases to {path}")
     elif what == "steps":
         out = gen_steps()
         path = os.path.join(HERE, "step_update.json.gz")

@@ -179,3 +179,21 @@ def test_step_update_validates_shapes():
         P.step_update(CsrMatrix.from_pairs(1, 2, []), CsrMatrix.from_pairs(2, 1, []), g, n, P.EngineOptions())
     with pytest.raises(ValueError):
         P.step_update(CsrMatrix.from_pairs(2, 3, []), CsrMatrix.from_pairs(2, 3, []), g, n, P.EngineOptions())
+
+
+def test_plan_ast_helpers():
+    from paper_2412_10287_b200 import plan
+
+    ast = plan.Concat((plan.Label("a"), plan.Star(plan.Label("b", True)), plan.Opt(plan.Label("c"))))
+    r = plan.reverse_ast(ast)  # query_compiler.py:77-90
+    assert r == plan.Concat((plan.Opt(plan.Label("c", True)), plan.Star(plan.Label("b", False)),
+                             plan.Label("a", True)))
+    assert plan.reverse_ast(r) == ast
+    d = {"k": "alt", "c": [{"k": "label", "name": "a", "inv": False},
+                           {"k": "plus", "c": {"k": "label", "name": "zz", "inv": True}}]}
+    assert plan.ast_from_json(d) == plan.Alt((plan.Label("a"), plan.Plus(plan.Label("zz", True))))
+    g = P.LabeledGraph.from_edges(3, ["a"], [(0, 0, 1)])
+    with pytest.raises(ValueError):
+        plan.eval_plan(g, plan.Label("a"), ("middle", 0), P.EngineOptions())
+    with pytest.raises(IndexError):
+        plan.eval_plan(g, plan.Label("a"), ("source", 3), P.EngineOptions())
