@@ -1155,16 +1155,28 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
             // queue, so heavy rows spread over SMs); its warps take them one at a
             // time from a shared counter, so fast warps do more of them
             (void)step;
-            for (;;) {
-                unsigned long long bi = 0;
-                if (lane == 0) bi = (unsigned long long)atomicAdd(&s_task, 1u) * gridDim.x + blockIdx.x;
-                bi = __shfl_sync(FULL, bi, 0);
-                if (bi >= nb) break;
-                int sh = 0;
+            // software pipeline: the next bundle's descriptor is in flight while
+            // this one is expanded (one dependent round trip less per bundle)
+            auto grab = [&](uint2* d) -> unsigned long long {
+                unsigned long long b = 0;
+                if (lane == 0) b = (unsigned long long)atomicAdd(&s_task, 1u) * gridDim.x + blockIdx.x;
+                b = __shfl_sync(FULL, b, 0);
+                if (b < nb) {
+                    int sh = 0;
 #pragma unroll
-                for (int h = 128; h >= 1; h >>= 1)
-                    if (sh + h <= kShards && s_bpre[sh + h] <= bi) sh += h;
-                const uint2 bd = ld_queue(bun + (unsigned long long)sh * p.shard_buncap + (bi - s_bpre[sh]), S.pf);
+                    for (int h = 128; h >= 1; h >>= 1)
+                        if (sh + h <= kShards && s_bpre[sh + h] <= b) sh += h;
+                    *d = ld_queue(bun + (unsigned long long)sh * p.shard_buncap + (b - s_bpre[sh]), S.pf);
+                }
+                return b;
+            };
+            uint2 bd_next = make_uint2(0u, kHoleY);
+            unsigned long long bi_next = grab(&bd_next);
+            for (;;) {
+                const unsigned long long bi = bi_next;
+                if (bi >= nb) break;
+                const uint2 bd = bd_next;
+                bi_next = grab(&bd_next);
                 if (bd.y == kHoleY) continue;
                 const uint32_t cnt = (bd.y & 127u) + 1;
                 int w[kEdgesPerLane], gj[kEdgesPerLane];
