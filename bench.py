@@ -69,6 +69,7 @@ def parse_args():
     ap.add_argument("--emit-mode", type=int, default=None, help="tuning: 0 inline, 1 plan, 2 adaptive")
     ap.add_argument("--emit-inline-max", type=int, default=None)
     ap.add_argument("--flags", type=int, default=None, help="tuning: push variants (RPQ_TUNE_FLAGS)")
+    ap.add_argument("--defer", type=float, default=None, help="tuning: RPQ_TUNE_DEFER factor")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between steps (diagnostic)")
     ap.add_argument("--profile", action="store_true",
@@ -299,6 +300,8 @@ def run_engine(args, rank, world, local_rank):
     pq.set_tuning(args.emit_mode, args.emit_inline_max)
     if args.flags is not None:
         P.engine.raise_for_status(P._lib.engine().rpq_query_set_tuning(pq.q, 3, float(args.flags)), "flags")
+    if args.defer is not None:
+        P.engine.raise_for_status(P._lib.engine().rpq_query_set_tuning(pq.q, 5, float(args.defer)), "defer")
     # one untimed run for the work counts (exact TE, |P|, levels) of this query
     pq.set_options(direction=args.direction, count_te=True)
     pq.launch(source, -1.0, handle)

@@ -169,6 +169,9 @@ RPQ_API int rpq_query_set_options(rpq_query* q, int32_t direction, int32_t count
                              bit 1 prefetch candidate targets' row pointers into L2 */
 #define RPQ_TUNE_SMALL 4  /* 1 (default): state spaces of <= 12,288 x 32 pairs run on one CTA
                              with shared-memory bitmaps; 0: always the grid kernel */
+#define RPQ_TUNE_DEFER 5  /* push level L does not emit F_{L+1}'s queue at discovery when
+                             m_f(F_L) x (densest slot's mean degree) x value > m_u (0: always emit;
+                             default 2) */
 #define RPQ_TUNE_TRACE 2  /* diagnostics: record per-CTA phase stamps of the first `value` levels */
 RPQ_API int rpq_query_set_tuning(rpq_query* q, int32_t key, double value);
 /* Enqueue one evaluation from `source` on `stream` (a cudaStream_t, or NULL for

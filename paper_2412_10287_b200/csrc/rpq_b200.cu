@@ -114,6 +114,7 @@ struct rpq_query {
     int emit_mode = 0;
     unsigned int emit_inline_max = 1u << 16;
     unsigned int run_flags = RF_NO_PROBE;
+    float defer_alpha = 2.0f;
     long long own_w0 = 0, own_w1 = 0;  // owned word range (partitioned step); empty = all
     bool small_ok = false;    // |Q| x |V| fits the single-CTA kernel
     int allow_small = 1;      // RPQ_TUNE_SMALL
@@ -933,6 +934,10 @@ int rpq_query_set_tuning(rpq_query* q, int32_t key, double value) {
             if (value < 0 || value > 4.0e9) return fail(RPQ_EINVAL, "bad inline threshold");
             q->emit_inline_max = (unsigned int)value;
             return RPQ_OK;
+        case RPQ_TUNE_DEFER:
+            if (!(value >= 0) || value > 1e6) return fail(RPQ_EINVAL, "defer factor must be >= 0");
+            q->defer_alpha = (float)value;
+            return RPQ_OK;
         case RPQ_TUNE_SMALL:
             if (value != 0 && value != 1) return fail(RPQ_EINVAL, "small-kernel switch must be 0 or 1");
             q->allow_small = (int)value;
@@ -985,6 +990,7 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     ra.bar_base = q->bar_next;
     ra.emit_mode = q->emit_mode;
     ra.emit_inline_max = q->emit_inline_max;
+    ra.defer_alpha = q->defer_alpha;
     ra.flags = q->run_flags;
     ra.source = source;
     ra.dir_mode = q->dir_mode;
@@ -1184,6 +1190,7 @@ int rpq_query_step_device(rpq_query* q, const uint32_t* d_m, uint32_t* d_p, uint
     ra.budget_ns = ~0ull;
     ra.bar_base = q->bar_next;
     ra.flags = q->run_flags;
+    ra.defer_alpha = q->defer_alpha;
     ra.own_w0 = q->own_w0;
     ra.own_w1 = q->own_w1;
     *reinterpret_cast<RunArgs*>(q->h_in) = ra;

@@ -116,6 +116,8 @@ struct RunArgs {
     unsigned int emit_inline_max;  // mode 2: inline while |F_L| < this
     unsigned int flags;            // RF_* push-path variants (tuning)
     long long own_w0, own_w1;      // step mode: owned word range of a partitioned rank (empty: all)
+    float defer_alpha;             // emit at discovery unless mf_L * dmax * this > m_u (0: always emit)
+    float pad3;
 };
 
 constexpr unsigned RF_NO_PROBE = 1u;     // claim with atomicOr without reading P first
@@ -281,6 +283,7 @@ struct View {
     int done;
     int dir;        // direction of the level about to run
     int plan;       // push level whose queue must first be emitted from F_L
+    int defer;      // push level: do not emit F_{L+1}'s queue at discovery (the next level is likely pull)
     int status;
     int iterations;
     unsigned long long nfront;  // |F_L|
@@ -676,6 +679,7 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
     // F_L's queue was emitted at discovery (exact m_f and bundles available)
     const int produced_by_push = prev_queued;
     int done = 0, iterations = 0, status = 0, next = DIR_PUSH, plan = 0;
+    bool defer = false;
     long long ledges = -1;
     if (abort) {
         status = ST_DEADLOCK;
@@ -723,6 +727,15 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
                 mf += __shfl_xor_sync(FULL, mf, d);
             }
             if (produced_by_push) mf = (float)nedge;
+            // a push level whose successor frontier could already warrant pull
+            // (its edges bounded by mf_L x the densest slot's mean degree) does
+            // not emit that frontier's queue at discovery: a pull level needs
+            // none, and a push level re-emits it from the bitmap (plan epoch)
+            if (S.run->defer_alpha > 0.0f) {
+                float dmax = 0.0f;
+                for (int sl = 0; sl < p.nslots; ++sl) dmax = fmaxf(dmax, S.nnz[sl] * inv_nv);
+                defer = mf * dmax * S.run->defer_alpha > mu;
+            }
             if (produced_by_push) {
                 next = (mf * S.run->alpha > mu) ? DIR_PULL : DIR_PUSH;
             } else {
@@ -754,6 +767,7 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
         v->status = status;
         v->iterations = iterations;
         v->nfront = nnew;
+        v->defer = next == DIR_PUSH && defer;
         if (blockIdx.x == 0) {  // results and statistics
             const unsigned long long now = globaltimer();
             atomicAdd(&ctl->pairs, nnew);  // fire-and-forget: no round trip on CTA 0's path
@@ -1067,6 +1081,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
             s_view.done = nf == 0;
             s_view.dir = dir;
             s_view.plan = dir == DIR_PUSH;
+            s_view.defer = 0;
             s_view.status = 0;
             s_view.iterations = 0;
             s_view.nfront = nf;
@@ -1094,15 +1109,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                 if (!s_front[q] || S.gbeg[q + 1] == S.gbeg[q]) continue;
                 const uint32_t* row = fcur + (long long)q * p.W;
                 for (long long w0 = gwarp * 32; w0 < Wn; w0 += nwarps * 32) {
+                    // a word per lane; their set bits dealt 32 per round to the
+                    // lanes (prefix over popcounts), so every stage_add is full
                     const long long wi = w0 + lane;
                     const uint32_t bits = wi < Wn ? row[wi] : 0u;
-                    unsigned any = __ballot_sync(FULL, bits != 0);
-                    while (any) {
-                        const int src_lane = __ffs(any) - 1;
-                        any &= any - 1;
-                        const uint32_t wb = __shfl_sync(FULL, bits, src_lane);
-                        const bool valid = (wb >> lane) & 1u;
-                        const int v = (int)((w0 + src_lane) * 32 + lane);
+                    const uint32_t cnt = __popc(bits);
+                    const uint32_t incl = warp_incl_scan(cnt, lane);
+                    const uint32_t excl = incl - cnt;
+                    const uint32_t total = __shfl_sync(FULL, incl, 31);
+                    for (uint32_t r0 = 0; r0 < total; r0 += 32) {
+                        const uint32_t x = r0 + lane;
+                        const bool valid = x < total;
+                        const int j = warp_upper_lane(excl, valid ? x : 0u);
+                        const uint32_t wb = __shfl_sync(FULL, bits, j);
+                        const uint32_t eb = __shfl_sync(FULL, excl, j);
+                        const int v = valid ? (int)((w0 + j) * 32 + __fns(wb, 0, (int)(x - eb) + 1)) : 0;
                         const uint32_t T = stage_add(p, S, o, stage, valid, q, v, lane);
                         if (lane == 0) nedge += T;
                     }
@@ -1140,7 +1161,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
         __syncthreads();  // s_task
         unsigned long long nnew = 0, nedge = 0;
         // emit F_{L+1}'s queue now (at discovery) or later from F's bitmap
-        const bool emit_inline = dir == DIR_PUSH &&
+        const bool emit_inline = dir == DIR_PUSH && !s_view.defer &&
                                  (s_run.emit_mode == 0 ||
                                   (s_run.emit_mode == 2 && s_view.nfront < s_run.emit_inline_max));
         const int queued = emit_inline ? 1 : 0;
