@@ -284,6 +284,7 @@ struct View {
     int dir;        // direction of the level about to run
     int plan;       // push level whose queue must first be emitted from F_L
     int defer;      // push level: do not emit F_{L+1}'s queue at discovery (the next level is likely pull)
+    float mf;       // m_f of the last decided frontier (growth estimate)
     int status;
     int iterations;
     unsigned long long nfront;  // |F_L|
@@ -727,15 +728,19 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
                 mf += __shfl_xor_sync(FULL, mf, d);
             }
             if (produced_by_push) mf = (float)nedge;
-            // a push level whose successor frontier could already warrant pull
-            // (its edges bounded by mf_L x the densest slot's mean degree) does
-            // not emit that frontier's queue at discovery: a pull level needs
-            // none, and a push level re-emits it from the bitmap (plan epoch)
+            // a push level whose successor frontier will likely warrant pull
+            // does not emit that frontier's queue at discovery: a pull level
+            // needs none (a push level re-emits it from the bitmap instead).
+            // Predicted m_f(F_{L+1}) = m_f(F_L) x min(last growth, densest
+            // slot's mean degree), tested like the real decision will be.
             if (S.run->defer_alpha > 0.0f) {
                 float dmax = 0.0f;
                 for (int sl = 0; sl < p.nslots; ++sl) dmax = fmaxf(dmax, S.nnz[sl] * inv_nv);
-                defer = mf * dmax * S.run->defer_alpha > mu;
+                const float growth = mf / fmaxf(v->mf, 1.0f);
+                defer = L > 0 && mf * fminf(growth, dmax) * S.run->defer_alpha > mu;
             }
+            __syncwarp();  // every lane has read the previous m_f
+            if (lane == 0) v->mf = mf;
             if (produced_by_push) {
                 next = (mf * S.run->alpha > mu) ? DIR_PULL : DIR_PUSH;
             } else {
@@ -912,7 +917,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
         s_sv[i] = 0;
         s_front[i] = 0;
     }
-    if (threadIdx.x == 0) s_run = *p.run;
+    if (threadIdx.x == 0) {
+        s_run = *p.run;
+        s_view.mf = 0.0f;
+        s_view.defer = 0;
+    }
     Smem S;
     S.pf = policy_evict_first();
     S.pl = policy_evict_last();
