@@ -878,6 +878,116 @@ __device__ unsigned long long frontier_edges(const Params& p, const Smem& S, con
     return te;
 }
 
+// Pull tasks of one level: every (target state, PV words of vertices) with an
+// active source state.  PV words per lane-task: more vertices in flight per
+// warp on large graphs, more tasks (balance) on small ones.
+template <int PV>
+__device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const uint32_t* fcur, uint32_t* fnext,
+                                           long long pw0, long long pw1, int lane, unsigned* s_task,
+                                           int s_nptarget, const int* s_ptarget, const unsigned int* s_front,
+                                           unsigned int* s_state, unsigned long long& nnew) {
+    const long long nblk = (pw1 - pw0 + PV - 1) / PV;
+    const long long ntask = (long long)s_nptarget * nblk;
+    for (;;) {
+        long long task = 0;
+        if (lane == 0) task = (long long)atomicAdd(s_task, 1u) * gridDim.x + blockIdx.x;
+        task = __shfl_sync(FULL, task, 0);
+        if (task >= ntask) break;
+        const int q2 = s_ptarget[task / nblk];
+        const long long word0 = pw0 + (task % nblk) * PV;
+        uint32_t vis[PV];
+        bool need[PV], found[PV];
+        int w[PV];
+#pragma unroll
+        for (int u = 0; u < PV; ++u)
+            vis[u] = word0 + u < pw1 ? ld_bits(p.visited + (long long)q2 * p.W + word0 + u, S.pl) : 0xFFFFFFFFu;
+        bool any_need = false;
+#pragma unroll
+        for (int u = 0; u < PV; ++u) {
+            w[u] = (int)((word0 + u) * 32 + lane);
+            need[u] = w[u] < p.nv && !((vis[u] >> lane) & 1u);
+            found[u] = false;
+            any_need |= need[u];
+        }
+        if (__ballot_sync(FULL, any_need) == 0) continue;
+        for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k) {
+            const int q = S.isrc[k];
+            if (!s_front[q]) continue;
+            bool look[PV], any_look = false;
+#pragma unroll
+            for (int u = 0; u < PV; ++u) {
+                look[u] = need[u] && !found[u];
+                any_look |= look[u];
+            }
+            if (__ballot_sync(FULL, any_look) == 0) break;
+            const Slot ps = S.slots[p.nslots + S.islot[k]];
+            const uint32_t* frow = fcur + (long long)q * p.W;
+            uint32_t lo[PV], hi[PV];
+#pragma unroll
+            for (int u = 0; u < PV; ++u) {
+                lo[u] = look[u] ? ld_stream_u32(ps.rowptr + w[u], S.pf) : 0u;
+                hi[u] = look[u] ? ld_stream_u32(ps.rowptr + w[u] + 1, S.pf) : 0u;
+            }
+            // the first kPullInline in-edges of every vertex: all loads in flight together
+            int cand[PV][kPullInline];
+#pragma unroll
+            for (int u = 0; u < PV; ++u)
+#pragma unroll
+                for (int i = 0; i < kPullInline; ++i)
+                    cand[u][i] = (lo[u] + i < hi[u]) ? ld_stream_i32(ps.col + lo[u] + i, S.pf) : -1;
+            uint32_t fw[PV][kPullInline];
+#pragma unroll
+            for (int u = 0; u < PV; ++u)
+#pragma unroll
+                for (int i = 0; i < kPullInline; ++i)
+                    fw[u][i] = cand[u][i] >= 0 ? ld_bits(frow + (cand[u][i] >> 5), S.pl) : 0u;
+#pragma unroll
+            for (int u = 0; u < PV; ++u)
+#pragma unroll
+                for (int i = 0; i < kPullInline; ++i)
+                    if (cand[u][i] >= 0 && ((fw[u][i] >> (cand[u][i] & 31)) & 1u)) found[u] = true;
+            // longer rows: the whole warp scans one row at a time, early exit
+#pragma unroll
+            for (int u = 0; u < PV; ++u) {
+                unsigned longrows = __ballot_sync(FULL, look[u] && !found[u] && hi[u] - lo[u] > kPullInline);
+                while (longrows) {
+                    const int ln = __ffs(longrows) - 1;
+                    longrows &= longrows - 1;
+                    const uint32_t rlo = __shfl_sync(FULL, lo[u], ln) + kPullInline;
+                    const uint32_t rhi = __shfl_sync(FULL, hi[u], ln);
+                    bool hit = false;
+                    for (uint32_t ed = rlo; ed < rhi; ed += 128) {
+                        int uu[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            uu[c] = ed + 32 * c + lane < rhi ? ld_stream_i32(ps.col + ed + 32 * c + lane, S.pf) : -1;
+                        bool h = false;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            if (uu[c] >= 0) h |= (ld_bits(frow + (uu[c] >> 5), S.pl) >> (uu[c] & 31)) & 1u;
+                        if (__ballot_sync(FULL, h)) {
+                            hit = true;
+                            break;
+                        }
+                    }
+                    if (hit && lane == ln) found[u] = true;
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < PV; ++u) {
+            const unsigned fmask = __ballot_sync(FULL, found[u]);
+            if (fmask && lane == u) {
+                const long long voff = (long long)q2 * p.W + word0 + u;
+                p.visited[voff] = vis[u] | fmask;
+                fnext[voff] = fmask;
+                nnew += __popc(fmask);
+                atomicAdd(&s_state[q2], (unsigned)__popc(fmask));
+            }
+        }
+    }
+}
+
 // Diagnostic stamp k of level L for this CTA (thread 0): 0 level start (after
 // the decision), 1 plan epoch done, 2 last warp done with the expansion,
 // 3 past the barrier, 4 counters flushed.
@@ -1315,106 +1425,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
             // targets: the owned word range (vertex-partitioned step), else all
             const long long pw0 = s_run.own_w1 > s_run.own_w0 ? s_run.own_w0 : 0;
             const long long pw1 = s_run.own_w1 > s_run.own_w0 ? min((long long)s_run.own_w1, Wn) : Wn;
-            const long long nblk = (pw1 - pw0 + kPullVerts - 1) / kPullVerts;
-            const long long ntask = (long long)s_nptarget * nblk;
-            for (;;) {
-                long long task = 0;
-                if (lane == 0) task = (long long)atomicAdd(&s_task, 1u) * gridDim.x + blockIdx.x;
-                task = __shfl_sync(FULL, task, 0);
-                if (task >= ntask) break;
-                const int q2 = s_ptarget[task / nblk];
-                const long long word0 = pw0 + (task % nblk) * kPullVerts;
-                uint32_t vis[kPullVerts];
-                bool need[kPullVerts], found[kPullVerts];
-                int w[kPullVerts];
-#pragma unroll
-                for (int u = 0; u < kPullVerts; ++u)
-                    vis[u] = word0 + u < pw1 ? ld_bits(p.visited + (long long)q2 * p.W + word0 + u, S.pl) : 0xFFFFFFFFu;
-                bool any_need = false;
-#pragma unroll
-                for (int u = 0; u < kPullVerts; ++u) {
-                    w[u] = (int)((word0 + u) * 32 + lane);
-                    need[u] = w[u] < p.nv && !((vis[u] >> lane) & 1u);
-                    found[u] = false;
-                    any_need |= need[u];
-                }
-                if (__ballot_sync(FULL, any_need) == 0) continue;
-                for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k) {
-                    const int q = S.isrc[k];
-                    if (!s_front[q]) continue;
-                    bool look[kPullVerts], any_look = false;
-#pragma unroll
-                    for (int u = 0; u < kPullVerts; ++u) {
-                        look[u] = need[u] && !found[u];
-                        any_look |= look[u];
-                    }
-                    if (__ballot_sync(FULL, any_look) == 0) break;
-                    const Slot ps = S.slots[p.nslots + S.islot[k]];
-                    const uint32_t* frow = fcur + (long long)q * p.W;
-                    uint32_t lo[kPullVerts], hi[kPullVerts];
-#pragma unroll
-                    for (int u = 0; u < kPullVerts; ++u) {
-                        lo[u] = look[u] ? ld_stream_u32(ps.rowptr + w[u], S.pf) : 0u;
-                        hi[u] = look[u] ? ld_stream_u32(ps.rowptr + w[u] + 1, S.pf) : 0u;
-                    }
-                    // the first kPullInline in-edges of every vertex: all loads in flight together
-                    int cand[kPullVerts][kPullInline];
-#pragma unroll
-                    for (int u = 0; u < kPullVerts; ++u)
-#pragma unroll
-                        for (int i = 0; i < kPullInline; ++i)
-                            cand[u][i] = (lo[u] + i < hi[u]) ? ld_stream_i32(ps.col + lo[u] + i, S.pf) : -1;
-                    uint32_t fw[kPullVerts][kPullInline];
-#pragma unroll
-                    for (int u = 0; u < kPullVerts; ++u)
-#pragma unroll
-                        for (int i = 0; i < kPullInline; ++i)
-                            fw[u][i] = cand[u][i] >= 0 ? ld_bits(frow + (cand[u][i] >> 5), S.pl) : 0u;
-#pragma unroll
-                    for (int u = 0; u < kPullVerts; ++u)
-#pragma unroll
-                        for (int i = 0; i < kPullInline; ++i)
-                            if (cand[u][i] >= 0 && ((fw[u][i] >> (cand[u][i] & 31)) & 1u)) found[u] = true;
-                    // longer rows: the whole warp scans one row at a time, early exit
-#pragma unroll
-                    for (int u = 0; u < kPullVerts; ++u) {
-                        unsigned longrows = __ballot_sync(FULL, look[u] && !found[u] && hi[u] - lo[u] > kPullInline);
-                        while (longrows) {
-                            const int ln = __ffs(longrows) - 1;
-                            longrows &= longrows - 1;
-                            const uint32_t rlo = __shfl_sync(FULL, lo[u], ln) + kPullInline;
-                            const uint32_t rhi = __shfl_sync(FULL, hi[u], ln);
-                            bool hit = false;
-                            for (uint32_t ed = rlo; ed < rhi; ed += 128) {
-                                int uu[4];
-#pragma unroll
-                                for (int c = 0; c < 4; ++c)
-                                    uu[c] = ed + 32 * c + lane < rhi ? ld_stream_i32(ps.col + ed + 32 * c + lane, S.pf) : -1;
-                                bool h = false;
-#pragma unroll
-                                for (int c = 0; c < 4; ++c)
-                                    if (uu[c] >= 0) h |= (ld_bits(frow + (uu[c] >> 5), S.pl) >> (uu[c] & 31)) & 1u;
-                                if (__ballot_sync(FULL, h)) {
-                                    hit = true;
-                                    break;
-                                }
-                            }
-                            if (hit && lane == ln) found[u] = true;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < kPullVerts; ++u) {
-                    const unsigned fmask = __ballot_sync(FULL, found[u]);
-                    if (fmask && lane == u) {
-                        const long long voff = (long long)q2 * p.W + word0 + u;
-                        p.visited[voff] = vis[u] | fmask;
-                        fnext[voff] = fmask;
-                        nnew += __popc(fmask);
-                        atomicAdd(&s_state[q2], (unsigned)__popc(fmask));
-                    }
-                }
-            }
+            if (pw1 - pw0 >= (long long)nwarps * 64)  // large: 8 words per task
+                pull_tasks<8>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front, s_state,
+                              nnew);
+            else
+                pull_tasks<kPullVerts>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front,
+                                       s_state, nnew);
         }
         if (p.trace && lane == 0) atomicMax(&s_wend, globaltimer());  // this warp's work done
         __syncthreads();
