@@ -131,7 +131,8 @@ def ncu_traffic(config):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region (NVML every
+    millisecond; nvidia-smi as the fallback)."""
 
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
@@ -143,7 +144,34 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _poll_nvml(self):
+        """NVML (pynvml) polling every millisecond; False if NVML is unusable."""
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(int(self.index))
+            smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+        except Exception:
+            return False
+        bits = [0x8, 0x40, 0x20, 0x4]  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+        while not self._stop.is_set():
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = get_reasons(h)
+                util = pynvml.nvmlDeviceGetUtilizationRates(h).gpu
+                self.samples.append([str(sm), str(smax)] + ["Active" if r & b else "Not Active" for b in bits]
+                                    + [str(util)])
+            except Exception:
+                pass
+            self._stop.wait(0.001)
+        return True
+
     def _poll(self):
+        if self._poll_nvml():
+            return
         cmd = ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
                "--format=csv,noheader,nounits"]
         while not self._stop.is_set():
