@@ -37,7 +37,7 @@ constexpr int kGroups = 2;             // phase 1: groups of a state expanded to
 constexpr int kGEdges = 2;             // phase 1: edges per lane and group per step
 
 struct BCnt {
-    unsigned int nact;         // active blocks of M_L (flags raised while producing it)
+    unsigned int nact;         // 1 if some discovery produced M_L (0 iff M_L is empty)
     unsigned int nheavy;       // heavy chunks produced while expanding level L
     unsigned int overflow;
     unsigned int expire;       // the deadline check at the top of level L failed
@@ -97,8 +97,10 @@ struct BParams {
 // L2) and only ORed into where that read shows missing bits; the read may
 // miss bits set earlier in this level, never bits of earlier levels, so the
 // bits ORed into M_{L+1} are exactly the discoveries of this level (a bit may
-// be discovered by several edges; ORs are idempotent).  The first discovery
-// into a 256-vertex block raises its activity flag for the next level.
+// be discovered by several edges; ORs are idempotent).  Every discovery
+// raises its 256-vertex block's activity flag for the next level (a plain
+// store: idempotent, nothing to wait for) and counts toward M_{L+1}'s
+// non-emptiness.
 template <int K>
 __device__ __forceinline__ void bvisit(const BParams& p, uint32_t* fnext, uint32_t* anext, const bool (&act)[K],
                                        const int (&t)[K], const int (&u)[K], const uint32_t (&w)[K],
@@ -110,23 +112,16 @@ __device__ __forceinline__ void bvisit(const BParams& p, uint32_t* fnext, uint32
         off[c] = (long long)t[c] * p.nvp + u[c];
         seen[c] = act[c] ? __ldcg(p.vis + off[c]) : 0xFFFFFFFFu;
     }
-    uint32_t* flag[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) {
         const uint32_t nw = w[c] & ~seen[c];
-        flag[c] = nullptr;
         if (nw) {
             atomicOr(p.vis + off[c], nw);  // results unused: RED
             atomicOr(fnext + off[c], nw);
-            flag[c] = anext + (long long)t[c] * p.nblk + (u[c] >> kBlockShift);
+            anext[(long long)t[c] * p.nblk + (u[c] >> kBlockShift)] = 1u;  // idempotent, no round trip
+            ++nact;  // M_{L+1} is non-empty iff some discovery happened
         }
     }
-    uint32_t fl[K];
-#pragma unroll
-    for (int c = 0; c < K; ++c) fl[c] = flag[c] ? __ldcg(flag[c]) : 1u;
-#pragma unroll
-    for (int c = 0; c < K; ++c)
-        if (!fl[c] && atomicExch(flag[c], 1u) == 0u) ++nact;
 }
 
 // Rows longer than kLightDeg become chunks of kChunk edges for phase 2 (one
@@ -186,7 +181,7 @@ __device__ __forceinline__ void bphase_end(const BParams& p, BCnt* nxt, unsigned
             if (v[1]) atomicAdd(&p.ctl->te, v[1]);
             if (v[2]) atomicAdd(&p.ctl->rows, v[2]);
             if (v[3]) atomicAdd(&cnt->items, v[3]);
-            if (v[4]) atomicAdd(&nxt->nact, (unsigned)v[4]);
+            if (v[4]) atomicOr(&nxt->nact, 1u);  // only non-emptiness matters (no 32-bit wrap)
             if (*s_or) atomicOr(&cnt->active, *s_or);
             *s_or = 0;
         }
@@ -274,7 +269,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
             const long long off = (long long)q * p.nvp + src;
             atomicOr(p.vis + off, 1u << lane);
             atomicOr(p.fw[0] + off, 1u << lane);
-            if (atomicExch(p.act[0] + (long long)q * p.nblk + (src >> kBlockShift), 1u) == 0u) ++nact;
+            p.act[0][(long long)q * p.nblk + (src >> kBlockShift)] = 1u;
+            ++nact;
         }
     }
     bphase_end(p, &ctl->bc[0], nact, 0ull, 0ull, 0ull, 0ull, 0u, &ctl->bc[0], s_red, &s_or);
