@@ -33,6 +33,7 @@ constexpr uint32_t kChunk = 256;       // edges per heavy chunk
 constexpr int kBlockShift = 8;         // activity flag per 2^8 vertices
 constexpr int kBlockWords = 1 << kBlockShift;
 constexpr int kBEdges = 4;             // edges per lane in flight per step (chunks)
+constexpr int kListCap = 4 * kThreads; // phase 1: a CTA lists up to this many of its blocks at once
 constexpr int kGroups = 2;             // phase 1: groups of a state expanded together
 constexpr int kGEdges = 2;             // phase 1: edges per lane and group per step
 
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
     __shared__ unsigned s_or;
     __shared__ unsigned s_task;
     __shared__ unsigned s_nlist;
-    __shared__ uint32_t s_list[kThreads];  // active blocks of the current group
+    __shared__ uint32_t s_list[kListCap];  // active blocks of the current group
     __shared__ int s_single;  // every (state, symbol) group has exactly one target (a DFA)
     __shared__ BatchArgs s_run;
 
@@ -339,14 +340,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
         // CTA c owns blocks c, c + G, c + 2G, ... (hubs spread over SMs); it
         // reads kThreads of their flags at once, lists the active ones in
         // shared memory, and its warps take them from a shared counter
-        for (long long i0 = 0; blockIdx.x + i0 * gridDim.x < nbt; i0 += kThreads) {
+        for (long long i0 = 0; blockIdx.x + i0 * gridDim.x < nbt; i0 += kListCap) {
             if (threadIdx.x == 0) {
                 s_nlist = 0;
                 s_task = 0;
             }
             __syncthreads();
-            {
-                const long long b = blockIdx.x + (i0 + threadIdx.x) * gridDim.x;
+            for (int t = threadIdx.x; t < kListCap; t += kThreads) {  // all flag loads in flight
+                const long long b = blockIdx.x + (i0 + t) * gridDim.x;
                 if (b < nbt && __ldcg(acur + b) != 0u) {
                     acur[b] = 0u;  // consumed (level L+2 raises it again)
                     s_list[atomicAdd(&s_nlist, 1u)] = (uint32_t)b;
