@@ -1082,7 +1082,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
         uint4* v4 = reinterpret_cast<uint4*>(p.visited);
         if (!step_mode)
             for (long long i = gtid; i < nbits4; i += gthreads) v4[i] = make_uint4(0, 0, 0, 0);
-        for (int f = step_mode ? 1 : 0; f < 3; ++f) {
+        // step mode: F_0 = M is the caller's and only F_1 (the output) is
+        // written; a full run clears all three
+        for (int f = step_mode ? 1 : 0; f < (step_mode ? 2 : 3); ++f) {
             uint4* f4 = reinterpret_cast<uint4*>(p.fb[f]);
             for (long long i = gtid; i < nbits4; i += gthreads) f4[i] = make_uint4(0, 0, 0, 0);
         }
@@ -1273,7 +1275,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
             for (int q = threadIdx.x; q < kMaxStates; q += blockDim.x) fz->state[q] = 0;
             if (threadIdx.x == 0) fz->nnew = 0;
         }
-        {  // zero the bitmap level L+1 will write F_{L+2} into
+        if (!step_mode) {  // zero the bitmap level L+1 will write F_{L+2} into
             uint4* z4 = reinterpret_cast<uint4*>(p.fb[(L + 2) % 3]);
             for (long long i = gtid; i < nbits4; i += gthreads) z4[i] = make_uint4(0, 0, 0, 0);
         }

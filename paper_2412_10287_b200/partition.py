@@ -256,7 +256,9 @@ def run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout=mat
 
     dev = shards[0].device
     if torch.device(dev).type == "cuda":
-        s = torch.cuda.Stream(dev)
+        s = getattr(shards[0], "stream", None)
+        if s is None:  # one stream per shard set, reused across queries
+            s = shards[0].stream = torch.cuda.Stream(dev)
         s.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(s):
             out = _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, s.cuda_stream,
