@@ -17,13 +17,10 @@ query_compiler.py:27-57), read duck-typed by class name and attributes; the
 mirror classes below exist for callers without the reference.
 """
 
-import math
 import time
 from dataclasses import dataclass
 
 import numpy as np
-
-from . import _lib
 
 
 @dataclass(frozen=True)
