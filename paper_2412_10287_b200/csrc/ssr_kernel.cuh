@@ -47,6 +47,7 @@ constexpr uint32_t kHoleY = 0xFFFFFFFFu;
 constexpr uint32_t kInline = 0x80000000u;
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kPullInline = 2;       // in-edges each lane tests before warp help
+constexpr unsigned kSeedMinBundle = 4;  // seed level: smallest bundle (edges)
 
 constexpr int ST_OVERFLOW = 100;
 constexpr int ST_DEADLOCK = 101;
@@ -1134,7 +1135,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
                 }
             }
             // small seed rows: 32-edge bundles spread the first level over more warps
-            const uint32_t bsz = edges < (unsigned long long)nwarps * 32 ? 32u : (uint32_t)kBundle;
+            // about one bundle per warp (4..128 edges): the source's neighbours
+            // are often hubs themselves (R-MAT: low ids), and each bundle's
+            // warp emits its discoveries' rows -- few per warp spreads that out
+            const unsigned long long per = (edges + nwarps - 1) / (unsigned long long)nwarps;
+            const uint32_t bsz = (uint32_t)min(max(per, (unsigned long long)kSeedMinBundle), (unsigned long long)kBundle);
             for (int r = 0; r < n; ++r) {
                 bundles += (s_sdeg[r + 1] - s_sdeg[r] + bsz - 1) / bsz;
                 s_sbun[r + 1] = bundles;
