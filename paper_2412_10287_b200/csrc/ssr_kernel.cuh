@@ -1269,8 +1269,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
         }
 
         // ---- expand epoch of level L -------------------------------------------
-        // small queues: emit small bundles so the next level spreads over more warps
-        const uint32_t bsz = (dir == DIR_PUSH ? s_bpre[kShards + 1] : s_view.nfront / 8) < (unsigned long long)nwarps
+        // small queues: emit small bundles so the next level spreads over more
+        // warps (threshold: 4 bundles per warp, measured a hair better than 1)
+        const uint32_t bsz = (dir == DIR_PUSH ? s_bpre[kShards + 1] : s_view.nfront / 8) <
+                                     (unsigned long long)nwarps * 4
                                  ? 32u : (uint32_t)kBundle;
         const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, bsz};
         if (threadIdx.x == 0) s_task = 0;
