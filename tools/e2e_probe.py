@@ -37,12 +37,19 @@ for _ in range(50):
     t = time.perf_counter(); q = dg.acquire_query(table); tick("acquire", t)
     t = time.perf_counter(); lib.rpq_query_set_options(q, 0, 0, 4.0); lib.rpq_query_set_output(q, 1); tick("set_opts", t)
     t = time.perf_counter(); lib.rpq_query_run(q, 0, -1.0, None); tick("run(enqueue)", t)
+    tq = time.perf_counter()
     st = _lib.RpqStats()
-    t = time.perf_counter(); lib.rpq_query_wait(q, ctypes.byref(st)); tick("wait", t)
+    t = time.perf_counter(); lib.rpq_query_wait(q, ctypes.byref(st)); tick("wait", t); tick("enqueue->done", tq)
     words = np.empty((g.num_vertices + 31) // 32, dtype=np.uint32)
     t = time.perf_counter(); lib.rpq_query_copy_reach_bits(q, _lib.ptr(words, ctypes.c_uint32), words.size); tick("copy_bits", t)
     t = time.perf_counter(); r = bits_to_reach(words, g.num_vertices); tick("unpack", t)
     tick("device_ms", 0); T["device_ms"][-1] = st.device_ms / 1e3
+    dg.release_query(table, q)
+    words2 = np.empty((g.num_vertices + 31) // 32, dtype=np.uint32)
+    q = dg.acquire_query(table)
+    t = time.perf_counter()
+    lib.rpq_query_eval(q, 0, -1.0, 0, 0, 4.0, 1, ctypes.byref(st), _lib.ptr(words2, ctypes.c_uint32), words2.size)
+    tick("rpq_query_eval (fused C)", t)
     dg.release_query(table, q)
 for k, v in T.items():
     print(f"{k:16s} median {1e6 * float(np.median(v)):9.1f} us")
