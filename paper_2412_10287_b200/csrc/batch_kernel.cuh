@@ -33,7 +33,9 @@ constexpr uint32_t kChunk = 256;       // edges per heavy chunk
 constexpr int kBlockShift = 8;         // activity flag per 2^8 vertices
 constexpr int kBlockWords = 1 << kBlockShift;
 constexpr int kBEdges = 4;             // edges per lane in flight per step (chunks)
-constexpr int kListCap = 4 * kThreads; // phase 1: a CTA lists up to this many of its blocks at once
+constexpr int kBThreads = kThreadsLarge;  // batch state spaces are large: 32 warps per SM
+constexpr int kBWarps = kBThreads / 32;
+constexpr int kListCap = 3 * kBThreads; // phase 1: a CTA lists up to this many of its blocks at once
 constexpr int kGroups = 2;             // phase 1: groups of a state expanded together
 constexpr int kGEdges = 2;             // phase 1: edges per lane and group per step
 
@@ -176,7 +178,7 @@ __device__ __forceinline__ void bphase_end(const BParams& p, BCnt* nxt, unsigned
     if (wid == 0) {
         unsigned long long v[5];
 #pragma unroll
-        for (int k = 0; k < 5; ++k) v[k] = warp_sum_u64(lane < kWarps ? s_red[5 * lane + k] : 0ull);
+        for (int k = 0; k < 5; ++k) v[k] = warp_sum_u64(lane < kBWarps ? s_red[5 * lane + k] : 0ull);
         if (lane == 0) {
             if (v[0]) atomicAdd(&cnt->nnew, v[0]);
             if (v[1]) atomicAdd(&p.ctl->te, v[1]);
@@ -189,9 +191,9 @@ __device__ __forceinline__ void bphase_end(const BParams& p, BCnt* nxt, unsigned
     }
 }
 
-__global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) {
+__global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ unsigned long long s_red[5 * kWarps];
+    __shared__ unsigned long long s_red[5 * kBWarps];
     __shared__ unsigned s_or;
     __shared__ unsigned s_task;
     __shared__ unsigned s_nlist;
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
         unsigned long long te = 0, rows = 0, nnew = 0, items = 0;
         uint32_t active = 0;
         // CTA c owns blocks c, c + G, c + 2G, ... (hubs spread over SMs); it
-        // reads kThreads of their flags at once, lists the active ones in
+        // reads kListCap of their flags at once, lists the active ones in
         // shared memory, and its warps take them from a shared counter
         for (long long i0 = 0; blockIdx.x + i0 * gridDim.x < nbt; i0 += kListCap) {
             if (threadIdx.x == 0) {
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
                 s_task = 0;
             }
             __syncthreads();
-            for (int t = threadIdx.x; t < kListCap; t += kThreads) {  // all flag loads in flight
+            for (int t = threadIdx.x; t < kListCap; t += kBThreads) {  // all flag loads in flight
                 const long long b = blockIdx.x + (i0 + t) * gridDim.x;
                 if (b < nbt && __ldcg(acur + b) != 0u) {
                     acur[b] = 0u;  // consumed (level L+2 raises it again)
@@ -492,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
         const unsigned nh = min((unsigned long long)ldcg(&cur->nheavy), p.heavy_cap);
         if (nh) {
             for (unsigned long long c = blockIdx.x + (unsigned long long)wid * gridDim.x; c < nh;
-                 c += (unsigned long long)gridDim.x * kWarps) {
+                 c += (unsigned long long)gridDim.x * kBWarps) {
                 const uint4 h = p.heavy[c];
                 const int g = (int)h.z;
                 const int32_t* col = s_slots[gslot[g]].col;
@@ -537,8 +539,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) batch_kernel(BParams p) 
     // transposed from source words to one bitmap per source
     if (status == 0) {
         const long long nblk = (p.nv + 127) / 128;
-        const long long gwarp = (long long)blockIdx.x * kWarps + wid;
-        const long long nwarps = (long long)gridDim.x * kWarps;
+        const long long gwarp = (long long)blockIdx.x * kBWarps + wid;
+        const long long nwarps = (long long)gridDim.x * kBWarps;
         unsigned long long cnt = 0;
         for (long long b = gwarp; b < nblk; b += nwarps) {
             uint32_t mine[4];

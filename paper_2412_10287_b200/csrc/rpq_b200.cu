@@ -124,6 +124,7 @@ struct rpq_query {
     cudaStream_t last_stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int grid = 0;
+    int nthreads = kThreads;  // ssr_kernel variant: kThreads or kThreadsLarge
     size_t smem = 0;
     bool ran = false;
     uint64_t edge_bound = 0;  // sum over groups of the slot's nnz
@@ -795,10 +796,14 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
         QTRY(cudaMemcpy(q->d_slot_nnz, q->slot_nnz.data(), q->slot_nnz.size() * sizeof(unsigned long long),
                         cudaMemcpyHostToDevice));
     q->smem = q->slots.size() * sizeof(Slot) + T.size() * sizeof(int32_t) + 16;
+    // large state spaces: the 32-warp variant (more loads in flight); small: 24 warps
+    const bool large = (long long)nstates * (long long)g->nv >= kLargePairs;
+    q->nthreads = large ? kThreadsLarge : kThreads;
+    const void* kfn = large ? (const void*)ssr_kernel<kThreadsLarge> : (const void*)ssr_kernel<kThreads>;
     if (q->smem > 48 * 1024)
-        QTRY(cudaFuncSetAttribute(ssr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q->smem));
+        QTRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q->smem));
     int per_sm = 0;
-    QTRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ssr_kernel, kThreads, q->smem));
+    QTRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, q->nthreads, q->smem));
     if (per_sm < 1) return bail(fail(RPQ_ECUDA, "step kernel cannot be resident"));
     q->grid = std::min(g->sm_count * per_sm, kShards);  // one queue shard per CTA
     if ((long long)nstates * q->W <= kSmallMaxWords) {
@@ -879,8 +884,9 @@ cudaError_t enqueue_run(rpq_query* q, cudaStream_t st, const Params* override = 
     if (small) {
         small_kernel<<<1, kSmallThreads, q->small_smem, st>>>(p);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    } else if ((e = cudaLaunchCooperativeKernel((const void*)ssr_kernel, dim3(q->grid), dim3(kThreads), args,
-                                                q->smem, st)) != cudaSuccess) {
+    } else if ((e = cudaLaunchCooperativeKernel(q->nthreads == kThreadsLarge ? (const void*)ssr_kernel<kThreadsLarge>
+                                                                             : (const void*)ssr_kernel<kThreads>,
+                                                dim3(q->grid), dim3(q->nthreads), args, q->smem, st)) != cudaSuccess) {
         return e;
     }
     // outputs: the control block's results prefix (and the answer bitmap)
@@ -1297,7 +1303,7 @@ int batch_alloc(rpq_query* q) {
     if (q->smem > 48 * 1024)
         BTRY(cudaFuncSetAttribute(batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q->smem));
     int per_sm = 0;
-    BTRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batch_kernel, kThreads, q->smem));
+    BTRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batch_kernel, kBThreads, q->smem));
     if (per_sm < 1) BTRY(cudaErrorInvalidConfiguration);
     q->bgrid = q->g->sm_count * per_sm;
     q->bbar_next = 0;
@@ -1362,7 +1368,7 @@ int rpq_query_run_batch(rpq_query* q, int32_t nsrc, const int32_t* sources, doub
     // the automaton tables live in the single-source input block: send it too
     CUDA_TRY(cudaMemcpyAsync(q->d_in, q->h_in, q->in_bytes, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(q->d_bargs, q->h_bargs, sizeof(BatchArgs), cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)batch_kernel, dim3(q->bgrid), dim3(kThreads), args, q->smem,
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)batch_kernel, dim3(q->bgrid), dim3(kBThreads), args, q->smem,
                                          st));
     CUDA_TRY(cudaMemcpyAsync(q->h_bctl, q->d_bctl, offsetof(BCtl, bc), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaEventRecord(q->ev1, st));

@@ -26,9 +26,14 @@
 
 namespace rpqk {
 
-constexpr int kThreads = 768;        // 24 warps per CTA, one CTA per SM
+// One CTA per SM; the thread count is a template parameter of the kernels:
+// 768 (24 warps, 80 registers) for small state spaces, where fewer spills win,
+// 1024 (32 warps, 64 registers) for large ones, where more warps in flight win
+constexpr int kThreads = 768;         // small state spaces
+constexpr int kThreadsLarge = 1024;   // large state spaces (and the batch kernel)
+constexpr long long kLargePairs = 8ll << 20;  // |Q| x |V| from which the large variant runs
 constexpr int kMinBlocks = 1;
-constexpr int kWarps = kThreads / 32;
+constexpr int kMaxWarps = kThreadsLarge / 32;
 constexpr int kEdgesPerLane = 4;     // push: edges each lane expands per bundle
 constexpr int kBundle = 32 * kEdgesPerLane;  // edges per bundle; an emission pass has
                                              // <= 32 segments, so a bundle spans <= 32
@@ -590,8 +595,9 @@ __device__ __forceinline__ void flush_counts(unsigned long long* nnew_dst, const
     }
     __syncthreads();
     if (wid == 0) {
-        unsigned long long a = lane < kWarps ? red[2 * lane] : 0ull;
-        unsigned long long c = lane < kWarps ? red[2 * lane + 1] : 0ull;
+        const int nwarp = (int)(blockDim.x >> 5);
+        unsigned long long a = lane < nwarp ? red[2 * lane] : 0ull;
+        unsigned long long c = lane < nwarp ? red[2 * lane + 1] : 0ull;
         a = warp_sum_u64(a);
         c = warp_sum_u64(c);
         if (lane == 0 && a && nnew_dst) atomicAdd(nnew_dst, a);
@@ -848,7 +854,7 @@ __device__ void decide_plan(const Params& p, unsigned e, int L, int lane, View* 
 }
 
 __device__ __forceinline__ void reset_qc(QCnt* qc, int tid) {
-    for (int i = tid; i <= kShards; i += kThreads) qc->shard[i] = 0;
+    for (int i = tid; i <= kShards; i += blockDim.x) qc->shard[i] = 0;
     if (tid == 0) {
         qc->edges = 0;
         qc->overflow = 0;
@@ -997,7 +1003,9 @@ __device__ __forceinline__ void stamp(const Params& p, int L, int k) {
         p.trace[((long long)L * gridDim.x + blockIdx.x) * 8 + k] = globaltimer() - p.ctl->t0;
 }
 
-__global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
+template <int NT>
+__global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
+    constexpr int kWarps = NT / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ unsigned long long s_red[2 * kWarps];
     __shared__ unsigned long long s_bpre[kShards + 2];
@@ -1519,7 +1527,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ssr_kernel(Params p) {
         __syncthreads();
         if (wid == 0) {
             cnt = warp_sum_u64(lane < kWarps ? s_red[2 * lane] : 0ull);
-            te = warp_sum_u64(lane < kWarps ? s_red[2 * lane + 1] : 0ull);
+            te = warp_sum_u64(lane < kWarps ? s_red[2 * lane + 1] : 0ull);  // (kWarps <= 32)
             if (lane == 0 && cnt) atomicAdd(&ctl->reach_count, cnt);
             if (lane == 0 && te) atomicAdd(&ctl->te_exact, te);
         }
