@@ -70,6 +70,9 @@ def parse_args():
     ap.add_argument("--emit-inline-max", type=int, default=None)
     ap.add_argument("--flags", type=int, default=None, help="tuning: push variants (RPQ_TUNE_FLAGS)")
     ap.add_argument("--defer", type=float, default=None, help="tuning: RPQ_TUNE_DEFER factor")
+    ap.add_argument("--reorder", action="store_true",
+                    help="experiment: relabel vertices by descending total degree before ingest")
+    ap.add_argument("--alpha", type=float, default=None, help="tuning: Beamer switch constant (default: engine's)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between steps (diagnostic)")
     ap.add_argument("--profile", action="store_true",
@@ -313,6 +316,12 @@ def run_engine(args, rank, world, local_rank):
     global QUERY, WORKLOAD
     QUERY, WORKLOAD = WORKLOADS[args.config]
     sg = datagen.generate(args.config)
+    if args.reorder:
+        deg = np.bincount(sg.src, minlength=sg.nv) + np.bincount(sg.dst, minlength=sg.nv)
+        newid = np.empty(sg.nv, dtype=np.int32)
+        newid[np.argsort(-deg, kind="stable")] = np.arange(sg.nv, dtype=np.int32)
+        sg.src, sg.dst = newid[sg.src], newid[sg.dst]
+        del deg, newid
     g = sg.labeled_graph()
     nj = load_automaton(args.config, QUERY)
     n = P.Automaton.from_json(nj)
@@ -331,10 +340,11 @@ def run_engine(args, rank, world, local_rank):
     if args.defer is not None:
         P.engine.raise_for_status(P._lib.engine().rpq_query_set_tuning(pq.q, 5, float(args.defer)), "defer")
     # one untimed run for the work counts (exact TE, |P|, levels) of this query
-    pq.set_options(direction=args.direction, count_te=True)
+    alpha = args.alpha if args.alpha is not None else P.EngineOptions().alpha
+    pq.set_options(direction=args.direction, count_te=True, alpha=alpha)
     pq.launch(source, -1.0, handle)
     st0 = pq.wait()
-    pq.set_options(direction=args.direction, count_te=False)
+    pq.set_options(direction=args.direction, count_te=False, alpha=alpha)
     per_state = pq.visited_counts()
     outdeg_q = np.bincount(pq.table.t_src, minlength=pq.table.nstates)
     x = int((per_state * outdeg_q).sum())
@@ -379,7 +389,7 @@ def run_engine(args, rank, world, local_rank):
     # e2e through the public API: automaton H2D + kernel + answer D2H per call
     e2e_s = []
     if not args.profile:
-        opts = P.EngineOptions(timeout=math.inf, direction=args.direction)
+        opts = P.EngineOptions(timeout=math.inf, direction=args.direction, alpha=alpha)
         for _ in range(args.warmup):  # untimed, like the device leg (first call creates the query)
             P.eval_ssr(g, n, source, opts)
         for k in range(args.steps):

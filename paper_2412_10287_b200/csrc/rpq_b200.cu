@@ -405,6 +405,22 @@ void free_query_buffers(rpq_query* q) {
     if (q->own_stream) cudaStreamDestroy(q->own_stream);
 }
 
+// A kernel's dynamic shared memory limit belongs to the function, shared by
+// every query and graph: raise it once to the device's opt-in maximum (each
+// launch still passes its own size).  Setting it to one query's size would
+// make an earlier, larger query's launches fail.
+cudaError_t allow_dyn_smem(const void* fn) {
+    int dev = 0, optin = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess) return e;
+    const int cap = optin - (int)fa.sharedSizeBytes;
+    if (fa.maxDynamicSharedSizeBytes >= cap) return cudaSuccess;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+}
+
 }  // namespace
 
 extern "C" {
@@ -519,8 +535,7 @@ int rpq_graph_create_coo(int32_t num_vertices, int32_t num_labels, int64_t nnz, 
     if (nnz > 0 && nl > 0) {
         // shared memory: nl counters (padded to even) + nl 64-bit range bases
         const size_t sm = nl <= 8192 ? (size_t)((nl + 1) & ~1) * 4 + (size_t)nl * 8 : 0;
-        if (sm > 48 * 1024)
-            GTRY(cudaFuncSetAttribute(label_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        if (sm > 48 * 1024) GTRY(allow_dyn_smem((const void*)label_scatter_kernel));
         label_scatter_kernel<<<1184, 256, sm>>>(d_src, d_dst, d_lab, nnz, nl, cursor, g->d_coo);
         GTRY(cudaGetLastError());
     }
@@ -795,13 +810,12 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     if (!q->slot_nnz.empty())
         QTRY(cudaMemcpy(q->d_slot_nnz, q->slot_nnz.data(), q->slot_nnz.size() * sizeof(unsigned long long),
                         cudaMemcpyHostToDevice));
-    q->smem = q->slots.size() * sizeof(Slot) + T.size() * sizeof(int32_t) + 16;
     // large state spaces: the 32-warp variant (more loads in flight); small: 24 warps
     const bool large = (long long)nstates * (long long)g->nv >= kLargePairs;
     q->nthreads = large ? kThreadsLarge : kThreads;
+    q->smem = kStageBytes(q->nthreads) + q->slots.size() * sizeof(Slot) + T.size() * sizeof(int32_t) + 16;
     const void* kfn = large ? (const void*)ssr_kernel<kThreadsLarge> : (const void*)ssr_kernel<kThreads>;
-    if (q->smem > 48 * 1024)
-        QTRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q->smem));
+    QTRY(allow_dyn_smem(kfn));
     int per_sm = 0;
     QTRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, q->nthreads, q->smem));
     if (per_sm < 1) return bail(fail(RPQ_ECUDA, "step kernel cannot be resident"));
@@ -810,8 +824,7 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
         q->small_smem = q->slots.size() * sizeof(Slot) + (T.size() * sizeof(int32_t) + 15) / 16 * 16 +
                         3 * (size_t)nstates * (size_t)q->W * sizeof(uint32_t);
         if (q->small_smem <= 200 * 1024) {
-            QTRY(cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)std::max<size_t>(q->small_smem, 48 * 1024)));
+            QTRY(allow_dyn_smem((const void*)small_kernel));
             q->small_ok = true;
         }
     }
@@ -1300,8 +1313,7 @@ int batch_alloc(rpq_query* q) {
     BTRY(cudaMalloc(&q->d_bargs, sizeof(BatchArgs)));
     BTRY(cudaMallocHost(&q->h_bargs, sizeof(BatchArgs)));
     BTRY(cudaMalloc(&q->d_bout, (size_t)kBatch * (size_t)q->W * 4));
-    if (q->smem > 48 * 1024)
-        BTRY(cudaFuncSetAttribute(batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q->smem));
+    BTRY(allow_dyn_smem((const void*)batch_kernel));
     int per_sm = 0;
     BTRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batch_kernel, kBThreads, q->smem));
     if (per_sm < 1) BTRY(cudaErrorInvalidConfiguration);

@@ -530,12 +530,26 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
 }
 
 // Per-warp staging of discovered pairs so that emission passes are full
-// (<= 63 staged; a pass emits 32).
+// (a pass emits 32).  stage_add keeps <= 63 staged; the push loop stages a
+// whole bundle (stage_put, <= 31 + 32 x kEdgesPerLane) and drains it once, so
+// its body holds one inlined emission instead of one per unrolled edge slot.
+constexpr int kStageCap = 32 * kEdgesPerLane + 32;
+__host__ __device__ constexpr size_t kStageBytes(int nthreads) { return (size_t)(nthreads / 32) * 2 * kStageCap * 4; }
 struct Stage {
-    int* q;  // smem [64]
-    int* w;  // smem [64]
+    int* q;  // smem [kStageCap]
+    int* w;  // smem [kStageCap]
     int n;
 };
+
+__device__ __forceinline__ void stage_put(Stage& st, bool fresh, int q, int w, int lane) {
+    const unsigned m = __ballot_sync(FULL, fresh);
+    if (fresh) {
+        const int pos = st.n + __popc(m & lanemask_lt());
+        st.q[pos] = q;
+        st.w[pos] = w;
+    }
+    st.n += __popc(m);
+}
 
 __device__ __forceinline__ uint32_t stage_add(const Params& p, const Smem& S, const Out& o, Stage& st,
                                               bool fresh, int q, int w, int lane) {
@@ -567,6 +581,33 @@ __device__ __forceinline__ uint32_t stage_add(const Params& p, const Smem& S, co
         st.n = rem;
         __syncwarp();
     }
+    return T;
+}
+
+// emit every full pass of 32 staged pairs; keep the remainder (< 32)
+__device__ __forceinline__ uint32_t stage_drain(const Params& p, const Smem& S, const Out& o, Stage& st,
+                                                int lane) {
+    if (st.n < 32) return 0;
+    __syncwarp();
+    uint32_t T = 0;
+    int base = 0;
+    for (; st.n - base >= 32; base += 32) {
+        const int qq = st.q[base + lane], ww = st.w[base + lane];
+        T += emit_pairs(p, S, o, true, qq, ww, lane);
+    }
+    const int rem = st.n - base;
+    int tq = 0, tw = 0;
+    if (lane < rem) {
+        tq = st.q[base + lane];
+        tw = st.w[base + lane];
+    }
+    __syncwarp();
+    if (lane < rem) {
+        st.q[lane] = tq;
+        st.w[lane] = tw;
+    }
+    st.n = rem;
+    __syncwarp();
     return T;
 }
 
@@ -1015,16 +1056,17 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
     __shared__ int s_ptarget[kMaxStates];            // pull target states of this level
     __shared__ int s_nptarget;
     __shared__ View s_view;
-    __shared__ int s_stage[kWarps][2][64];
     __shared__ unsigned long long s_resv;
     __shared__ unsigned s_task;  // next task index of this CTA in the current epoch
     __shared__ unsigned long long s_wend;  // diagnostics: latest warp done with the epoch
     __shared__ RunArgs s_run;
     __shared__ float s_nnz[kMaxSlots];
 
-    Slot* s_slots = reinterpret_cast<Slot*>(smem_raw);
+    // dynamic smem: [emission stages, kStageBytes(NT)] [slots] [tables]
+    int* s_stage = reinterpret_cast<int*>(smem_raw);
+    Slot* s_slots = reinterpret_cast<Slot*>(smem_raw + kStageBytes(NT));
     for (int i = threadIdx.x; i < p.nslots; i += blockDim.x) s_nnz[i] = (float)p.slot_nnz[i];
-    int32_t* s_tab = reinterpret_cast<int32_t*>(smem_raw + sizeof(Slot) * 2 * p.nslots);
+    int32_t* s_tab = reinterpret_cast<int32_t*>(smem_raw + kStageBytes(NT) + sizeof(Slot) * 2 * p.nslots);
     for (int i = threadIdx.x; i < 2 * p.nslots; i += blockDim.x) s_slots[i] = p.slots[i];
     for (int i = threadIdx.x; i < p.table_ints; i += blockDim.x) s_tab[i] = p.tables[i];
     if (threadIdx.x == 0) {
@@ -1069,8 +1111,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
     const bool cta0 = blockIdx.x == 0;
     __syncthreads();  // s_run, tables and counters above are read by every thread below
     Stage stage;
-    stage.q = s_stage[wid][0];
-    stage.w = s_stage[wid][1];
+    stage.q = s_stage + wid * 2 * kStageCap;
+    stage.w = s_stage + wid * 2 * kStageCap + kStageCap;
     stage.n = 0;
     // CTA 0 resets the control block (except the barrier counter, which only
     // grows); nobody else reads it before the first barrier
@@ -1414,10 +1456,11 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
                         const bool fresh = q2[u] >= 0 && !(old[u] & (1u << (w[u] & 31)));
                         nnew += fresh ? 1 : 0;
                         if (fresh) atomicAdd(&s_state[q2[u]], 1u);
-                        if (emit_inline) {
-                            const uint32_t T = stage_add(p, S, o, stage, fresh, q2[u], w[u], lane);
-                            if (lane == 0) nedge += T;
-                        }
+                        if (emit_inline) stage_put(stage, fresh, q2[u], w[u], lane);
+                    }
+                    if (emit_inline) {
+                        const uint32_t T = stage_drain(p, S, o, stage, lane);
+                        if (lane == 0) nedge += T;
                     }
                 }
             }

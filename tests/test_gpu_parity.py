@@ -254,3 +254,28 @@ def test_device_ingest_matches_host_csr(seed):
             want, st = oracle_bfs(og, oq, s)
             got = P.eval_ssr(dg, n, s, P.EngineOptions(timeout=math.inf))
             assert np.array_equal(got.reach, want) and got.iterations == st["iterations"]
+
+
+def test_queries_with_different_shared_memory_interleave():
+    """The kernels' dynamic shared memory limit is per function: a query
+    created after another with a smaller table must not shrink the limit the
+    first one launches with (run big, small, big on the grid kernel)."""
+    import json
+    import os
+
+    from oracle import OracleGraph, OracleQuery, oracle_bfs
+
+    sg = datagen.gen_rmat(13, 16, 8, 1.0, 31)
+    g = sg.labeled_graph()
+    og = OracleGraph(sg.nv, sg.nl, sg.src, sg.dst, sg.lab)
+    path = os.path.join(os.path.dirname(__file__), "golden", "extra_automata.json")
+    table = json.load(open(path))
+    opts = P.EngineOptions(timeout=math.inf, kernel="grid")
+    want, nfa = {}, {}
+    for query in ("(a ^a)* (b | c ^d)*", "a b*", "(a ^a)* (b | c ^d)*", "a b*"):
+        nj = table[query]
+        if query not in want:  # same automaton objects: the cached queries are reused
+            want[query] = oracle_bfs(og, OracleQuery(nj, sg.nl), 0)[0]
+            nfa[query] = automaton(nj)
+        got = P.eval_ssr(g, nfa[query], 0, opts)
+        assert np.array_equal(got.reach, want[query]), query

@@ -2,6 +2,8 @@
 
     python tools/ncu_lines.py gpurun_out/prof.ncu-rep paper_2412_10287_b200/librpq_b200.so [kernel]
 
+COL=<source-page column> replaces "Instructions Executed" as the second
+figure (e.g. COL="L2 Theoretical Sectors Global"); SORT=col orders by it.
 ncu's source page of a -lineinfo build lists SASS with stall samples; the
 cubin inside the .so carries the line table (nvdisasm --print-line-info), so
 function offsets map to lines of csrc/*.cuh.
@@ -47,8 +49,8 @@ def main():
     rows = list(csv.reader(io.StringIO(txt)))
     h = rows[1]
     si = h.index("Warp Stall Sampling (All Samples)")
-    ii = h.index("Instructions Executed")
-    addrs = [(int(r[0], 16), int(r[si] or 0), int(r[ii] or 0)) for r in rows[2:] if r and r[0].startswith("0x")]
+    ii = h.index(os.environ.get("COL", "Instructions Executed"))
+    addrs = [(int(r[0], 16), int(r[si] or 0), int(float(r[ii] or 0))) for r in rows[2:] if r and r[0].startswith("0x")]
     base = min(a for a, _, _ in addrs)
     lm = line_map(so, kernel)
     src_path = None
@@ -71,7 +73,8 @@ def main():
         return f"{os.path.basename(path)}:{ln}", (lines[ln - 1].strip()[:80] if ln <= len(lines) else "?")
 
     print(f"total samples {tot}")
-    for key, (smp, ins) in sorted(by_line.items(), key=lambda kv: -kv[1][0])[:int(os.environ.get("TOP", 30))]:
+    col = 1 if os.environ.get("SORT") == "col" else 0
+    for key, (smp, ins) in sorted(by_line.items(), key=lambda kv: -kv[1][col])[:int(os.environ.get("TOP", 30))]:
         loc, text = text_of(key)
         print(f"{smp:7d} {100.0 * smp / max(tot, 1):5.1f}% {ins:10d}  {loc}: {text}")
 
