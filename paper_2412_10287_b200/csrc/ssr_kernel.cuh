@@ -105,6 +105,9 @@ struct Ctl {
     // ---- working counters (zeroed by CTA 0 at the start of every run) -----
     QCnt qc[3];
     FCnt fc[3];
+    // tail-bundle counter of the queue qc[i] while it is the current one
+    // (reset with qc[i]); one 128-byte line each, away from the counters
+    unsigned long long steal[3][16];
 };
 
 // Per-run inputs, copied host->device with the automaton tables at the start
@@ -894,9 +897,11 @@ __device__ void decide_plan(const Params& p, unsigned e, int L, int lane, View* 
     }
 }
 
-__device__ __forceinline__ void reset_qc(QCnt* qc, int tid) {
+__device__ __forceinline__ void reset_qc(Ctl* ctl, int k, int tid) {
+    QCnt* qc = &ctl->qc[k];
     for (int i = tid; i <= kShards; i += blockDim.x) qc->shard[i] = 0;
     if (tid == 0) {
+        ctl->steal[k][0] = 0;
         qc->edges = 0;
         qc->overflow = 0;
         qc->expire = 0;
@@ -1149,7 +1154,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
     // emitted by one warp.  All seed bundles are inline (each lies in one row).
     if (!step_mode) {
         const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, 32u};
-        if (cta0) reset_qc(&ctl->qc[(e + 2) % 3], threadIdx.x);
+        if (cta0) reset_qc(ctl, (e + 2) % 3, threadIdx.x);
         unsigned long long nnew = 0, nedge = 0;
         const int src = S.run->source;
         if (cta0 && wid == 0) {  // claim the seed pairs
@@ -1279,7 +1284,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
             // ---- plan epoch: emit F_L's row segments from its bitmap (after pull)
             const uint32_t bsz = s_view.nfront < (unsigned long long)nwarps * 8 ? 32u : (uint32_t)kBundle;
             const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, bsz};
-            if (cta0) reset_qc(&ctl->qc[(e + 2) % 3], threadIdx.x);
+            if (cta0) reset_qc(ctl, (e + 2) % 3, threadIdx.x);
             unsigned long long nedge = 0;
             for (int q = 0; q < p.nstates; ++q) {
                 if (!s_front[q] || S.gbeg[q + 1] == S.gbeg[q]) continue;
@@ -1327,7 +1332,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
         const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, bsz};
         if (threadIdx.x == 0) s_task = 0;
         if (cta0) {
-            reset_qc(&ctl->qc[(e + 2) % 3], threadIdx.x);
+            reset_qc(ctl, (e + 2) % 3, threadIdx.x);
             FCnt* fz = &ctl->fc[(L + 2) % 3];
             for (int q = threadIdx.x; q < kMaxStates; q += blockDim.x) fz->state[q] = 0;
             if (threadIdx.x == 0) fz->nnew = 0;
@@ -1354,11 +1359,22 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
             // queue, so heavy rows spread over SMs); its warps take them one at a
             // time from a shared counter, so fast warps do more of them
             (void)step;
+            // On long queues (>= 64 bundles per CTA) the last eighth (past
+            // nb_own, a multiple of G) is dealt from one grid-wide counter
+            // instead: CTAs that finish their share early take the tail
+            // instead of idling at the barrier.  Short queues stay CTA-local
+            // (a global round trip per bundle costs more than the imbalance).
+            const unsigned long long G = gridDim.x;
+            const unsigned long long nb_own = nb >= 64 * G ? (nb - nb / 8) / G * G : nb;
+            unsigned long long* steal = &ctl->steal[e % 3][0];
             // software pipeline: the next bundle's descriptor is in flight while
             // this one is expanded (one dependent round trip less per bundle)
             auto grab = [&](uint2* d) -> unsigned long long {
                 unsigned long long b = 0;
-                if (lane == 0) b = (unsigned long long)atomicAdd(&s_task, 1u) * gridDim.x + blockIdx.x;
+                if (lane == 0) {
+                    b = (unsigned long long)atomicAdd(&s_task, 1u) * gridDim.x + blockIdx.x;
+                    if (b >= nb_own && nb_own < nb) b = nb_own + atomicAdd(steal, 1ull);
+                }
                 b = __shfl_sync(FULL, b, 0);
                 if (b < nb) {
                     int sh = 0;

@@ -20,6 +20,8 @@ def main():
     ap.add_argument("--levels", type=int, default=16)
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--direction", default="auto")
+    ap.add_argument("--query", type=int, default=0, help="index into the config's query templates")
+    ap.add_argument("--max-degree", action="store_true", help="source = max out-degree vertex (bench.py's)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -31,8 +33,11 @@ def main():
     c = datagen.CONFIGS[args.config]
     sg = datagen.generate(args.config)
     g = sg.labeled_graph()
-    n = P.Automaton.from_json(autos[args.config][c["queries"][0] + "|min"])
-    src = int(datagen.pick_sources(sg, args.config, count=1)[0])
+    n = P.Automaton.from_json(autos[args.config][c["queries"][args.query] + "|min"])
+    if args.max_degree:
+        src = int(np.argmax(sg.out_degree()))
+    else:
+        src = int(datagen.pick_sources(sg, args.config, count=1)[0])
     pq = P.PreparedQuery(g, n)
     pq.set_options(direction=args.direction)
     lib = _lib.engine()
