@@ -951,13 +951,28 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
         uint32_t vis[PV];
         bool need[PV], found[PV];
         int w[PV];
-#pragma unroll
-        for (int u = 0; u < PV; ++u)
-            vis[u] = word0 + u < pw1 ? ld_bits(p.visited + (long long)q2 * p.W + word0 + u, S.pl) : 0xFFFFFFFFu;
-        bool any_need = false;
+        // the first pulled in-slot (warp-uniform): its row pointers do not
+        // depend on P, so they are loaded with P's words (coalesced, one
+        // dependent round trip less per task; visited vertices' are wasted)
+        int k0 = -1;
+        for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k)
+            if (s_front[S.isrc[k]]) {
+                k0 = k;
+                break;
+            }
+        uint32_t lo[PV], hi[PV];
 #pragma unroll
         for (int u = 0; u < PV; ++u) {
             w[u] = (int)((word0 + u) * 32 + lane);
+            const bool in = word0 + u < pw1 && w[u] < p.nv;
+            vis[u] = word0 + u < pw1 ? ld_bits(p.visited + (long long)q2 * p.W + word0 + u, S.pl) : 0xFFFFFFFFu;
+            const uint32_t* rp = S.slots[p.nslots + S.islot[max(k0, 0)]].rowptr;
+            lo[u] = in && k0 >= 0 ? ld_stream_u32(rp + w[u], S.pf) : 0u;
+            hi[u] = in && k0 >= 0 ? ld_stream_u32(rp + w[u] + 1, S.pf) : 0u;
+        }
+        bool any_need = false;
+#pragma unroll
+        for (int u = 0; u < PV; ++u) {
             need[u] = w[u] < p.nv && !((vis[u] >> lane) & 1u);
             found[u] = false;
             any_need |= need[u];
@@ -975,11 +990,14 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
             if (__ballot_sync(FULL, any_look) == 0) break;
             const Slot ps = S.slots[p.nslots + S.islot[k]];
             const uint32_t* frow = fcur + (long long)q * p.W;
-            uint32_t lo[PV], hi[PV];
 #pragma unroll
             for (int u = 0; u < PV; ++u) {
-                lo[u] = look[u] ? ld_stream_u32(ps.rowptr + w[u], S.pf) : 0u;
-                hi[u] = look[u] ? ld_stream_u32(ps.rowptr + w[u] + 1, S.pf) : 0u;
+                if (k != k0) {
+                    lo[u] = look[u] ? ld_stream_u32(ps.rowptr + w[u], S.pf) : 0u;
+                    hi[u] = look[u] ? ld_stream_u32(ps.rowptr + w[u] + 1, S.pf) : 0u;
+                } else if (!look[u]) {
+                    hi[u] = lo[u];  // preloaded: mask the vertices that need no look
+                }
             }
             // the first kPullInline in-edges of every vertex: all loads in flight together
             int cand[PV][kPullInline];
