@@ -39,6 +39,7 @@ constexpr int kBundle = 32 * kEdgesPerLane;  // edges per bundle; an emission pa
                                              // <= 32 segments, so a bundle spans <= 32
 constexpr int kPullVerts = 4;        // pull: vertices (words of 32) per lane per task
 constexpr int kShards = 160;         // queue shards, one per CTA (+1 overflow shard)
+static_assert(kShards <= 256, "the push shard search (two ballots of 32 x 8) covers 256 shards");
 constexpr int kMaxStates = 256;
 constexpr int kMaxGroups = 256;      // group id is 8 bits in a segment
 constexpr int kMaxSlots = 128;
@@ -1395,10 +1396,14 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
                 }
                 b = __shfl_sync(FULL, b, 0);
                 if (b < nb) {
-                    int sh = 0;
-#pragma unroll
-                    for (int h = 128; h >= 1; h >>= 1)
-                        if (sh + h <= kShards && s_bpre[sh + h] <= b) sh += h;
+                    // shard of bundle b = #{i in [1, kShards] : s_bpre[i] <= b}
+                    // (s_bpre is non-decreasing): lanes test every 8th entry,
+                    // then the 7 inside the block found (two ballots; b is
+                    // warp-uniform, so every lane is here)
+                    const int ci = 8 * (lane + 1);
+                    const int c = __popc(__ballot_sync(FULL, ci <= kShards && s_bpre[ci] <= b));
+                    const int fi = 8 * c + 1 + lane;
+                    const int sh = 8 * c + __popc(__ballot_sync(FULL, lane < 7 && fi <= kShards && s_bpre[fi] <= b));
                     *d = ld_queue(bun + (unsigned long long)sh * p.shard_buncap + (b - s_bpre[sh]), S.pf);
                 }
                 return b;
