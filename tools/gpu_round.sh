@@ -24,3 +24,7 @@ timeout 300 python bench.py --profile --steps 3 --warmup 3 > $out/prof_plain_$ta
     python bench.py --profile --steps 3 --warmup 3 > $out/ncu_launches_$tag.log 2>&1; echo "ncu_launch_rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:ssr_kernel -s 2 -c 1 \
     -o $out/prof_cfg2_$tag python bench.py --profile --steps 3 --warmup 3 > $out/ncu_full_$tag.log 2>&1; echo "ncu_full_rc=$?"
+timeout 600 python bench.py --config cfg4 --profile --steps 3 --warmup 3 > $out/prof4_plain_$tag.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:ssr_kernel -s 2 -c 1 \
+    -o $out/prof_cfg4_$tag python bench.py --config cfg4 --profile --steps 3 --warmup 3 > $out/ncu4_full_$tag.log 2>&1; echo "ncu4_full_rc=$?"
+timeout 600 python tools/trace_probe.py cfg4 --query 2 --max-degree --levels 30 > $out/trace_cfg4_$tag.jsonl 2> $out/trace_cfg4_$tag.err; echo "trace4_rc=$?"

@@ -14,7 +14,13 @@ cp $G/launches_$T.csv profiles/r01_cfg2_launches.csv
 cp $G/trace_cfg2_$T.jsonl profiles/r01_cfg2_trace.jsonl
 cp $G/gpu_tests_$T.log profiles/r01_gpu_tests.log
 ncu -i $G/prof_cfg2_$T.ncu-rep --page details --csv > profiles/r01_cfg2_ssr_kernel_details.csv 2>/dev/null
-python tools/ncu_lines.py $G/prof_cfg2_$T.ncu-rep paper_2412_10287_b200/librpq_b200.so ssr_kernel > profiles/r01_cfg2_stall_lines.txt 2>&1
+# (cfg2 runs the 768-thread instance, cfg4 the 1,024-thread one)
+python tools/ncu_lines.py $G/prof_cfg2_$T.ncu-rep paper_2412_10287_b200/librpq_b200.so ssr_kernelILi768 > profiles/r01_cfg2_stall_lines.txt 2>&1
+if [ -f $G/prof_cfg4_$T.ncu-rep ]; then
+  ncu -i $G/prof_cfg4_$T.ncu-rep --page details --csv > profiles/r01_cfg4_ssr_kernel_details.csv 2>/dev/null
+  python tools/ncu_lines.py $G/prof_cfg4_$T.ncu-rep paper_2412_10287_b200/librpq_b200.so ssr_kernelILi1024 > profiles/r01_cfg4_stall_lines.txt 2>&1
+  cp $G/trace_cfg4_$T.jsonl profiles/r01_cfg4_trace.jsonl
+fi
 ncu -i $G/prof_cfg2_$T.ncu-rep --page raw --csv 2>/dev/null | T=$T python -c "
 import csv, json, os, sys
 r = list(csv.reader(sys.stdin)); h, u, v = r[0], r[1], r[2]
