@@ -905,7 +905,8 @@ cudaError_t enqueue_run(rpq_query* q, cudaStream_t st, const Params* override = 
     // outputs: the control block's results prefix (and the answer bitmap)
     if ((e = cudaMemcpyAsync(q->h_ctl, q->d_ctl, offsetof(Ctl, qc), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
         return e;
-    if (q->output_mode == 1 && q->g->nv > 0 &&
+    // (a step-mode run, `override`, projects no answer: nothing to copy)
+    if (q->output_mode == 1 && !override && q->g->nv > 0 &&
         (e = cudaMemcpyAsync(q->h_reach_bits, q->d_reach_bits, (size_t)((q->g->nv + 31) / 32) * 4,
                              cudaMemcpyDeviceToHost, st)) != cudaSuccess)
         return e;
