@@ -295,6 +295,7 @@ struct View {
     int plan;       // push level whose queue must first be emitted from F_L
     int defer;      // push level: do not emit F_{L+1}'s queue at discovery (the next level is likely pull)
     float mf;       // m_f of the last decided frontier (growth estimate)
+    float dmax;     // the densest slot's mean degree, nnz / |V| (constant per query)
     int status;
     int iterations;
     unsigned long long nfront;  // |F_L|
@@ -706,6 +707,8 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
                              View* v, unsigned long long* s_bpre, unsigned long long* s_sv,
                              unsigned int* s_front) {
     Ctl* ctl = p.ctl;
+    if (p.trace && L < p.trace_levels && lane == 0)  // diagnostics: decision entered
+        p.trace[((long long)L * gridDim.x + blockIdx.x) * 8 + 6] = globaltimer() - ctl->t0;
     const QCnt* qc = &ctl->qc[e % 3];
     const FCnt* fc = &ctl->fc[L % 3];
     // every load of the decision in flight at once (one L2 round trip)
@@ -729,6 +732,8 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
         }
     }
     __syncwarp();
+    if (p.trace && L < p.trace_levels && lane == 0)  // diagnostics: the decision's loads are back
+        p.trace[((long long)L * gridDim.x + blockIdx.x) * 8 + 5] = globaltimer() - ctl->t0;
     // F_L's queue was emitted at discovery (exact m_f and bundles available)
     const int produced_by_push = prev_queued;
     int done = 0, iterations = 0, status = 0, next = DIR_PUSH, plan = 0;
@@ -756,7 +761,7 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
             // average degrees after a pull level); m_u: in-edges of unvisited
             // targets whose source state has a frontier.  Pull when
             // m_f * alpha > m_u (Beamer's rule; alpha tuned for these kernels).
-            const float nv = (float)p.nv, inv_nv = 1.0f / (float)p.nv;
+            const float nv = (float)p.nv, inv_nv = __frcp_rn((float)p.nv);  // (no division subroutine)
             float mf = 0.0f, mu = 0.0f;
             int ntarget = 0;  // states a pull level would scan
             for (int q = lane; q < p.nstates; q += 32) {
@@ -786,9 +791,8 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
             // Predicted m_f(F_{L+1}) = m_f(F_L) x min(last growth, densest
             // slot's mean degree), tested like the real decision will be.
             if (S.run->defer_alpha > 0.0f) {
-                float dmax = 0.0f;
-                for (int sl = 0; sl < p.nslots; ++sl) dmax = fmaxf(dmax, S.nnz[sl] * inv_nv);
-                const float growth = mf / fmaxf(v->mf, 1.0f);
+                const float dmax = v->dmax;  // densest slot's mean degree (per query, set at start)
+                const float growth = __fdividef(mf, fmaxf(v->mf, 1.0f));
                 defer = L > 0 && mf * fminf(growth, dmax) * S.run->defer_alpha > mu;
             }
             __syncwarp();  // every lane has read the previous m_f
@@ -1106,6 +1110,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
         s_run = *p.run;
         s_view.mf = 0.0f;
         s_view.defer = 0;
+        float d = 0.0f;
+        for (int sl = 0; sl < p.nslots; ++sl) d = fmaxf(d, (float)p.slot_nnz[sl]);
+        s_view.dmax = d * __frcp_rn((float)max(p.nv, 1));
     }
     Smem S;
     S.pf = policy_evict_first();

@@ -69,6 +69,8 @@ def main():
                "plan_max": plan.max() if plan.any() else None,
                "work_min": t[:, 2].min(), "work_med": float(np.median(t[:, 2])), "work_max": t[:, 2].max(),
                "flush_max": t[:, 4].max(),
+               "dec_enter": (tr[L, :, 6].min(), tr[L, :, 6].max()),
+               "dec_loaded": (tr[L, :, 5].min(), tr[L, :, 5].max()),
                "dec_end": (tr[L, :, 7].min(), tr[L, :, 7].max()),
                "bar_min": t[:, 3].min(), "bar_max": t[:, 3].max(),
                "slowest_cta": int(np.argmax(t[:, 2]))}
