@@ -72,6 +72,8 @@ def parse_args():
     ap.add_argument("--defer", type=float, default=None, help="tuning: RPQ_TUNE_DEFER factor")
     ap.add_argument("--reorder", action="store_true",
                     help="experiment: relabel vertices by descending total degree before ingest")
+    ap.add_argument("--zero-copy", type=int, default=None, choices=[0, 1],
+                    help="tuning: RPQ_TUNE_ZERO_COPY (statistics block written straight to pinned host memory)")
     ap.add_argument("--alpha", type=float, default=None, help="tuning: Beamer switch constant (default: engine's)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between steps (diagnostic)")
@@ -339,6 +341,9 @@ def run_engine(args, rank, world, local_rank):
         P.engine.raise_for_status(P._lib.engine().rpq_query_set_tuning(pq.q, 3, float(args.flags)), "flags")
     if args.defer is not None:
         P.engine.raise_for_status(P._lib.engine().rpq_query_set_tuning(pq.q, 5, float(args.defer)), "defer")
+    if args.zero_copy is not None:
+        P.engine.raise_for_status(P._lib.engine().rpq_query_set_tuning(pq.q, 6, float(args.zero_copy)),
+                                  "zero_copy")
     # one untimed run for the work counts (exact TE, |P|, levels) of this query
     alpha = args.alpha if args.alpha is not None else P.EngineOptions().alpha
     pq.set_options(direction=args.direction, count_te=True, alpha=alpha)

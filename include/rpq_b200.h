@@ -173,6 +173,9 @@ RPQ_API int rpq_query_set_options(rpq_query* q, int32_t direction, int32_t count
                              m_f(F_L) x (densest slot's mean degree) x value > m_u (0: always emit;
                              default 2) */
 #define RPQ_TUNE_TRACE 2  /* diagnostics: record per-CTA phase stamps of the first `value` levels */
+#define RPQ_TUNE_ZERO_COPY 6  /* 1 (default): the grid kernel's last CTA writes the statistics
+                                 block straight into pinned host memory (no copy node after
+                                 the kernel); 0: a device-to-host copy after the kernel */
 RPQ_API int rpq_query_set_tuning(rpq_query* q, int32_t key, double value);
 /* Enqueue one evaluation from `source` on `stream` (a cudaStream_t, or NULL for
  * the query's own stream).  timeout_s < 0 or inf: no deadline.  The deadline is

@@ -97,6 +97,8 @@ struct rpq_query {
     uint2* d_bun[2] = {nullptr, nullptr};
     Ctl* d_ctl = nullptr;
     Ctl* h_ctl = nullptr;  // pinned
+    Ctl* h_ctl_dev = nullptr;  // its device view (unified addressing)
+    int zero_copy = 1;         // RPQ_TUNE_ZERO_COPY
     uint8_t* d_reach = nullptr;
     uint32_t* d_reach_bits = nullptr;
     uint32_t* h_reach_bits = nullptr;  // pinned; filled by run() when output_mode == 1
@@ -796,6 +798,7 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     }
     QTRY(cudaMalloc(&q->d_ctl, sizeof(Ctl)));
     QTRY(cudaMallocHost(&q->h_ctl, sizeof(Ctl)));
+    QTRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&q->h_ctl_dev), q->h_ctl, 0));
     QTRY(cudaMalloc(&q->d_reach, (size_t)(q->W * 32 + 32)));
     QTRY(cudaMalloc(&q->d_reach_bits, (size_t)q->W * sizeof(uint32_t)));
     QTRY(cudaMallocHost(&q->h_reach_bits, (size_t)q->W * sizeof(uint32_t)));
@@ -858,6 +861,7 @@ Params make_params(const rpq_query* q) {
         p.bun[b] = q->d_bun[b];
     }
     p.ctl = q->d_ctl;
+    p.host_ctl = q->zero_copy ? q->h_ctl_dev : nullptr;
     p.reach = q->d_reach;
     p.reach_bits = q->d_reach_bits;
     p.shard_segcap = q->shard_segcap;
@@ -893,6 +897,7 @@ cudaError_t enqueue_run(rpq_query* q, cudaStream_t st, const Params* override = 
     if ((e = cudaMemcpyAsync(q->d_in, q->h_in, q->in_bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
         return e;
     Params p = override ? *override : make_params(q);
+    if (small) p.host_ctl = nullptr;  // (the single-CTA kernel's block is copied below)
     void* args[] = {&p};
     if (small) {
         small_kernel<<<1, kSmallThreads, q->small_smem, st>>>(p);
@@ -903,7 +908,8 @@ cudaError_t enqueue_run(rpq_query* q, cudaStream_t st, const Params* override = 
         return e;
     }
     // outputs: the control block's results prefix (and the answer bitmap)
-    if ((e = cudaMemcpyAsync(q->h_ctl, q->d_ctl, offsetof(Ctl, qc), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    if (!p.host_ctl &&
+        (e = cudaMemcpyAsync(q->h_ctl, q->d_ctl, offsetof(Ctl, qc), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
         return e;
     // (a step-mode run, `override`, projects no answer: nothing to copy)
     if (q->output_mode == 1 && !override && q->g->nv > 0 &&
@@ -953,6 +959,20 @@ int rpq_query_set_tuning(rpq_query* q, int32_t key, double value) {
         case RPQ_TUNE_EMIT_INLINE_MAX:
             if (value < 0 || value > 4.0e9) return fail(RPQ_EINVAL, "bad inline threshold");
             q->emit_inline_max = (unsigned int)value;
+            return RPQ_OK;
+        case RPQ_TUNE_ZERO_COPY:
+            if (value != 0 && value != 1) return fail(RPQ_EINVAL, "zero-copy switch must be 0 or 1");
+            q->zero_copy = (int)value;
+            if (q->inflight) {  // let a run in flight finish with the old graph
+                CUDA_TRY(cudaStreamSynchronize(q->last_stream));
+                q->bar_next = q->h_ctl->bar;
+                q->inflight = false;
+            }
+            if (q->graph) {  // the captured run holds the old parameters and nodes
+                cudaGraphExecDestroy(q->graph);
+                q->graph = nullptr;
+                q->graph_mode = -1;
+            }
             return RPQ_OK;
         case RPQ_TUNE_DEFER:
             if (!(value >= 0) || value > 1e6) return fail(RPQ_EINVAL, "defer factor must be >= 0");

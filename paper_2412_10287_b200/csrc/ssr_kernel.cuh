@@ -109,6 +109,7 @@ struct Ctl {
     // tail-bundle counter of the queue qc[i] while it is the current one
     // (reset with qc[i]); one 128-byte line each, away from the counters
     unsigned long long steal[3][16];
+    unsigned int exits;  // CTAs past the epilogue (zero-copy results: the last one publishes)
 };
 
 // Per-run inputs, copied host->device with the automaton tables at the start
@@ -143,6 +144,8 @@ struct Params {
     uint2* seg[2];
     uint2* bun[2];
     Ctl* ctl;
+    Ctl* host_ctl;  // device view of the pinned host control block: the last CTA
+                    // writes the results prefix there (no copy node), or null
     uint8_t* reach;
     uint32_t* reach_bits;  // the answer as a bitmap (same bits as reach)
     unsigned long long shard_segcap, shard_buncap, ovf_segcap, ovf_buncap;
@@ -1619,6 +1622,26 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
             te = warp_sum_u64(lane < kWarps ? s_red[2 * lane + 1] : 0ull);  // (kWarps <= 32)
             if (lane == 0 && cnt) atomicAdd(&ctl->reach_count, cnt);
             if (lane == 0 && te) atomicAdd(&ctl->te_exact, te);
+        }
+    }
+
+    // zero-copy results: the last CTA out copies the results prefix (everything
+    // before the working counters) to pinned host memory
+    if (p.host_ctl) {
+        __shared__ int s_last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();  // this CTA's counter updates are visible first
+            s_last = atomicAdd(&ctl->exits, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            constexpr int nw = (int)(offsetof(Ctl, qc) / 4);
+            const unsigned* src = reinterpret_cast<const unsigned*>(ctl);
+            unsigned* dst = reinterpret_cast<unsigned*>(p.host_ctl);
+            for (int i = threadIdx.x; i < nw; i += blockDim.x) dst[i] = __ldcg(src + i);
+            __threadfence_system();
         }
     }
 }

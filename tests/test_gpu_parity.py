@@ -279,3 +279,34 @@ def test_queries_with_different_shared_memory_interleave():
             nfa[query] = automaton(nj)
         got = P.eval_ssr(g, nfa[query], 0, opts)
         assert np.array_equal(got.reach, want[query]), query
+
+
+def test_zero_copy_statistics_match_the_copy_path():
+    """RPQ_TUNE_ZERO_COPY: the grid kernel's last CTA writes the statistics
+    block into pinned host memory instead of a copy node; both paths report
+    the same run (answer, levels, counts), run after run."""
+    from paper_2412_10287_b200 import _lib
+
+    sg = datagen.gen_rmat(14, 16, 8, 1.0, 41)
+    g = sg.labeled_graph()
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(__file__), "golden", "extra_automata.json")
+    n = automaton(json.load(open(path))["^a (b|c)* d"])
+    src = int(np.argmax(sg.out_degree()))
+    pq = P.PreparedQuery(g, n)
+    pq.set_tuning(kernel="grid")
+    seen = []
+    for zc in (0, 1, 0, 1, 1):
+        assert _lib.engine().rpq_query_set_tuning(pq.q, 6, float(zc)) == 0, _lib.last_error()
+        pq.launch(src)
+        st = pq.wait().to_dict()
+        keep = {k: st[k] for k in ("status", "iterations", "levels", "te", "visited_pairs", "reach_count",
+                                   "level_new", "level_dir")}
+        seen.append((keep, pq.reach().copy()))
+    for keep, reach in seen[1:]:
+        assert keep == seen[0][0]
+        assert np.array_equal(reach, seen[0][1])
+    assert seen[0][0]["reach_count"] == int(seen[0][1].sum()) > 0
+    pq.close()
