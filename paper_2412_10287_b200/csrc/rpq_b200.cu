@@ -893,7 +893,9 @@ bool use_small(const rpq_query* q) { return q->small_ok && q->allow_small && q->
 
 cudaError_t enqueue_run(rpq_query* q, cudaStream_t st, const Params* override = nullptr, bool small = false) {
     cudaError_t e;
-    // inputs: run arguments + automaton tables in one pinned block
+    // inputs: run arguments + automaton tables in one pinned block (a copy
+    // node: the kernel prologue reading them from host memory instead was
+    // 65 us slower on cfg2 -- 148 CTAs of small uncached PCIe reads)
     if ((e = cudaMemcpyAsync(q->d_in, q->h_in, q->in_bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
         return e;
     Params p = override ? *override : make_params(q);
