@@ -98,6 +98,7 @@ struct rpq_query {
     Ctl* d_ctl = nullptr;
     Ctl* h_ctl = nullptr;  // pinned
     Ctl* h_ctl_dev = nullptr;  // its device view (unified addressing)
+    uint32_t* h_reach_bits_dev = nullptr;  // device view of h_reach_bits
     int zero_copy = 1;         // RPQ_TUNE_ZERO_COPY
     uint8_t* d_reach = nullptr;
     uint32_t* d_reach_bits = nullptr;
@@ -802,6 +803,7 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     QTRY(cudaMalloc(&q->d_reach, (size_t)(q->W * 32 + 32)));
     QTRY(cudaMalloc(&q->d_reach_bits, (size_t)q->W * sizeof(uint32_t)));
     QTRY(cudaMallocHost(&q->h_reach_bits, (size_t)q->W * sizeof(uint32_t)));
+    QTRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&q->h_reach_bits_dev), q->h_reach_bits, 0));
 
     QTRY(cudaStreamCreateWithFlags(&q->own_stream, cudaStreamNonBlocking));
     QTRY(cudaEventCreate(&q->ev0));
@@ -862,6 +864,7 @@ Params make_params(const rpq_query* q) {
     }
     p.ctl = q->d_ctl;
     p.host_ctl = q->zero_copy ? q->h_ctl_dev : nullptr;
+    p.host_bits = q->zero_copy && q->output_mode == 1 ? q->h_reach_bits_dev : nullptr;
     p.reach = q->d_reach;
     p.reach_bits = q->d_reach_bits;
     p.shard_segcap = q->shard_segcap;
@@ -899,7 +902,11 @@ cudaError_t enqueue_run(rpq_query* q, cudaStream_t st, const Params* override = 
     if ((e = cudaMemcpyAsync(q->d_in, q->h_in, q->in_bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
         return e;
     Params p = override ? *override : make_params(q);
-    if (small) p.host_ctl = nullptr;  // (the single-CTA kernel's block is copied below)
+    if (small) {  // (the single-CTA kernel's block and answer are copied below)
+        p.host_ctl = nullptr;
+        p.host_bits = nullptr;
+    }
+    if (override) p.host_bits = nullptr;  // a step projects no answer
     void* args[] = {&p};
     if (small) {
         small_kernel<<<1, kSmallThreads, q->small_smem, st>>>(p);
@@ -914,7 +921,7 @@ cudaError_t enqueue_run(rpq_query* q, cudaStream_t st, const Params* override = 
         (e = cudaMemcpyAsync(q->h_ctl, q->d_ctl, offsetof(Ctl, qc), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
         return e;
     // (a step-mode run, `override`, projects no answer: nothing to copy)
-    if (q->output_mode == 1 && !override && q->g->nv > 0 &&
+    if (q->output_mode == 1 && !override && !p.host_bits && q->g->nv > 0 &&
         (e = cudaMemcpyAsync(q->h_reach_bits, q->d_reach_bits, (size_t)((q->g->nv + 31) / 32) * 4,
                              cudaMemcpyDeviceToHost, st)) != cudaSuccess)
         return e;

@@ -146,6 +146,8 @@ struct Params {
     Ctl* ctl;
     Ctl* host_ctl;  // device view of the pinned host control block: the last CTA
                     // writes the results prefix there (no copy node), or null
+    uint32_t* host_bits;  // device view of the pinned answer bitmap (written by the
+                          // epilogue with the device one: no copy node), or null
     uint8_t* reach;
     uint32_t* reach_bits;  // the answer as a bitmap (same bits as reach)
     unsigned long long shard_segcap, shard_buncap, ovf_segcap, ovf_buncap;
@@ -1576,6 +1578,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
             for (int f = 0; f < p.nfinals; ++f) acc |= __ldcg(p.visited + (long long)S.finals[f] * p.W + i);
             cnt += __popc(acc);
             p.reach_bits[i] = acc;
+            if (p.host_bits) p.host_bits[i] = acc;  // coalesced: 128 B per warp over PCIe
             uint8_t* out = p.reach + i * 32;
             if (i * 32 + 32 <= p.nv) {
                 uint32_t bytes[8];
