@@ -338,11 +338,11 @@ def run_engine(args, rank, world, local_rank):
 
     pq.set_tuning(args.emit_mode, args.emit_inline_max)
     if args.flags is not None:
-        P.engine.raise_for_status(P._lib.engine().rpq_query_set_tuning(pq.q, 3, float(args.flags)), "flags")
+        P.engine.raise_for_status(P._lib.engine().rpq_query_set_tuning(pq.q, P._lib.TUNE_FLAGS, float(args.flags)), "flags")
     if args.defer is not None:
-        P.engine.raise_for_status(P._lib.engine().rpq_query_set_tuning(pq.q, 5, float(args.defer)), "defer")
+        P.engine.raise_for_status(P._lib.engine().rpq_query_set_tuning(pq.q, P._lib.TUNE_DEFER, float(args.defer)), "defer")
     if args.zero_copy is not None:
-        P.engine.raise_for_status(P._lib.engine().rpq_query_set_tuning(pq.q, 6, float(args.zero_copy)),
+        P.engine.raise_for_status(P._lib.engine().rpq_query_set_tuning(pq.q, P._lib.TUNE_ZERO_COPY, float(args.zero_copy)),
                                   "zero_copy")
     # one untimed run for the work counts (exact TE, |P|, levels) of this query
     alpha = args.alpha if args.alpha is not None else P.EngineOptions().alpha

@@ -26,6 +26,15 @@ DIR_PULL = 2
 
 STATS_LEVELS = 64
 
+# rpq_query_set_tuning keys (include/rpq_b200.h RPQ_TUNE_*)
+TUNE_EMIT_MODE = 0
+TUNE_EMIT_INLINE_MAX = 1
+TUNE_TRACE = 2
+TUNE_FLAGS = 3
+TUNE_SMALL = 4
+TUNE_DEFER = 5
+TUNE_ZERO_COPY = 6
+
 c_i32 = ctypes.c_int32
 c_i64 = ctypes.c_int64
 c_u64 = ctypes.c_uint64

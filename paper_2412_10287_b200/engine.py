@@ -405,12 +405,12 @@ class PreparedQuery:
     def set_tuning(self, emit_mode=None, emit_inline_max=None, kernel=None):
         lib = _lib.engine()
         if kernel is not None:
-            raise_for_status(lib.rpq_query_set_tuning(self.q, 4, 1.0 if kernel == "auto" else 0.0),
+            raise_for_status(lib.rpq_query_set_tuning(self.q, _lib.TUNE_SMALL, 1.0 if kernel == "auto" else 0.0),
                              "rpq_query_set_tuning")
         if emit_mode is not None:
-            raise_for_status(lib.rpq_query_set_tuning(self.q, 0, float(emit_mode)), "rpq_query_set_tuning")
+            raise_for_status(lib.rpq_query_set_tuning(self.q, _lib.TUNE_EMIT_MODE, float(emit_mode)), "rpq_query_set_tuning")
         if emit_inline_max is not None:
-            raise_for_status(lib.rpq_query_set_tuning(self.q, 1, float(emit_inline_max)),
+            raise_for_status(lib.rpq_query_set_tuning(self.q, _lib.TUNE_EMIT_INLINE_MAX, float(emit_inline_max)),
                              "rpq_query_set_tuning")
 
     def launch(self, source, timeout=-1.0, stream=None):

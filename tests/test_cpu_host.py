@@ -40,6 +40,19 @@ def test_engine_library_exports_header():
     assert _lib.engine().rpq_abi_version() == 1
 
 
+def test_header_constants_match_the_binding():
+    """Status codes and tuning keys: include/rpq_b200.h and _lib.py agree."""
+    text = open(os.path.join(ROOT, "include", "rpq_b200.h")).read()
+    defs = dict((k, int(v)) for k, v in re.findall(r"#define (RPQ_\w+)\s+(\d+)\b", text))
+    tune = {k[len("RPQ_TUNE_"):]: v for k, v in defs.items() if k.startswith("RPQ_TUNE_")}
+    assert len(tune) >= 7
+    for name, value in tune.items():
+        assert getattr(_lib, "TUNE_" + name) == value, name
+    for name in ("RPQ_OK", "RPQ_EINVAL", "RPQ_ERANGE", "RPQ_ETIMEOUT", "RPQ_ECUDA"):
+        assert getattr(_lib, name) == defs[name], name
+    assert _lib.BATCH == defs["RPQ_BATCH"] and _lib.STATS_LEVELS == defs["RPQ_STATS_LEVELS"]
+
+
 def test_engine_library_is_sm100a_only():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _build.ENGINE_SO],
                          capture_output=True, text=True).stdout

@@ -299,7 +299,7 @@ def test_zero_copy_statistics_match_the_copy_path():
     pq.set_tuning(kernel="grid")
     seen = []
     for zc in (0, 1, 0, 1, 1):
-        assert _lib.engine().rpq_query_set_tuning(pq.q, 6, float(zc)) == 0, _lib.last_error()
+        assert _lib.engine().rpq_query_set_tuning(pq.q, _lib.TUNE_ZERO_COPY, float(zc)) == 0, _lib.last_error()
         pq.launch(src)
         st = pq.wait().to_dict()
         keep = {k: st[k] for k in ("status", "iterations", "levels", "te", "visited_pairs", "reach_count",

@@ -41,7 +41,7 @@ def main():
     pq = P.PreparedQuery(g, n)
     pq.set_options(direction=args.direction)
     lib = _lib.engine()
-    assert lib.rpq_query_set_tuning(pq.q, 2, float(args.levels)) == 0, _lib.last_error()
+    assert lib.rpq_query_set_tuning(pq.q, _lib.TUNE_TRACE, float(args.levels)) == 0, _lib.last_error()
     s = torch.cuda.Stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for rep in range(4):

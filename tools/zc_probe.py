@@ -39,7 +39,7 @@ def main():
     ref = None
     for rnd in range(2):
         for zc in (0, 1):
-            assert lib.rpq_query_set_tuning(pq.q, 6, float(zc)) == 0, _lib.last_error()
+            assert lib.rpq_query_set_tuning(pq.q, _lib.TUNE_ZERO_COPY, float(zc)) == 0, _lib.last_error()
             ts = []
             for k in range(args.reps + 5):
                 flush.fill_(k & 0xFF)
