@@ -944,7 +944,7 @@ __device__ unsigned long long frontier_edges(const Params& p, const Smem& S, con
 // Pull tasks of one level: every (target state, PV words of vertices) with an
 // active source state.  PV words per lane-task: more vertices in flight per
 // warp on large graphs, more tasks (balance) on small ones.
-template <int PV>
+template <int PV, int INL>
 __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const uint32_t* fcur, uint32_t* fnext,
                                            long long pw0, long long pw1, int lane, unsigned* s_task,
                                            int s_nptarget, const int* s_ptarget, const unsigned int* s_front,
@@ -1009,32 +1009,32 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
                     hi[u] = lo[u];  // preloaded: mask the vertices that need no look
                 }
             }
-            // the first kPullInline in-edges of every vertex: all loads in flight together
-            int cand[PV][kPullInline];
+            // the first INL in-edges of every vertex: all loads in flight together
+            int cand[PV][INL];
 #pragma unroll
             for (int u = 0; u < PV; ++u)
 #pragma unroll
-                for (int i = 0; i < kPullInline; ++i)
+                for (int i = 0; i < INL; ++i)
                     cand[u][i] = (lo[u] + i < hi[u]) ? ld_stream_i32(ps.col + lo[u] + i, S.pf) : -1;
-            uint32_t fw[PV][kPullInline];
+            uint32_t fw[PV][INL];
 #pragma unroll
             for (int u = 0; u < PV; ++u)
 #pragma unroll
-                for (int i = 0; i < kPullInline; ++i)
+                for (int i = 0; i < INL; ++i)
                     fw[u][i] = cand[u][i] >= 0 ? ld_bits(frow + (cand[u][i] >> 5), S.pl) : 0u;
 #pragma unroll
             for (int u = 0; u < PV; ++u)
 #pragma unroll
-                for (int i = 0; i < kPullInline; ++i)
+                for (int i = 0; i < INL; ++i)
                     if (cand[u][i] >= 0 && ((fw[u][i] >> (cand[u][i] & 31)) & 1u)) found[u] = true;
             // longer rows: the whole warp scans one row at a time, early exit
 #pragma unroll
             for (int u = 0; u < PV; ++u) {
-                unsigned longrows = __ballot_sync(FULL, look[u] && !found[u] && hi[u] - lo[u] > kPullInline);
+                unsigned longrows = __ballot_sync(FULL, look[u] && !found[u] && hi[u] - lo[u] > INL);
                 while (longrows) {
                     const int ln = __ffs(longrows) - 1;
                     longrows &= longrows - 1;
-                    const uint32_t rlo = __shfl_sync(FULL, lo[u], ln) + kPullInline;
+                    const uint32_t rlo = __shfl_sync(FULL, lo[u], ln) + INL;
                     const uint32_t rhi = __shfl_sync(FULL, hi[u], ln);
                     bool hit = false;
                     for (uint32_t ed = rlo; ed < rhi; ed += 128) {
@@ -1536,12 +1536,25 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
             // targets: the owned word range (vertex-partitioned step), else all
             const long long pw0 = s_run.own_w1 > s_run.own_w0 ? s_run.own_w0 : 0;
             const long long pw1 = s_run.own_w1 > s_run.own_w0 ? min((long long)s_run.own_w1, Wn) : Wn;
-            if (pw1 - pw0 >= (long long)nwarps * 64)  // large: 8 words per task
-                pull_tasks<8>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front, s_state,
-                              nnew);
-            else
-                pull_tasks<kPullVerts>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front,
-                                       s_state, nnew);
+            // A dense frontier (> 22% of |V| pairs) usually answers at the first
+            // in-edge: probe one inline, a sparse one two.  Only in the
+            // large-state-space instance (cfg3: L3 204 -> 166 us, L2 275 -> 265;
+            // cfg5 -2.7%); the 768-thread one (cfg2) keeps its code unchanged.
+            const bool one_inline = NT == kThreadsLarge && (float)s_view.nfront > 0.22f * (float)p.nv;
+            if (pw1 - pw0 >= (long long)nwarps * 64) {  // large: 8 words per task
+                if (one_inline)
+                    pull_tasks<8, 1>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front,
+                                     s_state, nnew);
+                else
+                    pull_tasks<8, kPullInline>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget,
+                                               s_front, s_state, nnew);
+            } else if (one_inline) {
+                pull_tasks<kPullVerts, 1>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front,
+                                          s_state, nnew);
+            } else {
+                pull_tasks<kPullVerts, kPullInline>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget,
+                                                    s_front, s_state, nnew);
+            }
         }
         if (p.trace && lane == 0) atomicMax(&s_wend, globaltimer());  // this warp's work done
         __syncthreads();
