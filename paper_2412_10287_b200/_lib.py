@@ -161,8 +161,8 @@ ENGINE_SIGNATURES = {
     "rpq_query_destroy": (c_i32, [c_vp]),
     "rpq_query_row_words": (c_i32, [c_vp, P_i64]),
     "rpq_query_set_owned": (c_i32, [c_vp, c_i64, c_i64]),
-    "rpq_query_eval": (c_i32, [c_vp, c_i32, c_dbl, c_i32, c_i32, c_dbl, c_i32, ctypes.POINTER(RpqStats), P_u32,
-                               c_i64]),
+    # (stats and answer buffers as void*: the per-query fast path passes raw addresses)
+    "rpq_query_eval": (c_i32, [c_vp, c_i32, c_dbl, c_i32, c_i32, c_dbl, c_i32, c_vp, c_vp, c_i64]),
     "rpq_query_copy_trace": (c_i32, [c_vp, P_u64, c_i64, P_i32]),
     "rpq_query_step_device": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "rpq_query_run_batch": (c_i32, [c_vp, c_i32, P_i32, c_dbl, c_vp]),

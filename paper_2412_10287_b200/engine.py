@@ -18,6 +18,7 @@ loop's own accounting.  There is no CPU path: the CUDA library must load.
 import ctypes
 import dataclasses
 import math
+import threading
 import time
 import weakref
 from dataclasses import dataclass
@@ -187,6 +188,17 @@ def bits_to_reach(words, nv):
     return np.unpackbits(words.view(np.uint8), bitorder="little")[:nv]
 
 
+_TLS = threading.local()
+
+
+def _thread_stats():
+    """One rpq_stats block per thread, reused by every eval_ssr call."""
+    st = getattr(_TLS, "stats", None)
+    if st is None:
+        st = _TLS.stats = _lib.RpqStats()
+    return st
+
+
 def _run(g, n, source, opts, tag, *, want_stats=False):
     opts.validate()
     _check_vertex(g, source)
@@ -203,12 +215,12 @@ def _run(g, n, source, opts, tag, *, want_stats=False):
             raise QueryTimeout(time.monotonic() - t0, 0)
         budget = -1.0 if math.isinf(remaining) else remaining
         words = np.empty((g.num_vertices + 31) // 32, dtype=np.uint32)
-        stats = _lib.RpqStats()
-        # options, run, wait and the answer bitmap in one C call
+        stats = _thread_stats()  # read (or copied out) before this thread's next call
+        # options, run, wait and the answer bitmap in one C call (raw addresses)
         rc = lib.rpq_query_eval(q, int(source), budget, DIRECTIONS[opts.direction],
                                 int(opts.count_te or opts.debug_checks), opts.alpha,
-                                1 if opts.kernel == "auto" else 0, ctypes.byref(stats),
-                                _lib.ptr(words, ctypes.c_uint32) if words.size else None, words.size)
+                                1 if opts.kernel == "auto" else 0, ctypes.addressof(stats),
+                                words.ctypes.data if words.size else None, words.size)
         if rc == _lib.RPQ_ETIMEOUT:
             raise QueryTimeout(time.monotonic() - t0,
                                _iterations_for(tag, stats.iterations, table.starts.size))
