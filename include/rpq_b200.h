@@ -171,7 +171,7 @@ RPQ_API int rpq_query_set_options(rpq_query* q, int32_t direction, int32_t count
                              with shared-memory bitmaps; 0: always the grid kernel */
 #define RPQ_TUNE_DEFER 5  /* push level L does not emit F_{L+1}'s queue at discovery when
                              m_f(F_L) x (densest slot's mean degree) x value > m_u (0: always emit;
-                             default 2) */
+                             default 3) */
 #define RPQ_TUNE_TRACE 2  /* diagnostics: record per-CTA phase stamps of the first `value` levels */
 #define RPQ_TUNE_ZERO_COPY 6  /* 1 (default): the grid kernel's last CTA writes the statistics
                                  block straight into pinned host memory (no copy node after

@@ -117,7 +117,7 @@ struct rpq_query {
     int emit_mode = 0;
     unsigned int emit_inline_max = 1u << 16;
     unsigned int run_flags = RF_NO_PROBE;
-    float defer_alpha = 2.0f;
+    float defer_alpha = 3.0f;  // RPQ_TUNE_DEFER (profiles/r01_defer_sweep.txt)
     long long own_w0 = 0, own_w1 = 0;  // owned word range (partitioned step); empty = all
     bool small_ok = false;    // |Q| x |V| fits the single-CTA kernel
     int allow_small = 1;      // RPQ_TUNE_SMALL
