@@ -1,26 +1,30 @@
 #!/usr/bin/env python
 """Benchmark: 2-RPQ product edges traversed per second (GTEPS) and per-query
-latency on the BASELINE.json headline configuration (configs[1] = cfg2):
+latency on BASELINE.json's largest single-GPU configuration (configs[2] = cfg3):
 
-  R-MAT scale 20 (1,048,576 vertices), edge factor 16, (0.57, 0.19, 0.19, 0.05),
-  self-loops and duplicates removed, 16 Zipf(1.0) labels; two-way query
-  a ^b* c (the reference compiler's minimal 3-state DFA); source = the vertex
-  with the highest out-degree.  Synthetic, seeded (paper_2412_10287_b200/datagen.py).
+  R-MAT scale 24 (16,777,216 vertices), edge factor 16, (0.57, 0.19, 0.19, 0.05),
+  self-loops and duplicates removed, 64 Zipf(1.0) labels; two-way query
+  ^a (b|c)* d (the reference compiler's minimal 3-state DFA); sources drawn
+  uniformly from the vertices with out-degree >= 1 (BASELINE's rule; the first
+  8 draws of datagen.pick_sources).  Synthetic, seeded (paper_2412_10287_b200/datagen.py).
 
-A step is one single-source query evaluation (seed -> answer vector ready on
-the device).  `value` is device-timed with CUDA events around each step on
-the launching stream (inputs resident in HBM, L2 flushed between steps);
-`e2e` is the same metric through the public API `eval_ssr` with the automaton
-sent host->device every call and the uint8 answer read back to the host.
+A step evaluates every bench source once, one single-source query (seed ->
+answer vector ready on the device) per launch.  `value` = sum of the product
+edges traversed / sum of the query times, device-timed with CUDA events
+around each query on the launching stream (inputs resident in HBM, L2
+flushed before every query, outside the events); `e2e` is the same metric
+through the public API `eval_ssr` with the automaton sent host->device every
+call and the answer read back to the host.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference]
+                  [--config cfgN] [--sources S]
 
-With N > 1 (torchrun, one rank per GPU) every rank evaluates its own
-independent query -- rank r starts from the r-th highest out-degree vertex --
-with no data-path collective (weak scaling over independent queries).
-`--impl reference` times the reference algorithm's CPU restatement
-(oracle/rpq_oracle.c oracle_port, the hybrid loop of engine.py:197-232) on all
-host cores, one independent query per thread; rank 0 only.
+With N > 1 (torchrun, one rank per GPU) every rank evaluates its own S
+sources (the next S draws of the same rule) with no data-path collective
+(weak scaling over independent queries).  `--impl reference` times the
+reference algorithm's CPU restatement (oracle/rpq_oracle.c oracle_port, the
+hybrid loop of engine.py:197-232) on all host cores over the same sources;
+rank 0 only.
 """
 
 import argparse
@@ -35,18 +39,19 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))  # checker: cpu_baseline and --impl reference only
 
 METRIC = "2-RPQ edges traversed/sec (GTEPS)"
 UNIT = "GTEPS"
-CONFIG = "cfg2"
-QUERY = "a ^b* c"
+CONFIG = "cfg3"
+QUERY = "^a (b|c)* d"
 WORKLOADS = {
     "cfg1": ("a b*", "cfg1: Erdos-Renyi 10,000 V / 100,000 E, 4 uniform labels, query a b* "
                      "(2-state min DFA), source 0"),
     "cfg2": ("a ^b* c", "cfg2: R-MAT scale 20 (1,048,576 V), edge factor 16, abc=(0.57,0.19,0.19), "
                         "16 Zipf(1.0) labels, query a ^b* c (3-state min DFA), source = max out-degree"),
     "cfg3": ("^a (b|c)* d", "cfg3: R-MAT scale 24 (16,777,216 V), edge factor 16, 64 Zipf(1.0) labels, "
-                            "query ^a (b|c)* d (3-state min DFA), source = max out-degree"),
+                            "query ^a (b|c)* d (3-state min DFA), sources uniform over out-degree >= 1"),
     "cfg4": ("(a|b|c|d)*", "cfg4: Chung-Lu 90M V / 1.2B raw edges (exponent 2.1), 2,000 Zipf(1.1) labels, "
                            "query (a|b|c|d)* (1-state min DFA), source = max out-degree"),
     "cfg5": ("(a1 a2*) (a3 a4*) (a5 a6*) (a7 a8*) (a9 a10*) (a11 a12*) (a13 a14*) (a15 a16*)",
@@ -54,6 +59,13 @@ WORKLOADS = {
              "source = max out-degree"),
 }
 WORKLOAD = WORKLOADS[CONFIG][1]
+SOURCE_RULE = {
+    "cfg1": "vertex 0",
+    "cfg2": "highest out-degree vertex (ties: lowest id)",
+    "cfg3": "uniform over vertices with out-degree >= 1: datagen.pick_sources draws j = 0.. (seed 103)",
+    "cfg4": "uniform over vertices with out-degree >= 1: datagen.pick_sources draws j = 0.. (seed 104)",
+    "cfg5": "uniform over vertices with out-degree >= 1: datagen.pick_sources draws j = 0.. (seed 105)",
+}
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -64,6 +76,8 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["engine", "reference"], default="engine")
     ap.add_argument("--config", default=CONFIG)
+    ap.add_argument("--sources", type=int, default=8, help="sources per rank (uniform-source configs)")
+    ap.add_argument("--source", type=int, default=None, help="diagnostic: one fixed source instead")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--direction", choices=["auto", "push", "pull"], default="auto")
     ap.add_argument("--emit-mode", type=int, default=None, help="tuning: 0 inline, 1 plan, 2 adaptive")
@@ -75,7 +89,7 @@ def parse_args():
     ap.add_argument("--zero-copy", type=int, default=None, choices=[0, 1],
                     help="tuning: RPQ_TUNE_ZERO_COPY (statistics block written straight to pinned host memory)")
     ap.add_argument("--alpha", type=float, default=None, help="tuning: Beamer switch constant (default: engine's)")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between steps (diagnostic)")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no e2e leg, no CPU baseline, no clocks")
@@ -228,82 +242,135 @@ def algorithmic_bytes(te, x, pairs, levels, nstates, nv):
     return 4 * te + 8 * x + 8 * pairs + 2 * levels * math.ceil(nstates * nv / 8)
 
 
-def cpu_baseline(sg, nj, source, seconds, engine_reach):
-    """The reference algorithm's C restatement, one thread, bounded sample."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from oracle import OracleGraph, OracleQuery, oracle_port
-
-    og = OracleGraph(sg.nv, sg.nl, sg.src, sg.dst, sg.lab)
-    oq = OracleQuery(nj, sg.nl)
-    oq.prepare(og)
-    runs, total, te = 0, 0.0, None
-    reach = None
-    while total < seconds or runs == 0:
-        reach, st = oracle_port(og, oq, source, "hybrid", 100.0)
-        total += st["seconds"]
-        runs += 1
-    from oracle import oracle_bfs
-
-    _, bst = oracle_bfs(og, oq, source)
-    te = bst["te"]
+def workload_config(args, sg, sources, world):
+    """The `config` dict both arms print (identical keys and values)."""
     return {
-        "value": te * runs / total / 1e9,
-        "unit": UNIT,
-        "cores": 1,
-        "kind": "port",
-        "sample": (f"{CONFIG} {QUERY} from source {source}, {runs} sequential evaluations "
-                   f"({total:.1f} s) by oracle/rpq_oracle.c oracle_port (engine.py hybrid loop, "
-                   f"sorted-key sparse Boolean ops), 1 thread"),
-        "ms_per_query": 1e3 * total / runs,
-        "parity_with_engine": bool((reach == engine_reach).all()),
+        "workload": WORKLOAD, "vertices": sg.nv, "edges": sg.ne, "query": QUERY,
+        "sources": sources, "source_rule": SOURCE_RULE[args.config],
+        "l2": "flushed before every query (256 MiB write, outside the query events)",
+        "parallelism": (f"{world} GPUs, independent queries (each rank its own {len(sources)} sources)"
+                        if world > 1 else "1 GPU"),
     }
 
 
-def run_reference(args, rank, world):
-    if rank != 0:
-        return None
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from concurrent.futures import ThreadPoolExecutor
-
-    from oracle import OracleGraph, OracleQuery, oracle_bfs, oracle_port
+def bench_sources(sg, config, world, per_rank):
+    """BASELINE's source rule for the config; rank r of a weak-scaling run
+    takes its own `per_rank` draws (rank 0's are the same at every N)."""
     from paper_2412_10287_b200 import datagen
 
-    global QUERY, WORKLOAD
-    QUERY, WORKLOAD = WORKLOADS[args.config]
-    sg = datagen.generate(args.config)
-    nj = load_automaton(args.config, QUERY)
-    source = ranked_sources(sg, 1)[0]
+    if datagen.CONFIGS[config]["sources"] in ("zero", "max_out_degree"):
+        return ranked_sources(sg, world) if world > 1 else datagen.pick_sources(sg, config)
+    return datagen.pick_sources(sg, config, count=per_rank * world)
+
+
+def oracle_setup(sg, nj):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import OracleGraph, OracleQuery
+
     og = OracleGraph(sg.nv, sg.nl, sg.src, sg.dst, sg.lab)
     oq = OracleQuery(nj, sg.nl)
     oq.prepare(og)
-    _, bst = oracle_bfs(og, oq, source)
-    te = bst["te"]
+    return og, oq
+
+
+def cpu_baseline(og, oq, sources, te_by_source, seconds, engine_reach):
+    """The reference algorithm's C restatement (engine.py's hybrid loop), one
+    thread, a bounded sample: the bench's sources in order, cycled until
+    `seconds` of CPU work (at least one pass).  Every source's answer is
+    compared with the engine's (`parity_with_engine`)."""
+    from oracle import oracle_port
+
+    runs, total, te, parity = 0, 0.0, 0, True
+    while total < seconds or runs < len(sources):
+        s = sources[runs % len(sources)]
+        reach, st = oracle_port(og, oq, s, "hybrid", 100.0)
+        total += st["seconds"]
+        te += te_by_source[s]
+        if runs < len(sources):
+            parity &= bool((reach == engine_reach[s]).all())
+        runs += 1
+    return {
+        "value": te / total / 1e9,
+        "unit": UNIT,
+        "cores": 1,
+        "kind": "port",
+        "sample": (f"{args_config()} {QUERY}: {runs} sequential evaluations cycling over the bench's "
+                   f"{len(sources)} sources ({total:.1f} s) by oracle/rpq_oracle.c oracle_port "
+                   f"(engine.py hybrid loop, sorted-key sparse Boolean ops), 1 thread"),
+        "ms_per_query": 1e3 * total / runs,
+        "parity_with_engine": parity,
+        "parity_sources": len(sources),
+    }
+
+
+_CONFIG_NAME = [CONFIG]
+
+
+def args_config():
+    return _CONFIG_NAME[0]
+
+
+def select_workload(config):
+    global QUERY, WORKLOAD
+    QUERY, WORKLOAD = WORKLOADS[config]
+    _CONFIG_NAME[0] = config
+
+
+def run_reference(args, rank, world):
+    """The reference algorithm on the host cores: each step evaluates every
+    bench source concurrently, replicated to fill all host threads."""
+    if rank != 0:
+        return None
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle_bfs, oracle_port
+    from paper_2412_10287_b200 import datagen
+
+    select_workload(args.config)
+    sg = datagen.generate(args.config)
+    nj = load_automaton(args.config, QUERY)
+    all_sources = bench_sources(sg, args.config, world, args.sources)
+    sources = all_sources[: len(all_sources) // world]  # rank 0's share: the host runs one rank's work
+    og, oq = oracle_setup(sg, nj)
+    te = {s: oracle_bfs(og, oq, s)[1]["te"] for s in sources}
     threads = os.cpu_count() or 1
-    pool = ThreadPoolExecutor(max_workers=threads)
+    reps = max(1, threads // len(sources))
+    jobs = [s for _ in range(reps) for s in sources]
+    pool = ThreadPoolExecutor(max_workers=min(threads, len(jobs)))
 
     def step():
         t = time.perf_counter()
-        list(pool.map(lambda _: oracle_port(og, oq, source, "hybrid", 100.0), range(threads)))
+        list(pool.map(lambda s: oracle_port(og, oq, s, "hybrid", 100.0), jobs))
         return time.perf_counter() - t
 
     for _ in range(args.warmup):
         step()
     times = [step() for _ in range(args.steps)]
     total = sum(times)
-    value = threads * te * args.steps / total / 1e9
+    te_step = sum(te[s] for s in jobs)
+    value = te_step * args.steps / total / 1e9
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "vertices": sg.nv, "edges": sg.ne, "query": QUERY,
-                   "source": source, "te_per_query": te},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": (f"each step: {threads} concurrent evaluations of {QUERY} from "
-                                    f"source {source} (one per host thread) by "
-                                    "oracle/rpq_oracle.c oracle_port (hybrid loop)")},
+        "config": workload_config(args, sg, all_sources, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(threads, len(jobs)), "kind": "port",
+                         "sample": (f"each step: {len(jobs)} concurrent evaluations ({reps} x the "
+                                    f"{len(sources)} bench sources, one per host thread) of {QUERY} by "
+                                    "oracle/rpq_oracle.c oracle_port (engine.py hybrid loop)"),
+                         "te_per_step": te_step},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+
+
+def apply_tuning(P, pq, args):
+    pq.set_tuning(args.emit_mode, args.emit_inline_max)
+    lib = P._lib.engine()
+    for key, val, name in ((P._lib.TUNE_FLAGS, args.flags, "flags"), (P._lib.TUNE_DEFER, args.defer, "defer"),
+                           (P._lib.TUNE_ZERO_COPY, args.zero_copy, "zero_copy")):
+        if val is not None:
+            P.engine.raise_for_status(lib.rpq_query_set_tuning(pq.q, key, float(val)), name)
 
 
 def run_engine(args, rank, world, local_rank):
@@ -315,8 +382,7 @@ def run_engine(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    global QUERY, WORKLOAD
-    QUERY, WORKLOAD = WORKLOADS[args.config]
+    select_workload(args.config)
     sg = datagen.generate(args.config)
     if args.reorder:
         deg = np.bincount(sg.src, minlength=sg.nv) + np.bincount(sg.dst, minlength=sg.nv)
@@ -327,7 +393,11 @@ def run_engine(args, rank, world, local_rank):
     g = sg.labeled_graph()
     nj = load_automaton(args.config, QUERY)
     n = P.Automaton.from_json(nj)
-    source = ranked_sources(sg, world)[rank]
+    all_sources = bench_sources(sg, args.config, world, args.sources)
+    if args.source is not None:
+        all_sources = [args.source] * world
+    per = len(all_sources) // world
+    sources = all_sources[rank * per:(rank + 1) * per]
     pq = P.PreparedQuery(g, n, device=local_rank)
     # a dedicated (non-default) stream: the engine and the timing events share it
     stream = torch.cuda.Stream(dev)
@@ -335,27 +405,22 @@ def run_engine(args, rank, world, local_rank):
     handle = stream.cuda_stream
     assert handle, "need a real stream handle"
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    apply_tuning(P, pq, args)
 
-    pq.set_tuning(args.emit_mode, args.emit_inline_max)
-    if args.flags is not None:
-        P.engine.raise_for_status(P._lib.engine().rpq_query_set_tuning(pq.q, P._lib.TUNE_FLAGS, float(args.flags)), "flags")
-    if args.defer is not None:
-        P.engine.raise_for_status(P._lib.engine().rpq_query_set_tuning(pq.q, P._lib.TUNE_DEFER, float(args.defer)), "defer")
-    if args.zero_copy is not None:
-        P.engine.raise_for_status(P._lib.engine().rpq_query_set_tuning(pq.q, P._lib.TUNE_ZERO_COPY, float(args.zero_copy)),
-                                  "zero_copy")
-    # one untimed run for the work counts (exact TE, |P|, levels) of this query
+    # one untimed run per source for its work counts (exact TE, |P|, levels)
     alpha = args.alpha if args.alpha is not None else P.EngineOptions().alpha
-    pq.set_options(direction=args.direction, count_te=True, alpha=alpha)
-    pq.launch(source, -1.0, handle)
-    st0 = pq.wait()
-    pq.set_options(direction=args.direction, count_te=False, alpha=alpha)
-    per_state = pq.visited_counts()
     outdeg_q = np.bincount(pq.table.t_src, minlength=pq.table.nstates)
-    x = int((per_state * outdeg_q).sum())
-    te, pairs, iters = int(st0.te), int(st0.visited_pairs), int(st0.iterations)
-    b_alg = algorithmic_bytes(te, x, pairs, iters, pq.table.nstates, sg.nv)
-    engine_reach = pq.reach()
+    work = {}
+    for s in sources:
+        pq.set_options(direction=args.direction, count_te=True, alpha=alpha)
+        pq.launch(s, -1.0, handle)
+        st0 = pq.wait()
+        x = int((pq.visited_counts() * outdeg_q).sum())
+        te, pairs, iters = int(st0.te), int(st0.visited_pairs), int(st0.iterations)
+        work[s] = {"st0": st0, "te": te, "x": x, "pairs": pairs, "iters": iters,
+                   "bytes": algorithmic_bytes(te, x, pairs, iters, pq.table.nstates, sg.nv),
+                   "reach": pq.reach()}
+    pq.set_options(direction=args.direction, count_te=False, alpha=alpha)
 
     sampler = None
     if not args.profile:
@@ -364,47 +429,61 @@ def run_engine(args, rank, world, local_rank):
         sampler.start()
 
     for i in range(args.warmup):
-        flush.fill_(i & 0xFF)
-        pq.launch(source, -1.0, handle)
-        pq.wait()
+        for s in sources:
+            flush.fill_(i & 0xFF)
+            pq.launch(s, -1.0, handle)
+            pq.wait()
 
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in sources]
           for _ in range(args.steps)]
     launches = 0
-    level_ns = []  # per timed step: the kernel's own level stamps
+    level_ns = {s: [] for s in sources}  # per timed query: the kernel's own level stamps
     for k in range(args.steps):
-        if not args.no_flush:
-            flush.fill_(k & 0xFF)  # > L2: evicts the graph between steps (outside the events)
-        ev[k][0].record(stream)
-        pq.launch(source, -1.0, handle)
-        launches += 1
-        ev[k][1].record(stream)
-        st = pq.wait()
-        assert st.visited_pairs == pairs and st.iterations == iters
-        level_ns.append(list(st.level_ns[: min(iters + 1, 64)]))
+        for j, s in enumerate(sources):
+            if not args.no_flush:
+                flush.fill_((k + j) & 0xFF)  # > L2: evicts the graph between queries (outside the events)
+            ev[k][j][0].record(stream)
+            pq.launch(s, -1.0, handle)
+            launches += 1
+            ev[k][j][1].record(stream)
+            st = pq.wait()
+            w = work[s]
+            assert st.visited_pairs == w["pairs"] and st.iterations == w["iters"]
+            level_ns[s].append(list(st.level_ns[: min(w["iters"] + 1, 64)]))
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = sum(step_ms)
+    q_ms = {s: [ev[k][j][0].elapsed_time(ev[k][j][1]) for k in range(args.steps)] for j, s in enumerate(sources)}
+    total_ms = sum(sum(v) for v in q_ms.values())
+    te_step = sum(work[s]["te"] for s in sources)
+    b_step = sum(work[s]["bytes"] for s in sources)
 
     # e2e through the public API: automaton H2D + kernel + answer D2H per call
-    e2e_s = []
+    e2e_s, set_ms = [], []
     if not args.profile:
         opts = P.EngineOptions(timeout=math.inf, direction=args.direction, alpha=alpha)
         for _ in range(args.warmup):  # untimed, like the device leg (first call creates the query)
-            P.eval_ssr(g, n, source, opts)
+            for s in sources:
+                P.eval_ssr(g, n, s, opts)
         for k in range(args.steps):
-            flush.fill_(k & 0xFF)
-            torch.cuda.synchronize()
-            t = time.perf_counter()
-            res = P.eval_ssr(g, n, source, opts)
-            e2e_s.append(time.perf_counter() - t)
-            assert res.iterations == iters
-        assert np.array_equal(res.reach, engine_reach)
+            t_step = 0.0
+            for j, s in enumerate(sources):
+                flush.fill_((k + j) & 0xFF)
+                torch.cuda.synchronize()
+                t = time.perf_counter()
+                res = P.eval_ssr(g, n, s, opts)
+                t_step += time.perf_counter() - t
+                assert res.iterations == work[s]["iters"]
+                if k == 0:
+                    assert np.array_equal(res.reach, work[s]["reach"])
+                    # the reference's result type: set[int] built from the answer
+                    t = time.perf_counter()
+                    _ = res.reachable
+                    set_ms.append(1e3 * (time.perf_counter() - t))
+            e2e_s.append(t_step)
     clocks = sampler.stop() if sampler else None
 
     h2d, d2h_ctl = pq.io_bytes()
@@ -412,47 +491,54 @@ def run_engine(args, rank, world, local_rank):
     from paper_2412_10287_b200.multigpu import reduce_timing
 
     # max over ranks of the device time, sum over ranks of the product edges
-    total_max_ms, units = reduce_timing(total_ms, te * args.steps, dev)
+    total_max_ms, units = reduce_timing(total_ms, te_step * args.steps, dev)
     peak, peak_src = read_peaks()
-    per_level = per_level_roofline(st0, level_ns, x, pairs, pq.table.nstates, sg.nv, peak)
+    heavy = max(sources, key=lambda s: work[s]["te"])
+    hw = work[heavy]
+    per_level = per_level_roofline(hw["st0"], level_ns[heavy], hw["x"], hw["pairs"], pq.table.nstates,
+                                   sg.nv, peak)
     e2e_max_s, _ = reduce_timing(sum(e2e_s) if e2e_s else 0.0, 0, dev)
+    cfg = workload_config(args, sg, all_sources, world)
     pq.close()
     if rank != 0:
         return None
 
     value = units / (total_max_ms / 1e3) / 1e9
-    kernel_s = total_ms / args.steps / 1e3
-    achieved = b_alg / kernel_s / 1e9
+    kernel_s = total_ms / args.steps / 1e3  # one step = every source once
+    achieved = b_step / kernel_s / 1e9
+    nq = len(sources)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_max_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic",
-        "config": {
-            "workload": WORKLOAD, "vertices": sg.nv, "edges": sg.ne, "query": QUERY,
-            "automaton_states": pq.table.nstates, "sources": ranked_sources(sg, world),
-            "l2": "flushed between steps (256 MiB write, outside the step events)",
-            "parallelism": f"{world} independent queries (1 per GPU)" if world > 1 else "1 GPU",
-        },
+        "config": cfg,
         "per_query": {
-            "latency_ms_median": statistics.median(step_ms), "latency_ms_min": min(step_ms),
-            "te": te, "x": x, "visited_pairs": pairs, "iterations": iters,
-            "reach": int(st0.reach_count),
-            "level_new": list(st0.level_new[: iters + 1]),
-            "level_edges": list(st0.level_edges[: iters + 1]),
-            "level_dir": ["pull" if d else "push" for d in st0.level_dir[: iters]],
-            "level_end_us": [t / 1e3 for t in st0.level_ns[: iters + 1]],
-            "level_work_us": [t / 1e3 for t in st0.work_ns[: iters]],
-            "level_bar_us": [t / 1e3 for t in st0.bar_ns[: iters]],
+            "sources": sources,
+            "latency_ms_median": {str(s): statistics.median(q_ms[s]) for s in sources},
+            "latency_ms_median_all": statistics.median([t for s in sources for t in q_ms[s]]),
+            "te": {str(s): work[s]["te"] for s in sources},
+            "iterations": {str(s): work[s]["iters"] for s in sources},
+            "reach": {str(s): int(work[s]["st0"].reach_count) for s in sources},
+            "heaviest_source": heavy,
+            "heaviest": {
+                "latency_ms_median": statistics.median(q_ms[heavy]), "te": hw["te"], "x": hw["x"],
+                "visited_pairs": hw["pairs"], "iterations": hw["iters"],
+                "level_new": list(hw["st0"].level_new[: hw["iters"] + 1]),
+                "level_edges": list(hw["st0"].level_edges[: hw["iters"] + 1]),
+                "level_dir": ["pull" if d else "push" for d in hw["st0"].level_dir[: hw["iters"]]],
+            },
             "direction_policy": args.direction,
         },
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": ncu_traffic(args.config),
             "kernel": "rpq_ssr_kernel (persistent, one launch per query)",
-            "algorithmic_bytes_per_launch": b_alg, "peak_source": peak_src,
-            "note": "algorithmic bytes of SURVEY.md §8(d) per query / mean step time",
-            "per_level": per_level,
+            "algorithmic_bytes_per_step": b_step, "queries_per_step": nq,
+            "algorithmic_bytes_per_launch": b_step / nq, "peak_source": peak_src,
+            "note": ("SURVEY.md §8(d) algorithmic bytes summed over the step's queries / the step's summed "
+                     "query times; traffic = ncu dram bytes of one launch of the heaviest source"),
+            "per_level_heaviest_source": per_level,
             # the frontier step with the most edges (north_star's "frontier step" figure)
             "densest_level_frac": max(per_level, key=lambda lv: lv["edges"])["frac"] if per_level else None,
         },
@@ -461,10 +547,15 @@ def run_engine(args, rank, world, local_rank):
     }
     if e2e_s:
         out["e2e"] = {"value": units / e2e_max_s / 1e9, "unit": UNIT,
-                      "h2d_bytes_per_step": h2d + 4, "d2h_bytes_per_step": d2h,
-                      "latency_ms_median": 1e3 * statistics.median(e2e_s)}
+                      "h2d_bytes_per_step": nq * (h2d + 4), "d2h_bytes_per_step": nq * d2h,
+                      "latency_ms_median_per_query": 1e3 * statistics.median(e2e_s) / nq,
+                      "reachable_set_ms_per_query": statistics.mean(set_ms) if set_ms else None,
+                      "note": ("eval_ssr per source with host buffers (answer bitmap read back); "
+                               "reachable_set_ms = building the reference's set[int] from it, not in value")}
     if world == 1 and not args.no_cpu_baseline and not args.profile:
-        out["cpu_baseline"] = cpu_baseline(sg, nj, source, args.cpu_seconds, engine_reach)
+        og, oq = oracle_setup(sg, nj)
+        out["cpu_baseline"] = cpu_baseline(og, oq, sources, {s: work[s]["te"] for s in sources},
+                                           args.cpu_seconds, {s: work[s]["reach"] for s in sources})
     return out
 
 

@@ -1231,6 +1231,12 @@ int rpq_query_step_device(rpq_query* q, const uint32_t* d_m, uint32_t* d_p, uint
         CUDA_TRY(cudaStreamSynchronize(q->last_stream));
         q->bar_next = q->h_ctl->bar;
         q->inflight = false;
+        // the previous step's status would be overwritten by this run: a
+        // failed step (queue overflow, barrier abort) fails the chain here
+        const int prev = q->h_ctl->status;
+        if (prev == ST_OVERFLOW) return fail(RPQ_ECUDA, "internal: frontier queue capacity exceeded (previous step)");
+        if (prev == ST_DEADLOCK) return fail(RPQ_ECUDA, "internal: grid barrier spin limit exceeded (previous step)");
+        if (prev != 0) return fail(RPQ_ECUDA, "previous step failed with kernel status " + std::to_string(prev));
     }
     RunArgs ra{};
     ra.mode = 1;

@@ -1375,7 +1375,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
         __syncthreads();  // s_task
         unsigned long long nnew = 0, nedge = 0;
         // emit F_{L+1}'s queue now (at discovery) or later from F's bitmap
-        const bool emit_inline = dir == DIR_PUSH && !s_view.defer &&
+        // (a step-mode run stops after this level: nobody expands F_{L+1}'s queue)
+        const bool emit_inline = dir == DIR_PUSH && !s_view.defer && !step_mode &&
                                  (s_run.emit_mode == 0 ||
                                   (s_run.emit_mode == 2 && s_view.nfront < s_run.emit_inline_max));
         const int queued = emit_inline ? 1 : 0;
@@ -1574,7 +1575,11 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
             if (threadIdx.x == 0) {
                 s_view.done = 1;
                 s_view.status = 1;  // (no answer projection in step mode)
-                if (cta0) ctl->iterations = 1;
+                if (cta0) {
+                    ctl->iterations = 1;
+                    // no decision follows the step: record a barrier abort here
+                    if (ldcg(&ctl->abort)) ctl->status = ST_DEADLOCK;
+                }
             }
             __syncthreads();
             break;

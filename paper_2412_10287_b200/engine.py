@@ -209,11 +209,14 @@ def _run(g, n, source, opts, tag, *, want_stats=False):
     lib = _lib.engine()
     q = dg.acquire_query(table)
     try:
-        # _Clock.check(0) at the top of the first iteration (engine.py:87-89)
+        # _Clock.check(0) at the top of the first iteration (engine.py:87-89).
+        # The masked loop (`while m.nnz`, engine.py:157) never reaches it when
+        # the automaton has no start state, so that case returns normally.
         remaining = opts.timeout - (time.monotonic() - t0)
-        if remaining < 0 or opts.timeout == 0:
+        first_check = not (tag == "masked" and table.starts.size == 0)
+        if first_check and (remaining < 0 or opts.timeout <= 0):
             raise QueryTimeout(time.monotonic() - t0, 0)
-        budget = -1.0 if math.isinf(remaining) else remaining
+        budget = -1.0 if math.isinf(remaining) else max(remaining, 0.0)
         words = np.empty((g.num_vertices + 31) // 32, dtype=np.uint32)
         stats = _thread_stats()  # read (or copied out) before this thread's next call
         # options, run, wait and the answer bitmap in one C call (raw addresses)
@@ -323,9 +326,11 @@ def eval_ssr_batch(g, n, sources, opts, *, stats=None):
         bits = np.zeros((_lib.BATCH, max(words, 1)), dtype=np.uint32)
         for b0 in range(0, len(sources), _lib.BATCH):
             chunk = np.ascontiguousarray(sources[b0:b0 + _lib.BATCH], dtype=np.int32)
-            if opts.timeout == 0 and table.starts.size:
-                raise QueryTimeout(time.monotonic() - t0, 0)  # _Clock.check(0), engine.py:87-89
-            budget = -1.0 if math.isinf(opts.timeout) else float(opts.timeout)
+            # _Clock.check(0), engine.py:87-89: a zero or negative budget has
+            # already expired (the C side reads a negative budget as "none")
+            if opts.timeout <= 0 and table.starts.size:
+                raise QueryTimeout(time.monotonic() - t0, 0)
+            budget = -1.0 if math.isinf(opts.timeout) else max(float(opts.timeout), 0.0)
             raise_for_status(lib.rpq_query_run_batch(q, chunk.size, _lib.ptr(chunk, ctypes.c_int32), budget,
                                                      None), "rpq_query_run_batch")
             st = _lib.RpqBatchStats()
@@ -407,7 +412,8 @@ class PreparedQuery:
         self.dg = device_graph(g, device)
         self.table = transition_table(n, g.num_labels)
         self.dg.ensure_labels(self.table.labels)
-        self.q = self.dg.acquire_query(self.table)
+        # a private handle: set_options / set_tuning change it for good
+        self.q = self.dg.acquire_query(self.table, private=True)
         self.nv = int(g.num_vertices)
 
     def set_options(self, direction="auto", count_te=False, alpha=4.0):
@@ -488,7 +494,7 @@ class PreparedQuery:
 
     def close(self):
         if self.q is not None:
-            self.dg.release_query(self.table, self.q)
+            self.dg.destroy_query(self.q)
             self.q = None
 
     def __enter__(self):

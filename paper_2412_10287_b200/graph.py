@@ -309,12 +309,17 @@ class DeviceGraph:
         return int(_lib.engine().rpq_graph_device_bytes(self.handle))
 
     # -- query objects (device workspaces), pooled per transition table -------
-    def acquire_query(self, table):
+    def acquire_query(self, table, private=False):
+        """A query handle for ``table``: from the per-table pool, or (private)
+        a fresh one the caller may retune and must give back with
+        ``destroy_query`` -- never to the pool, so that eval_ssr never
+        inherits a PreparedQuery's tuning."""
         key = table.key
-        with self._lock:
-            pool = self._queries.setdefault(key, [])
-            if pool:
-                return pool.pop()
+        if not private:
+            with self._lock:
+                pool = self._queries.setdefault(key, [])
+                if pool:
+                    return pool.pop()
         lib = _lib.engine()
         h = ctypes.c_void_p()
         rc = lib.rpq_query_create(
@@ -330,6 +335,10 @@ class DeviceGraph:
     def release_query(self, table, q):
         with self._lock:
             self._queries.setdefault(table.key, []).append(q)
+
+    def destroy_query(self, q):
+        if q:
+            _lib.engine().rpq_query_destroy(q)
 
 
 _DEVICE_GRAPHS = weakref.WeakKeyDictionary()

@@ -350,10 +350,12 @@ def eval_ssr_partitioned(g, n, source, opts=None, group=None):
     EvalResult as eval_ssr (iterations counted like the masked loop)."""
     import torch
 
-    from .engine import EngineOptions, EvalResult, _check_vertex
+    from .engine import _SSR_EVALUATORS, EngineOptions, EvalResult, _check_vertex, _iterations_for
 
     opts = opts or EngineOptions()
     opts.validate()
+    if opts.algorithm not in _SSR_EVALUATORS:  # engine.py:246-250
+        raise ValueError(f"algorithm {opts.algorithm!r} does not evaluate compiled automata")
     _check_vertex(g, source)
     ex = DistExchange(group)
     table = transition_table(n, g.num_labels)
@@ -366,4 +368,7 @@ def eval_ssr_partitioned(g, n, source, opts=None, group=None):
                                    table.finals.tolist(), int(source), opts.timeout, bits=True)
     finally:
         sh.step.close()
-    return EvalResult(None, its, time.monotonic() - t0, "masked", bits=words, nv=g.num_vertices)
+    # the device loop counts like the masked one; each algorithm's own count
+    # follows from it (engine._iterations_for), and the tag is the caller's
+    return EvalResult(None, _iterations_for(opts.algorithm, its, table.starts.size), time.monotonic() - t0,
+                      opts.algorithm, bits=words, nv=g.num_vertices)
