@@ -32,6 +32,8 @@ def rank_names(nl, style="letters"):
 
 CHAIN16 = " ".join(f"(a{2 * i + 1} a{2 * i + 2}*)" for i in range(8))
 CHAIN16_TWOWAY = " ".join(f"(a{2 * i + 1} ^a{2 * i + 2}*)" for i in range(8))
+# the two-way variant on even labels in both directions: 25 states unminimized
+CHAIN16_BOTHWAY = " ".join(f"(a{2 * i + 1} (a{2 * i + 2}|^a{2 * i + 2})*)" for i in range(8))
 
 CONFIGS = {
     # cfg1: Erdos-Renyi 10k / 100k, 4 uniform labels, query a b*, source 0
@@ -50,7 +52,7 @@ CONFIGS = {
                  sources="uniform_outdeg", nsources=32),
     # cfg5: R-MAT scale 22, 32 labels, 8-group chain (+ two-way variant), 1,024 sources
     "cfg5": dict(kind="rmat", scale=22, ef=16, nl=32, zipf=1.0, seed=5, names="a_index",
-                 queries=[CHAIN16, CHAIN16_TWOWAY], sources="uniform_outdeg", nsources=1024),
+                 queries=[CHAIN16, CHAIN16_TWOWAY, CHAIN16_BOTHWAY], sources="uniform_outdeg", nsources=1024),
 }
 
 

@@ -34,3 +34,41 @@ def expected_reach(rec, nv):
 def unpack_bits(b64, nv):
     raw = np.frombuffer(base64.b64decode(b64), dtype=np.uint8)
     return np.unpackbits(raw, bitorder="little")[:nv].astype(np.uint8)
+
+
+def desk_bench():
+    """The reference's desk-scale benchmark (test_acceptance.py:238-335):
+    (golden record, graph arrays) from tests/golden/desk_bench.json.gz and
+    desk_graph.npz (written by make_golden.py desk)."""
+    import os
+
+    from conftest import GOLDEN, load_golden
+
+    rec = load_golden("desk_bench.json.gz")
+    z = np.load(os.path.join(GOLDEN, "desk_graph.npz"))
+    nl = len(rec["labels"])
+    csr = [(z[f"indptr_{l}"].astype(np.int64), z[f"indices_{l}"].astype(np.int64)) for l in range(nl)]
+    return rec, csr
+
+
+def desk_host_graph(rec, csr):
+    nv = rec["nv"]
+    return LabeledGraph(nv, rec["labels"], [CsrMatrix(nv, nv, ip, ix) for ip, ix in csr])
+
+
+def desk_oracle_graph(rec, csr):
+    from oracle import OracleGraph
+
+    src, dst, lab = [], [], []
+    for l, (ip, ix) in enumerate(csr):
+        src.append(np.repeat(np.arange(rec["nv"], dtype=np.int32), np.diff(ip)))
+        dst.append(ix.astype(np.int32))
+        lab.append(np.full(ix.size, l, dtype=np.int32))
+    return OracleGraph(rec["nv"], len(csr), np.concatenate(src), np.concatenate(dst), np.concatenate(lab))
+
+
+def answer_digest(reach):
+    """sha256 of the comma-joined sorted answer ids (test_acceptance.py:338-351's format)."""
+    import hashlib
+
+    return hashlib.sha256(",".join(str(v) for v in np.flatnonzero(reach).tolist()).encode()).hexdigest()

@@ -8,6 +8,7 @@ paper_2412_10287_b200/data/, and the tests read only those files.
     python tests/golden/make_golden.py automata    # compiled config queries
     python tests/golden/make_golden.py config cfg1 cfg2 [cfg3 cfg5 ...]
     python tests/golden/make_golden.py plan        # eval_plan (engine.py:292-390) on the same streams
+    python tests/golden/make_golden.py desk        # test_acceptance.py criteria 7/8: desk-scale bench
 
 Instance sources (each replays the reference test's own RNG stream):
   engine_random_15   test_engine.py:403-415 (seed 15, 40 instances, unknown label "zz")
@@ -338,6 +339,72 @@ def gen_config(cfg, sources=None, queries=None, minimize=True, count=None):
     return {"config": cfg, "nv": sg.nv, "ne": sg.ne, "digest": sg.digest(), "records": records}
 
 
+def gen_desk():
+    """The reference's desk-scale benchmark analogue (test_acceptance.py:238-335,
+    criterion 7) and its determinism bytes (criterion 8, :338-369): the same
+    generated graph (cli.generate_edges, seed 0xBE, 1e5 vertices, ~1e6 edges
+    with the test's label skew) and the same 1,000-entry workload (rng 0xC7:
+    10 families x {ssr, sdr} x 50 endpoints), evaluated by the reference with
+    each SSR algorithm.  Writes the graph in index space (desk_graph.npz) and
+    per entry the answer count, a sha256 of the sorted answer ids and every
+    algorithm's iteration count (desk_bench.json.gz)."""
+    import hashlib
+    import io
+
+    import test_acceptance as TA
+    from rpq.cli import generate_edges, parse_workload
+    from rpq.query_compiler import reverse as ref_reverse
+
+    buf = io.StringIO()
+    generate_edges(TA._NUM_VERTICES, sorted(TA._desk_scale_counts().items()), 0xBE, buf)
+    graph = helpers.load_text(buf.getvalue())
+    rng = random.Random(0xC7)
+    lines = []
+    for fam, pattern in enumerate(TA._QUERY_FAMILIES, start=1):
+        for mode in ("ssr", "sdr"):
+            for k in range(TA._ENDPOINTS_PER_COMBO):
+                endpoint = rng.choice(graph.vertices)
+                lines.append(f"q{fam:02d}-{mode}-{k:02d}\t{mode}\t{endpoint}\t{pattern}")
+    entries = parse_workload(io.StringIO("\n".join(lines) + "\n"))
+    arrays = {"nv": np.array([graph.num_vertices], dtype=np.int64)}
+    for l in range(graph.num_labels):
+        f = graph.forward[l]
+        arrays[f"indptr_{l}"] = np.asarray(f.indptr, dtype=np.int32)
+        arrays[f"indices_{l}"] = np.asarray(f.indices, dtype=np.int32)
+    np.savez_compressed(os.path.join(HERE, "desk_graph.npz"), **arrays)
+    autos = {pattern: nfa_json(ref_compile(parse_query(pattern), graph.label_ids))
+             for pattern in TA._QUERY_FAMILIES}
+    rows = []
+    chunks = []
+    t = time.time()
+    for e in entries:
+        n = ref_compile(parse_query(e.pattern), graph.label_ids)
+        v = graph.vertex_index(e.endpoint)
+        nn = n if e.mode == "ssr" else ref_reverse(n)
+        its = {}
+        reach = None
+        for alg, fn in (("masked", eval_ssr_masked), ("no_mask", eval_ssr_no_mask),
+                        ("hybrid", eval_ssr_hybrid)):
+            r = fn(graph, nn, v, EngineOptions(timeout=60.0))
+            its[alg] = r.iterations
+            assert reach is None or reach == r.reachable
+            reach = r.reachable
+        # criterion 8's bytes: eval_ssr / eval_sdr with the hybrid default
+        h = (eval_ssr if e.mode == "ssr" else eval_sdr)(graph, n, v, EngineOptions(algorithm="hybrid",
+                                                                                   timeout=60.0))
+        assert h.reachable == reach
+        ids = ",".join(str(x) for x in sorted(reach))
+        chunks.append(f"{e.id}:{ids}")
+        rows.append({"id": e.id, "mode": e.mode, "pattern": e.pattern, "vertex": v,
+                     "count": len(reach), "sha256": hashlib.sha256(ids.encode()).hexdigest(),
+                     "iterations": its})
+    c8 = hashlib.sha256("\n".join(chunks).encode()).hexdigest()
+    print(f"desk bench: {len(rows)} entries in {time.time() - t:.1f}s; criterion-8 sha256 {c8}")
+    return {"nv": graph.num_vertices, "labels": list(graph.labels), "automata": autos,
+            "entries": rows, "criterion8_sha256": c8,
+            "num_edges": int(sum(graph.forward[l].nnz for l in range(graph.num_labels)))}
+
+
 def main():
     what = sys.argv[1] if len(sys.argv) > 1 else "random"
     if what == "random":
@@ -352,6 +419,12 @@ def main():
         with gzip.open(path, "wt") as fh:
             json.dump(out, fh)
         print(f"wrote {len(out)} plan cases to {path}")
+    elif what == "desk":
+        out = gen_desk()
+        path = os.path.join(HERE, "desk_bench.json.gz")
+        with gzip.open(path, "wt") as fh:
+            json.dump(out, fh)
+        print(f"wrote {path}")
     elif what == "steps":
         out = gen_steps()
         path = os.path.join(HERE, "step_update.json.gz")

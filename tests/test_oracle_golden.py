@@ -118,3 +118,28 @@ def test_port_timeout(reference_instances):
         oracle_port(g, q, 0, "masked", timeout=0.0)
     reach, st = oracle_port(g, q, 0, "masked", timeout=math.inf)
     assert reach.sum() == nv and st["iterations"] == nv + 0  # 3000 steps + final empty one
+
+
+def test_desk_bench_oracle():
+    """Criterion 7's 1,000-entry workload (test_acceptance.py:238-335): both
+    oracle entry points reproduce the reference's answers (sha256 of the
+    sorted ids) and every algorithm's iteration count."""
+    from fixtures import answer_digest, desk_bench, desk_oracle_graph
+
+    rec, csr = desk_bench()
+    assert len(rec["entries"]) == 1000 and rec["num_edges"] > 900_000
+    og = desk_oracle_graph(rec, csr)
+    nl = len(rec["labels"])
+    queries = {}
+    for e in rec["entries"]:
+        key = (e["pattern"], e["mode"])
+        if key not in queries:
+            nj = rec["automata"][e["pattern"]]
+            queries[key] = OracleQuery(nj if e["mode"] == "ssr" else _reverse_json(nj), nl)
+        oq = queries[key]
+        reach, st = oracle_bfs(og, oq, e["vertex"])
+        assert int(reach.sum()) == e["count"] and answer_digest(reach) == e["sha256"], e["id"]
+        assert st["iterations"] == e["iterations"]["masked"], e["id"]
+        for alg in ("no_mask", "hybrid"):
+            r2, s2 = oracle_port(og, oq, e["vertex"], alg)
+            assert np.array_equal(r2, reach) and s2["iterations"] == e["iterations"][alg], (e["id"], alg)
