@@ -1,4 +1,6 @@
-"""Break down the host-side cost of one eval_ssr call on cfg2."""
+"""Break down the host-side cost of one eval_ssr call.
+
+    python tools/e2e_probe.py [cfg2] [source]   (default source: the config's first)"""
 import json
 import math
 import sys
@@ -14,13 +16,15 @@ from paper_2412_10287_b200 import _lib, datagen
 from paper_2412_10287_b200.engine import _table_for, bits_to_reach
 from paper_2412_10287_b200.graph import device_graph
 
-sg = datagen.generate("cfg2")
+CFG = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+sg = datagen.generate(CFG)
 g = sg.labeled_graph()
-nj = json.load(open("paper_2412_10287_b200/data/config_automata.json"))["cfg2"]["a ^b* c|min"]
+SRC = int(sys.argv[2]) if len(sys.argv) > 2 else int(datagen.pick_sources(sg, CFG, count=1)[0])
+nj = json.load(open("paper_2412_10287_b200/data/config_automata.json"))[CFG][datagen.CONFIGS[CFG]["queries"][0] + "|min"]
 n = P.Automaton.from_json(nj)
 opts = P.EngineOptions(timeout=math.inf)
 for _ in range(5):
-    P.eval_ssr(g, n, 0, opts)
+    P.eval_ssr(g, n, SRC, opts)
 lib = _lib.engine()
 T = {}
 
@@ -29,14 +33,14 @@ def tick(k, t):
     T.setdefault(k, []).append(time.perf_counter() - t)
 
 
-for _ in range(50):
-    t = time.perf_counter(); P.eval_ssr(g, n, 0, opts); tick("eval_ssr total", t)
+for _ in range(20):
+    t = time.perf_counter(); P.eval_ssr(g, n, SRC, opts); tick("eval_ssr total", t)
     t = time.perf_counter(); dg = device_graph(g); tick("device_graph", t)
     t = time.perf_counter(); table = _table_for(n, g.num_labels); tick("table", t)
     t = time.perf_counter(); dg.ensure_labels(table.labels); tick("ensure_labels", t)
     t = time.perf_counter(); q = dg.acquire_query(table); tick("acquire", t)
     t = time.perf_counter(); lib.rpq_query_set_options(q, 0, 0, 4.0); lib.rpq_query_set_output(q, 1); tick("set_opts", t)
-    t = time.perf_counter(); lib.rpq_query_run(q, 0, -1.0, None); tick("run(enqueue)", t)
+    t = time.perf_counter(); lib.rpq_query_run(q, SRC, -1.0, None); tick("run(enqueue)", t)
     tq = time.perf_counter()
     st = _lib.RpqStats()
     t = time.perf_counter(); lib.rpq_query_wait(q, ctypes.byref(st)); tick("wait", t); tick("enqueue->done", tq)
@@ -48,7 +52,7 @@ for _ in range(50):
     words2 = np.empty((g.num_vertices + 31) // 32, dtype=np.uint32)
     q = dg.acquire_query(table)
     t = time.perf_counter()
-    lib.rpq_query_eval(q, 0, -1.0, 0, 0, 4.0, 1, ctypes.byref(st), _lib.ptr(words2, ctypes.c_uint32), words2.size)
+    lib.rpq_query_eval(q, SRC, -1.0, 0, 0, 4.0, 1, ctypes.byref(st), _lib.ptr(words2, ctypes.c_uint32), words2.size)
     tick("rpq_query_eval (fused C)", t)
     dg.release_query(table, q)
 for k, v in T.items():
