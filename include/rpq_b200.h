@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define RPQ_ABI_VERSION 1
+#define RPQ_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define RPQ_API __attribute__((visibility("default")))
@@ -190,7 +190,8 @@ RPQ_API int rpq_query_wait(rpq_query* q, rpq_stats* stats);
 RPQ_API int rpq_query_eval(rpq_query* q, int32_t source, double timeout_s, int32_t direction, int32_t count_te,
                            double alpha, int32_t allow_small, rpq_stats* stats, uint32_t* reach_words,
                            int64_t nwords);
-/* Device pointer to the uint8[num_vertices] answer of the last run. */
+/* Device pointer to the uint8[num_vertices] answer of the last run (expanded
+ * from the answer bitmap on the run's stream on first request). */
 RPQ_API int rpq_query_reach_device(rpq_query* q, uint8_t** d_reach);
 /* Copy the answer of the last run to host (uint8[num_vertices], 1 = reachable). */
 RPQ_API int rpq_query_copy_reach(rpq_query* q, uint8_t* host_reach);
@@ -223,6 +224,14 @@ RPQ_API int rpq_query_step_device(rpq_query* q, const uint32_t* d_m, uint32_t* d
  * answer bitmap (ceil(nv/32) uint32 words, bit v%32 of word v/32) into pinned
  * host memory as part of every run, ready after rpq_query_wait. */
 RPQ_API int rpq_query_set_output(rpq_query* q, int32_t mode);
+/* Pinned, device-mapped host memory for answers (cudaHostAlloc mapped |
+ * portable).  An answer buffer passed to rpq_query_eval that lies inside such
+ * a block is written by the kernel epilogue directly over PCIe: no copy node
+ * and no host-side memcpy (the eval_ssr fast path's result arrays).  Replaces
+ * nothing in the reference (its answers are Python sets built by
+ * _project_finals, engine.py:112-114); rpq_host_free releases a block. */
+RPQ_API int rpq_host_alloc(int64_t bytes, void** out);
+RPQ_API int rpq_host_free(void* p);
 /* The answer of the last run as a bitmap (host copy). */
 RPQ_API int rpq_query_copy_reach_bits(rpq_query* q, uint32_t* host_words, int64_t nwords);
 /* Copy the full visited matrix P (nstates rows x ceil(nv/32) uint32 words). */

@@ -25,6 +25,7 @@ DIR_PUSH = 1
 DIR_PULL = 2
 
 STATS_LEVELS = 64
+ABI_VERSION = 2  # include/rpq_b200.h RPQ_ABI_VERSION
 
 # rpq_query_set_tuning keys (include/rpq_b200.h RPQ_TUNE_*)
 TUNE_EMIT_MODE = 0
@@ -156,6 +157,8 @@ ENGINE_SIGNATURES = {
     "rpq_query_copy_visited": (c_i32, [c_vp, P_u32, c_i64]),
     "rpq_query_step": (c_i32, [c_vp, P_u32, P_u32, c_i64, P_u32]),
     "rpq_query_set_output": (c_i32, [c_vp, c_i32]),
+    "rpq_host_alloc": (c_i32, [c_i64, ctypes.POINTER(c_vp)]),
+    "rpq_host_free": (c_i32, [c_vp]),
     "rpq_query_copy_reach_bits": (c_i32, [c_vp, P_u32, c_i64]),
     "rpq_query_io_bytes": (c_i32, [c_vp, P_i64, P_i64]),
     "rpq_query_destroy": (c_i32, [c_vp]),
@@ -215,7 +218,7 @@ def engine():
                         "`python -m paper_2412_10287_b200._build` (there is no CPU fallback)"
                     )
                 lib = _bind(_build.ENGINE_SO, ENGINE_SIGNATURES)
-                if lib.rpq_abi_version() != 1:
+                if lib.rpq_abi_version() != ABI_VERSION:
                     raise NativeLibraryMissing("librpq_b200.so ABI version mismatch")
                 _engine = lib
     return _engine

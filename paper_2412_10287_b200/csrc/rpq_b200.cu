@@ -47,6 +47,21 @@ int cuda_fail(cudaError_t e, const char* what) {
         if (e_ != cudaSuccess) return cuda_fail(e_, #expr); \
     } while (0)
 
+// Pinned, mapped host blocks handed out by rpq_host_alloc: base -> bytes.
+// A run whose answer buffer lies inside one has the kernel write the answer
+// there directly (no copy node, no host memcpy).
+std::mutex g_host_mu;
+std::map<uintptr_t, size_t> g_host_blocks;
+
+bool host_block_covers(const void* ptr, size_t bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(ptr);
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    auto it = g_host_blocks.upper_bound(a);
+    if (it == g_host_blocks.begin()) return false;
+    --it;
+    return a >= it->first && a + bytes <= it->first + it->second;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -104,9 +119,12 @@ struct rpq_query {
     uint32_t* d_reach_bits = nullptr;
     uint32_t* h_reach_bits = nullptr;  // pinned; filled by run() when output_mode == 1
     int output_mode = 0;
+    uint32_t* run_out_bits = nullptr;  // next run's caller-owned pinned answer buffer (rpq_query_eval)
+    bool out_direct = false;           // the last run wrote its answer there, not to h_reach_bits
+    bool reach_stale = true;           // d_reach (uint8) not yet expanded from d_reach_bits
 
-    cudaGraphExec_t graph = nullptr;  // captured run sequence (per output mode)
-    int graph_mode = -1;
+    cudaGraphExec_t graphs[4] = {nullptr, nullptr, nullptr, nullptr};  // captured run per variant
+    cudaGraphExec_t graph = nullptr;  // the current variant's (one of graphs[])
     bool graph_failed = false;
     bool inflight = false;
     unsigned long long shard_segcap = 0, shard_buncap = 0, ovf_segcap = 0, ovf_buncap = 0;
@@ -402,7 +420,8 @@ void free_query_buffers(rpq_query* q) {
     if (q->h_bargs) cudaFreeHost(q->h_bargs);
     if (q->d_bout) cudaFree(q->d_bout);
 
-    if (q->graph) cudaGraphExecDestroy(q->graph);
+    for (auto& gx : q->graphs)
+        if (gx) cudaGraphExecDestroy(gx);
     if (q->ev0) cudaEventDestroy(q->ev0);
     if (q->ev1) cudaEventDestroy(q->ev1);
     if (q->own_stream) cudaStreamDestroy(q->own_stream);
@@ -816,7 +835,11 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
         QTRY(cudaMemcpy(q->d_slot_nnz, q->slot_nnz.data(), q->slot_nnz.size() * sizeof(unsigned long long),
                         cudaMemcpyHostToDevice));
     // large state spaces: the 32-warp variant (more loads in flight); small: 24 warps
-    const bool large = (long long)nstates * (long long)g->nv >= kLargePairs;
+    bool large = (long long)nstates * (long long)g->nv >= kLargePairs;
+    if (const char* ev = std::getenv("RPQ_KERNEL_THREADS")) {  // experiments: force a variant
+        if (std::atoi(ev) == kThreads) large = false;
+        if (std::atoi(ev) == kThreadsLarge) large = true;
+    }
     q->nthreads = large ? kThreadsLarge : kThreads;
     q->smem = kStageBytes(q->nthreads) + q->slots.size() * sizeof(Slot) + T.size() * sizeof(int32_t) + 16;
     const void* kfn = large ? (const void*)ssr_kernel<kThreadsLarge> : (const void*)ssr_kernel<kThreads>;
@@ -932,11 +955,8 @@ cudaError_t enqueue_run(rpq_query* q, cudaStream_t st, const Params* override = 
 // per run.  Falls back to direct launches if capture is not possible.
 void build_graph(rpq_query* q) {
     const int variant = q->output_mode | (use_small(q) ? 2 : 0);
-    if (q->graph && q->graph_mode == variant) return;
-    if (q->graph) {
-        cudaGraphExecDestroy(q->graph);
-        q->graph = nullptr;
-    }
+    q->graph = q->graphs[variant];
+    if (q->graph) return;
     cudaGraph_t g = nullptr;
     if (cudaStreamBeginCapture(q->own_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
         cudaGetLastError();
@@ -946,14 +966,23 @@ void build_graph(rpq_query* q) {
     cudaError_t e = enqueue_run(q, q->own_stream, nullptr, use_small(q));
     cudaError_t e2 = cudaStreamEndCapture(q->own_stream, &g);
     if (e != cudaSuccess || e2 != cudaSuccess || !g ||
-        cudaGraphInstantiate(&q->graph, g, 0) != cudaSuccess) {
+        cudaGraphInstantiate(&q->graphs[variant], g, 0) != cudaSuccess) {
         cudaGetLastError();
-        q->graph = nullptr;
+        q->graphs[variant] = nullptr;
         q->graph_failed = true;
-    } else {
-        q->graph_mode = variant;
     }
+    q->graph = q->graphs[variant];
     if (g) cudaGraphDestroy(g);
+}
+
+// Captured runs hold the parameters of their capture: drop them all.
+void drop_graphs(rpq_query* q) {
+    for (auto& gx : q->graphs)
+        if (gx) {
+            cudaGraphExecDestroy(gx);
+            gx = nullptr;
+        }
+    q->graph = nullptr;
 }
 
 }  // namespace
@@ -977,11 +1006,7 @@ int rpq_query_set_tuning(rpq_query* q, int32_t key, double value) {
                 q->bar_next = q->h_ctl->bar;
                 q->inflight = false;
             }
-            if (q->graph) {  // the captured run holds the old parameters and nodes
-                cudaGraphExecDestroy(q->graph);
-                q->graph = nullptr;
-                q->graph_mode = -1;
-            }
+            drop_graphs(q);  // the captured runs hold the old parameters and nodes
             return RPQ_OK;
         case RPQ_TUNE_DEFER:
             if (!(value >= 0) || value > 1e6) return fail(RPQ_EINVAL, "defer factor must be >= 0");
@@ -1010,11 +1035,7 @@ int rpq_query_set_tuning(rpq_query* q, int32_t key, double value) {
                 CUDA_TRY(cudaMalloc(&q->d_trace, bytes));
                 CUDA_TRY(cudaMemset(q->d_trace, 0, bytes));
             }
-            if (q->graph) {  // the captured run holds the old parameters
-                cudaGraphExecDestroy(q->graph);
-                q->graph = nullptr;
-                q->graph_mode = -1;
-            }
+            drop_graphs(q);  // the captured runs hold the old parameters
             return RPQ_OK;
         }
         default:
@@ -1045,6 +1066,11 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     ra.dir_mode = q->dir_mode;
     ra.count_te = q->count_te;
     ra.alpha = q->alpha;
+    // the caller's pinned answer buffer (grid kernel only; the single-CTA
+    // kernel's answer goes through h_reach_bits)
+    ra.out_bits = use_small(q) ? nullptr : q->run_out_bits;
+    q->out_direct = ra.out_bits != nullptr;
+    q->reach_stale = true;
     if (!(timeout_s >= 0) || std::isinf(timeout_s) || timeout_s > 1.0e9)
         ra.budget_ns = ~0ull;
     else
@@ -1115,17 +1141,43 @@ int rpq_query_eval(rpq_query* q, int32_t source, double timeout_s, int32_t direc
     if (reach_words == nullptr ? nwords != 0 : nwords < words) return fail(RPQ_EINVAL, "answer buffer too small");
     int rc = rpq_query_set_options(q, direction, count_te, alpha);
     if (rc == RPQ_OK) rc = rpq_query_set_tuning(q, RPQ_TUNE_SMALL, allow_small ? 1.0 : 0.0);
-    if (rc == RPQ_OK) rc = rpq_query_set_output(q, reach_words ? 1 : 0);
+    // a buffer from rpq_host_alloc is written by the kernel itself (mapped
+    // pinned memory, unified addressing): no copy node and no host memcpy
+    const bool direct = reach_words && words && q->zero_copy && !use_small(q) &&
+                        host_block_covers(reach_words, (size_t)words * 4);
+    if (rc == RPQ_OK) rc = rpq_query_set_output(q, reach_words && !direct ? 1 : 0);
+    q->run_out_bits = direct ? reach_words : nullptr;
     if (rc == RPQ_OK) rc = rpq_query_run(q, source, timeout_s, nullptr);
+    q->run_out_bits = nullptr;
     if (rc != RPQ_OK) return rc;
     rc = rpq_query_wait(q, stats);
     if (rc != RPQ_OK) return rc;
-    if (reach_words && words) std::memcpy(reach_words, q->h_reach_bits, (size_t)words * 4);
+    if (reach_words && words && !direct) std::memcpy(reach_words, q->h_reach_bits, (size_t)words * 4);
     return RPQ_OK;
 }
 
+namespace {
+// The uint8[nv] answer vector of the last run, expanded from its bitmap on
+// the run's stream the first time it is asked for.
+int materialize_reach(rpq_query* q) {
+    if (!q->reach_stale || q->g->nv == 0) return RPQ_OK;
+    cudaStream_t st = q->last_stream ? q->last_stream : q->own_stream;
+    const long long words = ((long long)q->g->nv + 31) / 32;
+    reach_bytes_kernel<<<(unsigned)std::min<long long>((words + 255) / 256, 4L * q->g->sm_count), 256, 0, st>>>(
+        q->d_reach_bits, q->d_reach, words);
+    CUDA_TRY(cudaGetLastError());
+    q->reach_stale = false;
+    return RPQ_OK;
+}
+}  // namespace
+
 int rpq_query_reach_device(rpq_query* q, uint8_t** d_reach) {
     if (!q || !d_reach) return fail(RPQ_EINVAL, "null argument");
+    if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+    if (q->ran) {
+        const int rc = materialize_reach(q);
+        if (rc != RPQ_OK) return rc;
+    }
     *d_reach = q->d_reach;
     return RPQ_OK;
 }
@@ -1134,6 +1186,8 @@ int rpq_query_copy_reach(rpq_query* q, uint8_t* host_reach) {
     if (!q || !host_reach) return fail(RPQ_EINVAL, "null argument");
     if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
     if (q->g->nv == 0) return RPQ_OK;
+    const int rc = materialize_reach(q);
+    if (rc != RPQ_OK) return rc;
     CUDA_TRY(cudaMemcpyAsync(host_reach, q->d_reach, (size_t)q->g->nv, cudaMemcpyDeviceToHost,
                              q->last_stream ? q->last_stream : q->own_stream));
     CUDA_TRY(cudaStreamSynchronize(q->last_stream ? q->last_stream : q->own_stream));
@@ -1272,12 +1326,36 @@ int rpq_query_set_output(rpq_query* q, int32_t mode) {
     return RPQ_OK;
 }
 
+int rpq_host_alloc(int64_t bytes, void** out) {
+    if (!out || bytes <= 0) return fail(RPQ_EINVAL, "rpq_host_alloc: bad argument");
+    void* p = nullptr;
+    CUDA_TRY(cudaHostAlloc(&p, (size_t)bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    {
+        std::lock_guard<std::mutex> lk(g_host_mu);
+        g_host_blocks[reinterpret_cast<uintptr_t>(p)] = (size_t)bytes;
+    }
+    *out = p;
+    return RPQ_OK;
+}
+
+int rpq_host_free(void* p) {
+    if (!p) return RPQ_OK;
+    {
+        std::lock_guard<std::mutex> lk(g_host_mu);
+        auto it = g_host_blocks.find(reinterpret_cast<uintptr_t>(p));
+        if (it == g_host_blocks.end()) return fail(RPQ_EINVAL, "rpq_host_free: not an rpq_host_alloc block");
+        g_host_blocks.erase(it);
+    }
+    CUDA_TRY(cudaFreeHost(p));
+    return RPQ_OK;
+}
+
 int rpq_query_copy_reach_bits(rpq_query* q, uint32_t* host_words, int64_t nwords) {
     if (!q || (!host_words && nwords)) return fail(RPQ_EINVAL, "null argument");
     const int64_t words = ((int64_t)q->g->nv + 31) / 32;
     if (nwords < words) return fail(RPQ_EINVAL, "output buffer too small");
     if (!q->ran) return fail(RPQ_EINVAL, "query has not been run");
-    if (q->output_mode == 1) {  // already on the host (pinned), after rpq_query_wait
+    if (q->output_mode == 1 && !q->out_direct) {  // already on the host (pinned), after rpq_query_wait
         std::memcpy(host_words, q->h_reach_bits, (size_t)words * 4);
         return RPQ_OK;
     }

@@ -129,6 +129,8 @@ struct RunArgs {
     long long own_w0, own_w1;      // step mode: owned word range of a partitioned rank (empty: all)
     float defer_alpha;             // emit at discovery unless mf_L * dmax * this > m_u (0: always emit)
     float pad3;
+    uint32_t* out_bits;            // the caller's pinned answer bitmap (rpq_host_alloc), written by the
+                                   // epilogue over PCIe, or null (then Params::host_bits)
 };
 
 constexpr unsigned RF_NO_PROBE = 1u;     // claim with atomicOr without reading P first
@@ -544,7 +546,12 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
 // whole bundle (stage_put, <= 31 + 32 x kEdgesPerLane) and drains it once, so
 // its body holds one inlined emission instead of one per unrolled edge slot.
 constexpr int kStageCap = 32 * kEdgesPerLane + 32;
-__host__ __device__ constexpr size_t kStageBytes(int nthreads) { return (size_t)(nthreads / 32) * 2 * kStageCap * 4; }
+// Per-warp dynamic shared memory: the push emission stage, or (pull epochs)
+// the candidate list of pull_tasks<8>: 3 x 256 words + 8 found words.
+constexpr int kWarpScratchWords = (2 * kStageCap > 3 * 32 * 8 + 8) ? 2 * kStageCap : 3 * 32 * 8 + 8;
+__host__ __device__ constexpr size_t kStageBytes(int nthreads) {
+    return (size_t)(nthreads / 32) * kWarpScratchWords * 4;
+}
 struct Stage {
     int* q;  // smem [kStageCap]
     int* w;  // smem [kStageCap]
@@ -911,7 +918,8 @@ __device__ __forceinline__ void reset_qc(Ctl* ctl, int k, int tid) {
     QCnt* qc = &ctl->qc[k];
     for (int i = tid; i <= kShards; i += blockDim.x) qc->shard[i] = 0;
     if (tid == 0) {
-        ctl->steal[k][0] = 0;
+        ctl->steal[k][0] = 0;  // push tail
+        ctl->steal[k][8] = 0;  // pull tail
         qc->edges = 0;
         qc->overflow = 0;
         qc->expire = 0;
@@ -944,23 +952,47 @@ __device__ unsigned long long frontier_edges(const Params& p, const Smem& S, con
 // Pull tasks of one level: every (target state, PV words of vertices) with an
 // active source state.  PV words per lane-task: more vertices in flight per
 // warp on large graphs, more tasks (balance) on small ones.
-template <int PV, int INL>
+// Task dealing: round i of CTA c takes task i*G + (c + i) mod G -- a
+// rotation, so a CTA's tasks do not all share one residue of the vertex
+// blocks mod G (on R-MAT, in-degree depends on the id's bits: a fixed
+// residue made one CTA the slowest of every pull level by 40%).  On long
+// task lists the last quarter is dealt from one grid-wide counter instead.
+//
+// Per task and in-slot, the vertices that still need a look and have in-edges
+// in the slot are compacted into a warp-private candidate list in shared
+// memory (on R-MAT about one vertex in five): the gathers then run on full
+// warps instead of eight mostly-idle predicated rounds.  Each candidate lane
+// probes its row's first `first` in-edges, then continues lane-parallel two
+// edges per round up to kPullCont edges; rows still undecided after that
+// (rare: < 1% on cfg3) are scanned by the whole warp, 128 edges per step.
+constexpr int kPullCont = 8;
+template <int PV>
 __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const uint32_t* fcur, uint32_t* fnext,
                                            long long pw0, long long pw1, int lane, unsigned* s_task,
                                            int s_nptarget, const int* s_ptarget, const unsigned int* s_front,
-                                           unsigned int* s_state, unsigned long long& nnew) {
+                                           unsigned int* s_state, unsigned long long& nnew,
+                                           unsigned long long* steal, uint32_t* scratch, int first) {
     const long long nblk = (pw1 - pw0 + PV - 1) / PV;
     const long long ntask = (long long)s_nptarget * nblk;
+    const long long G = gridDim.x;
+    const long long nown = ntask >= 16 * G ? (ntask - ntask / 4) / G * G : ntask;
+    // warp scratch: candidate (u << 5 | lane, bit 31: long row), row start, row end; found words
+    uint32_t* cid = scratch;
+    uint32_t* clo = scratch + 32 * PV;
+    uint32_t* chi = scratch + 64 * PV;
+    uint32_t* cfound = scratch + 96 * PV;
+    const unsigned lt = lanemask_lt();
     for (;;) {
         long long task = 0;
-        if (lane == 0) task = (long long)atomicAdd(s_task, 1u) * gridDim.x + blockIdx.x;
+        if (lane == 0) {
+            const long long i = (long long)atomicAdd(s_task, 1u);
+            task = i * G + (blockIdx.x + i) % G;
+            if (task >= nown && nown < ntask) task = nown + (long long)atomicAdd(steal, 1ull);
+        }
         task = __shfl_sync(FULL, task, 0);
         if (task >= ntask) break;
         const int q2 = s_ptarget[task / nblk];
         const long long word0 = pw0 + (task % nblk) * PV;
-        uint32_t vis[PV];
-        bool need[PV], found[PV];
-        int w[PV];
         // the first pulled in-slot (warp-uniform): its row pointers do not
         // depend on P, so they are loaded with P's words (coalesced, one
         // dependent round trip less per task; visited vertices' are wasted)
@@ -970,101 +1002,139 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
                 k0 = k;
                 break;
             }
+        uint32_t need = 0, found = 0;  // bit u: this lane's vertex of word u
         uint32_t lo[PV], hi[PV];
-#pragma unroll
-        for (int u = 0; u < PV; ++u) {
-            w[u] = (int)((word0 + u) * 32 + lane);
-            const bool in = word0 + u < pw1 && w[u] < p.nv;
-            vis[u] = word0 + u < pw1 ? ld_bits(p.visited + (long long)q2 * p.W + word0 + u, S.pl) : 0xFFFFFFFFu;
+        {
+            uint32_t vis[PV];
             const uint32_t* rp = S.slots[p.nslots + S.islot[max(k0, 0)]].rowptr;
-            lo[u] = in && k0 >= 0 ? ld_stream_u32(rp + w[u], S.pf) : 0u;
-            hi[u] = in && k0 >= 0 ? ld_stream_u32(rp + w[u] + 1, S.pf) : 0u;
-        }
-        bool any_need = false;
 #pragma unroll
-        for (int u = 0; u < PV; ++u) {
-            need[u] = w[u] < p.nv && !((vis[u] >> lane) & 1u);
-            found[u] = false;
-            any_need |= need[u];
+            for (int u = 0; u < PV; ++u) {
+                const int w = (int)((word0 + u) * 32 + lane);
+                const bool in = word0 + u < pw1 && w < p.nv;
+                vis[u] = word0 + u < pw1 ? ld_bits(p.visited + (long long)q2 * p.W + word0 + u, S.pl) : 0xFFFFFFFFu;
+                lo[u] = in && k0 >= 0 ? ld_stream_u32(rp + w, S.pf) : 0u;
+                hi[u] = in && k0 >= 0 ? ld_stream_u32(rp + w + 1, S.pf) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < PV; ++u)
+                if ((int)((word0 + u) * 32 + lane) < p.nv && !((vis[u] >> lane) & 1u)) need |= 1u << u;
         }
-        if (__ballot_sync(FULL, any_need) == 0) continue;
+        if (__ballot_sync(FULL, need != 0) == 0) continue;
         for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k) {
             const int q = S.isrc[k];
             if (!s_front[q]) continue;
-            bool look[PV], any_look = false;
-#pragma unroll
-            for (int u = 0; u < PV; ++u) {
-                look[u] = need[u] && !found[u];
-                any_look |= look[u];
-            }
-            if (__ballot_sync(FULL, any_look) == 0) break;
+            const uint32_t look = need & ~found;
+            if (__ballot_sync(FULL, look != 0) == 0) break;
             const Slot ps = S.slots[p.nslots + S.islot[k]];
             const uint32_t* frow = fcur + (long long)q * p.W;
+            if (k != k0) {
 #pragma unroll
-            for (int u = 0; u < PV; ++u) {
-                if (k != k0) {
-                    lo[u] = look[u] ? ld_stream_u32(ps.rowptr + w[u], S.pf) : 0u;
-                    hi[u] = look[u] ? ld_stream_u32(ps.rowptr + w[u] + 1, S.pf) : 0u;
-                } else if (!look[u]) {
-                    hi[u] = lo[u];  // preloaded: mask the vertices that need no look
+                for (int u = 0; u < PV; ++u) {
+                    const int w = (int)((word0 + u) * 32 + lane);
+                    const bool lk = (look >> u) & 1u;
+                    lo[u] = lk ? ld_stream_u32(ps.rowptr + w, S.pf) : 0u;
+                    hi[u] = lk ? ld_stream_u32(ps.rowptr + w + 1, S.pf) : 0u;
                 }
             }
-            // the first INL in-edges of every vertex: all loads in flight together
-            int cand[PV][INL];
-#pragma unroll
-            for (int u = 0; u < PV; ++u)
-#pragma unroll
-                for (int i = 0; i < INL; ++i)
-                    cand[u][i] = (lo[u] + i < hi[u]) ? ld_stream_i32(ps.col + lo[u] + i, S.pf) : -1;
-            uint32_t fw[PV][INL];
-#pragma unroll
-            for (int u = 0; u < PV; ++u)
-#pragma unroll
-                for (int i = 0; i < INL; ++i)
-                    fw[u][i] = cand[u][i] >= 0 ? ld_bits(frow + (cand[u][i] >> 5), S.pl) : 0u;
-#pragma unroll
-            for (int u = 0; u < PV; ++u)
-#pragma unroll
-                for (int i = 0; i < INL; ++i)
-                    if (cand[u][i] >= 0 && ((fw[u][i] >> (cand[u][i] & 31)) & 1u)) found[u] = true;
-            // longer rows: the whole warp scans one row at a time, early exit
+            // compaction: the looking vertices with in-edges in this slot
+            int n = 0;
 #pragma unroll
             for (int u = 0; u < PV; ++u) {
-                unsigned longrows = __ballot_sync(FULL, look[u] && !found[u] && hi[u] - lo[u] > INL);
-                while (longrows) {
-                    const int ln = __ffs(longrows) - 1;
-                    longrows &= longrows - 1;
-                    const uint32_t rlo = __shfl_sync(FULL, lo[u], ln) + INL;
-                    const uint32_t rhi = __shfl_sync(FULL, hi[u], ln);
-                    bool hit = false;
-                    for (uint32_t ed = rlo; ed < rhi; ed += 128) {
-                        int uu[4];
+                const bool c = ((look >> u) & 1u) && hi[u] > lo[u];
+                const unsigned m = __ballot_sync(FULL, c);
+                if (c) {
+                    const int pos = n + __popc(m & lt);
+                    cid[pos] = (uint32_t)(u << 5 | lane);
+                    clo[pos] = lo[u];
+                    chi[pos] = hi[u];
+                }
+                n += __popc(m);
+            }
+            if (lane < PV) cfound[lane] = 0u;
+            __syncwarp();
+            bool any_long = false;
+            for (int j0 = 0; j0 < n; j0 += 32) {
+                const int j = j0 + lane;
+                const bool act = j < n;
+                const uint32_t l = act ? clo[j] : 0u, h = act ? chi[j] : 0u;
+                // first round: `first` in-edges, all loads in flight
+                const int c0 = act ? ld_stream_i32(ps.col + l, S.pf) : -1;
+                const int c1 = act && first > 1 && l + 1 < h ? ld_stream_i32(ps.col + l + 1, S.pf) : -1;
+                bool hit = (c0 >= 0 && ((ld_bits(frow + (c0 >> 5), S.pl) >> (c0 & 31)) & 1u)) ||
+                           (c1 >= 0 && ((ld_bits(frow + (c1 >> 5), S.pl) >> (c1 & 31)) & 1u));
+                uint32_t e = l + (uint32_t)first;
+                const uint32_t cap = min(h, l + (uint32_t)kPullCont);
+                // lane-parallel continuation, two in-edges per round
+                while (__ballot_sync(FULL, act && !hit && e < cap)) {
+                    if (act && !hit && e < cap) {
+                        const int d0 = ld_stream_i32(ps.col + e, S.pf);
+                        const int d1 = e + 1 < cap ? ld_stream_i32(ps.col + e + 1, S.pf) : -1;
+                        hit = ((ld_bits(frow + (d0 >> 5), S.pl) >> (d0 & 31)) & 1u) ||
+                              (d1 >= 0 && ((ld_bits(frow + (d1 >> 5), S.pl) >> (d1 & 31)) & 1u));
+                        e += 2;
+                    }
+                }
+                if (act && hit) {
+                    const uint32_t id = cid[j];
+                    atomicOr(&cfound[id >> 5], 1u << (id & 31u));
+                }
+                const bool lng = act && !hit && e < h;
+                if (lng) {
+                    cid[j] |= 0x80000000u;
+                    clo[j] = e;
+                }
+                any_long |= lng;
+            }
+            // rows still undecided: the whole warp scans each, early exit
+            if (__ballot_sync(FULL, any_long)) {
+                __syncwarp();
+                for (int j0 = 0; j0 < n; j0 += 32) {
+                    unsigned longs = __ballot_sync(FULL, j0 + lane < n && (cid[j0 + lane] >> 31));
+                    while (longs) {
+                        const int jj = j0 + __ffs(longs) - 1;
+                        longs &= longs - 1;
+                        const uint32_t rlo = clo[jj], rhi = chi[jj];
+                        bool hit = false;
+                        for (uint32_t ed = rlo; ed < rhi; ed += 128) {
+                            int uu[4];
 #pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            uu[c] = ed + 32 * c + lane < rhi ? ld_stream_i32(ps.col + ed + 32 * c + lane, S.pf) : -1;
-                        bool h = false;
+                            for (int c = 0; c < 4; ++c)
+                                uu[c] = ed + 32 * c + lane < rhi ? ld_stream_i32(ps.col + ed + 32 * c + lane, S.pf) : -1;
+                            bool hh = false;
 #pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            if (uu[c] >= 0) h |= (ld_bits(frow + (uu[c] >> 5), S.pl) >> (uu[c] & 31)) & 1u;
-                        if (__ballot_sync(FULL, h)) {
-                            hit = true;
-                            break;
+                            for (int c = 0; c < 4; ++c)
+                                if (uu[c] >= 0) hh |= (ld_bits(frow + (uu[c] >> 5), S.pl) >> (uu[c] & 31)) & 1u;
+                            if (__ballot_sync(FULL, hh)) {
+                                hit = true;
+                                break;
+                            }
+                        }
+                        if (hit && lane == 0) {
+                            const uint32_t id = cid[jj] & 0x7FFFFFFFu;
+                            atomicOr(&cfound[id >> 5], 1u << (id & 31u));
                         }
                     }
-                    if (hit && lane == ln) found[u] = true;
                 }
             }
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < PV; ++u) found |= ((cfound[u] >> lane) & 1u) << u;
+            __syncwarp();  // cfound / the candidate list are rewritten by the next slot or task
         }
+        // the warp owns these (q2, word) pairs this epoch: F is a plain store,
+        // P an OR without return; lane u writes word u
+        uint32_t fm = 0;
 #pragma unroll
         for (int u = 0; u < PV; ++u) {
-            const unsigned fmask = __ballot_sync(FULL, found[u]);
-            if (fmask && lane == u) {
-                const long long voff = (long long)q2 * p.W + word0 + u;
-                p.visited[voff] = vis[u] | fmask;
-                fnext[voff] = fmask;
-                nnew += __popc(fmask);
-                atomicAdd(&s_state[q2], (unsigned)__popc(fmask));
-            }
+            const unsigned m = __ballot_sync(FULL, (found >> u) & 1u);
+            if (lane == u) fm = m;
+        }
+        if (lane < PV && fm) {
+            const long long voff = (long long)q2 * p.W + word0 + lane;
+            red_or_bits(p.visited + voff, fm, S.pl);
+            fnext[voff] = fm;
+            nnew += __popc(fm);
+            atomicAdd(&s_state[q2], (unsigned)__popc(fm));
         }
     }
 }
@@ -1147,8 +1217,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
     const bool cta0 = blockIdx.x == 0;
     __syncthreads();  // s_run, tables and counters above are read by every thread below
     Stage stage;
-    stage.q = s_stage + wid * 2 * kStageCap;
-    stage.w = s_stage + wid * 2 * kStageCap + kStageCap;
+    stage.q = s_stage + wid * kWarpScratchWords;
+    stage.w = s_stage + wid * kWarpScratchWords + kStageCap;
     stage.n = 0;
     // CTA 0 resets the control block (except the barrier counter, which only
     // grows); nobody else reads it before the first barrier
@@ -1170,8 +1240,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
         if (!step_mode)
             for (long long i = gtid; i < nbits4; i += gthreads) v4[i] = make_uint4(0, 0, 0, 0);
         // step mode: F_0 = M is the caller's and only F_1 (the output) is
-        // written; a full run clears all three
-        for (int f = step_mode ? 1 : 0; f < (step_mode ? 2 : 3); ++f) {
+        // written; a full run clears F_0 and F_1 (level 0's expand epoch
+        // clears F_2 before anything is written into it)
+        for (int f = step_mode ? 1 : 0; f < 2; ++f) {
             uint4* f4 = reinterpret_cast<uint4*>(p.fb[f]);
             for (long long i = gtid; i < nbits4; i += gthreads) f4[i] = make_uint4(0, 0, 0, 0);
         }
@@ -1542,20 +1613,15 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
             // large-state-space instance (cfg3: L3 204 -> 166 us, L2 275 -> 265;
             // cfg5 -2.7%); the 768-thread one (cfg2) keeps its code unchanged.
             const bool one_inline = NT == kThreadsLarge && (float)s_view.nfront > 0.22f * (float)p.nv;
-            if (pw1 - pw0 >= (long long)nwarps * 64) {  // large: 8 words per task
-                if (one_inline)
-                    pull_tasks<8, 1>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front,
-                                     s_state, nnew);
-                else
-                    pull_tasks<8, kPullInline>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget,
-                                               s_front, s_state, nnew);
-            } else if (one_inline) {
-                pull_tasks<kPullVerts, 1>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front,
-                                          s_state, nnew);
-            } else {
-                pull_tasks<kPullVerts, kPullInline>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget,
-                                                    s_front, s_state, nnew);
-            }
+            unsigned long long* pull_steal = &ctl->steal[e % 3][8];
+            uint32_t* scratch = reinterpret_cast<uint32_t*>(s_stage) + (size_t)wid * kWarpScratchWords;
+            const int first = one_inline ? 1 : kPullInline;
+            if (pw1 - pw0 >= (long long)nwarps * 64)  // large: 8 words per task
+                pull_tasks<8>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front, s_state,
+                              nnew, pull_steal, scratch, first);
+            else
+                pull_tasks<kPullVerts>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front,
+                                       s_state, nnew, pull_steal, scratch, first);
         }
         if (p.trace && lane == 0) atomicMax(&s_wend, globaltimer());  // this warp's work done
         __syncthreads();
@@ -1589,27 +1655,17 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
     }
 
     // ---- epilogue: answer = OR of P's rows at final states (engine.py:112-114)
+    // The answer bitmap only: the uint8[|V|] vector is expanded from it on
+    // demand (reach_bytes_kernel, rpq_query_copy_reach), not on every run.
     if (s_view.status == 0) {
         unsigned long long cnt = 0;
+        uint32_t* const hb = s_run.out_bits ? s_run.out_bits : p.host_bits;
         for (long long i = gtid; i < Wn; i += gthreads) {
             uint32_t acc = 0;
             for (int f = 0; f < p.nfinals; ++f) acc |= __ldcg(p.visited + (long long)S.finals[f] * p.W + i);
             cnt += __popc(acc);
             p.reach_bits[i] = acc;
-            if (p.host_bits) p.host_bits[i] = acc;  // coalesced: 128 B per warp over PCIe
-            uint8_t* out = p.reach + i * 32;
-            if (i * 32 + 32 <= p.nv) {
-                uint32_t bytes[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint32_t nib = (acc >> (4 * k)) & 0xFu;
-                    bytes[k] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
-                }
-                reinterpret_cast<uint4*>(out)[0] = make_uint4(bytes[0], bytes[1], bytes[2], bytes[3]);
-                reinterpret_cast<uint4*>(out)[1] = make_uint4(bytes[4], bytes[5], bytes[6], bytes[7]);
-            } else {
-                for (int k = 0; i * 32 + k < p.nv; ++k) out[k] = (acc >> k) & 1u;
-            }
+            if (hb) hb[i] = acc;  // coalesced: 128 B per warp over PCIe
         }
         // exact push-model TE = sum over (q, v) in P of q's group out-degrees x targets
         unsigned long long te = 0;
@@ -1664,6 +1720,24 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
             for (int i = threadIdx.x; i < nw; i += blockDim.x) dst[i] = __ldcg(src + i);
             __threadfence_system();
         }
+    }
+}
+
+// uint8[nv] answer vector from the answer bitmap (bit v%32 of word v/32):
+// 32 bytes per word, two 16-byte stores (the buffer holds W * 32 + 32 bytes).
+__global__ void reach_bytes_kernel(const uint32_t* __restrict__ bits, uint8_t* __restrict__ out, long long words) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < words;
+         i += (long long)gridDim.x * blockDim.x) {
+        const uint32_t acc = bits[i];
+        uint32_t b4[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t nib = (acc >> (4 * k)) & 0xFu;
+            b4[k] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(out + i * 32);
+        dst[0] = make_uint4(b4[0], b4[1], b4[2], b4[3]);
+        dst[1] = make_uint4(b4[4], b4[5], b4[6], b4[7]);
     }
 }
 

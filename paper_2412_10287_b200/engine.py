@@ -188,6 +188,45 @@ def bits_to_reach(words, nv):
     return np.unpackbits(words.view(np.uint8), bitorder="little")[:nv]
 
 
+class _AnswerPool:
+    """Pinned, device-mapped host bitmaps for eval_ssr answers (rpq_host_alloc).
+    The kernel's epilogue writes the answer straight into one over PCIe, and
+    the EvalResult keeps it as its ``bits`` array: no copy node, no host
+    memcpy, no page faults on a fresh array.  A buffer returns to the pool when
+    the last array viewing it is garbage-collected."""
+
+    KEEP = 16  # free buffers kept per size
+
+    def __init__(self):
+        self._free = {}
+        self._lock = threading.Lock()
+
+    def take(self, nwords):
+        with self._lock:
+            lst = self._free.get(nwords)
+            ptr = lst.pop() if lst else None
+        if ptr is None:
+            p = ctypes.c_void_p()
+            raise_for_status(_lib.engine().rpq_host_alloc(nwords * 4, ctypes.byref(p)), "rpq_host_alloc")
+            ptr = p.value
+        buf = (ctypes.c_uint32 * nwords).from_address(ptr)
+        weakref.finalize(buf, self._give, nwords, ptr)
+        return np.ctypeslib.as_array(buf)
+
+    def _give(self, nwords, ptr):
+        with self._lock:
+            lst = self._free.setdefault(nwords, [])
+            if len(lst) < self.KEEP:
+                lst.append(ptr)
+                return
+        try:
+            _lib.engine().rpq_host_free(ptr)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+_ANSWERS = _AnswerPool()
+
 _TLS = threading.local()
 
 
@@ -217,7 +256,9 @@ def _run(g, n, source, opts, tag, *, want_stats=False):
         if first_check and (remaining < 0 or opts.timeout <= 0):
             raise QueryTimeout(time.monotonic() - t0, 0)
         budget = -1.0 if math.isinf(remaining) else max(remaining, 0.0)
-        words = np.empty((g.num_vertices + 31) // 32, dtype=np.uint32)
+        nwords = (g.num_vertices + 31) // 32
+        # large answers land in a pinned buffer the kernel writes directly
+        words = _ANSWERS.take(nwords) if nwords >= 4096 else np.empty(nwords, dtype=np.uint32)
         stats = _thread_stats()  # read (or copied out) before this thread's next call
         # options, run, wait and the answer bitmap in one C call (raw addresses)
         rc = lib.rpq_query_eval(q, int(source), budget, DIRECTIONS[opts.direction],

@@ -18,7 +18,6 @@ pytestmark = pytest.mark.gpu
 
 # test_cli.py:17 TRIANGLE: 3 -a-> 4, 4 -a-> 3, 3 -b-> 5 (vertices named in order of appearance)
 TRI_VERTICES = ["3", "4", "5"]
-TRI = P.LabeledGraph.from_edges(3, ["a", "b"], [(0, 0, 1), (1, 0, 0), (0, 1, 2)]) if False else None
 
 
 def triangle():
@@ -30,8 +29,7 @@ def triangle():
 
 
 def tri_compiler():
-    # the reference compiler's automata for the patterns these cases use (labels a=0, b=1)
-    a_star_b = P.Automaton(3, {(0, False): [(0, 0)], (1, False): [(0, 1)]}, [0], [1]) if False else None
+    # the reference compiler's automata (extra_automata.json: labels a=0, b=1, ...)
     import json
     import os
 
@@ -45,11 +43,11 @@ def test_bench_rows_and_errors():
     g = triangle()
     comp = tri_compiler()
     entries = cli.parse_workload(io.StringIO(
-        "q1\tssr\t3\ta* b\nbad-vertex\tssr\t42\ta\nbad-pattern\tssr\t3\ta )b\nq3\tssr\t4\ta+ b\n"))
+        "q1\tssr\t3\ta b*\nbad-vertex\tssr\t42\ta\nbad-pattern\tssr\t3\ta )b\nq3\tssr\t4\ta+ b\n"))
     rows = cli.run_bench(g, entries, P.EngineOptions(), compile_fn=comp)
     assert [r["status"] for r in rows] == ["ok", "error", "error", "ok"]
-    assert rows[0]["result_count"] == 1  # a* b from 3 reaches exactly vertex 5
-    assert rows[3]["result_count"] == 1
+    assert rows[0]["result_count"] == 1  # a b* from 3 reaches exactly vertex 4
+    assert rows[3]["result_count"] == 1  # a+ b from 4: {5}
     out = io.StringIO()
     cli.write_csv(rows, out)
     got = list(csv.reader(io.StringIO(out.getvalue())))
@@ -59,7 +57,7 @@ def test_bench_rows_and_errors():
 def test_bench_repeat_parallel_and_extended():
     g = triangle()
     comp = tri_compiler()
-    entries = cli.parse_workload(io.StringIO("".join(f"q{i}\tssr\t3\ta* b\n" for i in range(4))))
+    entries = cli.parse_workload(io.StringIO("".join(f"q{i}\tssr\t3\ta+ b\n" for i in range(4))))
     rows = cli.run_bench(g, entries, P.EngineOptions(), repeat=3, workers=2, compile_fn=comp, work=True)
     assert [r["id"] for r in rows] == ["q0", "q1", "q2", "q3"]
     assert all(r["result_count"] == 1 and r["status"] == "ok" for r in rows)
@@ -72,7 +70,7 @@ def test_bench_timeout_status():
     nv = 3001
     chain = CsrMatrix.from_pairs(nv, nv, [(i, i + 1) for i in range(3000)])
     g = P.LabeledGraph(nv, ["a"], [chain])
-    a_star = P.Automaton(1, {(0, False): [(0, 0)]}, [0], [0])
+    a_star = P.Automaton.build(1, {(0, False): [(0, 0)]}, [0], [0])
     entries = cli.parse_workload(io.StringIO("slow\tssr\t0\ta*\n"))
     rows = cli.run_bench(g, entries, P.EngineOptions(timeout=0.001, kernel="grid"),
                          compile_fn=lambda _p: a_star)

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--direction", default="auto")
     ap.add_argument("--query", type=int, default=0, help="index into the config's query templates")
     ap.add_argument("--max-degree", action="store_true", help="source = max out-degree vertex (bench.py's)")
+    ap.add_argument("--source", type=int, default=None, help="explicit source vertex")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -34,7 +35,9 @@ def main():
     sg = datagen.generate(args.config)
     g = sg.labeled_graph()
     n = P.Automaton.from_json(autos[args.config][c["queries"][args.query] + "|min"])
-    if args.max_degree:
+    if args.source is not None:
+        src = args.source
+    elif args.max_degree:
         src = int(np.argmax(sg.out_degree()))
     else:
         src = int(datagen.pick_sources(sg, args.config, count=1)[0])
