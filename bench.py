@@ -462,7 +462,8 @@ def run_engine(args, rank, world, local_rank):
     b_step = sum(work[s]["bytes"] for s in sources)
 
     # e2e through the public API: automaton H2D + kernel + answer D2H per call
-    e2e_s, set_ms = [], []
+    e2e_s, set_ms, e2e_dev_ms, d2h_answer, e2e_host_us = [], [], [], {}, []
+    nwords = (sg.nv + 31) // 32
     if not args.profile:
         opts = P.EngineOptions(timeout=math.inf, direction=args.direction, alpha=alpha)
         for _ in range(args.warmup):  # untimed, like the device leg (first call creates the query)
@@ -475,8 +476,14 @@ def run_engine(args, rank, world, local_rank):
                 torch.cuda.synchronize()
                 t = time.perf_counter()
                 res = P.eval_ssr(g, n, s, opts)
-                t_step += time.perf_counter() - t
+                dt = time.perf_counter() - t
+                t_step += dt
+                e2e_dev_ms.append(P.engine._thread_stats().device_ms)  # this call's device time
+                e2e_host_us.append(1e6 * dt - 1e3 * e2e_dev_ms[-1])
                 assert res.iterations == work[s]["iters"]
+                if s not in d2h_answer:  # bytes the answer took over PCIe: bitmap or (word, bits) pairs
+                    nz = int(np.count_nonzero(res.bits))
+                    d2h_answer[s] = 8 * nz if 2 * nz < nwords else 4 * nwords
                 if k == 0:
                     assert np.array_equal(res.reach, work[s]["reach"])
                     # the reference's result type: set[int] built from the answer
@@ -487,7 +494,6 @@ def run_engine(args, rank, world, local_rank):
     clocks = sampler.stop() if sampler else None
 
     h2d, d2h_ctl = pq.io_bytes()
-    d2h = d2h_ctl + (sg.nv + 31) // 32 * 4  # eval_ssr reads back the answer bitmap
     from paper_2412_10287_b200.multigpu import reduce_timing
 
     # max over ranks of the device time, sum over ranks of the product edges
@@ -547,11 +553,17 @@ def run_engine(args, rank, world, local_rank):
     }
     if e2e_s:
         out["e2e"] = {"value": units / e2e_max_s / 1e9, "unit": UNIT,
-                      "h2d_bytes_per_step": nq * (h2d + 4), "d2h_bytes_per_step": nq * d2h,
+                      "h2d_bytes_per_step": nq * (h2d + 4),
+                      "d2h_bytes_per_step": nq * d2h_ctl + sum(d2h_answer.get(s, 0) for s in sources),
                       "latency_ms_median_per_query": 1e3 * statistics.median(e2e_s) / nq,
+                      "device_ms_per_query": statistics.mean(e2e_dev_ms) if e2e_dev_ms else None,
+                      "host_us_per_query": {"median": statistics.median(e2e_host_us),
+                                            "mean": statistics.mean(e2e_host_us)} if e2e_host_us else None,
                       "reachable_set_ms_per_query": statistics.mean(set_ms) if set_ms else None,
-                      "note": ("eval_ssr per source with host buffers (answer bitmap read back); "
-                               "reachable_set_ms = building the reference's set[int] from it, not in value")}
+                      "note": ("eval_ssr per source with host buffers: automaton tables H2D, the answer D2H as "
+                               "the bitmap or, when sparse, (word, bits) pairs; device_ms = the calls' own "
+                               "CUDA-event time; reachable_set_ms = building the reference's set[int] from the "
+                               "answer, not in value")}
     if world == 1 and not args.no_cpu_baseline and not args.profile:
         og, oq = oracle_setup(sg, nj)
         out["cpu_baseline"] = cpu_baseline(og, oq, sources, {s: work[s]["te"] for s in sources},

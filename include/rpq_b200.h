@@ -84,6 +84,9 @@ typedef struct rpq_stats {
     int64_t work_ns[RPQ_STATS_LEVELS];      /* kernel start -> last CTA done with level L's work */
     int64_t bar_ns[RPQ_STATS_LEVELS];       /* kernel start -> CTA 0 past the barrier after level L */
     int8_t level_dir[RPQ_STATS_LEVELS];     /* 0 push, 1 pull */
+    int32_t answer_list;     /* rpq_query_eval_list only: 1 = the answer buffer holds answer_words
+                                (word index, word) uint32 pairs instead of the bitmap */
+    int64_t answer_words;    /* nonzero words of the answer bitmap (list runs) */
 } rpq_stats;
 
 /* Multi-source batches: up to RPQ_BATCH sources per run (one bit each). */
@@ -190,6 +193,15 @@ RPQ_API int rpq_query_wait(rpq_query* q, rpq_stats* stats);
 RPQ_API int rpq_query_eval(rpq_query* q, int32_t source, double timeout_s, int32_t direction, int32_t count_te,
                            double alpha, int32_t allow_small, rpq_stats* stats, uint32_t* reach_words,
                            int64_t nwords);
+/* rpq_query_eval whose answer may come back as a list: when reach_words lies
+ * in an rpq_host_alloc block and stats is non-NULL, a sparse answer (fewer
+ * than half of the bitmap's words nonzero) is written as stats->answer_words
+ * (word index, word) uint32 pairs at reach_words[0 ..) and stats->answer_list
+ * is set; otherwise the bitmap, as rpq_query_eval.  An empty answer moves no
+ * bytes.  (The reference's answer is a Python set, engine.py:112-114.) */
+RPQ_API int rpq_query_eval_list(rpq_query* q, int32_t source, double timeout_s, int32_t direction,
+                                int32_t count_te, double alpha, int32_t allow_small, rpq_stats* stats,
+                                uint32_t* reach_words, int64_t nwords);
 /* Device pointer to the uint8[num_vertices] answer of the last run (expanded
  * from the answer bitmap on the run's stream on first request). */
 RPQ_API int rpq_query_reach_device(rpq_query* q, uint8_t** d_reach);

@@ -66,6 +66,8 @@ class RpqStats(ctypes.Structure):
         ("work_ns", c_i64 * STATS_LEVELS),
         ("bar_ns", c_i64 * STATS_LEVELS),
         ("level_dir", ctypes.c_int8 * STATS_LEVELS),
+        ("answer_list", c_i32),
+        ("answer_words", c_i64),
     ]
 
     def to_dict(self):
@@ -166,6 +168,7 @@ ENGINE_SIGNATURES = {
     "rpq_query_set_owned": (c_i32, [c_vp, c_i64, c_i64]),
     # (stats and answer buffers as void*: the per-query fast path passes raw addresses)
     "rpq_query_eval": (c_i32, [c_vp, c_i32, c_dbl, c_i32, c_i32, c_dbl, c_i32, c_vp, c_vp, c_i64]),
+    "rpq_query_eval_list": (c_i32, [c_vp, c_i32, c_dbl, c_i32, c_i32, c_dbl, c_i32, c_vp, c_vp, c_i64]),
     "rpq_query_copy_trace": (c_i32, [c_vp, P_u64, c_i64, P_i32]),
     "rpq_query_step_device": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "rpq_query_run_batch": (c_i32, [c_vp, c_i32, P_i32, c_dbl, c_vp]),

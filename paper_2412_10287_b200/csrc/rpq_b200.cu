@@ -120,6 +120,7 @@ struct rpq_query {
     uint32_t* h_reach_bits = nullptr;  // pinned; filled by run() when output_mode == 1
     int output_mode = 0;
     uint32_t* run_out_bits = nullptr;  // next run's caller-owned pinned answer buffer (rpq_query_eval)
+    bool run_out_list = false;         // ... which may receive a (word index, word) pair list
     bool out_direct = false;           // the last run wrote its answer there, not to h_reach_bits
     bool reach_stale = true;           // d_reach (uint8) not yet expanded from d_reach_bits
 
@@ -1069,6 +1070,7 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     // the caller's pinned answer buffer (grid kernel only; the single-CTA
     // kernel's answer goes through h_reach_bits)
     ra.out_bits = use_small(q) ? nullptr : q->run_out_bits;
+    ra.out_list = ra.out_bits && q->run_out_list ? 1 : 0;
     q->out_direct = ra.out_bits != nullptr;
     q->reach_stale = true;
     if (!(timeout_s >= 0) || std::isinf(timeout_s) || timeout_s > 1.0e9)
@@ -1109,6 +1111,8 @@ int rpq_query_wait(rpq_query* q, rpq_stats* stats) {
         stats->segments = (int64_t)c.segments;
         stats->visited_pairs = (int64_t)c.pairs;
         stats->reach_count = (int64_t)c.reach_count;
+        stats->answer_list = q->out_direct ? c.ans_list : 0;
+        stats->answer_words = (int64_t)c.ans_words;
         stats->device_ms = ms;
         stats->pull_levels = c.pull_levels;
         for (int i = 0; i < RPQ_STATS_LEVELS; ++i) {
@@ -1134,8 +1138,9 @@ int rpq_query_wait(rpq_query* q, rpq_stats* stats) {
     return RPQ_OK;
 }
 
-int rpq_query_eval(rpq_query* q, int32_t source, double timeout_s, int32_t direction, int32_t count_te,
-                   double alpha, int32_t allow_small, rpq_stats* stats, uint32_t* reach_words, int64_t nwords) {
+namespace {
+int query_eval(rpq_query* q, int32_t source, double timeout_s, int32_t direction, int32_t count_te, double alpha,
+               int32_t allow_small, rpq_stats* stats, uint32_t* reach_words, int64_t nwords, bool allow_list) {
     if (!q) return fail(RPQ_EINVAL, "null query");
     const int64_t words = ((int64_t)q->g->nv + 31) / 32;
     if (reach_words == nullptr ? nwords != 0 : nwords < words) return fail(RPQ_EINVAL, "answer buffer too small");
@@ -1147,13 +1152,29 @@ int rpq_query_eval(rpq_query* q, int32_t source, double timeout_s, int32_t direc
                         host_block_covers(reach_words, (size_t)words * 4);
     if (rc == RPQ_OK) rc = rpq_query_set_output(q, reach_words && !direct ? 1 : 0);
     q->run_out_bits = direct ? reach_words : nullptr;
+    q->run_out_list = direct && allow_list && stats;
     if (rc == RPQ_OK) rc = rpq_query_run(q, source, timeout_s, nullptr);
     q->run_out_bits = nullptr;
+    q->run_out_list = false;
     if (rc != RPQ_OK) return rc;
     rc = rpq_query_wait(q, stats);
     if (rc != RPQ_OK) return rc;
     if (reach_words && words && !direct) std::memcpy(reach_words, q->h_reach_bits, (size_t)words * 4);
     return RPQ_OK;
+}
+}  // namespace
+
+int rpq_query_eval(rpq_query* q, int32_t source, double timeout_s, int32_t direction, int32_t count_te,
+                   double alpha, int32_t allow_small, rpq_stats* stats, uint32_t* reach_words, int64_t nwords) {
+    return query_eval(q, source, timeout_s, direction, count_te, alpha, allow_small, stats, reach_words, nwords,
+                      false);
+}
+
+int rpq_query_eval_list(rpq_query* q, int32_t source, double timeout_s, int32_t direction, int32_t count_te,
+                        double alpha, int32_t allow_small, rpq_stats* stats, uint32_t* reach_words,
+                        int64_t nwords) {
+    return query_eval(q, source, timeout_s, direction, count_te, alpha, allow_small, stats, reach_words, nwords,
+                      true);
 }
 
 namespace {

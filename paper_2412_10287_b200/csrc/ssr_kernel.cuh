@@ -97,6 +97,9 @@ struct Ctl {
     unsigned long long segments;
     unsigned long long pairs;
     unsigned long long reach_count;
+    unsigned long long ans_words;  // nonzero answer words (out_list runs)
+    int ans_list;                  // 1: the host answer buffer holds (word index, word) pairs
+    int pad_ans;
     long long level_new[64];
     long long level_edges[64];
     unsigned long long level_ns[64];
@@ -110,6 +113,7 @@ struct Ctl {
     // (reset with qc[i]); one 128-byte line each, away from the counters
     unsigned long long steal[3][16];
     unsigned int exits;  // CTAs past the epilogue (zero-copy results: the last one publishes)
+    unsigned long long ans_cursor;  // list-mode answer: next free pair
 };
 
 // Per-run inputs, copied host->device with the automaton tables at the start
@@ -128,7 +132,8 @@ struct RunArgs {
     unsigned int flags;            // RF_* push-path variants (tuning)
     long long own_w0, own_w1;      // step mode: owned word range of a partitioned rank (empty: all)
     float defer_alpha;             // emit at discovery unless mf_L * dmax * this > m_u (0: always emit)
-    float pad3;
+    int out_list;                  // out_bits may receive a (word index, word) pair list when that is
+                                   // smaller than the bitmap (sparse answers; Ctl::ans_list says which)
     uint32_t* out_bits;            // the caller's pinned answer bitmap (rpq_host_alloc), written by the
                                    // epilogue over PCIe, or null (then Params::host_bits)
 };
@@ -1658,14 +1663,44 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
     // The answer bitmap only: the uint8[|V|] vector is expanded from it on
     // demand (reach_bytes_kernel, rpq_query_copy_reach), not on every run.
     if (s_view.status == 0) {
-        unsigned long long cnt = 0;
+        unsigned long long cnt = 0, nzw = 0;
         uint32_t* const hb = s_run.out_bits ? s_run.out_bits : p.host_bits;
+        const bool maybe_list = hb && s_run.out_list;
         for (long long i = gtid; i < Wn; i += gthreads) {
             uint32_t acc = 0;
             for (int f = 0; f < p.nfinals; ++f) acc |= __ldcg(p.visited + (long long)S.finals[f] * p.W + i);
             cnt += __popc(acc);
+            nzw += acc != 0u;
             p.reach_bits[i] = acc;
-            if (hb) hb[i] = acc;  // coalesced: 128 B per warp over PCIe
+            if (hb && !maybe_list) hb[i] = acc;  // coalesced: 128 B per warp over PCIe
+        }
+        if (maybe_list) {
+            // the host gets whichever is smaller: the bitmap, or the nonzero
+            // words as (index, word) pairs -- an empty answer moves no bytes
+            nzw = warp_sum_u64(nzw);
+            if (lane == 0 && nzw) atomicAdd(&ctl->ans_words, nzw);
+            grid_barrier(ctl, ++e, s_run.bar_base);
+            const unsigned long long nz = ldcg(&ctl->ans_words);
+            const bool list = 2 * nz < (unsigned long long)Wn;
+            if (list) {
+                for (long long i0 = gwarp * 32; i0 < Wn; i0 += nwarps * 32) {
+                    const long long i = i0 + lane;
+                    const uint32_t acc = i < Wn ? __ldcg(p.reach_bits + i) : 0u;
+                    const unsigned m = __ballot_sync(FULL, acc != 0u);
+                    if (!m) continue;
+                    unsigned long long base = 0;
+                    if (lane == 0) base = atomicAdd(&ctl->ans_cursor, (unsigned long long)__popc(m));
+                    base = __shfl_sync(FULL, base, 0);
+                    if (acc) {
+                        const unsigned long long pos = base + __popc(m & lanemask_lt());
+                        hb[2 * pos] = (uint32_t)i;
+                        hb[2 * pos + 1] = acc;
+                    }
+                }
+            } else {
+                for (long long i = gtid; i < Wn; i += gthreads) hb[i] = __ldcg(p.reach_bits + i);
+            }
+            if (cta0 && threadIdx.x == 0) ctl->ans_list = list ? 1 : 0;
         }
         // exact push-model TE = sum over (q, v) in P of q's group out-degrees x targets
         unsigned long long te = 0;

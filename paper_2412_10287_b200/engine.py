@@ -83,11 +83,12 @@ class EvalResult:
     first access from ``reach``, the device's ``uint8[|V|]`` answer vector.
     """
 
-    __slots__ = ("_reach", "_bits", "_nv", "_reachable", "iterations", "elapsed", "algorithm", "stats")
+    __slots__ = ("_reach", "_bits", "_pairs", "_nv", "_reachable", "iterations", "elapsed", "algorithm", "stats")
 
-    def __init__(self, reach, iterations, elapsed, algorithm, stats=None, bits=None, nv=None):
+    def __init__(self, reach, iterations, elapsed, algorithm, stats=None, bits=None, nv=None, pairs=None):
         self._reach = reach
         self._bits = bits  # answer bitmap as read back from the device (uint32 words)
+        self._pairs = pairs  # or a sparse answer as read back: (word index, word) uint32 pairs
         self._nv = nv
         self._reachable = None
         self.iterations = iterations
@@ -99,12 +100,16 @@ class EvalResult:
     def reach(self):
         """uint8[|V|]: 1 where the vertex is an answer (decoded on first use)."""
         if self._reach is None:
-            self._reach = bits_to_reach(self._bits, self._nv)
+            self._reach = bits_to_reach(self.bits, self._nv)
         return self._reach
 
     @property
     def bits(self):
         """The answer as uint32 words, bit v % 32 of word v // 32."""
+        if self._bits is None and self._pairs is not None:
+            bits = np.zeros((self._nv + 31) // 32, dtype=np.uint32)
+            bits[self._pairs[0::2]] = self._pairs[1::2]
+            self._bits, self._pairs = bits, None
         if self._bits is None:
             packed = np.packbits(self._reach, bitorder="little")
             packed = np.concatenate([packed, np.zeros(-packed.size % 4, dtype=np.uint8)])
@@ -261,22 +266,29 @@ def _run(g, n, source, opts, tag, *, want_stats=False):
         words = _ANSWERS.take(nwords) if nwords >= 4096 else np.empty(nwords, dtype=np.uint32)
         stats = _thread_stats()  # read (or copied out) before this thread's next call
         # options, run, wait and the answer bitmap in one C call (raw addresses)
-        rc = lib.rpq_query_eval(q, int(source), budget, DIRECTIONS[opts.direction],
-                                int(opts.count_te or opts.debug_checks), opts.alpha,
-                                1 if opts.kernel == "auto" else 0, ctypes.addressof(stats),
-                                words.ctypes.data if words.size else None, words.size)
+        rc = lib.rpq_query_eval_list(q, int(source), budget, DIRECTIONS[opts.direction],
+                                     int(opts.count_te or opts.debug_checks), opts.alpha,
+                                     1 if opts.kernel == "auto" else 0, ctypes.addressof(stats),
+                                     words.ctypes.data if words.size else None, words.size)
         if rc == _lib.RPQ_ETIMEOUT:
             raise QueryTimeout(time.monotonic() - t0,
                                _iterations_for(tag, stats.iterations, table.starts.size))
         raise_for_status(rc, "rpq_query_eval")
         iterations = _iterations_for(tag, stats.iterations, table.starts.size)
+        pairs = None
+        if stats.answer_list:
+            # a sparse answer came back as (word index, word) pairs: keep a
+            # copy of them (the bitmap is built on first use) and let the
+            # pinned buffer go back to the pool
+            pairs = words[: 2 * int(stats.answer_words)].copy()
+            words = None
         if opts.debug_checks:
             _debug_invariants(lib, q, table, g.num_vertices, stats, iterations)
     finally:
         dg.release_query(table, q)
     return EvalResult(None, iterations, time.monotonic() - t0, tag,
                       stats.to_dict() if want_stats or opts.debug_checks or opts.count_te else None,
-                      bits=words, nv=g.num_vertices)
+                      bits=words, nv=g.num_vertices, pairs=pairs)
 
 
 def _debug_invariants(lib, q, table, nv, stats, iterations):
