@@ -72,3 +72,10 @@ def answer_digest(reach):
     import hashlib
 
     return hashlib.sha256(",".join(str(v) for v in np.flatnonzero(reach).tolist()).encode()).hexdigest()
+
+
+def reach_sha256(reach):
+    """sha256 of the little-endian packed answer bitmap (make_golden.reach_digest)."""
+    import hashlib
+
+    return hashlib.sha256(np.packbits(np.asarray(reach, dtype=np.uint8), bitorder="little").tobytes()).hexdigest()
