@@ -75,10 +75,18 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["engine", "reference"], default="engine")
+    ap.add_argument("--mode", choices=["replicas", "partitioned", "batch"], default="replicas",
+                    help="replicas: independent single-source queries per rank (default); partitioned: each "
+                         "query vertex-partitioned over all ranks (NCCL allgather per level, strong scaling); "
+                         "batch: the multi-source kernel over the config's source set, sources sharded over "
+                         "ranks (cfg5's 1,024)")
     ap.add_argument("--config", default=CONFIG)
-    ap.add_argument("--sources", type=int, default=8, help="sources per rank (uniform-source configs)")
+    ap.add_argument("--sources", type=int, default=None,
+                    help="sources per rank (uniform-source configs; default 8, batch mode: the config's set)")
     ap.add_argument("--source", type=int, default=None, help="diagnostic: one fixed source instead")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--automaton", choices=["min", "raw"], default="min",
+                    help="the reference compiler's minimal DFA (default) or its unminimized automaton")
     ap.add_argument("--direction", choices=["auto", "push", "pull"], default="auto")
     ap.add_argument("--emit-mode", type=int, default=None, help="tuning: 0 inline, 1 plan, 2 adaptive")
     ap.add_argument("--emit-inline-max", type=int, default=None)
@@ -96,9 +104,14 @@ def parse_args():
     return ap.parse_args()
 
 
+_AUTOMATON_KIND = ["min"]
+
+
 def load_automaton(config, query):
+    """The reference compiler's automaton for the config query: minimal DFA
+    (its default), or --automaton raw (minimize=False: cfg5's 17 states)."""
     with open(os.path.join(ROOT, "paper_2412_10287_b200", "data", "config_automata.json")) as fh:
-        return json.load(fh)[config][f"{query}|min"]
+        return json.load(fh)[config][f"{query}|{_AUTOMATON_KIND[0]}"]
 
 
 def ranked_sources(sg, k):
@@ -329,7 +342,7 @@ def run_reference(args, rank, world):
     select_workload(args.config)
     sg = datagen.generate(args.config)
     nj = load_automaton(args.config, QUERY)
-    all_sources = bench_sources(sg, args.config, world, args.sources)
+    all_sources = bench_sources(sg, args.config, world, args.sources or 8)
     sources = all_sources[: len(all_sources) // world]  # rank 0's share: the host runs one rank's work
     og, oq = oracle_setup(sg, nj)
     te = {s: oracle_bfs(og, oq, s)[1]["te"] for s in sources}
@@ -393,7 +406,7 @@ def run_engine(args, rank, world, local_rank):
     g = sg.labeled_graph()
     nj = load_automaton(args.config, QUERY)
     n = P.Automaton.from_json(nj)
-    all_sources = bench_sources(sg, args.config, world, args.sources)
+    all_sources = bench_sources(sg, args.config, world, args.sources or 8)
     if args.source is not None:
         all_sources = [args.source] * world
     per = len(all_sources) // world
@@ -571,21 +584,225 @@ def run_engine(args, rank, world, local_rank):
     return out
 
 
+def _timed_flush(flush, i):
+    flush.fill_(i & 0xFF)  # > L2: evicts the graph between queries (outside the events)
+
+
+def run_partitioned(args, rank, world, local_rank):
+    """One query at a time over all ranks, vertex-partitioned 1-D (SURVEY.md
+    §8(e) regime 2): every rank runs the step kernel on its owned targets and
+    the owned slices of the next frontier are allgathered (NCCL) per level.
+    Strong scaling: every rank evaluates the same sources; value = sum of TE /
+    the max over ranks of the device-timed query time."""
+    import numpy as np
+    import torch
+
+    import paper_2412_10287_b200 as P
+    from paper_2412_10287_b200 import datagen
+    from paper_2412_10287_b200.multigpu import reduce_timing
+    from paper_2412_10287_b200.partition import partitioned_query
+
+    dev = torch.device("cuda", local_rank)
+    select_workload(args.config)
+    sg = datagen.generate(args.config)
+    g = sg.labeled_graph()
+    nj = load_automaton(args.config, QUERY)
+    n = P.Automaton.from_json(nj)
+    sources = bench_sources(sg, args.config, 1, args.sources or 8)
+    if args.source is not None:
+        sources = [args.source]
+    # exact work per source (TE, levels) from the fused kernel on the full graph
+    work = {}
+    with P.PreparedQuery(g, n, device=local_rank) as fq:
+        fq.set_options(count_te=True)
+        for s in sources:
+            fq.launch(s, -1.0, None)
+            st = fq.wait()
+            work[s] = {"te": int(st.te), "iters": int(st.iterations), "reach": fq.reach()}
+    pq = partitioned_query(g, n)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    for i in range(args.warmup):
+        for s in sources:
+            words, its, _ = pq.run(s)
+            assert its == work[s]["iters"], (s, its, work[s]["iters"])
+            if i == 0:
+                got = np.unpackbits(words.view(np.uint8), bitorder="little")[: sg.nv]
+                assert np.array_equal(got, work[s]["reach"]), s
+    sampler = None
+    if not args.profile:
+        phys = os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[local_rank]
+        sampler = ClockSampler(phys)
+        sampler.start()
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    cur = torch.cuda.current_stream(dev)
+    q_ms = {s: [] for s in sources}
+    for k in range(args.steps):
+        for j, s in enumerate(sources):
+            _timed_flush(flush, k + j)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cur)
+            _, its, _ = pq.run(s)
+            e1.record(cur)
+            e1.synchronize()
+            q_ms[s].append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    torch.distributed.barrier()
+    clocks = sampler.stop() if sampler else None
+    total_ms = sum(sum(v) for v in q_ms.values())
+    te_step = sum(work[s]["te"] for s in sources)
+    total_max_ms, _ = reduce_timing(total_ms, 0, dev)
+    # per-level wall timings of the heaviest source (one profiled run)
+    heavy = max(sources, key=lambda s: work[s]["te"])
+    _, _, prof = pq.run(heavy, profile=True)
+    # e2e: the public call (answer bitmap gathered to the host)
+    e2e = []
+    if not args.profile:
+        for k in range(args.steps):
+            t_step = 0.0
+            for j, s in enumerate(sources):
+                _timed_flush(flush, k + j)
+                torch.cuda.synchronize()
+                torch.distributed.barrier()
+                t = time.perf_counter()
+                res = P.partition.eval_ssr_partitioned(g, n, s, P.EngineOptions(timeout=math.inf))
+                t_step += time.perf_counter() - t
+                assert res.iterations == work[s]["iters"]
+            e2e.append(t_step)
+    e2e_max, _ = reduce_timing(sum(e2e) if e2e else 0.0, 0, dev)
+    if rank != 0:
+        return None
+    value = te_step * args.steps / (total_max_ms / 1e3) / 1e9
+    ranges = pq.ranges
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_max_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {**workload_config(args, sg, sources, 1),
+                   "parallelism": f"{world} GPU(s), one query vertex-partitioned 1-D over all ranks "
+                                  f"(NCCL allgather of the owned frontier slices per level)"},
+        "mode": "partitioned",
+        "per_query": {
+            "latency_ms_median": {str(s): statistics.median(q_ms[s]) for s in sources},
+            "te": {str(s): work[s]["te"] for s in sources},
+            "iterations": {str(s): work[s]["iters"] for s in sources},
+            "heaviest_source": heavy,
+            "heaviest_level_wall_us": prof["levels_wall_us"],
+            "heaviest_step_ms": prof["step_ms"],
+        },
+        "partition": {"ranks": world, "word_ranges": [list(r) for r in ranges],
+                      "exchange_bytes_per_level": int(pq.table.nstates * max(w1 - w0 for w0, w1 in ranges) * 4
+                                                      * world)},
+        "gpu_launches": None,
+        "clocks": clocks,
+    }
+    if e2e:
+        out["e2e"] = {"value": te_step * args.steps / e2e_max / 1e9, "unit": UNIT,
+                      "h2d_bytes_per_step": 0, "d2h_bytes_per_step": len(sources) * ((sg.nv + 31) // 32) * 4,
+                      "note": "eval_ssr_partitioned per source; the answer bitmap gathered and read back"}
+    return out
+
+
+def run_batch_mode(args, rank, world, local_rank):
+    """Multi-source throughput: the config's source set (cfg5: 1,024 uniform
+    sources) sharded over ranks, 32 sources per launch of the bit-sliced batch
+    kernel; value = sum of TE over all sources / max over ranks of the
+    device time.  Weak scaling in the sources per rank."""
+    import torch
+
+    import paper_2412_10287_b200 as P
+    from paper_2412_10287_b200 import datagen
+    from paper_2412_10287_b200.multigpu import reduce_timing
+
+    dev = torch.device("cuda", local_rank)
+    select_workload(args.config)
+    sg = datagen.generate(args.config)
+    g = sg.labeled_graph()
+    nj = load_automaton(args.config, QUERY)
+    n = P.Automaton.from_json(nj)
+    total = args.sources or datagen.CONFIGS[args.config].get("nsources", 32)
+    all_sources = datagen.pick_sources(sg, args.config, count=total * world)
+    per = len(all_sources) // world
+    sources = all_sources[rank * per:(rank + 1) * per]
+    pq = P.PreparedQuery(g, n, device=local_rank)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    batches = [sources[b:b + 32] for b in range(0, len(sources), 32)]
+    te = 0
+    for b in batches:
+        pq.launch_batch(b, -1.0, stream.cuda_stream)
+        te += int(pq.wait_batch().te)
+    for _ in range(args.warmup):
+        for b in batches:
+            pq.launch_batch(b, -1.0, stream.cuda_stream)
+            pq.wait_batch()
+    sampler = None
+    if not args.profile:
+        phys = os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[local_rank]
+        sampler = ClockSampler(phys)
+        sampler.start()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ms = 0.0
+    launches = 0
+    for k in range(args.steps):
+        for i, b in enumerate(batches):
+            _timed_flush(flush, k + i)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            pq.launch_batch(b, -1.0, stream.cuda_stream)
+            e1.record(stream)
+            st = pq.wait_batch()
+            launches += 1
+            ms += e0.elapsed_time(e1)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = sampler.stop() if sampler else None
+    ms_max, te_all = reduce_timing(ms, te * args.steps, dev)
+    pq.close()
+    if rank != 0:
+        return None
+    return {
+        "metric": METRIC, "value": te_all / (ms_max / 1e3) / 1e9, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic",
+        "config": {**workload_config(args, sg, all_sources[:4] + ["..."], world),
+                   "sources_total": len(all_sources), "sources_per_rank": per,
+                   "parallelism": f"{world} GPU(s), sources sharded over ranks, 32 per batch-kernel launch"},
+        "mode": "batch", "gpu_launches": launches, "clocks": clocks,
+    }
+
+
 def main():
     args = parse_args()
+    _AUTOMATON_KIND[0] = args.automaton
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         out = run_reference(args, rank, world)
     else:
-        if world > 1:
+        dist_needed = world > 1 or args.mode == "partitioned"
+        if dist_needed:
             import torch
 
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29511")
+            os.environ.setdefault("RANK", str(rank))
+            os.environ.setdefault("WORLD_SIZE", str(world))
             torch.cuda.set_device(local_rank)
             torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        out = run_engine(args, rank, world, local_rank)
-        if world > 1:
+        if args.mode == "partitioned":
+            out = run_partitioned(args, rank, world, local_rank)
+        elif args.mode == "batch":
+            out = run_batch_mode(args, rank, world, local_rank)
+        else:
+            out = run_engine(args, rank, world, local_rank)
+        if dist_needed:
             import torch
 
             torch.distributed.destroy_process_group()

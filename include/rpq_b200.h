@@ -232,6 +232,14 @@ RPQ_API int rpq_query_row_words(const rpq_query* q, int64_t* row_words);
  * words, distinct.  Asynchronous; rpq_query_wait returns its status. */
 RPQ_API int rpq_query_step_device(rpq_query* q, const uint32_t* d_m, uint32_t* d_p, uint32_t* d_out,
                                   void* stream);
+/* A chain of device steps (one partitioned query): rpq_query_step_begin zeroes
+ * the chain's accumulator on `stream`; consecutive rpq_query_step_device calls
+ * with unchanged options then enqueue without any host round trip (each step
+ * whose M is non-empty counts one iteration of the masked loop, and a failed
+ * step latches its status); rpq_query_step_end waits and returns the count
+ * and the first failure.  engine.py:157-160 (`while m.nnz` iterations). */
+RPQ_API int rpq_query_step_begin(rpq_query* q, void* stream);
+RPQ_API int rpq_query_step_end(rpq_query* q, int64_t* steps);
 /* Output mode: 0 (default) keeps the answer on the device; 1 also copies the
  * answer bitmap (ceil(nv/32) uint32 words, bit v%32 of word v/32) into pinned
  * host memory as part of every run, ready after rpq_query_wait. */

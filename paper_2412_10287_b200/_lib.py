@@ -160,6 +160,8 @@ ENGINE_SIGNATURES = {
     "rpq_query_step": (c_i32, [c_vp, P_u32, P_u32, c_i64, P_u32]),
     "rpq_query_set_output": (c_i32, [c_vp, c_i32]),
     "rpq_host_alloc": (c_i32, [c_i64, ctypes.POINTER(c_vp)]),
+    "rpq_query_step_begin": (c_i32, [c_vp, c_vp]),
+    "rpq_query_step_end": (c_i32, [c_vp, ctypes.POINTER(c_i64)]),
     "rpq_host_free": (c_i32, [c_vp]),
     "rpq_query_copy_reach_bits": (c_i32, [c_vp, P_u32, c_i64]),
     "rpq_query_io_bytes": (c_i32, [c_vp, P_i64, P_i64]),

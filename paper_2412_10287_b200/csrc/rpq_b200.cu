@@ -151,6 +151,9 @@ struct rpq_query {
     bool ran = false;
     uint64_t edge_bound = 0;  // sum over groups of the slot's nnz
     unsigned long long* d_trace = nullptr;  // diagnostics (RPQ_TUNE_TRACE)
+    unsigned int* d_step_acc = nullptr;     // step runs: non-empty steps, sticky failure status
+    RunArgs step_ra{};                      // the input block of the last step_device run
+    bool step_ra_valid = false;             // ... is what h_in holds (identical runs need no sync)
     int trace_levels = 0;
 
     // multi-source batch workspace (batch_kernel.cuh), allocated on first use
@@ -403,6 +406,7 @@ void free_query_buffers(rpq_query* q) {
     }
 
     if (q->d_ctl) cudaFree(q->d_ctl);
+    if (q->d_step_acc) cudaFree(q->d_step_acc);
     if (q->h_ctl) cudaFreeHost(q->h_ctl);
     if (q->d_reach) cudaFree(q->d_reach);
     if (q->d_reach_bits) cudaFree(q->d_reach_bits);
@@ -818,6 +822,8 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
         QTRY(cudaMemset(q->d_seg[b], 0, (size_t)q->seg_alloc * sizeof(uint2)));
     }
     QTRY(cudaMalloc(&q->d_ctl, sizeof(Ctl)));
+    QTRY(cudaMalloc(&q->d_step_acc, 2 * sizeof(unsigned int)));
+    QTRY(cudaMemset(q->d_step_acc, 0, 2 * sizeof(unsigned int)));
     QTRY(cudaMallocHost(&q->h_ctl, sizeof(Ctl)));
     QTRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&q->h_ctl_dev), q->h_ctl, 0));
     QTRY(cudaMalloc(&q->d_reach, (size_t)(q->W * 32 + 32)));
@@ -909,6 +915,7 @@ Params make_params(const rpq_query* q) {
     p.table_ints = (int)q->tables.size();
     p.trace = q->d_trace;
     p.trace_levels = q->d_trace ? q->trace_levels : 0;
+    p.step_acc = q->d_step_acc;
     return p;
 }
 
@@ -1078,6 +1085,7 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     else
         ra.budget_ns = (unsigned long long)(timeout_s * 1e9);
     *reinterpret_cast<RunArgs*>(q->h_in) = ra;
+    q->step_ra_valid = false;
     if (!q->graph_failed) build_graph(q);
     // timing events bracket the whole run (graph event nodes cannot be timed)
     CUDA_TRY(cudaEventRecord(q->ev0, st));
@@ -1256,6 +1264,7 @@ int rpq_query_step(rpq_query* q, const uint32_t* m_words, const uint32_t* p_word
     ra.budget_ns = ~0ull;
     ra.bar_base = q->bar_next;
     *reinterpret_cast<RunArgs*>(q->h_in) = ra;
+    q->step_ra_valid = false;
     CUDA_TRY(cudaEventRecord(q->ev0, st));
     CUDA_TRY(enqueue_run(q, st));
     CUDA_TRY(cudaEventRecord(q->ev1, st));
@@ -1302,7 +1311,22 @@ int rpq_query_step_device(rpq_query* q, const uint32_t* d_m, uint32_t* d_p, uint
     if (d_out == d_m || d_out == d_p || d_m == d_p) return fail(RPQ_EINVAL, "M, P and the output must be distinct");
     if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
     cudaStream_t st = stream ? (cudaStream_t)stream : q->own_stream;
-    if (q->inflight) {  // the pinned input block is read by the previous run's copy
+    RunArgs ra{};
+    ra.mode = 1;
+    ra.dir_mode = q->dir_mode;  // auto: pull when M is dense against the owned targets
+    ra.alpha = q->alpha;
+    ra.budget_ns = ~0ull;
+    ra.bar_base = 0;  // the last CTA of every run resets the barrier counter
+    ra.flags = q->run_flags;
+    ra.defer_alpha = q->defer_alpha;
+    ra.own_w0 = q->own_w0;
+    ra.own_w1 = q->own_w1;
+    // consecutive steps with the same arguments on the same stream reuse the
+    // pinned input block as it is: no host round trip between levels (a
+    // failed step latches its status in step_acc, read by rpq_query_step_end)
+    const bool same = q->step_ra_valid && q->inflight && q->last_stream == st &&
+                      std::memcmp(&q->step_ra, &ra, sizeof(RunArgs)) == 0;
+    if (q->inflight && !same) {  // the pinned input block is read by the previous run's copy
         CUDA_TRY(cudaStreamSynchronize(q->last_stream));
         q->bar_next = q->h_ctl->bar;
         q->inflight = false;
@@ -1313,17 +1337,11 @@ int rpq_query_step_device(rpq_query* q, const uint32_t* d_m, uint32_t* d_p, uint
         if (prev == ST_DEADLOCK) return fail(RPQ_ECUDA, "internal: grid barrier spin limit exceeded (previous step)");
         if (prev != 0) return fail(RPQ_ECUDA, "previous step failed with kernel status " + std::to_string(prev));
     }
-    RunArgs ra{};
-    ra.mode = 1;
-    ra.dir_mode = q->dir_mode;  // auto: pull when M is dense against the owned targets
-    ra.alpha = q->alpha;
-    ra.budget_ns = ~0ull;
-    ra.bar_base = q->bar_next;
-    ra.flags = q->run_flags;
-    ra.defer_alpha = q->defer_alpha;
-    ra.own_w0 = q->own_w0;
-    ra.own_w1 = q->own_w1;
-    *reinterpret_cast<RunArgs*>(q->h_in) = ra;
+    if (!same) {
+        *reinterpret_cast<RunArgs*>(q->h_in) = ra;
+        q->step_ra = ra;
+    }
+    q->step_ra_valid = true;
     // the caller's buffers stand in for P and F_0 / F_1; F_2 is the query's
     // (step mode reads F_0, writes F_1, zeroes F_1 and F_2 first, keeps P)
     Params p = make_params(q);
@@ -1337,6 +1355,31 @@ int rpq_query_step_device(rpq_query* q, const uint32_t* d_m, uint32_t* d_p, uint
     q->last_stream = st;
     q->ran = true;
     q->inflight = true;
+    return RPQ_OK;
+}
+
+int rpq_query_step_begin(rpq_query* q, void* stream) {
+    if (!q) return fail(RPQ_EINVAL, "null query");
+    if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+    cudaStream_t st = stream ? (cudaStream_t)stream : q->own_stream;
+    CUDA_TRY(cudaMemsetAsync(q->d_step_acc, 0, 2 * sizeof(unsigned int), st));
+    return RPQ_OK;
+}
+
+int rpq_query_step_end(rpq_query* q, int64_t* steps) {
+    if (!q) return fail(RPQ_EINVAL, "null query");
+    if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+    if (q->inflight) {
+        CUDA_TRY(cudaStreamSynchronize(q->last_stream));
+        q->bar_next = q->h_ctl->bar;
+        q->inflight = false;
+    }
+    unsigned acc[2] = {0, 0};
+    CUDA_TRY(cudaMemcpy(acc, q->d_step_acc, sizeof(acc), cudaMemcpyDeviceToHost));
+    if (steps) *steps = (int64_t)acc[0];
+    if (acc[1] == (unsigned)ST_OVERFLOW) return fail(RPQ_ECUDA, "internal: frontier queue capacity exceeded (a step)");
+    if (acc[1] == (unsigned)ST_DEADLOCK) return fail(RPQ_ECUDA, "internal: grid barrier spin limit exceeded (a step)");
+    if (acc[1] != 0) return fail(RPQ_ECUDA, "a step failed with kernel status " + std::to_string(acc[1]));
     return RPQ_OK;
 }
 

@@ -85,7 +85,7 @@ struct FCnt {
 
 struct Ctl {
     // ---- results prefix: the only part copied back to the host ------------
-    unsigned int bar;        // monotonic barrier arrivals (never reset: runs continue from bar_base)
+    unsigned int bar;        // barrier arrivals of this run (the last CTA out resets it to 0)
     int abort;
     unsigned long long t0;
     int status;              // written by CTA 0 only, as are the fields below
@@ -166,6 +166,8 @@ struct Params {
     int maxT;
     int table_ints;
     unsigned long long* trace;  // diagnostics: [level][cta][4] globaltimer stamps, or null
+    unsigned int* step_acc;     // step mode: [0] steps that found M non-empty, [1] sticky failure
+                                // status of any step (zeroed by rpq_query_step_begin)
     int trace_levels;
 };
 
@@ -1357,6 +1359,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
                 s_front[q] = ldcg(&ctl->fc[0].state[q]);
                 nf += s_front[q];
             }
+            if (cta0 && nf && p.step_acc) atomicAdd(p.step_acc, 1u);  // an iteration of the masked loop
             int ntarget = 0;
             for (int q2 = 0; q2 < p.nstates; ++q2) {
                 bool t = false;
@@ -1737,9 +1740,13 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
         }
     }
 
-    // zero-copy results: the last CTA out copies the results prefix (everything
-    // before the working counters) to pinned host memory
-    if (p.host_ctl) {
+    // The last CTA out: every CTA is past its last barrier, so it resets the
+    // barrier counter for the next run on this query (runs on one query are
+    // stream-ordered: no host round trip for the next run's barrier base);
+    // zero-copy results: it copies the results prefix (everything before the
+    // working counters) to pinned host memory; step mode: a failed step
+    // latches its status for rpq_query_step_end.
+    {
         __shared__ int s_last;
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -1749,11 +1756,21 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
         __syncthreads();
         if (s_last) {
             __threadfence();
-            constexpr int nw = (int)(offsetof(Ctl, qc) / 4);
-            const unsigned* src = reinterpret_cast<const unsigned*>(ctl);
-            unsigned* dst = reinterpret_cast<unsigned*>(p.host_ctl);
-            for (int i = threadIdx.x; i < nw; i += blockDim.x) dst[i] = __ldcg(src + i);
-            __threadfence_system();
+            if (p.host_ctl) {
+                constexpr int nw = (int)(offsetof(Ctl, qc) / 4);
+                const unsigned* src = reinterpret_cast<const unsigned*>(ctl);
+                unsigned* dst = reinterpret_cast<unsigned*>(p.host_ctl);
+                for (int i = threadIdx.x; i < nw; i += blockDim.x) dst[i] = i == 0 ? 0u : __ldcg(src + i);
+                __threadfence_system();
+            }
+            if (threadIdx.x == 0) {
+                if (step_mode && p.step_acc) {
+                    const int st = ldcg(&ctl->status);
+                    if (st != 0) atomicCAS(p.step_acc + 1, 0u, (unsigned)st);
+                }
+                ctl->bar = 0;
+                ctl->exits = 0;
+            }
         }
     }
 }

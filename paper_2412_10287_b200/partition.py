@@ -206,6 +206,21 @@ class DeviceStep:
         raise_for_status(_lib.engine().rpq_query_step_device(self.pq.q, m.data_ptr(), p.data_ptr(),
                                                              out.data_ptr(), stream), "rpq_query_step_device")
 
+    def begin(self, stream):
+        """Start a chain of steps on `stream` (zeroes the chain's counters)."""
+        from .engine import raise_for_status
+
+        raise_for_status(_lib.engine().rpq_query_step_begin(self.pq.q, stream), "rpq_query_step_begin")
+
+    def count(self):
+        """Wait for the chain so far: the steps whose M was non-empty (raises
+        if any step of the chain failed)."""
+        from .engine import raise_for_status
+
+        n = ctypes.c_int64()
+        raise_for_status(_lib.engine().rpq_query_step_end(self.pq.q, ctypes.byref(n)), "rpq_query_step_end")
+        return int(n.value)
+
     def finish(self):
         """Status of the last step (raises on failure); its device time in ms."""
         from .engine import raise_for_status
@@ -268,7 +283,13 @@ def run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout=mat
     return _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, None, profile, bits)
 
 
-def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, stream, profile, bits):
+def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, stream, profile, bits,
+                depth=4):
+    """The masked loop, `depth` levels enqueued per host check: each step
+    counts (on the device) whether its M was non-empty, and once one finds M
+    empty every later step does too (its output stays zero), so the host
+    waits only once per `depth` levels and the iteration count is exact.
+    profile=True checks after every level (per-level timings)."""
     import torch
 
     t0 = time.monotonic()
@@ -277,7 +298,11 @@ def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, s
     row_words = shards[0].row_words
     k = len(ranges)
     wmax = max(max(w1 - w0 for w0, w1 in ranges), 1)
-    m = torch.zeros((nstates, row_words), dtype=torch.int32, device=dev)
+    m = getattr(shards[0], "_m", None)
+    if m is None or tuple(m.shape) != (nstates, row_words):
+        m = torch.zeros((nstates, row_words), dtype=torch.int32, device=dev)
+    else:
+        m.zero_()
     # one shard owning everything: the step's output IS the next frontier (no exchange)
     alone = k == 1 and len(shards) == 1
     send = [torch.zeros((nstates, wmax), dtype=torch.int32, device=dev) for _ in shards] if not alone else []
@@ -290,33 +315,53 @@ def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, s
         for sh in shards:
             if sh.w0 <= sw < sh.w1:
                 sh.p[q, sw] |= sb
-    iterations = 0
+    counted = hasattr(shards[0].step, "count")
+    if counted:
+        for sh in shards:
+            sh.step.begin(stream)
     levels_us = []
     step_ms = []  # profile: per level, each local shard's step kernel time
     sync = (lambda: torch.cuda.synchronize(dev)) if m.is_cuda else (lambda: None)
-    while bool(m.any()):
+    if not counted or profile:
+        depth = 1
+    enqueued = 0
+    iterations = 0
+    while True:
+        if not counted and not bool(m.any()):
+            break
         if time.monotonic() - t0 > timeout:  # _Clock.check, engine.py:87-89
             from .engine import QueryTimeout
 
             raise QueryTimeout(time.monotonic() - t0, iterations)
-        iterations += 1
-        for sh in shards:
-            sh.step(m, sh.p, sh.next, stream)
-        if alone:
-            m, shards[0].next = shards[0].next, m  # the step zeroes its output first
-        else:
-            for sh, sl in zip(shards, send):
-                sl[:, : sh.w1 - sh.w0].copy_(sh.next[:, sh.w0: sh.w1])
-            gathered = exchange.allgather(send)
-            for r, (w0, w1) in enumerate(ranges):
-                m[:, w0:w1].copy_(gathered[r, :, : w1 - w0])
+        for _ in range(depth):
+            for sh in shards:
+                sh.step(m, sh.p, sh.next, stream)
+            enqueued += 1
+            if alone:
+                m, shards[0].next = shards[0].next, m  # the step zeroes its output first
+            else:
+                for sh, sl in zip(shards, send):
+                    sl[:, : sh.w1 - sh.w0].copy_(sh.next[:, sh.w0: sh.w1])
+                gathered = exchange.allgather(send)
+                for r, (w0, w1) in enumerate(ranges):
+                    m[:, w0:w1].copy_(gathered[r, :, : w1 - w0])
         if profile:
             sync()
             levels_us.append((time.monotonic() - t0) * 1e6)
             step_ms.append([sh.step.finish() if hasattr(sh.step, "finish") else 0.0 for sh in shards])
+        if counted:
+            iterations = shards[0].step.count()  # waits for the enqueued levels
+            if iterations < enqueued:
+                break
+        else:
+            iterations = enqueued
+    shards[0]._m = m
     for sh in shards:
         if hasattr(sh.step, "finish"):
             sh.step.finish()
+    if profile:
+        levels_us = levels_us[: iterations + 1]
+        step_ms = step_ms[: iterations + 1]
     # answer: OR over final states of each owner's P, gathered
     slices = []
     for sh in shards:
@@ -331,7 +376,7 @@ def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, s
     g_host = gathered.cpu().numpy().view(np.uint32)
     for r, (w0, w1) in enumerate(ranges):
         words[w0:w1] = g_host[r, 0, : w1 - w0]
-    stats = {"levels_wall_us": levels_us, "ranges": ranges, "step_ms": step_ms}
+    stats = {"levels_wall_us": levels_us, "ranges": ranges, "step_ms": step_ms, "enqueued": enqueued}
     if bits:
         return words, iterations, stats
     return np.unpackbits(words.view(np.uint8), bitorder="little")[:nv], iterations, stats
@@ -344,31 +389,81 @@ def _or_rows(t):
     return acc
 
 
+class PartitionedQuery:
+    """One automaton on a vertex-partitioned graph, evaluated from many
+    sources: the partition, this rank's graph (upload + device CSR/CSC), its
+    step kernel and the bitmaps are built once.  One shard per
+    torch.distributed rank (device = the rank's current CUDA device)."""
+
+    def __init__(self, g, n, group=None, device=None):
+        import torch
+
+        self.g, self.n = g, n
+        self.exchange = DistExchange(group)
+        self.table = transition_table(n, g.num_labels)
+        self.ranges = partition_words(target_weights(g, self.table), self.exchange.world)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.shard = Shard(g, n, self.ranges, self.exchange.rank, dev)
+
+    def run(self, source, timeout=math.inf, profile=False):
+        """(answer bitmap words, masked-loop iterations, stats)."""
+        return run_levels([self.shard], self.exchange, self.ranges, self.g.num_vertices,
+                          self.table.starts.tolist(), self.table.finals.tolist(), int(source), timeout,
+                          profile=profile, bits=True)
+
+    def close(self):
+        if self.shard is not None:
+            self.shard.step.close()
+            self.shard = None
+
+
+_PARTITIONED = {}  # (id(g), id(n), group, world, rank, device) -> (weakrefs, PartitionedQuery)
+
+
+def partitioned_query(g, n, group=None):
+    """The cached PartitionedQuery of (g, n) on this rank (graphs and compiled
+    automata are not mutated after construction; the entry dies with them)."""
+    import weakref
+
+    import torch.distributed as dist
+    import torch
+
+    key = (id(g), id(n), id(group), dist.get_world_size(group), dist.get_rank(group), torch.cuda.current_device())
+    hit = _PARTITIONED.get(key)
+    if hit is not None and hit[0]() is g and hit[1]() is n:
+        return hit[2]
+    pq = PartitionedQuery(g, n, group)
+    try:
+        refs = (weakref.ref(g, lambda _r, k=key: _drop(k)), weakref.ref(n, lambda _r, k=key: _drop(k)))
+    except TypeError:
+        return pq
+    _PARTITIONED[key] = (refs[0], refs[1], pq)
+    return pq
+
+
+def _drop(key):
+    hit = _PARTITIONED.pop(key, None)
+    if hit is not None:
+        hit[2].close()
+
+
 def eval_ssr_partitioned(g, n, source, opts=None, group=None):
     """eval_ssr over vertex-partitioned ranks: one shard per torch.distributed
     rank (device = the rank's current CUDA device).  Returns the same
-    EvalResult as eval_ssr (iterations counted like the masked loop)."""
-    import torch
-
-    from .engine import _SSR_EVALUATORS, EngineOptions, EvalResult, _check_vertex, _iterations_for
+    EvalResult as eval_ssr: the caller's algorithm tag and that algorithm's
+    iteration count (engine._iterations_for of the masked count)."""
+    from .engine import _SSR_EVALUATORS, EngineOptions, EvalResult, QueryTimeout, _check_vertex, _iterations_for
 
     opts = opts or EngineOptions()
     opts.validate()
     if opts.algorithm not in _SSR_EVALUATORS:  # engine.py:246-250
         raise ValueError(f"algorithm {opts.algorithm!r} does not evaluate compiled automata")
     _check_vertex(g, source)
-    ex = DistExchange(group)
-    table = transition_table(n, g.num_labels)
-    ranges = partition_words(target_weights(g, table), ex.world)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    sh = Shard(g, n, ranges, ex.rank, dev)
     t0 = time.monotonic()
-    try:
-        words, its, _ = run_levels([sh], ex, ranges, g.num_vertices, table.starts.tolist(),
-                                   table.finals.tolist(), int(source), opts.timeout, bits=True)
-    finally:
-        sh.step.close()
-    # the device loop counts like the masked one; each algorithm's own count
-    # follows from it (engine._iterations_for), and the tag is the caller's
+    pq = partitioned_query(g, n, group)
+    table = pq.table
+    if table.starts.size and opts.timeout <= 0:  # _Clock.check(0), engine.py:87-89
+        raise QueryTimeout(time.monotonic() - t0, 0)
+    words, its, _ = pq.run(int(source), opts.timeout)
     return EvalResult(None, _iterations_for(opts.algorithm, its, table.starts.size), time.monotonic() - t0,
                       opts.algorithm, bits=words, nv=g.num_vertices)
