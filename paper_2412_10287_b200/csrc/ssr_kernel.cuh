@@ -973,22 +973,55 @@ __device__ unsigned long long frontier_edges(const Params& p, const Smem& S, con
 // edges per round up to kPullCont edges; rows still undecided after that
 // (rare: < 1% on cfg3) are scanned by the whole warp, 128 edges per step.
 constexpr int kPullCont = 8;
+//
+// Layout: a task covers PV words = 32*PV vertices; lane l owns the PV
+// consecutive vertices v0 = 32*word0 + PV*l ... v0 + PV - 1, so its row
+// pointers rowptr[v0 .. v0+PV] are PV/4 128-bit loads plus one shuffle (the
+// next lane's first), and its P / found bits are a PV-bit field of one word.
+template <int PV>
+__device__ __forceinline__ void load_rows(const uint32_t* rp, long long v0, int nv, int lane, uint32_t (&r)[PV + 1]) {
+    if (v0 + PV <= nv) {
+        const uint4* r4 = reinterpret_cast<const uint4*>(rp + v0);  // v0 % PV == 0: 16-byte aligned
+#pragma unroll
+        for (int c = 0; c < PV / 4; ++c) {
+            uint4 x;
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(r4 + c));
+            r[4 * c] = x.x;
+            r[4 * c + 1] = x.y;
+            r[4 * c + 2] = x.z;
+            r[4 * c + 3] = x.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < PV; ++j) r[j] = v0 + j <= nv ? __ldg(rp + v0 + j) : 0u;
+    }
+    // rowptr[v0 + PV]: the next lane's first (lane 31 and the tail load it)
+    const uint32_t nx = __shfl_down_sync(FULL, r[0], 1);
+    r[PV] = (lane < 31 && v0 + PV <= nv) ? nx : (v0 + PV <= nv ? __ldg(rp + v0 + PV) : r[PV - 1]);
+#pragma unroll
+    for (int j = 1; j <= PV; ++j)  // past the end: empty rows
+        if (v0 + j > nv) r[j] = r[j - 1];
+}
+
 template <int PV>
 __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const uint32_t* fcur, uint32_t* fnext,
                                            long long pw0, long long pw1, int lane, unsigned* s_task,
                                            int s_nptarget, const int* s_ptarget, const unsigned int* s_front,
                                            unsigned int* s_state, unsigned long long& nnew,
                                            unsigned long long* steal, uint32_t* scratch, int first) {
+    constexpr int LPW = 32 / PV;  // lanes per word
     const long long nblk = (pw1 - pw0 + PV - 1) / PV;
     const long long ntask = (long long)s_nptarget * nblk;
     const long long G = gridDim.x;
     const long long nown = ntask >= 16 * G ? (ntask - ntask / 4) / G * G : ntask;
-    // warp scratch: candidate (u << 5 | lane, bit 31: long row), row start, row end; found words
+    // warp scratch: candidate vertex offset (bit 31: long row), row start, row end; found words
     uint32_t* cid = scratch;
     uint32_t* clo = scratch + 32 * PV;
     uint32_t* chi = scratch + 64 * PV;
     uint32_t* cfound = scratch + 96 * PV;
-    const unsigned lt = lanemask_lt();
+    const uint32_t fmask_all = (1u << PV) - 1u;
+    const int sh = PV * (lane % LPW);  // this lane's bit offset in its word
     for (;;) {
         long long task = 0;
         if (lane == 0) {
@@ -1000,32 +1033,26 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
         if (task >= ntask) break;
         const int q2 = s_ptarget[task / nblk];
         const long long word0 = pw0 + (task % nblk) * PV;
+        const long long myword = word0 + lane / LPW;
+        const long long v0 = word0 * 32 + (long long)PV * lane;
         // the first pulled in-slot (warp-uniform): its row pointers do not
-        // depend on P, so they are loaded with P's words (coalesced, one
-        // dependent round trip less per task; visited vertices' are wasted)
+        // depend on P, so they are loaded with P's words (one dependent round
+        // trip less per task; visited vertices' are wasted)
         int k0 = -1;
         for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k)
             if (s_front[S.isrc[k]]) {
                 k0 = k;
                 break;
             }
-        uint32_t need = 0, found = 0;  // bit u: this lane's vertex of word u
-        uint32_t lo[PV], hi[PV];
-        {
-            uint32_t vis[PV];
-            const uint32_t* rp = S.slots[p.nslots + S.islot[max(k0, 0)]].rowptr;
-#pragma unroll
-            for (int u = 0; u < PV; ++u) {
-                const int w = (int)((word0 + u) * 32 + lane);
-                const bool in = word0 + u < pw1 && w < p.nv;
-                vis[u] = word0 + u < pw1 ? ld_bits(p.visited + (long long)q2 * p.W + word0 + u, S.pl) : 0xFFFFFFFFu;
-                lo[u] = in && k0 >= 0 ? ld_stream_u32(rp + w, S.pf) : 0u;
-                hi[u] = in && k0 >= 0 ? ld_stream_u32(rp + w + 1, S.pf) : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < PV; ++u)
-                if ((int)((word0 + u) * 32 + lane) < p.nv && !((vis[u] >> lane) & 1u)) need |= 1u << u;
-        }
+        uint32_t r[PV + 1];
+        const uint32_t pw = myword < pw1 ? ld_bits(p.visited + (long long)q2 * p.W + myword, S.pl) : 0xFFFFFFFFu;
+        load_rows<PV>(S.slots[p.nslots + S.islot[max(k0, 0)]].rowptr, v0, p.nv, lane, r);
+        // need: this lane's unvisited vertices (PV bits)
+        uint32_t need = ~(pw >> sh) & fmask_all;
+        if (v0 >= p.nv) need = 0;
+        else if (v0 + PV > p.nv) need &= (1u << (p.nv - v0)) - 1u;
+        if (myword >= pw1) need = 0;
+        uint32_t found = 0;
         if (__ballot_sync(FULL, need != 0) == 0) continue;
         for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k) {
             const int q = S.isrc[k];
@@ -1034,29 +1061,24 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
             if (__ballot_sync(FULL, look != 0) == 0) break;
             const Slot ps = S.slots[p.nslots + S.islot[k]];
             const uint32_t* frow = fcur + (long long)q * p.W;
-            if (k != k0) {
-#pragma unroll
-                for (int u = 0; u < PV; ++u) {
-                    const int w = (int)((word0 + u) * 32 + lane);
-                    const bool lk = (look >> u) & 1u;
-                    lo[u] = lk ? ld_stream_u32(ps.rowptr + w, S.pf) : 0u;
-                    hi[u] = lk ? ld_stream_u32(ps.rowptr + w + 1, S.pf) : 0u;
-                }
-            }
+            if (k != k0) load_rows<PV>(ps.rowptr, v0, p.nv, lane, r);
             // compaction: the looking vertices with in-edges in this slot
-            int n = 0;
+            uint32_t cm = 0;
 #pragma unroll
-            for (int u = 0; u < PV; ++u) {
-                const bool c = ((look >> u) & 1u) && hi[u] > lo[u];
-                const unsigned m = __ballot_sync(FULL, c);
-                if (c) {
-                    const int pos = n + __popc(m & lt);
-                    cid[pos] = (uint32_t)(u << 5 | lane);
-                    clo[pos] = lo[u];
-                    chi[pos] = hi[u];
+            for (int j = 0; j < PV; ++j)
+                if (((look >> j) & 1u) && r[j + 1] > r[j]) cm |= 1u << j;
+            const uint32_t cnt = __popc(cm);
+            const uint32_t incl = warp_incl_scan(cnt, lane);
+            const int n = (int)__shfl_sync(FULL, incl, 31);
+            int pos = (int)(incl - cnt);
+#pragma unroll
+            for (int j = 0; j < PV; ++j)
+                if ((cm >> j) & 1u) {
+                    cid[pos] = (uint32_t)(PV * lane + j);
+                    clo[pos] = r[j];
+                    chi[pos] = r[j + 1];
+                    ++pos;
                 }
-                n += __popc(m);
-            }
             if (lane < PV) cfound[lane] = 0u;
             __syncwarp();
             bool any_long = false;
@@ -1124,20 +1146,16 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
                 }
             }
             __syncwarp();
-#pragma unroll
-            for (int u = 0; u < PV; ++u) found |= ((cfound[u] >> lane) & 1u) << u;
+            found |= (cfound[lane / LPW] >> sh) & fmask_all;
             __syncwarp();  // cfound / the candidate list are rewritten by the next slot or task
         }
         // the warp owns these (q2, word) pairs this epoch: F is a plain store,
-        // P an OR without return; lane u writes word u
-        uint32_t fm = 0;
+        // P an OR without return; the first lane of each word writes it
+        uint32_t fm = found << sh;
 #pragma unroll
-        for (int u = 0; u < PV; ++u) {
-            const unsigned m = __ballot_sync(FULL, (found >> u) & 1u);
-            if (lane == u) fm = m;
-        }
-        if (lane < PV && fm) {
-            const long long voff = (long long)q2 * p.W + word0 + lane;
+        for (int d = 1; d < LPW; d <<= 1) fm |= __shfl_xor_sync(FULL, fm, d);
+        if (lane % LPW == 0 && fm) {
+            const long long voff = (long long)q2 * p.W + myword;
             red_or_bits(p.visited + voff, fm, S.pl);
             fnext[voff] = fm;
             nnew += __popc(fm);
