@@ -475,7 +475,7 @@ def run_engine(args, rank, world, local_rank):
     b_step = sum(work[s]["bytes"] for s in sources)
 
     # e2e through the public API: automaton H2D + kernel + answer D2H per call
-    e2e_s, set_ms, e2e_dev_ms, d2h_answer, e2e_host_us = [], [], [], {}, []
+    e2e_s, set_ms, e2e_dev_ms, d2h_answer, e2e_host_us, view_us = [], [], [], {}, [], []
     nwords = (sg.nv + 31) // 32
     if not args.profile:
         opts = P.EngineOptions(timeout=math.inf, direction=args.direction, alpha=alpha)
@@ -499,7 +499,12 @@ def run_engine(args, rank, world, local_rank):
                     d2h_answer[s] = 8 * nz if 2 * nz < nwords else 4 * nwords
                 if k == 0:
                     assert np.array_equal(res.reach, work[s]["reach"])
-                    # the reference's result type: set[int] built from the answer
+                    # the reference's result type: set[int] built from the answer,
+                    # and the lazy set view a drop-in shim returns instead
+                    t = time.perf_counter()
+                    view = res.answer_set
+                    assert len(view) == int(work[s]["st0"].reach_count)
+                    view_us.append(1e6 * (time.perf_counter() - t))
                     t = time.perf_counter()
                     _ = res.reachable
                     set_ms.append(1e3 * (time.perf_counter() - t))
@@ -573,6 +578,7 @@ def run_engine(args, rank, world, local_rank):
                       "host_us_per_query": {"median": statistics.median(e2e_host_us),
                                             "mean": statistics.mean(e2e_host_us)} if e2e_host_us else None,
                       "reachable_set_ms_per_query": statistics.mean(set_ms) if set_ms else None,
+                      "answer_set_view_us_per_query": statistics.mean(view_us) if view_us else None,
                       "note": ("eval_ssr per source with host buffers: automaton tables H2D, the answer D2H as "
                                "the bitmap or, when sparse, (word, bits) pairs; device_ms = the calls' own "
                                "CUDA-event time; reachable_set_ms = building the reference's set[int] from the "

@@ -15,6 +15,7 @@ much of P they re-expand), so all three run the same device BFS; the
 loop's own accounting.  There is no CPU path: the CUDA library must load.
 """
 
+import collections.abc
 import ctypes
 import dataclasses
 import math
@@ -76,6 +77,43 @@ class EngineOptions:
             raise ValueError("switch threshold must be >= 0")
 
 
+class AnswerSet(collections.abc.Set):
+    """A read-only ``set[int]`` view of an answer as the device returned it
+    (bitmap or sparse pairs): membership is one bit test, ``len`` the device's
+    answer count, iteration decodes on demand.  Compares equal to the
+    reference's ``set`` of the same vertices.  For callers that would
+    otherwise build the reference's ``reachable`` set (about 0.05 us per
+    answer vertex in CPython: 120 ms for cfg3's 2.3M answers)."""
+
+    __slots__ = ("_res",)
+
+    def __init__(self, res):
+        self._res = res
+
+    def __contains__(self, v):
+        try:
+            v = int(v)
+        except (TypeError, ValueError):
+            return False
+        res = self._res
+        if not 0 <= v < res._nv:
+            return False
+        if res._reachable is not None:
+            return v in res._reachable
+        return bool((int(res.bits[v >> 5]) >> (v & 31)) & 1)
+
+    def __len__(self):
+        return self._res.count
+
+    def __iter__(self):
+        return iter(np.flatnonzero(self._res.reach).tolist())
+
+    def __repr__(self):
+        return f"AnswerSet(|V|={self._res._nv}, size={len(self)})"
+
+    __hash__ = None
+
+
 class EvalResult:
     """Result of one evaluation (engine.py:71-76).
 
@@ -83,9 +121,12 @@ class EvalResult:
     first access from ``reach``, the device's ``uint8[|V|]`` answer vector.
     """
 
-    __slots__ = ("_reach", "_bits", "_pairs", "_nv", "_reachable", "iterations", "elapsed", "algorithm", "stats")
+    __slots__ = ("_reach", "_bits", "_pairs", "_nv", "_reachable", "_count", "iterations", "elapsed", "algorithm",
+                 "stats")
 
-    def __init__(self, reach, iterations, elapsed, algorithm, stats=None, bits=None, nv=None, pairs=None):
+    def __init__(self, reach, iterations, elapsed, algorithm, stats=None, bits=None, nv=None, pairs=None,
+                 count=None):
+        self._count = count  # |answer| as counted on the device, if known
         self._reach = reach
         self._bits = bits  # answer bitmap as read back from the device (uint32 words)
         self._pairs = pairs  # or a sparse answer as read back: (word index, word) uint32 pairs
@@ -115,6 +156,22 @@ class EvalResult:
             packed = np.concatenate([packed, np.zeros(-packed.size % 4, dtype=np.uint8)])
             self._bits = packed.view(np.uint32)
         return self._bits
+
+    @property
+    def count(self):
+        """|answer| (the device's count when it came with the result)."""
+        if self._count is None:
+            if self._reachable is not None:
+                self._count = len(self._reachable)
+            else:
+                self._count = int(np.bitwise_count(self.bits).sum()) if self._nv else 0
+        return self._count
+
+    @property
+    def answer_set(self):
+        """The answer as a lazy read-only set (AnswerSet): what a drop-in shim
+        hands to the reference's EvalResult instead of building ``reachable``."""
+        return AnswerSet(self)
 
     @property
     def reachable(self):
@@ -288,7 +345,7 @@ def _run(g, n, source, opts, tag, *, want_stats=False):
         dg.release_query(table, q)
     return EvalResult(None, iterations, time.monotonic() - t0, tag,
                       stats.to_dict() if want_stats or opts.debug_checks or opts.count_te else None,
-                      bits=words, nv=g.num_vertices, pairs=pairs)
+                      bits=words, nv=g.num_vertices, pairs=pairs, count=int(stats.reach_count))
 
 
 def _debug_invariants(lib, q, table, nv, stats, iterations):

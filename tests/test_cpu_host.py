@@ -210,3 +210,29 @@ def test_plan_ast_helpers():
         plan.eval_plan(g, plan.Label("a"), ("middle", 0), P.EngineOptions())
     with pytest.raises(IndexError):
         plan.eval_plan(g, plan.Label("a"), ("source", 3), P.EngineOptions())
+
+
+def test_answer_set_view_matches_the_reference_set():
+    """EvalResult.answer_set: the lazy set[int] a drop-in shim hands to the
+    reference's EvalResult (engine.py:71-76) instead of building `reachable`."""
+    import numpy as np
+
+    from paper_2412_10287_b200.engine import EvalResult
+
+    rng = np.random.default_rng(7)
+    nv = 5000
+    reach = (rng.random(nv) < 0.1).astype(np.uint8)
+    want = set(np.flatnonzero(reach).tolist())
+    bits = np.packbits(reach, bitorder="little")
+    bits = np.concatenate([bits, np.zeros(-bits.size % 4, np.uint8)]).view(np.uint32)
+    for kw in ({"bits": bits}, {"bits": bits, "count": len(want)}):
+        r = EvalResult(None, 3, 0.0, "hybrid", nv=nv, **kw)
+        a = r.answer_set
+        assert len(a) == len(want) and a == want and want == a and set(a) == want
+        assert all((v in a) == (v in want) for v in range(-3, nv + 3))
+        assert "7" not in a and None not in a
+    # sparse answers kept as (word, bits) pairs decode the same way
+    words = np.flatnonzero(bits)
+    pairs = np.stack([words.astype(np.uint32), bits[words]], axis=1).reshape(-1)
+    r = EvalResult(None, 3, 0.0, "hybrid", nv=nv, pairs=pairs)
+    assert r.answer_set == want and r.reachable == want and np.array_equal(r.reach, reach)
