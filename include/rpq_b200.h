@@ -116,6 +116,10 @@ typedef struct rpq_batch_stats {
 #define RPQ_DIR_PULL 2   /* always scan unvisited rows of the transpose (CSC) */
 
 RPQ_API int rpq_abi_version(void);
+/* 1 in the checked build (librpq_b200_checked.so, -DRPQ_CHECKED: device-side
+ * bounds checks on every data-dependent index; a failed check fails the run
+ * with RPQ_ECUDA "bounds check failed at file:line"), 0 otherwise. */
+RPQ_API int rpq_checked_build(void);
 RPQ_API const char* rpq_last_error(void);
 /* SM count, L2 bytes and HBM bytes of a device (for launch sizing / reports) */
 RPQ_API int rpq_device_info(int32_t device, int32_t* sm_count, int64_t* l2_bytes, int64_t* hbm_bytes);

@@ -18,6 +18,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 ENGINE_SO = os.path.join(PKG, "librpq_b200.so")
+CHECKED_SO = os.path.join(PKG, "librpq_b200_checked.so")  # -DRPQ_CHECKED (csrc/checks.cuh)
 DATAGEN_SO = os.path.join(PKG, "librpq_datagen.so")
 
 
@@ -33,17 +34,18 @@ def _run(cmd):
     subprocess.run(cmd, check=True)
 
 
-def build_engine(force=False):
+def build_engine(force=False, checked=False):
     import glob
 
     src = os.path.join(CSRC, "rpq_b200.cu")
+    out = CHECKED_SO if checked else ENGINE_SO
     deps = (glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
             + glob.glob(os.path.join(INCLUDE, "*.h")) + [__file__])
-    if force or _stale(ENGINE_SO, deps):
+    if force or _stale(out, deps):
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-v", "-I", INCLUDE,
-              "-shared", "-o", ENGINE_SO, src])
-    return ENGINE_SO
+              *(["-DRPQ_CHECKED"] if checked else []), "-shared", "-o", out, src])
+    return out
 
 
 def build_datagen(force=False):
@@ -57,6 +59,7 @@ def build_datagen(force=False):
 def build_all(force=False):
     build_datagen(force)
     build_engine(force)
+    build_engine(force, checked=True)
 
 
 if __name__ == "__main__":

@@ -136,6 +136,7 @@ class RpqBatchStats(ctypes.Structure):
 # symbol -> (restype, argtypes); the complete C ABI of include/rpq_b200.h
 ENGINE_SIGNATURES = {
     "rpq_abi_version": (c_i32, []),
+    "rpq_checked_build": (c_i32, []),
     "rpq_last_error": (ctypes.c_char_p, []),
     "rpq_device_info": (c_i32, [c_i32, P_i32, P_i64, P_i64]),
     "rpq_graph_create": (c_i32, [c_i32, c_i32, c_i32, ctypes.POINTER(c_vp)]),
@@ -217,12 +218,14 @@ def engine():
     if _engine is None:
         with _lock:
             if _engine is None:
-                if not os.path.exists(_build.ENGINE_SO):
+                # RPQ_ENGINE=checked: the bounds-checked build (tests/diagnostics)
+                path = _build.CHECKED_SO if os.environ.get("RPQ_ENGINE") == "checked" else _build.ENGINE_SO
+                if not os.path.exists(path):
                     raise NativeLibraryMissing(
-                        f"{_build.ENGINE_SO} is not built; run "
+                        f"{path} is not built; run "
                         "`python -m paper_2412_10287_b200._build` (there is no CPU fallback)"
                     )
-                lib = _bind(_build.ENGINE_SO, ENGINE_SIGNATURES)
+                lib = _bind(path, ENGINE_SIGNATURES)
                 if lib.rpq_abi_version() != ABI_VERSION:
                     raise NativeLibraryMissing("librpq_b200.so ABI version mismatch")
                 _engine = lib

@@ -113,7 +113,8 @@ __device__ __forceinline__ void bvisit(const BParams& p, uint32_t* fnext, uint32
 #pragma unroll
     for (int c = 0; c < K; ++c) {
         off[c] = (long long)t[c] * p.nvp + u[c];
-        seen[c] = act[c] ? __ldcg(p.vis + off[c]) : 0xFFFFFFFFu;
+        const bool ok = !act[c] || RPQ_CHECK(t[c] >= 0 && t[c] < p.nstates && u[c] >= 0 && u[c] < p.nv, RPQ_F_BATCH);
+        seen[c] = act[c] && ok ? __ldcg(p.vis + off[c]) : 0xFFFFFFFFu;
     }
 #pragma unroll
     for (int c = 0; c < K; ++c) {

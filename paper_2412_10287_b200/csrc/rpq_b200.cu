@@ -47,6 +47,27 @@ int cuda_fail(cudaError_t e, const char* what) {
         if (e_ != cudaSuccess) return cuda_fail(e_, #expr); \
     } while (0)
 
+// Checked build: a device bounds check that failed during the last run
+// (checks.cuh) fails the run.  The site is reset for the next run.
+int check_sites() {
+#ifdef RPQ_CHECKED
+    unsigned site = 0;
+    if (cudaMemcpyFromSymbol(&site, rpqk::g_check_site, sizeof(site)) != cudaSuccess) {
+        cudaGetLastError();
+        return RPQ_OK;
+    }
+    if (site) {
+        const unsigned zero = 0;
+        cudaMemcpyToSymbol(rpqk::g_check_site, &zero, sizeof(zero));
+        static const char* files[] = {"?", "ssr_kernel.cuh", "batch_kernel.cuh", "small_kernel.cuh"};
+        const unsigned f = site / 100000u;
+        return fail(RPQ_ECUDA, std::string("bounds check failed at ") + (f < 4 ? files[f] : "?") + ":" +
+                                   std::to_string(site % 100000u));
+    }
+#endif
+    return RPQ_OK;
+}
+
 // Pinned, mapped host blocks handed out by rpq_host_alloc: base -> bytes.
 // A run whose answer buffer lies inside one has the kernel write the answer
 // there directly (no copy node, no host memcpy).
@@ -186,19 +207,32 @@ int upload_csr(rpq_graph* g, LabelDev& L, int dir, int64_t nnz, const I* indptr,
         return fail(RPQ_EINVAL, "CSR indptr must start at 0 and end at nnz");
     const int64_t n_items = std::max<int64_t>(nv + 1, nnz);
     void* staging = nullptr;
-    CUDA_TRY(cudaMalloc(&staging, (size_t)n_items * sizeof(I)));
+    int* d_bad = nullptr;
+    CUDA_TRY(cudaMalloc(&staging, (size_t)n_items * sizeof(I) + 16));
+    d_bad = reinterpret_cast<int*>(reinterpret_cast<char*>(staging) + (size_t)n_items * sizeof(I));
+    CUDA_TRY(cudaMemset(d_bad, 0, sizeof(int)));
     CUDA_TRY(cudaMalloc(&L.rowptr[dir], (size_t)(nv + 1) * sizeof(uint32_t)));
     CUDA_TRY(cudaMalloc(&L.col[dir], (size_t)std::max<int64_t>(nnz, 1) * sizeof(int32_t)));
     CUDA_TRY(cudaMemcpy(staging, indptr, (size_t)(nv + 1) * sizeof(I), cudaMemcpyHostToDevice));
+    validate_csr_kernel<I><<<1184, 256>>>((const I*)staging, nv + 1, 0, nnz + 1, 1, d_bad);
     narrow_kernel<I, uint32_t><<<1184, 256>>>((const I*)staging, L.rowptr[dir], nv + 1);
     CUDA_TRY(cudaGetLastError());
     if (nnz > 0) {
         CUDA_TRY(cudaMemcpy(staging, indices, (size_t)nnz * sizeof(I), cudaMemcpyHostToDevice));
+        validate_csr_kernel<I><<<1184, 256>>>((const I*)staging, nnz, 0, nv, 0, d_bad);
         narrow_kernel<I, int32_t><<<1184, 256>>>((const I*)staging, L.col[dir], nnz);
         CUDA_TRY(cudaGetLastError());
     }
-    CUDA_TRY(cudaDeviceSynchronize());
+    int bad = 0;
+    CUDA_TRY(cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost));
     CUDA_TRY(cudaFree(staging));
+    if (bad) {
+        cudaFree(L.rowptr[dir]);
+        cudaFree(L.col[dir]);
+        L.rowptr[dir] = nullptr;
+        L.col[dir] = nullptr;
+        return fail(RPQ_EINVAL, "CSR structure invalid: indptr must be non-decreasing and columns in [0, |V|)");
+    }
     L.nnz[dir] = nnz;
     g->bytes += (nv + 1) * 4 + std::max<int64_t>(nnz, 1) * 4;
     return RPQ_OK;
@@ -453,6 +487,14 @@ cudaError_t allow_dyn_smem(const void* fn) {
 extern "C" {
 
 int rpq_abi_version(void) { return RPQ_ABI_VERSION; }
+
+int rpq_checked_build(void) {
+#ifdef RPQ_CHECKED
+    return 1;
+#else
+    return 0;
+#endif
+}
 
 const char* rpq_last_error(void) { return g_last_error.c_str(); }
 
@@ -902,6 +944,7 @@ Params make_params(const rpq_query* q) {
     p.ovf_segcap = q->ovf_segcap;
     p.ovf_buncap = q->ovf_buncap;
     p.seg_alloc = q->seg_alloc;
+    p.bun_alloc = q->bun_alloc;
     p.W = q->W;
     p.nv = q->g->nv;
     p.nstates = q->nstates;
@@ -1106,6 +1149,7 @@ int rpq_query_wait(rpq_query* q, rpq_stats* stats) {
     CUDA_TRY(cudaStreamSynchronize(q->last_stream));
     q->inflight = false;
     q->bar_next = q->h_ctl->bar;
+    if (const int crc = check_sites()) return crc;
     const Ctl& c = *q->h_ctl;
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, q->ev0, q->ev1));
@@ -1374,6 +1418,7 @@ int rpq_query_step_end(rpq_query* q, int64_t* steps) {
         q->bar_next = q->h_ctl->bar;
         q->inflight = false;
     }
+    if (const int crc = check_sites()) return crc;
     unsigned acc[2] = {0, 0};
     CUDA_TRY(cudaMemcpy(acc, q->d_step_acc, sizeof(acc), cudaMemcpyDeviceToHost));
     if (steps) *steps = (int64_t)acc[0];
@@ -1574,6 +1619,7 @@ int rpq_query_wait_batch(rpq_query* q, rpq_batch_stats* stats) {
     if (!q->bran) return fail(RPQ_EINVAL, "no batch has been run");
     CUDA_TRY(cudaStreamSynchronize(q->blast_stream));
     q->binflight = false;
+    if (const int crc = check_sites()) return crc;
     const BCtl& c = *q->h_bctl;
     q->bbar_next = c.bar;
     float ms = 0.f;

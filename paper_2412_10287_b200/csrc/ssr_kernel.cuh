@@ -24,6 +24,8 @@
 // same set: P only grows by (q', w) pairs with a frontier predecessor.
 #pragma once
 
+#include "checks.cuh"
+
 namespace rpqk {
 
 // One CTA per SM; the thread count is a template parameter of the kernels:
@@ -159,6 +161,7 @@ struct Params {
     uint32_t* reach_bits;  // the answer as a bitmap (same bits as reach)
     unsigned long long shard_segcap, shard_buncap, ovf_segcap, ovf_buncap;
     unsigned long long seg_alloc;
+    unsigned long long bun_alloc;  // bundles per queue buffer (bounds checks)
     unsigned long long budget_ns;
     long long W;             // words per bitmap row (multiple of 4)
     int nv;
@@ -395,6 +398,7 @@ struct Out {
 // (one candidate per lane).  Returns the edges emitted.
 __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, const Out& o, bool valid,
                                                int q, int w, int lane) {
+    if (valid && !RPQ_CHECK(q >= 0 && q < p.nstates && w >= 0 && w < p.nv, RPQ_F_SSR)) valid = false;
     const unsigned vmask = __ballot_sync(FULL, valid);
     if (vmask == 0) return 0;
     const int ng = valid ? (S.gbeg[q + 1] - S.gbeg[q]) : 0;
@@ -452,7 +456,8 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
             ok = __shfl_sync(FULL, ok, 0);
             hlo = __shfl_sync(FULL, hlo, 0);
             hhi = __shfl_sync(FULL, hhi, 0);
-            for (unsigned long long h = hlo + lane; h < hhi; h += 32) o.bun[h] = make_uint2(0u, kHoleY);
+            for (unsigned long long h = hlo + lane; h < hhi; h += 32)
+                if (RPQ_CHECK(h < p.bun_alloc, RPQ_F_SSR)) o.bun[h] = make_uint2(0u, kHoleY);
             if (!ok) {
                 if (lane == 0) atomicExch(&o.qc->overflow, 1u);
                 return 0;
@@ -483,10 +488,10 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
                             bd = make_uint2((uint32_t)(sbase + rj), ((pos - exj) << 7) | (cnt - 1));
                             need_seg = true;
                         }
-                        st_queue(o.bun + bbase + kb, bd, S.pf);
+                        if (RPQ_CHECK(bbase + kb < p.bun_alloc, RPQ_F_SSR)) st_queue(o.bun + bbase + kb, bd, S.pf);
                     }
                 }
-                if (__any_sync(FULL, need_seg) && deg[k] > 0)
+                if (__any_sync(FULL, need_seg) && deg[k] > 0 && RPQ_CHECK(sbase + rank[k] < p.seg_alloc, RPQ_F_SSR))
                     st_queue(o.seg + sbase + rank[k], make_uint2(lo[k], (deg[k] << 8) | (uint32_t)g[k]), S.pf);
                 sbase += nseg[k];
                 bbase += nb[k];
@@ -521,21 +526,23 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
             ok = __shfl_sync(FULL, ok, 0);
             hlo = __shfl_sync(FULL, hlo, 0);
             hhi = __shfl_sync(FULL, hhi, 0);
-            for (unsigned long long h = hlo + lane; h < hhi; h += 32) o.bun[h] = make_uint2(0u, kHoleY);
+            for (unsigned long long h = hlo + lane; h < hhi; h += 32)
+                if (RPQ_CHECK(h < p.bun_alloc, RPQ_F_SSR)) o.bun[h] = make_uint2(0u, kHoleY);
             if (!ok) {
                 if (lane == 0) atomicExch(&o.qc->overflow, 1u);
                 return emitted;
             }
             sbase = __shfl_sync(FULL, sbase, 0);
             bbase = __shfl_sync(FULL, bbase, 0);
-            if (hs) o.seg[sbase + rank] = make_uint2(lo, (take << 8) | (uint32_t)g);
+            if (hs && RPQ_CHECK(sbase + rank < p.seg_alloc, RPQ_F_SSR))
+                o.seg[sbase + rank] = make_uint2(lo, (take << 8) | (uint32_t)g);
             for (uint32_t kb0 = 0; kb0 < nb; kb0 += 32) {
                 const uint32_t kb = kb0 + lane;
                 const uint32_t pos = kb * o.bsz;
                 const int j = warp_upper_lane(excl, min(pos, T - 1));
                 const uint32_t exj = __shfl_sync(FULL, excl, j);
                 const int rj = __shfl_sync(FULL, rank, j);
-                if (kb < nb) {
+                if (kb < nb && RPQ_CHECK(bbase + kb < p.bun_alloc, RPQ_F_SSR)) {
                     const uint32_t cnt = min(o.bsz, T - pos);
                     o.bun[bbase + kb] = make_uint2((uint32_t)(sbase + rj), ((pos - exj) << 7) | (cnt - 1));
                 }
@@ -1067,6 +1074,7 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
 #pragma unroll
             for (int j = 0; j < PV; ++j)
                 if (((look >> j) & 1u) && r[j + 1] > r[j]) cm |= 1u << j;
+            if (cm && !RPQ_CHECK(r[PV] <= p.slot_nnz[S.islot[k] % p.nslots], RPQ_F_SSR)) cm = 0;
             const uint32_t cnt = __popc(cm);
             const uint32_t incl = warp_incl_scan(cnt, lane);
             const int n = (int)__shfl_sync(FULL, incl, 31);
@@ -1087,8 +1095,9 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
                 const bool act = j < n;
                 const uint32_t l = act ? clo[j] : 0u, h = act ? chi[j] : 0u;
                 // first round: `first` in-edges, all loads in flight
-                const int c0 = act ? ld_stream_i32(ps.col + l, S.pf) : -1;
-                const int c1 = act && first > 1 && l + 1 < h ? ld_stream_i32(ps.col + l + 1, S.pf) : -1;
+                int c0 = act ? ld_stream_i32(ps.col + l, S.pf) : -1;
+                int c1 = act && first > 1 && l + 1 < h ? ld_stream_i32(ps.col + l + 1, S.pf) : -1;
+                if (act && !RPQ_CHECK(c0 >= 0 && c0 < p.nv && c1 < p.nv && l < h, RPQ_F_SSR)) c0 = c1 = -1;
                 bool hit = (c0 >= 0 && ((ld_bits(frow + (c0 >> 5), S.pl) >> (c0 & 31)) & 1u)) ||
                            (c1 >= 0 && ((ld_bits(frow + (c1 >> 5), S.pl) >> (c1 & 31)) & 1u));
                 uint32_t e = l + (uint32_t)first;
@@ -1347,8 +1356,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
                     const unsigned long long pos = (b - s_sbun[r]) * bsz;
                     const unsigned long long deg = s_sdeg[r + 1] - s_sdeg[r];
                     const uint32_t cnt = (uint32_t)min((unsigned long long)bsz, deg - pos);
-                    o.bun[(unsigned long long)blockIdx.x * p.shard_buncap + k] =
-                        make_uint2(s_slo[r] + (uint32_t)pos, kInline | (s_sgrp[r] << 7) | (cnt - 1));
+                    if (RPQ_CHECK((unsigned long long)blockIdx.x * p.shard_buncap + k < p.bun_alloc, RPQ_F_SSR))
+                        o.bun[(unsigned long long)blockIdx.x * p.shard_buncap + k] =
+                            make_uint2(s_slo[r] + (uint32_t)pos, kInline | (s_sgrp[r] << 7) | (cnt - 1));
                 }
                 if (threadIdx.x == 0) s_resv = ((cta0 ? (unsigned long long)nrows : 0ull) << 32) | mine;
             }
@@ -1535,8 +1545,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
 #pragma unroll
                     for (int u = 0; u < kEdgesPerLane; ++u) {
                         const uint32_t ed = (uint32_t)(lane + 32 * u);
-                        gj[u] = ed < cnt ? g : -1;
-                        w[u] = ed < cnt ? ld_stream_i32(col + ed, S.pf) : 0;
+                        const bool okc = ed < cnt && RPQ_CHECK(bd.x + ed < p.slot_nnz[S.gslot[g] % p.nslots], RPQ_F_SSR);
+                        gj[u] = okc ? g : -1;
+                        w[u] = okc ? ld_stream_i32(col + ed, S.pf) : 0;
                     }
                 } else {
                     const uint32_t s0 = bd.x;
@@ -1563,8 +1574,11 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
                         const uint32_t sj = __shfl_sync(FULL, my_start, j);
                         const uint32_t exj = __shfl_sync(FULL, excl, j);
                         const int g = (int)__shfl_sync(FULL, my_grp, j);
-                        gj[u] = active ? g : -1;
-                        w[u] = active ? ld_stream_i32(S.slots[S.gslot[g]].col + sj + (ed - exj), S.pf) : 0;
+                        const bool okc = active && RPQ_CHECK(g >= 0 && g < p.ngroups &&
+                                                                 sj + (ed - exj) < p.slot_nnz[S.gslot[g] % p.nslots],
+                                                             RPQ_F_SSR);
+                        gj[u] = okc ? g : -1;
+                        w[u] = okc ? ld_stream_i32(S.slots[S.gslot[g]].col + sj + (ed - exj), S.pf) : 0;
                     }
                 }
                 // probe P for every target, then claim with atomicOr
@@ -1592,6 +1606,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
 #pragma unroll
                     for (int u = 0; u < kEdgesPerLane; ++u) {
                         const uint32_t bit = 1u << (w[u] & 31);
+                        if (q2[u] >= 0 && !RPQ_CHECK(q2[u] < p.nstates && w[u] >= 0 && w[u] < p.nv, RPQ_F_SSR))
+                            q2[u] = -1;
                         if (q2[u] >= 0 && !(old[u] & bit)) {
                             const long long off2 = (long long)q2[u] * p.W + (w[u] >> 5);
                             old[u] = or_bits(p.visited + off2, bit, S.pl);
@@ -1714,8 +1730,10 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
                     base = __shfl_sync(FULL, base, 0);
                     if (acc) {
                         const unsigned long long pos = base + __popc(m & lanemask_lt());
-                        hb[2 * pos] = (uint32_t)i;
-                        hb[2 * pos + 1] = acc;
+                        if (RPQ_CHECK(2 * pos + 1 < (unsigned long long)Wn, RPQ_F_SSR)) {
+                            hb[2 * pos] = (uint32_t)i;
+                            hb[2 * pos + 1] = acc;
+                        }
                     }
                 }
             } else {
@@ -1808,6 +1826,19 @@ __global__ void reach_bytes_kernel(const uint32_t* __restrict__ bits, uint8_t* _
         uint4* dst = reinterpret_cast<uint4*>(out + i * 32);
         dst[0] = make_uint4(b4[0], b4[1], b4[2], b4[3]);
         dst[1] = make_uint4(b4[4], b4[5], b4[6], b4[7]);
+    }
+}
+
+// Upload validation of a host CSR (the reference's SparseBoolMatrix checks its
+// own structure, sparse_bool.py:60-73; a duck-typed graph may not): indptr
+// non-decreasing within [0, nnz], columns within [0, nv).  *bad = 1 on failure.
+template <typename I>
+__global__ void validate_csr_kernel(const I* __restrict__ v, long long n, long long lo, long long hi, int monotone,
+                                    int* __restrict__ bad) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long x = (long long)v[i];
+        if (x < lo || x >= hi || (monotone && i + 1 < n && (long long)v[i + 1] < x)) *bad = 1;
     }
 }
 
