@@ -173,7 +173,8 @@ RPQ_API int rpq_query_set_options(rpq_query* q, int32_t direction, int32_t count
 #define RPQ_TUNE_EMIT_MODE 0
 #define RPQ_TUNE_EMIT_INLINE_MAX 1
 #define RPQ_TUNE_FLAGS 3  /* push variants: bit 0 (default on) claim without probing P first,
-                             bit 1 prefetch candidate targets' row pointers into L2 */
+                             bit 1 prefetch candidate targets' row pointers into L2,
+                             bit 2 never cut a push level's emission off at m_u / alpha */
 #define RPQ_TUNE_SMALL 4  /* 1 (default): state spaces of <= 12,288 x 32 pairs run on one CTA
                              with shared-memory bitmaps; 0: always the grid kernel */
 #define RPQ_TUNE_DEFER 5  /* push level L does not emit F_{L+1}'s queue at discovery when

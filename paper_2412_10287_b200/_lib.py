@@ -220,6 +220,7 @@ def engine():
             if _engine is None:
                 # RPQ_ENGINE=checked: the bounds-checked build (tests/diagnostics)
                 path = _build.CHECKED_SO if os.environ.get("RPQ_ENGINE") == "checked" else _build.ENGINE_SO
+                path = os.environ.get("RPQ_ENGINE_SO", path)  # experiments: an alternative build
                 if not os.path.exists(path):
                     raise NativeLibraryMissing(
                         f"{path} is not built; run "

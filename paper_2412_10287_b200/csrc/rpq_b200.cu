@@ -1068,7 +1068,7 @@ int rpq_query_set_tuning(rpq_query* q, int32_t key, double value) {
             q->allow_small = (int)value;
             return RPQ_OK;
         case RPQ_TUNE_FLAGS:
-            if (value < 0 || value > 3) return fail(RPQ_EINVAL, "flags must be in [0, 3]");
+            if (value < 0 || value > 7) return fail(RPQ_EINVAL, "flags must be in [0, 7]");
             q->run_flags = (unsigned)value;
             return RPQ_OK;
         case RPQ_TUNE_TRACE: {

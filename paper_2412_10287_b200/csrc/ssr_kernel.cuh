@@ -78,6 +78,8 @@ struct QCnt {
     unsigned long long edges;               // push-model edges emitted
     unsigned int overflow;
     unsigned int expire;                    // 1 + level whose deadline check failed
+    unsigned long long emit_progress;       // edges emitted so far this level (reported in chunks)
+    unsigned int emit_cut;                  // 1: the emission crossed View::cut_edges
 };
 
 struct FCnt {
@@ -142,6 +144,7 @@ struct RunArgs {
 
 constexpr unsigned RF_NO_PROBE = 1u;     // claim with atomicOr without reading P first
 constexpr unsigned RF_PREFETCH = 2u;     // prefetch candidate targets' row pointers into L2
+constexpr unsigned RF_NO_CUT = 4u;       // never cut a push level's emission off (View::cut_edges)
 
 struct Params {
     const RunArgs* run;
@@ -316,6 +319,9 @@ struct View {
     int status;
     int iterations;
     unsigned long long nfront;  // |F_L|
+    float cut_edges;            // push level: once the emitted successor edges exceed this, the next
+                                // level is pull whatever the rest emits (Beamer's m_f * alpha > m_u with
+                                // this level's m_u, which only shrinks): stop emitting (0: never)
 };
 
 // Grid barrier for a cooperative launch over a monotonic arrival counter:
@@ -746,6 +752,7 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
     const unsigned long long nedge = ldcg(&qc->edges);
     const unsigned int overflow = ldcg(&qc->overflow);
     const unsigned int expire = ldcg(&qc->expire);
+    const unsigned int emit_cut = ldcg(&qc->emit_cut);
     const int abort = ldcg(&ctl->abort);
     unsigned long long nbun, nseg;
     queue_scan(p, qc, lane, s_bpre, &nbun, &nseg);
@@ -764,6 +771,7 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
     const int produced_by_push = prev_queued;
     int done = 0, iterations = 0, status = 0, next = DIR_PUSH, plan = 0;
     bool defer = false;
+    float cut = 0.0f;
     long long ledges = -1;
     if (abort) {
         status = ST_DEADLOCK;
@@ -811,6 +819,12 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
                 mf += __shfl_xor_sync(FULL, mf, d);
             }
             if (produced_by_push) mf = (float)nedge;
+            // Emission cutoff for a push level: once its emitted successor
+            // edges exceed m_u / alpha, the next level will almost surely be
+            // pull (m_u only shrinks; the next frontier's states may read other
+            // in-slots, so this is a heuristic -- a cut forces pull below,
+            // which is always correct, only possibly slower)
+            cut = (S.run->flags & RF_NO_CUT) ? 0.0f : mu * __frcp_rn(S.run->alpha) * 1.01f + 64.0f;
             // a push level whose successor frontier will likely warrant pull
             // does not emit that frontier's queue at discovery: a pull level
             // needs none (a push level re-emits it from the bitmap instead).
@@ -833,6 +847,8 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
                 next = ((float)nnew * 24.0f > nv * (float)ntarget) ? DIR_PULL : DIR_PUSH;
             }
         }
+        // a cut-off emission left F_L's queue incomplete: pull
+        if (emit_cut && produced_by_push) next = DIR_PULL;
         if (next == DIR_PUSH) {
             if (produced_by_push) {
                 ledges = (long long)nedge;
@@ -855,6 +871,7 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
         v->iterations = iterations;
         v->nfront = nnew;
         v->defer = next == DIR_PUSH && defer;
+        v->cut_edges = next == DIR_PUSH && !defer ? cut : 0.0f;
         if (blockIdx.x == 0) {  // results and statistics
             const unsigned long long now = globaltimer();
             atomicAdd(&ctl->pairs, nnew);  // fire-and-forget: no round trip on CTA 0's path
@@ -937,6 +954,8 @@ __device__ __forceinline__ void reset_qc(Ctl* ctl, int k, int tid) {
         qc->edges = 0;
         qc->overflow = 0;
         qc->expire = 0;
+        qc->emit_progress = 0;
+        qc->emit_cut = 0;
     }
 }
 
@@ -986,29 +1005,39 @@ constexpr int kPullCont = 8;
 // pointers rowptr[v0 .. v0+PV] are PV/4 128-bit loads plus one shuffle (the
 // next lane's first), and its P / found bits are a PV-bit field of one word.
 template <int PV>
-__device__ __forceinline__ void load_rows(const uint32_t* rp, long long v0, int nv, int lane, uint32_t (&r)[PV + 1]) {
-    if (v0 + PV <= nv) {
-        const uint4* r4 = reinterpret_cast<const uint4*>(rp + v0);  // v0 % PV == 0: 16-byte aligned
+__device__ __forceinline__ void load_rows(const uint32_t* rp, long long v0, int nv, int lane, bool active,
+                                          uint64_t pol, uint32_t (&r)[PV + 1]) {
+    // lanes with nothing to look at skip their loads (a later in-slot of a
+    // target, once most of the lane's vertices are found or visited)
+    if (active) {
+        if (v0 + PV <= nv) {
+            const uint4* r4 = reinterpret_cast<const uint4*>(rp + v0);  // v0 % PV == 0: 16-byte aligned
 #pragma unroll
-        for (int c = 0; c < PV / 4; ++c) {
-            uint4 x;
-            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(r4 + c));
-            r[4 * c] = x.x;
-            r[4 * c + 1] = x.y;
-            r[4 * c + 2] = x.z;
-            r[4 * c + 3] = x.w;
+            for (int c = 0; c < PV / 4; ++c) {
+                uint4 x;
+                // streamed once per level: evict-first in L2, like every other adjacency read
+                asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                             : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(r4 + c), "l"(pol));
+                r[4 * c] = x.x;
+                r[4 * c + 1] = x.y;
+                r[4 * c + 2] = x.z;
+                r[4 * c + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < PV; ++j) r[j] = v0 + j <= nv ? ld_stream_u32(rp + v0 + j, pol) : 0u;
         }
-    } else {
-#pragma unroll
-        for (int j = 0; j < PV; ++j) r[j] = v0 + j <= nv ? __ldg(rp + v0 + j) : 0u;
     }
-    // rowptr[v0 + PV]: the next lane's first (lane 31 and the tail load it)
+    // rowptr[v0 + PV]: the next lane's first when it loaded, else our own load
     const uint32_t nx = __shfl_down_sync(FULL, r[0], 1);
-    r[PV] = (lane < 31 && v0 + PV <= nv) ? nx : (v0 + PV <= nv ? __ldg(rp + v0 + PV) : r[PV - 1]);
+    const bool next_loaded = __shfl_down_sync(FULL, active ? 1 : 0, 1) != 0;
+    if (active) {
+        r[PV] = (lane < 31 && next_loaded && v0 + PV <= nv) ? nx
+                                                            : (v0 + PV <= nv ? ld_stream_u32(rp + v0 + PV, pol) : r[PV - 1]);
 #pragma unroll
-    for (int j = 1; j <= PV; ++j)  // past the end: empty rows
-        if (v0 + j > nv) r[j] = r[j - 1];
+        for (int j = 1; j <= PV; ++j)  // past the end: empty rows
+            if (v0 + j > nv) r[j] = r[j - 1];
+    }
 }
 
 template <int PV>
@@ -1053,7 +1082,7 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
             }
         uint32_t r[PV + 1];
         const uint32_t pw = myword < pw1 ? ld_bits(p.visited + (long long)q2 * p.W + myword, S.pl) : 0xFFFFFFFFu;
-        load_rows<PV>(S.slots[p.nslots + S.islot[max(k0, 0)]].rowptr, v0, p.nv, lane, r);
+        load_rows<PV>(S.slots[p.nslots + S.islot[max(k0, 0)]].rowptr, v0, p.nv, lane, true, S.pf, r);
         // need: this lane's unvisited vertices (PV bits)
         uint32_t need = ~(pw >> sh) & fmask_all;
         if (v0 >= p.nv) need = 0;
@@ -1068,7 +1097,7 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
             if (__ballot_sync(FULL, look != 0) == 0) break;
             const Slot ps = S.slots[p.nslots + S.islot[k]];
             const uint32_t* frow = fcur + (long long)q * p.W;
-            if (k != k0) load_rows<PV>(ps.rowptr, v0, p.nv, lane, r);
+            if (k != k0) load_rows<PV>(ps.rowptr, v0, p.nv, lane, look != 0, S.pf, r);
             // compaction: the looking vertices with in-edges in this slot
             uint32_t cm = 0;
 #pragma unroll
@@ -1195,6 +1224,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
     __shared__ View s_view;
     __shared__ unsigned long long s_resv;
     __shared__ unsigned s_task;  // next task index of this CTA in the current epoch
+    __shared__ int s_cut;        // this level's emission was cut off (View::cut_edges)
+    __shared__ unsigned long long s_emitted;  // edges this CTA emitted this level
     __shared__ unsigned long long s_wend;  // diagnostics: latest warp done with the epoch
     __shared__ RunArgs s_run;
     __shared__ float s_nnz[kMaxSlots];
@@ -1219,6 +1250,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
         s_run = *p.run;
         s_view.mf = 0.0f;
         s_view.defer = 0;
+        s_view.cut_edges = 0.0f;
         float d = 0.0f;
         for (int sl = 0; sl < p.nslots; ++sl) d = fmaxf(d, (float)p.slot_nnz[sl]);
         s_view.dmax = d * __frcp_rn((float)max(p.nv, 1));
@@ -1401,6 +1433,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
             s_view.dir = dir;
             s_view.plan = dir == DIR_PUSH;
             s_view.defer = 0;
+        s_view.cut_edges = 0.0f;
             s_view.status = 0;
             s_view.iterations = 0;
             s_view.nfront = nf;
@@ -1468,7 +1501,11 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
                                      (unsigned long long)nwarps * 4
                                  ? 32u : (uint32_t)kBundle;
         const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, bsz};
-        if (threadIdx.x == 0) s_task = 0;
+        if (threadIdx.x == 0) {
+            s_task = 0;
+            s_cut = 0;
+            s_emitted = 0;
+        }
         if (cta0) {
             reset_qc(ctl, (e + 2) % 3, threadIdx.x);
             FCnt* fz = &ctl->fc[(L + 2) % 3];
@@ -1483,6 +1520,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
         unsigned long long nnew = 0, nedge = 0;
         // emit F_{L+1}'s queue now (at discovery) or later from F's bitmap
         // (a step-mode run stops after this level: nobody expands F_{L+1}'s queue)
+        // progress reports: about 4 per CTA before the cut
+        const unsigned long long cut_chunk =
+            s_view.cut_edges > 0.0f ? (unsigned long long)(s_view.cut_edges / (4.0f * (float)gridDim.x)) + 1ull : 0ull;
         const bool emit_inline = dir == DIR_PUSH && !s_view.defer && !step_mode &&
                                  (s_run.emit_mode == 0 ||
                                   (s_run.emit_mode == 2 && s_view.nfront < s_run.emit_inline_max));
@@ -1616,23 +1656,41 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
                             old[u] = 0xFFFFFFFFu;
                         }
                     }
+                    const bool emit_now = emit_inline && !*(volatile int*)&s_cut;
 #pragma unroll
                     for (int u = 0; u < kEdgesPerLane; ++u) {
                         const bool fresh = q2[u] >= 0 && !(old[u] & (1u << (w[u] & 31)));
                         nnew += fresh ? 1 : 0;
                         if (fresh) atomicAdd(&s_state[q2[u]], 1u);
-                        if (emit_inline) stage_put(stage, fresh, q2[u], w[u], lane);
+                        if (emit_now) stage_put(stage, fresh, q2[u], w[u], lane);
                     }
-                    if (emit_inline) {
+                    if (emit_now) {
                         const uint32_t T = stage_drain(p, S, o, stage, lane);
-                        if (lane == 0) nedge += T;
+                        if (lane == 0) {
+                            nedge += T;
+                            // report progress in chunks; past the cut, stop emitting
+                            if (cut_chunk && T) {
+                                const unsigned long long old_e = atomicAdd(&s_emitted, (unsigned long long)T);
+                                const unsigned long long c0 = old_e / cut_chunk, c1 = (old_e + T) / cut_chunk;
+                                if (c1 != c0) {
+                                    const unsigned long long g =
+                                        atomicAdd(&o.qc->emit_progress, (c1 - c0) * cut_chunk) + (c1 - c0) * cut_chunk;
+                                    if ((float)g >= s_view.cut_edges || ldcg(&o.qc->emit_cut)) {
+                                        o.qc->emit_cut = 1u;
+                                        s_cut = 1;
+                                    }
+                                }
+                            }
+                        }
+                        if (__shfl_sync(FULL, *(volatile int*)&s_cut, 0)) stage.n = 0;  // drop what is staged
                     }
                 }
             }
-            if (emit_inline) {
+            if (emit_inline && !*(volatile int*)&s_cut) {
                 const uint32_t T = stage_flush(p, S, o, stage, lane);
                 if (lane == 0) nedge += T;
             }
+            stage.n = 0;
         } else {
             // ---- pull: unvisited (q', w) scan A_s^T row w for a member of F_L[q]
             if (S.run->count_te)  // diagnostics: F_L's push-model edges (per-level roofline)
@@ -1658,7 +1716,10 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
             unsigned long long* pull_steal = &ctl->steal[e % 3][8];
             uint32_t* scratch = reinterpret_cast<uint32_t*>(s_stage) + (size_t)wid * kWarpScratchWords;
             const int first = one_inline ? 1 : kPullInline;
-            if (pw1 - pw0 >= (long long)nwarps * 64)  // large: 8 words per task
+#ifndef RPQ_PV8_WORDS_PER_WARP
+#define RPQ_PV8_WORDS_PER_WARP 16  // cfg5 (131k words, 4,736 warps): 8 words per task, pull levels 180 -> 123 us
+#endif
+            if (pw1 - pw0 >= (long long)nwarps * RPQ_PV8_WORDS_PER_WARP)  // large: 8 words per task
                 pull_tasks<8>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front, s_state,
                               nnew, pull_steal, scratch, first);
             else
