@@ -143,7 +143,7 @@ struct RunArgs {
 };
 
 constexpr unsigned RF_NO_PROBE = 1u;     // claim with atomicOr without reading P first
-constexpr unsigned RF_PREFETCH = 2u;     // prefetch candidate targets' row pointers into L2
+constexpr unsigned RF_PREFETCH = 2u;     // (retired: -30% on cfg4 in round 1; the bit is ignored)
 constexpr unsigned RF_NO_CUT = 4u;       // never cut a push level's emission off (View::cut_edges)
 
 struct Params {
@@ -1044,7 +1044,7 @@ template <int PV>
 __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const uint32_t* fcur, uint32_t* fnext,
                                            long long pw0, long long pw1, int lane, unsigned* s_task,
                                            int s_nptarget, const int* s_ptarget, const unsigned int* s_front,
-                                           unsigned int* s_state, unsigned long long& nnew,
+                                           unsigned int* s_state, unsigned int& nnew,
                                            unsigned long long* steal, uint32_t* scratch, int first) {
     constexpr int LPW = 32 / PV;  // lanes per word
     const long long nblk = (pw1 - pw0 + PV - 1) / PV;
@@ -1517,7 +1517,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
             for (long long i = gtid; i < nbits4; i += gthreads) z4[i] = make_uint4(0, 0, 0, 0);
         }
         __syncthreads();  // s_task
-        unsigned long long nnew = 0, nedge = 0;
+        unsigned int nnew = 0;  // this thread's discoveries this level (< 2^32)
+        unsigned long long nedge = 0;
         // emit F_{L+1}'s queue now (at discovery) or later from F's bitmap
         // (a step-mode run stops after this level: nobody expands F_{L+1}'s queue)
         // progress reports: about 4 per CTA before the cut
@@ -1637,9 +1638,6 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
                                     old[u] = ld_bits(p.visited + (long long)q2[u] * p.W + (w[u] >> 5), S.pl);
                                 else
                                     old[u] = 0u;
-                                if ((s_run.flags & RF_PREFETCH) && emit_inline)
-                                    for (int g2 = S.gbeg[q2[u]]; g2 < S.gbeg[q2[u] + 1]; ++g2)
-                                        prefetch_l2(S.slots[S.gslot[g2]].rowptr + w[u]);
                             }
                         }
                     }
