@@ -126,6 +126,8 @@ struct rpq_query {
     size_t in_bytes = 0, off_slots = 0, off_tables = 0;
     unsigned int bar_next = 0;      // barrier counter value the next run starts from
     unsigned long long* d_slot_nnz = nullptr;
+    float dmax_ne = 0.0f;  // the densest slot's mean degree over non-empty rows
+    int use_dmax_ne = 1;   // RPQ_TUNE_FLAGS bit 3 clears it (the round-1 all-rows mean)
 
     uint32_t* d_visited = nullptr;
     uint32_t* d_fb[3] = {nullptr, nullptr, nullptr};
@@ -157,7 +159,7 @@ struct rpq_query {
     int emit_mode = 0;
     unsigned int emit_inline_max = 1u << 16;
     unsigned int run_flags = RF_NO_PROBE;
-    float defer_alpha = 3.0f;  // RPQ_TUNE_DEFER (profiles/r01_defer_sweep.txt)
+    float defer_alpha = 1.5f;  // RPQ_TUNE_DEFER, with the non-empty-row degree (r02ab sweep: 3 mispredicts cfg5)
     long long own_w0 = 0, own_w1 = 0;  // owned word range (partitioned step); empty = all
     bool small_ok = false;    // |Q| x |V| fits the single-CTA kernel
     int allow_small = 1;      // RPQ_TUNE_SMALL
@@ -880,6 +882,19 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     if (!q->slots.empty()) std::memcpy(q->h_in + q->off_slots, q->slots.data(), q->slots.size() * sizeof(Slot));
     if (!T.empty()) std::memcpy(q->h_in + q->off_tables, T.data(), T.size() * sizeof(int32_t));
     QTRY(cudaMemset(q->d_ctl, 0, sizeof(Ctl)));
+    {   // mean degree over non-empty rows, per push slot (the defer predictor)
+        unsigned long long* d_cnt = nullptr;
+        QTRY(cudaMalloc(&d_cnt, sizeof(unsigned long long)));
+        for (size_t i = 0; i < ents.size(); ++i) {
+            if (!ents[i].rowptr[0] || q->slot_nnz[i] == 0) continue;
+            unsigned long long rows = 0;
+            QTRY(cudaMemset(d_cnt, 0, sizeof(unsigned long long)));
+            count_nonempty_kernel<<<4 * g->sm_count, 256>>>(ents[i].rowptr[0], g->nv, d_cnt);
+            QTRY(cudaMemcpy(&rows, d_cnt, sizeof(rows), cudaMemcpyDeviceToHost));
+            if (rows) q->dmax_ne = std::max(q->dmax_ne, (float)((double)q->slot_nnz[i] / (double)rows));
+        }
+        cudaFree(d_cnt);
+    }
     if (!q->slot_nnz.empty())
         QTRY(cudaMemcpy(q->d_slot_nnz, q->slot_nnz.data(), q->slot_nnz.size() * sizeof(unsigned long long),
                         cudaMemcpyHostToDevice));
@@ -959,6 +974,7 @@ Params make_params(const rpq_query* q) {
     p.trace = q->d_trace;
     p.trace_levels = q->d_trace ? q->trace_levels : 0;
     p.step_acc = q->d_step_acc;
+    p.dmax_ne = q->use_dmax_ne ? q->dmax_ne : 0.0f;
     return p;
 }
 
@@ -1068,8 +1084,17 @@ int rpq_query_set_tuning(rpq_query* q, int32_t key, double value) {
             q->allow_small = (int)value;
             return RPQ_OK;
         case RPQ_TUNE_FLAGS:
-            if (value < 0 || value > 7) return fail(RPQ_EINVAL, "flags must be in [0, 7]");
-            q->run_flags = (unsigned)value;
+            if (value < 0 || value > 15) return fail(RPQ_EINVAL, "flags must be in [0, 15]");
+            q->run_flags = (unsigned)value & 7u;
+            if (q->use_dmax_ne != !((unsigned)value & 8u)) {
+                if (q->inflight) {  // let a run in flight finish with the old graph
+                    CUDA_TRY(cudaStreamSynchronize(q->last_stream));
+                    q->bar_next = q->h_ctl->bar;
+                    q->inflight = false;
+                }
+                q->use_dmax_ne = !((unsigned)value & 8u);
+                drop_graphs(q);  // the captured runs carry the predictor's degree
+            }
             return RPQ_OK;
         case RPQ_TUNE_TRACE: {
             if (value < 0 || value > 4096) return fail(RPQ_EINVAL, "trace levels must be in [0, 4096]");

@@ -172,6 +172,7 @@ struct Params {
     int maxT;
     int table_ints;
     unsigned long long* trace;  // diagnostics: [level][cta][4] globaltimer stamps, or null
+    float dmax_ne;              // the densest slot's mean degree over its non-empty rows (0: unknown)
     unsigned int* step_acc;     // step mode: [0] steps that found M non-empty, [1] sticky failure
                                 // status of any step (zeroed by rpq_query_step_begin)
     int trace_levels;
@@ -1253,7 +1254,10 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
         s_view.cut_edges = 0.0f;
         float d = 0.0f;
         for (int sl = 0; sl < p.nslots; ++sl) d = fmaxf(d, (float)p.slot_nnz[sl]);
-        s_view.dmax = d * __frcp_rn((float)max(p.nv, 1));
+        // the defer prediction's degree: over non-empty rows when known (the
+        // discovered vertices of a BFS are biased to rows with edges; on R-MAT
+        // the mean over all rows underestimates their degree ~3x)
+        s_view.dmax = p.dmax_ne > 0.0f ? p.dmax_ne : d * __frcp_rn((float)max(p.nv, 1));
     }
     Smem S;
     S.pf = policy_evict_first();
@@ -1444,6 +1448,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
     // ---- level loop -----------------------------------------------------------
     int L = 0;
     int dir = DIR_PUSH;
+    uint32_t qbsz = kBundle;  // bundle size the current queue was emitted with (the seed's: not merged)
     for (;;) {
         if (s_view.done) break;
         stamp(p, L, 0);
@@ -1454,6 +1459,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
         if (dir == DIR_PUSH && s_view.plan) {
             // ---- plan epoch: emit F_L's row segments from its bitmap (after pull)
             const uint32_t bsz = s_view.nfront < (unsigned long long)nwarps * 8 ? 32u : (uint32_t)kBundle;
+            qbsz = bsz;
             const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, bsz};
             if (cta0) reset_qc(ctl, (e + 2) % 3, threadIdx.x);
             unsigned long long nedge = 0;
@@ -1501,6 +1507,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
                                      (unsigned long long)nwarps * 4
                                  ? 32u : (uint32_t)kBundle;
         const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, bsz};
+        const uint32_t qbsz_next = bsz;
         if (threadIdx.x == 0) {
             s_task = 0;
             s_cut = 0;
@@ -1549,6 +1556,16 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
             unsigned long long* steal = &ctl->steal[e % 3][0];
             // software pipeline: the next bundle's descriptor is in flight while
             // this one is expanded (one dependent round trip less per bundle)
+            // descriptor of bundle b (b warp-uniform): its shard is
+            // #{i in [1, kShards] : s_bpre[i] <= b} (s_bpre is non-decreasing):
+            // lanes test every 8th entry, then the 7 inside the block found
+            auto load_bundle = [&](unsigned long long b) -> uint2 {
+                const int ci = 8 * (lane + 1);
+                const int c = __popc(__ballot_sync(FULL, ci <= kShards && s_bpre[ci] <= b));
+                const int fi = 8 * c + 1 + lane;
+                const int sh = 8 * c + __popc(__ballot_sync(FULL, lane < 7 && fi <= kShards && s_bpre[fi] <= b));
+                return ld_queue(bun + (unsigned long long)sh * p.shard_buncap + (b - s_bpre[sh]), S.pf);
+            };
             auto grab = [&](uint2* d) -> unsigned long long {
                 unsigned long long b = 0;
                 if (lane == 0) {
@@ -1556,29 +1573,102 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
                     if (b >= nb_own && nb_own < nb) b = nb_own + atomicAdd(steal, 1ull);
                 }
                 b = __shfl_sync(FULL, b, 0);
-                if (b < nb) {
-                    // shard of bundle b = #{i in [1, kShards] : s_bpre[i] <= b}
-                    // (s_bpre is non-decreasing): lanes test every 8th entry,
-                    // then the 7 inside the block found (two ballots; b is
-                    // warp-uniform, so every lane is here)
-                    const int ci = 8 * (lane + 1);
-                    const int c = __popc(__ballot_sync(FULL, ci <= kShards && s_bpre[ci] <= b));
-                    const int fi = 8 * c + 1 + lane;
-                    const int sh = 8 * c + __popc(__ballot_sync(FULL, lane < 7 && fi <= kShards && s_bpre[fi] <= b));
-                    *d = ld_queue(bun + (unsigned long long)sh * p.shard_buncap + (b - s_bpre[sh]), S.pf);
-                }
+                if (b < nb) *d = load_bundle(b);
                 return b;
             };
+            // A large queue of small bundles (a level whose predecessor was
+            // small emits 32-edge bundles; R-MAT grows 200x a level early on):
+            // a warp takes 4 bundles per grab, one per edge slot of its lanes,
+            // instead of leaving three slots of every lane idle.
+            const bool merge4 = qbsz <= 32u && nb >= (unsigned long long)nwarps * 8;
             uint2 bd_next = make_uint2(0u, kHoleY);
-            unsigned long long bi_next = grab(&bd_next);
+            unsigned long long bi_next = merge4 ? 0ull : grab(&bd_next);
             for (;;) {
+                int w[kEdgesPerLane], gj[kEdgesPerLane];
+                if (merge4) {
+                    // the CTA's own indices i4 .. i4+3; those past nb_own (a
+                    // suffix) are replaced by as many from the grid-wide tail
+                    unsigned long long i4 = 0, t4 = 0;
+                    int u0 = kEdgesPerLane;  // first slot past nb_own
+                    if (lane == 0) {
+                        i4 = atomicAdd(&s_task, (unsigned)kEdgesPerLane);
+                        if (nb_own < nb)
+                            for (int u = kEdgesPerLane - 1; u >= 0; --u)
+                                if ((i4 + u) * G + blockIdx.x >= nb_own) u0 = u;
+                        if (u0 < kEdgesPerLane) t4 = nb_own + atomicAdd(steal, (unsigned long long)(kEdgesPerLane - u0));
+                    }
+                    i4 = __shfl_sync(FULL, i4, 0);
+                    t4 = __shfl_sync(FULL, t4, 0);
+                    u0 = __shfl_sync(FULL, u0, 0);
+                    // lane u < 4 loads descriptor u (all four in flight); the
+                    // decode below broadcasts them one at a time
+                    const uint2* myaddr = nullptr;
+                    bool anyb = false;
+#pragma unroll
+                    for (int u = 0; u < kEdgesPerLane; ++u) {
+                        unsigned long long b = (i4 + u) * G + blockIdx.x;
+                        if (u >= u0) b = t4 + (u - u0);
+                        if (b < nb) {
+                            const int ci = 8 * (lane + 1);
+                            const int c = __popc(__ballot_sync(FULL, ci <= kShards && s_bpre[ci] <= b));
+                            const int fi = 8 * c + 1 + lane;
+                            const int sh =
+                                8 * c + __popc(__ballot_sync(FULL, lane < 7 && fi <= kShards && s_bpre[fi] <= b));
+                            if (lane == u) myaddr = bun + (unsigned long long)sh * p.shard_buncap + (b - s_bpre[sh]);
+                            anyb = true;
+                        }
+                    }
+                    if (!anyb) break;
+                    const uint2 mybd = myaddr ? ld_queue(myaddr, S.pf) : make_uint2(0u, kHoleY);
+#pragma unroll
+                    for (int u = 0; u < kEdgesPerLane; ++u) {
+                        const uint2 bdu = make_uint2(__shfl_sync(FULL, mybd.x, u), __shfl_sync(FULL, mybd.y, u));
+                        gj[u] = -1;
+                        w[u] = 0;
+                        if (bdu.y == kHoleY) continue;  // warp-uniform
+                        const uint32_t cu = (bdu.y & 127u) + 1;
+                        if (bdu.y & kInline) {
+                            const int g = (int)((bdu.y >> 7) & 0xFFu);
+                            const bool okc = (uint32_t)lane < cu &&
+                                             RPQ_CHECK(bdu.x + lane < p.slot_nnz[S.gslot[g] % p.nslots], RPQ_F_SSR);
+                            gj[u] = okc ? g : -1;
+                            w[u] = okc ? ld_stream_i32(S.slots[S.gslot[g]].col + bdu.x + lane, S.pf) : 0;
+                        } else {
+                            const uint32_t off = (bdu.y >> 7) & 0xFFFFFFu;
+                            uint32_t my_start = 0, my_len = 0, my_grp = 0;
+                            if ((unsigned long long)bdu.x + lane < p.seg_alloc) {
+                                const uint2 sg = ld_queue(seg + bdu.x + lane, S.pf);
+                                my_start = sg.x;
+                                my_len = sg.y >> 8;
+                                my_grp = sg.y & 0xFFu;
+                            }
+                            if (lane == 0) {
+                                my_start += off;
+                                my_len -= off;
+                            }
+                            const uint32_t incl = warp_incl_scan(my_len, lane);
+                            const uint32_t excl = incl - my_len;
+                            const bool active = (uint32_t)lane < cu;
+                            const int j = warp_upper_lane(excl, active ? (uint32_t)lane : 0u);
+                            const uint32_t sj = __shfl_sync(FULL, my_start, j);
+                            const uint32_t exj = __shfl_sync(FULL, excl, j);
+                            const int g = (int)__shfl_sync(FULL, my_grp, j);
+                            const bool okc = active && RPQ_CHECK(g >= 0 && g < p.ngroups &&
+                                                                     sj + ((uint32_t)lane - exj) <
+                                                                         p.slot_nnz[S.gslot[g] % p.nslots],
+                                                                 RPQ_F_SSR);
+                            gj[u] = okc ? g : -1;
+                            w[u] = okc ? ld_stream_i32(S.slots[S.gslot[g]].col + sj + ((uint32_t)lane - exj), S.pf)
+                                       : 0;
+                        }
+                    }
+                } else {
                 const unsigned long long bi = bi_next;
                 if (bi >= nb) break;
                 const uint2 bd = bd_next;
                 bi_next = grab(&bd_next);
                 if (bd.y == kHoleY) continue;
                 const uint32_t cnt = (bd.y & 127u) + 1;
-                int w[kEdgesPerLane], gj[kEdgesPerLane];
                 if (bd.y & kInline) {
                     // one row: columns bd.x .. bd.x + cnt - 1
                     const int g = (int)((bd.y >> 7) & 0xFFu);
@@ -1622,6 +1712,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
                         w[u] = okc ? ld_stream_i32(S.slots[S.gslot[g]].col + sj + (ed - exj), S.pf) : 0;
                     }
                 }
+                }  // single bundle
                 // probe P for every target, then claim with atomicOr
                 for (int k = 0; k < p.maxT; ++k) {
                     uint32_t old[kEdgesPerLane];
@@ -1738,6 +1829,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
         stamp(p, L, 3);
         if (cta0 && threadIdx.x == 0 && L < 64) ctl->bar_ns[L] = globaltimer() - ctl->t0;
         ++L;
+        qbsz = qbsz_next;
         if (step_mode) {
             if (threadIdx.x == 0) {
                 s_view.done = 1;
@@ -1868,6 +1960,16 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
             }
         }
     }
+}
+
+// Non-empty rows of a CSR (the defer predictor's mean degree), one atomic per warp.
+__global__ void count_nonempty_kernel(const uint32_t* __restrict__ rowptr, long long nv,
+                                      unsigned long long* __restrict__ out) {
+    unsigned c = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x)
+        c += rowptr[i + 1] > rowptr[i];
+    c = __reduce_add_sync(0xFFFFFFFFu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
 }
 
 // uint8[nv] answer vector from the answer bitmap (bit v%32 of word v/32):
