@@ -1212,7 +1212,7 @@ __device__ __forceinline__ void stamp(const Params& p, int L, int k) {
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(Params p) {
+__global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_constant__ Params p) {
     constexpr int kWarps = NT / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ unsigned long long s_red[2 * kWarps];
