@@ -35,7 +35,6 @@ constexpr int kBlockWords = 1 << kBlockShift;
 constexpr int kBEdges = 4;             // edges per lane in flight per step (chunks)
 constexpr int kBThreads = kThreadsLarge;  // batch state spaces are large: 32 warps per SM
 constexpr int kBWarps = kBThreads / 32;
-constexpr int kListCap = 3 * kBThreads; // phase 1: a CTA lists up to this many of its blocks at once
 constexpr int kGroups = 2;             // phase 1: groups of a state expanded together
 constexpr int kGEdges = 2;             // phase 1: edges per lane and group per step
 
@@ -47,7 +46,8 @@ struct BCnt {
     unsigned long long nnew;   // |M_L| summed over sources (from the items)
     unsigned long long items;  // (state, vertex) words of M_L that were non-empty
     unsigned int active;       // sources with a non-empty M_L
-    unsigned int pad;
+    unsigned int nlist;        // active blocks of M_L listed (the level's global block list)
+    unsigned long long steal;  // the list's grid-wide tail counter
 };
 
 struct BCtl {
@@ -86,6 +86,7 @@ struct BParams {
     uint32_t* fw[2];
     uint32_t* act[2];  // [nstates][nblk] activity flags by level parity
     uint4* heavy;
+    uint32_t* blist;  // [nstates * nblk] the level's active blocks
     BCtl* ctl;
     uint32_t* out;   // [kBatch][W] answer bitmaps
     long long nvp;   // words per state row of vis / fw (>= nv, multiple of kBlockWords)
@@ -196,9 +197,7 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ unsigned long long s_red[5 * kBWarps];
     __shared__ unsigned s_or;
-    __shared__ unsigned s_task;
-    __shared__ unsigned s_nlist;
-    __shared__ uint32_t s_list[kListCap];  // active blocks of the current group
+    __shared__ uint32_t s_words[kBWarps * kBlockWords];  // each warp's current block of M_L words
     __shared__ int s_single;  // every (state, symbol) group has exactly one target (a DFA)
     __shared__ BatchArgs s_run;
 
@@ -321,6 +320,8 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
             old->nnew = 0;
             old->items = 0;
             old->active = 0;
+            old->nlist = 0;
+            old->steal = 0;
             if (L < 64) {
                 ctl->level_ns[L] = now - ctl->t0;
                 ctl->level_rows[L] = ldcg(&ctl->rows);
@@ -340,43 +341,58 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
         // ---- phase 1: a warp per active block; light rows now, heavy rows as chunks
         unsigned long long te = 0, rows = 0, nnew = 0, items = 0;
         uint32_t active = 0;
-        // CTA c owns blocks c, c + G, c + 2G, ... (hubs spread over SMs); it
-        // reads kListCap of their flags at once, lists the active ones in
-        // shared memory, and its warps take them from a shared counter
-        for (long long i0 = 0; blockIdx.x + i0 * gridDim.x < nbt; i0 += kListCap) {
-            if (threadIdx.x == 0) {
-                s_nlist = 0;
-                s_task = 0;
+        // The level's active blocks are listed grid-wide first (one flag read
+        // per block, coalesced; one atomic per warp), then dealt to every warp
+        // of the grid: the first three quarters by a fixed stride, the rest
+        // from one grid-wide counter, so the CTAs that finish early take the
+        // tail (a per-CTA share of the blocks left 38% of the samples waiting
+        // at the phase barriers).
+        for (long long b0 = (long long)blockIdx.x * kBThreads; b0 < nbt; b0 += (long long)gridDim.x * kBThreads) {
+            const long long b = b0 + threadIdx.x;
+            const bool a = b < nbt && __ldcg(acur + b) != 0u;
+            if (a) acur[b] = 0u;  // consumed (level L+2 raises it again)
+            const unsigned m = __ballot_sync(FULL, a);
+            if (m) {
+                unsigned base = 0;
+                if (lane == 0) base = atomicAdd(&cur->nlist, (unsigned)__popc(m));
+                base = __shfl_sync(FULL, base, 0);
+                if (a) p.blist[base + __popc(m & lanemask_lt())] = (uint32_t)b;
             }
-            __syncthreads();
-            for (int t = threadIdx.x; t < kListCap; t += kBThreads) {  // all flag loads in flight
-                const long long b = blockIdx.x + (i0 + t) * gridDim.x;
-                if (b < nbt && __ldcg(acur + b) != 0u) {
-                    acur[b] = 0u;  // consumed (level L+2 raises it again)
-                    s_list[atomicAdd(&s_nlist, 1u)] = (uint32_t)b;
-                }
-            }
-            __syncthreads();
-            const unsigned nlisted = s_nlist;
+        }
+        grid_barrier_on(&ctl->bar, &ctl->abort, ++e, bar_base);
+        const unsigned long long nlisted = ldcg(&cur->nlist);
+        const unsigned long long gwarp_b = (unsigned long long)blockIdx.x * kBWarps + wid;
+        const unsigned long long nwarps_b = (unsigned long long)gridDim.x * kBWarps;
+        const unsigned long long nown = nlisted - nlisted / 4;
+        unsigned long long kk = gwarp_b;
         for (;;) {
-            unsigned k = 0;
-            if (lane == 0) k = atomicAdd(&s_task, 1u);
-            k = __shfl_sync(FULL, k, 0);
+            unsigned long long k = kk;
+            if (k >= nown) {  // the stolen tail
+                if (lane == 0) k = nown + atomicAdd(&cur->steal, 1ull);
+                k = __shfl_sync(FULL, k, 0);
+            }
+            kk += nwarps_b;
             if (k >= nlisted) break;
-            const long long blk = s_list[k];
+            const long long blk = p.blist[k];
             const int q = (int)(blk / p.nblk);
             const long long v0 = (blk - (long long)q * p.nblk) * kBlockWords;
             uint32_t* row = fcur + (long long)q * p.nvp;
-            uint32_t wv[kBlockWords / 32];
+            // the block's words, all loads in flight, parked in this warp's
+            // shared slots (a register array indexed by the loop would be
+            // selected element by element)
+            uint32_t* wsm = s_words + wid * kBlockWords;
+            {
+                uint32_t wv[kBlockWords / 32];
 #pragma unroll
-            for (int r = 0; r < kBlockWords / 32; ++r) wv[r] = __ldcg(row + v0 + 32 * r + lane);  // all in flight
+                for (int r = 0; r < kBlockWords / 32; ++r) wv[r] = __ldcg(row + v0 + 32 * r + lane);
+#pragma unroll
+                for (int r = 0; r < kBlockWords / 32; ++r) wsm[32 * r + lane] = wv[r];
+            }
+            __syncwarp();
             const int ng = gbeg[q + 1] - gbeg[q];
 #pragma unroll 1
             for (int r = 0; r < kBlockWords / 32; ++r) {
-                uint32_t w = 0;
-#pragma unroll
-                for (int r2 = 0; r2 < kBlockWords / 32; ++r2)
-                    if (r2 == r) w = wv[r2];
+                const uint32_t w = wsm[32 * r + lane];
                 if (!__any_sync(FULL, w != 0u)) continue;
                 const int v = (int)(v0 + 32 * r + lane);
                 if (w) {
@@ -484,8 +500,6 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
                     }
                 }
             }
-        }
-            __syncthreads();  // s_list / s_task are refilled for the next group of blocks
         }
         bphase_end(p, nxt, nact, te, rows, nnew, items, active, cur, s_red, &s_or);
         nact = 0;

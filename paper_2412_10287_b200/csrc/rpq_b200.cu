@@ -184,6 +184,7 @@ struct rpq_query {
     uint32_t* d_bfw[2] = {nullptr, nullptr};
     uint32_t* d_bact[2] = {nullptr, nullptr};
     uint4* d_bheavy = nullptr;
+    uint32_t* d_blist = nullptr;  // the batch kernel's per-level active-block list
     BCtl* d_bctl = nullptr;
     BCtl* h_bctl = nullptr;  // pinned
     BatchArgs* d_bargs = nullptr;
@@ -455,6 +456,7 @@ void free_query_buffers(rpq_query* q) {
         if (q->d_bact[b]) cudaFree(q->d_bact[b]);
     }
     if (q->d_bheavy) cudaFree(q->d_bheavy);
+    if (q->d_blist) cudaFree(q->d_blist);
     if (q->d_bctl) cudaFree(q->d_bctl);
     if (q->h_bctl) cudaFreeHost(q->h_bctl);
     if (q->d_bargs) cudaFree(q->d_bargs);
@@ -1525,6 +1527,8 @@ int batch_alloc(rpq_query* q) {
                 q->d_bact[b] = nullptr;                               \
             }                                                         \
             if (q->d_bheavy) cudaFree(q->d_bheavy);                   \
+            if (q->d_blist) cudaFree(q->d_blist);                     \
+            q->d_blist = nullptr;                                     \
             if (q->d_bctl) cudaFree(q->d_bctl);                       \
             if (q->h_bctl) cudaFreeHost(q->h_bctl);                   \
             if (q->d_bargs) cudaFree(q->d_bargs);                     \
@@ -1554,6 +1558,7 @@ int batch_alloc(rpq_query* q) {
         BTRY(cudaMalloc(&q->d_bfw[b], words * 4));
         BTRY(cudaMalloc(&q->d_bact[b], (size_t)q->nstates * (size_t)q->bnblk * 4));
     }
+    BTRY(cudaMalloc(&q->d_blist, (size_t)q->nstates * (size_t)q->bnblk * sizeof(uint32_t)));
     BTRY(cudaMalloc(&q->d_bheavy, (size_t)q->bheavy_cap * sizeof(uint4)));
     BTRY(cudaMalloc(&q->d_bctl, sizeof(BCtl)));
     BTRY(cudaMemset(q->d_bctl, 0, sizeof(BCtl)));
@@ -1608,6 +1613,7 @@ int rpq_query_run_batch(rpq_query* q, int32_t nsrc, const int32_t* sources, doub
         p.act[b] = q->d_bact[b];
     }
     p.heavy = q->d_bheavy;
+    p.blist = q->d_blist;
     p.ctl = q->d_bctl;
     p.out = q->d_bout;
     p.nvp = q->bnvp;
