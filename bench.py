@@ -716,7 +716,7 @@ def run_partitioned(args, rank, world, local_rank):
 
 def run_batch_mode(args, rank, world, local_rank):
     """Multi-source throughput: the config's source set (cfg5: 1,024 uniform
-    sources) sharded over ranks, 32 sources per launch of the bit-sliced batch
+    sources) sharded over ranks, 64 sources per launch of the bit-sliced batch
     kernel; value = sum of TE over all sources / max over ranks of the
     device time.  Weak scaling in the sources per rank."""
     import torch
@@ -739,7 +739,7 @@ def run_batch_mode(args, rank, world, local_rank):
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
-    batches = [sources[b:b + 32] for b in range(0, len(sources), 32)]
+    batches = [sources[b:b + P._lib.BATCH] for b in range(0, len(sources), P._lib.BATCH)]
     te = 0
     for b in batches:
         pq.launch_batch(b, -1.0, stream.cuda_stream)
@@ -783,7 +783,7 @@ def run_batch_mode(args, rank, world, local_rank):
         "data": "synthetic",
         "config": {**workload_config(args, sg, all_sources[:4] + ["..."], world),
                    "sources_total": len(all_sources), "sources_per_rank": per,
-                   "parallelism": f"{world} GPU(s), sources sharded over ranks, 32 per batch-kernel launch"},
+                   "parallelism": f"{world} GPU(s), sources sharded over ranks, 64 per batch-kernel launch"},
         "mode": "batch", "gpu_launches": launches, "clocks": clocks,
     }
 

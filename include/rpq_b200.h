@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define RPQ_ABI_VERSION 2
+#define RPQ_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define RPQ_API __attribute__((visibility("default")))
@@ -90,7 +90,7 @@ typedef struct rpq_stats {
 } rpq_stats;
 
 /* Multi-source batches: up to RPQ_BATCH sources per run (one bit each). */
-#define RPQ_BATCH 32
+#define RPQ_BATCH 64
 
 typedef struct rpq_batch_stats {
     int32_t status;          /* RPQ_* of the run */

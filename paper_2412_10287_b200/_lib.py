@@ -25,7 +25,7 @@ DIR_PUSH = 1
 DIR_PULL = 2
 
 STATS_LEVELS = 64
-ABI_VERSION = 2  # include/rpq_b200.h RPQ_ABI_VERSION
+ABI_VERSION = 3  # include/rpq_b200.h RPQ_ABI_VERSION
 
 # rpq_query_set_tuning keys (include/rpq_b200.h RPQ_TUNE_*)
 TUNE_EMIT_MODE = 0
@@ -92,7 +92,7 @@ class RpqStats(ctypes.Structure):
         }
 
 
-BATCH = 32
+BATCH = 64  # include/rpq_b200.h RPQ_BATCH
 
 
 class RpqBatchStats(ctypes.Structure):

@@ -1,6 +1,6 @@
-// batch_kernel.cuh -- up to 32 single-source 2-RPQs from different sources in
+// batch_kernel.cuh -- up to 64 single-source 2-RPQs from different sources in
 // ONE persistent launch, bit-sliced: every (state q, vertex v) pair carries a
-// 32-bit word whose bit s says "(q, v) belongs to source s's set".  Per source
+// 64-bit word whose bit s says "(q, v) belongs to source s's set".  Per source
 // this is exactly the masked evaluator (rpq/engine.py:146-171):
 //   M_s <- step(M_s) <not P_s>;  P_s <- P_s + M_s
 // but a frontier row v is read ONCE for all sources whose frontier holds
@@ -8,8 +8,8 @@
 // (SURVEY.md §8(d) "batched sources", §8(e) regime 1).
 //
 // Layout:
-//   vis[q][v]     uint32 source word: P, one row of nvp words per state
-//   fw[L&1][q][v] uint32 source word: M at level L.  A word is cleared when
+//   vis[q][v]     64-bit source word: P, one row of nvp words per state
+//   fw[L&1][q][v] 64-bit source word: M at level L.  A word is cleared when
 //                 it is expanded, so fw[(L+1)&1] is all zero again when level
 //                 L+1 starts writing it
 //   act[L&1][q][b] one flag per 256-vertex block of M_L holding a non-empty
@@ -27,7 +27,8 @@
 
 namespace rpqk {
 
-constexpr int kBatch = 32;             // sources per launch (bits of a source word)
+constexpr int kBatch = 64;             // sources per launch (bits of a source word)
+using SW = unsigned long long;         // a source word: bit s = "in source s's set"
 constexpr uint32_t kLightDeg = 64;     // rows up to this many edges stay in phase 1
 constexpr uint32_t kChunk = 256;       // edges per heavy chunk
 constexpr int kBlockShift = 8;         // activity flag per 2^8 vertices
@@ -35,6 +36,7 @@ constexpr int kBlockWords = 1 << kBlockShift;
 constexpr int kBEdges = 4;             // edges per lane in flight per step (chunks)
 constexpr int kBThreads = kThreadsLarge;  // batch state spaces are large: 32 warps per SM
 constexpr int kBWarps = kBThreads / 32;
+constexpr size_t kBWordsBytes = (size_t)kBWarps * (1 << 8) * sizeof(unsigned long long);  // 64 KB
 constexpr int kGroups = 2;             // phase 1: groups of a state expanded together
 constexpr int kGEdges = 2;             // phase 1: edges per lane and group per step
 
@@ -45,8 +47,9 @@ struct BCnt {
     unsigned int expire;       // the deadline check at the top of level L failed
     unsigned long long nnew;   // |M_L| summed over sources (from the items)
     unsigned long long items;  // (state, vertex) words of M_L that were non-empty
-    unsigned int active;       // sources with a non-empty M_L
+    SW active;                 // sources with a non-empty M_L
     unsigned int nlist;        // active blocks of M_L listed (the level's global block list)
+    unsigned int pad2;
     unsigned long long steal;  // the list's grid-wide tail counter
 };
 
@@ -66,7 +69,7 @@ struct BCtl {
     unsigned long long level_new[64];
     unsigned long long level_ns[64];
     unsigned long long level_rows[64];  // edges read before level L starts (cumulative)
-    unsigned int level_active[64];
+    SW level_active[64];
     // ---- working counters ------------------------------------------------
     BCnt bc[3];
 };
@@ -78,14 +81,19 @@ struct BatchArgs {
     int sources[kBatch];
 };
 
+struct BHeavy {  // a heavy-row chunk: edges [a, b) of group g, for the sources of w
+    uint32_t a, b, g, pad;
+    SW w;
+};
+
 struct BParams {
     const BatchArgs* run;
     const int32_t* tables;
     const Slot* slots;
-    uint32_t* vis;
-    uint32_t* fw[2];
+    SW* vis;
+    SW* fw[2];
     uint32_t* act[2];  // [nstates][nblk] activity flags by level parity
-    uint4* heavy;
+    BHeavy* heavy;
     uint32_t* blist;  // [nstates * nblk] the level's active blocks
     BCtl* ctl;
     uint32_t* out;   // [kBatch][W] answer bitmaps
@@ -106,20 +114,20 @@ struct BParams {
 // store: idempotent, nothing to wait for) and counts toward M_{L+1}'s
 // non-emptiness.
 template <int K>
-__device__ __forceinline__ void bvisit(const BParams& p, uint32_t* fnext, uint32_t* anext, const bool (&act)[K],
-                                       const int (&t)[K], const int (&u)[K], const uint32_t (&w)[K],
+__device__ __forceinline__ void bvisit(const BParams& p, SW* fnext, uint32_t* anext, const bool (&act)[K],
+                                       const int (&t)[K], const int (&u)[K], const SW (&w)[K],
                                        unsigned& nact) {
     long long off[K];
-    uint32_t seen[K];
+    SW seen[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) {
         off[c] = (long long)t[c] * p.nvp + u[c];
         const bool ok = !act[c] || RPQ_CHECK(t[c] >= 0 && t[c] < p.nstates && u[c] >= 0 && u[c] < p.nv, RPQ_F_BATCH);
-        seen[c] = act[c] && ok ? __ldcg(p.vis + off[c]) : 0xFFFFFFFFu;
+        seen[c] = act[c] && ok ? __ldcg(p.vis + off[c]) : ~0ull;
     }
 #pragma unroll
     for (int c = 0; c < K; ++c) {
-        const uint32_t nw = w[c] & ~seen[c];
+        const SW nw = w[c] & ~seen[c];
         if (nw) {
             atomicOr(p.vis + off[c], nw);  // results unused: RED
             atomicOr(fnext + off[c], nw);
@@ -132,7 +140,7 @@ __device__ __forceinline__ void bvisit(const BParams& p, uint32_t* fnext, uint32
 // Rows longer than kLightDeg become chunks of kChunk edges for phase 2 (one
 // atomic per warp); returns the degree phase 1 expands itself (0 if chunked).
 __device__ __forceinline__ uint32_t split_heavy(const BParams& p, BCnt* cur, BCnt* nxt, int g, uint32_t lo,
-                                                uint32_t deg, uint32_t w, int lane) {
+                                                uint32_t deg, SW w, int lane) {
     const bool heavy = deg > kLightDeg;
     const uint32_t nch = heavy ? (deg + kChunk - 1) / kChunk : 0u;
     const uint32_t cincl = warp_incl_scan(nch, lane);
@@ -147,7 +155,13 @@ __device__ __forceinline__ uint32_t split_heavy(const BParams& p, BCnt* cur, BCn
                 if (c0 + c < p.heavy_cap) {
                     const uint32_t a = lo + c * kChunk;
                     const uint32_t b = min(lo + deg, a + kChunk);
-                    p.heavy[c0 + c] = make_uint4(a, b, (uint32_t)g, w);
+                    BHeavy hv;
+                    hv.a = a;
+                    hv.b = b;
+                    hv.g = (uint32_t)g;
+                    hv.pad = 0;
+                    hv.w = w;
+                    p.heavy[c0 + c] = hv;
                 } else {
                     atomicExch(&nxt->overflow, 1u);
                 }
@@ -161,8 +175,8 @@ __device__ __forceinline__ uint32_t split_heavy(const BParams& p, BCnt* cur, BCn
 // End of a phase: per-CTA sums into the counters.
 __device__ __forceinline__ void bphase_end(const BParams& p, BCnt* nxt, unsigned nact, unsigned long long te,
                                            unsigned long long rows, unsigned long long nnew,
-                                           unsigned long long items, uint32_t act, BCnt* cnt,
-                                           unsigned long long* s_red, unsigned* s_or) {
+                                           unsigned long long items, SW act, BCnt* cnt,
+                                           unsigned long long* s_red, SW* s_or) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned long long a = warp_sum_u64(nnew), b = warp_sum_u64(te), r = warp_sum_u64(rows);
     const unsigned long long it = warp_sum_u64(items), na = warp_sum_u64(nact);
@@ -196,13 +210,14 @@ __device__ __forceinline__ void bphase_end(const BParams& p, BCnt* nxt, unsigned
 __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ unsigned long long s_red[5 * kBWarps];
-    __shared__ unsigned s_or;
-    __shared__ uint32_t s_words[kBWarps * kBlockWords];  // each warp's current block of M_L words
+    __shared__ SW s_or;
     __shared__ int s_single;  // every (state, symbol) group has exactly one target (a DFA)
     __shared__ BatchArgs s_run;
 
-    Slot* s_slots = reinterpret_cast<Slot*>(smem_raw);
-    int32_t* s_tab = reinterpret_cast<int32_t*>(smem_raw + sizeof(Slot) * 2 * p.nslots);
+    // dynamic smem: [each warp's current block of M_L words: kBWords] [slots] [tables]
+    SW* s_words = reinterpret_cast<SW*>(smem_raw);
+    Slot* s_slots = reinterpret_cast<Slot*>(smem_raw + kBWordsBytes);
+    int32_t* s_tab = reinterpret_cast<int32_t*>(smem_raw + kBWordsBytes + sizeof(Slot) * 2 * p.nslots);
     for (int i = threadIdx.x; i < 2 * p.nslots; i += blockDim.x) s_slots[i] = p.slots[i];
     for (int i = threadIdx.x; i < p.table_ints; i += blockDim.x) s_tab[i] = p.tables[i];
     if (threadIdx.x == 0) {
@@ -246,7 +261,7 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
 
     // ---- epoch 0: P <- 0, M <- 0, no active block, for every source
     {
-        const long long n4 = (long long)p.nstates * p.nvp / 4;
+        const long long n4 = (long long)p.nstates * p.nvp * (long long)sizeof(SW) / 16;  // uint4 units
         uint4* a = reinterpret_cast<uint4*>(p.vis);
         uint4* b = reinterpret_cast<uint4*>(p.fw[0]);
         uint4* c = reinterpret_cast<uint4*>(p.fw[1]);
@@ -265,18 +280,18 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
 
     // ---- epoch 1: seed P_s = M_s = {(q_s, source_s)} (engine.py:106-109)
     unsigned nact = 0;
-    if (cta0 && wid == 0 && lane < s_run.nsrc) {
-        const int src = s_run.sources[lane];
+    if (cta0 && threadIdx.x < s_run.nsrc) {  // source s = thread s (two warps)
+        const int src = s_run.sources[threadIdx.x];
         for (int i = 0; i < p.nstarts; ++i) {
             const int q = starts[i];
             const long long off = (long long)q * p.nvp + src;
-            atomicOr(p.vis + off, 1u << lane);
-            atomicOr(p.fw[0] + off, 1u << lane);
+            atomicOr(p.vis + off, 1ull << threadIdx.x);
+            atomicOr(p.fw[0] + off, 1ull << threadIdx.x);
             p.act[0][(long long)q * p.nblk + (src >> kBlockShift)] = 1u;
             ++nact;
         }
     }
-    bphase_end(p, &ctl->bc[0], nact, 0ull, 0ull, 0ull, 0ull, 0u, &ctl->bc[0], s_red, &s_or);
+    bphase_end(p, &ctl->bc[0], nact, 0ull, 0ull, 0ull, 0ull, 0ull, &ctl->bc[0], s_red, &s_or);
     nact = 0;
     grid_barrier_on(&ctl->bar, &ctl->abort, ++e, bar_base);
 
@@ -302,10 +317,10 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
             const unsigned long long now = globaltimer();
             BCnt* old = &ctl->bc[(L + 2) % 3];  // level L-1's counters: statistics, then reset
             if (L > 0) {
-                const unsigned act = ldcg(&old->active);
+                const SW act = ldcg(&old->active);
                 const unsigned long long nn = ldcg(&old->nnew);
                 for (int s = 0; s < kBatch; ++s)
-                    if (act >> s & 1u) ctl->last_level[s] = L - 1;
+                    if (act >> s & 1ull) ctl->last_level[s] = L - 1;
                 ctl->pairs += nn;
                 if (L - 1 < 64) {
                     ctl->level_new[L - 1] = nn;
@@ -336,11 +351,11 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
         }
         uint32_t* acur = p.act[L & 1];
         uint32_t* anext = p.act[(L + 1) & 1];
-        uint32_t* fcur = p.fw[L & 1];
-        uint32_t* fnext = p.fw[(L + 1) & 1];
+        SW* fcur = p.fw[L & 1];
+        SW* fnext = p.fw[(L + 1) & 1];
         // ---- phase 1: a warp per active block; light rows now, heavy rows as chunks
         unsigned long long te = 0, rows = 0, nnew = 0, items = 0;
-        uint32_t active = 0;
+        SW active = 0;
         // The level's active blocks are listed grid-wide first (one flag read
         // per block, coalesced; one atomic per warp), then dealt to every warp
         // of the grid: the first three quarters by a fixed stride, the rest
@@ -376,13 +391,13 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
             const long long blk = p.blist[k];
             const int q = (int)(blk / p.nblk);
             const long long v0 = (blk - (long long)q * p.nblk) * kBlockWords;
-            uint32_t* row = fcur + (long long)q * p.nvp;
+            SW* row = fcur + (long long)q * p.nvp;
             // the block's words, all loads in flight, parked in this warp's
             // shared slots (a register array indexed by the loop would be
             // selected element by element)
-            uint32_t* wsm = s_words + wid * kBlockWords;
+            SW* wsm = s_words + wid * kBlockWords;
             {
-                uint32_t wv[kBlockWords / 32];
+                SW wv[kBlockWords / 32];
 #pragma unroll
                 for (int r = 0; r < kBlockWords / 32; ++r) wv[r] = __ldcg(row + v0 + 32 * r + lane);
 #pragma unroll
@@ -392,12 +407,12 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
             const int ng = gbeg[q + 1] - gbeg[q];
 #pragma unroll 1
             for (int r = 0; r < kBlockWords / 32; ++r) {
-                const uint32_t w = wsm[32 * r + lane];
-                if (!__any_sync(FULL, w != 0u)) continue;
+                const SW w = wsm[32 * r + lane];
+                if (!__any_sync(FULL, w != 0ull)) continue;
                 const int v = (int)(v0 + 32 * r + lane);
                 if (w) {
-                    row[v] = 0u;        // fw[L&1] must be zero when level L+1 writes it
-                    nnew += __popc(w);  // M_L's (pair, source) members, each in exactly one word
+                    row[v] = 0ull;        // fw[L&1] must be zero when level L+1 writes it
+                    nnew += __popcll(w);  // M_L's (pair, source) members, each in exactly one word
                     ++items;
                     active |= w;
                 }
@@ -434,7 +449,7 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
                             }
                             const int g = gbeg[q] + kg0 + k;
                             deg[k] -= lo[k];
-                            te += (unsigned long long)deg[k] * __popc(w);
+                            te += (unsigned long long)deg[k] * __popcll(w);
                             rows += deg[k];
                             deg[k] = split_heavy(p, cur, nxt, g, lo[k], deg[k], w, lane);
                             const uint32_t incl = warp_incl_scan(deg[k], lane);
@@ -446,7 +461,7 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
                             constexpr int K = kGroups * kGEdges;
                             bool act[K];
                             int tt[K], uu[K];
-                            uint32_t ww[K];
+                            SW ww[K];
 #pragma unroll
                             for (int k = 0; k < kGroups; ++k) {
 #pragma unroll
@@ -474,7 +489,7 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
                             lo = sl.rowptr[v];
                             deg = sl.rowptr[v + 1] - lo;
                         }
-                        te += (unsigned long long)deg * __popc(w);
+                        te += (unsigned long long)deg * __popcll(w);
                         rows += deg;
                         deg = split_heavy(p, cur, nxt, g, lo, deg, w, lane);
                         const uint32_t incl = warp_incl_scan(deg, lane);
@@ -486,14 +501,14 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
                             const int j = warp_upper_lane(excl, x);
                             const uint32_t lo_j = __shfl_sync(FULL, lo, j);
                             const uint32_t ex_j = __shfl_sync(FULL, excl, j);
-                            const uint32_t w_j = __shfl_sync(FULL, w, j);
+                            const SW w_j = __shfl_sync(FULL, w, j);
                             const bool a0 = x < T;
                             const int u = a0 ? col[lo_j + (x - ex_j)] : 0;
                             for (int t = toff[g]; t < toff[g + 1]; ++t) {
                                 const bool act[1] = {a0};
                                 const int tt[1] = {targets[t]};
                                 const int uu[1] = {u};
-                                const uint32_t ww[1] = {w_j};
+                                const SW ww[1] = {w_j};
                                 bvisit<1>(p, fnext, anext, act, tt, uu, ww, nact);
                             }
                         }
@@ -510,19 +525,19 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
         if (nh) {
             for (unsigned long long c = blockIdx.x + (unsigned long long)wid * gridDim.x; c < nh;
                  c += (unsigned long long)gridDim.x * kBWarps) {
-                const uint4 h = p.heavy[c];
-                const int g = (int)h.z;
+                const BHeavy h = p.heavy[c];
+                const int g = (int)h.g;
                 const int32_t* col = s_slots[gslot[g]].col;
                 const int t0 = toff[g], t1 = toff[g + 1];
                 if (s_single) {
-                    for (uint32_t a = h.x; a < h.y; a += 32 * kBEdges) {
+                    for (uint32_t a = h.a; a < h.b; a += 32 * kBEdges) {
                         bool act[kBEdges];
                         int tt[kBEdges], uu[kBEdges];
-                        uint32_t ww[kBEdges];
+                        SW ww[kBEdges];
 #pragma unroll
                         for (int c2 = 0; c2 < kBEdges; ++c2) {
                             const uint32_t x = a + 32 * c2 + lane;
-                            act[c2] = x < h.y;
+                            act[c2] = x < h.b;
                             uu[c2] = act[c2] ? col[x] : 0;
                             tt[c2] = targets[t0];
                             ww[c2] = h.w;
@@ -530,20 +545,20 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
                         bvisit<kBEdges>(p, fnext, anext, act, tt, uu, ww, nact);
                     }
                 } else {
-                    for (uint32_t a = h.x; a < h.y; a += 32) {
-                        const bool a0 = a + lane < h.y;
+                    for (uint32_t a = h.a; a < h.b; a += 32) {
+                        const bool a0 = a + lane < h.b;
                         const int u = a0 ? col[a + lane] : 0;
                         for (int t = t0; t < t1; ++t) {
                             const bool act[1] = {a0};
                             const int tt[1] = {targets[t]};
                             const int uu[1] = {u};
-                            const uint32_t ww[1] = {h.w};
+                            const SW ww[1] = {h.w};
                             bvisit<1>(p, fnext, anext, act, tt, uu, ww, nact);
                         }
                     }
                 }
             }
-            bphase_end(p, nxt, nact, 0ull, 0ull, 0ull, 0ull, 0u, cur, s_red, &s_or);
+            bphase_end(p, nxt, nact, 0ull, 0ull, 0ull, 0ull, 0ull, cur, s_red, &s_or);
             nact = 0;
             grid_barrier_on(&ctl->bar, &ctl->abort, ++e, bar_base);
         }
@@ -556,32 +571,41 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
         const long long nblk = (p.nv + 127) / 128;
         const long long gwarp = (long long)blockIdx.x * kBWarps + wid;
         const long long nwarps = (long long)gridDim.x * kBWarps;
-        unsigned long long cnt = 0;
+        unsigned long long cnt[2] = {0ull, 0ull};  // this lane's sources lane and 32 + lane
         for (long long b = gwarp; b < nblk; b += nwarps) {
-            uint32_t mine[4];
+            SW acc[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const long long v = b * 128 + 32 * k + lane;
-                uint32_t acc = 0;
+                acc[k] = 0;
                 if (v < p.nv)
-                    for (int f = 0; f < p.nfinals; ++f) acc |= p.vis[(long long)finals[f] * p.nvp + v];
-                mine[k] = 0;
-#pragma unroll 4
-                for (int s = 0; s < kBatch; ++s) {
-                    const uint32_t bits = __ballot_sync(FULL, (acc >> s) & 1u);
-                    if (lane == s) mine[k] = bits;
-                }
+                    for (int f = 0; f < p.nfinals; ++f) acc[k] |= p.vis[(long long)finals[f] * p.nvp + v];
             }
-            if (lane < s_run.nsrc) {
-                *reinterpret_cast<uint4*>(p.out + (long long)lane * p.W + b * 4) =
-                    make_uint4(mine[0], mine[1], mine[2], mine[3]);
-                cnt += __popc(mine[0]) + __popc(mine[1]) + __popc(mine[2]) + __popc(mine[3]);
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t mine[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    mine[k] = 0;
+#pragma unroll 4
+                    for (int s = 0; s < 32; ++s) {
+                        const uint32_t bits = __ballot_sync(FULL, (acc[k] >> (32 * half + s)) & 1ull);
+                        if (lane == s) mine[k] = bits;
+                    }
+                }
+                const int src = 32 * half + lane;
+                if (src < s_run.nsrc) {
+                    *reinterpret_cast<uint4*>(p.out + (long long)src * p.W + b * 4) =
+                        make_uint4(mine[0], mine[1], mine[2], mine[3]);
+                    cnt[half] += __popc(mine[0]) + __popc(mine[1]) + __popc(mine[2]) + __popc(mine[3]);
+                }
             }
         }
         // per source: shared-memory sums, then one global atomic per CTA
         if (threadIdx.x < kBatch) s_red[threadIdx.x] = 0ull;
         __syncthreads();
-        if (lane < s_run.nsrc && cnt) atomicAdd(&s_red[lane], cnt);
+        for (int half = 0; half < 2; ++half)
+            if (32 * half + lane < s_run.nsrc && cnt[half]) atomicAdd(&s_red[32 * half + lane], cnt[half]);
         __syncthreads();
         if (threadIdx.x < s_run.nsrc && s_red[threadIdx.x])
             atomicAdd(&ctl->reach_count[threadIdx.x], s_red[threadIdx.x]);

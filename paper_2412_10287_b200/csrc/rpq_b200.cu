@@ -180,10 +180,11 @@ struct rpq_query {
     int trace_levels = 0;
 
     // multi-source batch workspace (batch_kernel.cuh), allocated on first use
-    uint32_t* d_bvis = nullptr;
-    uint32_t* d_bfw[2] = {nullptr, nullptr};
+    SW* d_bvis = nullptr;
+    SW* d_bfw[2] = {nullptr, nullptr};
     uint32_t* d_bact[2] = {nullptr, nullptr};
-    uint4* d_bheavy = nullptr;
+    BHeavy* d_bheavy = nullptr;
+    size_t bsmem = 0;  // the batch kernel's dynamic shared memory
     uint32_t* d_blist = nullptr;  // the batch kernel's per-level active-block list
     BCtl* d_bctl = nullptr;
     BCtl* h_bctl = nullptr;  // pinned
@@ -1553,13 +1554,13 @@ int batch_alloc(rpq_query* q) {
     q->bheavy_cap = q->edge_bound / kLightDeg + q->edge_bound / kChunk + 1024;
     if (q->bheavy_cap >= 0xFFFFFFFFull) return fail(RPQ_EINVAL, "batch chunk list would exceed 2^32 entries");
     const size_t words = (size_t)q->nstates * (size_t)q->bnvp;
-    BTRY(cudaMalloc(&q->d_bvis, words * 4));
+    BTRY(cudaMalloc(&q->d_bvis, words * sizeof(SW)));
     for (int b = 0; b < 2; ++b) {
-        BTRY(cudaMalloc(&q->d_bfw[b], words * 4));
+        BTRY(cudaMalloc(&q->d_bfw[b], words * sizeof(SW)));
         BTRY(cudaMalloc(&q->d_bact[b], (size_t)q->nstates * (size_t)q->bnblk * 4));
     }
     BTRY(cudaMalloc(&q->d_blist, (size_t)q->nstates * (size_t)q->bnblk * sizeof(uint32_t)));
-    BTRY(cudaMalloc(&q->d_bheavy, (size_t)q->bheavy_cap * sizeof(uint4)));
+    BTRY(cudaMalloc(&q->d_bheavy, (size_t)q->bheavy_cap * sizeof(BHeavy)));
     BTRY(cudaMalloc(&q->d_bctl, sizeof(BCtl)));
     BTRY(cudaMemset(q->d_bctl, 0, sizeof(BCtl)));
     BTRY(cudaMallocHost(&q->h_bctl, sizeof(BCtl)));
@@ -1568,7 +1569,8 @@ int batch_alloc(rpq_query* q) {
     BTRY(cudaMalloc(&q->d_bout, (size_t)kBatch * (size_t)q->W * 4));
     BTRY(allow_dyn_smem((const void*)batch_kernel));
     int per_sm = 0;
-    BTRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batch_kernel, kBThreads, q->smem));
+    q->bsmem = kBWordsBytes + q->slots.size() * sizeof(Slot) + q->tables.size() * sizeof(int32_t) + 16;
+    BTRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batch_kernel, kBThreads, q->bsmem));
     if (per_sm < 1) BTRY(cudaErrorInvalidConfiguration);
     q->bgrid = q->g->sm_count * per_sm;
     q->bbar_next = 0;
@@ -1580,7 +1582,7 @@ int batch_alloc(rpq_query* q) {
 
 int rpq_query_run_batch(rpq_query* q, int32_t nsrc, const int32_t* sources, double timeout_s, void* stream) {
     if (!q) return fail(RPQ_EINVAL, "null query");
-    if (nsrc < 1 || nsrc > kBatch) return fail(RPQ_EINVAL, "nsrc must be in [1, 32]");
+    if (nsrc < 1 || nsrc > kBatch) return fail(RPQ_EINVAL, "nsrc must be in [1, " + std::to_string(kBatch) + "]");
     if (!sources) return fail(RPQ_EINVAL, "null sources");
     for (int i = 0; i < nsrc; ++i)
         if (sources[i] < 0 || sources[i] >= q->g->nv)
@@ -1634,7 +1636,7 @@ int rpq_query_run_batch(rpq_query* q, int32_t nsrc, const int32_t* sources, doub
     // the automaton tables live in the single-source input block: send it too
     CUDA_TRY(cudaMemcpyAsync(q->d_in, q->h_in, q->in_bytes, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(q->d_bargs, q->h_bargs, sizeof(BatchArgs), cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)batch_kernel, dim3(q->bgrid), dim3(kBThreads), args, q->smem,
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)batch_kernel, dim3(q->bgrid), dim3(kBThreads), args, q->bsmem,
                                          st));
     CUDA_TRY(cudaMemcpyAsync(q->h_bctl, q->d_bctl, offsetof(BCtl, bc), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaEventRecord(q->ev1, st));

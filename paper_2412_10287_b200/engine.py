@@ -413,9 +413,9 @@ def eval_ssr_batch(g, n, sources, opts, *, stats=None):
     """uint8[len(sources), |V|]: row i is eval_ssr(g, n, sources[i], opts)'s answer.
 
     Defined as the per-source loop; the reference has no
-    multi-source entry point.  Evaluated 32 sources per kernel launch with
+    multi-source entry point.  Evaluated 64 sources per kernel launch with
     bit-sliced frontiers (batch_kernel.cuh).  ``opts.timeout`` bounds each
-    launch of up to 32 sources.  If ``stats`` is a list, the statistics of
+    launch of up to 64 sources.  If ``stats`` is a list, the statistics of
     every launch are appended to it."""
     opts.validate()
     sources = [int(s) for s in sources]
@@ -555,7 +555,7 @@ class PreparedQuery:
         return stats
 
     def launch_batch(self, sources, timeout=-1.0, stream=None):
-        """Enqueue one multi-source run (<= 32 sources, bit-sliced)."""
+        """Enqueue one multi-source run (<= 64 sources, bit-sliced)."""
         src = np.ascontiguousarray([int(s) for s in sources], dtype=np.int32)
         for s in src:
             _check_vertex(self.g, int(s))

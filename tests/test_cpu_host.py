@@ -37,7 +37,7 @@ def test_engine_library_exports_header():
         assert hasattr(lib, s), s
     # the ctypes binding covers exactly the header
     assert syms == set(_lib.ENGINE_SIGNATURES)
-    assert _lib.engine().rpq_abi_version() == _lib.ABI_VERSION == 2
+    assert _lib.engine().rpq_abi_version() == _lib.ABI_VERSION == 3
 
 
 def test_header_constants_match_the_binding():

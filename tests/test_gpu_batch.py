@@ -62,8 +62,9 @@ def test_rmat_batch_vs_oracle(scale, seed, query):
     deg = sg.out_degree()
     rng = np.random.default_rng(seed)
     nz = np.flatnonzero(deg)
-    # 37 sources: two batches; hubs, a duplicate, isolated vertices, randoms
-    srcs = [int(np.argmax(deg)), 0, 0, sg.nv - 1] + [int(x) for x in rng.choice(nz, 33)]
+    # BATCH + 5 sources: two launches (the second partial); hubs, a
+    # duplicate, isolated vertices, randoms
+    srcs = [int(np.argmax(deg)), 0, 0, sg.nv - 1] + [int(x) for x in rng.choice(nz, P._lib.BATCH + 1)]
     stats = []
     got = P.eval_ssr_batch(g, n, srcs, P.EngineOptions(timeout=math.inf), stats=stats)
     assert len(stats) == 2
@@ -71,7 +72,7 @@ def test_rmat_batch_vs_oracle(scale, seed, query):
     for i, s in enumerate(srcs):
         want, st = oracle_bfs(og, oq, s)
         assert np.array_equal(got[i], want), (query, i, s)
-        b, k = divmod(i, 32)
+        b, k = divmod(i, P._lib.BATCH)
         assert stats[b]["iterations"][k] == st["iterations"], (query, s)
         assert stats[b]["reach_count"][k] == int(want.sum())
         te += st["te"]

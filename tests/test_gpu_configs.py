@@ -88,7 +88,7 @@ def test_cfg5_raw_automata_goldens(cfg5):
 ])
 def test_cfg5_bench_sources_batched(cfg5, query, kind, count):
     """BASELINE cfg5: the first `count` of the 1,024 uniform sources through
-    eval_ssr_batch (32 per launch) vs the oracle: answers, per-source
+    eval_ssr_batch (64 per launch) vs the oracle: answers, per-source
     iteration counts, and the batch's summed TE and |P|."""
     from oracle import OracleGraph
 
@@ -104,8 +104,8 @@ def test_cfg5_bench_sources_batched(cfg5, query, kind, count):
     for i, s in enumerate(srcs):
         w, st = want[s]
         assert np.array_equal(rows[i], w), (query, kind, s)
-        b = stats[i // 32]
-        assert b["iterations"][i % 32] == st["iterations"], (query, s)
+        b = stats[i // P._lib.BATCH]
+        assert b["iterations"][i % P._lib.BATCH] == st["iterations"], (query, s)
         te += st["te"]
         pairs += st["pairs"]
     assert sum(x["te"] for x in stats) == te

@@ -1,4 +1,4 @@
-"""Multi-source throughput: the bit-sliced batch kernel (32 sources per
+"""Multi-source throughput: the bit-sliced batch kernel (64 sources per
 launch) against the single-source kernel run once per source, on the same
 sources of a BASELINE config (default cfg5, 1,024 sources).
 
@@ -40,17 +40,17 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     pq = P.PreparedQuery(g, n)
     # batch kernel
-    pq.launch_batch(srcs[:32], -1.0, stream.cuda_stream)
+    pq.launch_batch(srcs[:64], -1.0, stream.cuda_stream)
     pq.wait_batch()
     te_b = 0
     ms_b = 0.0
     rows_b = 0
     levels = []
     detail = None
-    for b0 in range(0, len(srcs), 32):
+    for b0 in range(0, len(srcs), 64):
         with torch.cuda.stream(stream):
             flush.fill_(1)
-        pq.launch_batch(srcs[b0:b0 + 32], -1.0, stream.cuda_stream)
+        pq.launch_batch(srcs[b0:b0 + 64], -1.0, stream.cuda_stream)
         st = pq.wait_batch()
         te_b += int(st.te)
         rows_b += int(st.rows)
@@ -75,8 +75,8 @@ def main():
         st = pq.wait()
         ms_s += float(st.device_ms)
     # batch TE over the same prefix (whole batches)
-    for b0 in range(0, args.single, 32):
-        pq.launch_batch(srcs[b0:b0 + 32], -1.0, stream.cuda_stream)
+    for b0 in range(0, args.single, 64):
+        pq.launch_batch(srcs[b0:b0 + 64], -1.0, stream.cuda_stream)
         te_s_prefix_batch += int(pq.wait_batch().te)
     pq.close()
     out = {
