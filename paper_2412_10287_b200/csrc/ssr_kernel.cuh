@@ -1059,17 +1059,21 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
     uint32_t* cfound = scratch + 96 * PV;
     const uint32_t fmask_all = (1u << PV) - 1u;
     const int sh = PV * (lane % LPW);  // this lane's bit offset in its word
+    // task indices fit 32 bits (targets x blocks <= 256 x 2^28): 32-bit
+    // division and modulo (64-bit ones are ~100-instruction subroutines)
+    const uint32_t nblk32 = (uint32_t)nblk, G32 = (uint32_t)G;
     for (;;) {
-        long long task = 0;
+        uint32_t task = 0;
         if (lane == 0) {
-            const long long i = (long long)atomicAdd(s_task, 1u);
-            task = i * G + (blockIdx.x + i) % G;
-            if (task >= nown && nown < ntask) task = nown + (long long)atomicAdd(steal, 1ull);
+            const uint32_t i = atomicAdd(s_task, 1u);
+            task = i * G32 + (blockIdx.x + i) % G32;
+            if (task >= (uint32_t)nown && nown < ntask) task = (uint32_t)nown + (uint32_t)atomicAdd(steal, 1ull);
         }
         task = __shfl_sync(FULL, task, 0);
-        if (task >= ntask) break;
-        const int q2 = s_ptarget[task / nblk];
-        const long long word0 = pw0 + (task % nblk) * PV;
+        if ((long long)task >= ntask) break;
+        const uint32_t tq = task / nblk32;
+        const int q2 = s_ptarget[tq];
+        const long long word0 = pw0 + (long long)(task - tq * nblk32) * PV;
         const long long myword = word0 + lane / LPW;
         const long long v0 = word0 * 32 + (long long)PV * lane;
         // the first pulled in-slot (warp-uniform): its row pointers do not
