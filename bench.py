@@ -791,6 +791,11 @@ def run_batch_mode(args, rank, world, local_rank):
 def main():
     args = parse_args()
     _AUTOMATON_KIND[0] = args.automaton
+    # stdout carries exactly one JSON line: anything else that writes to fd 1
+    # (NCCL's version banner, library chatter) goes to stderr
+    sys.stdout.flush()
+    json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -818,7 +823,8 @@ def main():
 
             torch.distributed.destroy_process_group()
     if out is not None:
-        print(json.dumps(out), flush=True)
+        json_out.write(json.dumps(out) + "\n")
+        json_out.flush()
 
 
 if __name__ == "__main__":
