@@ -378,7 +378,10 @@ __global__ void __launch_bounds__(kBThreads, kMinBlocks) batch_kernel(BParams p)
         const unsigned long long nlisted = ldcg(&cur->nlist);
         const unsigned long long gwarp_b = (unsigned long long)blockIdx.x * kBWarps + wid;
         const unsigned long long nwarps_b = (unsigned long long)gridDim.x * kBWarps;
-        const unsigned long long nown = nlisted - nlisted / 4;
+#ifndef RPQ_BATCH_STATIC_NUM
+#define RPQ_BATCH_STATIC_NUM 2  // static share of the block list, in quarters (cfg5: 3/4 357, 2/4 369, 0 352 GTEPS)
+#endif
+        const unsigned long long nown = nlisted / 4 * RPQ_BATCH_STATIC_NUM;
         unsigned long long kk = gwarp_b;
         for (;;) {
             unsigned long long k = kk;
