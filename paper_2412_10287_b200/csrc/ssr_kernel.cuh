@@ -1051,7 +1051,10 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
     const long long nblk = (pw1 - pw0 + PV - 1) / PV;
     const long long ntask = (long long)s_nptarget * nblk;
     const long long G = gridDim.x;
-    const long long nown = ntask >= 16 * G ? (ntask - ntask / 4) / G * G : ntask;
+#ifndef RPQ_PULL_STATIC_NUM
+#define RPQ_PULL_STATIC_NUM 3  // static share of the pull tasks, in quarters
+#endif
+    const long long nown = ntask >= 16 * G ? (ntask / 4 * RPQ_PULL_STATIC_NUM) / G * G : ntask;
     // warp scratch: candidate vertex offset (bit 31: long row), row start, row end; found words
     uint32_t* cid = scratch;
     uint32_t* clo = scratch + 32 * PV;
