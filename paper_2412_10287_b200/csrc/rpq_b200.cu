@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstddef>
 #include <cmath>
 #include <cstdio>
@@ -146,6 +147,8 @@ struct rpq_query {
     bool run_out_list = false;         // ... which may receive a (word index, word) pair list
     bool out_direct = false;           // the last run wrote its answer there, not to h_reach_bits
     bool reach_stale = true;           // d_reach (uint8) not yet expanded from d_reach_bits
+    unsigned int run_seq = 0;          // number of the last rpq_query_run (Ctl::done_seq)
+    bool last_zc = false;              // the last run's kernel writes the results prefix to the host
 
     cudaGraphExec_t graphs[4] = {nullptr, nullptr, nullptr, nullptr};  // captured run per variant
     cudaGraphExec_t graph = nullptr;  // the current variant's (one of graphs[])
@@ -1148,6 +1151,8 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     // the caller's pinned answer buffer (grid kernel only; the single-CTA
     // kernel's answer goes through h_reach_bits)
     ra.out_bits = use_small(q) ? nullptr : q->run_out_bits;
+    ra.run_seq = ++q->run_seq;
+    q->last_zc = q->zero_copy && !use_small(q);
     ra.out_list = ra.out_bits && q->run_out_list ? 1 : 0;
     q->out_direct = ra.out_bits != nullptr;
     q->reach_stale = true;
@@ -1171,16 +1176,39 @@ int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) 
     return RPQ_OK;
 }
 
-int rpq_query_wait(rpq_query* q, rpq_stats* stats) {
+namespace {
+// Wait for the last run.  poll: the grid kernel's last CTA writes the results
+// prefix to pinned host memory and then the run's number; spinning on that
+// flag returns as soon as it lands (a stream synchronize wakes up several us
+// later).  device_ms is then the kernel's own time (globaltimer), without the
+// launch.  Anything unusual (no flag, an error) falls back to the stream.
+int wait_impl(rpq_query* q, rpq_stats* stats, bool poll) {
     if (!q) return fail(RPQ_EINVAL, "null query");
     if (!q->ran) return fail(RPQ_EINVAL, "query has not been run");
-    CUDA_TRY(cudaStreamSynchronize(q->last_stream));
+    bool polled = false;
+#ifndef RPQ_CHECKED
+    if (poll && q->last_zc) {
+        volatile const unsigned* flag = &q->h_ctl->done_seq;
+        for (unsigned long long i = 1;; ++i) {
+            if (*flag == q->run_seq) {
+                polled = true;
+                break;
+            }
+            if ((i & 255) == 0 && cudaStreamQuery(q->last_stream) != cudaErrorNotReady) break;
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+    }
+#endif
+    if (!polled) CUDA_TRY(cudaStreamSynchronize(q->last_stream));
     q->inflight = false;
-    q->bar_next = q->h_ctl->bar;
+    q->bar_next = polled ? 0u : q->h_ctl->bar;
     if (const int crc = check_sites()) return crc;
     const Ctl& c = *q->h_ctl;
     float ms = 0.f;
-    CUDA_TRY(cudaEventElapsedTime(&ms, q->ev0, q->ev1));
+    if (polled)
+        ms = (float)((double)(c.t_end - c.t0) * 1e-6);
+    else
+        CUDA_TRY(cudaEventElapsedTime(&ms, q->ev0, q->ev1));
     if (stats) {
         std::memset(stats, 0, sizeof(*stats));
         stats->status = c.status;
@@ -1217,6 +1245,9 @@ int rpq_query_wait(rpq_query* q, rpq_stats* stats) {
     if (c.status != 0) return fail(RPQ_ECUDA, "kernel status " + std::to_string(c.status));
     return RPQ_OK;
 }
+}  // namespace
+
+int rpq_query_wait(rpq_query* q, rpq_stats* stats) { return wait_impl(q, stats, false); }
 
 namespace {
 int query_eval(rpq_query* q, int32_t source, double timeout_s, int32_t direction, int32_t count_te, double alpha,
@@ -1237,7 +1268,7 @@ int query_eval(rpq_query* q, int32_t source, double timeout_s, int32_t direction
     q->run_out_bits = nullptr;
     q->run_out_list = false;
     if (rc != RPQ_OK) return rc;
-    rc = rpq_query_wait(q, stats);
+    rc = wait_impl(q, stats, true);
     if (rc != RPQ_OK) return rc;
     if (reach_words && words && !direct) std::memcpy(reach_words, q->h_reach_bits, (size_t)words * 4);
     return RPQ_OK;

@@ -101,6 +101,9 @@ struct Ctl {
     unsigned long long segments;
     unsigned long long pairs;
     unsigned long long reach_count;
+    unsigned long long t_end;      // globaltimer when the last CTA left (device time = t_end - t0)
+    unsigned int done_seq;         // RunArgs::run_seq, written to the host copy last (completion flag)
+    unsigned int pad_done;
     unsigned long long ans_words;  // nonzero answer words (out_list runs)
     int ans_list;                  // 1: the host answer buffer holds (word index, word) pairs
     int pad_ans;
@@ -136,6 +139,7 @@ struct RunArgs {
     unsigned int flags;            // RF_* push-path variants (tuning)
     long long own_w0, own_w1;      // step mode: owned word range of a partitioned rank (empty: all)
     float defer_alpha;             // emit at discovery unless mf_L * dmax * this > m_u (0: always emit)
+    unsigned int run_seq;          // this run's number: the host polls Ctl::done_seq for it
     int out_list;                  // out_bits may receive a (word index, word) pair list when that is
                                    // smaller than the bitmap (sparse answers; Ctl::ans_list says which)
     uint32_t* out_bits;            // the caller's pinned answer bitmap (rpq_host_alloc), written by the
@@ -1944,18 +1948,32 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
         __shared__ int s_last;
         __syncthreads();
         if (threadIdx.x == 0) {
-            __threadfence();  // this CTA's counter updates are visible first
+            // this CTA's counter updates (and, with host outputs, its answer
+            // words over PCIe) are visible before it counts itself out
+            if (p.host_ctl) __threadfence_system();
+            else __threadfence();
             s_last = atomicAdd(&ctl->exits, 1u) == gridDim.x - 1;
         }
         __syncthreads();
         if (s_last) {
             __threadfence();
             if (p.host_ctl) {
+                if (threadIdx.x == 0) ctl->t_end = globaltimer();
+                __syncthreads();
                 constexpr int nw = (int)(offsetof(Ctl, qc) / 4);
+                constexpr int iseq = (int)(offsetof(Ctl, done_seq) / 4);
                 const unsigned* src = reinterpret_cast<const unsigned*>(ctl);
                 unsigned* dst = reinterpret_cast<unsigned*>(p.host_ctl);
-                for (int i = threadIdx.x; i < nw; i += blockDim.x) dst[i] = i == 0 ? 0u : __ldcg(src + i);
+                for (int i = threadIdx.x; i < nw; i += blockDim.x)
+                    if (i != iseq) dst[i] = i == 0 ? 0u : __ldcg(src + i);
                 __threadfence_system();
+                __syncthreads();
+                // the completion flag goes last: a host that sees it sees the
+                // results prefix and every CTA's answer words
+                if (threadIdx.x == 0) {
+                    *(volatile unsigned*)(dst + iseq) = s_run.run_seq;
+                    __threadfence_system();
+                }
             }
             if (threadIdx.x == 0) {
                 if (step_mode && p.step_acc) {
