@@ -1861,6 +1861,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
     // ---- epilogue: answer = OR of P's rows at final states (engine.py:112-114)
     // The answer bitmap only: the uint8[|V|] vector is expanded from it on
     // demand (reach_bytes_kernel, rpq_query_copy_reach), not on every run.
+    stamp(p, L, 1);  // diagnostics: epilogue entered (row L's slots 1-4 are free: the loop broke before its stamps)
+    int wrote_host = 0;  // this thread stored answer words to pinned host memory (over PCIe)
     if (s_view.status == 0) {
         unsigned long long cnt = 0, nzw = 0;
         uint32_t* const hb = s_run.out_bits ? s_run.out_bits : p.host_bits;
@@ -1871,8 +1873,12 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
             cnt += __popc(acc);
             nzw += acc != 0u;
             p.reach_bits[i] = acc;
-            if (hb && !maybe_list) hb[i] = acc;  // coalesced: 128 B per warp over PCIe
+            if (hb && !maybe_list) {
+                hb[i] = acc;  // coalesced: 128 B per warp over PCIe
+                wrote_host = 1;
+            }
         }
+        stamp(p, L, 2);  // diagnostics: projection written
         if (maybe_list) {
             // the host gets whichever is smaller: the bitmap, or the nonzero
             // words as (index, word) pairs -- an empty answer moves no bytes
@@ -1895,13 +1901,18 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
                         if (RPQ_CHECK(2 * pos + 1 < (unsigned long long)Wn, RPQ_F_SSR)) {
                             hb[2 * pos] = (uint32_t)i;
                             hb[2 * pos + 1] = acc;
+                            wrote_host = 1;
                         }
                     }
                 }
             } else {
-                for (long long i = gtid; i < Wn; i += gthreads) hb[i] = __ldcg(p.reach_bits + i);
+                for (long long i = gtid; i < Wn; i += gthreads) {
+                    hb[i] = __ldcg(p.reach_bits + i);
+                    wrote_host = 1;
+                }
             }
             if (cta0 && threadIdx.x == 0) ctl->ans_list = list ? 1 : 0;
+            stamp(p, L, 3);  // diagnostics: answer transport written
         }
         // exact push-model TE = sum over (q, v) in P of q's group out-degrees x targets
         unsigned long long te = 0;
@@ -1944,37 +1955,44 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
     // zero-copy results: it copies the results prefix (everything before the
     // working counters) to pinned host memory; step mode: a failed step
     // latches its status for rpq_query_step_end.
+    stamp(p, L, 4);  // diagnostics: epilogue done
     {
         __shared__ int s_last;
-        __syncthreads();
+        // A system-scope fence costs ~20 us when all 148 CTAs issue one at
+        // once (they serialize): only CTAs whose threads stored answer words
+        // over PCIe pay it; everyone else orders its counters at GPU scope.
+        wrote_host = __syncthreads_or(wrote_host);
         if (threadIdx.x == 0) {
-            // this CTA's counter updates (and, with host outputs, its answer
-            // words over PCIe) are visible before it counts itself out
-            if (p.host_ctl) __threadfence_system();
+            // this CTA's counter updates (and its answer words over PCIe, if
+            // it wrote any) are visible before it counts itself out
+            if (wrote_host) __threadfence_system();
             else __threadfence();
             s_last = atomicAdd(&ctl->exits, 1u) == gridDim.x - 1;
         }
         __syncthreads();
         if (s_last) {
             __threadfence();
-            if (p.host_ctl) {
-                if (threadIdx.x == 0) ctl->t_end = globaltimer();
-                __syncthreads();
+            if (p.host_ctl && wid == 0) {
+                // one warp copies the results prefix (~3 KB): one system fence
+                // per writing warp, so as few writing warps as possible
+                if (lane == 0) ctl->t_end = globaltimer();
+                __syncwarp();
                 constexpr int nw = (int)(offsetof(Ctl, qc) / 4);
                 constexpr int iseq = (int)(offsetof(Ctl, done_seq) / 4);
                 const unsigned* src = reinterpret_cast<const unsigned*>(ctl);
                 unsigned* dst = reinterpret_cast<unsigned*>(p.host_ctl);
-                for (int i = threadIdx.x; i < nw; i += blockDim.x)
+                for (int i = lane; i < nw; i += 32)
                     if (i != iseq) dst[i] = i == 0 ? 0u : __ldcg(src + i);
                 __threadfence_system();
-                __syncthreads();
+                __syncwarp();
                 // the completion flag goes last: a host that sees it sees the
                 // results prefix and every CTA's answer words
-                if (threadIdx.x == 0) {
+                if (lane == 0) {
                     *(volatile unsigned*)(dst + iseq) = s_run.run_seq;
                     __threadfence_system();
                 }
             }
+            __syncthreads();
             if (threadIdx.x == 0) {
                 if (step_mode && p.step_acc) {
                     const int st = ldcg(&ctl->status);

@@ -62,9 +62,21 @@ def main():
     d = st.to_dict()
     print(json.dumps({"config": args.config, "device_ms": st.device_ms, "iterations": st.iterations,
                       "dirs": d["level_dir"], "new": d["level_new"]}))
-    for L in range(min(st.iterations, args.levels)):
+    for L in range(args.levels):
         t = tr[L]
         if not t[:, 0].any():
+            # the row of the deciding level that ended the loop: its decision
+            # stamps (5-7) and the epilogue's (1: entered, 2: projection
+            # written, 3: answer transport written, 4: done)
+            ep = {"L": L, "epilogue": True,
+                  "dec_enter": (tr[L, :, 6].min(), tr[L, :, 6].max()),
+                  "dec_end": (tr[L, :, 7].min(), tr[L, :, 7].max())}
+            for k, name in ((1, "entered"), (2, "projected"), (3, "transport"), (4, "done")):
+                col = t[:, k]
+                if col.any():
+                    ep[name] = (col.min(), col.max())
+            print(json.dumps({k: [round(float(x), 2) for x in v] if isinstance(v, tuple) else v
+                              for k, v in ep.items()}))
             break
         plan = t[:, 1]
         row = {"L": L, "dir": d["level_dir"][L] if L < len(d["level_dir"]) else None,
