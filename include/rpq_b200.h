@@ -175,7 +175,8 @@ RPQ_API int rpq_query_set_options(rpq_query* q, int32_t direction, int32_t count
 #define RPQ_TUNE_FLAGS 3  /* push variants: bit 0 (default on) claim without probing P first,
                              bit 1 prefetch candidate targets' row pointers into L2,
                              bit 2 never cut a push level's emission off at m_u / alpha,
-                             bit 3 defer prediction with the all-rows mean degree (round 1) */
+                             bit 3 defer prediction with the all-rows mean degree (round 1),
+                             bit 4 push without the shared-memory claim cache */
 #define RPQ_TUNE_SMALL 4  /* 1 (default): state spaces of <= 12,288 x 32 pairs run on one CTA
                              with shared-memory bitmaps; 0: always the grid kernel */
 #define RPQ_TUNE_DEFER 5  /* push level L does not emit F_{L+1}'s queue at discovery when

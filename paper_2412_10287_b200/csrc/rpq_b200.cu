@@ -1090,8 +1090,8 @@ int rpq_query_set_tuning(rpq_query* q, int32_t key, double value) {
             q->allow_small = (int)value;
             return RPQ_OK;
         case RPQ_TUNE_FLAGS:
-            if (value < 0 || value > 15) return fail(RPQ_EINVAL, "flags must be in [0, 15]");
-            q->run_flags = (unsigned)value & 7u;
+            if (value < 0 || value > 31) return fail(RPQ_EINVAL, "flags must be in [0, 31]");
+            q->run_flags = (unsigned)value & 23u;  // (bit 3 is host-side: use_dmax_ne)
             if (q->use_dmax_ne != !((unsigned)value & 8u)) {
                 if (q->inflight) {  // let a run in flight finish with the old graph
                     CUDA_TRY(cudaStreamSynchronize(q->last_stream));

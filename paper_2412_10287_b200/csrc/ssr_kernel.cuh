@@ -80,6 +80,7 @@ struct QCnt {
     unsigned int expire;                    // 1 + level whose deadline check failed
     unsigned long long emit_progress;       // edges emitted so far this level (reported in chunks)
     unsigned int emit_cut;                  // 1: the emission crossed View::cut_edges
+    unsigned int big;                       // 1: some bundle of this queue holds more than 32 edges
 };
 
 struct FCnt {
@@ -149,6 +150,7 @@ struct RunArgs {
 constexpr unsigned RF_NO_PROBE = 1u;     // claim with atomicOr without reading P first
 constexpr unsigned RF_PREFETCH = 2u;     // (retired: -30% on cfg4 in round 1; the bit is ignored)
 constexpr unsigned RF_NO_CUT = 4u;       // never cut a push level's emission off (View::cut_edges)
+constexpr unsigned RF_NO_CACHE = 16u;    // push without the shared-memory claim cache
 
 struct Params {
     const RunArgs* run;
@@ -324,6 +326,7 @@ struct View {
     int status;
     int iterations;
     unsigned long long nfront;  // |F_L|
+    int qbig;                   // F_L's queue holds bundles of more than 32 edges (QCnt::big)
     float cut_edges;            // push level: once the emitted successor edges exceed this, the next
                                 // level is pull whatever the rest emits (Beamer's m_f * alpha > m_u with
                                 // this level's m_u, which only shrinks): stop emitting (0: never)
@@ -403,6 +406,12 @@ struct Out {
     uint2* bun;
     unsigned long long* s_resv;  // this CTA's shard fill: (segments << 32) | bundles
     uint32_t bsz;                // edges per emitted bundle (32..kBundle)
+    float gain;                  // > 0: a pass emitting T edges of a group cuts them into bundles of
+                                 // clamp(T * gain, bsz, kBundle) edges.  A level with few bundles emits
+                                 // small ones so that its successor spreads over every warp -- but when
+                                 // every pass emits thousands of edges (R-MAT grows 200x a level early
+                                 // on) the successor has bundles to spare, and 32-edge ones cost it four
+                                 // descriptors where one would do
 };
 
 // Warp-cooperative emission of the row segments of (state q, vertex w) pairs
@@ -439,7 +448,8 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
             huge |= deg[k] > kSegLenMax;
         }
         if (!__any_sync(FULL, huge)) {
-            uint32_t excl[kFastGroups], T[kFastGroups], nb[kFastGroups], nseg[kFastGroups];
+            uint32_t excl[kFastGroups], T[kFastGroups], nb[kFastGroups], nseg[kFastGroups], bszk[kFastGroups];
+            bool anybig = false;
             int rank[kFastGroups];
             uint32_t NS = 0, NB = 0, TT = 0;
 #pragma unroll
@@ -451,13 +461,18 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
                     const uint32_t incl = warp_incl_scan(deg[k], lane);
                     excl[k] = incl - deg[k];
                     T[k] = __shfl_sync(FULL, incl, 31);
-                    nb[k] = (T[k] + o.bsz - 1) / o.bsz;
+                    bszk[k] = o.bsz;
+                    if (o.gain > 0.0f)
+                        bszk[k] = min((uint32_t)kBundle, max(o.bsz, (uint32_t)((float)T[k] * o.gain)));
+                    anybig |= bszk[k] > 32u && T[k] > 32u;
+                    nb[k] = (T[k] + bszk[k] - 1) / bszk[k];
                     NS += nseg[k];
                     NB += nb[k];
                     TT += T[k];
                 } else {
                     rank[k] = 0;
                     nseg[k] = nb[k] = T[k] = excl[k] = 0;
+                    bszk[k] = o.bsz;
                 }
             }
             if (NB == 0) return 0;
@@ -473,6 +488,7 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
                 if (lane == 0) atomicExch(&o.qc->overflow, 1u);
                 return 0;
             }
+            if (anybig && o.bsz <= 32u && lane == 0) o.qc->big = 1u;  // (same value from every writer)
             sbase = __shfl_sync(FULL, sbase, 0);
             bbase = __shfl_sync(FULL, bbase, 0);
 #pragma unroll
@@ -482,8 +498,8 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
                 bool need_seg = false;
                 for (uint32_t kb0 = 0; kb0 < nb[k]; kb0 += 32) {
                     const uint32_t kb = kb0 + lane;
-                    const uint32_t pos = kb * o.bsz;
-                    const uint32_t cnt = kb < nb[k] ? min(o.bsz, T[k] - pos) : 1u;
+                    const uint32_t pos = kb * bszk[k];
+                    const uint32_t cnt = kb < nb[k] ? min(bszk[k], T[k] - pos) : 1u;
                     const uint32_t first = min(pos, T[k] - 1);
                     const int j = warp_upper_lane(excl[k], first);
                     const int jl = warp_upper_lane(excl[k], min(pos + cnt - 1, T[k] - 1));
@@ -758,6 +774,7 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
     const unsigned int overflow = ldcg(&qc->overflow);
     const unsigned int expire = ldcg(&qc->expire);
     const unsigned int emit_cut = ldcg(&qc->emit_cut);
+    const unsigned int qbig = ldcg(&qc->big);
     const int abort = ldcg(&ctl->abort);
     unsigned long long nbun, nseg;
     queue_scan(p, qc, lane, s_bpre, &nbun, &nseg);
@@ -875,6 +892,7 @@ __device__ void decide_level(const Params& p, const Smem& S, unsigned e, int L, 
         v->status = status;
         v->iterations = iterations;
         v->nfront = nnew;
+        v->qbig = (int)qbig;
         v->defer = next == DIR_PUSH && defer;
         v->cut_edges = next == DIR_PUSH && !defer ? cut : 0.0f;
         if (blockIdx.x == 0) {  // results and statistics
@@ -936,6 +954,7 @@ __device__ void decide_plan(const Params& p, unsigned e, int L, int lane, View* 
     if (lane == 0) {
         v->done = done;
         v->plan = 0;
+        v->qbig = 0;  // (a plan epoch emits with gain 0)
         v->status = status;
         v->iterations = iterations;
         if (blockIdx.x == 0) {
@@ -961,6 +980,7 @@ __device__ __forceinline__ void reset_qc(Ctl* ctl, int k, int tid) {
         qc->expire = 0;
         qc->emit_progress = 0;
         qc->emit_cut = 0;
+        qc->big = 0;
     }
 }
 
@@ -1069,14 +1089,17 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
     // task indices fit 32 bits (targets x blocks <= 256 x 2^28): 32-bit
     // division and modulo (64-bit ones are ~100-instruction subroutines)
     const uint32_t nblk32 = (uint32_t)nblk, G32 = (uint32_t)G;
-    for (;;) {
-        uint32_t task = 0;
+    auto grab = [&]() -> uint32_t {
+        uint32_t t = 0;
         if (lane == 0) {
             const uint32_t i = atomicAdd(s_task, 1u);
-            task = i * G32 + (blockIdx.x + i) % G32;
-            if (task >= (uint32_t)nown && nown < ntask) task = (uint32_t)nown + (uint32_t)atomicAdd(steal, 1ull);
+            t = i * G32 + (blockIdx.x + i) % G32;
+            if (t >= (uint32_t)nown && nown < ntask) t = (uint32_t)nown + (uint32_t)atomicAdd(steal, 1ull);
         }
-        task = __shfl_sync(FULL, task, 0);
+        return __shfl_sync(FULL, t, 0);
+    };
+    for (;;) {
+        const uint32_t task = grab();
         if ((long long)task >= ntask) break;
         const uint32_t tq = task / nblk32;
         const int q2 = s_ptarget[tq];
@@ -1214,6 +1237,218 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
     }
 }
 
+#ifndef RPQ_NO_PULL_QUEUE
+// Pull with a per-warp candidate queue that outlives the task.  pull_tasks
+// gathers each task's candidates on their own: about 36 per 256-vertex task on
+// cfg3, so every second gather round runs on a handful of lanes, and a row
+// whose first probe misses keeps its lane (and the warp) in a serial
+// continuation.  Here candidates (vertex, row cursor, row end) of consecutive
+// tasks accumulate in shared memory and are probed in uniform rounds of 64
+// (two per lane, all column loads in flight, then all frontier probes); a miss
+// with edges left goes back on the queue with its cursor advanced, so no lane
+// waits on another's row.  A discovery is a RED into P and F (the warp dealt
+// the vertex is the only one looking at the pair this level, and each pair
+// is queued at most once per in-slot, so no claim is needed).
+constexpr int kPQCap = 256;             // entries (3 words each) per warp: kWarpScratchWords
+constexpr int kPQRound = 64;
+constexpr uint32_t kPQRequeueMax = 16;  // a miss with more edges left than this is scanned by the whole warp
+
+template <int PV>
+__device__ __forceinline__ void pull_tasks_q(const Params& p, const Smem& S, const uint32_t* fcur, uint32_t* fnext,
+                                             long long pw0, long long pw1, int lane, unsigned* s_task,
+                                             int s_nptarget, const int* s_ptarget, const unsigned int* s_front,
+                                             unsigned int* s_state, unsigned int& nnew,
+                                             unsigned long long* steal, uint32_t* scratch, int first) {
+    constexpr int LPW = 32 / PV;  // lanes per word
+    const long long nblk = (pw1 - pw0 + PV - 1) / PV;
+    const long long ntask = (long long)s_nptarget * nblk;
+    const long long G = gridDim.x;
+    const long long nown = ntask >= 16 * G ? (ntask / 4 * RPQ_PULL_STATIC_NUM) / G * G : ntask;
+    uint32_t* ev = scratch;
+    uint32_t* elo = scratch + kPQCap;
+    uint32_t* ehi = scratch + 2 * kPQCap;
+    uint32_t* cfound = scratch + 3 * kPQCap;
+    const uint32_t fmask_all = (1u << PV) - 1u;
+    const int sh = PV * (lane % LPW);
+    const uint32_t nblk32 = (uint32_t)nblk, G32 = (uint32_t)G;
+    int n = 0;            // queued entries (warp-uniform)
+    int qk = -1;          // the in-transition the queued entries belong to
+    int qq2 = 0;          // its target state
+    bool qmulti = false;  // the target has several active in-slots: hits are also recorded in cfound
+    long long qv0 = 0;    // (qmulti) first vertex of the task the entries belong to
+    auto grab = [&]() -> uint32_t {
+        uint32_t t = 0;
+        if (lane == 0) {
+            const uint32_t i = atomicAdd(s_task, 1u);
+            t = i * G32 + (blockIdx.x + i) % G32;
+            if (t >= (uint32_t)nown && nown < ntask) t = (uint32_t)nown + (uint32_t)atomicAdd(steal, 1ull);
+        }
+        return __shfl_sync(FULL, t, 0);
+    };
+    // one round: the last <= 64 entries of the queue
+    auto round = [&]() {
+        const int np = min(n, kPQRound);
+        const int base = n - np;
+        const Slot ps = S.slots[p.nslots + S.islot[qk]];
+        const uint32_t* frow = fcur + (long long)S.isrc[qk] * p.W;
+        uint32_t v[2], l[2], h[2];
+        bool act[2], hit[2];
+        int c0[2], c1[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int idx = base + 32 * u + lane;
+            act[u] = idx < n;
+            v[u] = act[u] ? ev[idx] : 0u;
+            l[u] = act[u] ? elo[idx] : 0u;
+            h[u] = act[u] ? ehi[idx] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            c0[u] = act[u] ? ld_stream_i32(ps.col + l[u], S.pf) : -1;
+            c1[u] = act[u] && first > 1 && l[u] + 1 < h[u] ? ld_stream_i32(ps.col + l[u] + 1, S.pf) : -1;
+            if (act[u] && !RPQ_CHECK(c0[u] >= 0 && c0[u] < p.nv && c1[u] < p.nv && l[u] < h[u] &&
+                                         h[u] <= p.slot_nnz[S.islot[qk] % p.nslots] && v[u] < (uint32_t)p.nv,
+                                     RPQ_F_SSR)) {
+                c0[u] = c1[u] = -1;
+                h[u] = l[u];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            hit[u] = (c0[u] >= 0 && ((ld_bits(frow + (c0[u] >> 5), S.pl) >> (c0[u] & 31)) & 1u)) ||
+                     (c1[u] >= 0 && ((ld_bits(frow + (c1[u] >> 5), S.pl) >> (c1[u] & 31)) & 1u));
+        n = base;
+        __syncwarp();  // every lane holds its entries: the tail may be rewritten
+        unsigned nhit = 0;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const uint32_t e = l[u] + (uint32_t)first;
+            const bool miss = act[u] && !hit[u] && e < h[u];
+            const bool lng = miss && h[u] - e > kPQRequeueMax;
+            const unsigned mreq = __ballot_sync(FULL, miss && !lng);
+            if (miss && !lng) {
+                const int pos = n + __popc(mreq & lanemask_lt());
+                ev[pos] = v[u];
+                elo[pos] = e;
+                ehi[pos] = h[u];
+            }
+            n += __popc(mreq);
+            // long rows: the whole warp scans each, 128 edges per step, early exit
+            unsigned longs = __ballot_sync(FULL, lng);
+            while (longs) {
+                const int sl = __ffs(longs) - 1;
+                longs &= longs - 1;
+                const uint32_t rlo = __shfl_sync(FULL, e, sl), rhi = __shfl_sync(FULL, h[u], sl);
+                bool found_row = false;
+                for (uint32_t ed = rlo; ed < rhi; ed += 128) {
+                    int uu[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        uu[c] = ed + 32 * c + lane < rhi ? ld_stream_i32(ps.col + ed + 32 * c + lane, S.pf) : -1;
+                    bool hh = false;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (uu[c] >= 0 && RPQ_CHECK(uu[c] < p.nv, RPQ_F_SSR))
+                            hh |= (ld_bits(frow + (uu[c] >> 5), S.pl) >> (uu[c] & 31)) & 1u;
+                    if (__ballot_sync(FULL, hh)) {
+                        found_row = true;
+                        break;
+                    }
+                }
+                if (found_row && lane == sl) hit[u] = true;
+            }
+            if (act[u] && hit[u]) {
+                const long long off = (long long)qq2 * p.W + (v[u] >> 5);
+                const uint32_t bit = 1u << (v[u] & 31u);
+                red_or_bits(p.visited + off, bit, S.pl);
+                red_or_bits(fnext + off, bit, S.pl);
+                if (qmulti) {
+                    const uint32_t rel = v[u] - (uint32_t)qv0;
+                    if (rel < 32u * PV) atomicOr(&cfound[rel >> 5], 1u << (rel & 31u));
+                }
+                ++nnew;
+            }
+            nhit += __popc(__ballot_sync(FULL, act[u] && hit[u]));
+        }
+        if (lane == 0 && nhit) atomicAdd(&s_state[qq2], nhit);
+        __syncwarp();
+    };
+    for (;;) {
+        const uint32_t task = grab();
+        if ((long long)task >= ntask) break;
+        const uint32_t tq = task / nblk32;
+        const int q2 = s_ptarget[tq];
+        const long long word0 = pw0 + (long long)(task - tq * nblk32) * PV;
+        const long long myword = word0 + lane / LPW;
+        const long long v0 = word0 * 32 + (long long)PV * lane;
+        int k0 = -1, nact = 0;
+        for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k)
+            if (s_front[S.isrc[k]]) {
+                if (k0 < 0) k0 = k;
+                ++nact;
+            }
+        const bool multi = nact > 1;
+        uint32_t r[PV + 1];
+        const uint32_t pw = myword < pw1 ? ld_bits(p.visited + (long long)q2 * p.W + myword, S.pl) : 0xFFFFFFFFu;
+        load_rows<PV>(S.slots[p.nslots + S.islot[max(k0, 0)]].rowptr, v0, p.nv, lane, true, S.pf, r);
+        uint32_t need = ~(pw >> sh) & fmask_all;
+        if (v0 >= p.nv) need = 0;
+        else if (v0 + PV > p.nv) need &= (1u << (p.nv - v0)) - 1u;
+        if (myword >= pw1) need = 0;
+        uint32_t found = 0;
+        if (__ballot_sync(FULL, need != 0) == 0) continue;
+        for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k) {
+            if (!s_front[S.isrc[k]]) continue;
+            const uint32_t look = need & ~found;
+            if (__ballot_sync(FULL, look != 0) == 0) break;
+            if (k != k0) load_rows<PV>(S.slots[p.nslots + S.islot[k]].rowptr, v0, p.nv, lane, look != 0, S.pf, r);
+            uint32_t cm = 0;
+#pragma unroll
+            for (int j = 0; j < PV; ++j)
+                if (((look >> j) & 1u) && r[j + 1] > r[j]) cm |= 1u << j;
+            const uint32_t cnt = __popc(cm);
+            const uint32_t incl = warp_incl_scan(cnt, lane);
+            const int nadd = (int)__shfl_sync(FULL, incl, 31);
+            if (nadd == 0) continue;
+            // entries of another in-transition (or, for a target with several
+            // in-slots, of another task) are finished first; so is whatever
+            // does not leave room for this task's candidates
+            if (n > 0 && (qk != k || multi)) {
+                while (n > 0) round();
+            }
+            while (n + nadd > kPQCap) round();
+            qk = k;
+            qq2 = q2;
+            qmulti = multi;
+            qv0 = word0 * 32;
+            if (multi) {
+                if (lane < PV) cfound[lane] = 0u;
+                __syncwarp();
+            }
+            int pos = n + (int)(incl - cnt);
+#pragma unroll
+            for (int j = 0; j < PV; ++j)
+                if ((cm >> j) & 1u) {
+                    ev[pos] = (uint32_t)(v0 + j);
+                    elo[pos] = r[j];
+                    ehi[pos] = r[j + 1];
+                    ++pos;
+                }
+            n += nadd;
+            __syncwarp();
+            if (multi) {
+                while (n > 0) round();
+                found |= (cfound[lane / LPW] >> sh) & fmask_all;
+                __syncwarp();
+            } else {
+                while (n >= kPQRound) round();
+            }
+        }
+    }
+    while (n > 0) round();
+}
+#endif  // RPQ_NO_PULL_QUEUE
+
 // Diagnostic stamp k of level L for this CTA (thread 0): 0 level start (after
 // the decision), 1 plan epoch done, 2 last warp done with the expansion,
 // 3 past the barrier, 4 counters flushed.
@@ -1233,6 +1468,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
     __shared__ unsigned int s_state[kMaxStates];     // this CTA's discoveries per state
     __shared__ int s_ptarget[kMaxStates];            // pull target states of this level
     __shared__ int s_nptarget;
+    __shared__ int s_pmulti;  // some pull target of this level has several active in-slots
     __shared__ View s_view;
     __shared__ unsigned long long s_resv;
     __shared__ unsigned s_task;  // next task index of this CTA in the current epoch
@@ -1262,6 +1498,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
         s_run = *p.run;
         s_view.mf = 0.0f;
         s_view.defer = 0;
+        s_view.qbig = 0;
         s_view.cut_edges = 0.0f;
         float d = 0.0f;
         for (int sl = 0; sl < p.nslots; ++sl) d = fmaxf(d, (float)p.slot_nnz[sl]);
@@ -1336,7 +1573,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
     // share of their bundles -- a hub source's row (millions of edges) is not
     // emitted by one warp.  All seed bundles are inline (each lies in one row).
     if (!step_mode) {
-        const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, 32u};
+        const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, 32u, 0.0f};
         if (cta0) reset_qc(ctl, (e + 2) % 3, threadIdx.x);
         unsigned long long nnew = 0, nedge = 0;
         const int src = S.run->source;
@@ -1456,6 +1693,33 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
     }
     __syncthreads();
 
+#ifndef RPQ_NO_CLAIM_CACHE
+    // Claim cache (push): a direct-mapped table in shared memory of P words
+    // this CTA has seen, {word index + 1, bits known set}.  An edge whose
+    // target bit is known set makes no claim.  On skewed graphs most edges of
+    // a push level end on a few hub vertices whose P words share a handful of
+    // 128-byte lines: their claims queue at one L2 slice and every warp waits
+    // in that queue (cfg3: 2% of a level's claims hit one line).  Entries only
+    // hold bits that are set in P (P only grows), so a stale or lost entry
+    // costs a claim, never an answer.  One 64-bit shared access per entry:
+    // tag and bits cannot tear.  The table lives in the part of each warp's
+    // scratch the emission stage does not use (pull epochs overwrite it: it is
+    // cleared before the next push epoch).
+    constexpr int kPcPerWarp = 128;
+    constexpr int kPcEntries = (kWarps >= 32 ? 32 : 16) * kPcPerWarp;  // a power of two
+    constexpr int kPcShift = kWarps >= 32 ? 20 : 21;                    // 32 - log2(kPcEntries)
+    static_assert(2 * kStageCap + 2 * kPcPerWarp <= kWarpScratchWords, "claim cache fits beside the stage");
+    static_assert((2 * kStageCap) % 2 == 0 && kWarpScratchWords % 2 == 0, "8-byte aligned entries");
+    auto pc_entry_at = [&](int i) -> unsigned long long* {
+        return reinterpret_cast<unsigned long long*>(s_stage + (i >> 7) * kWarpScratchWords + 2 * kStageCap +
+                                                     2 * (i & (kPcPerWarp - 1)));
+    };
+    auto pc_entry = [&](uint32_t tag) -> unsigned long long* {
+        return pc_entry_at((int)((tag * 0x9E3779B1u) >> kPcShift));
+    };
+    const bool use_pc = (long long)p.nstates * p.W < 0xFFFFFFF0ll && !(s_run.flags & RF_NO_CACHE);
+    bool pc_dirty = true;
+#endif
     // ---- level loop -----------------------------------------------------------
     int L = 0;
     int dir = DIR_PUSH;
@@ -1471,13 +1735,46 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
             // ---- plan epoch: emit F_L's row segments from its bitmap (after pull)
             const uint32_t bsz = s_view.nfront < (unsigned long long)nwarps * 8 ? 32u : (uint32_t)kBundle;
             qbsz = bsz;
-            const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, bsz};
+            const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, bsz, 0.0f};
             if (cta0) reset_qc(ctl, (e + 2) % 3, threadIdx.x);
             unsigned long long nedge = 0;
+#ifndef RPQ_PLAN_STATIC
+            // chunks of 32 words (1,024 vertices) of every state with a
+            // frontier and out-groups, dealt like pull tasks: a rotation over
+            // the CTAs, the last quarter from a grid-wide counter (a fixed
+            // stride left the warps on F's dense stretches far behind)
+            if (threadIdx.x == 0) {
+                int n = 0;
+                for (int q = 0; q < p.nstates; ++q)
+                    if (s_front[q] && S.gbeg[q + 1] != S.gbeg[q]) s_ptarget[n++] = q;
+                s_nptarget = n;
+                s_task = 0;
+            }
+            __syncthreads();
+            const uint32_t nchunk = (uint32_t)((Wn + 31) >> 5), G32 = gridDim.x;
+            const uint32_t nptask = (uint32_t)s_nptarget * nchunk;
+            const uint32_t npown = nptask >= 16 * G32 ? (nptask / 4 * 3) / G32 * G32 : nptask;
+            unsigned long long* plan_steal = &ctl->steal[e % 3][0];
+            for (;;) {
+                uint32_t t = 0;
+                if (lane == 0) {
+                    const uint32_t i = atomicAdd(&s_task, 1u);
+                    t = i * G32 + (blockIdx.x + i) % G32;
+                    if (t >= npown && npown < nptask) t = npown + (uint32_t)atomicAdd(plan_steal, 1ull);
+                }
+                t = __shfl_sync(FULL, t, 0);
+                if (t >= nptask) break;
+                const uint32_t tq = t / nchunk;
+                const int q = s_ptarget[tq];
+                const uint32_t* row = fcur + (long long)q * p.W;
+                {
+                    const long long w0 = (long long)(t - tq * nchunk) * 32;
+#else
             for (int q = 0; q < p.nstates; ++q) {
                 if (!s_front[q] || S.gbeg[q + 1] == S.gbeg[q]) continue;
                 const uint32_t* row = fcur + (long long)q * p.W;
                 for (long long w0 = gwarp * 32; w0 < Wn; w0 += nwarps * 32) {
+#endif
                     // a word per lane; their set bits dealt 32 per round to the
                     // lanes (prefix over popcounts), so every stage_add is full
                     const long long wi = w0 + lane;
@@ -1517,7 +1814,15 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
         const uint32_t bsz = (dir == DIR_PUSH ? s_bpre[kShards + 1] : s_view.nfront / 8) <
                                      (unsigned long long)nwarps * 4
                                  ? 32u : (uint32_t)kBundle;
-        const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, bsz};
+#ifdef RPQ_NO_BUNDLE_GAIN
+        const float gain = 0.0f;
+#else
+        // bundles the successor level wants: 4 per warp; this level has
+        // s_bpre[kShards + 1] bundles, each the source of about one pass
+        const float gain = dir == DIR_PUSH && bsz < (uint32_t)kBundle
+                               ? (float)s_bpre[kShards + 1] / (float)(nwarps * 4) : 0.0f;
+#endif
+        const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, bsz, gain};
         const uint32_t qbsz_next = bsz;
         if (threadIdx.x == 0) {
             s_task = 0;
@@ -1534,6 +1839,13 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
             uint4* z4 = reinterpret_cast<uint4*>(p.fb[(L + 2) % 3]);
             for (long long i = gtid; i < nbits4; i += gthreads) z4[i] = make_uint4(0, 0, 0, 0);
         }
+#ifndef RPQ_NO_CLAIM_CACHE
+        if (dir == DIR_PUSH && pc_dirty) {  // (CTA-uniform)
+            for (int i = threadIdx.x; i < kPcEntries; i += NT) *pc_entry_at(i) = 0ull;
+            pc_dirty = false;
+        }
+        if (dir == DIR_PULL) pc_dirty = true;  // the pull scratch overwrites the cache
+#endif
         __syncthreads();  // s_task
         unsigned int nnew = 0;  // this thread's discoveries this level (< 2^32)
         unsigned long long nedge = 0;
@@ -1591,7 +1903,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
             // small emits 32-edge bundles; R-MAT grows 200x a level early on):
             // a warp takes 4 bundles per grab, one per edge slot of its lanes,
             // instead of leaving three slots of every lane idle.
-            const bool merge4 = qbsz <= 32u && nb >= (unsigned long long)nwarps * 8;
+            const bool merge4 = qbsz <= 32u && !s_view.qbig && nb >= (unsigned long long)nwarps * 8;
             uint2 bd_next = make_uint2(0u, kHoleY);
             unsigned long long bi_next = merge4 ? 0ull : grab(&bd_next);
             for (;;) {
@@ -1740,9 +2052,17 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
                                     old[u] = ld_bits(p.visited + (long long)q2[u] * p.W + (w[u] >> 5), S.pl);
                                 else
                                     old[u] = 0u;
+#ifndef RPQ_NO_CLAIM_CACHE
+                                if (use_pc) {
+                                    const uint32_t tag = (uint32_t)((long long)q2[u] * p.W + (w[u] >> 5)) + 1u;
+                                    const unsigned long long ent = *pc_entry(tag);
+                                    if ((uint32_t)(ent >> 32) == tag) old[u] |= (uint32_t)ent;
+                                }
+#endif
                             }
                         }
                     }
+                    unsigned claimed = 0;  // edge slots whose claim went to global memory
 #pragma unroll
                     for (int u = 0; u < kEdgesPerLane; ++u) {
                         const uint32_t bit = 1u << (w[u] & 31);
@@ -1751,17 +2071,53 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
                         if (q2[u] >= 0 && !(old[u] & bit)) {
                             const long long off2 = (long long)q2[u] * p.W + (w[u] >> 5);
                             old[u] = or_bits(p.visited + off2, bit, S.pl);
+                            claimed |= 1u << u;
+#ifdef RPQ_PUSH_SERIAL_CLAIMS
                             if (!(old[u] & bit)) red_or_bits(fnext + off2, bit, S.pl);
+#endif
                         } else {
                             old[u] = 0xFFFFFFFFu;
                         }
                     }
+#ifndef RPQ_PUSH_SERIAL_CLAIMS
+                    // the F bits in a second pass: the claims above are volatile
+                    // asm statements, kept in program order, so a RED between
+                    // two of them would wait for the first claim's return before
+                    // the second is issued (four serial L2 round trips per bundle)
+#pragma unroll
+                    for (int u = 0; u < kEdgesPerLane; ++u) {
+                        const uint32_t bit = 1u << (w[u] & 31);
+                        if (q2[u] >= 0 && !(old[u] & bit))
+                            red_or_bits(fnext + (long long)q2[u] * p.W + (w[u] >> 5), bit, S.pl);
+#ifndef RPQ_NO_CLAIM_CACHE
+                        // what the claim returned is now known of the whole word
+                        if (use_pc && ((claimed >> u) & 1u)) {
+                            const uint32_t tag = (uint32_t)((long long)q2[u] * p.W + (w[u] >> 5)) + 1u;
+                            *pc_entry(tag) = ((unsigned long long)tag << 32) | (old[u] | bit);
+                        }
+#endif
+                    }
+#endif
+                    (void)claimed;
                     const bool emit_now = emit_inline && !*(volatile int*)&s_cut;
 #pragma unroll
                     for (int u = 0; u < kEdgesPerLane; ++u) {
                         const bool fresh = q2[u] >= 0 && !(old[u] & (1u << (w[u] & 31)));
                         nnew += fresh ? 1 : 0;
+#ifdef RPQ_PUSH_SERIAL_CLAIMS
                         if (fresh) atomicAdd(&s_state[q2[u]], 1u);
+#else
+                        // per-state counts: one shared atomic per distinct state among the
+                        // fresh lanes (32 lanes on one shared address serialize)
+                        unsigned fmk = __ballot_sync(FULL, fresh);
+                        while (fmk) {
+                            const int ld = __ffs(fmk) - 1;
+                            const int qL = __shfl_sync(FULL, q2[u], ld);
+                            const unsigned grp = __ballot_sync(FULL, fresh && q2[u] == qL);
+                            if (lane == ld) atomicAdd(&s_state[qL], (unsigned)__popc(grp));
+                            fmk &= ~grp;
+                        }
+#endif
                         if (emit_now) stage_put(stage, fresh, q2[u], w[u], lane);
                     }
                     if (emit_now) {
@@ -1797,12 +2153,15 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
                 nedge += frontier_edges(p, S, fcur, gtid, gthreads, Wn);
             if (threadIdx.x == 0) {
                 int n = 0;
+                int multi = 0;
                 for (int q2 = 0; q2 < p.nstates; ++q2) {
-                    bool any = false;
-                    for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k) any |= s_front[S.isrc[k]] != 0;
+                    int any = 0;
+                    for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k) any += s_front[S.isrc[k]] != 0;
                     if (any) s_ptarget[n++] = q2;
+                    multi |= any > 1;
                 }
                 s_nptarget = n;
+                s_pmulti = multi;
             }
             __syncthreads();
             // targets: the owned word range (vertex-partitioned step), else all
@@ -1818,6 +2177,16 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
             const int first = one_inline ? 1 : kPullInline;
 #ifndef RPQ_PV8_WORDS_PER_WARP
 #define RPQ_PV8_WORDS_PER_WARP 16  // cfg5 (131k words, 4,736 warps): 8 words per task, pull levels 180 -> 123 us
+#endif
+#ifndef RPQ_NO_PULL_QUEUE
+            // the queued variant when every target of the level has one active
+            // in-slot (cfg3: pull levels 149 -> 143 and 110 -> 96 us); targets
+            // with several need each slot's answers before the next and drain
+            // the queue per slot, which costs more than it saves (cfg5: +10%)
+            if (pw1 - pw0 >= (long long)nwarps * RPQ_PV8_WORDS_PER_WARP && !s_pmulti)
+                pull_tasks_q<8>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front, s_state,
+                                nnew, pull_steal, scratch, first);
+            else
 #endif
             if (pw1 - pw0 >= (long long)nwarps * RPQ_PV8_WORDS_PER_WARP)  // large: 8 words per task
                 pull_tasks<8>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front, s_state,
