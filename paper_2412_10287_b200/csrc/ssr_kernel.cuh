@@ -1007,6 +1007,25 @@ __device__ unsigned long long frontier_edges(const Params& p, const Smem& S, con
     return te;
 }
 
+// n / d and n % d for 32-bit n with inv = floor(2^32 / d) (d >= 2; d == 1: inv
+// = 2^32 - 1): the estimate __umulhi(n, inv) is the quotient or one less.  A
+// hardware-free 32-bit division is ~20 instructions, and the task dealing of
+// the pull and plan epochs does two per task.
+struct FastDiv {
+    uint32_t d, inv;
+    __device__ __forceinline__ explicit FastDiv(uint32_t d_) : d(d_), inv(d_ > 1 ? (uint32_t)(0x100000000ull / d_) : 0xFFFFFFFFu) {}
+    __device__ __forceinline__ uint32_t div(uint32_t n, uint32_t* rem) const {
+        uint32_t q = __umulhi(n, inv);
+        uint32_t r = n - q * d;
+        if (r >= d) {
+            r -= d;
+            ++q;
+        }
+        *rem = r;
+        return q;
+    }
+};
+
 // Pull tasks of one level: every (target state, PV words of vertices) with an
 // active source state.  PV words per lane-task: more vertices in flight per
 // warp on large graphs, more tasks (balance) on small ones.
@@ -1032,6 +1051,28 @@ constexpr int kPullCont = 8;
 template <int PV>
 __device__ __forceinline__ void load_rows(const uint32_t* rp, long long v0, int nv, int lane, bool active,
                                           uint64_t pol, uint32_t (&r)[PV + 1]) {
+    // the common case, a block wholly inside the vertex range with every lane
+    // looking (warp-uniform): two 128-bit loads, the next lane's first pointer
+    // by shuffle, lane 31's from memory -- none of the end-of-range fix-ups
+    // below (they were 36 instructions per task)
+    if (v0 - (long long)PV * lane + 32 * PV <= nv && __all_sync(FULL, active)) {
+        const uint4* r4 = reinterpret_cast<const uint4*>(rp + v0);
+        uint32_t last = 0;
+        if (lane == 31) last = ld_stream_u32(rp + v0 + PV, pol);
+#pragma unroll
+        for (int c = 0; c < PV / 4; ++c) {
+            uint4 x;
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                         : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(r4 + c), "l"(pol));
+            r[4 * c] = x.x;
+            r[4 * c + 1] = x.y;
+            r[4 * c + 2] = x.z;
+            r[4 * c + 3] = x.w;
+        }
+        const uint32_t nx = __shfl_down_sync(FULL, r[0], 1);
+        r[PV] = lane < 31 ? nx : last;
+        return;
+    }
     // lanes with nothing to look at skip their loads (a later in-slot of a
     // target, once most of the lane's vertices are found or visited)
     if (active) {
@@ -1088,12 +1129,15 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
     const int sh = PV * (lane % LPW);  // this lane's bit offset in its word
     // task indices fit 32 bits (targets x blocks <= 256 x 2^28): 32-bit
     // division and modulo (64-bit ones are ~100-instruction subroutines)
-    const uint32_t nblk32 = (uint32_t)nblk, G32 = (uint32_t)G;
+    const uint32_t G32 = (uint32_t)G;
+    const FastDiv dblk((uint32_t)nblk), dG(G32);
     auto grab = [&]() -> uint32_t {
         uint32_t t = 0;
         if (lane == 0) {
             const uint32_t i = atomicAdd(s_task, 1u);
-            t = i * G32 + (blockIdx.x + i) % G32;
+            uint32_t rot;
+            dG.div(blockIdx.x + i, &rot);
+            t = i * G32 + rot;
             if (t >= (uint32_t)nown && nown < ntask) t = (uint32_t)nown + (uint32_t)atomicAdd(steal, 1ull);
         }
         return __shfl_sync(FULL, t, 0);
@@ -1101,9 +1145,10 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
     for (;;) {
         const uint32_t task = grab();
         if ((long long)task >= ntask) break;
-        const uint32_t tq = task / nblk32;
+        uint32_t blk;
+        const uint32_t tq = dblk.div(task, &blk);
         const int q2 = s_ptarget[tq];
-        const long long word0 = pw0 + (long long)(task - tq * nblk32) * PV;
+        const long long word0 = pw0 + (long long)blk * PV;
         const long long myword = word0 + lane / LPW;
         const long long v0 = word0 * 32 + (long long)PV * lane;
         // the first pulled in-slot (warp-uniform): its row pointers do not
@@ -1238,25 +1283,27 @@ __device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const
 }
 
 #ifndef RPQ_NO_PULL_QUEUE
-// Pull with a per-warp candidate queue that outlives the task.  pull_tasks
-// gathers each task's candidates on their own: about 36 per 256-vertex task on
-// cfg3, so every second gather round runs on a handful of lanes, and a row
-// whose first probe misses keeps its lane (and the warp) in a serial
-// continuation.  Here candidates (vertex, row cursor, row end) of consecutive
-// tasks accumulate in shared memory and are probed in uniform rounds of 64
-// (two per lane, all column loads in flight, then all frontier probes); a miss
-// with edges left goes back on the queue with its cursor advanced, so no lane
-// waits on another's row.  A discovery is a RED into P and F (the warp dealt
-// the vertex is the only one looking at the pair this level, and each pair
-// is queued at most once per in-slot, so no claim is needed).
-constexpr int kPQCap = 256;             // entries (3 words each) per warp: kWarpScratchWords
+// Pull with a per-warp candidate queue that outlives the task, for levels
+// whose targets each have ONE active in-slot (s_pk[tq]: that in-transition).
+// pull_tasks gathers each task's candidates on their own: about 36 per
+// 256-vertex task on cfg3, so every second gather round runs on a handful of
+// lanes, and a row whose first probe misses keeps its lane (and the warp) in
+// a serial continuation.  Here candidates {vertex, row cursor, row end} of
+// consecutive tasks accumulate in shared memory (one 16-byte entry each) and
+// are probed in uniform rounds of 64 (two per lane, all column loads in
+// flight, then all frontier probes); a miss with edges left goes back on the
+// queue with its cursor advanced, so no lane waits on another's row.  A
+// discovery is a RED into P and F: the warp dealt the vertex is the only one
+// looking at the pair this level, and each pair is queued once.
+constexpr int kPQCap = 192;             // entries (16 bytes each) per warp: kWarpScratchWords
 constexpr int kPQRound = 64;
 constexpr uint32_t kPQRequeueMax = 16;  // a miss with more edges left than this is scanned by the whole warp
+static_assert(4 * kPQCap <= kWarpScratchWords, "the candidate queue fits the warp scratch");
 
 template <int PV>
 __device__ __forceinline__ void pull_tasks_q(const Params& p, const Smem& S, const uint32_t* fcur, uint32_t* fnext,
                                              long long pw0, long long pw1, int lane, unsigned* s_task,
-                                             int s_nptarget, const int* s_ptarget, const unsigned int* s_front,
+                                             int s_nptarget, const int* s_ptarget, const int* s_pk,
                                              unsigned int* s_state, unsigned int& nnew,
                                              unsigned long long* steal, uint32_t* scratch, int first) {
     constexpr int LPW = 32 / PV;  // lanes per word
@@ -1264,53 +1311,38 @@ __device__ __forceinline__ void pull_tasks_q(const Params& p, const Smem& S, con
     const long long ntask = (long long)s_nptarget * nblk;
     const long long G = gridDim.x;
     const long long nown = ntask >= 16 * G ? (ntask / 4 * RPQ_PULL_STATIC_NUM) / G * G : ntask;
-    uint32_t* ev = scratch;
-    uint32_t* elo = scratch + kPQCap;
-    uint32_t* ehi = scratch + 2 * kPQCap;
-    uint32_t* cfound = scratch + 3 * kPQCap;
+    uint4* ent = reinterpret_cast<uint4*>(scratch);  // (the warp scratch is 16-byte aligned)
     const uint32_t fmask_all = (1u << PV) - 1u;
     const int sh = PV * (lane % LPW);
-    const uint32_t nblk32 = (uint32_t)nblk, G32 = (uint32_t)G;
-    int n = 0;            // queued entries (warp-uniform)
-    int qk = -1;          // the in-transition the queued entries belong to
-    int qq2 = 0;          // its target state
-    bool qmulti = false;  // the target has several active in-slots: hits are also recorded in cfound
-    long long qv0 = 0;    // (qmulti) first vertex of the task the entries belong to
-    auto grab = [&]() -> uint32_t {
-        uint32_t t = 0;
-        if (lane == 0) {
-            const uint32_t i = atomicAdd(s_task, 1u);
-            t = i * G32 + (blockIdx.x + i) % G32;
-            if (t >= (uint32_t)nown && nown < ntask) t = (uint32_t)nown + (uint32_t)atomicAdd(steal, 1ull);
-        }
-        return __shfl_sync(FULL, t, 0);
-    };
+    const FastDiv dblk((uint32_t)nblk), dG((uint32_t)G);
+    const uint32_t G32 = (uint32_t)G;
+    int n = 0;    // queued entries (warp-uniform)
+    int qk = -1;  // the in-transition the queued entries belong to
+    int qq2 = 0;  // its target state
     // one round: the last <= 64 entries of the queue
     auto round = [&]() {
         const int np = min(n, kPQRound);
         const int base = n - np;
         const Slot ps = S.slots[p.nslots + S.islot[qk]];
         const uint32_t* frow = fcur + (long long)S.isrc[qk] * p.W;
-        uint32_t v[2], l[2], h[2];
+        uint4 en[2];
         bool act[2], hit[2];
         int c0[2], c1[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const int idx = base + 32 * u + lane;
             act[u] = idx < n;
-            v[u] = act[u] ? ev[idx] : 0u;
-            l[u] = act[u] ? elo[idx] : 0u;
-            h[u] = act[u] ? ehi[idx] : 0u;
+            en[u] = act[u] ? ent[idx] : make_uint4(0u, 0u, 0u, 0u);  // {vertex, cursor, row end, -}
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            c0[u] = act[u] ? ld_stream_i32(ps.col + l[u], S.pf) : -1;
-            c1[u] = act[u] && first > 1 && l[u] + 1 < h[u] ? ld_stream_i32(ps.col + l[u] + 1, S.pf) : -1;
-            if (act[u] && !RPQ_CHECK(c0[u] >= 0 && c0[u] < p.nv && c1[u] < p.nv && l[u] < h[u] &&
-                                         h[u] <= p.slot_nnz[S.islot[qk] % p.nslots] && v[u] < (uint32_t)p.nv,
+            c0[u] = act[u] ? ld_stream_i32(ps.col + en[u].y, S.pf) : -1;
+            c1[u] = act[u] && first > 1 && en[u].y + 1 < en[u].z ? ld_stream_i32(ps.col + en[u].y + 1, S.pf) : -1;
+            if (act[u] && !RPQ_CHECK(c0[u] >= 0 && c0[u] < p.nv && c1[u] < p.nv && en[u].y < en[u].z &&
+                                         en[u].z <= p.slot_nnz[S.islot[qk] % p.nslots] && en[u].x < (uint32_t)p.nv,
                                      RPQ_F_SSR)) {
                 c0[u] = c1[u] = -1;
-                h[u] = l[u];
+                en[u].z = en[u].y;
             }
         }
 #pragma unroll
@@ -1322,23 +1354,18 @@ __device__ __forceinline__ void pull_tasks_q(const Params& p, const Smem& S, con
         unsigned nhit = 0;
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            const uint32_t e = l[u] + (uint32_t)first;
-            const bool miss = act[u] && !hit[u] && e < h[u];
-            const bool lng = miss && h[u] - e > kPQRequeueMax;
+            const uint32_t e = en[u].y + (uint32_t)first;
+            const bool miss = act[u] && !hit[u] && e < en[u].z;
+            const bool lng = miss && en[u].z - e > kPQRequeueMax;
             const unsigned mreq = __ballot_sync(FULL, miss && !lng);
-            if (miss && !lng) {
-                const int pos = n + __popc(mreq & lanemask_lt());
-                ev[pos] = v[u];
-                elo[pos] = e;
-                ehi[pos] = h[u];
-            }
+            if (miss && !lng) ent[n + __popc(mreq & lanemask_lt())] = make_uint4(en[u].x, e, en[u].z, 0u);
             n += __popc(mreq);
             // long rows: the whole warp scans each, 128 edges per step, early exit
             unsigned longs = __ballot_sync(FULL, lng);
             while (longs) {
                 const int sl = __ffs(longs) - 1;
                 longs &= longs - 1;
-                const uint32_t rlo = __shfl_sync(FULL, e, sl), rhi = __shfl_sync(FULL, h[u], sl);
+                const uint32_t rlo = __shfl_sync(FULL, e, sl), rhi = __shfl_sync(FULL, en[u].z, sl);
                 bool found_row = false;
                 for (uint32_t ed = rlo; ed < rhi; ed += 128) {
                     int uu[4];
@@ -1358,14 +1385,10 @@ __device__ __forceinline__ void pull_tasks_q(const Params& p, const Smem& S, con
                 if (found_row && lane == sl) hit[u] = true;
             }
             if (act[u] && hit[u]) {
-                const long long off = (long long)qq2 * p.W + (v[u] >> 5);
-                const uint32_t bit = 1u << (v[u] & 31u);
+                const long long off = (long long)qq2 * p.W + (en[u].x >> 5);
+                const uint32_t bit = 1u << (en[u].x & 31u);
                 red_or_bits(p.visited + off, bit, S.pl);
                 red_or_bits(fnext + off, bit, S.pl);
-                if (qmulti) {
-                    const uint32_t rel = v[u] - (uint32_t)qv0;
-                    if (rel < 32u * PV) atomicOr(&cfound[rel >> 5], 1u << (rel & 31u));
-                }
                 ++nnew;
             }
             nhit += __popc(__ballot_sync(FULL, act[u] && hit[u]));
@@ -1374,76 +1397,71 @@ __device__ __forceinline__ void pull_tasks_q(const Params& p, const Smem& S, con
         __syncwarp();
     };
     for (;;) {
-        const uint32_t task = grab();
+        uint32_t task = 0;
+        if (lane == 0) {
+            const uint32_t i = atomicAdd(s_task, 1u);
+            uint32_t rot;
+            dG.div(blockIdx.x + i, &rot);
+            task = i * G32 + rot;
+            if (task >= (uint32_t)nown && nown < ntask) task = (uint32_t)nown + (uint32_t)atomicAdd(steal, 1ull);
+        }
+        task = __shfl_sync(FULL, task, 0);
         if ((long long)task >= ntask) break;
-        const uint32_t tq = task / nblk32;
+        uint32_t blk;
+        const uint32_t tq = dblk.div(task, &blk);
         const int q2 = s_ptarget[tq];
-        const long long word0 = pw0 + (long long)(task - tq * nblk32) * PV;
+        const int k = s_pk[tq];
+        const long long word0 = pw0 + (long long)blk * PV;
         const long long myword = word0 + lane / LPW;
         const long long v0 = word0 * 32 + (long long)PV * lane;
-        int k0 = -1, nact = 0;
-        for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k)
-            if (s_front[S.isrc[k]]) {
-                if (k0 < 0) k0 = k;
-                ++nact;
-            }
-        const bool multi = nact > 1;
         uint32_t r[PV + 1];
         const uint32_t pw = myword < pw1 ? ld_bits(p.visited + (long long)q2 * p.W + myword, S.pl) : 0xFFFFFFFFu;
-        load_rows<PV>(S.slots[p.nslots + S.islot[max(k0, 0)]].rowptr, v0, p.nv, lane, true, S.pf, r);
+        load_rows<PV>(S.slots[p.nslots + S.islot[k]].rowptr, v0, p.nv, lane, true, S.pf, r);
         uint32_t need = ~(pw >> sh) & fmask_all;
-        if (v0 >= p.nv) need = 0;
-        else if (v0 + PV > p.nv) need &= (1u << (p.nv - v0)) - 1u;
-        if (myword >= pw1) need = 0;
-        uint32_t found = 0;
-        if (__ballot_sync(FULL, need != 0) == 0) continue;
-        for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k) {
-            if (!s_front[S.isrc[k]]) continue;
-            const uint32_t look = need & ~found;
-            if (__ballot_sync(FULL, look != 0) == 0) break;
-            if (k != k0) load_rows<PV>(S.slots[p.nslots + S.islot[k]].rowptr, v0, p.nv, lane, look != 0, S.pf, r);
-            uint32_t cm = 0;
-#pragma unroll
-            for (int j = 0; j < PV; ++j)
-                if (((look >> j) & 1u) && r[j + 1] > r[j]) cm |= 1u << j;
-            const uint32_t cnt = __popc(cm);
-            const uint32_t incl = warp_incl_scan(cnt, lane);
-            const int nadd = (int)__shfl_sync(FULL, incl, 31);
-            if (nadd == 0) continue;
-            // entries of another in-transition (or, for a target with several
-            // in-slots, of another task) are finished first; so is whatever
-            // does not leave room for this task's candidates
-            if (n > 0 && (qk != k || multi)) {
-                while (n > 0) round();
-            }
-            while (n + nadd > kPQCap) round();
-            qk = k;
-            qq2 = q2;
-            qmulti = multi;
-            qv0 = word0 * 32;
-            if (multi) {
-                if (lane < PV) cfound[lane] = 0u;
-                __syncwarp();
-            }
-            int pos = n + (int)(incl - cnt);
-#pragma unroll
-            for (int j = 0; j < PV; ++j)
-                if ((cm >> j) & 1u) {
-                    ev[pos] = (uint32_t)(v0 + j);
-                    elo[pos] = r[j];
-                    ehi[pos] = r[j + 1];
-                    ++pos;
-                }
-            n += nadd;
-            __syncwarp();
-            if (multi) {
-                while (n > 0) round();
-                found |= (cfound[lane / LPW] >> sh) & fmask_all;
-                __syncwarp();
-            } else {
-                while (n >= kPQRound) round();
-            }
+        if (word0 * 32 + 32 * PV > p.nv) {  // (warp-uniform: the last block of a row)
+            if (v0 >= p.nv) need = 0;
+            else if (v0 + PV > p.nv) need &= (1u << (p.nv - v0)) - 1u;
         }
+        if (myword >= pw1) need = 0;
+        // the unvisited vertices with in-edges in the slot
+        uint32_t cm = need;
+#pragma unroll
+        for (int j = 0; j < PV; ++j)
+            if (r[j + 1] == r[j]) cm &= ~(1u << j);
+        const uint32_t cnt = __popc(cm);
+        const uint32_t incl = warp_incl_scan(cnt, lane);
+        const int nadd = (int)__shfl_sync(FULL, incl, 31);
+        if (nadd == 0) continue;
+        // entries of another in-transition are finished first; so is whatever
+        // does not leave room for this task's candidates
+        if (qk != k)
+            while (n > 0) round();
+        while (n + nadd > kPQCap && n > 0) round();
+        qk = k;
+        qq2 = q2;
+        if (nadd > kPQCap) {
+            // (more candidates than the queue holds -- at most 32 * PV: in two halves)
+            for (int half = 0; half < 2; ++half) {
+                const uint32_t hm = half ? cm & ~((1u << (PV / 2)) - 1u) : cm & ((1u << (PV / 2)) - 1u);
+                const uint32_t hc = __popc(hm);
+                const uint32_t hi_ = warp_incl_scan(hc, lane);
+                int pos = (int)(hi_ - hc);
+#pragma unroll
+                for (int j = 0; j < PV; ++j)
+                    if ((hm >> j) & 1u) ent[pos++] = make_uint4((uint32_t)(v0 + j), r[j], r[j + 1], 0u);
+                n = (int)__shfl_sync(FULL, hi_, 31);
+                __syncwarp();
+                while (n > 0) round();
+            }
+            continue;
+        }
+        int pos = n + (int)(incl - cnt);
+#pragma unroll
+        for (int j = 0; j < PV; ++j)
+            if ((cm >> j) & 1u) ent[pos++] = make_uint4((uint32_t)(v0 + j), r[j], r[j + 1], 0u);
+        n += nadd;
+        __syncwarp();
+        while (n >= kPQRound) round();
     }
     while (n > 0) round();
 }
@@ -1469,6 +1487,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
     __shared__ int s_ptarget[kMaxStates];            // pull target states of this level
     __shared__ int s_nptarget;
     __shared__ int s_pmulti;  // some pull target of this level has several active in-slots
+    __shared__ int s_pk[kMaxStates];  // first active in-transition of each pull target
     __shared__ View s_view;
     __shared__ unsigned long long s_resv;
     __shared__ unsigned s_task;  // next task index of this CTA in the current epoch
@@ -1755,20 +1774,24 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
             const uint32_t nptask = (uint32_t)s_nptarget * nchunk;
             const uint32_t npown = nptask >= 16 * G32 ? (nptask / 4 * 3) / G32 * G32 : nptask;
             unsigned long long* plan_steal = &ctl->steal[e % 3][0];
+            const FastDiv dchunk(nchunk), dG(G32);
             for (;;) {
                 uint32_t t = 0;
                 if (lane == 0) {
                     const uint32_t i = atomicAdd(&s_task, 1u);
-                    t = i * G32 + (blockIdx.x + i) % G32;
+                    uint32_t rot;
+                    dG.div(blockIdx.x + i, &rot);
+                    t = i * G32 + rot;
                     if (t >= npown && npown < nptask) t = npown + (uint32_t)atomicAdd(plan_steal, 1ull);
                 }
                 t = __shfl_sync(FULL, t, 0);
                 if (t >= nptask) break;
-                const uint32_t tq = t / nchunk;
+                uint32_t chunk;
+                const uint32_t tq = dchunk.div(t, &chunk);
                 const int q = s_ptarget[tq];
                 const uint32_t* row = fcur + (long long)q * p.W;
                 {
-                    const long long w0 = (long long)(t - tq * nchunk) * 32;
+                    const long long w0 = (long long)chunk * 32;
 #else
             for (int q = 0; q < p.nstates; ++q) {
                 if (!s_front[q] || S.gbeg[q + 1] == S.gbeg[q]) continue;
@@ -2155,9 +2178,13 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
                 int n = 0;
                 int multi = 0;
                 for (int q2 = 0; q2 < p.nstates; ++q2) {
-                    int any = 0;
-                    for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k) any += s_front[S.isrc[k]] != 0;
-                    if (any) s_ptarget[n++] = q2;
+                    int any = 0, kf = 0;
+                    for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k)
+                        if (s_front[S.isrc[k]] != 0 && any++ == 0) kf = k;
+                    if (any) {
+                        s_pk[n] = kf;  // the first (for the queued pull: the only) active in-transition
+                        s_ptarget[n++] = q2;
+                    }
                     multi |= any > 1;
                 }
                 s_nptarget = n;
@@ -2184,7 +2211,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
             // with several need each slot's answers before the next and drain
             // the queue per slot, which costs more than it saves (cfg5: +10%)
             if (pw1 - pw0 >= (long long)nwarps * RPQ_PV8_WORDS_PER_WARP && !s_pmulti)
-                pull_tasks_q<8>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front, s_state,
+                pull_tasks_q<8>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_pk, s_state,
                                 nnew, pull_steal, scratch, first);
             else
 #endif
