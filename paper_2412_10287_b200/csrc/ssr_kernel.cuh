@@ -46,7 +46,10 @@ constexpr int kMaxStates = 256;
 constexpr int kMaxGroups = 256;      // group id is 8 bits in a segment
 constexpr int kMaxSlots = 128;
 constexpr uint32_t kSegLenMax = (1u << 24) - 1;
-constexpr int kFastGroups = 4;       // emission: groups per state handled in one pass
+#ifndef RPQ_FAST_GROUPS
+#define RPQ_FAST_GROUPS 2
+#endif
+constexpr int kFastGroups = RPQ_FAST_GROUPS;       // emission: groups per state handled in one pass
 // bundle = uint2 {x, y}; y bit 31 = inline, bits 0..6 = edges - 1,
 //   inline  : x = column offset of the first edge, y bits 7..14 = group
 //   indirect: x = index of the first segment, y bits 7..30 = offset into it
@@ -448,8 +451,12 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
             huge |= deg[k] > kSegLenMax;
         }
         if (!__any_sync(FULL, huge)) {
-            uint32_t excl[kFastGroups], T[kFastGroups], nb[kFastGroups], nseg[kFastGroups], bszk[kFastGroups];
+            uint32_t excl[kFastGroups], T[kFastGroups], nb[kFastGroups], nseg[kFastGroups];
             bool anybig = false;
+            // bundle size of a group's T edges (recomputed where needed: no register array)
+            auto bsz_of = [&](uint32_t Tk) -> uint32_t {
+                return o.gain > 0.0f ? min((uint32_t)kBundle, max(o.bsz, (uint32_t)((float)Tk * o.gain))) : o.bsz;
+            };
             int rank[kFastGroups];
             uint32_t NS = 0, NB = 0, TT = 0;
 #pragma unroll
@@ -461,18 +468,15 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
                     const uint32_t incl = warp_incl_scan(deg[k], lane);
                     excl[k] = incl - deg[k];
                     T[k] = __shfl_sync(FULL, incl, 31);
-                    bszk[k] = o.bsz;
-                    if (o.gain > 0.0f)
-                        bszk[k] = min((uint32_t)kBundle, max(o.bsz, (uint32_t)((float)T[k] * o.gain)));
-                    anybig |= bszk[k] > 32u && T[k] > 32u;
-                    nb[k] = (T[k] + bszk[k] - 1) / bszk[k];
+                    const uint32_t bk = bsz_of(T[k]);
+                    anybig |= bk > 32u && T[k] > 32u;
+                    nb[k] = (T[k] + bk - 1) / bk;
                     NS += nseg[k];
                     NB += nb[k];
                     TT += T[k];
                 } else {
                     rank[k] = 0;
                     nseg[k] = nb[k] = T[k] = excl[k] = 0;
-                    bszk[k] = o.bsz;
                 }
             }
             if (NB == 0) return 0;
@@ -498,8 +502,9 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
                 bool need_seg = false;
                 for (uint32_t kb0 = 0; kb0 < nb[k]; kb0 += 32) {
                     const uint32_t kb = kb0 + lane;
-                    const uint32_t pos = kb * bszk[k];
-                    const uint32_t cnt = kb < nb[k] ? min(bszk[k], T[k] - pos) : 1u;
+                    const uint32_t bk = bsz_of(T[k]);
+                    const uint32_t pos = kb * bk;
+                    const uint32_t cnt = kb < nb[k] ? min(bk, T[k] - pos) : 1u;
                     const uint32_t first = min(pos, T[k] - 1);
                     const int j = warp_upper_lane(excl[k], first);
                     const int jl = warp_upper_lane(excl[k], min(pos + cnt - 1, T[k] - 1));
