@@ -95,6 +95,7 @@ struct LabelDev {
     uint32_t* rowptr[2] = {nullptr, nullptr};
     int32_t* col[2] = {nullptr, nullptr};
     int64_t nnz[2] = {0, 0};
+    uint32_t* ne[2] = {nullptr, nullptr};  // non-empty-row bitmaps (Slot::ne), built on first pull use
 };
 
 struct rpq_graph {
@@ -127,6 +128,8 @@ struct rpq_query {
     size_t in_bytes = 0, off_slots = 0, off_tables = 0;
     unsigned int bar_next = 0;      // barrier counter value the next run starts from
     unsigned long long* d_slot_nnz = nullptr;
+    std::vector<const uint32_t*> ne_tab;   // per slot: non-empty-row bitmap of the transpose (Params::ne_tab)
+    const uint32_t** d_ne_tab = nullptr;
     float dmax_ne = 0.0f;  // the densest slot's mean degree over non-empty rows
     int use_dmax_ne = 1;   // RPQ_TUNE_FLAGS bit 3 clears it (the round-1 all-rows mean)
 
@@ -249,8 +252,10 @@ void free_label(LabelDev& L) {
     for (int d = 0; d < 2; ++d) {
         if (L.rowptr[d]) cudaFree(L.rowptr[d]);
         if (L.col[d]) cudaFree(L.col[d]);
+        if (L.ne[d]) cudaFree(L.ne[d]);
         L.rowptr[d] = nullptr;
         L.col[d] = nullptr;
+        L.ne[d] = nullptr;
     }
     L.resident = false;
 }
@@ -438,6 +443,7 @@ void free_query_buffers(rpq_query* q) {
     if (q->d_in) cudaFree(q->d_in);
     if (q->h_in) cudaFreeHost(q->h_in);
     if (q->d_slot_nnz) cudaFree(q->d_slot_nnz);
+    if (q->d_ne_tab) cudaFree(q->d_ne_tab);
     if (q->d_visited) cudaFree(q->d_visited);
     for (int f = 0; f < 3; ++f)
         if (q->d_fb[f]) cudaFree(q->d_fb[f]);
@@ -714,6 +720,28 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
         const uint32_t* rowptr[2];
         const int32_t* col[2];
         int64_t nnz[2];
+        LabelDev* ne_of;     // the label whose direction ne_dir is the transpose (its non-empty-row
+        int ne_dir;          // bitmap is built after the query's own buffers are allocated)
+    };
+    // words per bitmap row, as the query's bitmaps are laid out (a multiple of 4)
+    const long long ne_words = (((long long)g->nv + 31) / 32 + 3) / 4 * 4;
+    auto ensure_ne = [&](LabelDev& L, int d) -> const uint32_t* {
+        if (L.ne[d] || !L.rowptr[d]) return L.ne[d];
+        if (cudaMalloc(&L.ne[d], (size_t)ne_words * sizeof(uint32_t)) != cudaSuccess) {
+            L.ne[d] = nullptr;  // (the kernel falls back to reading row pointers)
+            cudaGetLastError();
+            return nullptr;
+        }
+        nonempty_bitmap_kernel<<<4 * g->sm_count, 256>>>(L.rowptr[d], g->nv, L.ne[d], ne_words);
+        // (query streams do not synchronize with the default stream: finish it here, once per label)
+        if (cudaStreamSynchronize(0) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFree(L.ne[d]);
+            L.ne[d] = nullptr;
+            return nullptr;
+        }
+        g->bytes += ne_words * (long long)sizeof(uint32_t);
+        return L.ne[d];
     };
     std::vector<SlotEnt> ents;
     {
@@ -722,10 +750,11 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
         for (auto& k : slot_keys) {
             const int rc = materialize_label(g, k.first);  // device edge list, if any
             if (rc != RPQ_OK) return rc;
-            const LabelDev& L = g->labels[k.first];
+            LabelDev& L = g->labels[k.first];
             ents.push_back(SlotEnt{{L.rowptr[k.second], L.rowptr[1 - k.second]},
                                    {L.col[k.second], L.col[1 - k.second]},
-                                   {L.nnz[k.second], L.nnz[1 - k.second]}});
+                                   {L.nnz[k.second], L.nnz[1 - k.second]},
+                                   &L, 1 - k.second});
         }
         // A state that reads several symbols into the same targets (e.g. the
         // one state of (a|b|c|d)*) gets one merged slot: its rows are the
@@ -755,7 +784,7 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
                         if (rc != RPQ_OK) return rc;
                         sl = (int)ents.size();
                         ents.push_back(SlotEnt{{M->rowptr[0], M->rowptr[1]}, {M->col[0], M->col[1]},
-                                               {M->nnz[0], M->nnz[1]}});
+                                               {M->nnz[0], M->nnz[1]}, M, 1});
                         merged_slot[syms] = sl;
                     }
                 }
@@ -823,6 +852,7 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     T.insert(T.end(), islot.begin(), islot.end());
     for (int pass = 0; pass < 2; ++pass)  // pass 1: the transposes
         for (auto& en : ents) q->slots.push_back(Slot{en.rowptr[pass], en.col[pass]});
+
     for (auto& en : ents) q->slot_nnz.push_back((unsigned long long)en.nnz[0]);
 
     // queue capacities: every (state, vertex) pair is discovered at most once,
@@ -904,6 +934,15 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
     if (!q->slot_nnz.empty())
         QTRY(cudaMemcpy(q->d_slot_nnz, q->slot_nnz.data(), q->slot_nnz.size() * sizeof(unsigned long long),
                         cudaMemcpyHostToDevice));
+    {   // non-empty-row bitmaps of the pulled (transposed) slots, cached per label
+        std::lock_guard<std::mutex> lk(g->mu);
+        for (auto& en : ents) q->ne_tab.push_back(ensure_ne(*en.ne_of, en.ne_dir));
+    }
+    if (!q->ne_tab.empty()) {
+        QTRY(cudaMalloc(&q->d_ne_tab, q->ne_tab.size() * sizeof(const uint32_t*)));
+        QTRY(cudaMemcpy(q->d_ne_tab, q->ne_tab.data(), q->ne_tab.size() * sizeof(const uint32_t*),
+                        cudaMemcpyHostToDevice));
+    }
     // large state spaces: the 32-warp variant (more loads in flight); small: 24 warps
     bool large = (long long)nstates * (long long)g->nv >= kLargePairs;
     if (const char* ev = std::getenv("RPQ_KERNEL_THREADS")) {  // experiments: force a variant
@@ -949,6 +988,7 @@ Params make_params(const rpq_query* q) {
     p.tables = reinterpret_cast<const int32_t*>(q->d_in + q->off_tables);
     p.slots = reinterpret_cast<const Slot*>(q->d_in + q->off_slots);
     p.slot_nnz = q->d_slot_nnz;
+    p.ne_tab = q->d_ne_tab;
     p.visited = q->d_visited;
     for (int f = 0; f < 3; ++f) p.fb[f] = q->d_fb[f];
     for (int b = 0; b < 2; ++b) {

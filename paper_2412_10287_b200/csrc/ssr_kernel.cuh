@@ -33,7 +33,10 @@ namespace rpqk {
 // 1024 (32 warps, 64 registers) for large ones, where more warps in flight win
 constexpr int kThreads = 768;         // small state spaces
 constexpr int kThreadsLarge = 1024;   // large state spaces (and the batch kernel)
-constexpr long long kLargePairs = 8ll << 20;  // |Q| x |V| from which the large variant runs
+#ifndef RPQ_LARGE_PAIRS
+#define RPQ_LARGE_PAIRS (8ll << 20)
+#endif
+constexpr long long kLargePairs = RPQ_LARGE_PAIRS;  // |Q| x |V| from which the large variant runs
 constexpr int kMinBlocks = 1;
 constexpr int kMaxWarps = kThreadsLarge / 32;
 constexpr int kEdgesPerLane = 4;     // push: edges each lane expands per bundle
@@ -185,6 +188,10 @@ struct Params {
     unsigned int* step_acc;     // step mode: [0] steps that found M non-empty, [1] sticky failure
                                 // status of any step (zeroed by rpq_query_step_begin)
     int trace_levels;
+    // per slot: the non-empty-row bitmap of A_s^T (bit v set when row v has
+    // edges; W words), or null -- kept out of Slot (a 24-byte Slot cost the
+    // push levels 15%: cfg3's dense one 70 -> 80 us)
+    const uint32_t* const* ne_tab;
 };
 
 struct Smem {
@@ -199,6 +206,7 @@ struct Smem {
     const int32_t* islot;    // [nin]
     const Slot* slots;       // [2*nslots]
     const float* nnz;        // [nslots] edges of each slot (decision estimates)
+    const uint32_t* const* ne;  // [nslots] non-empty-row bitmaps of the transposes (or null entries)
     const RunArgs* run;      // this run's inputs (shared-memory copy)
     uint64_t pf;             // L2 policy: evict first (graph, queues)
     uint64_t pl;             // L2 policy: evict last (P and F bitmaps)
@@ -1472,6 +1480,186 @@ __device__ __forceinline__ void pull_tasks_q(const Params& p, const Smem& S, con
 }
 #endif  // RPQ_NO_PULL_QUEUE
 
+#ifndef RPQ_NO_PULL_NE
+// Pull over the slot's non-empty-row bitmap (Slot::ne), for levels whose
+// targets each have one active in-slot.  The queued pull above still reads
+// every row pointer of every unvisited vertex to learn which rows have
+// in-edges (one in five to seven on R-MAT) and spends ~250 instructions per
+// 256-vertex task doing so; its levels are bound by instruction issue, not by
+// bytes.  Here a task is 32 words = 1,024 vertices: lane l reads P's word and
+// the bitmap's, candidates = ~P & ne, and only candidates' row pointers are
+// ever loaded -- by the probing round, next to each other (a lane's
+// candidates are queued consecutively, so adjacent lanes of a round read
+// adjacent rows).  Queue entries are vertex ids; a round probes the last 64.
+constexpr int kNECap = 768;  // entries per warp (kWarpScratchWords >= 768)
+static_assert(kNECap <= kWarpScratchWords, "the vertex queue fits the warp scratch");
+
+__device__ __forceinline__ void pull_tasks_ne(const Params& p, const Smem& S, const uint32_t* fcur, uint32_t* fnext,
+                                              long long pw0, long long pw1, int lane, unsigned* s_task,
+                                              int s_nptarget, const int* s_ptarget, const int* s_pk,
+                                              unsigned int* s_state, unsigned int& nnew,
+                                              unsigned long long* steal, uint32_t* ent, int first) {
+    const long long nblk = (pw1 - pw0 + 31) >> 5;
+    const long long ntask = (long long)s_nptarget * nblk;
+    const long long G = gridDim.x;
+    const long long nown = ntask >= 16 * G ? (ntask / 4 * RPQ_PULL_STATIC_NUM) / G * G : ntask;
+    const FastDiv dblk((uint32_t)nblk), dG((uint32_t)G);
+    const uint32_t G32 = (uint32_t)G;
+    int n = 0;    // queued vertices (warp-uniform)
+    int qk = -1;  // the in-transition they belong to
+    int qq2 = 0;  // its target state
+    auto round = [&]() {
+        const int np = min(n, 64);
+        const int base = n - np;
+        const Slot ps = S.slots[p.nslots + S.islot[qk]];
+        const uint32_t* frow = fcur + (long long)S.isrc[qk] * p.W;
+        uint32_t v[2], lo[2], hi[2], e[2];
+        bool act[2], hit[2];
+        int c0[2], c1[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int idx = base + 32 * u + lane;
+            act[u] = idx < n;
+            v[u] = act[u] ? ent[idx] : 0u;
+            if (act[u] && !RPQ_CHECK(v[u] < (uint32_t)p.nv, RPQ_F_SSR)) act[u] = false;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            lo[u] = act[u] ? ld_stream_u32(ps.rowptr + v[u], S.pf) : 0u;
+            hi[u] = act[u] ? ld_stream_u32(ps.rowptr + v[u] + 1, S.pf) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (act[u] && !RPQ_CHECK(lo[u] <= hi[u] && hi[u] <= p.slot_nnz[S.islot[qk] % p.nslots], RPQ_F_SSR))
+                hi[u] = lo[u];
+            if (lo[u] >= hi[u]) act[u] = false;  // (cannot happen for a bitmap built from these rows)
+            c0[u] = act[u] ? ld_stream_i32(ps.col + lo[u], S.pf) : -1;
+            c1[u] = act[u] && first > 1 && lo[u] + 1 < hi[u] ? ld_stream_i32(ps.col + lo[u] + 1, S.pf) : -1;
+            if (act[u] && !RPQ_CHECK(c0[u] >= 0 && c0[u] < p.nv && c1[u] < p.nv, RPQ_F_SSR)) c0[u] = c1[u] = -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            hit[u] = (c0[u] >= 0 && ((ld_bits(frow + (c0[u] >> 5), S.pl) >> (c0[u] & 31)) & 1u)) ||
+                     (c1[u] >= 0 && ((ld_bits(frow + (c1[u] >> 5), S.pl) >> (c1[u] & 31)) & 1u));
+            e[u] = lo[u] + (uint32_t)first;
+        }
+        n = base;
+        // misses continue lane-parallel, two in-edges per entry and round, up
+        // to kPullCont edges of the row; longer rows are scanned by the warp
+        for (;;) {
+            bool go[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) go[u] = act[u] && !hit[u] && e[u] < min(hi[u], lo[u] + (uint32_t)kPullCont);
+            if (!__ballot_sync(FULL, go[0] || go[1])) break;
+            int d0[2], d1[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                d0[u] = go[u] ? ld_stream_i32(ps.col + e[u], S.pf) : -1;
+                d1[u] = go[u] && e[u] + 1 < hi[u] ? ld_stream_i32(ps.col + e[u] + 1, S.pf) : -1;
+                if (go[u] && !RPQ_CHECK(d0[u] >= 0 && d0[u] < p.nv && d1[u] < p.nv, RPQ_F_SSR)) d0[u] = d1[u] = -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+                if (go[u]) {
+                    hit[u] = (d0[u] >= 0 && ((ld_bits(frow + (d0[u] >> 5), S.pl) >> (d0[u] & 31)) & 1u)) ||
+                             (d1[u] >= 0 && ((ld_bits(frow + (d1[u] >> 5), S.pl) >> (d1[u] & 31)) & 1u));
+                    e[u] += 2;
+                }
+        }
+        unsigned nhit = 0;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            unsigned longs = __ballot_sync(FULL, act[u] && !hit[u] && e[u] < hi[u]);
+            while (longs) {
+                const int sl = __ffs(longs) - 1;
+                longs &= longs - 1;
+                const uint32_t rlo = __shfl_sync(FULL, e[u], sl), rhi = __shfl_sync(FULL, hi[u], sl);
+                bool found_row = false;
+                for (uint32_t ed = rlo; ed < rhi; ed += 128) {
+                    int uu[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        uu[c] = ed + 32 * c + lane < rhi ? ld_stream_i32(ps.col + ed + 32 * c + lane, S.pf) : -1;
+                    bool hh = false;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (uu[c] >= 0 && RPQ_CHECK(uu[c] < p.nv, RPQ_F_SSR))
+                            hh |= (ld_bits(frow + (uu[c] >> 5), S.pl) >> (uu[c] & 31)) & 1u;
+                    if (__ballot_sync(FULL, hh)) {
+                        found_row = true;
+                        break;
+                    }
+                }
+                if (found_row && lane == sl) hit[u] = true;
+            }
+            if (act[u] && hit[u]) {
+                const long long off = (long long)qq2 * p.W + (v[u] >> 5);
+                const uint32_t bit = 1u << (v[u] & 31u);
+                red_or_bits(p.visited + off, bit, S.pl);
+                red_or_bits(fnext + off, bit, S.pl);
+                ++nnew;
+            }
+            nhit += __popc(__ballot_sync(FULL, act[u] && hit[u]));
+        }
+        if (lane == 0 && nhit) atomicAdd(&s_state[qq2], nhit);
+        __syncwarp();  // (the queue's tail is rewritten by the next append)
+    };
+    for (;;) {
+        uint32_t task = 0;
+        if (lane == 0) {
+            const uint32_t i = atomicAdd(s_task, 1u);
+            uint32_t rot;
+            dG.div(blockIdx.x + i, &rot);
+            task = i * G32 + rot;
+            if (task >= (uint32_t)nown && nown < ntask) task = (uint32_t)nown + (uint32_t)atomicAdd(steal, 1ull);
+        }
+        task = __shfl_sync(FULL, task, 0);
+        if ((long long)task >= ntask) break;
+        uint32_t blk;
+        const uint32_t tq = dblk.div(task, &blk);
+        const int q2 = s_ptarget[tq];
+        const int k = s_pk[tq];
+        const long long word = pw0 + (long long)blk * 32 + lane;
+        uint32_t cm = 0;
+        if (word < pw1) {
+            const uint32_t pwv = ld_bits(p.visited + (long long)q2 * p.W + word, S.pl);
+            const uint32_t nev = ld_stream_u32(S.ne[S.islot[k]] + word, S.pf);
+            cm = ~pwv & nev;  // (bits past |V| are clear in the bitmap)
+        }
+        if (__ballot_sync(FULL, cm != 0) == 0) continue;
+        if (qk != k)
+            while (n > 0) round();
+        qk = k;
+        qq2 = q2;
+        // append lane by lane (a lane's candidates are consecutive entries);
+        // a block with more candidates than the queue has room for goes in
+        // two halves of 16 lanes (<= 512 candidates each)
+        const uint32_t cnt = __popc(cm);
+        const uint32_t incl = warp_incl_scan(cnt, lane);
+        const uint32_t total = __shfl_sync(FULL, incl, 31);
+        const uint32_t half0 = __shfl_sync(FULL, incl, 15);
+        const bool split = n + (int)total > kNECap;
+        for (int part = 0; part < (split ? 2 : 1); ++part) {
+            const bool mine = !split || (lane >> 4) == part;
+            const uint32_t padd = !split ? total : part == 0 ? half0 : total - half0;
+            const uint32_t pbase = split && part == 1 ? half0 : 0u;
+            while (n > 0 && n + (int)padd > kNECap) round();
+            int pos = n + (int)(incl - cnt - pbase);
+            uint32_t m = mine ? cm : 0u;
+            const uint32_t vb = (uint32_t)(word << 5);
+            while (m) {
+                ent[pos++] = vb + (uint32_t)(__ffs(m) - 1);
+                m &= m - 1;
+            }
+            n += (int)padd;
+            __syncwarp();
+            while (n >= 64) round();
+        }
+    }
+    while (n > 0) round();
+}
+#endif  // RPQ_NO_PULL_NE
+
 // Diagnostic stamp k of level L for this CTA (thread 0): 0 level start (after
 // the decision), 1 plan epoch done, 2 last warp done with the expansion,
 // 3 past the barrier, 4 counters flushed.
@@ -1492,6 +1680,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
     __shared__ int s_ptarget[kMaxStates];            // pull target states of this level
     __shared__ int s_nptarget;
     __shared__ int s_pmulti;  // some pull target of this level has several active in-slots
+    __shared__ int s_pne;     // every pull target's in-slot has a non-empty-row bitmap
     __shared__ int s_pk[kMaxStates];  // first active in-transition of each pull target
     __shared__ View s_view;
     __shared__ unsigned long long s_resv;
@@ -1501,11 +1690,15 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
     __shared__ unsigned long long s_wend;  // diagnostics: latest warp done with the epoch
     __shared__ RunArgs s_run;
     __shared__ float s_nnz[kMaxSlots];
+    __shared__ const uint32_t* s_ne[kMaxSlots];
 
     // dynamic smem: [emission stages, kStageBytes(NT)] [slots] [tables]
     int* s_stage = reinterpret_cast<int*>(smem_raw);
     Slot* s_slots = reinterpret_cast<Slot*>(smem_raw + kStageBytes(NT));
-    for (int i = threadIdx.x; i < p.nslots; i += blockDim.x) s_nnz[i] = (float)p.slot_nnz[i];
+    for (int i = threadIdx.x; i < p.nslots; i += blockDim.x) {
+        s_nnz[i] = (float)p.slot_nnz[i];
+        s_ne[i] = p.ne_tab ? p.ne_tab[i] : nullptr;
+    }
     int32_t* s_tab = reinterpret_cast<int32_t*>(smem_raw + kStageBytes(NT) + sizeof(Slot) * 2 * p.nslots);
     for (int i = threadIdx.x; i < 2 * p.nslots; i += blockDim.x) s_slots[i] = p.slots[i];
     for (int i = threadIdx.x; i < p.table_ints; i += blockDim.x) s_tab[i] = p.tables[i];
@@ -1537,6 +1730,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
     S.run = &s_run;
     S.slots = s_slots;
     S.nnz = s_nnz;
+    S.ne = s_ne;
     S.gbeg = s_tab;
     S.gslot = S.gbeg + p.nstates + 1;
     S.toff = S.gslot + p.ngroups;
@@ -2181,12 +2375,13 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
                 nedge += frontier_edges(p, S, fcur, gtid, gthreads, Wn);
             if (threadIdx.x == 0) {
                 int n = 0;
-                int multi = 0;
+                int multi = 0, ne_ok = 1;
                 for (int q2 = 0; q2 < p.nstates; ++q2) {
                     int any = 0, kf = 0;
                     for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k)
                         if (s_front[S.isrc[k]] != 0 && any++ == 0) kf = k;
                     if (any) {
+                        ne_ok &= S.ne[S.islot[kf]] != nullptr;
                         s_pk[n] = kf;  // the first (for the queued pull: the only) active in-transition
                         s_ptarget[n++] = q2;
                     }
@@ -2194,6 +2389,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
                 }
                 s_nptarget = n;
                 s_pmulti = multi;
+                s_pne = ne_ok;
             }
             __syncthreads();
             // targets: the owned word range (vertex-partitioned step), else all
@@ -2215,6 +2411,12 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
             // in-slot (cfg3: pull levels 149 -> 143 and 110 -> 96 us); targets
             // with several need each slot's answers before the next and drain
             // the queue per slot, which costs more than it saves (cfg5: +10%)
+#ifndef RPQ_NO_PULL_NE
+            if (pw1 - pw0 >= (long long)nwarps * RPQ_PV8_WORDS_PER_WARP && !s_pmulti && s_pne)
+                pull_tasks_ne(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_pk, s_state,
+                              nnew, pull_steal, scratch, first);
+            else
+#endif
             if (pw1 - pw0 >= (long long)nwarps * RPQ_PV8_WORDS_PER_WARP && !s_pmulti)
                 pull_tasks_q<8>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_pk, s_state,
                                 nnew, pull_steal, scratch, first);
@@ -2414,6 +2616,18 @@ __global__ void count_nonempty_kernel(const uint32_t* __restrict__ rowptr, long 
         c += rowptr[i + 1] > rowptr[i];
     c = __reduce_add_sync(0xFFFFFFFFu, c);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
+// Non-empty-row bitmap of a CSR (Slot::ne): bit v of word v / 32 set when row v
+// has edges; `words` words (bits past nv clear).  One ballot per 32 rows.
+__global__ void nonempty_bitmap_kernel(const uint32_t* __restrict__ rowptr, long long nv, uint32_t* __restrict__ out,
+                                       long long words) {
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < words * 32;
+         v += (long long)gridDim.x * blockDim.x) {  // (warp-uniform trip count: bounds are multiples of 32)
+        const bool ne = v < nv && rowptr[v + 1] > rowptr[v];
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, ne);
+        if ((threadIdx.x & 31) == 0) out[v >> 5] = m;
+    }
 }
 
 // uint8[nv] answer vector from the answer bitmap (bit v%32 of word v/32):
