@@ -1751,6 +1751,17 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
     const long long Wn = ((long long)p.nv + 31) >> 5;  // used words per bitmap row
     const long long nbits4 = (long long)p.nstates * p.W / 4;
     const bool cta0 = blockIdx.x == 0;
+    // The bitmap level L+1 will write F_{L+2} into is F_{L-1}'s, free since
+    // the barrier that ended level L-1: warps 1.. zero it while warp 0 takes
+    // level L's decision (its loads are a 1.3 us round trip in which the CTA
+    // had nothing else to do; the stores used to open the expand epoch).
+    auto zero_next = [&](int L_) {
+#ifndef RPQ_ZERO_IN_EXPAND
+        uint4* z4 = reinterpret_cast<uint4*>(p.fb[(L_ + 2) % 3]);
+        const long long zt = (long long)blockIdx.x * (NT - 32) + (threadIdx.x - 32);
+        for (long long i = zt; i < nbits4; i += (long long)gridDim.x * (NT - 32)) z4[i] = make_uint4(0, 0, 0, 0);
+#endif
+    };
     __syncthreads();  // s_run, tables and counters above are read by every thread below
     Stage stage;
     stage.q = s_stage + wid * kWarpScratchWords;
@@ -1871,6 +1882,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
     if (!step_mode) {
         grid_barrier(ctl, ++e, s_run.bar_base);
         if (wid == 0) decide_level(p, S, e, 0, 1, DIR_PUSH, lane, &s_view, s_bpre, s_sv, s_front);
+        else zero_next(0);
     } else {
         // one step from F_0 = M: count M per state (one epoch), then pull
         // (when M is dense against the owned targets) or push (emit M's rows
@@ -2057,10 +2069,12 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
             for (int q = threadIdx.x; q < kMaxStates; q += blockDim.x) fz->state[q] = 0;
             if (threadIdx.x == 0) fz->nnew = 0;
         }
+#ifdef RPQ_ZERO_IN_EXPAND
         if (!step_mode) {  // zero the bitmap level L+1 will write F_{L+2} into
             uint4* z4 = reinterpret_cast<uint4*>(p.fb[(L + 2) % 3]);
             for (long long i = gtid; i < nbits4; i += gthreads) z4[i] = make_uint4(0, 0, 0, 0);
         }
+#endif
 #ifndef RPQ_NO_CLAIM_CACHE
         if (dir == DIR_PUSH && pc_dirty) {  // (CTA-uniform)
             for (int i = threadIdx.x; i < kPcEntries; i += NT) *pc_entry_at(i) = 0ull;
@@ -2458,6 +2472,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
             break;
         }
         if (wid == 0) decide_level(p, S, e, L, queued, dir, lane, &s_view, s_bpre, s_sv, s_front);
+        else zero_next(L);
         __syncthreads();
     }
 
