@@ -936,7 +936,10 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
                         cudaMemcpyHostToDevice));
     {   // non-empty-row bitmaps of the pulled (transposed) slots, cached per label
         std::lock_guard<std::mutex> lk(g->mu);
-        for (auto& en : ents) q->ne_tab.push_back(ensure_ne(*en.ne_of, en.ne_dir));
+        for (auto& en : ents) {
+            q->ne_tab.push_back(ensure_ne(*en.ne_of, en.ne_dir));
+            if (!q->ne_tab.back() && en.rowptr[1]) return bail(fail(RPQ_ECUDA, "out of device memory (row bitmaps)"));
+        }
     }
     if (!q->ne_tab.empty()) {
         QTRY(cudaMalloc(&q->d_ne_tab, q->ne_tab.size() * sizeof(const uint32_t*)));

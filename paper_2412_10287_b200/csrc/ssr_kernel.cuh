@@ -42,7 +42,6 @@ constexpr int kMaxWarps = kThreadsLarge / 32;
 constexpr int kEdgesPerLane = 4;     // push: edges each lane expands per bundle
 constexpr int kBundle = 32 * kEdgesPerLane;  // edges per bundle; an emission pass has
                                              // <= 32 segments, so a bundle spans <= 32
-constexpr int kPullVerts = 4;        // pull: vertices (words of 32) per lane per task
 constexpr int kShards = 160;         // queue shards, one per CTA (+1 overflow shard)
 static_assert(kShards <= 256, "the push shard search (two ballots of 32 x 8) covers 256 shards");
 constexpr int kMaxStates = 256;
@@ -1039,346 +1038,118 @@ struct FastDiv {
     }
 };
 
-// Pull tasks of one level: every (target state, PV words of vertices) with an
-// active source state.  PV words per lane-task: more vertices in flight per
-// warp on large graphs, more tasks (balance) on small ones.
-// Task dealing: round i of CTA c takes task i*G + (c + i) mod G -- a
-// rotation, so a CTA's tasks do not all share one residue of the vertex
-// blocks mod G (on R-MAT, in-degree depends on the id's bits: a fixed
-// residue made one CTA the slowest of every pull level by 40%).  On long
-// task lists the last quarter is dealt from one grid-wide counter instead.
-//
-// Per task and in-slot, the vertices that still need a look and have in-edges
-// in the slot are compacted into a warp-private candidate list in shared
-// memory (on R-MAT about one vertex in five): the gathers then run on full
-// warps instead of eight mostly-idle predicated rounds.  Each candidate lane
-// probes its row's first `first` in-edges, then continues lane-parallel two
-// edges per round up to kPullCont edges; rows still undecided after that
-// (rare: < 1% on cfg3) are scanned by the whole warp, 128 edges per step.
-constexpr int kPullCont = 8;
-//
-// Layout: a task covers PV words = 32*PV vertices; lane l owns the PV
-// consecutive vertices v0 = 32*word0 + PV*l ... v0 + PV - 1, so its row
-// pointers rowptr[v0 .. v0+PV] are PV/4 128-bit loads plus one shuffle (the
-// next lane's first), and its P / found bits are a PV-bit field of one word.
-template <int PV>
-__device__ __forceinline__ void load_rows(const uint32_t* rp, long long v0, int nv, int lane, bool active,
-                                          uint64_t pol, uint32_t (&r)[PV + 1]) {
-    // the common case, a block wholly inside the vertex range with every lane
-    // looking (warp-uniform): two 128-bit loads, the next lane's first pointer
-    // by shuffle, lane 31's from memory -- none of the end-of-range fix-ups
-    // below (they were 36 instructions per task)
-    if (v0 - (long long)PV * lane + 32 * PV <= nv && __all_sync(FULL, active)) {
-        const uint4* r4 = reinterpret_cast<const uint4*>(rp + v0);
-        uint32_t last = 0;
-        if (lane == 31) last = ld_stream_u32(rp + v0 + PV, pol);
-#pragma unroll
-        for (int c = 0; c < PV / 4; ++c) {
-            uint4 x;
-            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
-                         : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(r4 + c), "l"(pol));
-            r[4 * c] = x.x;
-            r[4 * c + 1] = x.y;
-            r[4 * c + 2] = x.z;
-            r[4 * c + 3] = x.w;
-        }
-        const uint32_t nx = __shfl_down_sync(FULL, r[0], 1);
-        r[PV] = lane < 31 ? nx : last;
-        return;
-    }
-    // lanes with nothing to look at skip their loads (a later in-slot of a
-    // target, once most of the lane's vertices are found or visited)
-    if (active) {
-        if (v0 + PV <= nv) {
-            const uint4* r4 = reinterpret_cast<const uint4*>(rp + v0);  // v0 % PV == 0: 16-byte aligned
-#pragma unroll
-            for (int c = 0; c < PV / 4; ++c) {
-                uint4 x;
-                // streamed once per level: evict-first in L2, like every other adjacency read
-                asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
-                             : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(r4 + c), "l"(pol));
-                r[4 * c] = x.x;
-                r[4 * c + 1] = x.y;
-                r[4 * c + 2] = x.z;
-                r[4 * c + 3] = x.w;
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < PV; ++j) r[j] = v0 + j <= nv ? ld_stream_u32(rp + v0 + j, pol) : 0u;
-        }
-    }
-    // rowptr[v0 + PV]: the next lane's first when it loaded, else our own load
-    const uint32_t nx = __shfl_down_sync(FULL, r[0], 1);
-    const bool next_loaded = __shfl_down_sync(FULL, active ? 1 : 0, 1) != 0;
-    if (active) {
-        r[PV] = (lane < 31 && next_loaded && v0 + PV <= nv) ? nx
-                                                            : (v0 + PV <= nv ? ld_stream_u32(rp + v0 + PV, pol) : r[PV - 1]);
-#pragma unroll
-        for (int j = 1; j <= PV; ++j)  // past the end: empty rows
-            if (v0 + j > nv) r[j] = r[j - 1];
-    }
-}
-
-template <int PV>
-__device__ __forceinline__ void pull_tasks(const Params& p, const Smem& S, const uint32_t* fcur, uint32_t* fnext,
-                                           long long pw0, long long pw1, int lane, unsigned* s_task,
-                                           int s_nptarget, const int* s_ptarget, const unsigned int* s_front,
-                                           unsigned int* s_state, unsigned int& nnew,
-                                           unsigned long long* steal, uint32_t* scratch, int first) {
-    constexpr int LPW = 32 / PV;  // lanes per word
-    const long long nblk = (pw1 - pw0 + PV - 1) / PV;
-    const long long ntask = (long long)s_nptarget * nblk;
-    const long long G = gridDim.x;
+constexpr int kPullCont = 8;  // in-edges a lane probes on its own before the warp scans the row
 #ifndef RPQ_PULL_STATIC_NUM
 #define RPQ_PULL_STATIC_NUM 3  // static share of the pull tasks, in quarters
 #endif
-    const long long nown = ntask >= 16 * G ? (ntask / 4 * RPQ_PULL_STATIC_NUM) / G * G : ntask;
-    // warp scratch: candidate vertex offset (bit 31: long row), row start, row end; found words
-    uint32_t* cid = scratch;
-    uint32_t* clo = scratch + 32 * PV;
-    uint32_t* chi = scratch + 64 * PV;
-    uint32_t* cfound = scratch + 96 * PV;
-    const uint32_t fmask_all = (1u << PV) - 1u;
-    const int sh = PV * (lane % LPW);  // this lane's bit offset in its word
-    // task indices fit 32 bits (targets x blocks <= 256 x 2^28): 32-bit
-    // division and modulo (64-bit ones are ~100-instruction subroutines)
-    const uint32_t G32 = (uint32_t)G;
-    const FastDiv dblk((uint32_t)nblk), dG(G32);
-    auto grab = [&]() -> uint32_t {
-        uint32_t t = 0;
-        if (lane == 0) {
-            const uint32_t i = atomicAdd(s_task, 1u);
-            uint32_t rot;
-            dG.div(blockIdx.x + i, &rot);
-            t = i * G32 + rot;
-            if (t >= (uint32_t)nown && nown < ntask) t = (uint32_t)nown + (uint32_t)atomicAdd(steal, 1ull);
-        }
-        return __shfl_sync(FULL, t, 0);
-    };
-    for (;;) {
-        const uint32_t task = grab();
-        if ((long long)task >= ntask) break;
-        uint32_t blk;
-        const uint32_t tq = dblk.div(task, &blk);
-        const int q2 = s_ptarget[tq];
-        const long long word0 = pw0 + (long long)blk * PV;
-        const long long myword = word0 + lane / LPW;
-        const long long v0 = word0 * 32 + (long long)PV * lane;
-        // the first pulled in-slot (warp-uniform): its row pointers do not
-        // depend on P, so they are loaded with P's words (one dependent round
-        // trip less per task; visited vertices' are wasted)
-        int k0 = -1;
-        for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k)
-            if (s_front[S.isrc[k]]) {
-                k0 = k;
-                break;
-            }
-        uint32_t r[PV + 1];
-        const uint32_t pw = myword < pw1 ? ld_bits(p.visited + (long long)q2 * p.W + myword, S.pl) : 0xFFFFFFFFu;
-        load_rows<PV>(S.slots[p.nslots + S.islot[max(k0, 0)]].rowptr, v0, p.nv, lane, true, S.pf, r);
-        // need: this lane's unvisited vertices (PV bits)
-        uint32_t need = ~(pw >> sh) & fmask_all;
-        if (v0 >= p.nv) need = 0;
-        else if (v0 + PV > p.nv) need &= (1u << (p.nv - v0)) - 1u;
-        if (myword >= pw1) need = 0;
-        uint32_t found = 0;
-        if (__ballot_sync(FULL, need != 0) == 0) continue;
-        for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k) {
-            const int q = S.isrc[k];
-            if (!s_front[q]) continue;
-            const uint32_t look = need & ~found;
-            if (__ballot_sync(FULL, look != 0) == 0) break;
-            const Slot ps = S.slots[p.nslots + S.islot[k]];
-            const uint32_t* frow = fcur + (long long)q * p.W;
-            if (k != k0) load_rows<PV>(ps.rowptr, v0, p.nv, lane, look != 0, S.pf, r);
-            // compaction: the looking vertices with in-edges in this slot
-            uint32_t cm = 0;
-#pragma unroll
-            for (int j = 0; j < PV; ++j)
-                if (((look >> j) & 1u) && r[j + 1] > r[j]) cm |= 1u << j;
-            if (cm && !RPQ_CHECK(r[PV] <= p.slot_nnz[S.islot[k] % p.nslots], RPQ_F_SSR)) cm = 0;
-            const uint32_t cnt = __popc(cm);
-            const uint32_t incl = warp_incl_scan(cnt, lane);
-            const int n = (int)__shfl_sync(FULL, incl, 31);
-            int pos = (int)(incl - cnt);
-#pragma unroll
-            for (int j = 0; j < PV; ++j)
-                if ((cm >> j) & 1u) {
-                    cid[pos] = (uint32_t)(PV * lane + j);
-                    clo[pos] = r[j];
-                    chi[pos] = r[j + 1];
-                    ++pos;
-                }
-            if (lane < PV) cfound[lane] = 0u;
-            __syncwarp();
-            bool any_long = false;
-            for (int j0 = 0; j0 < n; j0 += 32) {
-                const int j = j0 + lane;
-                const bool act = j < n;
-                const uint32_t l = act ? clo[j] : 0u, h = act ? chi[j] : 0u;
-                // first round: `first` in-edges, all loads in flight
-                int c0 = act ? ld_stream_i32(ps.col + l, S.pf) : -1;
-                int c1 = act && first > 1 && l + 1 < h ? ld_stream_i32(ps.col + l + 1, S.pf) : -1;
-                if (act && !RPQ_CHECK(c0 >= 0 && c0 < p.nv && c1 < p.nv && l < h, RPQ_F_SSR)) c0 = c1 = -1;
-                bool hit = (c0 >= 0 && ((ld_bits(frow + (c0 >> 5), S.pl) >> (c0 & 31)) & 1u)) ||
-                           (c1 >= 0 && ((ld_bits(frow + (c1 >> 5), S.pl) >> (c1 & 31)) & 1u));
-                uint32_t e = l + (uint32_t)first;
-                const uint32_t cap = min(h, l + (uint32_t)kPullCont);
-                // lane-parallel continuation, two in-edges per round
-                while (__ballot_sync(FULL, act && !hit && e < cap)) {
-                    if (act && !hit && e < cap) {
-                        const int d0 = ld_stream_i32(ps.col + e, S.pf);
-                        const int d1 = e + 1 < cap ? ld_stream_i32(ps.col + e + 1, S.pf) : -1;
-                        hit = ((ld_bits(frow + (d0 >> 5), S.pl) >> (d0 & 31)) & 1u) ||
-                              (d1 >= 0 && ((ld_bits(frow + (d1 >> 5), S.pl) >> (d1 & 31)) & 1u));
-                        e += 2;
-                    }
-                }
-                if (act && hit) {
-                    const uint32_t id = cid[j];
-                    atomicOr(&cfound[id >> 5], 1u << (id & 31u));
-                }
-                const bool lng = act && !hit && e < h;
-                if (lng) {
-                    cid[j] |= 0x80000000u;
-                    clo[j] = e;
-                }
-                any_long |= lng;
-            }
-            // rows still undecided: the whole warp scans each, early exit
-            if (__ballot_sync(FULL, any_long)) {
-                __syncwarp();
-                for (int j0 = 0; j0 < n; j0 += 32) {
-                    unsigned longs = __ballot_sync(FULL, j0 + lane < n && (cid[j0 + lane] >> 31));
-                    while (longs) {
-                        const int jj = j0 + __ffs(longs) - 1;
-                        longs &= longs - 1;
-                        const uint32_t rlo = clo[jj], rhi = chi[jj];
-                        bool hit = false;
-                        for (uint32_t ed = rlo; ed < rhi; ed += 128) {
-                            int uu[4];
-#pragma unroll
-                            for (int c = 0; c < 4; ++c)
-                                uu[c] = ed + 32 * c + lane < rhi ? ld_stream_i32(ps.col + ed + 32 * c + lane, S.pf) : -1;
-                            bool hh = false;
-#pragma unroll
-                            for (int c = 0; c < 4; ++c)
-                                if (uu[c] >= 0) hh |= (ld_bits(frow + (uu[c] >> 5), S.pl) >> (uu[c] & 31)) & 1u;
-                            if (__ballot_sync(FULL, hh)) {
-                                hit = true;
-                                break;
-                            }
-                        }
-                        if (hit && lane == 0) {
-                            const uint32_t id = cid[jj] & 0x7FFFFFFFu;
-                            atomicOr(&cfound[id >> 5], 1u << (id & 31u));
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-            found |= (cfound[lane / LPW] >> sh) & fmask_all;
-            __syncwarp();  // cfound / the candidate list are rewritten by the next slot or task
-        }
-        // the warp owns these (q2, word) pairs this epoch: F is a plain store,
-        // P an OR without return; the first lane of each word writes it
-        uint32_t fm = found << sh;
-#pragma unroll
-        for (int d = 1; d < LPW; d <<= 1) fm |= __shfl_xor_sync(FULL, fm, d);
-        if (lane % LPW == 0 && fm) {
-            const long long voff = (long long)q2 * p.W + myword;
-            red_or_bits(p.visited + voff, fm, S.pl);
-            fnext[voff] = fm;
-            nnew += __popc(fm);
-            atomicAdd(&s_state[q2], (unsigned)__popc(fm));
-        }
-    }
-}
 
-#ifndef RPQ_NO_PULL_QUEUE
-// Pull with a per-warp candidate queue that outlives the task, for levels
-// whose targets each have ONE active in-slot (s_pk[tq]: that in-transition).
-// pull_tasks gathers each task's candidates on their own: about 36 per
-// 256-vertex task on cfg3, so every second gather round runs on a handful of
-// lanes, and a row whose first probe misses keeps its lane (and the warp) in
-// a serial continuation.  Here candidates {vertex, row cursor, row end} of
-// consecutive tasks accumulate in shared memory (one 16-byte entry each) and
-// are probed in uniform rounds of 64 (two per lane, all column loads in
-// flight, then all frontier probes); a miss with edges left goes back on the
-// queue with its cursor advanced, so no lane waits on another's row.  A
+
+// Pull over the in-slots' non-empty-row bitmaps (Params::ne_tab).  Reading
+// every row pointer of every unvisited vertex to learn which rows have
+// in-edges (one in five to seven on R-MAT) cost ~250 instructions per
+// 256-vertex task, and the pull levels were bound by instruction issue, not
+// by bytes.  Here a task is TW words of vertices (32 on large graphs: 1,024
+// vertices): lane l reads P's word and the bitmap's, candidates = ~P & ne, and
+// only candidates' row pointers are ever loaded -- by the probing round, next
+// to each other (a lane's candidates are queued consecutively, so adjacent
+// lanes of a round read adjacent rows).  The queue holds vertex ids and
+// outlives the task: rounds always probe 64 (two per lane, every load of a
+// stage in flight together), whatever a single task contributes.  A
 // discovery is a RED into P and F: the warp dealt the vertex is the only one
-// looking at the pair this level, and each pair is queued once.
-constexpr int kPQCap = 192;             // entries (16 bytes each) per warp: kWarpScratchWords
-constexpr int kPQRound = 64;
-constexpr uint32_t kPQRequeueMax = 16;  // a miss with more edges left than this is scanned by the whole warp
-static_assert(4 * kPQCap <= kWarpScratchWords, "the candidate queue fits the warp scratch");
+// looking at the pair this level.
+// A target with several active in-slots (s_pk < 0) takes them one at a time:
+// a slot's rounds finish (recording their hits in `found`) before the next
+// slot looks at what is still missing.
+#ifndef RPQ_NE_TW
+#define RPQ_NE_TW 32  // words of vertices per pull task on large graphs
+#endif
+constexpr int kNECap = 736;  // queued vertices per warp; + 32 found words <= kWarpScratchWords
+static_assert(kNECap + 32 <= kWarpScratchWords, "the vertex queue and the found words fit the warp scratch");
 
-template <int PV>
-__device__ __forceinline__ void pull_tasks_q(const Params& p, const Smem& S, const uint32_t* fcur, uint32_t* fnext,
-                                             long long pw0, long long pw1, int lane, unsigned* s_task,
-                                             int s_nptarget, const int* s_ptarget, const int* s_pk,
-                                             unsigned int* s_state, unsigned int& nnew,
-                                             unsigned long long* steal, uint32_t* scratch, int first) {
-    constexpr int LPW = 32 / PV;  // lanes per word
-    const long long nblk = (pw1 - pw0 + PV - 1) / PV;
+template <int TW>
+__device__ __forceinline__ void pull_tasks_ne(const Params& p, const Smem& S, const uint32_t* fcur, uint32_t* fnext,
+                                              long long pw0, long long pw1, int lane, unsigned* s_task,
+                                              int s_nptarget, const int* s_ptarget, const int* s_pk,
+                                              const unsigned int* s_front, unsigned int* s_state, unsigned int& nnew,
+                                              unsigned long long* steal, uint32_t* ent, int first) {
+    const long long nblk = (pw1 - pw0 + TW - 1) / TW;
     const long long ntask = (long long)s_nptarget * nblk;
     const long long G = gridDim.x;
     const long long nown = ntask >= 16 * G ? (ntask / 4 * RPQ_PULL_STATIC_NUM) / G * G : ntask;
-    uint4* ent = reinterpret_cast<uint4*>(scratch);  // (the warp scratch is 16-byte aligned)
-    const uint32_t fmask_all = (1u << PV) - 1u;
-    const int sh = PV * (lane % LPW);
     const FastDiv dblk((uint32_t)nblk), dG((uint32_t)G);
     const uint32_t G32 = (uint32_t)G;
-    int n = 0;    // queued entries (warp-uniform)
-    int qk = -1;  // the in-transition the queued entries belong to
-    int qq2 = 0;  // its target state
-    // one round: the last <= 64 entries of the queue
+    uint32_t* found = ent + kNECap;  // [32] hits of the current task (targets with several in-slots)
+    int n = 0;              // queued vertices (warp-uniform)
+    int qk = -1;            // the in-transition they belong to
+    int qq2 = 0;            // its target state
+    uint32_t qvb = 0;       // first vertex of the task whose hits `found` records
+    bool qrec = false;      // record hits in `found`
     auto round = [&]() {
-        const int np = min(n, kPQRound);
+        const int np = min(n, 64);
         const int base = n - np;
         const Slot ps = S.slots[p.nslots + S.islot[qk]];
         const uint32_t* frow = fcur + (long long)S.isrc[qk] * p.W;
-        uint4 en[2];
+        uint32_t v[2], lo[2], hi[2], e[2];
         bool act[2], hit[2];
         int c0[2], c1[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const int idx = base + 32 * u + lane;
             act[u] = idx < n;
-            en[u] = act[u] ? ent[idx] : make_uint4(0u, 0u, 0u, 0u);  // {vertex, cursor, row end, -}
+            v[u] = act[u] ? ent[idx] : 0u;
+            if (act[u] && !RPQ_CHECK(v[u] < (uint32_t)p.nv, RPQ_F_SSR)) act[u] = false;
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            c0[u] = act[u] ? ld_stream_i32(ps.col + en[u].y, S.pf) : -1;
-            c1[u] = act[u] && first > 1 && en[u].y + 1 < en[u].z ? ld_stream_i32(ps.col + en[u].y + 1, S.pf) : -1;
-            if (act[u] && !RPQ_CHECK(c0[u] >= 0 && c0[u] < p.nv && c1[u] < p.nv && en[u].y < en[u].z &&
-                                         en[u].z <= p.slot_nnz[S.islot[qk] % p.nslots] && en[u].x < (uint32_t)p.nv,
-                                     RPQ_F_SSR)) {
-                c0[u] = c1[u] = -1;
-                en[u].z = en[u].y;
-            }
+            lo[u] = act[u] ? ld_stream_u32(ps.rowptr + v[u], S.pf) : 0u;
+            hi[u] = act[u] ? ld_stream_u32(ps.rowptr + v[u] + 1, S.pf) : 0u;
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
+        for (int u = 0; u < 2; ++u) {
+            if (act[u] && !RPQ_CHECK(lo[u] <= hi[u] && hi[u] <= p.slot_nnz[S.islot[qk] % p.nslots], RPQ_F_SSR))
+                hi[u] = lo[u];
+            if (lo[u] >= hi[u]) act[u] = false;  // (cannot happen for a bitmap built from these rows)
+            c0[u] = act[u] ? ld_stream_i32(ps.col + lo[u], S.pf) : -1;
+            c1[u] = act[u] && first > 1 && lo[u] + 1 < hi[u] ? ld_stream_i32(ps.col + lo[u] + 1, S.pf) : -1;
+            if (act[u] && !RPQ_CHECK(c0[u] >= 0 && c0[u] < p.nv && c1[u] < p.nv, RPQ_F_SSR)) c0[u] = c1[u] = -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
             hit[u] = (c0[u] >= 0 && ((ld_bits(frow + (c0[u] >> 5), S.pl) >> (c0[u] & 31)) & 1u)) ||
                      (c1[u] >= 0 && ((ld_bits(frow + (c1[u] >> 5), S.pl) >> (c1[u] & 31)) & 1u));
+            e[u] = lo[u] + (uint32_t)first;
+        }
         n = base;
-        __syncwarp();  // every lane holds its entries: the tail may be rewritten
+        // misses continue lane-parallel, two in-edges per entry and round, up
+        // to kPullCont edges of the row; longer rows are scanned by the warp
+        for (;;) {
+            bool go[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) go[u] = act[u] && !hit[u] && e[u] < min(hi[u], lo[u] + (uint32_t)kPullCont);
+            if (!__ballot_sync(FULL, go[0] || go[1])) break;
+            int d0[2], d1[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                d0[u] = go[u] ? ld_stream_i32(ps.col + e[u], S.pf) : -1;
+                d1[u] = go[u] && e[u] + 1 < hi[u] ? ld_stream_i32(ps.col + e[u] + 1, S.pf) : -1;
+                if (go[u] && !RPQ_CHECK(d0[u] >= 0 && d0[u] < p.nv && d1[u] < p.nv, RPQ_F_SSR)) d0[u] = d1[u] = -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+                if (go[u]) {
+                    hit[u] = (d0[u] >= 0 && ((ld_bits(frow + (d0[u] >> 5), S.pl) >> (d0[u] & 31)) & 1u)) ||
+                             (d1[u] >= 0 && ((ld_bits(frow + (d1[u] >> 5), S.pl) >> (d1[u] & 31)) & 1u));
+                    e[u] += 2;
+                }
+        }
         unsigned nhit = 0;
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            const uint32_t e = en[u].y + (uint32_t)first;
-            const bool miss = act[u] && !hit[u] && e < en[u].z;
-            const bool lng = miss && en[u].z - e > kPQRequeueMax;
-            const unsigned mreq = __ballot_sync(FULL, miss && !lng);
-            if (miss && !lng) ent[n + __popc(mreq & lanemask_lt())] = make_uint4(en[u].x, e, en[u].z, 0u);
-            n += __popc(mreq);
-            // long rows: the whole warp scans each, 128 edges per step, early exit
-            unsigned longs = __ballot_sync(FULL, lng);
+            unsigned longs = __ballot_sync(FULL, act[u] && !hit[u] && e[u] < hi[u]);
             while (longs) {
                 const int sl = __ffs(longs) - 1;
                 longs &= longs - 1;
-                const uint32_t rlo = __shfl_sync(FULL, e, sl), rhi = __shfl_sync(FULL, en[u].z, sl);
+                const uint32_t rlo = __shfl_sync(FULL, e[u], sl), rhi = __shfl_sync(FULL, hi[u], sl);
                 bool found_row = false;
                 for (uint32_t ed = rlo; ed < rhi; ed += 128) {
                     int uu[4];
@@ -1398,18 +1169,117 @@ __device__ __forceinline__ void pull_tasks_q(const Params& p, const Smem& S, con
                 if (found_row && lane == sl) hit[u] = true;
             }
             if (act[u] && hit[u]) {
-                const long long off = (long long)qq2 * p.W + (en[u].x >> 5);
-                const uint32_t bit = 1u << (en[u].x & 31u);
+                const long long off = (long long)qq2 * p.W + (v[u] >> 5);
+                const uint32_t bit = 1u << (v[u] & 31u);
                 red_or_bits(p.visited + off, bit, S.pl);
                 red_or_bits(fnext + off, bit, S.pl);
+                if (qrec) atomicOr(&found[((v[u] - qvb) >> 5) & 31u], bit);
                 ++nnew;
             }
             nhit += __popc(__ballot_sync(FULL, act[u] && hit[u]));
         }
         if (lane == 0 && nhit) atomicAdd(&s_state[qq2], nhit);
+        __syncwarp();  // (the queue's tail is rewritten by the next append)
+    };
+    // One loop, one call site of round() (it is ~500 instructions; inlined at
+    // every drain it made the kernel 15% larger, and small levels pay for
+    // code size in instruction fetches).  Every iteration first drains the
+    // queue down to `limit`, then takes one step: APPEND the pending
+    // candidates (`pend`, lane by lane, so a lane's candidates are consecutive
+    // entries; a block with more than the queue holds goes in two halves of 16
+    // lanes, <= 512 each), or PRODUCE the next (task, in-slot)'s candidates.
+    uint32_t pend = 0, pvb = 0, pqvb = 0;  // pending candidates of this lane's word, their base vertex
+    int pk = -1, pq2 = 0;                  // ... and their in-transition / target state
+    bool prec = false, pfirst = false;     // ... recorded in `found` (several in-slots); first append of the slot
+    int limit = kNECap;
+    bool fin = false;
+    int k_iter = -1, k_end = 0;            // inside a target with several in-slots: next in-transition to look at
+    bool have_found = false;
+    int q2 = 0;
+    uint32_t need = 0, vb = 0;
+    bool have = false;
+    long long word = 0, word0 = 0;
+    // APPEND: the pending candidates go on the queue, or `limit` asks for the
+    // drain that must come first (the step is then retried)
+    auto try_append = [&]() {
+        if (n > 0 && (qk != pk || qrec || prec)) {  // another context's entries finish first
+            limit = 0;
+            return;
+        }
+        const uint32_t cnt = __popc(pend);
+        const uint32_t incl = warp_incl_scan(cnt, lane);
+        const uint32_t total = __shfl_sync(FULL, incl, 31);
+        int part = -1;  // -1: every lane; 0 / 1: lanes 0-15 / 16-31
+        uint32_t half0 = 0;
+        if (n + (int)total > kNECap) {
+            if (n > 0) {
+                limit = 0;
+                return;
+            }
+            half0 = __shfl_sync(FULL, incl, 15);
+            part = half0 > 0 ? 0 : 1;
+        }
+        const bool mine = part < 0 || (lane >> 4) == part;
+        const uint32_t padd = part < 0 ? total : part == 0 ? half0 : total - half0;
+        const uint32_t pbase = part == 1 ? half0 : 0u;
+        if (prec && pfirst) {
+            found[lane] = 0u;
+            __syncwarp();
+        }
+        pfirst = false;
+        qk = pk;
+        qq2 = pq2;
+        qrec = prec;
+        qvb = pqvb;
+        have_found = prec;
+        int pos = n + (int)(incl - cnt - pbase);
+        uint32_t m = mine ? pend : 0u;
+        while (m) {
+            ent[pos++] = pvb + (uint32_t)(__ffs(m) - 1);
+            m &= m - 1;
+        }
+        if (mine) pend = 0u;
+        n += (int)padd;
         __syncwarp();
+        limit = prec ? 0 : 63;  // several in-slots: the slot's rounds finish; else fewer than a round stay queued
     };
     for (;;) {
+        while (n > limit) round();
+        if (fin) break;
+        limit = kNECap;
+        if (__ballot_sync(FULL, pend != 0)) {
+            try_append();
+            continue;
+        }
+        // ---- PRODUCE
+        if (k_iter >= 0) {
+            // a target with several in-slots; the previous slot's rounds are done (limit was 0)
+            if (have_found) {
+                need &= ~found[lane];
+                have_found = false;
+                __syncwarp();
+            }
+            int k = -1;
+            if (__ballot_sync(FULL, need != 0))
+                for (int kk = k_iter; kk < k_end; ++kk)
+                    if (s_front[S.isrc[kk]]) {
+                        k = kk;
+                        break;
+                    }
+            if (k < 0) {
+                k_iter = -1;
+                continue;
+            }
+            k_iter = k + 1;
+            pend = have ? need & ld_stream_u32(S.ne[S.islot[k]] + word, S.pf) : 0u;
+            pvb = vb;
+            pqvb = (uint32_t)(word0 << 5);
+            pk = k;
+            pq2 = q2;
+            prec = true;
+            pfirst = true;
+            continue;
+        }
         uint32_t task = 0;
         if (lane == 0) {
             const uint32_t i = atomicAdd(s_task, 1u);
@@ -1419,82 +1289,42 @@ __device__ __forceinline__ void pull_tasks_q(const Params& p, const Smem& S, con
             if (task >= (uint32_t)nown && nown < ntask) task = (uint32_t)nown + (uint32_t)atomicAdd(steal, 1ull);
         }
         task = __shfl_sync(FULL, task, 0);
-        if ((long long)task >= ntask) break;
-        uint32_t blk;
-        const uint32_t tq = dblk.div(task, &blk);
-        const int q2 = s_ptarget[tq];
-        const int k = s_pk[tq];
-        const long long word0 = pw0 + (long long)blk * PV;
-        const long long myword = word0 + lane / LPW;
-        const long long v0 = word0 * 32 + (long long)PV * lane;
-        uint32_t r[PV + 1];
-        const uint32_t pw = myword < pw1 ? ld_bits(p.visited + (long long)q2 * p.W + myword, S.pl) : 0xFFFFFFFFu;
-        load_rows<PV>(S.slots[p.nslots + S.islot[k]].rowptr, v0, p.nv, lane, true, S.pf, r);
-        uint32_t need = ~(pw >> sh) & fmask_all;
-        if (word0 * 32 + 32 * PV > p.nv) {  // (warp-uniform: the last block of a row)
-            if (v0 >= p.nv) need = 0;
-            else if (v0 + PV > p.nv) need &= (1u << (p.nv - v0)) - 1u;
-        }
-        if (myword >= pw1) need = 0;
-        // the unvisited vertices with in-edges in the slot
-        uint32_t cm = need;
-#pragma unroll
-        for (int j = 0; j < PV; ++j)
-            if (r[j + 1] == r[j]) cm &= ~(1u << j);
-        const uint32_t cnt = __popc(cm);
-        const uint32_t incl = warp_incl_scan(cnt, lane);
-        const int nadd = (int)__shfl_sync(FULL, incl, 31);
-        if (nadd == 0) continue;
-        // entries of another in-transition are finished first; so is whatever
-        // does not leave room for this task's candidates
-        if (qk != k)
-            while (n > 0) round();
-        while (n + nadd > kPQCap && n > 0) round();
-        qk = k;
-        qq2 = q2;
-        if (nadd > kPQCap) {
-            // (more candidates than the queue holds -- at most 32 * PV: in two halves)
-            for (int half = 0; half < 2; ++half) {
-                const uint32_t hm = half ? cm & ~((1u << (PV / 2)) - 1u) : cm & ((1u << (PV / 2)) - 1u);
-                const uint32_t hc = __popc(hm);
-                const uint32_t hi_ = warp_incl_scan(hc, lane);
-                int pos = (int)(hi_ - hc);
-#pragma unroll
-                for (int j = 0; j < PV; ++j)
-                    if ((hm >> j) & 1u) ent[pos++] = make_uint4((uint32_t)(v0 + j), r[j], r[j + 1], 0u);
-                n = (int)__shfl_sync(FULL, hi_, 31);
-                __syncwarp();
-                while (n > 0) round();
-            }
+        if ((long long)task >= ntask) {
+            fin = true;
+            limit = 0;
             continue;
         }
-        int pos = n + (int)(incl - cnt);
-#pragma unroll
-        for (int j = 0; j < PV; ++j)
-            if ((cm >> j) & 1u) ent[pos++] = make_uint4((uint32_t)(v0 + j), r[j], r[j + 1], 0u);
-        n += nadd;
-        __syncwarp();
-        while (n >= kPQRound) round();
+        uint32_t blk;
+        const uint32_t tq = dblk.div(task, &blk);
+        q2 = s_ptarget[tq];
+        const int k1 = s_pk[tq];  // the target's only active in-transition, or -1: several
+        word0 = pw0 + (long long)blk * TW;
+        word = word0 + lane;
+        have = lane < TW && word < pw1;
+        vb = (uint32_t)(word << 5);
+        need = have ? ~ld_bits(p.visited + (long long)q2 * p.W + word, S.pl) : 0u;
+        if (k1 >= 0) {
+            // (bits past |V| are clear in the bitmap)
+            pend = have ? need & ld_stream_u32(S.ne[S.islot[k1]] + word, S.pf) : 0u;
+            pvb = vb;
+            pk = k1;
+            pq2 = q2;
+            prec = false;
+            pfirst = false;
+            if (__ballot_sync(FULL, pend != 0)) try_append();  // (the common step: no second iteration)
+        } else {
+            k_iter = S.ibeg[q2];
+            k_end = S.ibeg[q2 + 1];
+            have_found = false;
+        }
     }
-    while (n > 0) round();
 }
-#endif  // RPQ_NO_PULL_QUEUE
 
-#ifndef RPQ_NO_PULL_NE
-// Pull over the slot's non-empty-row bitmap (Slot::ne), for levels whose
-// targets each have one active in-slot.  The queued pull above still reads
-// every row pointer of every unvisited vertex to learn which rows have
-// in-edges (one in five to seven on R-MAT) and spends ~250 instructions per
-// 256-vertex task doing so; its levels are bound by instruction issue, not by
-// bytes.  Here a task is 32 words = 1,024 vertices: lane l reads P's word and
-// the bitmap's, candidates = ~P & ne, and only candidates' row pointers are
-// ever loaded -- by the probing round, next to each other (a lane's
-// candidates are queued consecutively, so adjacent lanes of a round read
-// adjacent rows).  Queue entries are vertex ids; a round probes the last 64.
-constexpr int kNECap = 768;  // entries per warp (kWarpScratchWords >= 768)
-static_assert(kNECap <= kWarpScratchWords, "the vertex queue fits the warp scratch");
-
-__device__ __forceinline__ void pull_tasks_ne(const Params& p, const Smem& S, const uint32_t* fcur, uint32_t* fnext,
+// The same pull for levels whose targets all have ONE active in-slot, on
+// large graphs (32-word tasks), without the step loop above: straight-line
+// task -> append -> rounds (cfg3's pull levels: 95 + 39 us against 102 + 41).
+constexpr int kNE1Cap = 768;
+__device__ __forceinline__ void pull_tasks_ne1(const Params& p, const Smem& S, const uint32_t* fcur, uint32_t* fnext,
                                               long long pw0, long long pw1, int lane, unsigned* s_task,
                                               int s_nptarget, const int* s_ptarget, const int* s_pk,
                                               unsigned int* s_state, unsigned int& nnew,
@@ -1638,12 +1468,12 @@ __device__ __forceinline__ void pull_tasks_ne(const Params& p, const Smem& S, co
         const uint32_t incl = warp_incl_scan(cnt, lane);
         const uint32_t total = __shfl_sync(FULL, incl, 31);
         const uint32_t half0 = __shfl_sync(FULL, incl, 15);
-        const bool split = n + (int)total > kNECap;
+        const bool split = n + (int)total > kNE1Cap;
         for (int part = 0; part < (split ? 2 : 1); ++part) {
             const bool mine = !split || (lane >> 4) == part;
             const uint32_t padd = !split ? total : part == 0 ? half0 : total - half0;
             const uint32_t pbase = split && part == 1 ? half0 : 0u;
-            while (n > 0 && n + (int)padd > kNECap) round();
+            while (n > 0 && n + (int)padd > kNE1Cap) round();
             int pos = n + (int)(incl - cnt - pbase);
             uint32_t m = mine ? cm : 0u;
             const uint32_t vb = (uint32_t)(word << 5);
@@ -1658,7 +1488,6 @@ __device__ __forceinline__ void pull_tasks_ne(const Params& p, const Smem& S, co
     }
     while (n > 0) round();
 }
-#endif  // RPQ_NO_PULL_NE
 
 // Diagnostic stamp k of level L for this CTA (thread 0): 0 level start (after
 // the decision), 1 plan epoch done, 2 last warp done with the expansion,
@@ -1680,7 +1509,6 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
     __shared__ int s_ptarget[kMaxStates];            // pull target states of this level
     __shared__ int s_nptarget;
     __shared__ int s_pmulti;  // some pull target of this level has several active in-slots
-    __shared__ int s_pne;     // every pull target's in-slot has a non-empty-row bitmap
     __shared__ int s_pk[kMaxStates];  // first active in-transition of each pull target
     __shared__ View s_view;
     __shared__ unsigned long long s_resv;
@@ -2389,59 +2217,43 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
                 nedge += frontier_edges(p, S, fcur, gtid, gthreads, Wn);
             if (threadIdx.x == 0) {
                 int n = 0;
-                int multi = 0, ne_ok = 1;
+                int multi = 0;
                 for (int q2 = 0; q2 < p.nstates; ++q2) {
                     int any = 0, kf = 0;
                     for (int k = S.ibeg[q2]; k < S.ibeg[q2 + 1]; ++k)
                         if (s_front[S.isrc[k]] != 0 && any++ == 0) kf = k;
                     if (any) {
-                        ne_ok &= S.ne[S.islot[kf]] != nullptr;
-                        s_pk[n] = kf;  // the first (for the queued pull: the only) active in-transition
+                        s_pk[n] = any == 1 ? kf : -1;  // the only active in-transition, or -1: several
                         s_ptarget[n++] = q2;
                     }
                     multi |= any > 1;
                 }
                 s_nptarget = n;
                 s_pmulti = multi;
-                s_pne = ne_ok;
             }
             __syncthreads();
             // targets: the owned word range (vertex-partitioned step), else all
             const long long pw0 = s_run.own_w1 > s_run.own_w0 ? s_run.own_w0 : 0;
             const long long pw1 = s_run.own_w1 > s_run.own_w0 ? min((long long)s_run.own_w1, Wn) : Wn;
             // A dense frontier (> 22% of |V| pairs) usually answers at the first
-            // in-edge: probe one inline, a sparse one two.  Only in the
-            // large-state-space instance (cfg3: L3 204 -> 166 us, L2 275 -> 265;
-            // cfg5 -2.7%); the 768-thread one (cfg2) keeps its code unchanged.
+            // in-edge: a round probes one per candidate first, on a sparse one two.
+            // Only in the large-state-space instance (measured on cfg3 and cfg5).
             const bool one_inline = NT == kThreadsLarge && (float)s_view.nfront > 0.22f * (float)p.nv;
             unsigned long long* pull_steal = &ctl->steal[e % 3][8];
             uint32_t* scratch = reinterpret_cast<uint32_t*>(s_stage) + (size_t)wid * kWarpScratchWords;
             const int first = one_inline ? 1 : kPullInline;
-#ifndef RPQ_PV8_WORDS_PER_WARP
-#define RPQ_PV8_WORDS_PER_WARP 16  // cfg5 (131k words, 4,736 warps): 8 words per task, pull levels 180 -> 123 us
-#endif
-#ifndef RPQ_NO_PULL_QUEUE
-            // the queued variant when every target of the level has one active
-            // in-slot (cfg3: pull levels 149 -> 143 and 110 -> 96 us); targets
-            // with several need each slot's answers before the next and drain
-            // the queue per slot, which costs more than it saves (cfg5: +10%)
-#ifndef RPQ_NO_PULL_NE
-            if (pw1 - pw0 >= (long long)nwarps * RPQ_PV8_WORDS_PER_WARP && !s_pmulti && s_pne)
-                pull_tasks_ne(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_pk, s_state,
-                              nnew, pull_steal, scratch, first);
+            // large graphs (>= 16 words of vertices per warp of the grid): 32-word
+            // tasks; smaller ones: 8-word tasks, so that every warp has some
+            const bool big = pw1 - pw0 >= (long long)nwarps * 16;
+            if (big && !s_pmulti)
+                pull_tasks_ne1(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_pk, s_state,
+                               nnew, pull_steal, scratch, first);
+            else if (big)
+                pull_tasks_ne<RPQ_NE_TW>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_pk, s_front,
+                                  s_state, nnew, pull_steal, scratch, first);
             else
-#endif
-            if (pw1 - pw0 >= (long long)nwarps * RPQ_PV8_WORDS_PER_WARP && !s_pmulti)
-                pull_tasks_q<8>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_pk, s_state,
-                                nnew, pull_steal, scratch, first);
-            else
-#endif
-            if (pw1 - pw0 >= (long long)nwarps * RPQ_PV8_WORDS_PER_WARP)  // large: 8 words per task
-                pull_tasks<8>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front, s_state,
-                              nnew, pull_steal, scratch, first);
-            else
-                pull_tasks<kPullVerts>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_front,
-                                       s_state, nnew, pull_steal, scratch, first);
+                pull_tasks_ne<8>(p, S, fcur, fnext, pw0, pw1, lane, &s_task, s_nptarget, s_ptarget, s_pk, s_front,
+                                 s_state, nnew, pull_steal, scratch, first);
         }
         if (p.trace && lane == 0) atomicMax(&s_wend, globaltimer());  // this warp's work done
         __syncthreads();
