@@ -283,6 +283,20 @@ RPQ_API int rpq_query_copy_batch_bits(rpq_query* q, uint32_t* host_words, int64_
 /* Device pointer to the same bitmaps (RPQ_BATCH rows of *row_words words). */
 RPQ_API int rpq_query_batch_bits_device(rpq_query* q, uint32_t** d_bits, int64_t* row_words);
 
+/* eval_ssr for automata beyond the persistent kernel's table limits (more than
+ * 256 states or (state, symbol) groups, more than 128 distinct symbols): the
+ * reference's masked loop (rpq/engine.py:146-171; it iterates N.alphabet and
+ * has no such limit) as one device push step per level over the transition
+ * list in global memory.  Same answer (packed: bit v%32 of word v/32, nwords >=
+ * ceil(nv/32)) and the same iteration count; stats carries iterations,
+ * visited_pairs, te, reach_count and the per-level counts.  One-shot:
+ * workspaces are allocated and freed inside the call. */
+RPQ_API int rpq_ssr_wide(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_t* t_src,
+                         const int32_t* t_label, const uint8_t* t_inv, const int32_t* t_dst,
+                         int32_t nstarts, const int32_t* starts, int32_t nfinals, const int32_t* finals,
+                         int32_t source, double timeout_s, uint32_t* out_bits, int64_t nwords,
+                         rpq_stats* stats);
+
 /* One-shot eval_ssr. */
 RPQ_API int rpq_ssr(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_t* t_src,
             const int32_t* t_label, const uint8_t* t_inv, const int32_t* t_dst,

@@ -180,7 +180,15 @@ ENGINE_SIGNATURES = {
     "rpq_query_batch_bits_device": (c_i32, [c_vp, ctypes.POINTER(P_u32), P_i64]),
     "rpq_ssr": (c_i32, [c_vp, c_i32, c_i32, P_i32, P_i32, P_u8, P_i32, c_i32, P_i32, c_i32, P_i32,
                         c_i32, c_dbl, P_u8, ctypes.POINTER(RpqStats)]),
+    "rpq_ssr_wide": (c_i32, [c_vp, c_i32, c_i32, P_i32, P_i32, P_u8, P_i32, c_i32, P_i32, c_i32, P_i32,
+                             c_i32, c_dbl, P_u32, c_i64, ctypes.POINTER(RpqStats)]),
 }
+
+# table limits of the persistent kernel (csrc/ssr_kernel.cuh kMaxStates / kMaxGroups /
+# kMaxSlots); automata beyond them run through rpq_ssr_wide
+MAX_STATES = 256
+MAX_GROUPS = 256
+MAX_SLOTS = 128
 
 DATAGEN_SIGNATURES = {
     "rpqgen_draw": (c_u64, [c_u64, c_u64, c_u64]),

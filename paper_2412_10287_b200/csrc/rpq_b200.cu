@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 #include <map>
 #include <mutex>
 #include <set>
@@ -23,6 +24,7 @@
 #include "ssr_kernel.cuh"
 #include "batch_kernel.cuh"
 #include "small_kernel.cuh"
+#include "wide_kernel.cuh"
 #include "ingest.cuh"
 
 using namespace rpqk;
@@ -1791,6 +1793,136 @@ int rpq_query_destroy(rpq_query* q) {
     if (q->ran && q->last_stream) cudaStreamSynchronize(q->last_stream);
     free_query_buffers(q);
     delete q;
+    return RPQ_OK;
+}
+
+int rpq_ssr_wide(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_t* t_src,
+                 const int32_t* t_label, const uint8_t* t_inv, const int32_t* t_dst, int32_t nstarts,
+                 const int32_t* starts, int32_t nfinals, const int32_t* finals, int32_t source,
+                 double timeout_s, uint32_t* out_bits, int64_t nwords, rpq_stats* stats) {
+    if (!g) return fail(RPQ_EINVAL, "null graph");
+    if (nstates < 1) return fail(RPQ_EINVAL, "nstates must be >= 1");
+    if (ntrans < 0 || nstarts < 0 || nfinals < 0) return fail(RPQ_EINVAL, "negative count");
+    if ((ntrans && (!t_src || !t_label || !t_inv || !t_dst)) || (nstarts && !starts) || (nfinals && !finals))
+        return fail(RPQ_EINVAL, "null automaton array");
+    if (source < 0 || source >= g->nv)
+        return fail(RPQ_ERANGE, "vertex index " + std::to_string(source) + " out of range");
+    const long long Wn = ((long long)g->nv + 31) / 32;
+    if (out_bits && nwords < Wn) return fail(RPQ_EINVAL, "answer buffer too small");
+    const auto t0 = std::chrono::steady_clock::now();
+    auto elapsed = [&]() { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    std::vector<WideTrans> tr;
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        if (cudaSetDevice(g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+        for (int i = 0; i < ntrans; ++i) {
+            if (t_src[i] < 0 || t_src[i] >= nstates || t_dst[i] < 0 || t_dst[i] >= nstates)
+                return fail(RPQ_EINVAL, "transition state out of range");
+            if (t_label[i] < 0) return fail(RPQ_EINVAL, "negative label index");
+            if (t_label[i] >= g->nl) continue;  // engine.py:100-101
+            const int rc = materialize_label(g, t_label[i]);
+            if (rc != RPQ_OK) return rc;
+            const LabelDev& L = g->labels[t_label[i]];
+            const int d = t_inv[i] ? 1 : 0;
+            if (L.nnz[d] == 0) continue;
+            tr.push_back(WideTrans{L.rowptr[d], L.col[d], t_src[i], t_dst[i]});
+        }
+    }
+    for (int i = 0; i < nstarts; ++i)
+        if (starts[i] < 0 || starts[i] >= nstates) return fail(RPQ_EINVAL, "start state out of range");
+    for (int i = 0; i < nfinals; ++i)
+        if (finals[i] < 0 || finals[i] >= nstates) return fail(RPQ_EINVAL, "final state out of range");
+    const long long W = (Wn + 3) / 4 * 4;
+    const size_t bitmap_bytes = (size_t)W * nstates * sizeof(uint32_t);
+    WideTrans* d_tr = nullptr;
+    uint32_t *d_p = nullptr, *d_f[2] = {nullptr, nullptr}, *d_out = nullptr;
+    unsigned int* d_cnt[2] = {nullptr, nullptr};
+    unsigned long long* d_tot = nullptr;
+    int32_t *d_starts = nullptr, *d_finals = nullptr;
+    auto cleanup = [&]() {
+        cudaFree(d_tr); cudaFree(d_p); cudaFree(d_f[0]); cudaFree(d_f[1]); cudaFree(d_out);
+        cudaFree(d_cnt[0]); cudaFree(d_cnt[1]); cudaFree(d_tot); cudaFree(d_starts); cudaFree(d_finals);
+    };
+#define WTRY(expr)                                   \
+    do {                                             \
+        cudaError_t e_ = (expr);                     \
+        if (e_ != cudaSuccess) {                     \
+            cleanup();                               \
+            return cuda_fail(e_, #expr);             \
+        }                                            \
+    } while (0)
+    WTRY(cudaMalloc(&d_tr, std::max<size_t>(tr.size(), 1) * sizeof(WideTrans)));
+    WTRY(cudaMalloc(&d_p, bitmap_bytes));
+    for (int f = 0; f < 2; ++f) {
+        WTRY(cudaMalloc(&d_f[f], bitmap_bytes));
+        WTRY(cudaMalloc(&d_cnt[f], (size_t)nstates * sizeof(unsigned int)));
+    }
+    WTRY(cudaMalloc(&d_out, (size_t)W * sizeof(uint32_t)));
+    WTRY(cudaMalloc(&d_tot, 3 * sizeof(unsigned long long)));
+    WTRY(cudaMalloc(&d_starts, std::max<size_t>(nstarts, 1) * sizeof(int32_t)));
+    WTRY(cudaMalloc(&d_finals, std::max<size_t>(nfinals, 1) * sizeof(int32_t)));
+    if (!tr.empty()) WTRY(cudaMemcpy(d_tr, tr.data(), tr.size() * sizeof(WideTrans), cudaMemcpyHostToDevice));
+    if (nstarts) WTRY(cudaMemcpy(d_starts, starts, (size_t)nstarts * sizeof(int32_t), cudaMemcpyHostToDevice));
+    if (nfinals) WTRY(cudaMemcpy(d_finals, finals, (size_t)nfinals * sizeof(int32_t), cudaMemcpyHostToDevice));
+    WTRY(cudaMemset(d_p, 0, bitmap_bytes));
+    WTRY(cudaMemset(d_f[0], 0, bitmap_bytes));
+    WTRY(cudaMemset(d_cnt[0], 0, (size_t)nstates * sizeof(unsigned int)));
+    WTRY(cudaMemset(d_tot, 0, 3 * sizeof(unsigned long long)));
+    unsigned long long tot[3] = {0, 0, 0};
+    unsigned long long pairs = 0, te = 0;
+    int iterations = 0, status = RPQ_OK;
+    rpq_stats st{};
+    if (nstarts) {
+        wide_seed_kernel<<<1, 256>>>(d_starts, nstarts, source, W, d_p, d_f[0], d_cnt[0], d_tot);
+        WTRY(cudaMemcpy(tot, d_tot, sizeof(tot), cudaMemcpyDeviceToHost));
+    }
+    unsigned long long nfront = tot[0];
+    pairs = nfront;
+    if (stats) st.level_new[0] = (int64_t)nfront;
+    // the masked loop (engine.py:156-160): while M: check the clock; step; count
+    for (int L = 0; nfront > 0; ++L) {
+        if (timeout_s >= 0 && elapsed() > timeout_s) {
+            status = RPQ_ETIMEOUT;
+            break;
+        }
+        const int cur = L & 1, nxt = cur ^ 1;
+        WTRY(cudaMemsetAsync(d_f[nxt], 0, bitmap_bytes));
+        WTRY(cudaMemsetAsync(d_cnt[nxt], 0, (size_t)nstates * sizeof(unsigned int)));
+        WTRY(cudaMemsetAsync(d_tot, 0, 2 * sizeof(unsigned long long)));
+        wide_step_kernel<<<4 * g->sm_count, 256>>>(d_tr, (int)tr.size(), d_p, d_f[cur], d_f[nxt], W, g->nv,
+                                                  d_cnt[cur], d_cnt[nxt], d_tot);
+        WTRY(cudaGetLastError());
+        WTRY(cudaMemcpy(tot, d_tot, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        ++iterations;
+        nfront = tot[0];
+        pairs += nfront;
+        te += tot[1];
+        if (stats && L + 1 < RPQ_STATS_LEVELS) {
+            st.level_new[L + 1] = (int64_t)nfront;
+            st.level_edges[L] = (int64_t)tot[1];
+        }
+    }
+    if (status == RPQ_OK) {
+        WTRY(cudaMemsetAsync(d_tot + 2, 0, sizeof(unsigned long long)));
+        wide_project_kernel<<<4 * g->sm_count, 256>>>(d_finals, nfinals, d_p, W, Wn, d_out, d_tot);
+        WTRY(cudaGetLastError());
+        WTRY(cudaMemcpy(tot + 2, d_tot + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        if (out_bits) WTRY(cudaMemcpy(out_bits, d_out, (size_t)Wn * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    }
+#undef WTRY
+    cleanup();
+    if (stats) {
+        st.status = status;
+        st.iterations = iterations;
+        st.levels = iterations > 0 ? iterations - 1 : 0;
+        st.grid = 4 * g->sm_count;
+        st.te = (int64_t)te;
+        st.visited_pairs = (int64_t)pairs;
+        st.reach_count = (int64_t)tot[2];
+        st.device_ms = (float)(elapsed() * 1e3);
+        *stats = st;
+    }
+    if (status == RPQ_ETIMEOUT) return fail(RPQ_ETIMEOUT, "query timed out");
     return RPQ_OK;
 }
 

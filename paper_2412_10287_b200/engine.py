@@ -300,6 +300,47 @@ def _thread_stats():
     return st
 
 
+def _is_wide(table):
+    """True when the automaton exceeds the persistent kernel's table limits
+    (more than 256 states or (state, symbol) groups, more than 128 symbols).
+    The reference has no such limit (engine.py:99-102 iterates N.alphabet)."""
+    if table.nstates > _lib.MAX_STATES:
+        return True
+    if table.t_src.size <= _lib.MAX_SLOTS:
+        return False
+    sym = table.t_label.astype(np.int64) * 2 + table.t_inv
+    if np.unique(sym).size > _lib.MAX_SLOTS:
+        return True
+    return np.unique(table.t_src.astype(np.int64) * (2 << 32) + sym).size > _lib.MAX_GROUPS
+
+
+def _run_wide(g, dg, table, source, opts, tag, t0, want_stats):
+    """eval_ssr for automata beyond the kernel tables: rpq_ssr_wide, one device
+    push step per level over the transition list (same answer, same counts)."""
+    lib = _lib.engine()
+    remaining = opts.timeout - (time.monotonic() - t0)
+    first_check = not (tag == "masked" and table.starts.size == 0)
+    if first_check and (remaining < 0 or opts.timeout <= 0):
+        raise QueryTimeout(time.monotonic() - t0, 0)
+    budget = -1.0 if math.isinf(remaining) else max(remaining, 0.0)
+    nwords = (g.num_vertices + 31) // 32
+    words = np.zeros(max(nwords, 1), dtype=np.uint32)
+    stats = _lib.RpqStats()
+    rc = lib.rpq_ssr_wide(dg.handle, table.nstates, table.t_src.size, _lib.ptr(table.t_src, ctypes.c_int32),
+                          _lib.ptr(table.t_label, ctypes.c_int32), _lib.ptr(table.t_inv, ctypes.c_uint8),
+                          _lib.ptr(table.t_dst, ctypes.c_int32), table.starts.size,
+                          _lib.ptr(table.starts, ctypes.c_int32), table.finals.size,
+                          _lib.ptr(table.finals, ctypes.c_int32), int(source), budget,
+                          _lib.ptr(words, ctypes.c_uint32), words.size, ctypes.byref(stats))
+    if rc == _lib.RPQ_ETIMEOUT:
+        raise QueryTimeout(time.monotonic() - t0, _iterations_for(tag, stats.iterations, table.starts.size))
+    raise_for_status(rc, "rpq_ssr_wide")
+    iterations = _iterations_for(tag, stats.iterations, table.starts.size)
+    return EvalResult(None, iterations, time.monotonic() - t0, tag,
+                      stats.to_dict() if want_stats or opts.debug_checks or opts.count_te else None,
+                      bits=words[:nwords], nv=g.num_vertices, pairs=None, count=int(stats.reach_count))
+
+
 def _run(g, n, source, opts, tag, *, want_stats=False):
     opts.validate()
     _check_vertex(g, source)
@@ -307,6 +348,8 @@ def _run(g, n, source, opts, tag, *, want_stats=False):
     dg = device_graph(g, opts.device)
     table = _table_for(n, g.num_labels)
     dg.ensure_labels(table.labels)
+    if _is_wide(table):
+        return _run_wide(g, dg, table, source, opts, tag, t0, want_stats)
     lib = _lib.engine()
     q = dg.acquire_query(table)
     try:
