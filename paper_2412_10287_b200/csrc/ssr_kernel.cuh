@@ -18,7 +18,8 @@
 //                     by the warp that discovers a pair (sharded counters).
 //
 // Per level the direction is push (expand the queue) or pull (every
-// unvisited (q', w) scans A_s^T row w for a frontier member of the source
+// unvisited (q', w) whose row w of A_s^T is non-empty -- read off a bitmap per
+// slot, Params::ne_tab -- scans that row for a frontier member of the source
 // state, early exit), chosen from the frontier's edge count against the
 // unvisited edge estimate (Beamer's rule).  Either way the result is the
 // same set: P only grows by (q', w) pairs with a frontier predecessor.
@@ -599,9 +600,11 @@ __device__ __forceinline__ uint32_t emit_pairs(const Params& p, const Smem& S, c
 // whole bundle (stage_put, <= 31 + 32 x kEdgesPerLane) and drains it once, so
 // its body holds one inlined emission instead of one per unrolled edge slot.
 constexpr int kStageCap = 32 * kEdgesPerLane + 32;
-// Per-warp dynamic shared memory: the push emission stage, or (pull epochs)
-// the candidate list of pull_tasks<8>: 3 x 256 words + 8 found words.
-constexpr int kWarpScratchWords = (2 * kStageCap > 3 * 32 * 8 + 8) ? 2 * kStageCap : 3 * 32 * 8 + 8;
+// Per-warp dynamic shared memory: the push emission stage (with the warp's
+// share of the claim cache behind it), or (pull epochs) the
+// candidate queue: 768 vertex ids (736 + 32 found words in the step-loop variant).
+constexpr int kWarpScratchWords = 776;
+static_assert(kWarpScratchWords >= 2 * kStageCap, "the emission stage fits the warp scratch");
 __host__ __device__ constexpr size_t kStageBytes(int nthreads) {
     return (size_t)(nthreads / 32) * kWarpScratchWords * 4;
 }

@@ -236,3 +236,31 @@ def test_answer_set_view_matches_the_reference_set():
     pairs = np.stack([words.astype(np.uint32), bits[words]], axis=1).reshape(-1)
     r = EvalResult(None, 3, 0.0, "hybrid", nv=nv, pairs=pairs)
     assert r.answer_set == want and r.reachable == want and np.array_equal(r.reach, reach)
+
+
+def test_wide_automata_are_routed_past_the_table_limits():
+    """engine._is_wide mirrors rpq_query_create's limits (csrc/ssr_kernel.cuh
+    kMaxStates / kMaxGroups / kMaxSlots): such automata go to rpq_ssr_wide
+    instead of raising (the reference evaluates any automaton)."""
+    import re
+
+    from paper_2412_10287_b200 import _lib, engine
+    from paper_2412_10287_b200.automaton import TransitionTable
+
+    src = open(os.path.join(ROOT, "paper_2412_10287_b200", "csrc", "ssr_kernel.cuh")).read()
+    for name, val in (("kMaxStates", _lib.MAX_STATES), ("kMaxGroups", _lib.MAX_GROUPS), ("kMaxSlots", _lib.MAX_SLOTS)):
+        assert int(re.search(rf"constexpr int {name} = (\d+);", src).group(1)) == val
+
+    def table(nstates, trans):
+        s, l, i, d = (np.array(x) for x in zip(*trans)) if trans else ([], [], [], [])
+        return TransitionTable(nstates, s, l, i, d, [0], [0])
+
+    assert not engine._is_wide(table(3, [(0, 0, 0, 1), (1, 1, 1, 2)]))
+    assert not engine._is_wide(table(256, [(q, 0, 0, (q + 1) % 256) for q in range(256)]))
+    assert engine._is_wide(table(257, [(0, 0, 0, 1)]))
+    # 129 symbols (label, inverted) on 2 states
+    assert engine._is_wide(table(2, [(0, l // 2, l % 2, 1) for l in range(129)]))
+    assert not engine._is_wide(table(2, [(0, l // 2, l % 2, 1) for l in range(128)]))
+    # 257 (state, symbol) groups on 129 states x 2 symbols
+    assert engine._is_wide(table(129, [(q, 0, i, q) for q in range(129) for i in (0, 1)][:257]))
+    assert not engine._is_wide(table(129, [(q, 0, i, q) for q in range(129) for i in (0, 1)][:256]))
