@@ -309,12 +309,14 @@ def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, s
     for sh in shards:
         sh.p.zero_()
     # seed M = P = {(q_s, source)} (engine.py:106-109, :154-155); P on its owner
+    # (m and p are zero here: a fill of the one word is the OR, without the
+    # gather / scatter kernels of an indexed update)
     sw, sb = source >> 5, _bit(source)
-    for q in starts:
-        m[q, sw] |= sb
+    for q in set(starts):
+        m[q, sw: sw + 1].fill_(sb)
         for sh in shards:
             if sh.w0 <= sw < sh.w1:
-                sh.p[q, sw] |= sb
+                sh.p[q, sw: sw + 1].fill_(sb)
     counted = hasattr(shards[0].step, "count")
     if counted:
         for sh in shards:
@@ -333,7 +335,9 @@ def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, s
             from .engine import QueryTimeout
 
             raise QueryTimeout(time.monotonic() - t0, iterations)
-        for _ in range(depth):
+        # (the first check after two levels: a source without a matching
+        # out-edge -- half of cfg3's -- is done after its first step)
+        for _ in range(min(depth, 2) if enqueued == 0 else depth):
             for sh in shards:
                 sh.step(m, sh.p, sh.next, stream)
             enqueued += 1
@@ -366,27 +370,34 @@ def _run_levels(shards, exchange, ranges, nv, starts, finals, source, timeout, s
     slices = []
     for sh in shards:
         sl = torch.zeros((1, wmax), dtype=torch.int32, device=dev)
-        if finals:
-            acc = sh.p[list(finals), sh.w0: sh.w1]
-            acc = acc[0:1].clone() if acc.shape[0] == 1 else _or_rows(acc)
+        fl = sorted(set(finals))
+        if fl:
+            acc = sh.p[fl[0]: fl[0] + 1, sh.w0: sh.w1]
+            if len(fl) > 1:
+                acc = acc.clone()
+                for f in fl[1:]:
+                    acc |= sh.p[f: f + 1, sh.w0: sh.w1]
             sl[:, : sh.w1 - sh.w0] = acc
         slices.append(sl)
     gathered = exchange.allgather(slices)
     words = np.zeros(max(row_words, 1), dtype=np.uint32)
-    g_host = gathered.cpu().numpy().view(np.uint32)
+    if gathered.is_cuda:
+        # a pinned staging buffer, kept with the shard set (a pageable copy of
+        # cfg3's 2 MB answer costs more than the query's device time)
+        host = getattr(shards[0], "_host", None)
+        if host is None or host.shape != gathered.shape:
+            host = shards[0]._host = torch.empty(gathered.shape, dtype=gathered.dtype, pin_memory=True)
+        host.copy_(gathered, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        g_host = host.numpy().view(np.uint32)
+    else:
+        g_host = gathered.cpu().numpy().view(np.uint32)
     for r, (w0, w1) in enumerate(ranges):
         words[w0:w1] = g_host[r, 0, : w1 - w0]
     stats = {"levels_wall_us": levels_us, "ranges": ranges, "step_ms": step_ms, "enqueued": enqueued}
     if bits:
         return words, iterations, stats
     return np.unpackbits(words.view(np.uint8), bitorder="little")[:nv], iterations, stats
-
-
-def _or_rows(t):
-    acc = t[0:1].clone()
-    for i in range(1, t.shape[0]):
-        acc |= t[i:i + 1]
-    return acc
 
 
 class PartitionedQuery:
