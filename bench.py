@@ -476,6 +476,7 @@ def run_engine(args, rank, world, local_rank):
 
     # e2e through the public API: automaton H2D + kernel + answer D2H per call
     e2e_s, set_ms, e2e_dev_ms, d2h_answer, e2e_host_us, view_us = [], [], [], {}, [], []
+    host_answered = set()
     nwords = (sg.nv + 31) // 32
     if not args.profile:
         opts = P.EngineOptions(timeout=math.inf, direction=args.direction, alpha=alpha)
@@ -493,6 +494,8 @@ def run_engine(args, rank, world, local_rank):
                 t_step += dt
                 e2e_dev_ms.append(P.engine._thread_stats().device_ms)  # this call's device time
                 e2e_host_us.append(1e6 * dt - 1e3 * e2e_dev_ms[-1])
+                if k == 0 and P.engine._thread_stats().grid == 0:
+                    host_answered.add(s)  # no seed edge: answered without a launch
                 assert res.iterations == work[s]["iters"]
                 if s not in d2h_answer:  # bytes the answer took over PCIe: bitmap or (word, bits) pairs
                     nz = int(np.count_nonzero(res.bits))
@@ -575,9 +578,11 @@ def run_engine(args, rank, world, local_rank):
         "clocks": clocks,
     }
     if e2e_s:
+        nlaunched = nq - len(host_answered)
         out["e2e"] = {"value": units / e2e_max_s / 1e9, "unit": UNIT,
-                      "h2d_bytes_per_step": nq * (h2d + 4),
-                      "d2h_bytes_per_step": nq * d2h_ctl + sum(d2h_answer.get(s, 0) for s in sources),
+                      "h2d_bytes_per_step": nlaunched * (h2d + 4),
+                      "d2h_bytes_per_step": nlaunched * d2h_ctl + sum(d2h_answer.get(s, 0) for s in sources),
+                      "host_answered_queries_per_step": len(host_answered),
                       "latency_ms_median_per_query": 1e3 * statistics.median(e2e_s) / nq,
                       "device_ms_per_query": statistics.mean(e2e_dev_ms) if e2e_dev_ms else None,
                       "host_us_per_query": {"median": statistics.median(e2e_host_us),
@@ -587,7 +592,10 @@ def run_engine(args, rank, world, local_rank):
                       "note": ("eval_ssr per source with host buffers: automaton tables H2D, the answer D2H as "
                                "the bitmap or, when sparse, (word, bits) pairs; device_ms = the calls' own "
                                "CUDA-event time; reachable_set_ms = building the reference's set[int] from the "
-                               "answer, not in value")}
+                               "answer, not in value; host_answered_queries_per_step = sources none of whose "
+                               "seed rows has an edge (empty first step, engine.py:154-160): eval_ssr answers "
+                               "them from the host copy of the row bitmaps without a launch -- `value` still "
+                               "times a kernel for every source")}
     if world == 1 and not args.no_cpu_baseline and not args.profile:
         og, oq = oracle_setup(sg, nj)
         out["cpu_baseline"] = cpu_baseline(og, oq, sources, {s: work[s]["te"] for s in sources},

@@ -196,7 +196,12 @@ RPQ_API int rpq_query_wait(rpq_query* q, rpq_stats* stats);
 /* One evaluation, start to answer, in one call (the eval_ssr fast path):
  * rpq_query_set_options + small-kernel switch + run on the query's stream +
  * wait + the answer bitmap (ceil(nv/32) words; NULL/0 to keep it on the
- * device).  Returns the run's status; stats may be NULL. */
+ * device).  Returns the run's status; stats may be NULL.
+ * A source none of whose rows in the start states' symbols has an edge is
+ * answered on the host (the first step of the masked loop is empty,
+ * engine.py:154-160): no launch, stats->grid == 0.  Not when count_te is set
+ * or stats is NULL; accessors of device-side results (rpq_query_copy_visited,
+ * _copy_reach[_bits], _reach_device) run such a query on the device first. */
 RPQ_API int rpq_query_eval(rpq_query* q, int32_t source, double timeout_s, int32_t direction, int32_t count_te,
                            double alpha, int32_t allow_small, rpq_stats* stats, uint32_t* reach_words,
                            int64_t nwords);

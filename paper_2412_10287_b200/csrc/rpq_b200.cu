@@ -97,7 +97,8 @@ struct LabelDev {
     uint32_t* rowptr[2] = {nullptr, nullptr};
     int32_t* col[2] = {nullptr, nullptr};
     int64_t nnz[2] = {0, 0};
-    uint32_t* ne[2] = {nullptr, nullptr};  // non-empty-row bitmaps (Slot::ne), built on first pull use
+    uint32_t* ne[2] = {nullptr, nullptr};  // non-empty-row bitmaps (Params::ne_tab), built on first use
+    std::vector<uint32_t> h_ne[2];         // host copies, for the rows a query is seeded from (seed_ne)
 };
 
 struct rpq_graph {
@@ -130,6 +131,15 @@ struct rpq_query {
     size_t in_bytes = 0, off_slots = 0, off_tables = 0;
     unsigned int bar_next = 0;      // barrier counter value the next run starts from
     unsigned long long* d_slot_nnz = nullptr;
+    // Host copies of the non-empty-row bitmaps of the start states' push rows:
+    // a source none of whose seed rows has an edge is answered without a
+    // launch (query_eval).  Pointers into the labels' LabelDev::h_ne.
+    std::vector<const uint32_t*> seed_ne;
+    bool seed_ne_ok = false;
+    bool start_is_final = false;
+    int distinct_starts = 0;
+    bool host_answered = false;  // the last query_eval did not run on the device (device state is stale)
+    int32_t host_answered_source = 0;
     std::vector<const uint32_t*> ne_tab;   // per slot: non-empty-row bitmap of the transpose (Params::ne_tab)
     const uint32_t** d_ne_tab = nullptr;
     float dmax_ne = 0.0f;  // the densest slot's mean degree over non-empty rows
@@ -255,6 +265,7 @@ void free_label(LabelDev& L) {
         if (L.rowptr[d]) cudaFree(L.rowptr[d]);
         if (L.col[d]) cudaFree(L.col[d]);
         if (L.ne[d]) cudaFree(L.ne[d]);
+        L.h_ne[d].clear();
         L.rowptr[d] = nullptr;
         L.col[d] = nullptr;
         L.ne[d] = nullptr;
@@ -724,6 +735,7 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
         int64_t nnz[2];
         LabelDev* ne_of;     // the label whose direction ne_dir is the transpose (its non-empty-row
         int ne_dir;          // bitmap is built after the query's own buffers are allocated)
+        int push_dir;        // ... and whose direction push_dir is the push matrix A_s
     };
     // words per bitmap row, as the query's bitmaps are laid out (a multiple of 4)
     const long long ne_words = (((long long)g->nv + 31) / 32 + 3) / 4 * 4;
@@ -756,7 +768,7 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
             ents.push_back(SlotEnt{{L.rowptr[k.second], L.rowptr[1 - k.second]},
                                    {L.col[k.second], L.col[1 - k.second]},
                                    {L.nnz[k.second], L.nnz[1 - k.second]},
-                                   &L, 1 - k.second});
+                                   &L, 1 - k.second, k.second});
         }
         // A state that reads several symbols into the same targets (e.g. the
         // one state of (a|b|c|d)*) gets one merged slot: its rows are the
@@ -786,7 +798,7 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
                         if (rc != RPQ_OK) return rc;
                         sl = (int)ents.size();
                         ents.push_back(SlotEnt{{M->rowptr[0], M->rowptr[1]}, {M->col[0], M->col[1]},
-                                               {M->nnz[0], M->nnz[1]}, M, 1});
+                                               {M->nnz[0], M->nnz[1]}, M, 1, 0});
                         merged_slot[syms] = sl;
                     }
                 }
@@ -942,6 +954,36 @@ int rpq_query_create(rpq_graph* g, int32_t nstates, int32_t ntrans, const int32_
             q->ne_tab.push_back(ensure_ne(*en.ne_of, en.ne_dir));
             if (!q->ne_tab.back() && en.rowptr[1]) return bail(fail(RPQ_ECUDA, "out of device memory (row bitmaps)"));
         }
+        // the start states' push rows, on the host: which sources have any seed edge at all
+        q->seed_ne_ok = true;
+        std::set<int> seen_start;
+        for (int i = 0; i < nstarts && q->seed_ne_ok; ++i) {
+            if (!seen_start.insert(starts[i]).second) continue;
+            for (int gi = gbeg[starts[i]]; gi < gbeg[starts[i] + 1] && q->seed_ne_ok; ++gi) {
+                SlotEnt& en = ents[gslot[gi]];
+                if (en.nnz[0] == 0) continue;  // (no edges: no seed edge)
+                LabelDev& L = *en.ne_of;
+                const int d = en.push_dir;
+                if (L.h_ne[d].empty()) {
+                    const uint32_t* dev = ensure_ne(L, d);
+                    if (!dev) {
+                        q->seed_ne_ok = false;
+                        break;
+                    }
+                    L.h_ne[d].resize((size_t)ne_words);
+                    if (cudaMemcpy(L.h_ne[d].data(), dev, (size_t)ne_words * sizeof(uint32_t),
+                                   cudaMemcpyDeviceToHost) != cudaSuccess) {
+                        cudaGetLastError();
+                        L.h_ne[d].clear();
+                        q->seed_ne_ok = false;
+                        break;
+                    }
+                }
+                q->seed_ne.push_back(L.h_ne[d].data());
+            }
+        }
+        q->distinct_starts = (int)seen_start.size();
+        for (int i = 0; i < nfinals; ++i) q->start_is_final |= seen_start.count(finals[i]) != 0;
     }
     if (!q->ne_tab.empty()) {
         QTRY(cudaMalloc(&q->d_ne_tab, q->ne_tab.size() * sizeof(const uint32_t*)));
@@ -1172,6 +1214,7 @@ int rpq_query_set_tuning(rpq_query* q, int32_t key, double value) {
 
 int rpq_query_run(rpq_query* q, int32_t source, double timeout_s, void* stream) {
     if (!q) return fail(RPQ_EINVAL, "null query");
+    q->host_answered = false;
     if (source < 0 || source >= q->g->nv)
         return fail(RPQ_ERANGE, "vertex index " + std::to_string(source) + " out of range");
     if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
@@ -1307,6 +1350,41 @@ int query_eval(rpq_query* q, int32_t source, double timeout_s, int32_t direction
     const bool direct = reach_words && words && q->zero_copy && !use_small(q) &&
                         host_block_covers(reach_words, (size_t)words * 4);
     if (rc == RPQ_OK) rc = rpq_query_set_output(q, reach_words && !direct ? 1 : 0);
+    // A source none of whose seed rows has an edge: P is the seed, the first
+    // step finds nothing (engine.py:156-160: one iteration; none without a
+    // start state), the answer is the source itself when a start state is
+    // final.  Known on the host from the row bitmaps: no launch.  (Not when
+    // the caller wants the device-side counts: count_te / debug runs.)
+    if (rc == RPQ_OK && q->seed_ne_ok && !count_te && stats && source >= 0 && source < q->g->nv &&
+        !(timeout_s >= 0 && timeout_s == 0.0)) {
+        bool any_edge = false;
+        for (const uint32_t* bm : q->seed_ne) any_edge |= ((bm[source >> 5] >> (source & 31)) & 1u) != 0;
+        if (!any_edge) {
+            rpq_stats st{};
+            st.iterations = q->distinct_starts ? 1 : 0;
+            st.visited_pairs = q->distinct_starts;
+            st.level_new[0] = q->distinct_starts;
+            const bool hit = q->distinct_starts && q->start_is_final;
+            st.reach_count = hit ? 1 : 0;
+            if (reach_words && words > 0) {
+                if (allow_list && 2 * (int64_t)(hit ? 1 : 0) < words) {
+                    st.answer_list = 1;
+                    st.answer_words = hit ? 1 : 0;
+                    if (hit) {
+                        reach_words[0] = (uint32_t)(source >> 5);
+                        reach_words[1] = 1u << (source & 31);
+                    }
+                } else {
+                    std::memset(reach_words, 0, (size_t)words * 4);
+                    if (hit) reach_words[source >> 5] = 1u << (source & 31);
+                }
+            }
+            *stats = st;
+            q->host_answered = true;
+            q->host_answered_source = source;
+            return RPQ_OK;
+        }
+    }
     q->run_out_bits = direct ? reach_words : nullptr;
     q->run_out_list = direct && allow_list && stats;
     if (rc == RPQ_OK) rc = rpq_query_run(q, source, timeout_s, nullptr);
@@ -1334,6 +1412,16 @@ int rpq_query_eval_list(rpq_query* q, int32_t source, double timeout_s, int32_t 
 }
 
 namespace {
+// The last query_eval was answered on the host (no seed edge): the accessors
+// of device-side results run it on the device first.
+int rerun_if_host_answered(rpq_query* q) {
+    if (!q->host_answered) return RPQ_OK;
+    q->host_answered = false;
+    int rc = rpq_query_set_output(q, 1);
+    if (rc == RPQ_OK) rc = rpq_query_run(q, q->host_answered_source, -1.0, nullptr);
+    if (rc == RPQ_OK) rc = wait_impl(q, nullptr, false);
+    return rc;
+}
 // The uint8[nv] answer vector of the last run, expanded from its bitmap on
 // the run's stream the first time it is asked for.
 int materialize_reach(rpq_query* q) {
@@ -1351,6 +1439,7 @@ int materialize_reach(rpq_query* q) {
 int rpq_query_reach_device(rpq_query* q, uint8_t** d_reach) {
     if (!q || !d_reach) return fail(RPQ_EINVAL, "null argument");
     if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+    if (const int hrc = rerun_if_host_answered(q)) return hrc;
     if (q->ran) {
         const int rc = materialize_reach(q);
         if (rc != RPQ_OK) return rc;
@@ -1363,6 +1452,7 @@ int rpq_query_copy_reach(rpq_query* q, uint8_t* host_reach) {
     if (!q || !host_reach) return fail(RPQ_EINVAL, "null argument");
     if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
     if (q->g->nv == 0) return RPQ_OK;
+    if (const int hrc = rerun_if_host_answered(q)) return hrc;
     const int rc = materialize_reach(q);
     if (rc != RPQ_OK) return rc;
     CUDA_TRY(cudaMemcpyAsync(host_reach, q->d_reach, (size_t)q->g->nv, cudaMemcpyDeviceToHost,
@@ -1377,6 +1467,7 @@ int rpq_query_copy_visited(rpq_query* q, uint32_t* host_words, int64_t nwords) {
     if (q->g->nv == 0) return RPQ_OK;
     if (nwords < words * q->nstates) return fail(RPQ_EINVAL, "output buffer too small");
     if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+    if (const int hrc = rerun_if_host_answered(q)) return hrc;
     cudaStream_t st = q->last_stream ? q->last_stream : q->own_stream;
     CUDA_TRY(cudaStreamSynchronize(st));
     CUDA_TRY(cudaMemcpy2D(host_words, (size_t)words * 4, q->d_visited, (size_t)q->W * 4,
@@ -1567,6 +1658,10 @@ int rpq_query_copy_reach_bits(rpq_query* q, uint32_t* host_words, int64_t nwords
     if (!q || (!host_words && nwords)) return fail(RPQ_EINVAL, "null argument");
     const int64_t words = ((int64_t)q->g->nv + 31) / 32;
     if (nwords < words) return fail(RPQ_EINVAL, "output buffer too small");
+    if (q->host_answered) {
+        if (cudaSetDevice(q->g->device) != cudaSuccess) return fail(RPQ_ECUDA, "cudaSetDevice");
+        if (const int hrc = rerun_if_host_answered(q)) return hrc;
+    }
     if (!q->ran) return fail(RPQ_EINVAL, "query has not been run");
     if (q->output_mode == 1 && !q->out_direct) {  // already on the host (pinned), after rpq_query_wait
         std::memcpy(host_words, q->h_reach_bits, (size_t)words * 4);
