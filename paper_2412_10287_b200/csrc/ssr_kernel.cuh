@@ -1041,7 +1041,10 @@ struct FastDiv {
     }
 };
 
-constexpr int kPullCont = 8;  // in-edges a lane probes on its own before the warp scans the row
+#ifndef RPQ_PULL_CONT
+#define RPQ_PULL_CONT 8
+#endif
+constexpr int kPullCont = RPQ_PULL_CONT;  // in-edges a lane probes on its own before the warp scans the row
 #ifndef RPQ_PULL_STATIC_NUM
 #define RPQ_PULL_STATIC_NUM 3  // static share of the pull tasks, in quarters
 #endif
@@ -1879,13 +1882,16 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
         const uint32_t bsz = (dir == DIR_PUSH ? s_bpre[kShards + 1] : s_view.nfront / 8) <
                                      (unsigned long long)nwarps * 4
                                  ? 32u : (uint32_t)kBundle;
+#ifndef RPQ_GAIN_BUNDLES
+#define RPQ_GAIN_BUNDLES 4
+#endif
 #ifdef RPQ_NO_BUNDLE_GAIN
         const float gain = 0.0f;
 #else
         // bundles the successor level wants: 4 per warp; this level has
         // s_bpre[kShards + 1] bundles, each the source of about one pass
         const float gain = dir == DIR_PUSH && bsz < (uint32_t)kBundle
-                               ? (float)s_bpre[kShards + 1] / (float)(nwarps * 4) : 0.0f;
+                               ? (float)s_bpre[kShards + 1] / (float)(nwarps * RPQ_GAIN_BUNDLES) : 0.0f;
 #endif
         const Out o{&ctl->qc[(e + 1) % 3], p.seg[(e + 1) & 1], p.bun[(e + 1) & 1], &s_resv, bsz, gain};
         const uint32_t qbsz_next = bsz;
