@@ -1329,6 +1329,9 @@ __device__ __forceinline__ void pull_tasks_ne(const Params& p, const Smem& S, co
 // The same pull for levels whose targets all have ONE active in-slot, on
 // large graphs (32-word tasks), without the step loop above: straight-line
 // task -> append -> rounds (cfg3's pull levels: 95 + 39 us against 102 + 41).
+#ifndef RPQ_NE_PER_LANE
+#define RPQ_NE_PER_LANE 2
+#endif
 constexpr int kNE1Cap = 768;
 __device__ __forceinline__ void pull_tasks_ne1(const Params& p, const Smem& S, const uint32_t* fcur, uint32_t* fnext,
                                               long long pw0, long long pw1, int lane, unsigned* s_task,
@@ -1341,31 +1344,32 @@ __device__ __forceinline__ void pull_tasks_ne1(const Params& p, const Smem& S, c
     const long long nown = ntask >= 16 * G ? (ntask / 4 * RPQ_PULL_STATIC_NUM) / G * G : ntask;
     const FastDiv dblk((uint32_t)nblk), dG((uint32_t)G);
     const uint32_t G32 = (uint32_t)G;
+    constexpr int U = RPQ_NE_PER_LANE;  // candidates per lane and round
     int n = 0;    // queued vertices (warp-uniform)
     int qk = -1;  // the in-transition they belong to
     int qq2 = 0;  // its target state
     auto round = [&]() {
-        const int np = min(n, 64);
+        const int np = min(n, 32 * U);
         const int base = n - np;
         const Slot ps = S.slots[p.nslots + S.islot[qk]];
         const uint32_t* frow = fcur + (long long)S.isrc[qk] * p.W;
-        uint32_t v[2], lo[2], hi[2], e[2];
-        bool act[2], hit[2];
-        int c0[2], c1[2];
+        uint32_t v[U], lo[U], hi[U], e[U];
+        bool act[U], hit[U];
+        int c0[U], c1[U];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < U; ++u) {
             const int idx = base + 32 * u + lane;
             act[u] = idx < n;
             v[u] = act[u] ? ent[idx] : 0u;
             if (act[u] && !RPQ_CHECK(v[u] < (uint32_t)p.nv, RPQ_F_SSR)) act[u] = false;
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < U; ++u) {
             lo[u] = act[u] ? ld_stream_u32(ps.rowptr + v[u], S.pf) : 0u;
             hi[u] = act[u] ? ld_stream_u32(ps.rowptr + v[u] + 1, S.pf) : 0u;
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < U; ++u) {
             if (act[u] && !RPQ_CHECK(lo[u] <= hi[u] && hi[u] <= p.slot_nnz[S.islot[qk] % p.nslots], RPQ_F_SSR))
                 hi[u] = lo[u];
             if (lo[u] >= hi[u]) act[u] = false;  // (cannot happen for a bitmap built from these rows)
@@ -1374,7 +1378,7 @@ __device__ __forceinline__ void pull_tasks_ne1(const Params& p, const Smem& S, c
             if (act[u] && !RPQ_CHECK(c0[u] >= 0 && c0[u] < p.nv && c1[u] < p.nv, RPQ_F_SSR)) c0[u] = c1[u] = -1;
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < U; ++u) {
             hit[u] = (c0[u] >= 0 && ((ld_bits(frow + (c0[u] >> 5), S.pl) >> (c0[u] & 31)) & 1u)) ||
                      (c1[u] >= 0 && ((ld_bits(frow + (c1[u] >> 5), S.pl) >> (c1[u] & 31)) & 1u));
             e[u] = lo[u] + (uint32_t)first;
@@ -1383,19 +1387,22 @@ __device__ __forceinline__ void pull_tasks_ne1(const Params& p, const Smem& S, c
         // misses continue lane-parallel, two in-edges per entry and round, up
         // to kPullCont edges of the row; longer rows are scanned by the warp
         for (;;) {
-            bool go[2];
+            bool go[U];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) go[u] = act[u] && !hit[u] && e[u] < min(hi[u], lo[u] + (uint32_t)kPullCont);
-            if (!__ballot_sync(FULL, go[0] || go[1])) break;
-            int d0[2], d1[2];
+            for (int u = 0; u < U; ++u) go[u] = act[u] && !hit[u] && e[u] < min(hi[u], lo[u] + (uint32_t)kPullCont);
+            bool anygo = false;
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < U; ++u) anygo |= go[u];
+            if (!__ballot_sync(FULL, anygo)) break;
+            int d0[U], d1[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
                 d0[u] = go[u] ? ld_stream_i32(ps.col + e[u], S.pf) : -1;
                 d1[u] = go[u] && e[u] + 1 < hi[u] ? ld_stream_i32(ps.col + e[u] + 1, S.pf) : -1;
                 if (go[u] && !RPQ_CHECK(d0[u] >= 0 && d0[u] < p.nv && d1[u] < p.nv, RPQ_F_SSR)) d0[u] = d1[u] = -1;
             }
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
+            for (int u = 0; u < U; ++u)
                 if (go[u]) {
                     hit[u] = (d0[u] >= 0 && ((ld_bits(frow + (d0[u] >> 5), S.pl) >> (d0[u] & 31)) & 1u)) ||
                              (d1[u] >= 0 && ((ld_bits(frow + (d1[u] >> 5), S.pl) >> (d1[u] & 31)) & 1u));
@@ -1404,7 +1411,7 @@ __device__ __forceinline__ void pull_tasks_ne1(const Params& p, const Smem& S, c
         }
         unsigned nhit = 0;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < U; ++u) {
             unsigned longs = __ballot_sync(FULL, act[u] && !hit[u] && e[u] < hi[u]);
             while (longs) {
                 const int sl = __ffs(longs) - 1;
@@ -1489,7 +1496,7 @@ __device__ __forceinline__ void pull_tasks_ne1(const Params& p, const Smem& S, c
             }
             n += (int)padd;
             __syncwarp();
-            while (n >= 64) round();
+            while (n >= 32 * U) round();
         }
     }
     while (n > 0) round();
