@@ -1543,6 +1543,13 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
     int32_t* s_tab = reinterpret_cast<int32_t*>(smem_raw + kStageBytes(NT) + sizeof(Slot) * 2 * p.nslots);
     for (int i = threadIdx.x; i < 2 * p.nslots; i += blockDim.x) s_slots[i] = p.slots[i];
     for (int i = threadIdx.x; i < p.table_ints; i += blockDim.x) s_tab[i] = p.tables[i];
+    // the push path's hottest tables again at compile-time shared addresses
+    // (with 64 registers their run-time offsets were recomputed at every
+    // use: 11% of cfg4's instructions were address arithmetic)
+    __shared__ int32_t s_gbeg[kMaxStates + 1], s_gslot[kMaxGroups], s_toff[kMaxGroups + 1];
+    for (int i = threadIdx.x; i <= p.nstates; i += blockDim.x) s_gbeg[i] = p.tables[i];
+    for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gslot[i] = p.tables[p.nstates + 1 + i];
+    for (int i = threadIdx.x; i <= p.ngroups; i += blockDim.x) s_toff[i] = p.tables[p.nstates + 1 + p.ngroups + i];
     if (threadIdx.x == 0) {
         s_resv = 0;
         s_wend = 0;
@@ -1572,10 +1579,10 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
     S.slots = s_slots;
     S.nnz = s_nnz;
     S.ne = s_ne;
-    S.gbeg = s_tab;
-    S.gslot = S.gbeg + p.nstates + 1;
-    S.toff = S.gslot + p.ngroups;
-    S.targets = S.toff + p.ngroups + 1;
+    S.gbeg = s_gbeg;
+    S.gslot = s_gslot;
+    S.toff = s_toff;
+    S.targets = s_tab + (p.nstates + 1) + p.ngroups + (p.ngroups + 1);
     S.starts = S.targets + p.ntargets;
     S.finals = S.starts + p.nstarts;
     S.ibeg = S.finals + p.nfinals;
@@ -1932,8 +1939,11 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
         // emit F_{L+1}'s queue now (at discovery) or later from F's bitmap
         // (a step-mode run stops after this level: nobody expands F_{L+1}'s queue)
         // progress reports: about 4 per CTA before the cut
-        const unsigned long long cut_chunk =
-            s_view.cut_edges > 0.0f ? (unsigned long long)(s_view.cut_edges / (4.0f * (float)gridDim.x)) + 1ull : 0ull;
+        // (a power of two: the per-drain progress test below is two shifts, not two 64-bit divisions)
+        const int cut_shift =
+            s_view.cut_edges > 0.0f
+                ? 63 - __clzll((unsigned long long)(s_view.cut_edges / (4.0f * (float)gridDim.x)) + 1ull) : -1;
+        const unsigned long long cut_chunk = cut_shift >= 0 ? 1ull << cut_shift : 0ull;
         const bool emit_inline = dir == DIR_PUSH && !s_view.defer && !step_mode &&
                                  (s_run.emit_mode == 0 ||
                                   (s_run.emit_mode == 2 && s_view.nfront < s_run.emit_inline_max));
@@ -2207,10 +2217,10 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
                             // report progress in chunks; past the cut, stop emitting
                             if (cut_chunk && T) {
                                 const unsigned long long old_e = atomicAdd(&s_emitted, (unsigned long long)T);
-                                const unsigned long long c0 = old_e / cut_chunk, c1 = (old_e + T) / cut_chunk;
+                                const unsigned long long c0 = old_e >> cut_shift, c1 = (old_e + T) >> cut_shift;
                                 if (c1 != c0) {
                                     const unsigned long long g =
-                                        atomicAdd(&o.qc->emit_progress, (c1 - c0) * cut_chunk) + (c1 - c0) * cut_chunk;
+                                        atomicAdd(&o.qc->emit_progress, (c1 - c0) << cut_shift) + ((c1 - c0) << cut_shift);
                                     if ((float)g >= s_view.cut_edges || ldcg(&o.qc->emit_cut)) {
                                         o.qc->emit_cut = 1u;
                                         s_cut = 1;
