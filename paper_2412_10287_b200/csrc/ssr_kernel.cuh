@@ -28,6 +28,9 @@
 #include "checks.cuh"
 
 namespace rpqk {
+#ifndef RPQ_CUT_SHIFT_UP
+#define RPQ_CUT_SHIFT_UP 1
+#endif
 
 // One CTA per SM; the thread count is a template parameter of the kernels:
 // 768 (24 warps, 80 registers) for small state spaces, where fewer spills win,
@@ -1542,14 +1545,22 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
     }
     int32_t* s_tab = reinterpret_cast<int32_t*>(smem_raw + kStageBytes(NT) + sizeof(Slot) * 2 * p.nslots);
     for (int i = threadIdx.x; i < 2 * p.nslots; i += blockDim.x) s_slots[i] = p.slots[i];
-    for (int i = threadIdx.x; i < p.table_ints; i += blockDim.x) s_tab[i] = p.tables[i];
-    // the push path's hottest tables again at compile-time shared addresses
-    // (with 64 registers their run-time offsets were recomputed at every
-    // use: 11% of cfg4's instructions were address arithmetic)
+    // the push path's hottest tables (gbeg, gslot, toff: the first three of
+    // the block) also at compile-time shared addresses: with 64 registers
+    // their run-time offsets were recomputed at every use (11% of cfg4's
+    // instructions were address arithmetic).  Filled in the same pass (a second
+    // round of global loads in the prologue cost every query 1-2 us).
     __shared__ int32_t s_gbeg[kMaxStates + 1], s_gslot[kMaxGroups], s_toff[kMaxGroups + 1];
-    for (int i = threadIdx.x; i <= p.nstates; i += blockDim.x) s_gbeg[i] = p.tables[i];
-    for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gslot[i] = p.tables[p.nstates + 1 + i];
-    for (int i = threadIdx.x; i <= p.ngroups; i += blockDim.x) s_toff[i] = p.tables[p.nstates + 1 + p.ngroups + i];
+    {
+        const int o1 = p.nstates + 1, o2 = o1 + p.ngroups, o3 = o2 + p.ngroups + 1;
+        for (int i = threadIdx.x; i < p.table_ints; i += blockDim.x) {
+            const int32_t v = p.tables[i];
+            s_tab[i] = v;
+            if (i < o1) s_gbeg[i] = v;
+            else if (i < o2) s_gslot[i - o1] = v;
+            else if (i < o3) s_toff[i - o2] = v;
+        }
+    }
     if (threadIdx.x == 0) {
         s_resv = 0;
         s_wend = 0;
@@ -1939,10 +1950,12 @@ __global__ void __launch_bounds__(NT, kMinBlocks) ssr_kernel(const __grid_consta
         // emit F_{L+1}'s queue now (at discovery) or later from F's bitmap
         // (a step-mode run stops after this level: nobody expands F_{L+1}'s queue)
         // progress reports: about 4 per CTA before the cut
-        // (a power of two: the per-drain progress test below is two shifts, not two 64-bit divisions)
+        // (a power of two, the next one up: the per-drain progress test below is
+        // two shifts, not two 64-bit divisions; rounded down, the finer reports
+        // cost cfg3 1%)
         const int cut_shift =
             s_view.cut_edges > 0.0f
-                ? 63 - __clzll((unsigned long long)(s_view.cut_edges / (4.0f * (float)gridDim.x)) + 1ull) : -1;
+                ? 63 - __clzll((unsigned long long)(s_view.cut_edges / (4.0f * (float)gridDim.x)) + 1ull) + RPQ_CUT_SHIFT_UP : -1;
         const unsigned long long cut_chunk = cut_shift >= 0 ? 1ull << cut_shift : 0ull;
         const bool emit_inline = dir == DIR_PUSH && !s_view.defer && !step_mode &&
                                  (s_run.emit_mode == 0 ||
